@@ -67,7 +67,8 @@ class Params_c(C.Structure):
                 ("lambda_max", C.c_double), ("beta_max", C.c_double), ("eps_inner_abs", C.c_double),
                 ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
-                ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double)]
+                ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
+                ("al_sigma_decay", C.c_double)]
 
 
 class Report_c(C.Structure):
@@ -126,7 +127,7 @@ def params_c(pr) -> Params_c:
     return Params_c(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max,
                     pr.beta_max, pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled,
                     pr.tron_gtol_rel, pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel,
-                    pr.al_sigma_max_rel)
+                    pr.al_sigma_max_rel, pr.al_sigma_decay)
 
 
 class Oracle:

@@ -718,8 +718,8 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
             double X[6] = {x[0], x[1], x[2], x[3],
                            clampd(1.0 - s1 / c.r2, 0.0, 1.0), clampd(1.0 - s2 / c.r2, 0.0, 1.0)};
             c.al = 1;
-            c.mu[0] = al[0]; c.mu[1] = al[1]; c.sig = al[2];
-            if (!(c.sig > 0.0)) c.sig = sig0;
+            c.mu[0] = al[0]; c.mu[1] = al[1];
+            c.sig = dmax(sig0, al[2] * pr->al_sigma_decay);
             double smax = pr->al_sigma_max_rel * sig0;
             double hprev = INFINITY;
             int k;

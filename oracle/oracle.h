@@ -46,7 +46,7 @@ typedef struct {
     int32_t inner_min, inner_cap, outer_enabled;
     double tron_gtol_rel;
     int32_t tron_maxit, al_maxit;
-    double al_eta_star, al_sigma0_rel, al_sigma_max_rel;
+    double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
 } orc_params;
 
 typedef struct {

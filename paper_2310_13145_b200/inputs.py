@@ -182,8 +182,9 @@ class Params:
     tron_maxit: int = 100
     al_maxit: int = 50
     al_eta_star: float = 1e-10
-    al_sigma0_rel: float = 1.0
+    al_sigma0_rel: float = 10.0
     al_sigma_max_rel: float = 1e8
+    al_sigma_decay: float = 0.1
 
 
 # --------------------------------------------------------------------------------------

@@ -1,0 +1,223 @@
+"""Whole-iteration pins for the oracle's two-level ADMM (Alg. 1).
+
+* (7e)/(7f) exactness: z^{l+1}, y^{l+1} of every row recomputed here from the rows of
+  Eq. (5) (R3/R6/R7) evaluated on the state the oracle returned, and the z
+  closed form checked against 1-D numerical minimisation of the row's L terms;
+* the outer update: lambda <- clip(lambda + beta z), beta x tau iff
+  ||z|| > theta ||z||_prev, tau = 6, theta = 0.8;
+* MATPOWER case9 single-period ACOPF optimum (golden, 5296.69 $/h) and AC feasibility of
+  the converged consensus point;
+* Eq. 3 feasibility of every schedule, determinism."""
+import dataclasses
+import json
+import os
+
+import numpy as np
+import pytest
+from scipy.optimize import minimize_scalar
+
+import oracle
+from paper_2310_13145_b200 import inputs
+
+from test_oracle_dp import feasible
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "case9_acopf.json")))
+SPEC = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def rows_residual(pb, pr, s0, s1):
+    """r = A x^{l+1} + B xbar^{l+1} per row (Eq. 5) from two consecutive states; slacks are
+    the exact minimisers given the x-step's shifted bounds (built from s0)."""
+    T, G, L = pb.T, pb.ngen, pb.nbranch
+    rpq, rva, ruc = pr.rho_pq, pr.rho_va, pr.rho_uc
+    zg0, yg0 = s0["zg"].reshape(12, G, T), s0["yg"].reshape(12, G, T)
+    u = s1["u"].reshape(G, T).astype(float)
+    p, q, ph = (s1[k].reshape(G, T) for k in ("p", "q", "ph"))
+    on0, su0, sd0 = (s0[k].reshape(G, T) for k in ("ub_on", "ub_su", "ub_sd"))
+    on1, su1, sd1 = (s1[k].reshape(G, T) for k in ("ub_on", "ub_su", "ub_sd"))
+    pbar, qbar = s1["pbar"].reshape(G, T), s1["qbar"].reshape(G, T)
+    rg = np.zeros((12, G, T))
+    for g in range(G):
+        for t in range(T):
+            up = pb.u0[g] if t == 0 else u[g, t - 1]
+            su, sd = max(0.0, u[g, t] - up), max(0.0, up - u[g, t])
+            onp0 = pb.u0[g] if t == 0 else on0[g, t - 1]
+            onp1 = pb.u0[g] if t == 0 else on1[g, t - 1]
+
+            def b(k, v):
+                return v - zg0[k, g, t] - yg0[k, g, t] / ruc
+            bpl, bpu = b(3, pb.pmin[g] * on0[g, t]), b(4, pb.pmax[g] * on0[g, t])
+            bql, bqu = b(5, pb.qmin[g] * on0[g, t]), b(6, pb.qmax[g] * on0[g, t])
+            brl = b(7, -pb.ramp_dn[g] * on0[g, t] - pb.sd_ramp[g] * sd0[g, t])
+            bru = b(8, pb.ramp_up[g] * onp0 + pb.su_ramp[g] * su0[g, t])
+            d = p[g, t] - ph[g, t]
+            spl, spu = max(0, p[g, t] - bpl), max(0, bpu - p[g, t])
+            sql, squ = max(0, q[g, t] - bql), max(0, bqu - q[g, t])
+            srd, sru = max(0, d - brl), max(0, bru - d)
+            rg[0, g, t] = u[g, t] - on1[g, t]
+            rg[1, g, t] = su - su1[g, t]
+            rg[2, g, t] = sd - sd1[g, t]
+            rg[3, g, t] = p[g, t] - spl - pb.pmin[g] * on1[g, t]
+            rg[4, g, t] = p[g, t] + spu - pb.pmax[g] * on1[g, t]
+            rg[5, g, t] = q[g, t] - sql - pb.qmin[g] * on1[g, t]
+            rg[6, g, t] = q[g, t] + squ - pb.qmax[g] * on1[g, t]
+            rg[7, g, t] = d - srd + pb.ramp_dn[g] * on1[g, t] + pb.sd_ramp[g] * sd1[g, t]  # Eq. 4d
+            rg[8, g, t] = d + sru - pb.ramp_up[g] * onp1 - pb.su_ramp[g] * su1[g, t]
+            rg[9, g, t] = p[g, t] - pbar[g, t]
+            rg[10, g, t] = q[g, t] - qbar[g, t]
+            rg[11, g, t] = 0.0 if t == 0 else ph[g, t] - pbar[g, t - 1]
+    x, f, fb = s1["x"].reshape(L, T, 4), s1["f"].reshape(L, T, 4), s1["fbar"].reshape(L, T, 4)
+    wb, tb = s1["wbar"].reshape(-1, T), s1["thbar"].reshape(-1, T)
+    rb = np.zeros((8, L, T))
+    for k in range(4):
+        rb[k] = f[:, :, k] - fb[:, :, k]
+    rb[4] = x[:, :, 0] - wb[pb.br_from]
+    rb[5] = x[:, :, 1] - wb[pb.br_to]
+    rb[6] = x[:, :, 2] - tb[pb.br_from]
+    rb[7] = x[:, :, 3] - tb[pb.br_to]
+    rhog = np.array([ruc] * 9 + [rpq] * 3)[:, None, None] * np.ones((12, G, T))
+    rhob = np.array([rpq] * 4 + [rva] * 4)[:, None, None] * np.ones((8, L, T))
+    return rg, rb, rhog, rhob
+
+
+def test_z_y_updates_exact():
+    pb = inputs.case9(T=4)
+    pr = inputs.Params(rho_pq=5e3, rho_va=1e4, rho_uc=1e4, outer_enabled=0)
+    o = oracle.Oracle(pb, pr)
+    o.iterate(3)
+    s0 = o.get_state()
+    o.iterate(1)
+    s1 = o.get_state()
+    rg, rb, rhog, rhob = rows_residual(pb, pr, s0, s1)
+    beta = s0["scal"][0]
+    for r, rho, z0k, y0k, l0k, z1k, y1k, n in ((rg, rhog, "zg", "yg", "lg", "zg", "yg", 12),
+                                               (rb, rhob, "zb", "yb", "lb", "zb", "yb", 8)):
+        lam = s0[l0k].reshape(n, -1)
+        y0 = s0[y0k].reshape(n, -1)
+        z1 = s1[z1k].reshape(n, -1)
+        y1 = s1[y1k].reshape(n, -1)
+        r = r.reshape(n, -1)
+        rho = rho.reshape(n, -1)
+        zref = -(lam + y0 + rho * r) / (beta + rho)
+        if n == 12:
+            zref[11].reshape(pb.ngen, pb.T)[:, 0] = 0.0     # no RC row at t = 1
+        assert np.allclose(z1, zref, rtol=1e-9, atol=1e-11)
+        yref = y0 + rho * (r + z1)
+        if n == 12:
+            yref[11].reshape(pb.ngen, pb.T)[:, 0] = y0[11].reshape(pb.ngen, pb.T)[:, 0]
+        assert np.allclose(y1, yref, rtol=1e-9, atol=1e-9)
+    # the closed form is the argmin of lambda z + beta/2 z^2 + y(r+z) + rho/2 (r+z)^2 (7e)
+    for k in range(5):
+        lam, y, rho, r = 0.3 * k, 1.0 - k, 1e4, 1e-3 * (k - 2)
+        z = -(lam + y + rho * r) / (beta + rho)
+        res = minimize_scalar(lambda v: lam * v + beta / 2 * v * v + y * (r + v) + rho / 2 * (r + v) ** 2,
+                              bracket=(-1, 1), tol=1e-14)
+        assert z == pytest.approx(res.x, abs=1e-9)
+    g = SPEC["z_update"]
+    assert -(g["lambda"] + g["y"] + g["rho"] * g["r"]) / (g["beta"] + g["rho"]) == pytest.approx(g["z"], rel=1e-15)
+
+
+def test_outer_update_rule():
+    pb = inputs.case9(T=4)
+    pr = inputs.Params(rho_pq=5e3, rho_va=1e4, rho_uc=1e4)
+    o = oracle.Oracle(pb, pr)
+    seen = 0
+    prev = o.get_state()
+    for _ in range(200):
+        o.iterate(1)
+        cur = o.get_state()
+        b0, b1 = prev["scal"][0], cur["scal"][0]
+        k0, k1 = prev["scal"][2], cur["scal"][2]
+        if k1 != k0:
+            seen += 1
+            assert k1 == k0 + 1
+            for zk, lk in (("zg", "lg"), ("zb", "lb")):
+                ref = np.clip(prev[lk] + b0 * cur[zk], -pr.lambda_max, pr.lambda_max)
+                assert np.allclose(cur[lk], ref, rtol=1e-15, atol=0)
+            zn = np.sqrt(np.sum(cur["zg"] ** 2) + np.sum(cur["zb"] ** 2))
+            if k0 > 1 and zn > pr.theta * prev["scal"][1] * (1 + 1e-12):
+                assert b1 == min(pr.tau * b0, pr.beta_max)
+            elif k0 == 1 or zn < pr.theta * prev["scal"][1] * (1 - 1e-12):
+                assert b1 == b0
+            assert cur["scal"][1] == pytest.approx(zn, rel=1e-12)
+        else:
+            assert b1 == b0 and np.array_equal(cur["lg"], prev["lg"])
+        prev = cur
+    assert seen >= 3
+
+
+def test_case9_acopf_optimum():
+    """T=1, all units forced on (hold = 1), discount 1, no ramps -> MATPOWER optimum."""
+    pb = inputs.case9(T=1, factors=[1.0], discount=1.0, ramps=False)
+    pb.hold[:] = 1
+    assert pb.pd.sum() * pb.base_mva == pytest.approx(GOLD["total_load_mw"])
+    assert pb.qd.sum() * pb.base_mva == pytest.approx(GOLD["total_load_mvar"])
+    pr = inputs.Params(rho_pq=5e3, rho_va=1e4, rho_uc=1e4)
+    o = oracle.Oracle(pb, pr)
+    o.iterate(1000)
+    rep = o.report()
+    assert rep["primal_inf"] < 1e-5
+    assert rep["objective"] == pytest.approx(GOLD["objective"], abs=0.01)
+    st = o.get_state()
+    assert np.allclose(st["p"] * pb.base_mva, GOLD["pg_mw"], atol=0.02)
+    # AC feasibility of the consensus point: V = sqrt(wbar) e^{j thbar}, S = V conj(Ybus V)
+    V = np.sqrt(st["wbar"]) * np.exp(1j * st["thbar"])
+    S = np.zeros(pb.nbus, dtype=complex)
+    for l in range(pb.nbranch):
+        y = pb.br_y[l]
+        i, j = pb.br_from[l], pb.br_to[l]
+        S[i] += V[i] * np.conj((y[0] + 1j * y[4]) * V[i] + (y[1] + 1j * y[5]) * V[j])
+        S[j] += V[j] * np.conj((y[2] + 1j * y[6]) * V[i] + (y[3] + 1j * y[7]) * V[j])
+    inj = np.zeros(pb.nbus, dtype=complex)
+    np.add.at(inj, pb.gen_bus, st["pbar"] + 1j * st["qbar"])
+    inj -= pb.pd[0] + 1j * pb.qd[0]
+    assert np.max(np.abs(S - inj)) < 100 * rep["primal_inf"] + 1e-9
+    assert np.all(st["wbar"] >= pb.bus_vmin ** 2 - 1e-4) and np.all(st["wbar"] <= pb.bus_vmax ** 2 + 1e-4)
+
+
+def test_case9_uc_schedules_and_determinism():
+    pb, pr = inputs.build_config("case9")
+    a = oracle.Oracle(pb, pr)
+    b = oracle.Oracle(pb, pr)
+    for _ in range(20):
+        a.iterate(10)
+        b.iterate(10)
+        sa, sb = a.get_state(), b.get_state()
+        for k in sa:
+            assert np.array_equal(sa[k], sb[k]), k
+        u = sa["u"].reshape(pb.ngen, pb.T)
+        for g in range(pb.ngen):
+            assert feasible(list(u[g]), int(pb.u0[g]), int(pb.min_up[g]), int(pb.min_dn[g]), int(pb.hold[g]))
+    rep = a.report()
+    assert rep["inner_total"] == 200
+    assert rep["primal_inf"] < 5e-2
+
+
+def test_dp_switching_instance():
+    """SURVEY 8(d) #1b: an expensive unit whose commitment the DP switches off."""
+    pb = inputs.case9(T=6, factors=[0.6, 0.7, 1, 1, 0.7, 0.6], discount=0.5)
+    pb.c0[2] = 5000.0
+    pb.sd_ramp[:] = pb.pmax
+    pr = inputs.Params(rho_pq=5e3, rho_va=1e4, rho_uc=3e3)
+    o = oracle.Oracle(pb, pr)
+    o.iterate(400)
+    st = o.get_state()
+    u = st["u"].reshape(pb.ngen, pb.T)
+    assert u[2].sum() == 0 and u[0].sum() == pb.T
+    assert o.report()["primal_inf"] < 1e-3
+
+
+def test_consensus_fixed_point():
+    """A converged point is (numerically) a fixed point of one more sweep."""
+    pb = inputs.case9(T=1, factors=[1.0], discount=1.0, ramps=False)
+    pb.hold[:] = 1
+    pr = inputs.Params(rho_pq=5e3, rho_va=1e4, rho_uc=1e4)
+    o = oracle.Oracle(pb, pr)
+    o.iterate(1500)
+    s0 = o.get_state()
+    o.iterate(1)
+    s1 = o.get_state()
+    res = o.report()["primal_inf"]
+    assert res < 1e-5
+    for k in ("p", "q", "pbar", "qbar", "wbar", "x", "f"):
+        assert np.allclose(s0[k], s1[k], atol=100 * res), k

@@ -1,0 +1,212 @@
+"""Pins for oracle S3: branch flows (Eq. 2e-2j), the TRON solver and the branch solve
+(7b line part, "six variables", P:456 ExaTron).
+
+Independent references: complex power S = V conj(Y V) of the MATPOWER pi-model, torch
+autograd (fp64) for first and second derivatives, SciPy BVLS for box QPs, a planted exact
+power-flow point, and a dense grid search for a binding thermal limit (Eq. 2c-2d)."""
+import numpy as np
+import pytest
+import torch
+from scipy.optimize import lsq_linear
+
+import oracle
+from paper_2310_13145_b200 import inputs
+
+TWO_PI = 2 * np.pi
+
+
+def flows_complex(y, x):
+    wi, wj, ti, tj = x
+    Vi = np.sqrt(wi) * np.exp(1j * ti)
+    Vj = np.sqrt(wj) * np.exp(1j * tj)
+    yff, yft = y[0] + 1j * y[4], y[1] + 1j * y[5]
+    ytf, ytt = y[2] + 1j * y[6], y[3] + 1j * y[7]
+    sij = Vi * np.conj(yff * Vi + yft * Vj)
+    sji = Vj * np.conj(ytf * Vi + ytt * Vj)
+    return np.array([sij.real, sij.imag, sji.real, sji.imag])
+
+
+def flows_torch(y, x):
+    wi, wj, ti, tj = x[0], x[1], x[2], x[3]
+    vi, vj = torch.sqrt(wi), torch.sqrt(wj)
+    # V_i = vi e^{j ti}; write complex products out in real arithmetic
+    yffr, yftr, ytfr, yttr, yffi, yfti, ytfi, ytti = [float(v) for v in y]
+    Vir, Vii = vi * torch.cos(ti), vi * torch.sin(ti)
+    Vjr, Vji = vj * torch.cos(tj), vj * torch.sin(tj)
+
+    def cm(ar, ai, br, bi):
+        return ar * br - ai * bi, ar * bi + ai * br
+    Iir = cm(yffr, yffi, Vir, Vii)[0] + cm(yftr, yfti, Vjr, Vji)[0]
+    Iii = cm(yffr, yffi, Vir, Vii)[1] + cm(yftr, yfti, Vjr, Vji)[1]
+    Ijr = cm(ytfr, ytfi, Vir, Vii)[0] + cm(yttr, ytti, Vjr, Vji)[0]
+    Iji = cm(ytfr, ytfi, Vir, Vii)[1] + cm(yttr, ytti, Vjr, Vji)[1]
+    sij = cm(Vir, Vii, Iir, -Iii)
+    sji = cm(Vjr, Vji, Ijr, -Iji)
+    return torch.stack([sij[0], sij[1], sji[0], sji[1]])
+
+
+def test_admittance_symmetric_and_ybus():
+    """tap = 1, shift = 0 -> symmetric two-port; tap/shift vs a dense Y-bus."""
+    y = inputs.branch_admittance(0.01, 0.1, 0.02)
+    assert y[1] == y[2] and y[5] == y[6]
+    r, x, b, tap, sh = 0.02, 0.08, 0.03, 1.04, 5.0
+    y = inputs.branch_admittance(r, x, b, tap, sh)
+    ys = 1 / complex(r, x)
+    a = tap * np.exp(1j * np.radians(sh))
+    # textbook: I_f = (ys + jb/2)/|a|^2 V_f - ys/conj(a) V_t ; I_t = -ys/a V_f + (ys + jb/2) V_t
+    Vf, Vt = 1.02 * np.exp(0.1j), 0.97 * np.exp(-0.05j)
+    If = (ys + 1j * b / 2) / abs(a) ** 2 * Vf - ys / np.conj(a) * Vt
+    It = -ys / a * Vf + (ys + 1j * b / 2) * Vt
+    f = flows_complex(y, [abs(Vf) ** 2, abs(Vt) ** 2, np.angle(Vf), np.angle(Vt)])
+    assert np.allclose(f, [(Vf * np.conj(If)).real, (Vf * np.conj(If)).imag,
+                           (Vt * np.conj(It)).real, (Vt * np.conj(It)).imag], atol=1e-12)
+
+
+def test_flows_and_derivatives():
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        y = inputs.branch_admittance(rng.uniform(0, 0.05), rng.uniform(0.02, 0.3), rng.uniform(0, 0.3),
+                                     rng.uniform(0.95, 1.05), rng.uniform(-5, 5))
+        x = np.array([rng.uniform(0.8, 1.2), rng.uniform(0.8, 1.2), rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5)])
+        f, J, H = oracle.branch_flows(y, x)
+        assert np.allclose(f, flows_complex(y, x), atol=1e-12)
+        xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+        Jt = torch.autograd.functional.jacobian(lambda v: flows_torch(y, v), xt).numpy()
+        assert np.allclose(J, Jt, atol=1e-10)
+        for k in range(4):
+            Hk = torch.autograd.functional.hessian(lambda v: flows_torch(y, v)[k], xt).numpy()
+            assert np.allclose(H[k], Hk, atol=1e-10)
+    # flat start identities: w_i = w_j = 1, theta_i = theta_j -> C = 1, S = 0
+    y = inputs.branch_admittance(0.0, 0.1, 0.0)
+    f, _, _ = oracle.branch_flows(y, np.array([1.0, 1.0, 0.2, 0.2]))
+    assert np.allclose(f, 0.0, atol=1e-12)
+
+
+def test_tron_on_box_qps():
+    """TRON on random convex box QPs (n <= 8) matches BVLS."""
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        n = int(rng.integers(1, 9))
+        M = rng.normal(size=(n + 2, n))
+        A = M.T @ M + 0.1 * np.eye(n)
+        b = rng.normal(size=n) * 3
+        lo = -rng.uniform(0, 1, n)
+        hi = rng.uniform(0, 1, n)
+        x, it = oracle.tron_quadratic(A, b, lo, hi, np.zeros(n), gtol=1e-11, maxit=300)
+        assert it >= 0
+        Lc = np.linalg.cholesky(A)
+        ref = lsq_linear(Lc.T, -np.linalg.solve(Lc, b), bounds=(lo, hi), method="bvls", tol=1e-15).x
+        fo = 0.5 * x @ A @ x + b @ x
+        fr = 0.5 * ref @ A @ ref + b @ ref
+        assert fo <= fr + 1e-9 * (1 + abs(fr))
+        assert np.allclose(x, ref, atol=1e-7)
+
+
+def test_tron_scalar_examples():
+    """(x-0.3)^2 -> 0.3 and (x+1)^2 -> 0 on [0,1]."""
+    x, _ = oracle.tron_quadratic(np.array([[2.0]]), np.array([-0.6]), np.array([0.0]), np.array([1.0]), np.array([0.9]))
+    assert x[0] == pytest.approx(0.3, abs=1e-12)
+    x, _ = oracle.tron_quadratic(np.array([[2.0]]), np.array([2.0]), np.array([0.0]), np.array([1.0]), np.array([0.9]))
+    assert x[0] == 0.0
+
+
+def F_branch(y, x, tau, rpq, rva):
+    f = flows_complex(y, x)
+    return 0.5 * rpq * np.sum((f - tau[:4]) ** 2) + 0.5 * rva * np.sum((np.asarray(x) - tau[4:]) ** 2)
+
+
+def grad_torch(y, x, tau, rpq, rva):
+    xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    f = flows_torch(y, xt)
+    t = torch.tensor(tau, dtype=torch.float64)
+    F = 0.5 * rpq * torch.sum((f - t[:4]) ** 2) + 0.5 * rva * torch.sum((xt - t[4:]) ** 2)
+    F.backward()
+    return xt.grad.numpy()
+
+
+PR = inputs.Params(rho_pq=5e3, rho_va=1e4, rho_uc=1e4)
+
+
+def test_branch_planted_point():
+    """targets = an exact power-flow point -> the solver returns it."""
+    rng = np.random.default_rng(2)
+    for _ in range(40):
+        y = inputs.branch_admittance(rng.uniform(0, 0.04), rng.uniform(0.03, 0.2), rng.uniform(0, 0.2))
+        xs = np.array([rng.uniform(0.85, 1.15), rng.uniform(0.85, 1.15), rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3)])
+        tau = np.concatenate([flows_complex(y, xs), xs])
+        x0 = xs + rng.normal(size=4) * 0.02
+        x, al, f, st = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 0.0, tau, 5e3, 1e4, PR, x0, np.zeros(3))
+        assert np.allclose(x, xs, atol=1e-8)
+        assert np.allclose(f, flows_complex(y, x), atol=1e-12)   # Eq. 2i-2j by construction
+        assert st[1] == 0
+
+
+def test_branch_kkt_random():
+    """Projected gradient (torch autograd) at the returned point <= TRON tolerance."""
+    rng = np.random.default_rng(3)
+    lo = np.array([0.81, 0.81, -TWO_PI, -TWO_PI])
+    hi = np.array([1.21, 1.21, TWO_PI, TWO_PI])
+    for _ in range(60):
+        y = inputs.branch_admittance(rng.uniform(0, 0.04), rng.uniform(0.03, 0.2), rng.uniform(0, 0.2))
+        tau = np.concatenate([rng.normal(size=4) * 0.5, [rng.uniform(0.7, 1.3), rng.uniform(0.7, 1.3)],
+                              rng.normal(size=2) * 0.1])
+        x0 = np.array([1.0, 1.0, 0.0, 0.0])
+        x, al, f, st = oracle.branch_solve(y, lo[:2], hi[:2], 0.0, tau, 5e3, 1e4, PR, x0, np.zeros(3))
+        g = grad_torch(y, x, tau, 5e3, 1e4)
+        pg = np.clip(x - g, lo, hi) - x
+        assert np.max(np.abs(pg)) <= 2e-9 * 1e4
+        assert st[1] == 0
+        # a local minimum: no better point nearby within the box
+        F0 = F_branch(y, x, tau, 5e3, 1e4)
+        for _k in range(20):
+            xp = np.clip(x + rng.normal(size=4) * 1e-4, lo, hi)
+            assert F_branch(y, xp, tau, 5e3, 1e4) >= F0 - 1e-9
+
+
+def test_branch_huge_rate_inactive():
+    """rate huge -> thermal multipliers stay 0 and the result equals the unlimited one."""
+    rng = np.random.default_rng(4)
+    y = inputs.branch_admittance(0.01, 0.08, 0.1)
+    tau = np.concatenate([rng.normal(size=4) * 0.5, [1.0, 1.0, 0.05, -0.05]])
+    x0 = np.array([1.0, 1.0, 0.0, 0.0])
+    a = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 0.0, tau, 5e3, 1e4, PR, x0, np.zeros(3))
+    b = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 1e6, tau, 5e3, 1e4, PR, x0, np.zeros(3))
+    assert np.array_equal(a[0], b[0]) and b[1][0] == 0 and b[1][1] == 0 and b[3][2] == 0
+
+
+def test_branch_binding_limit_grid_search():
+    """Binding Eq. 2c-2d: the AL result is feasible and at least as good as the best point
+    of a dense feasible grid over (w_i, w_j, delta) with the optimal angle mean."""
+    y = inputs.branch_admittance(0.01, 0.1, 0.05)
+    rpq, rva = 5e3, 1e4
+    rate = 0.6
+    for seed in range(4):
+        rng = np.random.default_rng(100 + seed)
+        xs = np.array([1.0, 0.98, 0.12, 0.0]) + rng.normal(size=4) * 0.01
+        fs = flows_complex(y, xs)
+        tau = np.concatenate([fs * 1.15, xs])         # targets push the flow above the rate
+        x, al, f, st = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], rate, tau, rpq, rva, PR,
+                                           xs.copy(), np.zeros(3))
+        assert st[2] == 1                              # AL path taken
+        assert f[0] ** 2 + f[1] ** 2 <= rate ** 2 * (1 + 1e-8)
+        assert f[2] ** 2 + f[3] ** 2 <= rate ** 2 * (1 + 1e-8)
+        Fx = F_branch(y, x, tau, rpq, rva)
+        # grid: w_i, w_j, delta; theta mean chosen optimally for the va terms
+        wi = np.linspace(x[0] - 0.02, x[0] + 0.02, 41)
+        wj = np.linspace(x[1] - 0.02, x[1] + 0.02, 41)
+        dl = np.linspace((x[2] - x[3]) - 0.02, (x[2] - x[3]) + 0.02, 41)
+        Wi, Wj, D = np.meshgrid(wi, wj, dl, indexing="ij")
+        m = 0.5 * (tau[6] + tau[7] - D)            # theta_j minimising the va terms given delta
+        Ti, Tj = m + D, m
+        Vi = np.sqrt(Wi) * np.exp(1j * Ti)
+        Vj = np.sqrt(Wj) * np.exp(1j * Tj)
+        yff, yft, ytf, ytt = y[0] + 1j * y[4], y[1] + 1j * y[5], y[2] + 1j * y[6], y[3] + 1j * y[7]
+        sij = Vi * np.conj(yff * Vi + yft * Vj)
+        sji = Vj * np.conj(ytf * Vi + ytt * Vj)
+        F = 0.5 * rpq * ((sij.real - tau[0]) ** 2 + (sij.imag - tau[1]) ** 2 + (sji.real - tau[2]) ** 2
+                         + (sji.imag - tau[3]) ** 2) \
+            + 0.5 * rva * ((Wi - tau[4]) ** 2 + (Wj - tau[5]) ** 2 + (Ti - tau[6]) ** 2 + (Tj - tau[7]) ** 2)
+        feas = (np.abs(sij) <= rate) & (np.abs(sji) <= rate)
+        assert feas.any()
+        Fg = F[feas].min()
+        assert Fx <= Fg + 1e-6 * abs(Fg)
