@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark of the UC-ACOPF two-level ADMM hot path (arXiv 2310.13145) on B200.
+
+A "step" is one inner ADMM iteration = all hot-path rows of SURVEY.md 8(a): UC DP (7a),
+generator closed form + batched branch TRON solves (7b), ubar box-QPs (7c), bus closed form
+(7d), z/y for every coupling row (7e-7f), residual reduction, inner test and outer
+(lambda, beta) update.  Workload at N=1: BASELINE.json configs[4], the 2869-bus
+pegase-shaped synthetic grid with T=48 (the largest single-GPU configuration; the north
+star's "largest case").  Inputs are seeded synthetic data (paper_2310_13145_b200.inputs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ucac|reference] [--config NAME]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (oracle/) on the
+host cores on a bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADMM iters/sec & branch-subproblem solves/sec; time-to-residual 1e-4, 1/2/4/8 B200"
+UNIT = "ADMM inner iterations/s"
+# FP64 flops per TRON Newton iteration of k_branch, from the ncu SASS instruction counts
+# (DFMA = 2, DADD/DMUL = 1) divided by the Newton iterations the kernel reported for the same
+# launch -- profiles/r01_branch_flops.md.  Used for the FP64 roofline of the branch kernel.
+FLOPS_PER_NEWTON_ITER = 1450.0
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def fp64_peak_tflops(sm_mhz: float) -> float:
+    """B200 FP64 (non-tensor) peak: 148 SMs x 64 FP64 FMA lanes/clk x 2 flop."""
+    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_sample(pb, pr, steps: int, budget_s: float):
+    """time the oracle (single thread, as it stands) on a bounded number of iterations."""
+    import oracle
+    o = oracle.Oracle(pb, pr)
+    t0 = time.perf_counter()
+    n = 0
+    while n < steps:
+        o.iterate(1)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return n, dt, o.report()
+
+
+def run_reference(args, pb, pr, rank, world):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    import oracle
+    o = oracle.Oracle(pb, pr)
+    for _ in range(args.warmup):
+        o.iterate(1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.iterate(1)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    v = args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, paper_2310_13145_b200.inputs)",
+        "config": {"workload": f"{args.config} (B={pb.nbus}, G={pb.ngen}, L={pb.nbranch}, T={pb.T})",
+                   "rows": pb.nrows(), "branch_solves_per_step": pb.nbranch * pb.T, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} timed inner iterations after {args.warmup} warm-up, "
+                                   f"single-threaded C oracle (-O2 -ffp-contract=off)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "branch_solves_per_s": v * pb.nbranch * pb.T,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def problem_bytes(pb) -> int:
+    import numpy as np
+    tot = 0
+    for v in vars(pb).values():
+        if isinstance(v, np.ndarray):
+            tot += v.nbytes
+    return tot
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ucac", choices=["ucac", "reference"])
+    ap.add_argument("--config", default="pegase2869")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2310_13145_b200 import inputs
+    pb, pr = inputs.build_config(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, pb, pr, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2310_13145_b200 import ucac
+
+    ctx = ucac.Context(pb, pr)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    sizes = ctx.sizes()
+    l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    # warm-up
+    ctx.iterate(args.warmup)
+    torch.cuda.synchronize()
+    rep0 = ctx.report()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: one graph-launched step per event pair, L2 flushed between steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                l2_flush.zero_()
+                starts[k].record(stream)
+                ctx.iterate(1)
+                ends[k].record(stream)
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    rep1 = ctx.report()
+    newton = rep1["tron_iters"] - rep0["tron_iters"]
+
+    # ---- per-kernel device times (same kernels launched eagerly with an event pair each)
+    kms, klaunch = ctx.iterate_timed(args.steps)
+    rep2 = ctx.report()
+    newton_timed = rep2["tron_iters"] - rep1["tron_iters"]
+    ksum = sum(kms.values())
+    dom = max(kms, key=kms.get)
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median") or 1965.0
+    if dom == "k_branch":
+        flops = newton_timed * FLOPS_PER_NEWTON_ITER
+        achieved = flops / (kms[dom] * 1e-3) / 1e12
+        peak = fp64_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": dom,
+                    "peak_note": "FP64 non-tensor: 148 SM x 64 DFMA/clk x 2 at sm_max_mhz from MEASURED_PEAKS.json "
+                                 "(derived, DESIGN.md 8); flops = Newton iterations x FLOPS_PER_NEWTON_ITER",
+                    "share_of_step": kms[dom] / ksum, "kernel_ms_per_step": kms[dom] / args.steps}
+    else:
+        bytes_ = sizes["alg_bytes"][dom] * args.steps
+        achieved = bytes_ / (kms[dom] * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": dom, "share_of_step": kms[dom] / ksum,
+                    "kernel_ms_per_step": kms[dom] / args.steps}
+    sweep = {}
+    for k in ("k_bus", "k_ubar", "k_gen"):
+        b = sizes["alg_bytes"][k] * args.steps
+        gbs = b / (kms[k] * 1e-3) / 1e9
+        sweep[k] = {"alg_GBps": gbs, "frac_hbm": gbs / peaks.get("hbm_gbs", 6650.0),
+                    "ms_per_step": kms[k] / args.steps}
+
+    # ---- e2e: the public API from host buffers (create = H2D of the problem, iterate,
+    #      residuals + solution = D2H), per step = one inner iteration
+    e2e = None
+    if rank == 0 or True:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx2 = ucac.Context(pb, pr)
+        ctx2.iterate(args.steps)
+        _ = ctx2.report()
+        sol = ctx2.solution()
+        t1 = time.perf_counter()
+        ctx2.close()
+        h2d = problem_bytes(pb.normalized())
+        d2h = sum(v.nbytes for v in sol.values()) + 200
+        e2e = {"value": args.steps / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(d2h / args.steps),
+               "note": "ucac_create(host arrays) + ucac_iterate(K) + ucac_residuals + ucac_get_solution, wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n, dt, _ = oracle_sample(pb, pr, 10 ** 6, args.cpu_budget)
+        cpu = {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{n} inner iterations of the same workload from the cold start, "
+                         f"single-threaded C oracle ({dt:.1f} s budget {args.cpu_budget:.0f} s)"}
+
+    if rank == 0:
+        v = args.steps * world / (tot_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, paper_2310_13145_b200.inputs)",
+            "config": {"workload": f"{args.config} (B={pb.nbus}, G={pb.ngen}, L={pb.nbranch}, T={pb.T})",
+                       "rows": pb.nrows(), "branch_solves_per_step": pb.nbranch * pb.T,
+                       "l2": "flushed (256 MiB memset) before every timed step",
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "branch_solves_per_s": v * pb.nbranch * pb.T,
+            "newton_iters_per_s": newton * world / (tot_ms * 1e-3),
+            "newton_per_solve": newton / max(1, args.steps * pb.nbranch * pb.T),
+            "primal_inf": rep1["primal_inf"],
+            "roofline": roofline,
+            "sweep_kernels": sweep,
+            "kernel_ms_per_step": {k: v_ / args.steps for k, v_ in kms.items()},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 5 * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,195 @@
+/*
+ * ucac.h -- C ABI of the B200-native hot path of the component-decomposed two-level ADMM
+ * for unit commitment with AC optimal power flow (Zhang, Kim & Kim, arXiv 2310.13145,
+ * "On Solving Unit Commitment with Alternating Current Optimal Power Flow on GPU").
+ *
+ * Citations "P:n" are lines of the paper's LaTeX source; "Rk" are the readings
+ * registered in DESIGN.md section 3 where the paper is silent or garbled.
+ *
+ * One inner ADMM iteration (Alg. 1 lines 4-9; steps (7a)-(7f)) runs
+ * entirely on the device as hand-written fp64 sm_100a kernels:
+ *   (7a) UC dynamic program per generator            (Alg. 2)
+ *   (7b) generator closed form per (g,t) + branch trust-region Newton per (l,t)
+ *   (7c) ubar box-QP per (g, period group)
+ *   (7d) bus closed form per (i,t)
+ *   (7e) z, (7f) y per coupling row
+ *   residual reduction, inner test and outer (lambda, beta) update.
+ *
+ * Conventions (all entry points):
+ *  - Units: per unit on base_mva (p, q, flows in pu; w = |V|^2 in pu^2; angles in rad);
+ *    costs in $ per 1-h period with p in MW inside the cost (c2 (S p)^2 + c1 S p).
+ *  - Arrays: plain HOST pointers unless a name says "_dev".  Component-major, period-minor:
+ *    element (c, t) of a [C*T] array is at c*T + t (t = 0 is the paper's period 1), except
+ *    the demand arrays pd/qd which are period-major [T*nbus] (P_{t,i} at t*nbus + i).
+ *  - Ownership: ucac_create deep-copies every input; the caller may free them on return.
+ *    The context owns all device memory.  Output buffers are caller-allocated with the sizes
+ *    stated per call.
+ *  - Errors: every call returns ucac_status; nothing throws or aborts across the ABI.
+ *    ucac_last_error(ctx) (or ucac_last_error(NULL) after a failed create) gives a message.
+ *  - Threading: one context per host thread; no global mutable state.
+ *  - The library requires a CUDA device of compute capability 10.0 (B200, sm_100a).  It never
+ *    falls back to the CPU: without a device every call returns UCAC_ECUDA.
+ */
+#ifndef UCAC_H
+#define UCAC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ucac_ctx ucac_ctx;
+
+typedef enum {
+    UCAC_OK = 0,
+    UCAC_EINVAL = 1,       /* invalid argument or problem data (message says which)        */
+    UCAC_ENOMEM = 2,       /* device or host allocation failed                               */
+    UCAC_ECUDA = 3,        /* CUDA runtime error or no sm_100 device                         */
+    UCAC_ENCCL = 4,        /* NCCL error (multi-GPU contexts)                                */
+    UCAC_ENUMERIC = 5,     /* a non-finite iterate was produced (report.err_* say where)     */
+    UCAC_ESTATE = 6,       /* call not valid in the current state                            */
+    UCAC_EUNSUPPORTED = 7
+} ucac_status;
+
+/* Network, Eq. (2).  Branch l = (i -> j) carries the MATPOWER two-port
+ * admittance entries of Eq. 2e-2h: br_y[8*l + k], k = Gii,Gij,Gji,Gjj,Bii,Bij,Bji,Bjj (R1:
+ * the to-side equations 2g-2h are read with ji labels).  br_rate = rbar_ij of Eq. 2c-2d,
+ * 0 = unlimited (R12).  Bus voltage bounds enter as w in [vmin^2, vmax^2] (Eq. 2k). */
+typedef struct {
+    int32_t nbus, ngen, nbranch, ref_bus;
+    double base_mva;
+    const double *bus_gs, *bus_bs, *bus_vmin, *bus_vmax;   /* [nbus]                     */
+    const int32_t *br_from, *br_to;                         /* [nbranch], 0-based         */
+    const double *br_y;                                     /* [nbranch*8]                */
+    const double *br_rate;                                  /* [nbranch] pu               */
+    const int32_t *gen_bus;                                 /* [ngen]                     */
+    const double *gen_pmin, *gen_pmax, *gen_qmin, *gen_qmax; /* [ngen] pu, Eq. 4a-4b      */
+} ucac_network;
+
+/* Horizon and demand P_{t,i}, Q_{t,i}. */
+typedef struct {
+    int32_t T;
+    const double *pd, *qd;                                  /* [T*nbus] period-major      */
+} ucac_horizon;
+
+/* f^OPF = c2 (S p)^2 + c1 S p; f^UC = c0 u^on + C^SU u^su + C^SD u^sd (R13). */
+typedef struct {
+    const double *c2, *c1, *c0, *startup, *shutdown;        /* [ngen]                     */
+} ucac_costs;
+
+/* UC data: ramps (Eq. 4c-4d), min up/down (Eq. 3d-3e) and the
+ * initial state x_0: u0, hold = L_g if u0 = 1 else F_g (Eq. 3a-3b), p0 = p_{0,g}. */
+typedef struct {
+    const double *ramp_up, *ramp_dn, *su_ramp, *sd_ramp;    /* [ngen] pu / period         */
+    const int32_t *min_up, *min_dn;                         /* [ngen] in [1, T] (R15)     */
+    const int32_t *u0, *hold;                               /* [ngen]                     */
+    const double *p0;                                       /* [ngen] pu                  */
+    const int8_t *u_init;   /* [ngen*T] initial schedule or NULL = continue u0 (R23)       */
+} ucac_uc;
+
+/* ADMM parameters: rho per class; tau, theta; beta0, bounds and the inner
+ * test (R20-R22); branch solver constants (R9, R10). */
+typedef struct {
+    double rho_pq, rho_va, rho_uc;
+    double beta0, tau, theta, lambda_max, beta_max;
+    double eps_inner_abs;
+    int32_t inner_min, inner_cap, outer_enabled;
+    double tron_gtol_rel;
+    int32_t tron_maxit, al_maxit;
+    double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
+} ucac_params;
+
+/* Multi-GPU (bus-graph cut).  NULL = single GPU. */
+typedef struct {
+    int32_t rank, nranks, device;
+    unsigned char nccl_id[128];     /* ncclUniqueId broadcast by the caller              */
+    const int32_t *bus_part;        /* [nbus] owner rank, or NULL = library partitions    */
+} ucac_dist;
+
+/* Create a context: validate (EINVAL with a message: non-finite data, vmin <= 0 or
+ * vmin > vmax, pmin > pmax, qmin > qmax, c2 < 0, min_up/min_dn outside [1,T], hold outside
+ * [0,T], from == to, bus without branch, bad indices, rho <= 0), lay the data out on the
+ * device, and run the cold start of P:459 (R23).  cuda_stream: a cudaStream_t to run on,
+ * or NULL for a context-owned stream.  On failure *out = NULL. */
+ucac_status ucac_create(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *cost,
+                        const ucac_uc *uc, const ucac_params *prm, const ucac_dist *dist,
+                        void *cuda_stream, ucac_ctx **out);
+
+/* Run n inner iterations (each = steps 7a-7f + residuals + the outer update when the inner
+ * test fires), asynchronously on the context stream.  If stop_on_primal > 0 the loop stops on
+ * the device after the first iteration whose primal infeasibility ||Ax+Bxbar||_inf
+ * is <= primal_target; *n_done (if not NULL) then receives the number run (synchronises).
+ * Hitting n is not an error.  ENUMERIC when an iterate became non-finite. */
+ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_primal, double primal_target,
+                         int32_t *n_done);
+
+/* Same iterations launched kernel by kernel with a CUDA event pair around every launch;
+ * kernel_ms[k] receives the summed device time of kernel k (order: ucac_kernel_name(k)),
+ * launches[k] the number of launches.  Used by the benchmark for per-kernel rooflines. */
+#define UCAC_NKERNELS 5
+ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches);
+const char *ucac_kernel_name(int32_t k);
+
+/* Status after the last iteration (synchronises the stream). */
+typedef struct {
+    double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective, beta;
+    int64_t inner_total, outer_total, tron_iters, tron_capped, al_active, al_capped;
+    int32_t inner_since_outer, outer_k;
+    int32_t err_kernel, err_iter;     /* first non-finite: kernel id + 1 (0 = none), iteration */
+} ucac_report;
+ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *rep);
+
+/* Solution (host buffers): u_on [ngen*T]; p, q [ngen*T]; wbar, thetabar [nbus*T];
+ * flows [nbranch*T*4] = (p_ij, q_ij, p_ji, q_ji) of the branch x-side. */
+typedef struct {
+    int8_t *u_on;
+    double *p, *q, *wbar, *thetabar, *flows;
+} ucac_solution;
+ucac_status ucac_get_solution(ucac_ctx *ctx, ucac_solution *sol);
+
+/* Full iterate in the canonical layout of DESIGN.md 4 (host buffers, sizes in brackets;
+ * GT = ngen*T, LT = nbranch*T, BT = nbus*T).  Row kinds per (g,t): D_ON D_SU D_SD PL PU QL
+ * QU RD RU GP GQ RC; per (l,t): FP_IJ FQ_IJ FP_JI FQ_JI W_I W_J A_I A_J; row arrays are
+ * [kind][comp*T + t].  x and f are [LT][4] (w_i w_j th_i th_j / p_ij q_ij p_ji q_ji),
+ * fbar [LT][4], al [LT][3] = (mu_ij, mu_ji, sigma) of the thermal AL.
+ * scal[8] = beta, ||z||_prev, outer k, inner total, inner since outer, 0, 0, 0.
+ * Used for checkpoint/resume and for iteration-by-iteration parity with the oracle. */
+typedef struct {
+    int8_t *u;                                               /* [GT]        */
+    double *p, *q, *ph, *ub_on, *ub_su, *ub_sd, *pbar, *qbar; /* [GT]        */
+    double *zg, *yg, *lg;                                    /* [12*GT]     */
+    double *x, *f, *fbar;                                    /* [4*LT]      */
+    double *al;                                              /* [3*LT]      */
+    double *zb, *yb, *lb;                                    /* [8*LT]      */
+    double *wbar, *thbar;                                    /* [BT]        */
+    double *scal;                                            /* [8]         */
+} ucac_state;
+ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st);
+ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st);
+
+/* Batched UC DP (Alg. 2) on caller stage costs: L [ngen*T*4] with L[(g*T+t)*4 + a*2 + b] =
+ * L^UC_{g,t}(a, b).  Outputs sched [ngen*T] (int8) and cost [ngen].  Tie -> stay
+ * (P:380), windows clipped at T (R15), forced prefix of hold periods (R14).  When on_device
+ * != 0 all five array arguments are device pointers and the call runs asynchronously on
+ * cuda_stream (NULL = legacy default stream); otherwise they are host pointers. */
+ucac_status ucac_dp_batch(int32_t ngen, int32_t T, const double *L, const int32_t *min_up,
+                          const int32_t *min_dn, const int32_t *u0, const int32_t *hold,
+                          int8_t *sched, double *cost, int32_t on_device, void *cuda_stream);
+
+/* Bytes moved and sizes, for the benchmark's roofline arithmetic. */
+typedef struct {
+    int64_t nrows, gen_periods, branch_periods, bus_periods;
+    int64_t alg_bytes_per_iter;         /* algorithmic HBM bytes of one inner iteration   */
+    int64_t alg_bytes[UCAC_NKERNELS];   /* per kernel                                     */
+} ucac_sizes;
+ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz);
+
+void *ucac_stream(ucac_ctx *ctx);                 /* the cudaStream_t the context runs on */
+const char *ucac_last_error(const ucac_ctx *ctx); /* NULL ctx: last create failure (thread-local) */
+void ucac_destroy(ucac_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,520 @@
+// k_branch.cu -- step (7b) line part: one bound-constrained trust-region Newton solve per
+// (branch, period) ("tiny nonlinear optimization problem with six variables",
+// P:456 ExaTron), batched over all L*T pairs, fp64 on sm_100a.
+//
+// Mapping: one THREAD per (l,t) solve -- the 4- (or 6-) variable Newton
+// system, its gradient and Hessian live in registers; there is no cross-lane work at all,
+// so all 32 lanes do useful FP64 math (a warp-per-solve mapping would leave >= 28 lanes
+// idle for n <= 6).  Consecutive threads are consecutive (l,t) pairs, so every row array
+// load/store of the warp is one coalesced 256-B segment.
+//
+// Flows are linear in phi = (w_i, w_j, C, S) with C = sqrt(w_i w_j) cos(th_i - th_j),
+// S = sqrt(w_i w_j) sin(...) (Eq. 2e-2j): f = M phi.  Hence
+//   grad_x F = J^T G_phi + rho_va (x - tau_x),
+//   Hess_x F = J^T K_phi J + G_C d2C + G_S d2S + rho_va I,  K_phi = rho_pq M^T M (+ AL terms)
+// with J = d phi / d x.  K_phi has 7 distinct entries for the plain problem.
+//
+// The TRON variant (Cauchy search, Steihaug-Toint CG on the free variables, projected
+// search, ratio test) is the one specified in DESIGN.md 5.3; the oracle implements the same
+// algorithm independently (oracle/oracle.c) with a straightforward evaluation.
+#include "ucac_dev.cuh"
+
+namespace ucac {
+namespace {
+
+constexpr double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
+constexpr double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-12;
+constexpr double TR_EPSF = 1e-10;
+constexpr double TWO_PI = 6.283185307179586;
+
+template <bool AL>
+struct BrFun {
+    double Gii, Gij, Gji, Gjj, Bii, Bij, Bji, Bjj;
+    double tau[8];
+    double rpq, rva;
+    double K00, K02, K03, K11, K12, K13, K22;   // rho_pq M^T M (K01 = K23 = 0, K33 = K22)
+    double mu0, mu1, sig, r2inv;                // AL only
+
+    __device__ __forceinline__ void setup() {
+        K00 = rpq * (Gii * Gii + Bii * Bii);
+        K02 = rpq * (Gii * Gij + Bii * Bij);
+        K03 = rpq * (Gii * Bij - Bii * Gij);
+        K11 = rpq * (Gjj * Gjj + Bjj * Bjj);
+        K12 = rpq * (Gjj * Gji + Bjj * Bji);
+        K13 = rpq * (Bjj * Gji - Gjj * Bji);
+        K22 = rpq * (Gij * Gij + Bij * Bij + Gji * Gji + Bji * Bji);
+    }
+
+    __device__ __forceinline__ void flows(const double *x, double &C, double &S, double &f0,
+                                          double &f1, double &f2, double &f3) const {
+        double R = sqrt(x[0] * x[1]);
+        double sn, cs;
+        sincos(x[2] - x[3], &sn, &cs);
+        C = R * cs;
+        S = R * sn;
+        f0 = Gii * x[0] + Gij * C + Bij * S;
+        f1 = -Bii * x[0] - Bij * C + Gij * S;
+        f2 = Gjj * x[1] + Gji * C - Bji * S;
+        f3 = -Bjj * x[1] - Bji * C - Gji * S;
+    }
+
+    // objective only
+    __device__ __forceinline__ double value(const double *x) const {
+        double C, S, f0, f1, f2, f3;
+        flows(x, C, S, f0, f1, f2, f3);
+        double e0 = f0 - tau[0], e1 = f1 - tau[1], e2 = f2 - tau[2], e3 = f3 - tau[3];
+        double F = 0.5 * rpq * (e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; m++) {
+            double d = x[m] - tau[4 + m];
+            v += d * d;
+        }
+        F += 0.5 * rva * v;
+        if (AL) {
+            double h0 = (f0 * f0 + f1 * f1) * r2inv - 1.0 + x[4];
+            double h1 = (f2 * f2 + f3 * f3) * r2inv - 1.0 + x[5];
+            F += mu0 * h0 + 0.5 * sig * h0 * h0 + mu1 * h1 + 0.5 * sig * h1 * h1;
+        }
+        return F;
+    }
+
+    // objective, gradient and (optionally) Hessian
+    template <int N, bool HESS>
+    __device__ __forceinline__ void eval(const double *x, double &F, double *g, double (*H)[N]) const {
+        double C, S, f0, f1, f2, f3;
+        flows(x, C, S, f0, f1, f2, f3);
+        double e0 = f0 - tau[0], e1 = f1 - tau[1], e2 = f2 - tau[2], e3 = f3 - tau[3];
+        F = 0.5 * rpq * (e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; m++) {
+            double d = x[m] - tau[4 + m];
+            v += d * d;
+        }
+        F += 0.5 * rva * v;
+        // phi-space gradient rho_pq M^T e
+        double Gw0 = rpq * (e0 * Gii - e1 * Bii);
+        double Gw1 = rpq * (e2 * Gjj - e3 * Bjj);
+        double GC = rpq * (e0 * Gij - e1 * Bij + e2 * Gji - e3 * Bji);
+        double GS = rpq * (e0 * Bij + e1 * Gij - e2 * Bji - e3 * Gji);
+        double k00 = K00, k01 = 0.0, k02 = K02, k03 = K03, k11 = K11, k12 = K12, k13 = K13;
+        double k22 = K22, k23 = 0.0, k33 = K22;
+        double dh0[4], dh1[4], lam0 = 0.0, lam1 = 0.0;
+        if (AL) {
+            double h0 = (f0 * f0 + f1 * f1) * r2inv - 1.0 + x[4];
+            double h1 = (f2 * f2 + f3 * f3) * r2inv - 1.0 + x[5];
+            F += mu0 * h0 + 0.5 * sig * h0 * h0 + mu1 * h1 + 0.5 * sig * h1 * h1;
+            double tw = 2.0 * r2inv;
+            dh0[0] = tw * (f0 * Gii - f1 * Bii);
+            dh0[1] = 0.0;
+            dh0[2] = tw * (f0 * Gij - f1 * Bij);
+            dh0[3] = tw * (f0 * Bij + f1 * Gij);
+            dh1[0] = 0.0;
+            dh1[1] = tw * (f2 * Gjj - f3 * Bjj);
+            dh1[2] = tw * (f2 * Gji - f3 * Bji);
+            dh1[3] = tw * (-f2 * Bji - f3 * Gji);
+            lam0 = mu0 + sig * h0;
+            lam1 = mu1 + sig * h1;
+            Gw0 += lam0 * dh0[0];
+            Gw1 += lam1 * dh1[1];
+            GC += lam0 * dh0[2] + lam1 * dh1[2];
+            GS += lam0 * dh0[3] + lam1 * dh1[3];
+            if (HESS) {
+                double a0 = lam0 * tw, a1 = lam1 * tw;
+                k00 += a0 * (Gii * Gii + Bii * Bii) + sig * dh0[0] * dh0[0];
+                k02 += a0 * (Gii * Gij + Bii * Bij) + sig * dh0[0] * dh0[2];
+                k03 += a0 * (Gii * Bij - Bii * Gij) + sig * dh0[0] * dh0[3];
+                k11 += a1 * (Gjj * Gjj + Bjj * Bjj) + sig * dh1[1] * dh1[1];
+                k12 += a1 * (Gjj * Gji + Bjj * Bji) + sig * dh1[1] * dh1[2];
+                k13 += a1 * (Bjj * Gji - Gjj * Bji) + sig * dh1[1] * dh1[3];
+                double m0 = a0 * (Gij * Gij + Bij * Bij), m1 = a1 * (Gji * Gji + Bji * Bji);
+                k22 += m0 + m1 + sig * (dh0[2] * dh0[2] + dh1[2] * dh1[2]);
+                k33 += m0 + m1 + sig * (dh0[3] * dh0[3] + dh1[3] * dh1[3]);
+                k23 += sig * (dh0[2] * dh0[3] + dh1[2] * dh1[3]);
+                k01 += sig * (dh0[0] * dh0[1] + dh1[0] * dh1[1]);
+            }
+        }
+        double i2wi = 0.5 / x[0], i2wj = 0.5 / x[1];
+        double dC[4] = {C * i2wi, C * i2wj, -S, S};
+        double dS[4] = {S * i2wi, S * i2wj, C, -C};
+#pragma unroll
+        for (int m = 0; m < 4; m++) g[m] = GC * dC[m] + GS * dS[m] + rva * (x[m] - tau[4 + m]);
+        g[0] += Gw0;
+        g[1] += Gw1;
+        if (AL) {
+            g[4] = lam0;
+            g[5] = lam1;
+        }
+        if (!HESS) return;
+        // P = K_phi J  (rows a = phi index, cols m = x index)
+        double P[4][4];
+        const double Kr[4][4] = {{k00, k01, k02, k03}, {k01, k11, k12, k13}, {k02, k12, k22, k23},
+                                 {k03, k13, k23, k33}};
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+#pragma unroll
+            for (int m = 0; m < 4; m++) P[a][m] = Kr[a][2] * dC[m] + Kr[a][3] * dS[m];
+            P[a][0] += Kr[a][0];
+            P[a][1] += Kr[a][1];
+        }
+#pragma unroll
+        for (int m = 0; m < 4; m++) {
+#pragma unroll
+            for (int n = m; n < 4; n++) {
+                double h = dC[m] * P[2][n] + dS[m] * P[3][n];
+                if (m == 0) h += P[0][n];
+                if (m == 1) h += P[1][n];
+                H[m][n] = h;
+            }
+        }
+        // curvature of C, S
+        double A = GC * C + GS * S, Bq = GS * C - GC * S;
+        H[0][0] += -A * i2wi * i2wi;
+        H[1][1] += -A * i2wj * i2wj;
+        H[0][1] += A * i2wi * i2wj;
+        H[0][2] += Bq * i2wi;
+        H[0][3] += -Bq * i2wi;
+        H[1][2] += Bq * i2wj;
+        H[1][3] += -Bq * i2wj;
+        H[2][2] += -A;
+        H[3][3] += -A;
+        H[2][3] += A;
+#pragma unroll
+        for (int m = 0; m < 4; m++) H[m][m] += rva;
+        if (AL) {
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                double j0 = dh0[2] * dC[m] + dh0[3] * dS[m];
+                double j1 = dh1[2] * dC[m] + dh1[3] * dS[m];
+                if (m == 0) { j0 += dh0[0]; j1 += dh1[0]; }
+                if (m == 1) { j0 += dh0[1]; j1 += dh1[1]; }
+                H[m][4] = sig * j0;
+                H[m][5] = sig * j1;
+            }
+            H[4][4] = sig;
+            H[5][5] = sig;
+            H[4][5] = 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < N; m++)
+#pragma unroll
+            for (int n = 0; n < m; n++) H[m][n] = H[n][m];
+    }
+};
+
+template <int N>
+__device__ __forceinline__ double dotn(const double *a, const double *b) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; i++) s += a[i] * b[i];
+    return s;
+}
+template <int N>
+__device__ __forceinline__ void matvec(const double (*H)[N], const double *v, double *o) {
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; j++) s += H[i][j] * v[j];
+        o[i] = s;
+    }
+}
+template <int N>
+__device__ __forceinline__ double qmodel(const double *g, const double (*H)[N], const double *s) {
+    double Hs[N];
+    matvec<N>(H, s, Hs);
+    return dotn<N>(g, s) + 0.5 * dotn<N>(s, Hs);
+}
+__device__ __forceinline__ double clampd(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+
+template <int N>
+__device__ __forceinline__ void pstep(const double *x, const double *lo, const double *hi,
+                                      const double *g, double a, double *s) {
+#pragma unroll
+    for (int i = 0; i < N; i++) s[i] = clampd(x[i] - a * g[i], lo[i], hi[i]) - x[i];
+}
+template <int N>
+__device__ __forceinline__ bool cauchy_ok(const double *g, const double (*H)[N], const double *s, double delta) {
+    return sqrt(dotn<N>(s, s)) <= delta && qmodel<N>(g, H, s) <= TR_MU0 * dotn<N>(g, s);
+}
+template <int N>
+__device__ __forceinline__ double bnd_tau(const double *a, const double *p, double delta) {
+    double aa = dotn<N>(a, a), ap = dotn<N>(a, p), pp = dotn<N>(p, p);
+    if (pp <= 0.0) return 0.0;
+    double gap = fmax(delta * delta - aa, 0.0);
+    double rad = sqrt(ap * ap + pp * gap);
+    return ap > 0.0 ? gap / (ap + rad) : (rad - ap) / pp;
+}
+
+// Projected trust-region Newton.  Returns true when ||P(x-g)-x||_inf <= gtol.
+template <int N, class Fun>
+__device__ bool tron(const Fun &fn, double *x, const double *lo, const double *hi, double gtol,
+                     int maxit, int &iters) {
+    double f, g[N], H[N][N];
+#pragma unroll
+    for (int i = 0; i < N; i++) x[i] = clampd(x[i], lo[i], hi[i]);
+    fn.template eval<N, true>(x, f, g, H);
+    double delta = TR_DELTA0, alpha = 1.0;
+    int it = 0;
+    for (; it < maxit; it++) {
+        double pgn = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; i++) pgn = fmax(pgn, fabs(clampd(x[i] - g[i], lo[i], hi[i]) - x[i]));
+        if (pgn <= gtol) {
+            iters = it;
+            return true;
+        }
+        // --- Cauchy point: backtrack (x0.1) or extrapolate (x10) along P(x - a g)
+        double sc[N];
+        {
+            double a = alpha;
+            pstep<N>(x, lo, hi, g, a, sc);
+            if (!cauchy_ok<N>(g, H, sc, delta)) {
+                for (int k = 0; k < 60; k++) {
+                    a *= 0.1;
+                    pstep<N>(x, lo, hi, g, a, sc);
+                    if (cauchy_ok<N>(g, H, sc, delta)) break;
+                }
+            } else {
+                for (int k = 0; k < 20; k++) {
+                    double sp[N];
+#pragma unroll
+                    for (int i = 0; i < N; i++) sp[i] = sc[i];
+                    double ap = a;
+                    a *= 10.0;
+                    pstep<N>(x, lo, hi, g, a, sc);
+                    bool same = true;
+#pragma unroll
+                    for (int i = 0; i < N; i++) same = same && (sc[i] == sp[i]);
+                    if (!cauchy_ok<N>(g, H, sc, delta) || same) {
+                        a = ap;
+#pragma unroll
+                        for (int i = 0; i < N; i++) sc[i] = sp[i];
+                        break;
+                    }
+                }
+            }
+            alpha = a;
+        }
+        // --- Steihaug-Toint CG on the free variables at x + sc, region ||sc + w|| <= delta
+        bool fr[N];
+        double gq[N], w[N];
+        {
+            double Hs[N];
+            matvec<N>(H, sc, Hs);
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                double xc = x[i] + sc[i];
+                fr[i] = (xc > lo[i]) && (xc < hi[i]);
+                gq[i] = g[i] + Hs[i];
+                w[i] = 0.0;
+            }
+            double r[N], p[N];
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                r[i] = fr[i] ? -gq[i] : 0.0;
+                p[i] = r[i];
+            }
+            double rr = dotn<N>(r, r);
+            if (rr != 0.0) {
+                double tol2 = TR_CGTOL * TR_CGTOL * rr;
+                for (int k = 0; k < N; k++) {
+                    double Hp[N], t[N];
+                    matvec<N>(H, p, Hp);
+#pragma unroll
+                    for (int i = 0; i < N; i++) if (!fr[i]) Hp[i] = 0.0;
+                    double kap = dotn<N>(p, Hp);
+#pragma unroll
+                    for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
+                    if (kap <= 0.0) {
+                        double tau = bnd_tau<N>(t, p, delta);
+#pragma unroll
+                        for (int i = 0; i < N; i++) w[i] += tau * p[i];
+                        break;
+                    }
+                    double a = rr / kap;
+                    double tt[N];
+#pragma unroll
+                    for (int i = 0; i < N; i++) tt[i] = t[i] + a * p[i];
+                    if (sqrt(dotn<N>(tt, tt)) >= delta) {
+                        double tau = bnd_tau<N>(t, p, delta);
+#pragma unroll
+                        for (int i = 0; i < N; i++) w[i] += tau * p[i];
+                        break;
+                    }
+#pragma unroll
+                    for (int i = 0; i < N; i++) {
+                        w[i] += a * p[i];
+                        r[i] -= a * Hp[i];
+                    }
+                    double rn = dotn<N>(r, r);
+                    if (rn <= tol2) break;
+                    double b = rn / rr;
+#pragma unroll
+                    for (int i = 0; i < N; i++) p[i] = r[i] + b * p[i];
+                    rr = rn;
+                }
+            }
+        }
+        // --- projected search along w from the Cauchy point
+        double s[N];
+        {
+            double qc = qmodel<N>(g, H, sc);
+            double b = 1.0;
+            bool found = false;
+            for (int k = 0; k < 20; k++) {
+                double ds[N];
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
+                    ds[i] = s[i] - sc[i];
+                }
+                if (qmodel<N>(g, H, s) <= qc + TR_MU0 * dotn<N>(gq, ds)) {
+                    found = true;
+                    break;
+                }
+                b *= 0.5;
+            }
+            if (!found) {
+#pragma unroll
+                for (int i = 0; i < N; i++) s[i] = sc[i];
+            }
+        }
+        // --- ratio test
+        double pred = -qmodel<N>(g, H, s);
+        double xn[N], gn[N], fnew;
+#pragma unroll
+        for (int i = 0; i < N; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
+        fn.template eval<N, false>(xn, fnew, gn, nullptr);
+        double ared = f - fnew;
+        if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dotn<N>(g, s) + dotn<N>(gn, s));
+        double ratio = pred > 0.0 ? ared / pred : -1.0;
+        double snorm = sqrt(dotn<N>(s, s));
+        if (ratio > TR_ETA0) {
+#pragma unroll
+            for (int i = 0; i < N; i++) x[i] = xn[i];
+            fn.template eval<N, true>(x, f, g, H);
+        }
+        if (ratio < TR_ETA1) delta = TR_SIG1 * fmin(snorm, delta);
+        else if (ratio > TR_ETA2) delta = fmax(delta, TR_SIG3 * snorm);
+    }
+    iters = it;
+    double pgn = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; i++) pgn = fmax(pgn, fabs(clampd(x[i] - g[i], lo[i], hi[i]) - x[i]));
+    return pgn <= gtol;
+}
+
+__device__ __forceinline__ void warp_add_u64(unsigned long long *dst, unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+__global__ void __launch_bounds__(128) k_branch(Dev d) {
+    if (d.st->done) return;
+    const int LT = d.L * d.T;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0;
+    if (k < LT) {
+        const int l = k / d.T, t = k - l * d.T;
+        const int bi = d.bfrom[l], bj = d.bto[l];
+        BrFun<false> F4;
+        F4.Gii = d.y[0 * d.L + l]; F4.Gij = d.y[1 * d.L + l]; F4.Gji = d.y[2 * d.L + l]; F4.Gjj = d.y[3 * d.L + l];
+        F4.Bii = d.y[4 * d.L + l]; F4.Bij = d.y[5 * d.L + l]; F4.Bji = d.y[6 * d.L + l]; F4.Bjj = d.y[7 * d.L + l];
+        F4.rpq = d.rpq;
+        F4.rva = d.rva;
+        const size_t LTs = (size_t)LT;
+        // x-step targets tau = xbar - z - y/rho
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+            F4.tau[r] = d.fbar[r * LTs + k] - d.zb[r * LTs + k] - d.yb[r * LTs + k] / d.rpq;
+        const size_t wi = (size_t)bi * d.T + t, wj = (size_t)bj * d.T + t;
+        F4.tau[4] = d.wbar[wi] - d.zb[B_WI * LTs + k] - d.yb[B_WI * LTs + k] / d.rva;
+        F4.tau[5] = d.wbar[wj] - d.zb[B_WJ * LTs + k] - d.yb[B_WJ * LTs + k] / d.rva;
+        F4.tau[6] = d.thbar[wi] - d.zb[B_AI * LTs + k] - d.yb[B_AI * LTs + k] / d.rva;
+        F4.tau[7] = d.thbar[wj] - d.zb[B_AJ * LTs + k] - d.yb[B_AJ * LTs + k] / d.rva;
+        F4.setup();
+        double lo[6], hi[6];
+        lo[0] = d.vmin[bi] * d.vmin[bi]; hi[0] = d.vmax[bi] * d.vmax[bi];
+        lo[1] = d.vmin[bj] * d.vmin[bj]; hi[1] = d.vmax[bj] * d.vmax[bj];
+        lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
+        lo[4] = 0.0; hi[4] = 1.0; lo[5] = 0.0; hi[5] = 1.0;
+        double x[6];
+#pragma unroll
+        for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
+        int it = 0;
+        bool ok = tron<4>(F4, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
+        c_it += it;
+        c_cap += !ok;
+        const double rate = d.rate[l];
+        const double r2 = rate * rate;
+        const double sig0 = d.al_sigma0_rel * d.rpq * r2;
+        double mu0 = 0.0, mu1 = 0.0, sig = sig0;
+        double C, S, f0, f1, f2, f3;
+        F4.flows(x, C, S, f0, f1, f2, f3);
+        if (rate > 0.0) {
+            double s1 = f0 * f0 + f1 * f1, s2 = f2 * f2 + f3 * f3;
+            if (s1 > r2 || s2 > r2) {
+                // 6-variable slack form, method of multipliers (R9)
+                BrFun<true> F6;
+                F6.Gii = F4.Gii; F6.Gij = F4.Gij; F6.Gji = F4.Gji; F6.Gjj = F4.Gjj;
+                F6.Bii = F4.Bii; F6.Bij = F4.Bij; F6.Bji = F4.Bji; F6.Bjj = F4.Bjj;
+#pragma unroll
+                for (int r = 0; r < 8; r++) F6.tau[r] = F4.tau[r];
+                F6.rpq = F4.rpq; F6.rva = F4.rva;
+                F6.K00 = F4.K00; F6.K02 = F4.K02; F6.K03 = F4.K03; F6.K11 = F4.K11;
+                F6.K12 = F4.K12; F6.K13 = F4.K13; F6.K22 = F4.K22;
+                F6.r2inv = 1.0 / r2;
+                x[4] = clampd(1.0 - s1 / r2, 0.0, 1.0);
+                x[5] = clampd(1.0 - s2 / r2, 0.0, 1.0);
+                mu0 = d.al[0 * LTs + k];
+                mu1 = d.al[1 * LTs + k];
+                sig = fmax(sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
+                const double smax = d.al_sigma_max_rel * sig0;
+                double hprev = INFINITY;
+                int kk = 0;
+                c_al = 1;
+                for (; kk < d.al_maxit; kk++) {
+                    F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
+                    ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
+                    c_it += it;
+                    c_cap += !ok;
+                    F4.flows(x, C, S, f0, f1, f2, f3);
+                    double h1 = (f0 * f0 + f1 * f1) / r2 - 1.0 + x[4];
+                    double h2 = (f2 * f2 + f3 * f3) / r2 - 1.0 + x[5];
+                    double hm = fmax(fabs(h1), fabs(h2));
+                    if (hm <= d.al_eta_star) break;
+                    mu0 += sig * h1;
+                    mu1 += sig * h2;
+                    if (hm > 0.25 * hprev) sig = fmin(10.0 * sig, smax);
+                    hprev = hm;
+                }
+                c_alcap = kk >= d.al_maxit;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
+        d.f[0 * LTs + k] = f0;
+        d.f[1 * LTs + k] = f1;
+        d.f[2 * LTs + k] = f2;
+        d.f[3 * LTs + k] = f3;
+        d.al[0 * LTs + k] = mu0;
+        d.al[1 * LTs + k] = mu1;
+        d.al[2 * LTs + k] = sig;
+    }
+    warp_add_u64(d.cnt + 0, c_it);
+    warp_add_u64(d.cnt + 1, c_cap);
+    warp_add_u64(d.cnt + 2, c_al);
+    warp_add_u64(d.cnt + 3, c_alcap);
+}
+
+}  // namespace
+
+void launch_branch(const Dev &d, cudaStream_t s) {
+    const int n = d.L * d.T;
+    k_branch<<<(n + 127) / 128, 128, 0, s>>>(d);
+}
+
+}  // namespace ucac

@@ -1,0 +1,392 @@
+// k_gen.cu -- steps (7a) and (7b, generator part), plus the cold-start kernel (S0) and the
+// standalone batched DP.  Compiled with -fmad=false: every expression here is evaluated
+// in the operation order written (the same order the oracle's definition uses), so that the
+// integer DP decisions ("stay" when c_stay <= c_switch) are taken on the same fp64
+// values and commitment schedules match the oracle bit for bit.
+//
+// Mapping: one WARP per generator.  Lanes = periods for the stage costs L_t(a,b), the
+// switch-window sums and the per-(g,t) generator x-update (t = lane, lane+32, ...); the
+// backward recursion of Algorithm 2 is inherently sequential in t and runs on
+// lane 0 over a shared-memory table (O(T) with 2 states).
+#include "ucac_dev.cuh"
+
+namespace ucac {
+namespace {
+
+// phi_v(b) = y (b - ubar + z) + rho/2 (b - ubar + z)^2 (duplicate rows; R18)
+__device__ __forceinline__ double phi(double b, double ub, double y, double z, double rho) {
+    double e = (b - ub) + z;
+    return y * e + 0.5 * rho * e * e;
+}
+
+// stage cost L^UC_{g,t}(a,b) with su, sd inferred, f^UC (R13)
+__device__ __forceinline__ double stage_cost(int a, int b, double c0, double csu, double csd, double rho,
+                                             const double *ub, const double *y, const double *z) {
+    int su = b > a, sd = a > b;
+    double v = c0 * (double)b;
+    v = v + csu * (double)su;
+    v = v + csd * (double)sd;
+    v = v + phi((double)b, ub[0], y[0], z[0], rho);
+    v = v + phi((double)su, ub[1], y[1], z[1], rho);
+    v = v + phi((double)sd, ub[2], y[2], z[2], rho);
+    return v;
+}
+
+struct DpSmem {
+    double *L;     // [T*4]
+    double *acc;   // [T*2] switch cost before continuation: L_t(s,n) + sum_{t'} L_{t'}(n,n)
+    double *c;     // [(T+1)*2]
+    int *e;        // [T*2] last period of the forced window (R15: clipped at T)
+    int *dd;       // [T*2] decision: -1 stay, else window end
+    int8_t *u;     // [T]
+};
+
+__host__ __device__ inline size_t dp_smem_bytes(int T) {
+    return (size_t)(T * 4 + T * 2 + (T + 1) * 2) * 8 + (size_t)T * 2 * 4 * 2 + (size_t)((T + 7) / 8) * 8;
+}
+
+__device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
+    DpSmem s;
+    s.L = (double *)base;
+    s.acc = s.L + T * 4;
+    s.c = s.acc + T * 2;
+    s.e = (int *)(s.c + (T + 1) * 2);
+    s.dd = s.e + T * 2;
+    s.u = (int8_t *)(s.dd + T * 2);
+    return s;
+}
+
+// Algorithm 2 on a warp; s.L must be filled.  Returns the optimal cost on lane 0.
+__device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int hold) {
+    const int lane = threadIdx.x & 31;
+    for (int t = lane; t < T; t += 32) {
+#pragma unroll
+        for (int st = 0; st < 2; st++) {
+            int n = 1 - st;
+            int m = n ? TU : TD;
+            int e = t + m - 1;
+            if (e > T - 1) e = T - 1;
+            double acc = s.L[t * 4 + st * 2 + n];
+            for (int tt = t + 1; tt <= e; tt++) acc = acc + s.L[tt * 4 + n * 2 + n];   // R17
+            s.acc[t * 2 + st] = acc;
+            s.e[t * 2 + st] = e;
+        }
+    }
+    __syncwarp();
+    double cost = 0.0;
+    if (lane == 0) {
+        s.c[T * 2 + 0] = 0.0;
+        s.c[T * 2 + 1] = 0.0;
+        for (int t = T - 1; t >= 0; t--) {
+#pragma unroll
+            for (int st = 0; st < 2; st++) {
+                double stay = s.L[t * 4 + st * 2 + st] + s.c[(t + 1) * 2 + st];        // Eq. 10
+                int e = s.e[t * 2 + st];
+                double sw = s.acc[t * 2 + st] + s.c[(e + 1) * 2 + (1 - st)];             // Eq. 11
+                if (stay <= sw) {
+                    s.c[t * 2 + st] = stay;
+                    s.dd[t * 2 + st] = -1;
+                } else {
+                    s.c[t * 2 + st] = sw;
+                    s.dd[t * 2 + st] = e;
+                }
+            }
+        }
+        for (int t = 0; t < hold; t++) {                                                  // R14
+            s.u[t] = (int8_t)u0;
+            cost = cost + s.L[t * 4 + u0 * 2 + u0];
+        }
+        cost = cost + s.c[hold * 2 + u0];
+        int t = hold, st = u0;
+        while (t < T) {
+            int dec = s.dd[t * 2 + st];
+            if (dec < 0) {
+                s.u[t] = (int8_t)st;
+                t++;
+            } else {
+                for (int tt = t; tt <= dec; tt++) s.u[tt] = (int8_t)(1 - st);
+                st = 1 - st;
+                t = dec + 1;
+            }
+        }
+    }
+    __syncwarp();
+    return cost;
+}
+
+// ---------------------------------------------------------------- generator x-update (S2)
+struct GenIn {
+    int first;
+    double c2S2, c1S, rpq, ruc, tp, tq, tph, p0, bpl, bpu, bql, bqu, brl, bru, pL, pU, qL, qU;
+};
+
+__device__ __forceinline__ double gen_obj_p(const GenIn &g, double p, double ph) {
+    double v = g.c2S2 * p * p + g.c1S * p;
+    double e = p - g.tp;
+    v = v + 0.5 * g.rpq * e * e;
+    if (!g.first) {
+        e = ph - g.tph;
+        v = v + 0.5 * g.rpq * e * e;
+    }
+    e = p - g.bpl;
+    if (e < 0.0) v = v + 0.5 * g.ruc * e * e;
+    e = p - g.bpu;
+    if (e > 0.0) v = v + 0.5 * g.ruc * e * e;
+    double dd = p - ph;
+    e = dd - g.brl;
+    if (e < 0.0) v = v + 0.5 * g.ruc * e * e;
+    e = dd - g.bru;
+    if (e > 0.0) v = v + 0.5 * g.ruc * e * e;
+    return v;
+}
+__device__ __forceinline__ double gen_obj_q(const GenIn &g, double q) {
+    double e = q - g.tq;
+    double v = 0.5 * g.rpq * e * e;
+    e = q - g.bql;
+    if (e < 0.0) v = v + 0.5 * g.ruc * e * e;
+    e = q - g.bqu;
+    if (e > 0.0) v = v + 0.5 * g.ruc * e * e;
+    return v;
+}
+
+// exact minimiser of the generator subproblem by activity-pattern enumeration
+// (DESIGN.md 5.2): 16 patterns x {p free} + 4 ramp patterns x {p = pL, p = pU}.
+__device__ void gen_solve(const GenIn &g, double &po, double &qo, double &pho) {
+    double best = INFINITY, bp = g.pL, bph = g.first ? g.p0 : g.tph;
+    if (g.first) {
+        for (int pat = 0; pat < 16; pat++) {
+            int alo = pat & 1, ahi = (pat >> 1) & 1, rlo = (pat >> 2) & 1, rhi = (pat >> 3) & 1;
+            double den = 2.0 * g.c2S2 + g.rpq;
+            double num = -g.c1S + g.rpq * g.tp;
+            if (alo) { den = den + g.ruc; num = num + g.ruc * g.bpl; }
+            if (ahi) { den = den + g.ruc; num = num + g.ruc * g.bpu; }
+            if (rlo) { den = den + g.ruc; num = num + g.ruc * (g.brl + g.p0); }
+            if (rhi) { den = den + g.ruc; num = num + g.ruc * (g.bru + g.p0); }
+            double p = num / den;
+            if (p >= g.pL && p <= g.pU) {
+                double v = gen_obj_p(g, p, g.p0);
+                if (v < best) { best = v; bp = p; }
+            }
+        }
+        double v = gen_obj_p(g, g.pL, g.p0);
+        if (v < best) { best = v; bp = g.pL; }
+        v = gen_obj_p(g, g.pU, g.p0);
+        if (v < best) { best = v; bp = g.pU; }
+        bph = g.p0;
+    } else {
+        for (int pat = 0; pat < 16; pat++) {
+            int alo = pat & 1, ahi = (pat >> 1) & 1, rlo = (pat >> 2) & 1, rhi = (pat >> 3) & 1;
+            double A = 2.0 * g.c2S2 + g.rpq;
+            double b1 = -g.c1S + g.rpq * g.tp;
+            if (alo) { A = A + g.ruc; b1 = b1 + g.ruc * g.bpl; }
+            if (ahi) { A = A + g.ruc; b1 = b1 + g.ruc * g.bpu; }
+            double R = 0.0, rb = 0.0;
+            if (rlo) { R = R + g.ruc; rb = rb + g.ruc * g.brl; }
+            if (rhi) { R = R + g.ruc; rb = rb + g.ruc * g.bru; }
+            b1 = b1 + rb;
+            double b2 = g.rpq * g.tph - rb;
+            double det = (A + R) * (g.rpq + R) - R * R;
+            double p = (b1 * (g.rpq + R) + R * b2) / det;
+            double ph = ((A + R) * b2 + R * b1) / det;
+            if (p >= g.pL && p <= g.pU) {
+                double v = gen_obj_p(g, p, ph);
+                if (v < best) { best = v; bp = p; bph = ph; }
+            }
+        }
+        for (int kb = 0; kb < 2; kb++) {
+            double pb = kb ? g.pU : g.pL;
+            for (int pat = 0; pat < 4; pat++) {
+                int rlo = pat & 1, rhi = (pat >> 1) & 1;
+                double R = 0.0, rb = 0.0;
+                if (rlo) { R = R + g.ruc; rb = rb + g.ruc * g.brl; }
+                if (rhi) { R = R + g.ruc; rb = rb + g.ruc * g.bru; }
+                double ph = (g.rpq * g.tph - rb + R * pb) / (g.rpq + R);
+                double v = gen_obj_p(g, pb, ph);
+                if (v < best) { best = v; bp = pb; bph = ph; }
+            }
+        }
+    }
+    double bestq = INFINITY, bq = g.qL;
+    for (int pat = 0; pat < 4; pat++) {
+        int lo = pat & 1, hi = (pat >> 1) & 1;
+        double den = g.rpq, num = g.rpq * g.tq;
+        if (lo) { den = den + g.ruc; num = num + g.ruc * g.bql; }
+        if (hi) { den = den + g.ruc; num = num + g.ruc * g.bqu; }
+        double qq = num / den;
+        if (qq >= g.qL && qq <= g.qU) {
+            double v = gen_obj_q(g, qq);
+            if (v < bestq) { bestq = v; bq = qq; }
+        }
+    }
+    double v = gen_obj_q(g, g.qL);
+    if (v < bestq) { bestq = v; bq = g.qL; }
+    v = gen_obj_q(g, g.qU);
+    if (v < bestq) { bestq = v; bq = g.qU; }
+    po = bp;
+    qo = bq;
+    pho = bph;
+}
+
+#define ZG(k, i) d.zg[(size_t)(k) * GT + (i)]
+#define YG(k, i) d.yg[(size_t)(k) * GT + (i)]
+
+__global__ void __launch_bounds__(128) k_gen(Dev d) {
+    if (d.st->done) return;
+    extern __shared__ __align__(16) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (g >= d.G) return;
+    const int T = d.T;
+    const size_t GT = (size_t)d.G * T;
+    DpSmem s = dp_carve(smem + (size_t)warp * dp_smem_bytes(T), T);
+    const double ruc = d.ruc, rpq = d.rpq;
+    // ---- (7a): stage costs on iterate l (ubar^l, y^l, z^l of the duplicate rows)
+    const double c0 = d.c0[g], csu = d.csu[g], csd = d.csd[g];
+    for (int t = lane; t < T; t += 32) {
+        const size_t i = (size_t)g * T + t;
+        double ub[3] = {d.ub_on[i], d.ub_su[i], d.ub_sd[i]};
+        double yy[3] = {YG(G_DON, i), YG(G_DSU, i), YG(G_DSD, i)};
+        double zz[3] = {ZG(G_DON, i), ZG(G_DSU, i), ZG(G_DSD, i)};
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) s.L[t * 4 + a * 2 + b] = stage_cost(a, b, c0, csu, csd, ruc, ub, yy, zz);
+    }
+    __syncwarp();
+    dp_warp(s, T, d.tu[g], d.td[g], d.u0[g], d.hold[g]);
+    for (int t = lane; t < T; t += 32) d.u[(size_t)g * T + t] = s.u[t];
+    // ---- (7b) generator part on iterate l
+    const double S = d.S;
+    GenIn in;
+    in.c2S2 = d.c2[g] * S * S;
+    in.c1S = d.c1[g] * S;
+    in.rpq = rpq;
+    in.ruc = ruc;
+    in.p0 = d.p0[g];
+    in.pL = fmin(0.0, d.pmin[g]);
+    in.pU = d.pmax[g];
+    in.qL = fmin(0.0, d.qmin[g]);
+    in.qU = fmax(0.0, d.qmax[g]);
+    const double pmin = d.pmin[g], pmax = d.pmax[g], qmin = d.qmin[g], qmax = d.qmax[g];
+    const double rdn = d.rdn[g], sdn = d.sdn[g], rup = d.rup[g], sup = d.sup[g];
+    const double u0 = (double)d.u0[g];
+    for (int t = lane; t < T; t += 32) {
+        const size_t i = (size_t)g * T + t;
+        const double on = d.ub_on[i], su = d.ub_su[i], sd = d.ub_sd[i];
+        const double onp = t == 0 ? u0 : d.ub_on[i - 1];
+        in.first = t == 0;
+        in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) / rpq;
+        in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) / rpq;
+        in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / rpq;
+        in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) / ruc;
+        in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) / ruc;
+        in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) / ruc;
+        in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) / ruc;
+        in.brl = -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) / ruc;
+        in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) / ruc;
+        double po, qo, pho;
+        gen_solve(in, po, qo, pho);
+        d.p[i] = po;
+        d.q[i] = qo;
+        d.ph[i] = pho;
+    }
+}
+
+__global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
+                           const int *hold, int8_t *sched, double *cost) {
+    extern __shared__ __align__(16) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (g >= G) return;
+    DpSmem s = dp_carve(smem + (size_t)warp * dp_smem_bytes(T), T);
+    for (int k = lane; k < T * 4; k += 32) s.L[k] = L[(size_t)g * T * 4 + k];
+    __syncwarp();
+    double c = dp_warp(s, T, tu[g], td[g], u0[g], hold[g]);
+    for (int t = lane; t < T; t += 32) sched[(size_t)g * T + t] = s.u[t];
+    if (lane == 0) cost[g] = c;
+}
+
+// ---------------------------------------------------------------- cold start (S0)
+__global__ void k_init(Dev d, const int8_t *u_init) {
+    const int T = d.T;
+    const long long GT = (long long)d.G * T, LT = (long long)d.L * T, BT = (long long)d.B * T;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < GT + LT + BT;
+         k += (long long)gridDim.x * blockDim.x) {
+        if (k < GT) {
+            const int g = (int)(k / T), t = (int)(k - (long long)g * T);
+            const int ut = u_init ? u_init[k] : d.u0[g];
+            const int up = t == 0 ? d.u0[g] : (u_init ? u_init[k - 1] : d.u0[g]);
+            const double pm = 0.5 * (d.pmin[g] + d.pmax[g]);
+            d.u[k] = (int8_t)ut;
+            d.p[k] = pm;
+            d.q[k] = 0.5 * (d.qmin[g] + d.qmax[g]);
+            d.ph[k] = t == 0 ? d.p0[g] : pm;
+            d.ub_on[k] = (double)ut;
+            d.ub_su[k] = ut > up ? 1.0 : 0.0;
+            d.ub_sd[k] = up > ut ? 1.0 : 0.0;
+            d.pbar[k] = pm;
+            d.qbar[k] = d.q[k];
+        } else if (k < GT + LT) {
+            const long long kk = k - GT;
+            const int l = (int)(kk / T);
+            const int i = d.bfrom[l], j = d.bto[l];
+            const double vi = 0.5 * (d.vmin[i] + d.vmax[i]), vj = 0.5 * (d.vmin[j] + d.vmax[j]);
+            const double wi = vi * vi, wj = vj * vj;
+            const double R = sqrt(wi * wj);
+            const double C = R * cos(0.0), S = R * sin(0.0);
+            const double Gii = d.y[0 * d.L + l], Gij = d.y[1 * d.L + l], Gji = d.y[2 * d.L + l], Gjj = d.y[3 * d.L + l];
+            const double Bii = d.y[4 * d.L + l], Bij = d.y[5 * d.L + l], Bji = d.y[6 * d.L + l], Bjj = d.y[7 * d.L + l];
+            // Eq. 2e-2h, evaluated in the oracle's order (a w_i + b w_j) + c C + d S
+            const double f0 = Gii * wi + 0.0 * wj + Gij * C + Bij * S;
+            const double f1 = -Bii * wi + 0.0 * wj + -Bij * C + Gij * S;
+            const double f2 = 0.0 * wi + Gjj * wj + Gji * C + -Bji * S;
+            const double f3 = 0.0 * wi + -Bjj * wj + -Bji * C + -Gji * S;
+            const double r = d.rate[l];
+            d.x[0 * LT + kk] = wi;
+            d.x[1 * LT + kk] = wj;
+            d.x[2 * LT + kk] = 0.0;
+            d.x[3 * LT + kk] = 0.0;
+            d.f[0 * LT + kk] = f0; d.f[1 * LT + kk] = f1; d.f[2 * LT + kk] = f2; d.f[3 * LT + kk] = f3;
+            d.fbar[0 * LT + kk] = f0; d.fbar[1 * LT + kk] = f1; d.fbar[2 * LT + kk] = f2; d.fbar[3 * LT + kk] = f3;
+            d.al[0 * LT + kk] = 0.0;
+            d.al[1 * LT + kk] = 0.0;
+            d.al[2 * LT + kk] = d.al_sigma0_rel * d.rpq * (r * r);
+        } else {
+            const long long kk = k - GT - LT;
+            const int i = (int)(kk / T);
+            const double v = 0.5 * (d.vmin[i] + d.vmax[i]);
+            d.wbar[kk] = v * v;
+            d.thbar[kk] = 0.0;
+        }
+    }
+}
+
+}  // namespace
+
+static size_t gen_smem(int T, int warps) { return dp_smem_bytes(T) * warps; }
+
+void launch_gen(const Dev &d, cudaStream_t s) {
+    const int warps = 4;
+    k_gen<<<(d.G + warps - 1) / warps, warps * 32, gen_smem(d.T, warps), s>>>(d);
+}
+
+void launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
+                     const int *hold, int8_t *sched, double *cost, cudaStream_t s) {
+    const int warps = 4;
+    k_dp_batch<<<(G + warps - 1) / warps, warps * 32, gen_smem(T, warps), s>>>(G, T, L, tu, td, u0, hold,
+                                                                                sched, cost);
+}
+
+void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s) {
+    k_init<<<296, 256, 0, s>>>(d, u_init_dev);
+}
+
+size_t gen_smem_bytes(int T) { return gen_smem(T, 4); }
+cudaError_t gen_set_smem_attr(int T) {
+    size_t b = gen_smem(T, 4);
+    cudaError_t e = cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+}
+
+}  // namespace ucac

@@ -1,0 +1,496 @@
+// k_sweep.cu -- steps (7c) ubar, (7d) bus, (7e) z, (7f) y for every coupling row, the
+// residual/objective partial reductions (S8), the final reduction with the inner test and
+// the outer (lambda, beta) decision (S9).  Compiled with -fmad=false (operation
+// order as written, matching the oracle's definitions).
+//
+// Ownership (no write conflicts, no atomics): every coupling row's xbar side, z and y are
+// written by exactly one thread:
+//   k_bus   thread (i,t): the generator copies pbar_g,t, qbar_g,t of g at i (rows GP_t, GQ_t and
+//           RC_{t+1}), the flow copies of every branch end at i (FP, FQ) and wbar_i,t, thbar_i,t
+//           (rows W, A of every end at i);
+//   k_ubar  thread (g,t): the group (ubar^on_t, ubar^sd_t, ubar^su_{t+1}) and its rows D_ON_t,
+//           D_SD_t, PL_t..RD_t, D_SU_{t+1}, RU_{t+1}; thread (g,0) also group 0 (ubar^su_1).
+// The outer update lambda <- clip(lambda + beta z) decided at the end of iteration l is
+// applied lazily by the owning thread at the start of its row update in iteration l+1 (the
+// x-steps never read lambda), which saves a full pass over all rows.
+#include "ucac_dev.cuh"
+
+namespace ucac {
+namespace {
+
+struct Acc {
+    double v[NPART];
+    __device__ Acc() {
+#pragma unroll
+        for (int k = 0; k < NPART; k++) v[k] = 0.0;
+    }
+};
+
+// (7e) z = -(lambda + y + rho r)/(beta + rho), (7f) y += rho (r + z); S8 terms
+__device__ __forceinline__ void zy_row(double r, double rho, double beta, double *zp, double *yp, double *lp,
+                                       int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+    double lam = *lp;
+    double zo = *zp;
+    if (pending) {
+        double v = lam + beta_lam * zo;
+        lam = v < -lmax ? -lmax : (v > lmax ? lmax : v);
+        *lp = lam;
+    }
+    double y = *yp;
+    double zz = -((lam + y) + rho * r) / (beta + rho);
+    *zp = zz;
+    *yp = y + rho * (r + zz);
+    double rz = r + zz;
+    a.v[P_PINF] = fmax(a.v[P_PINF], fabs(r));
+    a.v[P_RZINF] = fmax(a.v[P_RZINF], fabs(rz));
+    a.v[P_RZ2] = a.v[P_RZ2] + rz * rz;
+    a.v[P_ZINF] = fmax(a.v[P_ZINF], fabs(zz));
+    a.v[P_Z2] = a.v[P_Z2] + zz * zz;
+    a.v[P_DINF] = fmax(a.v[P_DINF], rho * fabs(dxb));
+    if (!isfinite(r) || !isfinite(zz)) a.v[P_BAD] = 1.0;
+}
+
+// deterministic block reduction -> part[blockIdx.x][NPART]
+__device__ void block_reduce_store(Acc &a, double *part) {
+    __shared__ double sh[32][NPART];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NPART; k++) {
+        double v = a.v[k];
+        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            double w = __shfl_down_sync(0xffffffffu, v, o);
+            v = isum ? v + w : fmax(v, w);
+        }
+        if (lane == 0) sh[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NPART) {
+        const int k = threadIdx.x;
+        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
+        double v = sh[0][k];
+        for (int w = 1; w < nw; w++) v = isum ? v + sh[w][k] : fmax(v, sh[w][k]);
+        part[(size_t)blockIdx.x * NPART + k] = v;
+    }
+}
+
+#define ZG(k, i) d.zg[(size_t)(k) * GT + (i)]
+#define YG(k, i) d.yg[(size_t)(k) * GT + (i)]
+#define LG(k, i) d.lg[(size_t)(k) * GT + (i)]
+#define ZB(k, i) d.zb[(size_t)(k) * LT + (i)]
+#define YB(k, i) d.yb[(size_t)(k) * LT + (i)]
+#define LB(k, i) d.lb[(size_t)(k) * LT + (i)]
+#define FX(k, i) d.f[(size_t)(k) * LT + (i)]
+#define FB(k, i) d.fbar[(size_t)(k) * LT + (i)]
+#define XX(k, i) d.x[(size_t)(k) * LT + (i)]
+
+constexpr int BUS_THREADS = 128;
+constexpr int UBAR_THREADS = 128;
+
+// ------------------------------------------------------------------------- (7d) bus
+__global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t GT = (size_t)d.G * T, LT = (size_t)d.L * T;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const double rpq = d.rpq, rva = d.rva;
+    const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
+    const int pending = d.st->pending_outer;
+    Acc acc;
+    if (k < d.B * T) {
+        const int i = k / T, t = k - i * T;
+        const int g0 = d.bg_ptr[i], g1 = d.bg_ptr[i + 1];
+        const int e0 = d.be_ptr[i], e1 = d.be_ptr[i + 1];
+        const int ne = e1 - e0;
+        // ---- pass 1: sums of the 2x2 KKT system, canonical order (gens, ends, wbar)
+        double AP = 0.0, AQ = 0.0, C = 0.0, rP = d.pd[k], rQ = d.qd[k];
+        for (int a = g0; a < g1; a++) {
+            const size_t gi = (size_t)d.bg_idx[a] * T + t;
+            const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) / rpq;
+            double th, aa;
+            if (t < T - 1) {
+                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) / rpq;
+                th = (tgp + trc) * 0.5;
+                aa = 2.0 * rpq;
+            } else {
+                th = tgp;
+                aa = rpq;
+            }
+            AP = AP + 1.0 / aa;
+            rP = rP - th;
+            const double thq = d.q[gi] + ZG(G_GQ, gi) + YG(G_GQ, gi) / rpq;
+            AQ = AQ + 1.0 / rpq;
+            rQ = rQ - thq;
+        }
+        double wsum = 0.0, tsum = 0.0;
+        for (int a = e0; a < e1; a++) {
+            const int code = d.be_idx[a];
+            const int l = code >> 1, side = code & 1;
+            const size_t li = (size_t)l * T + t;
+            const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
+            const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
+            const double thp = FX(kp, li) + ZB(kp, li) + YB(kp, li) / rpq;
+            AP = AP + 1.0 / rpq;
+            rP = rP + thp;
+            const double thq = FX(kq, li) + ZB(kq, li) + YB(kq, li) / rpq;
+            AQ = AQ + 1.0 / rpq;
+            rQ = rQ + thq;
+            wsum = wsum + (XX(side ? 1 : 0, li) + ZB(kw, li) + YB(kw, li) / rva);
+            tsum = tsum + (XX(side ? 3 : 2, li) + ZB(ka, li) + YB(ka, li) / rva);
+        }
+        const double thw = wsum / (double)ne;
+        const double aw = (double)ne * rva;
+        const double alw = -d.gs[i], bew = d.bs[i];
+        AP = AP + alw * alw / aw;
+        AQ = AQ + bew * bew / aw;
+        C = C + alw * bew / aw;
+        rP = rP - alw * thw;
+        rQ = rQ - bew * thw;
+        const double det = AP * AQ - C * C;
+        const double muP = (rP * AQ - C * rQ) / det;
+        const double muQ = (AP * rQ - C * rP) / det;
+        // ---- pass 2: copies (v = tauhat + (alpha muP + beta muQ)/a) and their rows
+        for (int a = g0; a < g1; a++) {
+            const size_t gi = (size_t)d.bg_idx[a] * T + t;
+            const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) / rpq;
+            double th, aa, trc = 0.0;
+            if (t < T - 1) {
+                trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) / rpq;
+                th = (tgp + trc) * 0.5;
+                aa = 2.0 * rpq;
+            } else {
+                th = tgp;
+                aa = rpq;
+            }
+            const double pb = th + muP / aa;
+            const double thq = d.q[gi] + ZG(G_GQ, gi) + YG(G_GQ, gi) / rpq;
+            const double qb = thq + muQ / rpq;
+            const double pbo = d.pbar[gi], qbo = d.qbar[gi];
+            d.pbar[gi] = pb;
+            d.qbar[gi] = qb;
+            zy_row(d.p[gi] - pb, rpq, beta, &ZG(G_GP, gi), &YG(G_GP, gi), &LG(G_GP, gi), pending, beta_lam, lmax,
+                   pb - pbo, acc);
+            zy_row(d.q[gi] - qb, rpq, beta, &ZG(G_GQ, gi), &YG(G_GQ, gi), &LG(G_GQ, gi), pending, beta_lam, lmax,
+                   qb - qbo, acc);
+            if (t < T - 1)
+                zy_row(d.ph[gi + 1] - pb, rpq, beta, &ZG(G_RC, gi + 1), &YG(G_RC, gi + 1), &LG(G_RC, gi + 1),
+                       pending, beta_lam, lmax, pb - pbo, acc);
+        }
+        const double wb = thw + (alw * muP + bew * muQ) / aw;
+        const double tb = (i == d.ref_bus) ? 0.0 : tsum / (double)ne;
+        const double wbo = d.wbar[k], tbo = d.thbar[k];
+        d.wbar[k] = wb;
+        d.thbar[k] = tb;
+        for (int a = e0; a < e1; a++) {
+            const int code = d.be_idx[a];
+            const int l = code >> 1, side = code & 1;
+            const size_t li = (size_t)l * T + t;
+            const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
+            const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
+            const double fp = FX(kp, li), fq = FX(kq, li);
+            const double pb = (fp + ZB(kp, li) + YB(kp, li) / rpq) + (-muP) / rpq;
+            const double qb = (fq + ZB(kq, li) + YB(kq, li) / rpq) + (-muQ) / rpq;
+            const double pbo = FB(kp, li), qbo = FB(kq, li);
+            FB(kp, li) = pb;
+            FB(kq, li) = qb;
+            zy_row(fp - pb, rpq, beta, &ZB(kp, li), &YB(kp, li), &LB(kp, li), pending, beta_lam, lmax, pb - pbo, acc);
+            zy_row(fq - qb, rpq, beta, &ZB(kq, li), &YB(kq, li), &LB(kq, li), pending, beta_lam, lmax, qb - qbo, acc);
+            zy_row(XX(side ? 1 : 0, li) - wb, rva, beta, &ZB(kw, li), &YB(kw, li), &LB(kw, li), pending, beta_lam,
+                   lmax, wb - wbo, acc);
+            zy_row(XX(side ? 3 : 2, li) - tb, rva, beta, &ZB(ka, li), &YB(ka, li), &LB(ka, li), pending, beta_lam,
+                   lmax, tb - tbo, acc);
+        }
+    }
+    block_reduce_store(acc, d.part_bus);
+}
+
+// ------------------------------------------------------------------------- (7c) ubar
+__device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+__device__ void solve_small(int nf, double A[3][3], const double *b, double *x) {
+    if (nf == 1) {
+        x[0] = b[0] / A[0][0];
+        return;
+    }
+    if (nf == 2) {
+        double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+        x[0] = (b[0] * A[1][1] - A[0][1] * b[1]) / det;
+        x[1] = (A[0][0] * b[1] - b[0] * A[1][0]) / det;
+        return;
+    }
+    double det = A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1]) - A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+                 A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+    for (int k = 0; k < 3; k++) {
+        double M[3][3];
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) M[i][j] = (j == k) ? b[i] : A[i][j];
+        double dk = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) - M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                    M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+        x[k] = dk / det;
+    }
+}
+
+// exact box-QP over [0,1]^n, n <= 3, by the 3^n activity states
+__device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, double *v) {
+    double H[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, bb[3] = {0, 0, 0};
+    for (int i = 0; i < n; i++) {
+        for (int j = 0; j < n; j++) {
+            double s = 0.0;
+            for (int k = 0; k < m; k++) s = s + c[k][i] * c[k][j];
+            H[i][j] = s;
+        }
+        double s = 0.0;
+        for (int k = 0; k < m; k++) s = s + c[k][i] * e[k];
+        bb[i] = s;
+    }
+    int ncand = n == 3 ? 27 : (n == 2 ? 9 : 3);
+    double best = INFINITY;
+    for (int i = 0; i < n; i++) v[i] = 0.0;
+    for (int idx = 0; idx < ncand; idx++) {
+        int st[3], r = idx;
+        for (int i = 0; i < n; i++) {
+            st[i] = r % 3;
+            r /= 3;
+        }
+        double vv[3] = {0, 0, 0};
+        int fi[3], nf = 0;
+        for (int i = 0; i < n; i++) {
+            if (st[i] == 0) fi[nf++] = i;
+            else vv[i] = (st[i] == 1) ? 0.0 : 1.0;
+        }
+        if (nf > 0) {
+            double A[3][3], rhs[3], sol[3];
+            for (int a = 0; a < nf; a++) {
+                double s = bb[fi[a]];
+                for (int j = 0; j < n; j++)
+                    if (st[j] != 0) s = s - H[fi[a]][j] * vv[j];
+                rhs[a] = s;
+                for (int b2 = 0; b2 < nf; b2++) A[a][b2] = H[fi[a]][fi[b2]];
+            }
+            solve_small(nf, A, rhs, sol);
+            for (int a = 0; a < nf; a++) vv[fi[a]] = sol[a];
+        }
+        for (int i = 0; i < n; i++) vv[i] = clamp01(vv[i]);
+        double obj = 0.0;
+        for (int k = 0; k < m; k++) {
+            double rr = e[k];
+            for (int i = 0; i < n; i++) rr = rr - c[k][i] * vv[i];
+            obj = obj + 0.5 * rr * rr;
+        }
+        if (obj < best) {
+            best = obj;
+            for (int i = 0; i < n; i++) v[i] = vv[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t GT = (size_t)d.G * T;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const double ruc = d.ruc;
+    const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
+    const int pending = d.st->pending_outer;
+    Acc acc;
+    if (k < d.G * T) {
+        const int g = k / T, t = k - g * T;
+        const size_t i = (size_t)k;
+        const double Pm = d.pmin[g], PM = d.pmax[g], Qm = d.qmin[g], QM = d.qmax[g];
+        const double RDn = d.rdn[g], SDn = d.sdn[g], RUp = d.rup[g], SUp = d.sup[g];
+        const int u0 = d.u0[g];
+        // old group values (iterate l) -- the x-step's shifted bounds use them (R19)
+        const double on_o = d.ub_on[i], sd_o = d.ub_sd[i], su_o = d.ub_su[i];
+        const double onp_o = t == 0 ? (double)u0 : d.ub_on[i - 1];
+        const int ut = d.u[i], up = t == 0 ? u0 : d.u[i - 1];
+        const int sdt = up > ut, sut = ut > up;
+        const double p = d.p[i], q = d.q[i], ph = d.ph[i];
+        // slacks (x-variables of 7b) recomputed exactly as the x-step defines them
+        const double bpl = Pm * on_o - ZG(G_PL, i) - YG(G_PL, i) / ruc;
+        const double bpu = PM * on_o - ZG(G_PU, i) - YG(G_PU, i) / ruc;
+        const double bql = Qm * on_o - ZG(G_QL, i) - YG(G_QL, i) / ruc;
+        const double bqu = QM * on_o - ZG(G_QU, i) - YG(G_QU, i) / ruc;
+        const double brl = -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) / ruc;
+        const double dd = p - ph;
+        const double spl = fmax(0.0, p - bpl), spu = fmax(0.0, bpu - p);
+        const double sql = fmax(0.0, q - bql), squ = fmax(0.0, bqu - q);
+        const double srd = fmax(0.0, dd - brl);
+        double cm[9][3], e[9];
+        int m = 0;
+#define ROW(a0, a1, a2, ev)   \
+    do {                      \
+        cm[m][0] = (a0);      \
+        cm[m][1] = (a1);      \
+        cm[m][2] = (a2);      \
+        e[m++] = (ev);        \
+    } while (0)
+        ROW(1.0, 0.0, 0.0, (double)ut + ZG(G_DON, i) + YG(G_DON, i) / ruc);
+        ROW(0.0, 1.0, 0.0, (double)sdt + ZG(G_DSD, i) + YG(G_DSD, i) / ruc);
+        ROW(Pm, 0.0, 0.0, (p - spl) + ZG(G_PL, i) + YG(G_PL, i) / ruc);
+        ROW(PM, 0.0, 0.0, (p + spu) + ZG(G_PU, i) + YG(G_PU, i) / ruc);
+        ROW(Qm, 0.0, 0.0, (q - sql) + ZG(G_QL, i) + YG(G_QL, i) / ruc);
+        ROW(QM, 0.0, 0.0, (q + squ) + ZG(G_QU, i) + YG(G_QU, i) / ruc);
+        ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) / ruc);
+        int n = 2;
+        int sun = 0;
+        double pn = 0.0, phn = 0.0, sru_n = 0.0, su_on = 0.0;
+        if (t < T - 1) {
+            const size_t j = i + 1;
+            const int un = d.u[j];
+            sun = un > ut;
+            pn = d.p[j];
+            phn = d.ph[j];
+            su_on = d.ub_su[j];
+            const double bru_n = RUp * on_o + SUp * su_on - ZG(G_RU, j) - YG(G_RU, j) / ruc;
+            sru_n = fmax(0.0, bru_n - (pn - phn));
+            ROW(0.0, 0.0, 1.0, (double)sun + ZG(G_DSU, j) + YG(G_DSU, j) / ruc);
+            ROW(RUp, 0.0, SUp, ((pn - phn) + sru_n) + ZG(G_RU, j) + YG(G_RU, j) / ruc);
+            n = 3;
+        }
+#undef ROW
+        double v[3];
+        boxqp3(n, m, cm, e, v);
+        const double on_n = v[0], sd_n = v[1];
+        d.ub_on[i] = on_n;
+        d.ub_sd[i] = sd_n;
+        // rows of the group with the new ubar (r = x-part - c'ubar)
+        const double don = on_n - on_o, dsd = sd_n - sd_o;
+        zy_row((double)ut - on_n, ruc, beta, &ZG(G_DON, i), &YG(G_DON, i), &LG(G_DON, i), pending, beta_lam, lmax, don, acc);
+        zy_row((double)sdt - sd_n, ruc, beta, &ZG(G_DSD, i), &YG(G_DSD, i), &LG(G_DSD, i), pending, beta_lam, lmax, dsd, acc);
+        zy_row((p - spl) - Pm * on_n, ruc, beta, &ZG(G_PL, i), &YG(G_PL, i), &LG(G_PL, i), pending, beta_lam, lmax, Pm * don, acc);
+        zy_row((p + spu) - PM * on_n, ruc, beta, &ZG(G_PU, i), &YG(G_PU, i), &LG(G_PU, i), pending, beta_lam, lmax, PM * don, acc);
+        zy_row((q - sql) - Qm * on_n, ruc, beta, &ZG(G_QL, i), &YG(G_QL, i), &LG(G_QL, i), pending, beta_lam, lmax, Qm * don, acc);
+        zy_row((q + squ) - QM * on_n, ruc, beta, &ZG(G_QU, i), &YG(G_QU, i), &LG(G_QU, i), pending, beta_lam, lmax, QM * don, acc);
+        zy_row((dd - srd) + RDn * on_n + SDn * sd_n, ruc, beta, &ZG(G_RD, i), &YG(G_RD, i), &LG(G_RD, i), pending, beta_lam,
+               lmax, RDn * don + SDn * dsd, acc);
+        if (t < T - 1) {
+            const size_t j = i + 1;
+            const double su_n = v[2];
+            d.ub_su[j] = su_n;
+            const double dsu = su_n - su_on;
+            zy_row((double)sun - su_n, ruc, beta, &ZG(G_DSU, j), &YG(G_DSU, j), &LG(G_DSU, j), pending, beta_lam, lmax, dsu,
+                   acc);
+            zy_row(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, beta, &ZG(G_RU, j), &YG(G_RU, j), &LG(G_RU, j),
+                   pending, beta_lam, lmax, RUp * don + SUp * dsu, acc);
+        }
+        if (t == 0) {
+            // group 0 = (ubar^su_1): rows D_SU_1, RU_1 (ubar^on_0 := u0, R4)
+            const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) / ruc;
+            const double sru = fmax(0.0, bru - dd);
+            double c1[2][3] = {{1.0, 0.0, 0.0}, {SUp, 0.0, 0.0}};
+            double e1[2];
+            e1[0] = (double)sut + ZG(G_DSU, i) + YG(G_DSU, i) / ruc;
+            e1[1] = (dd + sru) - RUp * (double)u0 + ZG(G_RU, i) + YG(G_RU, i) / ruc;
+            double v1[3];
+            boxqp3(1, 2, c1, e1, v1);
+            d.ub_su[i] = v1[0];
+            const double dsu = v1[0] - su_o;
+            zy_row((double)sut - v1[0], ruc, beta, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
+                   acc);
+            zy_row((dd + sru) - RUp * (double)u0 - SUp * v1[0], ruc, beta, &ZG(G_RU, i), &YG(G_RU, i), &LG(G_RU, i),
+                   pending, beta_lam, lmax, SUp * dsu, acc);
+        }
+        // objective, Eq. 1a with f^OPF = c2 (S p)^2 + c1 S p and f^UC (R13)
+        const double Sp = d.S * p;
+        acc.v[P_OBJ] = d.c2[g] * Sp * Sp + d.c1[g] * Sp + d.c0[g] * (double)ut + d.csu[g] * (double)sut +
+                       d.csd[g] * (double)sdt;
+    }
+    block_reduce_store(acc, d.part_ubar);
+}
+
+// ------------------------------------------------------------------------- S8 / S9
+__global__ void __launch_bounds__(256) k_reduce(Dev d) {
+    if (d.st->done) return;
+    __shared__ double sh[256][NPART];
+    const int tid = threadIdx.x;
+    double v[NPART];
+#pragma unroll
+    for (int k = 0; k < NPART; k++) v[k] = 0.0;
+    const int nb = d.nblk_bus, nu = d.nblk_ubar;
+    for (int b = tid; b < nb + nu; b += 256) {
+        const double *pp = b < nb ? d.part_bus + (size_t)b * NPART : d.part_ubar + (size_t)(b - nb) * NPART;
+#pragma unroll
+        for (int k = 0; k < NPART; k++) {
+            const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
+            v[k] = isum ? v[k] + pp[k] : fmax(v[k], pp[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NPART; k++) sh[tid][k] = v[k];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (tid < s) {
+#pragma unroll
+            for (int k = 0; k < NPART; k++) {
+                const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
+                sh[tid][k] = isum ? sh[tid][k] + sh[tid + s][k] : fmax(sh[tid][k], sh[tid + s][k]);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        DevStatus *st = d.st;
+        st->primal_inf = sh[0][P_PINF];
+        st->rz_inf = sh[0][P_RZINF];
+        st->rz_2 = sqrt(sh[0][P_RZ2]);
+        st->z_inf = sh[0][P_ZINF];
+        st->z_2 = sqrt(sh[0][P_Z2]);
+        st->dual_inf = sh[0][P_DINF];
+        st->objective = sh[0][P_OBJ];
+        st->tron_iters += d.cnt[0];
+        st->tron_capped += d.cnt[1];
+        st->al_active += d.cnt[2];
+        st->al_capped += d.cnt[3];
+        d.cnt[0] = d.cnt[1] = d.cnt[2] = d.cnt[3] = 0;
+        st->inner_total += 1;
+        st->inner_since += 1;
+        if ((sh[0][P_BAD] != 0.0 || !isfinite(sh[0][P_RZ2]) || !isfinite(sh[0][P_OBJ])) && st->err_kernel == 0) {
+            st->err_kernel = 1 + K_REDUCE;
+            st->err_iter = (int)st->inner_total;
+        }
+        st->pending_outer = 0;
+        if (d.outer_enabled && st->inner_since >= d.inner_min) {
+            const double thr = fmax(d.eps_inner_abs, 1e-2 / (double)st->outer_k);
+            if (st->rz_inf <= thr || st->inner_since >= d.inner_cap) {
+                const double zn = st->z_2;
+                st->pending_outer = 1;
+                st->beta_lam = st->beta;
+                if (st->outer_k > 1 && zn > d.theta * st->znorm_prev) st->beta = fmin(d.tau * st->beta, d.beta_max);
+                st->znorm_prev = zn;
+                st->outer_k += 1;
+                st->inner_since = 0;
+            }
+        }
+        if (st->stop_on_primal && st->primal_inf <= st->primal_target) st->done = 1;
+    }
+}
+
+// materialise a pending lambda update (before a state dump)
+__global__ void k_apply_outer(Dev d) {
+    if (!d.st->pending_outer) return;
+    const double bl = d.st->beta_lam, lmax = d.lambda_max;
+    const size_t ng = (size_t)NGROW * d.G * d.T, nbr = (size_t)NBROW * d.L * d.T;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < ng + nbr; k += (size_t)gridDim.x * blockDim.x) {
+        double *lp = k < ng ? d.lg + k : d.lb + (k - ng);
+        const double z = k < ng ? d.zg[k] : d.zb[k - ng];
+        const double v = *lp + bl * z;
+        *lp = v < -lmax ? -lmax : (v > lmax ? lmax : v);
+    }
+}
+__global__ void k_clear_pending(Dev d) { d.st->pending_outer = 0; }
+
+}  // namespace
+
+int nblk_bus(int B, int T) { return (B * T + BUS_THREADS - 1) / BUS_THREADS; }
+int nblk_ubar(int G, int T) { return (G * T + UBAR_THREADS - 1) / UBAR_THREADS; }
+
+void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d); }
+void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
+void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, 256, 0, s>>>(d); }
+void launch_apply_outer(const Dev &d, cudaStream_t s) {
+    k_apply_outer<<<296, 256, 0, s>>>(d);
+    k_clear_pending<<<1, 1, 0, s>>>(d);
+}
+
+}  // namespace ucac

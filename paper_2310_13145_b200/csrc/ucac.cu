@@ -1,0 +1,706 @@
+// ucac.cu -- host runtime of libucac.so: the C ABI of include/ucac.h.
+//
+// create: validate -> build the device layout (SoA, CSR incidence in canonical order) ->
+// cold start kernel.  iterate: a CUDA graph of U inner iterations (fork/join so that the
+// branch solves run concurrently with the generator DP/x-update, and the bus update with
+// the ubar update), launched back to back; no host round trip inside the loop.  The device
+// status word carries the inner test, the outer (lambda, beta) decision and the
+// stop-on-primal flag, so the host never has to look at the iterate.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ucac.h"
+#include "ucac_dev.cuh"
+
+namespace ucac {
+void launch_apply_outer(const Dev &d, cudaStream_t s);
+cudaError_t gen_set_smem_attr(int T);
+size_t gen_smem_bytes(int T);
+}  // namespace ucac
+
+using namespace ucac;
+
+static thread_local std::string g_create_err;
+
+struct ucac_ctx {
+    Dev d{};
+    int G = 0, L = 0, B = 0, T = 0;
+    cudaStream_t s = nullptr, s2 = nullptr;
+    bool own_stream = false;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int gunroll[2] = {1, 16};
+    std::vector<void *> dalloc;
+    DevStatus *st_host = nullptr;   // pinned mirror
+    std::string err;
+    std::vector<cudaEvent_t> tev;   // timed-iteration event pool
+    ucac_params prm{};
+    bool ctl_dirty = true;          // device control fields may hold a stop/done state
+};
+
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+            return UCAC_ECUDA;                                                             \
+        }                                                                                  \
+    } while (0)
+
+static ucac_status fail(ucac_ctx *ctx, ucac_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    else g_create_err = buf;
+    return s;
+}
+
+template <class Tp>
+static Tp *dnew(ucac_ctx *ctx, size_t n, cudaError_t &e) {
+    void *p = nullptr;
+    e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(Tp));
+    if (e == cudaSuccess) {
+        ctx->dalloc.push_back(p);
+        e = cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(Tp), ctx->s);
+    }
+    return (Tp *)p;
+}
+
+template <class Tp>
+static cudaError_t up(ucac_ctx *ctx, Tp *dst, const Tp *src, size_t n) {
+    return cudaMemcpyAsync(dst, src, n * sizeof(Tp), cudaMemcpyHostToDevice, ctx->s);
+}
+
+static bool finite_all(const double *a, size_t n) {
+    for (size_t i = 0; i < n; i++)
+        if (!std::isfinite(a[i])) return false;
+    return true;
+}
+
+static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co,
+                            const ucac_uc *uc, const ucac_params *p) {
+#define BAD(...) return fail(nullptr, UCAC_EINVAL, __VA_ARGS__)
+    if (!net || !hz || !co || !uc || !p) BAD("null argument");
+    const int B = net->nbus, G = net->ngen, L = net->nbranch, T = hz->T;
+    if (B <= 0 || G <= 0 || L <= 0 || T <= 0) BAD("empty problem: nbus=%d ngen=%d nbranch=%d T=%d", B, G, L, T);
+    if (net->ref_bus < 0 || net->ref_bus >= B) BAD("ref_bus %d out of range", net->ref_bus);
+    if (!(net->base_mva > 0)) BAD("base_mva must be > 0");
+    if (!(p->rho_pq > 0) || !(p->rho_va > 0) || !(p->rho_uc > 0)) BAD("rho must be > 0");
+    if (!(p->beta0 > 0) || !(p->tau > 1) || !(p->theta > 0 && p->theta < 1)) BAD("bad beta0/tau/theta");
+    const double *dd[] = {net->bus_gs, net->bus_bs, net->bus_vmin, net->bus_vmax};
+    for (auto a : dd)
+        if (!a || !finite_all(a, B)) BAD("bus arrays must be finite");
+    for (int i = 0; i < B; i++)
+        if (!(net->bus_vmin[i] > 0) || net->bus_vmin[i] > net->bus_vmax[i]) BAD("bus %d: need 0 < vmin <= vmax", i);
+    if (!hz->pd || !hz->qd || !finite_all(hz->pd, (size_t)T * B) || !finite_all(hz->qd, (size_t)T * B))
+        BAD("demand must be finite");
+    if (!net->br_from || !net->br_to || !net->br_y || !net->br_rate) BAD("branch arrays missing");
+    if (!finite_all(net->br_y, (size_t)L * 8) || !finite_all(net->br_rate, L)) BAD("branch data must be finite");
+    std::vector<int> deg(B, 0);
+    for (int l = 0; l < L; l++) {
+        int i = net->br_from[l], j = net->br_to[l];
+        if (i < 0 || i >= B || j < 0 || j >= B) BAD("branch %d: bus index out of range", l);
+        if (i == j) BAD("branch %d: from == to", l);
+        if (net->br_rate[l] < 0) BAD("branch %d: negative rate", l);
+        deg[i]++;
+        deg[j]++;
+    }
+    for (int i = 0; i < B; i++)
+        if (deg[i] == 0) BAD("bus %d has no branch (bus 2x2 system singular)", i);
+    const double *gd[] = {net->gen_pmin, net->gen_pmax, net->gen_qmin, net->gen_qmax, co->c2, co->c1, co->c0,
+                          co->startup, co->shutdown, uc->ramp_up, uc->ramp_dn, uc->su_ramp, uc->sd_ramp, uc->p0};
+    for (auto a : gd)
+        if (!a || !finite_all(a, G)) BAD("generator arrays must be finite");
+    if (!net->gen_bus || !uc->min_up || !uc->min_dn || !uc->u0 || !uc->hold) BAD("generator index arrays missing");
+    for (int g = 0; g < G; g++) {
+        if (net->gen_bus[g] < 0 || net->gen_bus[g] >= B) BAD("gen %d: bus out of range", g);
+        if (net->gen_pmin[g] > net->gen_pmax[g]) BAD("gen %d: pmin > pmax", g);
+        if (net->gen_qmin[g] > net->gen_qmax[g]) BAD("gen %d: qmin > qmax", g);
+        if (co->c2[g] < 0) BAD("gen %d: c2 < 0", g);
+        if (uc->min_up[g] < 1 || uc->min_up[g] > T || uc->min_dn[g] < 1 || uc->min_dn[g] > T)
+            BAD("gen %d: min up/down must be in [1, T] (R15)", g);
+        if (uc->u0[g] != 0 && uc->u0[g] != 1) BAD("gen %d: u0 must be 0/1", g);
+        if (uc->hold[g] < 0 || uc->hold[g] > T) BAD("gen %d: hold must be in [0, T]", g);
+    }
+    if (uc->u_init)
+        for (size_t k = 0; k < (size_t)G * T; k++)
+            if (uc->u_init[k] != 0 && uc->u_init[k] != 1) BAD("u_init must be 0/1");
+    if (p->tron_maxit < 1 || p->al_maxit < 1 || p->inner_min < 0 || p->inner_cap < 1) BAD("bad iteration caps");
+    return UCAC_OK;
+#undef BAD
+}
+
+static ucac_status build_graphs(ucac_ctx *ctx);
+
+extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co,
+                                   const ucac_uc *uc, const ucac_params *prm, const ucac_dist *dist,
+                                   void *cuda_stream, ucac_ctx **out) {
+    if (!out) return fail(nullptr, UCAC_EINVAL, "out is NULL");
+    *out = nullptr;
+    ucac_status vs = validate(net, hz, co, uc, prm);
+    if (vs != UCAC_OK) return vs;
+    if (dist && dist->nranks > 1)
+        return fail(nullptr, UCAC_EUNSUPPORTED, "multi-rank contexts: use the partitioned runtime (DESIGN.md 9)");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "%s", cudaGetErrorString(e));
+    if (prop.major != 10) return fail(nullptr, UCAC_ECUDA, "libucac is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+
+    ucac_ctx *ctx = new ucac_ctx();
+    ctx->prm = *prm;
+    const int B = net->nbus, G = net->ngen, L = net->nbranch, T = hz->T;
+    ctx->B = B; ctx->G = G; ctx->L = L; ctx->T = T;
+    auto bail = [&](ucac_status s) {
+        g_create_err = ctx->err;
+        ucac_destroy(ctx);
+        return s;
+    };
+    if (cuda_stream) {
+        ctx->s = (cudaStream_t)cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "stream"));
+        ctx->own_stream = true;
+    }
+    if (cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
+    if (cudaMallocHost(&ctx->st_host, sizeof(DevStatus)) != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
+    memset(ctx->st_host, 0, sizeof(DevStatus));
+
+    Dev &d = ctx->d;
+    d.G = G; d.L = L; d.B = B; d.T = T;
+    d.ref_bus = net->ref_bus;
+    d.S = net->base_mva;
+    d.rpq = prm->rho_pq; d.rva = prm->rho_va; d.ruc = prm->rho_uc;
+    d.tau = prm->tau; d.theta = prm->theta; d.lambda_max = prm->lambda_max; d.beta_max = prm->beta_max;
+    d.eps_inner_abs = prm->eps_inner_abs;
+    d.inner_min = prm->inner_min; d.inner_cap = prm->inner_cap; d.outer_enabled = prm->outer_enabled;
+    d.tron_gtol = prm->tron_gtol_rel * std::max(prm->rho_pq, prm->rho_va);
+    d.tron_maxit = prm->tron_maxit; d.al_maxit = prm->al_maxit;
+    d.al_eta_star = prm->al_eta_star; d.al_sigma0_rel = prm->al_sigma0_rel;
+    d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
+    d.nblk_bus = nblk_bus(B, T);
+    d.nblk_ubar = nblk_ubar(G, T);
+
+    const size_t GT = (size_t)G * T, LT = (size_t)L * T, BT = (size_t)B * T;
+#define ALLOC(field, type, n)                                   \
+    do {                                                        \
+        auto p_ = dnew<type>(ctx, (n), e);                      \
+        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc %s", #field)); \
+        d.field = p_;                                           \
+    } while (0)
+#define UPLOAD(field, type, src, n)                             \
+    do {                                                        \
+        type *p_ = dnew<type>(ctx, (n), e);                     \
+        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc %s", #field)); \
+        if (up<type>(ctx, p_, (src), (n)) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "upload %s", #field)); \
+        d.field = p_;                                           \
+    } while (0)
+    // static generator data
+    UPLOAD(gbus, int, net->gen_bus, G);
+    UPLOAD(tu, int, uc->min_up, G);
+    UPLOAD(td, int, uc->min_dn, G);
+    UPLOAD(u0, int, uc->u0, G);
+    UPLOAD(hold, int, uc->hold, G);
+    UPLOAD(pmin, double, net->gen_pmin, G);
+    UPLOAD(pmax, double, net->gen_pmax, G);
+    UPLOAD(qmin, double, net->gen_qmin, G);
+    UPLOAD(qmax, double, net->gen_qmax, G);
+    UPLOAD(c2, double, co->c2, G);
+    UPLOAD(c1, double, co->c1, G);
+    UPLOAD(c0, double, co->c0, G);
+    UPLOAD(csu, double, co->startup, G);
+    UPLOAD(csd, double, co->shutdown, G);
+    UPLOAD(rup, double, uc->ramp_up, G);
+    UPLOAD(rdn, double, uc->ramp_dn, G);
+    UPLOAD(sup, double, uc->su_ramp, G);
+    UPLOAD(sdn, double, uc->sd_ramp, G);
+    UPLOAD(p0, double, uc->p0, G);
+    // branch data, admittance as SoA [8][L]
+    std::vector<double> ysoa((size_t)8 * L);
+    for (int l = 0; l < L; l++)
+        for (int k = 0; k < 8; k++) ysoa[(size_t)k * L + l] = net->br_y[(size_t)l * 8 + k];
+    UPLOAD(y, double, ysoa.data(), (size_t)8 * L);
+    UPLOAD(rate, double, net->br_rate, L);
+    UPLOAD(bfrom, int, net->br_from, L);
+    UPLOAD(bto, int, net->br_to, L);
+    // bus data, demand transposed to [B][T]
+    UPLOAD(gs, double, net->bus_gs, B);
+    UPLOAD(bs, double, net->bus_bs, B);
+    UPLOAD(vmin, double, net->bus_vmin, B);
+    UPLOAD(vmax, double, net->bus_vmax, B);
+    std::vector<double> pdT(BT), qdT(BT);
+    for (int t = 0; t < T; t++)
+        for (int i = 0; i < B; i++) {
+            pdT[(size_t)i * T + t] = hz->pd[(size_t)t * B + i];
+            qdT[(size_t)i * T + t] = hz->qd[(size_t)t * B + i];
+        }
+    UPLOAD(pd, double, pdT.data(), BT);
+    UPLOAD(qd, double, qdT.data(), BT);
+    // CSR incidence, canonical order: generators by index, ends by (l, side)
+    std::vector<int> bgp(B + 1, 0), bep(B + 1, 0), bgi(G), bei((size_t)2 * L);
+    for (int g = 0; g < G; g++) bgp[net->gen_bus[g] + 1]++;
+    for (int l = 0; l < L; l++) {
+        bep[net->br_from[l] + 1]++;
+        bep[net->br_to[l] + 1]++;
+    }
+    for (int i = 0; i < B; i++) {
+        bgp[i + 1] += bgp[i];
+        bep[i + 1] += bep[i];
+    }
+    {
+        std::vector<int> fg(B, 0), fe(B, 0);
+        for (int g = 0; g < G; g++) {
+            int i = net->gen_bus[g];
+            bgi[bgp[i] + fg[i]++] = g;
+        }
+        for (int l = 0; l < L; l++) {
+            int i = net->br_from[l], j = net->br_to[l];
+            bei[bep[i] + fe[i]++] = 2 * l;
+            bei[bep[j] + fe[j]++] = 2 * l + 1;
+        }
+    }
+    UPLOAD(bg_ptr, int, bgp.data(), B + 1);
+    UPLOAD(bg_idx, int, bgi.data(), G);
+    UPLOAD(be_ptr, int, bep.data(), B + 1);
+    UPLOAD(be_idx, int, bei.data(), (size_t)2 * L);
+    // iterate
+    ALLOC(u, int8_t, GT);
+    ALLOC(p, double, GT);
+    ALLOC(q, double, GT);
+    ALLOC(ph, double, GT);
+    ALLOC(ub_on, double, GT);
+    ALLOC(ub_su, double, GT);
+    ALLOC(ub_sd, double, GT);
+    ALLOC(pbar, double, GT);
+    ALLOC(qbar, double, GT);
+    ALLOC(zg, double, NGROW * GT);
+    ALLOC(yg, double, NGROW * GT);
+    ALLOC(lg, double, NGROW * GT);
+    ALLOC(x, double, 4 * LT);
+    ALLOC(f, double, 4 * LT);
+    ALLOC(fbar, double, 4 * LT);
+    ALLOC(al, double, 3 * LT);
+    ALLOC(zb, double, NBROW * LT);
+    ALLOC(yb, double, NBROW * LT);
+    ALLOC(lb, double, NBROW * LT);
+    ALLOC(wbar, double, BT);
+    ALLOC(thbar, double, BT);
+    ALLOC(part_bus, double, (size_t)d.nblk_bus * NPART);
+    ALLOC(part_ubar, double, (size_t)d.nblk_ubar * NPART);
+    ALLOC(cnt, unsigned long long, 4);
+    ALLOC(st, DevStatus, 1);
+    int8_t *uinit = nullptr;
+    if (uc->u_init) {
+        uinit = dnew<int8_t>(ctx, GT, e);
+        if (e != cudaSuccess || up<int8_t>(ctx, uinit, uc->u_init, GT) != cudaSuccess)
+            return bail(fail(ctx, UCAC_ECUDA, "u_init upload"));
+    }
+    // status: beta = beta0, k = 1 (R21)
+    DevStatus st0{};
+    st0.beta = prm->beta0;
+    st0.outer_k = 1;
+    *ctx->st_host = st0;
+    if (cudaMemcpyAsync(d.st, ctx->st_host, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s) != cudaSuccess)
+        return bail(fail(ctx, UCAC_ECUDA, "status upload"));
+    if (gen_set_smem_attr(T) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "T=%d needs %zu B of shared memory", T, gen_smem_bytes(T)));
+    launch_init(d, uinit, ctx->s);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init kernel: %s", cudaGetErrorString(e)));
+    e = cudaStreamSynchronize(ctx->s);
+    if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init: %s", cudaGetErrorString(e)));
+    ucac_status gs = build_graphs(ctx);
+    if (gs != UCAC_OK) return bail(gs);
+    *out = ctx;
+    return UCAC_OK;
+#undef ALLOC
+#undef UPLOAD
+}
+
+// one inner iteration: [branch || gen] -> [bus || ubar] -> reduce
+static void enqueue_iteration(ucac_ctx *ctx) {
+    cudaEventRecord(ctx->ev_fork, ctx->s);
+    cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
+    launch_gen(ctx->d, ctx->s2);
+    launch_branch(ctx->d, ctx->s);
+    cudaEventRecord(ctx->ev_join, ctx->s2);
+    cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
+    cudaEventRecord(ctx->ev_fork, ctx->s);
+    cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
+    launch_ubar(ctx->d, ctx->s2);
+    launch_bus(ctx->d, ctx->s);
+    cudaEventRecord(ctx->ev_join, ctx->s2);
+    cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
+    launch_reduce(ctx->d, ctx->s);
+}
+
+static ucac_status build_graphs(ucac_ctx *ctx) {
+    for (int gi = 0; gi < 2; gi++) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < ctx->gunroll[gi]; k++) enqueue_iteration(ctx);
+        CK(cudaStreamEndCapture(ctx->s, &g));
+        cudaError_t e = cudaGraphInstantiate(&ctx->gexec[gi], g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+    }
+    return UCAC_OK;
+}
+
+static ucac_status set_control(ucac_ctx *ctx, int stop, double target) {
+    // write stop_on_primal, primal_target and clear done (three fields of the device status);
+    // nothing to do when the last call ran without stop_on_primal and this one does too
+    if (!stop && !ctx->ctl_dirty) return UCAC_OK;
+    ctx->ctl_dirty = stop != 0;
+    DevStatus *h = ctx->st_host;
+    h->stop_on_primal = stop;
+    h->primal_target = target;
+    h->done = 0;
+    DevStatus *dd = ctx->d.st;
+    CK(cudaMemcpyAsync(&dd->done, &h->done, sizeof(int), cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaMemcpyAsync(&dd->stop_on_primal, &h->stop_on_primal, sizeof(int), cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaMemcpyAsync(&dd->primal_target, &h->primal_target, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+    return UCAC_OK;
+}
+
+static ucac_status pull_status(ucac_ctx *ctx) {
+    CK(cudaMemcpyAsync(ctx->st_host, ctx->d.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_primal, double primal_target,
+                                    int32_t *n_done) {
+    if (!ctx) return UCAC_EINVAL;
+    if (n < 0) return fail(ctx, UCAC_EINVAL, "n < 0");
+    long long before = 0;
+    if (n_done) {
+        ucac_status s = pull_status(ctx);
+        if (s != UCAC_OK) return s;
+        before = ctx->st_host->inner_total;
+    }
+    ucac_status s = set_control(ctx, stop_on_primal > 0, primal_target);
+    if (s != UCAC_OK) return s;
+    int big = ctx->gunroll[1];
+    int nb = n / big, nr = n % big;
+    for (int k = 0; k < nb; k++) CK(cudaGraphLaunch(ctx->gexec[1], ctx->s));
+    for (int k = 0; k < nr; k++) CK(cudaGraphLaunch(ctx->gexec[0], ctx->s));
+    CK(cudaGetLastError());
+    if (n_done) {
+        s = pull_status(ctx);
+        if (s != UCAC_OK) return s;
+        *n_done = (int32_t)(ctx->st_host->inner_total - before);
+        if (ctx->st_host->err_kernel) return fail(ctx, UCAC_ENUMERIC, "non-finite iterate at iteration %d", ctx->st_host->err_iter);
+    }
+    return UCAC_OK;
+}
+
+static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce"};
+extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
+
+extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
+    if (!ctx || n < 0) return UCAC_EINVAL;
+    ucac_status s = set_control(ctx, 0, 0.0);
+    if (s != UCAC_OK) return s;
+    const size_t need = (size_t)n * NKERN * 2;
+    while (ctx->tev.size() < need) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        ctx->tev.push_back(ev);
+    }
+    for (int it = 0; it < n; it++) {
+        for (int k = 0; k < NKERN; k++) {
+            cudaEvent_t a = ctx->tev[((size_t)it * NKERN + k) * 2], b = ctx->tev[((size_t)it * NKERN + k) * 2 + 1];
+            CK(cudaEventRecord(a, ctx->s));
+            switch (k) {
+                case K_BRANCH: launch_branch(ctx->d, ctx->s); break;
+                case K_GEN: launch_gen(ctx->d, ctx->s); break;
+                case K_BUS: launch_bus(ctx->d, ctx->s); break;
+                case K_UBAR: launch_ubar(ctx->d, ctx->s); break;
+                default: launch_reduce(ctx->d, ctx->s); break;
+            }
+            CK(cudaEventRecord(b, ctx->s));
+        }
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->s));
+    for (int k = 0; k < NKERN; k++) {
+        double tot = 0.0;
+        for (int it = 0; it < n; it++) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ctx->tev[((size_t)it * NKERN + k) * 2], ctx->tev[((size_t)it * NKERN + k) * 2 + 1]));
+            tot += ms;
+        }
+        if (kernel_ms) kernel_ms[k] = tot;
+        if (launches) launches[k] = n;
+    }
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
+    if (!ctx || !r) return UCAC_EINVAL;
+    ucac_status s = pull_status(ctx);
+    if (s != UCAC_OK) return s;
+    const DevStatus *h = ctx->st_host;
+    r->primal_inf = h->primal_inf;
+    r->rz_inf = h->rz_inf;
+    r->rz_2 = h->rz_2;
+    r->z_inf = h->z_inf;
+    r->z_2 = h->z_2;
+    r->dual_inf = h->dual_inf;
+    r->objective = h->objective;
+    r->beta = h->beta;
+    r->inner_total = h->inner_total;
+    r->outer_total = h->outer_k - 1;
+    r->tron_iters = (int64_t)h->tron_iters;
+    r->tron_capped = (int64_t)h->tron_capped;
+    r->al_active = (int64_t)h->al_active;
+    r->al_capped = (int64_t)h->al_capped;
+    r->inner_since_outer = (int32_t)h->inner_since;
+    r->outer_k = (int32_t)h->outer_k;
+    r->err_kernel = h->err_kernel;
+    r->err_iter = h->err_iter;
+    if (h->err_kernel) return fail(ctx, UCAC_ENUMERIC, "non-finite iterate at iteration %d", h->err_iter);
+    return UCAC_OK;
+}
+
+template <class Tp>
+static cudaError_t down(ucac_ctx *ctx, Tp *dst, const Tp *src, size_t n) {
+    return cudaMemcpyAsync(dst, src, n * sizeof(Tp), cudaMemcpyDeviceToHost, ctx->s);
+}
+
+// [K][n] device SoA <-> [n][K] canonical host
+static ucac_status soa_to_aos(ucac_ctx *ctx, double *host, const double *dev, size_t n, int K) {
+    std::vector<double> tmp(n * K);
+    CK(down(ctx, tmp.data(), dev, n * K));
+    CK(cudaStreamSynchronize(ctx->s));
+    for (size_t i = 0; i < n; i++)
+        for (int k = 0; k < K; k++) host[i * K + k] = tmp[(size_t)k * n + i];
+    return UCAC_OK;
+}
+static ucac_status aos_to_soa(ucac_ctx *ctx, double *dev, const double *host, size_t n, int K) {
+    std::vector<double> tmp(n * K);
+    for (size_t i = 0; i < n; i++)
+        for (int k = 0; k < K; k++) tmp[(size_t)k * n + i] = host[i * K + k];
+    CK(up(ctx, dev, tmp.data(), n * K));
+    CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st) {
+    if (!ctx || !st) return UCAC_EINVAL;
+    launch_apply_outer(ctx->d, ctx->s);
+    CK(cudaGetLastError());
+    const Dev &d = ctx->d;
+    const size_t GT = (size_t)ctx->G * ctx->T, LT = (size_t)ctx->L * ctx->T, BT = (size_t)ctx->B * ctx->T;
+    CK(down(ctx, st->u, d.u, GT));
+    CK(down(ctx, st->p, d.p, GT));
+    CK(down(ctx, st->q, d.q, GT));
+    CK(down(ctx, st->ph, d.ph, GT));
+    CK(down(ctx, st->ub_on, d.ub_on, GT));
+    CK(down(ctx, st->ub_su, d.ub_su, GT));
+    CK(down(ctx, st->ub_sd, d.ub_sd, GT));
+    CK(down(ctx, st->pbar, d.pbar, GT));
+    CK(down(ctx, st->qbar, d.qbar, GT));
+    CK(down(ctx, st->zg, d.zg, NGROW * GT));
+    CK(down(ctx, st->yg, d.yg, NGROW * GT));
+    CK(down(ctx, st->lg, d.lg, NGROW * GT));
+    CK(down(ctx, st->zb, d.zb, NBROW * LT));
+    CK(down(ctx, st->yb, d.yb, NBROW * LT));
+    CK(down(ctx, st->lb, d.lb, NBROW * LT));
+    CK(down(ctx, st->wbar, d.wbar, BT));
+    CK(down(ctx, st->thbar, d.thbar, BT));
+    ucac_status s;
+    if ((s = soa_to_aos(ctx, st->x, d.x, LT, 4)) != UCAC_OK) return s;
+    if ((s = soa_to_aos(ctx, st->f, d.f, LT, 4)) != UCAC_OK) return s;
+    if ((s = soa_to_aos(ctx, st->fbar, d.fbar, LT, 4)) != UCAC_OK) return s;
+    if ((s = soa_to_aos(ctx, st->al, d.al, LT, 3)) != UCAC_OK) return s;
+    if ((s = pull_status(ctx)) != UCAC_OK) return s;
+    const DevStatus *h = ctx->st_host;
+    st->scal[0] = h->beta;
+    st->scal[1] = h->znorm_prev;
+    st->scal[2] = (double)h->outer_k;
+    st->scal[3] = (double)h->inner_total;
+    st->scal[4] = (double)h->inner_since;
+    st->scal[5] = st->scal[6] = st->scal[7] = 0.0;
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
+    if (!ctx || !st) return UCAC_EINVAL;
+    const Dev &d = ctx->d;
+    const size_t GT = (size_t)ctx->G * ctx->T, LT = (size_t)ctx->L * ctx->T, BT = (size_t)ctx->B * ctx->T;
+    CK(cudaStreamSynchronize(ctx->s));
+    CK(up(ctx, d.u, (const int8_t *)st->u, GT));
+    CK(up(ctx, d.p, (const double *)st->p, GT));
+    CK(up(ctx, d.q, (const double *)st->q, GT));
+    CK(up(ctx, d.ph, (const double *)st->ph, GT));
+    CK(up(ctx, d.ub_on, (const double *)st->ub_on, GT));
+    CK(up(ctx, d.ub_su, (const double *)st->ub_su, GT));
+    CK(up(ctx, d.ub_sd, (const double *)st->ub_sd, GT));
+    CK(up(ctx, d.pbar, (const double *)st->pbar, GT));
+    CK(up(ctx, d.qbar, (const double *)st->qbar, GT));
+    CK(up(ctx, d.zg, (const double *)st->zg, NGROW * GT));
+    CK(up(ctx, d.yg, (const double *)st->yg, NGROW * GT));
+    CK(up(ctx, d.lg, (const double *)st->lg, NGROW * GT));
+    CK(up(ctx, d.zb, (const double *)st->zb, NBROW * LT));
+    CK(up(ctx, d.yb, (const double *)st->yb, NBROW * LT));
+    CK(up(ctx, d.lb, (const double *)st->lb, NBROW * LT));
+    CK(up(ctx, d.wbar, (const double *)st->wbar, BT));
+    CK(up(ctx, d.thbar, (const double *)st->thbar, BT));
+    ucac_status s;
+    if ((s = aos_to_soa(ctx, d.x, st->x, LT, 4)) != UCAC_OK) return s;
+    if ((s = aos_to_soa(ctx, d.f, st->f, LT, 4)) != UCAC_OK) return s;
+    if ((s = aos_to_soa(ctx, d.fbar, st->fbar, LT, 4)) != UCAC_OK) return s;
+    if ((s = aos_to_soa(ctx, d.al, st->al, LT, 3)) != UCAC_OK) return s;
+    if ((s = pull_status(ctx)) != UCAC_OK) return s;
+    DevStatus *h = ctx->st_host;
+    h->beta = st->scal[0];
+    h->beta_lam = 0.0;
+    h->znorm_prev = st->scal[1];
+    h->outer_k = (long long)st->scal[2];
+    h->inner_total = (long long)st->scal[3];
+    h->inner_since = (long long)st->scal[4];
+    h->pending_outer = 0;
+    h->done = 0;
+    h->err_kernel = 0;
+    CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaMemsetAsync(d.cnt, 0, 4 * sizeof(unsigned long long), ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_get_solution(ucac_ctx *ctx, ucac_solution *sol) {
+    if (!ctx || !sol) return UCAC_EINVAL;
+    const Dev &d = ctx->d;
+    const size_t GT = (size_t)ctx->G * ctx->T, LT = (size_t)ctx->L * ctx->T, BT = (size_t)ctx->B * ctx->T;
+    if (sol->u_on) CK(down(ctx, sol->u_on, d.u, GT));
+    if (sol->p) CK(down(ctx, sol->p, d.p, GT));
+    if (sol->q) CK(down(ctx, sol->q, d.q, GT));
+    if (sol->wbar) CK(down(ctx, sol->wbar, d.wbar, BT));
+    if (sol->thetabar) CK(down(ctx, sol->thetabar, d.thbar, BT));
+    if (sol->flows) {
+        ucac_status s = soa_to_aos(ctx, sol->flows, d.f, LT, 4);
+        if (s != UCAC_OK) return s;
+    }
+    CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_dp_batch(int32_t ngen, int32_t T, const double *L, const int32_t *min_up,
+                                     const int32_t *min_dn, const int32_t *u0, const int32_t *hold, int8_t *sched,
+                                     double *cost, int32_t on_device, void *cuda_stream) {
+    if (ngen <= 0 || T <= 0 || !L || !min_up || !min_dn || !u0 || !hold || !sched || !cost) {
+        g_create_err = "ucac_dp_batch: bad arguments";
+        return UCAC_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (gen_set_smem_attr(T) != cudaSuccess) {
+        g_create_err = "ucac_dp_batch: shared memory";
+        return UCAC_ECUDA;
+    }
+    if (on_device) {
+        launch_dp_batch(ngen, T, L, min_up, min_dn, u0, hold, sched, cost, s);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            g_create_err = cudaGetErrorString(e);
+            return UCAC_ECUDA;
+        }
+        return UCAC_OK;
+    }
+    for (int g = 0; g < ngen; g++)
+        if (min_up[g] < 1 || min_up[g] > T || min_dn[g] < 1 || min_dn[g] > T || hold[g] < 0 || hold[g] > T ||
+            (u0[g] != 0 && u0[g] != 1)) {
+            g_create_err = "ucac_dp_batch: min_up/min_dn in [1,T], hold in [0,T], u0 in {0,1}";
+            return UCAC_EINVAL;
+        }
+    double *dL = nullptr, *dc = nullptr;
+    int *dtu = nullptr, *dtd = nullptr, *du0 = nullptr, *dh = nullptr;
+    int8_t *ds = nullptr;
+    const size_t GT = (size_t)ngen * T;
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc(&dL, GT * 4 * 8)) != cudaSuccess || (e = cudaMalloc(&dc, ngen * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&dtu, ngen * 4)) != cudaSuccess || (e = cudaMalloc(&dtd, ngen * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&du0, ngen * 4)) != cudaSuccess || (e = cudaMalloc(&dh, ngen * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&ds, GT)) != cudaSuccess) {
+    } else {
+        cudaMemcpyAsync(dL, L, GT * 4 * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dtu, min_up, ngen * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dtd, min_dn, ngen * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(du0, u0, ngen * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dh, hold, ngen * 4, cudaMemcpyHostToDevice, s);
+        launch_dp_batch(ngen, T, dL, dtu, dtd, du0, dh, ds, dc, s);
+        cudaMemcpyAsync(sched, ds, GT, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(cost, dc, ngen * 8, cudaMemcpyDeviceToHost, s);
+        e = cudaStreamSynchronize(s);
+    }
+    cudaFree(dL); cudaFree(dc); cudaFree(dtu); cudaFree(dtd); cudaFree(du0); cudaFree(dh); cudaFree(ds);
+    if (e != cudaSuccess) {
+        g_create_err = cudaGetErrorString(e);
+        return UCAC_ECUDA;
+    }
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz) {
+    if (!ctx || !sz) return UCAC_EINVAL;
+    const int64_t G = ctx->G, L = ctx->L, B = ctx->B, T = ctx->T;
+    const int64_t GT = G * T, LT = L * T, BT = B * T;
+    sz->nrows = G * (12 * T - 1) + 8 * LT;
+    sz->gen_periods = GT;
+    sz->branch_periods = LT;
+    sz->bus_periods = BT;
+    // Algorithmic bytes: every array element a kernel must read or write once.
+    // k_branch: read fbar(4) z(8) y(8) x(4) al(3) + wbar/thbar of both ends (4); write x(4) f(4) al(3)
+    //           -> 38 doubles per (l,t); static y(8) rate from/to per branch.
+    sz->alg_bytes[K_BRANCH] = LT * 38 * 8 + L * (9 * 8 + 2 * 4);
+    // k_gen: read ubar(3) pbar qbar z,y of 12 rows (24) ; write p q ph (3) + u (1 B)
+    sz->alg_bytes[K_GEN] = GT * (29 * 8 + 1) + G * 24 * 8;
+    // k_bus: per gen-period: read p q ph z,y,lambda of GP GQ RC (9) pbar qbar (2), write pbar qbar z y (8)
+    //        per branch end-period: read f(2) x(2) z,y,lambda(12) fbar(2), write fbar(2) z,y(8)
+    //        per bus-period: read pd qd wbar thbar, write wbar thbar
+    sz->alg_bytes[K_BUS] = GT * 19 * 8 + 2 * LT * 28 * 8 + BT * 6 * 8;
+    // k_ubar: per gen-period: read u p q ph ubar(3) z,y,lambda of 9 rows (27); write ubar(3) z,y (18)
+    sz->alg_bytes[K_UBAR] = GT * (51 * 8 + 1);
+    sz->alg_bytes[K_REDUCE] = (int64_t)(ctx->d.nblk_bus + ctx->d.nblk_ubar) * NPART * 8;
+    int64_t tot = 0;
+    for (int k = 0; k < NKERN; k++) tot += sz->alg_bytes[k];
+    sz->alg_bytes_per_iter = tot;
+    return UCAC_OK;
+}
+
+extern "C" void *ucac_stream(ucac_ctx *ctx) { return ctx ? (void *)ctx->s : nullptr; }
+
+extern "C" const char *ucac_last_error(const ucac_ctx *ctx) {
+    if (!ctx) return g_create_err.c_str();
+    return ctx->err.c_str();
+}
+
+extern "C" void ucac_destroy(ucac_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->s) cudaStreamSynchronize(ctx->s);
+    for (auto &g : ctx->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto ev : ctx->tev) cudaEventDestroy(ev);
+    for (void *p : ctx->dalloc) cudaFree(p);
+    if (ctx->st_host) cudaFreeHost(ctx->st_host);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->s2) cudaStreamDestroy(ctx->s2);
+    if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);
+    delete ctx;
+}

@@ -1,0 +1,104 @@
+// ucac_dev.cuh -- device-side layout of the UC-ACOPF ADMM hot path (B200, sm_100a, fp64).
+//
+// Everything the kernels touch lives in one POD `Dev` passed by value to every kernel.
+// Layout: component-major, period-minor SoA; row state is [kind][comp*T + t]
+// so that a warp whose lanes are consecutive periods of one component (or consecutive
+// (component, period) pairs) reads each row kind as one coalesced 256-B segment.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ucac {
+
+// coupling-row kinds (Eq. 5; R3 ramp-down in the Eq. 4d form, R6 ramp copy,
+// R7 angle consensus)
+enum GenRow { G_DON = 0, G_DSU, G_DSD, G_PL, G_PU, G_QL, G_QU, G_RD, G_RU, G_GP, G_GQ, G_RC, NGROW };
+enum BrRow { B_FPIJ = 0, B_FQIJ, B_FPJI, B_FQJI, B_WI, B_WJ, B_AI, B_AJ, NBROW };
+
+// kernel ids (ucac_kernel_name)
+enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, NKERN = 5 };
+
+// per-block reduction record (S8): max |r|, max |r+z|, sum (r+z)^2, max |z|, sum z^2,
+// max rho |dxbar|, objective, non-finite flag
+enum Part { P_PINF = 0, P_RZINF, P_RZ2, P_ZINF, P_Z2, P_DINF, P_OBJ, P_BAD, NPART };
+
+struct DevStatus {
+    double beta;          // current beta^k
+    double beta_lam;      // beta used by the pending lambda update
+    double znorm_prev;    // ||z||_2 at the previous outer update
+    long long outer_k;    // k (starts at 1)
+    long long inner_total;
+    long long inner_since;
+    int pending_outer;    // lambda <- clip(lambda + beta_lam z) to apply at the next sweep
+    int done;             // stop_on_primal reached: kernels return immediately
+    int stop_on_primal;
+    int err_kernel, err_iter;
+    int pad_;
+    double primal_target;
+    double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective;
+    unsigned long long tron_iters, tron_capped, al_active, al_capped;
+};
+
+struct Dev {
+    int G, L, B, T;
+    int ref_bus;
+    int nblk_bus, nblk_ubar;
+    double S;                         // base MVA
+    double rpq, rva, ruc;             // rho classes
+    double tau, theta, lambda_max, beta_max, eps_inner_abs;
+    int inner_min, inner_cap, outer_enabled;
+    double tron_gtol;                 // absolute: tron_gtol_rel * max(rho_pq, rho_va)
+    int tron_maxit, al_maxit;
+    double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
+
+    // ---- static generator data [G]
+    const int *gbus, *tu, *td, *u0, *hold;
+    const double *pmin, *pmax, *qmin, *qmax, *c2, *c1, *c0, *csu, *csd;
+    const double *rup, *rdn, *sup, *sdn, *p0;
+    // ---- static branch data
+    const double *y;                  // [8][L] SoA: Gii Gij Gji Gjj Bii Bij Bji Bjj
+    const double *rate;               // [L]
+    const int *bfrom, *bto;           // [L]
+    // ---- static bus data
+    const double *gs, *bs, *vmin, *vmax;  // [B]
+    const double *pd, *qd;            // [B][T]
+    const int *bg_ptr, *bg_idx;       // CSR bus -> generators (index order)
+    const int *be_ptr, *be_idx;       // CSR bus -> branch ends (2*l + side), (l, side) order
+
+    // ---- iterate
+    int8_t *u;                        // [G*T]
+    double *p, *q, *ph;               // [G*T]
+    double *ub_on, *ub_su, *ub_sd;    // [G*T]
+    double *pbar, *qbar;              // [G*T]
+    double *zg, *yg, *lg;             // [12][G*T]
+    double *x;                        // [4][L*T]  w_i w_j th_i th_j
+    double *f;                        // [4][L*T]  p_ij q_ij p_ji q_ji
+    double *fbar;                     // [4][L*T]
+    double *al;                       // [3][L*T]  mu_ij mu_ji sigma
+    double *zb, *yb, *lb;             // [8][L*T]
+    double *wbar, *thbar;             // [B*T]
+
+    // ---- reduction scratch
+    double *part_bus;                 // [nblk_bus][NPART]
+    double *part_ubar;                // [nblk_ubar][NPART]
+    unsigned long long *cnt;          // [4] per-iteration TRON counters (zeroed by reduce)
+    DevStatus *st;
+};
+
+__host__ __device__ inline size_t gi(const Dev &d, int g, int t) { return (size_t)g * d.T + t; }
+
+}  // namespace ucac
+
+// launch wrappers (one per translation unit)
+namespace ucac {
+void launch_branch(const Dev &d, cudaStream_t s);
+void launch_gen(const Dev &d, cudaStream_t s);
+void launch_bus(const Dev &d, cudaStream_t s);
+void launch_ubar(const Dev &d, cudaStream_t s);
+void launch_reduce(const Dev &d, cudaStream_t s);
+void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s);
+void launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
+                     const int *hold, int8_t *sched, double *cost, cudaStream_t s);
+int nblk_bus(int B, int T);
+int nblk_ubar(int G, int T);
+}  // namespace ucac

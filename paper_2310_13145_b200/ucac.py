@@ -1,0 +1,285 @@
+"""Thin ctypes binding of libucac.so (include/ucac.h).  Argument marshalling only: every
+step of the ADMM hot path runs in the CUDA kernels behind the C ABI.  There is no CPU
+fallback: if the library or a B200 is missing, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import build as _build
+
+_lock = threading.Lock()
+_lib = None
+
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int32)
+i8p = C.POINTER(C.c_int8)
+i64p = C.POINTER(C.c_int64)
+
+NKERNELS = 5
+KERNELS = ["k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce"]
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ENUMERIC", 6: "ESTATE", 7: "EUNSUPPORTED"}
+
+
+class UcacError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"ucac {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Network(C.Structure):
+    _fields_ = [("nbus", C.c_int32), ("ngen", C.c_int32), ("nbranch", C.c_int32), ("ref_bus", C.c_int32),
+                ("base_mva", C.c_double), ("bus_gs", dp), ("bus_bs", dp), ("bus_vmin", dp), ("bus_vmax", dp),
+                ("br_from", ip), ("br_to", ip), ("br_y", dp), ("br_rate", dp), ("gen_bus", ip),
+                ("gen_pmin", dp), ("gen_pmax", dp), ("gen_qmin", dp), ("gen_qmax", dp)]
+
+
+class Horizon(C.Structure):
+    _fields_ = [("T", C.c_int32), ("pd", dp), ("qd", dp)]
+
+
+class Costs(C.Structure):
+    _fields_ = [("c2", dp), ("c1", dp), ("c0", dp), ("startup", dp), ("shutdown", dp)]
+
+
+class Uc(C.Structure):
+    _fields_ = [("ramp_up", dp), ("ramp_dn", dp), ("su_ramp", dp), ("sd_ramp", dp), ("min_up", ip),
+                ("min_dn", ip), ("u0", ip), ("hold", ip), ("p0", dp), ("u_init", i8p)]
+
+
+class Params(C.Structure):
+    _fields_ = [("rho_pq", C.c_double), ("rho_va", C.c_double), ("rho_uc", C.c_double),
+                ("beta0", C.c_double), ("tau", C.c_double), ("theta", C.c_double),
+                ("lambda_max", C.c_double), ("beta_max", C.c_double), ("eps_inner_abs", C.c_double),
+                ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
+                ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
+                ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
+                ("al_sigma_decay", C.c_double)]
+
+
+class Report(C.Structure):
+    _fields_ = [("primal_inf", C.c_double), ("rz_inf", C.c_double), ("rz_2", C.c_double),
+                ("z_inf", C.c_double), ("z_2", C.c_double), ("dual_inf", C.c_double),
+                ("objective", C.c_double), ("beta", C.c_double),
+                ("inner_total", C.c_int64), ("outer_total", C.c_int64), ("tron_iters", C.c_int64),
+                ("tron_capped", C.c_int64), ("al_active", C.c_int64), ("al_capped", C.c_int64),
+                ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32),
+                ("err_kernel", C.c_int32), ("err_iter", C.c_int32)]
+
+
+class Solution(C.Structure):
+    _fields_ = [("u_on", i8p), ("p", dp), ("q", dp), ("wbar", dp), ("thetabar", dp), ("flows", dp)]
+
+
+STATE_FIELDS = [("u", np.int8, "GT"), ("p", np.float64, "GT"), ("q", np.float64, "GT"),
+                ("ph", np.float64, "GT"), ("ub_on", np.float64, "GT"), ("ub_su", np.float64, "GT"),
+                ("ub_sd", np.float64, "GT"), ("pbar", np.float64, "GT"), ("qbar", np.float64, "GT"),
+                ("zg", np.float64, "12GT"), ("yg", np.float64, "12GT"), ("lg", np.float64, "12GT"),
+                ("x", np.float64, "4LT"), ("f", np.float64, "4LT"), ("fbar", np.float64, "4LT"),
+                ("al", np.float64, "3LT"), ("zb", np.float64, "8LT"), ("yb", np.float64, "8LT"),
+                ("lb", np.float64, "8LT"), ("wbar", np.float64, "BT"), ("thbar", np.float64, "BT"),
+                ("scal", np.float64, "8")]
+
+
+class State(C.Structure):
+    _fields_ = [(n, i8p if t == np.int8 else dp) for n, t, _ in STATE_FIELDS]
+
+
+class Sizes(C.Structure):
+    _fields_ = [("nrows", C.c_int64), ("gen_periods", C.c_int64), ("branch_periods", C.c_int64),
+                ("bus_periods", C.c_int64), ("alg_bytes_per_iter", C.c_int64),
+                ("alg_bytes", C.c_int64 * NKERNELS)]
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def lib(build_if_missing: bool = True):
+    """Load libucac.so (building it in-tree with nvcc if missing)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build.LIB
+            if not os.path.exists(path):
+                if not build_if_missing:
+                    raise UcacError(3, f"{path} missing; run __graft_entry__.build()")
+                _build.build()
+            L = C.CDLL(path)
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def _declare(L):
+    L.ucac_create.argtypes = [C.POINTER(Network), C.POINTER(Horizon), C.POINTER(Costs), C.POINTER(Uc),
+                              C.POINTER(Params), C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.ucac_create.restype = C.c_int
+    L.ucac_iterate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_int32)]
+    L.ucac_iterate.restype = C.c_int
+    L.ucac_iterate_timed.argtypes = [C.c_void_p, C.c_int32, dp, i64p]
+    L.ucac_iterate_timed.restype = C.c_int
+    L.ucac_kernel_name.argtypes = [C.c_int32]
+    L.ucac_kernel_name.restype = C.c_char_p
+    L.ucac_residuals.argtypes = [C.c_void_p, C.POINTER(Report)]
+    L.ucac_residuals.restype = C.c_int
+    L.ucac_get_solution.argtypes = [C.c_void_p, C.POINTER(Solution)]
+    L.ucac_get_solution.restype = C.c_int
+    L.ucac_get_state.argtypes = [C.c_void_p, C.POINTER(State)]
+    L.ucac_get_state.restype = C.c_int
+    L.ucac_set_state.argtypes = [C.c_void_p, C.POINTER(State)]
+    L.ucac_set_state.restype = C.c_int
+    L.ucac_dp_batch.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    L.ucac_dp_batch.restype = C.c_int
+    L.ucac_get_sizes.argtypes = [C.c_void_p, C.POINTER(Sizes)]
+    L.ucac_get_sizes.restype = C.c_int
+    L.ucac_stream.argtypes = [C.c_void_p]
+    L.ucac_stream.restype = C.c_void_p
+    L.ucac_last_error.argtypes = [C.c_void_p]
+    L.ucac_last_error.restype = C.c_char_p
+    L.ucac_destroy.argtypes = [C.c_void_p]
+    L.ucac_destroy.restype = None
+
+
+EXPORTED = ["ucac_create", "ucac_iterate", "ucac_iterate_timed", "ucac_kernel_name", "ucac_residuals",
+            "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
+            "ucac_stream", "ucac_last_error", "ucac_destroy"]
+
+
+def _check(rc, h=None):
+    if rc != 0:
+        msg = lib().ucac_last_error(h)
+        raise UcacError(rc, msg.decode() if msg else "")
+
+
+def params_struct(pr) -> Params:
+    return Params(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max, pr.beta_max,
+                  pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled, pr.tron_gtol_rel,
+                  pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel, pr.al_sigma_max_rel,
+                  pr.al_sigma_decay)
+
+
+class Context:
+    """One ADMM context on the current CUDA device (ucac_create .. ucac_destroy)."""
+
+    def __init__(self, pb, pr, stream: int = 0):
+        self.L = lib()
+        pb = pb.normalized()
+        self.pb, self.pr = pb, pr
+        keep = []
+
+        def a(x, t=dp):
+            x = np.ascontiguousarray(x)
+            keep.append(x)
+            return x.ctypes.data_as(t)
+        net = Network(pb.nbus, pb.ngen, pb.nbranch, pb.ref_bus, pb.base_mva, a(pb.bus_gs), a(pb.bus_bs),
+                      a(pb.bus_vmin), a(pb.bus_vmax), a(pb.br_from, ip), a(pb.br_to, ip), a(pb.br_y.reshape(-1)),
+                      a(pb.br_rate), a(pb.gen_bus, ip), a(pb.pmin), a(pb.pmax), a(pb.qmin), a(pb.qmax))
+        hz = Horizon(pb.T, a(pb.pd.reshape(-1)), a(pb.qd.reshape(-1)))
+        co = Costs(a(pb.c2), a(pb.c1), a(pb.c0), a(pb.csu), a(pb.csd))
+        ui = a(np.ascontiguousarray(pb.u_init, dtype=np.int8).reshape(-1), i8p) if pb.u_init is not None else None
+        uc = Uc(a(pb.ramp_up), a(pb.ramp_dn), a(pb.su_ramp), a(pb.sd_ramp), a(pb.min_up, ip), a(pb.min_dn, ip),
+                a(pb.u0, ip), a(pb.hold, ip), a(pb.p0), ui)
+        prm = params_struct(pr)
+        h = C.c_void_p()
+        rc = self.L.ucac_create(C.byref(net), C.byref(hz), C.byref(co), C.byref(uc), C.byref(prm), None,
+                                C.c_void_p(stream) if stream else None, C.byref(h))
+        _check(rc, None)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.ucac_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self.L.ucac_stream(self.h) or 0)
+
+    def iterate(self, n: int = 1, stop_on_primal: float | None = None) -> int | None:
+        done = C.c_int32(0)
+        if stop_on_primal is None:
+            _check(self.L.ucac_iterate(self.h, n, 0, 0.0, None), self.h)
+            return None
+        _check(self.L.ucac_iterate(self.h, n, 1, float(stop_on_primal), C.byref(done)), self.h)
+        return done.value
+
+    def iterate_timed(self, n: int):
+        ms = np.zeros(NKERNELS)
+        cnt = np.zeros(NKERNELS, dtype=np.int64)
+        _check(self.L.ucac_iterate_timed(self.h, n, ms.ctypes.data_as(dp), cnt.ctypes.data_as(i64p)), self.h)
+        return dict(zip(KERNELS, ms)), dict(zip(KERNELS, cnt))
+
+    def report(self) -> dict:
+        r = Report()
+        _check(self.L.ucac_residuals(self.h, C.byref(r)), self.h)
+        return {n: getattr(r, n) for n, _ in Report._fields_}
+
+    def solution(self) -> dict:
+        pb = self.pb
+        GT, LT, BT = pb.ngen * pb.T, pb.nbranch * pb.T, pb.nbus * pb.T
+        out = {"u_on": np.zeros(GT, np.int8), "p": np.zeros(GT), "q": np.zeros(GT), "wbar": np.zeros(BT),
+               "thetabar": np.zeros(BT), "flows": np.zeros(4 * LT)}
+        s = Solution(out["u_on"].ctypes.data_as(i8p), *[out[k].ctypes.data_as(dp) for k in
+                                                         ("p", "q", "wbar", "thetabar", "flows")])
+        _check(self.L.ucac_get_solution(self.h, C.byref(s)), self.h)
+        return out
+
+    def _sizes(self):
+        pb = self.pb
+        GT, LT, BT = pb.ngen * pb.T, pb.nbranch * pb.T, pb.nbus * pb.T
+        return {"GT": GT, "12GT": 12 * GT, "4LT": 4 * LT, "3LT": 3 * LT, "8LT": 8 * LT, "BT": BT, "8": 8}
+
+    def get_state(self) -> dict:
+        sz = self._sizes()
+        st = {n: np.zeros(sz[s], dtype=t) for n, t, s in STATE_FIELDS}
+        sc = State(*[st[n].ctypes.data_as(i8p if t == np.int8 else dp) for n, t, _ in STATE_FIELDS])
+        _check(self.L.ucac_get_state(self.h, C.byref(sc)), self.h)
+        return st
+
+    def set_state(self, st: dict):
+        sz = self._sizes()
+        arr = {n: np.ascontiguousarray(st[n], dtype=t).reshape(-1) for n, t, _ in STATE_FIELDS}
+        for n, t, s in STATE_FIELDS:
+            if arr[n].size != sz[s]:
+                raise ValueError(f"state field {n}: {arr[n].size} != {sz[s]}")
+        sc = State(*[arr[n].ctypes.data_as(i8p if t == np.int8 else dp) for n, t, _ in STATE_FIELDS])
+        _check(self.L.ucac_set_state(self.h, C.byref(sc)), self.h)
+
+    def sizes(self) -> dict:
+        s = Sizes()
+        _check(self.L.ucac_get_sizes(self.h, C.byref(s)), self.h)
+        d = {n: getattr(s, n) for n, _ in Sizes._fields_ if n != "alg_bytes"}
+        d["alg_bytes"] = dict(zip(KERNELS, list(s.alg_bytes)))
+        return d
+
+
+def dp_batch(L, min_up, min_dn, u0, hold):
+    """Batched DP (Alg. 2) on host arrays; L [ngen, T, 2, 2]."""
+    Lh = np.ascontiguousarray(L, dtype=np.float64)
+    G, T = Lh.shape[0], Lh.shape[1]
+    sched = np.zeros((G, T), dtype=np.int8)
+    cost = np.zeros(G)
+    arrs = [np.ascontiguousarray(v, dtype=np.int32) for v in (min_up, min_dn, u0, hold)]
+    rc = lib().ucac_dp_batch(G, T, Lh.ctypes.data, *[x.ctypes.data for x in arrs], sched.ctypes.data,
+                             cost.ctypes.data, 0, None)
+    _check(rc, None)
+    return sched, cost
+
+
+def dp_batch_device(G, T, L_ptr, tu_ptr, td_ptr, u0_ptr, hold_ptr, sched_ptr, cost_ptr, stream=0):
+    """Batched DP on device pointers (asynchronous on `stream`)."""
+    rc = lib().ucac_dp_batch(G, T, L_ptr, tu_ptr, td_ptr, u0_ptr, hold_ptr, sched_ptr, cost_ptr, 1,
+                             C.c_void_p(stream) if stream else None)
+    _check(rc, None)
