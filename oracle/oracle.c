@@ -464,7 +464,7 @@ static double qmodel(int n, const double *g, const double *H, const double *s) {
  * specified in DESIGN.md 5.3 (constants R10).  Returns 1 if ||P(x-g)-x||_inf <= gtol. */
 static const double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
 static const double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-12;
-static const double TR_EPSF = 1e-10;
+static const double TR_EPSF = 1e-10, TR_STALL = 1e-14;
 
 static void pstep(int n, const double *x, const double *lo, const double *hi,
                   const double *d, double a, double *s) {
@@ -599,6 +599,12 @@ static int tron(int n, double *x, const double *lo, const double *hi, eval_fn ev
         for (int i = 0; i < n; i++) gq[i] = g[i] + Hs[i];
         steihaug(n, H, gq, fr, sc, delta, w);
         prsrch(n, x, lo, hi, g, H, sc, w, s);
+        /* stall: a step at the rounding level of x means the gradient floor is reached */
+        {
+            double xm = 0.0;
+            for (int i = 0; i < n; i++) xm = dmax(xm, fabs(x[i]));
+            if (nrm2(n, s) <= TR_STALL * (1.0 + xm)) { *iters = it; return 1; }
+        }
         double pred = -qmodel(n, g, H, s);
         for (int i = 0; i < n; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
         ev(ctx, xn, &fn, gn, Hn);

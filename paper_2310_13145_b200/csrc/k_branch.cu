@@ -24,7 +24,7 @@ namespace {
 
 constexpr double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
 constexpr double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-12;
-constexpr double TR_EPSF = 1e-10;
+constexpr double TR_EPSF = 1e-10, TR_STALL = 1e-14;
 constexpr double TWO_PI = 6.283185307179586;
 
 template <bool AL>
@@ -379,6 +379,16 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
             if (!found) {
 #pragma unroll
                 for (int i = 0; i < N; i++) s[i] = sc[i];
+            }
+        }
+        // --- stall: a step at the rounding level of x means the gradient floor is reached
+        {
+            double xm = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; i++) xm = fmax(xm, fabs(x[i]));
+            if (sqrt(dotn<N>(s, s)) <= TR_STALL * (1.0 + xm)) {
+                iters = it;
+                return true;
             }
         }
         // --- ratio test

@@ -178,12 +178,12 @@ class Params:
     inner_min: int = 5
     inner_cap: int = 1000
     outer_enabled: int = 1
-    tron_gtol_rel: float = 1e-9
+    tron_gtol_rel: float = 1e-11
     tron_maxit: int = 100
     al_maxit: int = 50
     al_eta_star: float = 1e-10
     al_sigma0_rel: float = 10.0
-    al_sigma_max_rel: float = 1e8
+    al_sigma_max_rel: float = 1e3
     al_sigma_decay: float = 0.1
 
 
