@@ -55,7 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(OUT, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers + [os.path.abspath(__file__)]):
-            cmd = [nvcc(), *ARCH, *COMMON, *flags, "-Xptxas", "-v", "-c", s, "-o", o]
+            extra = os.environ.get("UCAC_EXTRA_NVCC", "").split()   # tuning sweeps only
+            cmd = [nvcc(), *ARCH, *COMMON, *flags, *extra, "-Xptxas", "-v", "-c", s, "-o", o]
             jobs.append(cmd)
 
     def run(cmd):

@@ -422,88 +422,160 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long *dst, unsigned l
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
-__global__ void __launch_bounds__(128) k_branch(Dev d) {
+// load the data of solve k = l*T + t: admittances, targets tau = xbar - z - y/rho (5.1), w bounds
+__device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F, double *wlo, double *whi) {
+    const size_t LTs = (size_t)d.L * d.T;
+    const int l = k / d.T, t = k - l * d.T;
+    const int bi = d.bfrom[l], bj = d.bto[l];
+    F.Gii = d.y[0 * d.L + l]; F.Gij = d.y[1 * d.L + l]; F.Gji = d.y[2 * d.L + l]; F.Gjj = d.y[3 * d.L + l];
+    F.Bii = d.y[4 * d.L + l]; F.Bij = d.y[5 * d.L + l]; F.Bji = d.y[6 * d.L + l]; F.Bjj = d.y[7 * d.L + l];
+    F.rpq = d.rpq;
+    F.rva = d.rva;
+#pragma unroll
+    for (int r = 0; r < 4; r++) F.tau[r] = d.fbar[r * LTs + k] - d.zb[r * LTs + k] - d.yb[r * LTs + k] / d.rpq;
+    const size_t wi = (size_t)bi * d.T + t, wj = (size_t)bj * d.T + t;
+    F.tau[4] = d.wbar[wi] - d.zb[B_WI * LTs + k] - d.yb[B_WI * LTs + k] / d.rva;
+    F.tau[5] = d.wbar[wj] - d.zb[B_WJ * LTs + k] - d.yb[B_WJ * LTs + k] / d.rva;
+    F.tau[6] = d.thbar[wi] - d.zb[B_AI * LTs + k] - d.yb[B_AI * LTs + k] / d.rva;
+    F.tau[7] = d.thbar[wj] - d.zb[B_AJ * LTs + k] - d.yb[B_AJ * LTs + k] / d.rva;
+    F.setup();
+    wlo[0] = d.vmin[bi] * d.vmin[bi];
+    whi[0] = d.vmax[bi] * d.vmax[bi];
+    wlo[1] = d.vmin[bj] * d.vmin[bj];
+    whi[1] = d.vmax[bj] * d.vmax[bj];
+}
+
+// Phase 1: 4-variable fast path for every (l,t).  Solves whose result violates Eq. 2c-2d are
+// appended to the AL queue and finished by k_branch_al (R9); the rest are final here.
+// Bus-side targets of the 8 rows of solve k for step (7d): tauhat = x-part + z + y/rho
+// (DESIGN.md 5.5), written right after the solve so the bus kernel reads 4 values per incident
+// end instead of the row state.  (x + z) + y/rho has no multiply-add to contract, so this is
+// the same value the oracle forms.
+__device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x, double f0, double f1,
+                                            double f2, double f3) {
+    const size_t LTs = (size_t)d.L * d.T;
+    const double xs[8] = {f0, f1, f2, f3, x[0], x[1], x[2], x[3]};
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const double rho = r < 4 ? d.rpq : d.rva;
+        d.tauh[r * LTs + k] = xs[r] + d.zb[r * LTs + k] + d.yb[r * LTs + k] / rho;
+    }
+}
+
+#ifndef UCAC_BRANCH_TPB
+#define UCAC_BRANCH_TPB 128
+#endif
+#ifndef UCAC_BRANCH_MINB
+#define UCAC_BRANCH_MINB 3
+#endif
+#ifndef UCAC_AL_BLOCKS_PER_SM
+#define UCAC_AL_BLOCKS_PER_SM 4
+#endif
+__global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(Dev d) {
     if (d.st->done) return;
     const int LT = d.L * d.T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0;
+    unsigned long long c_it = 0, c_cap = 0;
     if (k < LT) {
-        const int l = k / d.T, t = k - l * d.T;
-        const int bi = d.bfrom[l], bj = d.bto[l];
-        BrFun<false> F4;
-        F4.Gii = d.y[0 * d.L + l]; F4.Gij = d.y[1 * d.L + l]; F4.Gji = d.y[2 * d.L + l]; F4.Gjj = d.y[3 * d.L + l];
-        F4.Bii = d.y[4 * d.L + l]; F4.Bij = d.y[5 * d.L + l]; F4.Bji = d.y[6 * d.L + l]; F4.Bjj = d.y[7 * d.L + l];
-        F4.rpq = d.rpq;
-        F4.rva = d.rva;
         const size_t LTs = (size_t)LT;
-        // x-step targets tau = xbar - z - y/rho
-#pragma unroll
-        for (int r = 0; r < 4; r++)
-            F4.tau[r] = d.fbar[r * LTs + k] - d.zb[r * LTs + k] - d.yb[r * LTs + k] / d.rpq;
-        const size_t wi = (size_t)bi * d.T + t, wj = (size_t)bj * d.T + t;
-        F4.tau[4] = d.wbar[wi] - d.zb[B_WI * LTs + k] - d.yb[B_WI * LTs + k] / d.rva;
-        F4.tau[5] = d.wbar[wj] - d.zb[B_WJ * LTs + k] - d.yb[B_WJ * LTs + k] / d.rva;
-        F4.tau[6] = d.thbar[wi] - d.zb[B_AI * LTs + k] - d.yb[B_AI * LTs + k] / d.rva;
-        F4.tau[7] = d.thbar[wj] - d.zb[B_AJ * LTs + k] - d.yb[B_AJ * LTs + k] / d.rva;
-        F4.setup();
-        double lo[6], hi[6];
-        lo[0] = d.vmin[bi] * d.vmin[bi]; hi[0] = d.vmax[bi] * d.vmax[bi];
-        lo[1] = d.vmin[bj] * d.vmin[bj]; hi[1] = d.vmax[bj] * d.vmax[bj];
+        BrFun<false> F4;
+        double lo[4], hi[4];
+        load_solve(d, k, F4, lo, hi);
         lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
-        lo[4] = 0.0; hi[4] = 1.0; lo[5] = 0.0; hi[5] = 1.0;
-        double x[6];
+        double x[4];
 #pragma unroll
         for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
         int it = 0;
         bool ok = tron<4>(F4, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
-        c_it += it;
-        c_cap += !ok;
-        const double rate = d.rate[l];
-        const double r2 = rate * rate;
-        const double sig0 = d.al_sigma0_rel * d.rpq * r2;
-        double mu0 = 0.0, mu1 = 0.0, sig = sig0;
+        c_it = it;
+        c_cap = !ok;
         double C, S, f0, f1, f2, f3;
         F4.flows(x, C, S, f0, f1, f2, f3);
-        if (rate > 0.0) {
-            double s1 = f0 * f0 + f1 * f1, s2 = f2 * f2 + f3 * f3;
-            if (s1 > r2 || s2 > r2) {
-                // 6-variable slack form, method of multipliers (R9)
-                BrFun<true> F6;
-                F6.Gii = F4.Gii; F6.Gij = F4.Gij; F6.Gji = F4.Gji; F6.Gjj = F4.Gjj;
-                F6.Bii = F4.Bii; F6.Bij = F4.Bij; F6.Bji = F4.Bji; F6.Bjj = F4.Bjj;
+        const double rate = d.rate[k / d.T];
+        const double r2 = rate * rate;
 #pragma unroll
-                for (int r = 0; r < 8; r++) F6.tau[r] = F4.tau[r];
-                F6.rpq = F4.rpq; F6.rva = F4.rva;
-                F6.K00 = F4.K00; F6.K02 = F4.K02; F6.K03 = F4.K03; F6.K11 = F4.K11;
-                F6.K12 = F4.K12; F6.K13 = F4.K13; F6.K22 = F4.K22;
-                F6.r2inv = 1.0 / r2;
-                x[4] = clampd(1.0 - s1 / r2, 0.0, 1.0);
-                x[5] = clampd(1.0 - s2 / r2, 0.0, 1.0);
-                mu0 = d.al[0 * LTs + k];
-                mu1 = d.al[1 * LTs + k];
-                sig = fmax(sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
-                const double smax = d.al_sigma_max_rel * sig0;
-                double hprev = INFINITY;
-                int kk = 0;
-                c_al = 1;
-                for (; kk < d.al_maxit; kk++) {
-                    F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
-                    ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
-                    c_it += it;
-                    c_cap += !ok;
-                    F4.flows(x, C, S, f0, f1, f2, f3);
-                    double h1 = (f0 * f0 + f1 * f1) / r2 - 1.0 + x[4];
-                    double h2 = (f2 * f2 + f3 * f3) / r2 - 1.0 + x[5];
-                    double hm = fmax(fabs(h1), fabs(h2));
-                    if (hm <= d.al_eta_star) break;
-                    mu0 += sig * h1;
-                    mu1 += sig * h2;
-                    if (hm > 0.25 * hprev) sig = fmin(10.0 * sig, smax);
-                    hprev = hm;
-                }
-                c_alcap = kk >= d.al_maxit;
-            }
+        for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
+        d.f[0 * LTs + k] = f0;
+        d.f[1 * LTs + k] = f1;
+        d.f[2 * LTs + k] = f2;
+        d.f[3 * LTs + k] = f3;
+        if (rate > 0.0 && (f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2)) {
+            const unsigned pos = atomicAdd(d.alq_cnt, 1u);
+            d.alq[pos] = k;
+        } else {
+            d.al[0 * LTs + k] = 0.0;
+            d.al[1 * LTs + k] = 0.0;
+            d.al[2 * LTs + k] = d.al_sigma0_rel * d.rpq * r2;
+            emit_tauhat(d, k, x, f0, f1, f2, f3);
         }
+    }
+    warp_add_u64(d.cnt + 0, c_it);
+    warp_add_u64(d.cnt + 1, c_cap);
+}
+
+// Phase 2: the queued thermal-active solves (6-variable slack AL, R36), pulled one at a time
+// by every thread of a persistent grid, so the heavy tail is spread over all SMs.
+__global__ void __launch_bounds__(64) k_branch_al(Dev d) {
+    if (d.st->done) return;
+    const size_t LTs = (size_t)d.L * d.T;
+    const unsigned n = *((volatile unsigned *)d.alq_cnt);
+    unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0;
+    for (;;) {
+        const unsigned idx = atomicAdd(d.alq_cnt + 1, 1u);
+        if (idx >= n) break;
+        const int k = d.alq[idx];
+        BrFun<true> F6;
+        double lo[6], hi[6];
+        {
+            BrFun<false> F4;
+            load_solve(d, k, F4, lo, hi);
+            F6.Gii = F4.Gii; F6.Gij = F4.Gij; F6.Gji = F4.Gji; F6.Gjj = F4.Gjj;
+            F6.Bii = F4.Bii; F6.Bij = F4.Bij; F6.Bji = F4.Bji; F6.Bjj = F4.Bjj;
+#pragma unroll
+            for (int r = 0; r < 8; r++) F6.tau[r] = F4.tau[r];
+            F6.rpq = F4.rpq; F6.rva = F4.rva;
+            F6.K00 = F4.K00; F6.K02 = F4.K02; F6.K03 = F4.K03; F6.K11 = F4.K11;
+            F6.K12 = F4.K12; F6.K13 = F4.K13; F6.K22 = F4.K22;
+        }
+        lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
+        lo[4] = 0.0; hi[4] = 1.0; lo[5] = 0.0; hi[5] = 1.0;
+        const double rate = d.rate[k / d.T];
+        const double r2 = rate * rate;
+        const double sig0 = d.al_sigma0_rel * d.rpq * r2;
+        F6.r2inv = 1.0 / r2;
+        double x[6];
+#pragma unroll
+        for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
+        {
+            const double f0 = d.f[0 * LTs + k], f1 = d.f[1 * LTs + k], f2 = d.f[2 * LTs + k], f3 = d.f[3 * LTs + k];
+            x[4] = clampd(1.0 - (f0 * f0 + f1 * f1) / r2, 0.0, 1.0);
+            x[5] = clampd(1.0 - (f2 * f2 + f3 * f3) / r2, 0.0, 1.0);
+        }
+        double mu0 = d.al[0 * LTs + k], mu1 = d.al[1 * LTs + k];
+        double sig = fmax(sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
+        const double smax = d.al_sigma_max_rel * sig0;
+        double hprev = INFINITY;
+        double C, S, f0, f1, f2, f3;
+        int kk = 0;
+        c_al += 1;
+        for (; kk < d.al_maxit; kk++) {
+            F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
+            int it = 0;
+            bool ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
+            c_it += it;
+            c_cap += !ok;
+            F6.flows(x, C, S, f0, f1, f2, f3);
+            double h1 = (f0 * f0 + f1 * f1) / r2 - 1.0 + x[4];
+            double h2 = (f2 * f2 + f3 * f3) / r2 - 1.0 + x[5];
+            double hm = fmax(fabs(h1), fabs(h2));
+            if (hm <= d.al_eta_star) break;
+            mu0 += sig * h1;
+            mu1 += sig * h2;
+            if (hm > 0.25 * hprev) sig = fmin(10.0 * sig, smax);
+            hprev = hm;
+        }
+        c_alcap += kk >= d.al_maxit;
+        F6.flows(x, C, S, f0, f1, f2, f3);
 #pragma unroll
         for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
         d.f[0 * LTs + k] = f0;
@@ -513,18 +585,20 @@ __global__ void __launch_bounds__(128) k_branch(Dev d) {
         d.al[0 * LTs + k] = mu0;
         d.al[1 * LTs + k] = mu1;
         d.al[2 * LTs + k] = sig;
+        emit_tauhat(d, k, x, f0, f1, f2, f3);
     }
-    warp_add_u64(d.cnt + 0, c_it);
-    warp_add_u64(d.cnt + 1, c_cap);
-    warp_add_u64(d.cnt + 2, c_al);
-    warp_add_u64(d.cnt + 3, c_alcap);
+    if (c_it) atomicAdd(d.cnt + 0, c_it);
+    if (c_cap) atomicAdd(d.cnt + 1, c_cap);
+    if (c_al) atomicAdd(d.cnt + 2, c_al);
+    if (c_alcap) atomicAdd(d.cnt + 3, c_alcap);
 }
 
 }  // namespace
 
 void launch_branch(const Dev &d, cudaStream_t s) {
     const int n = d.L * d.T;
-    k_branch<<<(n + 127) / 128, 128, 0, s>>>(d);
+    k_branch<<<(n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB, UCAC_BRANCH_TPB, 0, s>>>(d);
 }
+void launch_branch_al(const Dev &d, cudaStream_t s) { k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, 64, 0, s>>>(d); }
 
 }  // namespace ucac

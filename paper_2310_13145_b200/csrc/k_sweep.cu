@@ -84,15 +84,21 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 #define FX(k, i) d.f[(size_t)(k) * LT + (i)]
 #define FB(k, i) d.fbar[(size_t)(k) * LT + (i)]
 #define XX(k, i) d.x[(size_t)(k) * LT + (i)]
+#define TH(k, i) d.tauh[(size_t)(k) * LT + (i)]
 
 constexpr int BUS_THREADS = 128;
 constexpr int UBAR_THREADS = 128;
+constexpr int ROWS_THREADS = 128;
 
 // ------------------------------------------------------------------------- (7d) bus
+// k_bus: one thread per (i,t) solves the bus 2x2 KKT system from the bus-side targets of its
+// generators' rows (read here) and of its incident branch ends (tauhat, written by k_branch),
+// in canonical CSR order; writes the generator copies (and their rows GP, GQ, RC_{t+1}),
+// wbar, thbar and (muP, muQ, dwbar, dthbar) for k_rows.
 __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
-    const size_t GT = (size_t)d.G * T, LT = (size_t)d.L * T;
+    const size_t GT = (size_t)d.G * T, LT = (size_t)d.L * T, BT = (size_t)d.B * T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const double rpq = d.rpq, rva = d.rva;
     const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
         const int g0 = d.bg_ptr[i], g1 = d.bg_ptr[i + 1];
         const int e0 = d.be_ptr[i], e1 = d.be_ptr[i + 1];
         const int ne = e1 - e0;
-        // ---- pass 1: sums of the 2x2 KKT system, canonical order (gens, ends, wbar)
+        // ---- sums of the 2x2 KKT system, canonical order (gens, ends, wbar)
         double AP = 0.0, AQ = 0.0, C = 0.0, rP = d.pd[k], rQ = d.qd[k];
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
@@ -130,14 +136,13 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
             const size_t li = (size_t)l * T + t;
             const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
             const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
-            const double thp = FX(kp, li) + ZB(kp, li) + YB(kp, li) / rpq;
+            const double thp = TH(kp, li), thq = TH(kq, li), thw = TH(kw, li), tha = TH(ka, li);
             AP = AP + 1.0 / rpq;
             rP = rP + thp;
-            const double thq = FX(kq, li) + ZB(kq, li) + YB(kq, li) / rpq;
             AQ = AQ + 1.0 / rpq;
             rQ = rQ + thq;
-            wsum = wsum + (XX(side ? 1 : 0, li) + ZB(kw, li) + YB(kw, li) / rva);
-            tsum = tsum + (XX(side ? 3 : 2, li) + ZB(ka, li) + YB(ka, li) / rva);
+            wsum = wsum + thw;
+            tsum = tsum + tha;
         }
         const double thw = wsum / (double)ne;
         const double aw = (double)ne * rva;
@@ -150,13 +155,13 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
         const double det = AP * AQ - C * C;
         const double muP = (rP * AQ - C * rQ) / det;
         const double muQ = (AP * rQ - C * rP) / det;
-        // ---- pass 2: copies (v = tauhat + (alpha muP + beta muQ)/a) and their rows
+        // ---- generator copies and their rows
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
             const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) / rpq;
-            double th, aa, trc = 0.0;
+            double th, aa;
             if (t < T - 1) {
-                trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) / rpq;
+                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) / rpq;
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
             } else {
@@ -182,28 +187,54 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
         const double wbo = d.wbar[k], tbo = d.thbar[k];
         d.wbar[k] = wb;
         d.thbar[k] = tb;
-        for (int a = e0; a < e1; a++) {
-            const int code = d.be_idx[a];
-            const int l = code >> 1, side = code & 1;
-            const size_t li = (size_t)l * T + t;
-            const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
-            const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
-            const double fp = FX(kp, li), fq = FX(kq, li);
-            const double pb = (fp + ZB(kp, li) + YB(kp, li) / rpq) + (-muP) / rpq;
-            const double qb = (fq + ZB(kq, li) + YB(kq, li) / rpq) + (-muQ) / rpq;
-            const double pbo = FB(kp, li), qbo = FB(kq, li);
-            FB(kp, li) = pb;
-            FB(kq, li) = qb;
-            zy_row(fp - pb, rpq, beta, &ZB(kp, li), &YB(kp, li), &LB(kp, li), pending, beta_lam, lmax, pb - pbo, acc);
-            zy_row(fq - qb, rpq, beta, &ZB(kq, li), &YB(kq, li), &LB(kq, li), pending, beta_lam, lmax, qb - qbo, acc);
-            zy_row(XX(side ? 1 : 0, li) - wb, rva, beta, &ZB(kw, li), &YB(kw, li), &LB(kw, li), pending, beta_lam,
-                   lmax, wb - wbo, acc);
-            zy_row(XX(side ? 3 : 2, li) - tb, rva, beta, &ZB(ka, li), &YB(ka, li), &LB(ka, li), pending, beta_lam,
-                   lmax, tb - tbo, acc);
-        }
+        d.bmu[0 * BT + k] = muP;
+        d.bmu[1 * BT + k] = muQ;
+        d.bmu[2 * BT + k] = wb - wbo;
+        d.bmu[3 * BT + k] = tb - tbo;
     }
     block_reduce_store(acc, d.part_bus);
+    (void)LT;
 }
+
+// k_rows: one thread per (l,t) finishes step (7d) for the two ends of branch l (flow copies
+// fbar = tauhat - mu/rho_pq) and runs (7e)/(7f) for its 8 rows.  Same (l,t) mapping and
+// coalescing as k_branch.
+__global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t LT = (size_t)d.L * T, BT = (size_t)d.B * T;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const double rpq = d.rpq, rva = d.rva;
+    const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
+    const int pending = d.st->pending_outer;
+    Acc acc;
+    if (k < d.L * T) {
+        const int l = k / T, t = k - l * T;
+#pragma unroll
+        for (int side = 0; side < 2; side++) {
+            const int bus = side ? d.bto[l] : d.bfrom[l];
+            const size_t bk = (size_t)bus * T + t;
+            const double muP = d.bmu[0 * BT + bk], muQ = d.bmu[1 * BT + bk];
+            const double dwb = d.bmu[2 * BT + bk], dtb = d.bmu[3 * BT + bk];
+            const double wb = d.wbar[bk], tb = d.thbar[bk];
+            const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
+            const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
+            const double pb = TH(kp, k) + (-muP) / rpq;
+            const double qb = TH(kq, k) + (-muQ) / rpq;
+            const double pbo = FB(kp, k), qbo = FB(kq, k);
+            FB(kp, k) = pb;
+            FB(kq, k) = qb;
+            zy_row(FX(kp, k) - pb, rpq, beta, &ZB(kp, k), &YB(kp, k), &LB(kp, k), pending, beta_lam, lmax, pb - pbo, acc);
+            zy_row(FX(kq, k) - qb, rpq, beta, &ZB(kq, k), &YB(kq, k), &LB(kq, k), pending, beta_lam, lmax, qb - qbo, acc);
+            zy_row(XX(side ? 1 : 0, k) - wb, rva, beta, &ZB(kw, k), &YB(kw, k), &LB(kw, k), pending, beta_lam, lmax, dwb,
+                   acc);
+            zy_row(XX(side ? 3 : 2, k) - tb, rva, beta, &ZB(ka, k), &YB(ka, k), &LB(ka, k), pending, beta_lam, lmax, dtb,
+                   acc);
+        }
+    }
+    block_reduce_store(acc, d.part_rows);
+}
+
 
 // ------------------------------------------------------------------------- (7c) ubar
 __device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -407,9 +438,10 @@ __global__ void __launch_bounds__(256) k_reduce(Dev d) {
     double v[NPART];
 #pragma unroll
     for (int k = 0; k < NPART; k++) v[k] = 0.0;
-    const int nb = d.nblk_bus, nu = d.nblk_ubar;
-    for (int b = tid; b < nb + nu; b += 256) {
-        const double *pp = b < nb ? d.part_bus + (size_t)b * NPART : d.part_ubar + (size_t)(b - nb) * NPART;
+    const int nb = d.nblk_bus, nu = d.nblk_ubar, nr = d.nblk_rows;
+    for (int b = tid; b < nb + nu + nr; b += 256) {
+        const double *pp = b < nb ? d.part_bus + (size_t)b * NPART
+                         : (b < nb + nu ? d.part_ubar + (size_t)(b - nb) * NPART : d.part_rows + (size_t)(b - nb - nu) * NPART);
 #pragma unroll
         for (int k = 0; k < NPART; k++) {
             const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
@@ -443,6 +475,8 @@ __global__ void __launch_bounds__(256) k_reduce(Dev d) {
         st->al_active += d.cnt[2];
         st->al_capped += d.cnt[3];
         d.cnt[0] = d.cnt[1] = d.cnt[2] = d.cnt[3] = 0;
+        d.alq_cnt[0] = 0;
+        d.alq_cnt[1] = 0;
         st->inner_total += 1;
         st->inner_since += 1;
         if ((sh[0][P_BAD] != 0.0 || !isfinite(sh[0][P_RZ2]) || !isfinite(sh[0][P_OBJ])) && st->err_kernel == 0) {
@@ -484,8 +518,10 @@ __global__ void k_clear_pending(Dev d) { d.st->pending_outer = 0; }
 
 int nblk_bus(int B, int T) { return (B * T + BUS_THREADS - 1) / BUS_THREADS; }
 int nblk_ubar(int G, int T) { return (G * T + UBAR_THREADS - 1) / UBAR_THREADS; }
+int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; }
 
 void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d); }
+void launch_rows(const Dev &d, cudaStream_t s) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d); }
 void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
 void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, 256, 0, s>>>(d); }
 void launch_apply_outer(const Dev &d, cudaStream_t s) {

@@ -195,6 +195,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
     d.nblk_bus = nblk_bus(B, T);
     d.nblk_ubar = nblk_ubar(G, T);
+    d.nblk_rows = nblk_rows(L, T);
 
     const size_t GT = (size_t)G * T, LT = (size_t)L * T, BT = (size_t)B * T;
 #define ALLOC(field, type, n)                                   \
@@ -302,7 +303,12 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ALLOC(thbar, double, BT);
     ALLOC(part_bus, double, (size_t)d.nblk_bus * NPART);
     ALLOC(part_ubar, double, (size_t)d.nblk_ubar * NPART);
+    ALLOC(part_rows, double, (size_t)d.nblk_rows * NPART);
+    ALLOC(tauh, double, NBROW * LT);
+    ALLOC(bmu, double, 4 * BT);
     ALLOC(cnt, unsigned long long, 4);
+    ALLOC(alq, int, LT);
+    ALLOC(alq_cnt, unsigned, 2);
     ALLOC(st, DevStatus, 1);
     int8_t *uinit = nullptr;
     if (uc->u_init) {
@@ -337,12 +343,14 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
     launch_gen(ctx->d, ctx->s2);
     launch_branch(ctx->d, ctx->s);
+    launch_branch_al(ctx->d, ctx->s);
     cudaEventRecord(ctx->ev_join, ctx->s2);
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
     cudaEventRecord(ctx->ev_fork, ctx->s);
     cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
     launch_ubar(ctx->d, ctx->s2);
     launch_bus(ctx->d, ctx->s);
+    launch_rows(ctx->d, ctx->s);
     cudaEventRecord(ctx->ev_join, ctx->s2);
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
     launch_reduce(ctx->d, ctx->s);
@@ -409,7 +417,7 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
     return UCAC_OK;
 }
 
-static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce"};
+static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows"};
 extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
 
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
@@ -431,6 +439,8 @@ extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kern
                 case K_GEN: launch_gen(ctx->d, ctx->s); break;
                 case K_BUS: launch_bus(ctx->d, ctx->s); break;
                 case K_UBAR: launch_ubar(ctx->d, ctx->s); break;
+                case K_BRANCH_AL: launch_branch_al(ctx->d, ctx->s); break;
+                case K_ROWS: launch_rows(ctx->d, ctx->s); break;
                 default: launch_reduce(ctx->d, ctx->s); break;
             }
             CK(cudaEventRecord(b, ctx->s));
@@ -580,6 +590,7 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     h->err_kernel = 0;
     CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
     CK(cudaMemsetAsync(d.cnt, 0, 4 * sizeof(unsigned long long), ctx->s));
+    CK(cudaMemsetAsync(d.alq_cnt, 0, 2 * sizeof(unsigned), ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     return UCAC_OK;
 }
@@ -665,18 +676,23 @@ extern "C" ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz) {
     sz->branch_periods = LT;
     sz->bus_periods = BT;
     // Algorithmic bytes: every array element a kernel must read or write once.
-    // k_branch: read fbar(4) z(8) y(8) x(4) al(3) + wbar/thbar of both ends (4); write x(4) f(4) al(3)
-    //           -> 38 doubles per (l,t); static y(8) rate from/to per branch.
-    sz->alg_bytes[K_BRANCH] = LT * 38 * 8 + L * (9 * 8 + 2 * 4);
+    // k_branch: read fbar(4) z(8) y(8) x(4) al(3) + wbar/thbar of both ends (4); write x(4) f(4) al(3) tauhat(8)
+    sz->alg_bytes[K_BRANCH] = LT * 46 * 8 + L * (9 * 8 + 2 * 4);
     // k_gen: read ubar(3) pbar qbar z,y of 12 rows (24) ; write p q ph (3) + u (1 B)
     sz->alg_bytes[K_GEN] = GT * (29 * 8 + 1) + G * 24 * 8;
     // k_bus: per gen-period: read p q ph z,y,lambda of GP GQ RC (9) pbar qbar (2), write pbar qbar z y (8)
     //        per branch end-period: read f(2) x(2) z,y,lambda(12) fbar(2), write fbar(2) z,y(8)
     //        per bus-period: read pd qd wbar thbar, write wbar thbar
-    sz->alg_bytes[K_BUS] = GT * 19 * 8 + 2 * LT * 28 * 8 + BT * 6 * 8;
+    // k_bus: per gen-period read p q ph z,y,lambda of GP GQ RC (9) pbar qbar (2), write pbar qbar z y (8);
+    //        per end-period read tauhat (4); per bus-period read pd qd wbar thbar, write wbar thbar + 4 bmu
+    sz->alg_bytes[K_BUS] = GT * 19 * 8 + 2 * LT * 4 * 8 + BT * 10 * 8;
+    // k_rows: per (l,t) read tauhat p,q (4) f (4) x (4) z,y,lambda (24) fbar (4) + bmu/wbar/thbar of 2 buses (12);
+    //         write fbar (4) z y (16)
+    sz->alg_bytes[K_ROWS] = LT * 72 * 8;
     // k_ubar: per gen-period: read u p q ph ubar(3) z,y,lambda of 9 rows (27); write ubar(3) z,y (18)
     sz->alg_bytes[K_UBAR] = GT * (51 * 8 + 1);
-    sz->alg_bytes[K_REDUCE] = (int64_t)(ctx->d.nblk_bus + ctx->d.nblk_ubar) * NPART * 8;
+    sz->alg_bytes[K_REDUCE] = (int64_t)(ctx->d.nblk_bus + ctx->d.nblk_ubar + ctx->d.nblk_rows) * NPART * 8;
+    sz->alg_bytes[K_BRANCH_AL] = 0;  // data-dependent: 49 doubles per queued (l,t)
     int64_t tot = 0;
     for (int k = 0; k < NKERN; k++) tot += sz->alg_bytes[k];
     sz->alg_bytes_per_iter = tot;

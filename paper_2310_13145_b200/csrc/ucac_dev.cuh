@@ -16,7 +16,7 @@ enum GenRow { G_DON = 0, G_DSU, G_DSD, G_PL, G_PU, G_QL, G_QU, G_RD, G_RU, G_GP,
 enum BrRow { B_FPIJ = 0, B_FQIJ, B_FPJI, B_FQJI, B_WI, B_WJ, B_AI, B_AJ, NBROW };
 
 // kernel ids (ucac_kernel_name)
-enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, NKERN = 5 };
+enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, K_BRANCH_AL = 5, K_ROWS = 6, NKERN = 7 };
 
 // per-block reduction record (S8): max |r|, max |r+z|, sum (r+z)^2, max |z|, sum z^2,
 // max rho |dxbar|, objective, non-finite flag
@@ -42,7 +42,7 @@ struct DevStatus {
 struct Dev {
     int G, L, B, T;
     int ref_bus;
-    int nblk_bus, nblk_ubar;
+    int nblk_bus, nblk_ubar, nblk_rows;
     double S;                         // base MVA
     double rpq, rva, ruc;             // rho classes
     double tau, theta, lambda_max, beta_max, eps_inner_abs;
@@ -82,6 +82,11 @@ struct Dev {
     double *part_bus;                 // [nblk_bus][NPART]
     double *part_ubar;                // [nblk_ubar][NPART]
     unsigned long long *cnt;          // [4] per-iteration TRON counters (zeroed by reduce)
+    double *tauh;                     // [8][L*T] bus-side targets x + z + y/rho of the branch rows
+    double *bmu;                      // [4][B*T] muP, muQ, wbar - wbar_old, thbar - thbar_old
+    double *part_rows;                // [nblk_rows][NPART]
+    int *alq;                         // [L*T] queue of thermal-active solves (phase 2)
+    unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
     DevStatus *st;
 };
 
@@ -92,8 +97,11 @@ __host__ __device__ inline size_t gi(const Dev &d, int g, int t) { return (size_
 // launch wrappers (one per translation unit)
 namespace ucac {
 void launch_branch(const Dev &d, cudaStream_t s);
+void launch_branch_al(const Dev &d, cudaStream_t s);
 void launch_gen(const Dev &d, cudaStream_t s);
 void launch_bus(const Dev &d, cudaStream_t s);
+void launch_rows(const Dev &d, cudaStream_t s);
+int nblk_rows(int L, int T);
 void launch_ubar(const Dev &d, cudaStream_t s);
 void launch_reduce(const Dev &d, cudaStream_t s);
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s);

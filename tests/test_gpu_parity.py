@@ -20,6 +20,26 @@ FLOAT_FIELDS = ["p", "q", "ph", "ub_on", "ub_su", "ub_sd", "pbar", "qbar", "zg",
 SCALED = {"yg", "yb", "lg", "lb", "al"}
 
 
+KIND_SHAPE = {"zg": (12, -1), "yg": (12, -1), "lg": (12, -1), "zb": (8, -1), "yb": (8, -1), "lb": (8, -1)}
+COL_SHAPE = {"x": 4, "f": 4, "fbar": 4, "al": 3}
+
+
+def kind_scale(k, b):
+    """max(|b_i|, RMS of b_i's row kind): the normwise-relative scale of DESIGN.md 10 (residual
+    quantities such as z = -(lambda + y + rho r)/(beta + rho) cancel O(|x|) operands, so their
+    rounding error is relative to the kind's magnitude, not to their own)."""
+    if k in KIND_SHAPE:
+        m = b.reshape(KIND_SHAPE[k])
+        rms = np.sqrt(np.mean(m * m, axis=1, keepdims=True)) if m.size else m
+        return np.maximum(np.abs(m), rms).reshape(b.shape)
+    if k in COL_SHAPE:
+        m = b.reshape(-1, COL_SHAPE[k])
+        rms = np.sqrt(np.mean(m * m, axis=0, keepdims=True)) if m.size else m
+        return np.maximum(np.abs(m), rms).reshape(b.shape)
+    rms = np.sqrt(np.mean(b * b)) if b.size else 0.0
+    return np.maximum(np.abs(b), rms)
+
+
 def compare(gs, os_, rho_max, where="", eta_star=1e-10):
     assert np.array_equal(gs["u"], os_["u"]), f"schedule mismatch {where}"
     worst = {}
@@ -33,7 +53,7 @@ def compare(gs, os_, rho_max, where="", eta_star=1e-10):
             sig = b.reshape(-1, 3)[:, 2]
             atol = np.repeat(10.0 * sig * eta_star, 3) + ATOL * rho_max
             atol = atol.reshape(b.shape)
-        err = np.abs(a - b) - (atol + RTOL * np.abs(b))
+        err = np.abs(a - b) - (atol + RTOL * kind_scale(k, b))
         worst[k] = float(np.max(err)) if err.size else -1.0
         if worst[k] > 0:
             i = int(np.argmax(err))
