@@ -587,6 +587,13 @@ static int tron(int n, double *x, const double *lo, const double *hi, eval_fn ev
     for (int i = 0; i < n; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     ev(ctx, x, &f, g, H);
     double delta = TR_DELTA0, alpha = 1.0;
+    {
+        /* first Cauchy trial length: the model minimiser along -g (R41) */
+        double Hg[MAXN];
+        matvec(n, H, g, Hg);
+        double gHg = dot(n, g, Hg), gg = dot(n, g, g);
+        if (gHg > 0.0 && gg > 0.0) alpha = gg / gHg;
+    }
     int it;
     for (it = 0; it < maxit; it++) {
         if (pgnorm(n, x, g, lo, hi) <= gtol) { *iters = it; return 1; }

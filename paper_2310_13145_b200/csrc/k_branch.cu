@@ -256,6 +256,13 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
     for (int i = 0; i < N; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     fn.template eval<N, true>(x, f, g, H);
     double delta = TR_DELTA0, alpha = 1.0;
+    {
+        // first Cauchy trial length: the model minimiser along -g (R41)
+        double Hg[N];
+        matvec<N>(H, g, Hg);
+        const double gHg = dotn<N>(g, Hg), gg = dotn<N>(g, g);
+        if (gHg > 0.0 && gg > 0.0) alpha = gg / gHg;
+    }
     int it = 0;
     for (; it < maxit; it++) {
         double pgn = 0.0;

@@ -1,4 +1,5 @@
-// k_gen.cu -- steps (7a) and (7b, generator part), plus the cold-start kernel (S0) and the
+// k_gen.cu -- steps (7a) (k_gen: UC DP, warp per generator) and (7b, generator part; k_genx:
+// thread per (g,t)), plus the cold-start kernel (S0) and the
 // standalone batched DP.  Compiled with -fmad=false: every expression here is evaluated
 // in the operation order written (the same order the oracle's definition uses), so that the
 // integer DP decisions ("stay" when c_stay <= c_switch) are taken on the same fp64
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(128) k_gen(Dev d) {
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;
     DpSmem s = dp_carve(smem + (size_t)warp * dp_smem_bytes(T), T);
-    const double ruc = d.ruc, rpq = d.rpq;
+    const double ruc = d.ruc;
     // ---- (7a): stage costs on iterate l (ubar^l, y^l, z^l of the duplicate rows)
     const double c0 = d.c0[g], csu = d.csu[g], csd = d.csd[g];
     for (int t = lane; t < T; t += 32) {
@@ -255,7 +256,17 @@ __global__ void __launch_bounds__(128) k_gen(Dev d) {
     __syncwarp();
     dp_warp(s, T, d.tu[g], d.td[g], d.u0[g], d.hold[g]);
     for (int t = lane; t < T; t += 32) d.u[(size_t)g * T + t] = s.u[t];
-    // ---- (7b) generator part on iterate l
+}
+
+// (7b) generator part on iterate l: one thread per (g,t) (S2)
+__global__ void __launch_bounds__(128) k_genx(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t GT = (size_t)d.G * T;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= d.G * T) return;
+    const int g = k / T, t = k - g * T;
+    const double ruc = d.ruc, rpq = d.rpq;
     const double S = d.S;
     GenIn in;
     in.c2S2 = d.c2[g] * S * S;
@@ -270,26 +281,24 @@ __global__ void __launch_bounds__(128) k_gen(Dev d) {
     const double pmin = d.pmin[g], pmax = d.pmax[g], qmin = d.qmin[g], qmax = d.qmax[g];
     const double rdn = d.rdn[g], sdn = d.sdn[g], rup = d.rup[g], sup = d.sup[g];
     const double u0 = (double)d.u0[g];
-    for (int t = lane; t < T; t += 32) {
-        const size_t i = (size_t)g * T + t;
-        const double on = d.ub_on[i], su = d.ub_su[i], sd = d.ub_sd[i];
-        const double onp = t == 0 ? u0 : d.ub_on[i - 1];
-        in.first = t == 0;
-        in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) / rpq;
-        in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) / rpq;
-        in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / rpq;
-        in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) / ruc;
-        in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) / ruc;
-        in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) / ruc;
-        in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) / ruc;
-        in.brl = -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) / ruc;
-        in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) / ruc;
-        double po, qo, pho;
-        gen_solve(in, po, qo, pho);
-        d.p[i] = po;
-        d.q[i] = qo;
-        d.ph[i] = pho;
-    }
+    const size_t i = (size_t)k;
+    const double on = d.ub_on[i], su = d.ub_su[i], sd = d.ub_sd[i];
+    const double onp = t == 0 ? u0 : d.ub_on[i - 1];
+    in.first = t == 0;
+    in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) / rpq;
+    in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) / rpq;
+    in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / rpq;
+    in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) / ruc;
+    in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) / ruc;
+    in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) / ruc;
+    in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) / ruc;
+    in.brl = -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) / ruc;
+    in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) / ruc;
+    double po, qo, pho;
+    gen_solve(in, po, qo, pho);
+    d.p[i] = po;
+    d.q[i] = qo;
+    d.ph[i] = pho;
 }
 
 __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
@@ -369,6 +378,7 @@ void launch_gen(const Dev &d, cudaStream_t s) {
     const int warps = 4;
     k_gen<<<(d.G + warps - 1) / warps, warps * 32, gen_smem(d.T, warps), s>>>(d);
 }
+void launch_genx(const Dev &d, cudaStream_t s) { k_genx<<<(d.G * d.T + 127) / 128, 128, 0, s>>>(d); }
 
 void launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                      const int *hold, int8_t *sched, double *cost, cudaStream_t s) {

@@ -87,7 +87,7 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 #define TH(k, i) d.tauh[(size_t)(k) * LT + (i)]
 
 constexpr int BUS_THREADS = 128;
-constexpr int UBAR_THREADS = 128;
+constexpr int UBAR_THREADS = 64;
 constexpr int ROWS_THREADS = 128;
 
 // ------------------------------------------------------------------------- (7d) bus
@@ -431,15 +431,17 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
 }
 
 // ------------------------------------------------------------------------- S8 / S9
-__global__ void __launch_bounds__(256) k_reduce(Dev d) {
+constexpr int RED_THREADS = 1024;
+__global__ void __launch_bounds__(RED_THREADS) k_reduce(Dev d) {
     if (d.st->done) return;
-    __shared__ double sh[256][NPART];
-    const int tid = threadIdx.x;
+    __shared__ double sw[RED_THREADS / 32][NPART];
+    __shared__ double sh[1][NPART];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double v[NPART];
 #pragma unroll
     for (int k = 0; k < NPART; k++) v[k] = 0.0;
     const int nb = d.nblk_bus, nu = d.nblk_ubar, nr = d.nblk_rows;
-    for (int b = tid; b < nb + nu + nr; b += 256) {
+    for (int b = tid; b < nb + nu + nr; b += RED_THREADS) {
         const double *pp = b < nb ? d.part_bus + (size_t)b * NPART
                          : (b < nb + nu ? d.part_ubar + (size_t)(b - nb) * NPART : d.part_rows + (size_t)(b - nb - nu) * NPART);
 #pragma unroll
@@ -448,19 +450,27 @@ __global__ void __launch_bounds__(256) k_reduce(Dev d) {
             v[k] = isum ? v[k] + pp[k] : fmax(v[k], pp[k]);
         }
     }
+    // fixed-shape tree: warp butterflies, then warp results in index order
 #pragma unroll
-    for (int k = 0; k < NPART; k++) sh[tid][k] = v[k];
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (tid < s) {
+    for (int k = 0; k < NPART; k++) {
+        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
+        double x = v[k];
 #pragma unroll
-            for (int k = 0; k < NPART; k++) {
-                const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
-                sh[tid][k] = isum ? sh[tid][k] + sh[tid + s][k] : fmax(sh[tid][k], sh[tid + s][k]);
-            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_down_sync(0xffffffffu, x, o);
+            x = isum ? x + w : fmax(x, w);
         }
-        __syncthreads();
+        if (lane == 0) sw[warp][k] = x;
     }
+    __syncthreads();
+    if (tid < NPART) {
+        const int k = tid;
+        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
+        double x = sw[0][k];
+        for (int w = 1; w < RED_THREADS / 32; w++) x = isum ? x + sw[w][k] : fmax(x, sw[w][k]);
+        sh[0][k] = x;
+    }
+    __syncthreads();
     if (tid == 0) {
         DevStatus *st = d.st;
         st->primal_inf = sh[0][P_PINF];
@@ -523,7 +533,7 @@ int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; 
 void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d); }
 void launch_rows(const Dev &d, cudaStream_t s) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d); }
 void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
-void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, 256, 0, s>>>(d); }
+void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }
 void launch_apply_outer(const Dev &d, cudaStream_t s) {
     k_apply_outer<<<296, 256, 0, s>>>(d);
     k_clear_pending<<<1, 1, 0, s>>>(d);

@@ -337,23 +337,40 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
 #undef UPLOAD
 }
 
-// one inner iteration: [branch || gen] -> [bus || ubar] -> reduce
+// one inner iteration.  Dependency order (also the order of the eager, timed path):
+//   (7a) k_gen -> (7b) k_genx, k_branch, k_branch_al -> (7d) k_bus, k_rows -> (7c) k_ubar -> S8/S9.
+// In the graph the generator chain k_gen -> k_genx -> k_ubar (which never reads a branch
+// result) runs on a second stream, forked AFTER the register-bound fast-path branch kernel
+// (sharing the SMs with it halves its occupancy) and overlapping the latency-bound thermal
+// AL tail; the bus solve joins both chains.
+static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BRANCH_AL, K_BUS, K_ROWS, K_UBAR, K_REDUCE};
+
+static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
+    switch (k) {
+        case K_BRANCH: launch_branch(ctx->d, s); break;
+        case K_BRANCH_AL: launch_branch_al(ctx->d, s); break;
+        case K_GEN: launch_gen(ctx->d, s); break;
+        case K_GENX: launch_genx(ctx->d, s); break;
+        case K_BUS: launch_bus(ctx->d, s); break;
+        case K_ROWS: launch_rows(ctx->d, s); break;
+        case K_UBAR: launch_ubar(ctx->d, s); break;
+        default: launch_reduce(ctx->d, s); break;
+    }
+}
+
 static void enqueue_iteration(ucac_ctx *ctx) {
+    launch_kernel(ctx, K_BRANCH, ctx->s);
     cudaEventRecord(ctx->ev_fork, ctx->s);
     cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
-    launch_gen(ctx->d, ctx->s2);
-    launch_branch(ctx->d, ctx->s);
-    launch_branch_al(ctx->d, ctx->s);
+    launch_kernel(ctx, K_GEN, ctx->s2);
+    launch_kernel(ctx, K_GENX, ctx->s2);
+    launch_kernel(ctx, K_UBAR, ctx->s2);
     cudaEventRecord(ctx->ev_join, ctx->s2);
+    launch_kernel(ctx, K_BRANCH_AL, ctx->s);
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
-    cudaEventRecord(ctx->ev_fork, ctx->s);
-    cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
-    launch_ubar(ctx->d, ctx->s2);
-    launch_bus(ctx->d, ctx->s);
-    launch_rows(ctx->d, ctx->s);
-    cudaEventRecord(ctx->ev_join, ctx->s2);
-    cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
-    launch_reduce(ctx->d, ctx->s);
+    launch_kernel(ctx, K_BUS, ctx->s);
+    launch_kernel(ctx, K_ROWS, ctx->s);
+    launch_kernel(ctx, K_REDUCE, ctx->s);
 }
 
 static ucac_status build_graphs(ucac_ctx *ctx) {
@@ -417,7 +434,8 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
     return UCAC_OK;
 }
 
-static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows"};
+static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows",
+                                    "k_genx"};
 extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
 
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
@@ -431,18 +449,11 @@ extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kern
         ctx->tev.push_back(ev);
     }
     for (int it = 0; it < n; it++) {
-        for (int k = 0; k < NKERN; k++) {
+        for (int j = 0; j < NKERN; j++) {
+            const int k = kOrder[j];   // the graph's dependency order; events indexed by kernel id
             cudaEvent_t a = ctx->tev[((size_t)it * NKERN + k) * 2], b = ctx->tev[((size_t)it * NKERN + k) * 2 + 1];
             CK(cudaEventRecord(a, ctx->s));
-            switch (k) {
-                case K_BRANCH: launch_branch(ctx->d, ctx->s); break;
-                case K_GEN: launch_gen(ctx->d, ctx->s); break;
-                case K_BUS: launch_bus(ctx->d, ctx->s); break;
-                case K_UBAR: launch_ubar(ctx->d, ctx->s); break;
-                case K_BRANCH_AL: launch_branch_al(ctx->d, ctx->s); break;
-                case K_ROWS: launch_rows(ctx->d, ctx->s); break;
-                default: launch_reduce(ctx->d, ctx->s); break;
-            }
+            launch_kernel(ctx, k, ctx->s);
             CK(cudaEventRecord(b, ctx->s));
         }
     }
@@ -679,7 +690,10 @@ extern "C" ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz) {
     // k_branch: read fbar(4) z(8) y(8) x(4) al(3) + wbar/thbar of both ends (4); write x(4) f(4) al(3) tauhat(8)
     sz->alg_bytes[K_BRANCH] = LT * 46 * 8 + L * (9 * 8 + 2 * 4);
     // k_gen: read ubar(3) pbar qbar z,y of 12 rows (24) ; write p q ph (3) + u (1 B)
-    sz->alg_bytes[K_GEN] = GT * (29 * 8 + 1) + G * 24 * 8;
+    // k_gen (DP): read ubar, z, y of the 3 duplicate rows (9); write u (1 B)
+    sz->alg_bytes[K_GEN] = GT * (9 * 8 + 1);
+    // k_genx: read ubar(3) pbar qbar (2) z,y of 9 rows (18); write p q ph (3)
+    sz->alg_bytes[K_GENX] = GT * 26 * 8 + G * 24 * 8;
     // k_bus: per gen-period: read p q ph z,y,lambda of GP GQ RC (9) pbar qbar (2), write pbar qbar z y (8)
     //        per branch end-period: read f(2) x(2) z,y,lambda(12) fbar(2), write fbar(2) z,y(8)
     //        per bus-period: read pd qd wbar thbar, write wbar thbar

@@ -16,7 +16,8 @@ enum GenRow { G_DON = 0, G_DSU, G_DSD, G_PL, G_PU, G_QL, G_QU, G_RD, G_RU, G_GP,
 enum BrRow { B_FPIJ = 0, B_FQIJ, B_FPJI, B_FQJI, B_WI, B_WJ, B_AI, B_AJ, NBROW };
 
 // kernel ids (ucac_kernel_name)
-enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, K_BRANCH_AL = 5, K_ROWS = 6, NKERN = 7 };
+enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, K_BRANCH_AL = 5, K_ROWS = 6,
+                K_GENX = 7, NKERN = 8 };
 
 // per-block reduction record (S8): max |r|, max |r+z|, sum (r+z)^2, max |z|, sum z^2,
 // max rho |dxbar|, objective, non-finite flag
@@ -99,6 +100,7 @@ namespace ucac {
 void launch_branch(const Dev &d, cudaStream_t s);
 void launch_branch_al(const Dev &d, cudaStream_t s);
 void launch_gen(const Dev &d, cudaStream_t s);
+void launch_genx(const Dev &d, cudaStream_t s);
 void launch_bus(const Dev &d, cudaStream_t s);
 void launch_rows(const Dev &d, cudaStream_t s);
 int nblk_rows(int L, int T);
