@@ -226,7 +226,8 @@ __device__ __forceinline__ double qmodel(const double *g, const double (*H)[N], 
     matvec<N>(H, s, Hs);
     return dotn<N>(g, s) + 0.5 * dotn<N>(s, Hs);
 }
-__device__ __forceinline__ double clampd(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+// compare/select clamp (the oracle's form; cheaper than fmin/fmax with their NaN handling)
+__device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 template <int N>
 __device__ __forceinline__ void pstep(const double *x, const double *lo, const double *hi,
