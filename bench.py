@@ -181,7 +181,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2310_13145_b200 import ucac
 
-    ctx = ucac.Context(pb, pr)
+    def make_dist():
+        """N > 1: the bus-graph cut of the same problem, NCCL halo exchange"""
+        if world == 1:
+            return None
+        obj = [ucac.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return {"rank": rank, "nranks": world, "comm_mode": 0, "nccl_id": obj[0]}
+
+    ctx = ucac.Context(pb, pr, dist=make_dist())
     stream = torch.cuda.ExternalStream(ctx.stream)
     sizes = ctx.sizes()
     l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -196,6 +204,20 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def allmax(v):
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(v):
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     # ---- timed region: one graph-launched step per event pair, L2 flushed between steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -209,63 +231,60 @@ def main():
                 ends[k].record(stream)
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = allmax(sum(step_ms))
     rep1 = ctx.report()
-    newton = rep1["tron_iters"] - rep0["tron_iters"]
-
-    # ---- per-kernel device times (same kernels launched eagerly with an event pair each)
-    kms, klaunch = ctx.iterate_timed(args.steps)
-    rep2 = ctx.report()
-    newton_timed = rep2["tron_iters"] - rep1["tron_iters"]
-    ksum = sum(kms.values())
-    dom = max(kms, key=kms.get)
+    newton = allsum(rep1["tron_iters"] - rep0["tron_iters"])
     peaks = measured_peaks()
     clocks = clk.summary()
-    sm_mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median") or 1965.0
-    if dom == "k_branch":
-        flops = newton_timed * FLOPS_PER_NEWTON_ITER
-        achieved = flops / (kms[dom] * 1e-3) / 1e12
-        peak = fp64_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
-        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": dom,
-                    "peak_note": "FP64 non-tensor: 148 SM x 64 DFMA/clk x 2 at sm_max_mhz from MEASURED_PEAKS.json "
-                                 "(derived, DESIGN.md 8); flops = Newton iterations x FLOPS_PER_NEWTON_ITER",
-                    "share_of_step": kms[dom] / ksum, "kernel_ms_per_step": kms[dom] / args.steps}
-    else:
-        bytes_ = sizes["alg_bytes"][dom] * args.steps
-        achieved = bytes_ / (kms[dom] * 1e-3) / 1e9
-        peak = peaks.get("hbm_gbs", 6650.0)
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": dom, "share_of_step": kms[dom] / ksum,
-                    "kernel_ms_per_step": kms[dom] / args.steps}
-    sweep = {}
-    for k in ("k_bus", "k_ubar", "k_gen"):
-        b = sizes["alg_bytes"][k] * args.steps
-        gbs = b / (kms[k] * 1e-3) / 1e9
-        sweep[k] = {"alg_GBps": gbs, "frac_hbm": gbs / peaks.get("hbm_gbs", 6650.0),
-                    "ms_per_step": kms[k] / args.steps}
+
+    # ---- per-kernel device times (same kernels launched eagerly with an event pair each), 1 GPU
+    roofline, sweep, kms = None, None, None
+    if world == 1:
+        kms, klaunch = ctx.iterate_timed(args.steps)
+        rep2 = ctx.report()
+        newton_timed = rep2["tron_iters"] - rep1["tron_iters"]
+        ksum = sum(kms.values())
+        dom = max(kms, key=kms.get)
+        if dom in ("k_branch", "k_branch_al"):
+            flops = newton_timed * FLOPS_PER_NEWTON_ITER
+            kt = kms["k_branch"] + kms["k_branch_al"]
+            achieved = flops / (kt * 1e-3) / 1e12
+            peak = fp64_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
+            roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                        "traffic": None, "kernel": "k_branch+k_branch_al",
+                        "peak_note": "FP64 non-tensor: 148 SM x 64 DFMA/clk x 2 at sm_max_mhz from MEASURED_PEAKS.json "
+                                     "(derived, DESIGN.md 8); flops = Newton iterations x FLOPS_PER_NEWTON_ITER",
+                        "share_of_step": kt / ksum, "kernel_ms_per_step": kt / args.steps}
+        else:
+            bytes_ = sizes["alg_bytes"][dom] * args.steps
+            achieved = bytes_ / (kms[dom] * 1e-3) / 1e9
+            peak = peaks.get("hbm_gbs", 6650.0)
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "traffic": None, "kernel": dom, "share_of_step": kms[dom] / ksum,
+                        "kernel_ms_per_step": kms[dom] / args.steps}
+        sweep = {}
+        for k in ("k_bus", "k_rows", "k_ubar", "k_genx", "k_gen"):
+            b = sizes["alg_bytes"][k] * args.steps
+            gbs = b / (kms[k] * 1e-3) / 1e9
+            sweep[k] = {"alg_GBps": gbs, "frac_hbm": gbs / peaks.get("hbm_gbs", 6650.0),
+                        "ms_per_step": kms[k] / args.steps}
 
     # ---- e2e: the public API from host buffers (create = H2D of the problem, iterate,
-    #      residuals + solution = D2H), per step = one inner iteration
-    e2e = None
-    if rank == 0 or True:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        ctx2 = ucac.Context(pb, pr)
-        ctx2.iterate(args.steps)
-        _ = ctx2.report()
-        sol = ctx2.solution()
-        t1 = time.perf_counter()
-        ctx2.close()
-        h2d = problem_bytes(pb.normalized())
-        d2h = sum(v.nbytes for v in sol.values()) + 200
-        e2e = {"value": args.steps / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
-               "d2h_bytes_per_step": int(d2h / args.steps),
-               "note": "ucac_create(host arrays) + ucac_iterate(K) + ucac_residuals + ucac_get_solution, wall clock"}
+    #      residuals + solution = D2H), per step = one inner iteration, max over ranks
+    barrier()
+    t0 = time.perf_counter()
+    ctx2 = ucac.Context(pb, pr, dist=make_dist())
+    ctx2.iterate(args.steps)
+    _ = ctx2.report()
+    sol = ctx2.solution()
+    t1 = time.perf_counter()
+    ctx2.close()
+    e2e_s = allmax(t1 - t0)
+    h2d = problem_bytes(pb.normalized()) * world
+    d2h = allsum(sum(v.nbytes for v in sol.values()) + 200)
+    e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
+           "d2h_bytes_per_step": int(d2h / args.steps),
+           "note": "ucac_create(host arrays) + ucac_iterate(K) + ucac_residuals + ucac_get_solution, wall clock"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -275,26 +294,27 @@ def main():
                          f"single-threaded C oracle ({dt:.1f} s budget {args.cpu_budget:.0f} s)"}
 
     if rank == 0:
-        v = args.steps * world / (tot_ms * 1e-3)
+        v = args.steps / (tot_ms * 1e-3)
         line = {
             "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, paper_2310_13145_b200.inputs)",
             "config": {"workload": f"{args.config} (B={pb.nbus}, G={pb.ngen}, L={pb.nbranch}, T={pb.T})",
                        "rows": pb.nrows(), "branch_solves_per_step": pb.nbranch * pb.T,
                        "l2": "flushed (256 MiB memset) before every timed step",
-                       "parallelism": "replicas" if world > 1 else "single GPU"},
+                       "parallelism": f"bus-graph cut over {world} GPUs, NCCL halo exchange" if world > 1
+                       else "single GPU"},
             "branch_solves_per_s": v * pb.nbranch * pb.T,
-            "newton_iters_per_s": newton * world / (tot_ms * 1e-3),
+            "newton_iters_per_s": newton / (tot_ms * 1e-3),
             "newton_per_solve": newton / max(1, args.steps * pb.nbranch * pb.T),
             "primal_inf": rep1["primal_inf"],
             "roofline": roofline,
             "sweep_kernels": sweep,
-            "kernel_ms_per_step": {k: v_ / args.steps for k, v_ in kms.items()},
+            "kernel_ms_per_step": {k: v_ / args.steps for k, v_ in kms.items()} if kms else None,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 5 * args.steps,
+            "gpu_launches": (8 if world == 1 else 13) * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -100,12 +100,37 @@ typedef struct {
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
 } ucac_params;
 
-/* Multi-GPU (bus-graph cut).  NULL = single GPU. */
+/* Multi-GPU (bus-graph cut).  NULL = single GPU.
+ * Bus i belongs to rank bus_part[i]; generators follow their bus, branch (i -> j) follows bus
+ * i.  Every rank passes the SAME global problem and builds its local part with a halo: each
+ * inner iteration exchanges the cut ends' bus targets (4 doubles per cut branch-period) and
+ * the to-bus results back (6 per export bus-period), plus a 12-double reduction record
+ * (all-gather / all-reduce, NCCL over NVLink, captured in the iteration graph).
+ * comm_mode 0: one process per GPU, NCCL communicator from nccl_id (ucac_nccl_unique_id on rank
+ * 0, broadcast by the caller); the caller selects the device before create.
+ * comm_mode 1: in-process loopback group of nranks contexts on one device, iterated together
+ * with ucac_iterate_group (bitwise the single-GPU iteration; for tests and one-GPU runs). */
 typedef struct {
-    int32_t rank, nranks, device;
-    unsigned char nccl_id[128];     /* ncclUniqueId broadcast by the caller              */
-    const int32_t *bus_part;        /* [nbus] owner rank, or NULL = library partitions    */
+    int32_t rank, nranks, comm_mode;
+    unsigned char nccl_id[128];     /* ncclUniqueId (comm_mode 0)                          */
+    const int32_t *bus_part;        /* [nbus] owner rank, or NULL = ucac_partition(bus_xy)  */
+    const double *bus_xy;           /* [nbus*2] bus coordinates for the partitioner, or NULL */
 } ucac_dist;
+
+/* Deterministic bus-graph cut: weighted recursive coordinate bisection on bus_xy (weights
+ * 1 + branches owned, balancing the branch solves), or weighted BFS-order chunks when bus_xy
+ * is NULL.  part[nbus] receives ranks in [0, nparts).  Host only (no device needed). */
+ucac_status ucac_partition(int32_t nbus, int32_t nbranch, const int32_t *br_from, const int32_t *br_to,
+                           const double *bus_xy, int32_t nparts, int32_t *part);
+/* Halo of rank `rank` under `part` (host only): sizes[6] = owned buses, ghost buses, local
+ * branches, phantom branches (remote branches whose to-bus is owned), cut branches (local
+ * branches with a remote to-bus), export buses (owned to-buses of phantoms); the lists (global
+ * ids, ascending; any may be NULL) are caller-allocated with those sizes. */
+ucac_status ucac_halo_lists(int32_t nbus, int32_t nbranch, const int32_t *br_from, const int32_t *br_to,
+                            const int32_t *part, int32_t nparts, int32_t rank, int32_t *sizes,
+                            int32_t *own_bus, int32_t *ghost_bus, int32_t *local_branch, int32_t *phantom,
+                            int32_t *cut_branch, int32_t *export_bus);
+ucac_status ucac_nccl_unique_id(unsigned char *id /* [128] */);
 
 /* Create a context: validate (EINVAL with a message: non-finite data, vmin <= 0 or
  * vmin > vmax, pmin > pmax, qmin > qmax, c2 < 0, min_up/min_dn outside [1,T], hold outside
@@ -123,6 +148,15 @@ ucac_status ucac_create(const ucac_network *net, const ucac_horizon *hz, const u
  * Hitting n is not an error.  ENUMERIC when an iterate became non-finite. */
 ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_primal, double primal_target,
                          int32_t *n_done);
+
+/* n inner iterations of a comm_mode-1 loopback group: ctxs[r] is rank r of nranks = n contexts
+ * of one problem on the current device.  Synchronous. */
+ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t iters);
+
+/* Global ids of the context's local components (which: 0 generators, 1 branches, 2 owned
+ * buses), ascending; ids may be NULL to query *count.  The state/solution arrays of a
+ * multi-rank context are laid out over exactly these components. */
+ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids, int32_t *count);
 
 /* Same iterations launched kernel by kernel with a CUDA event pair around every launch;
  * kernel_ms[k] receives the summed device time of kernel k (order: ucac_kernel_name(k)),

@@ -28,7 +28,9 @@ UNITS = {
     "k_gen.cu": ["-fmad=false"],
     "k_sweep.cu": ["-fmad=false"],
     "ucac.cu": [],
+    "partition.cu": [],
 }
+LIBS = ["-lnccl"]
 
 
 def nvcc() -> str:
@@ -47,7 +49,7 @@ def _stale(target: str, deps) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
-    headers = [os.path.join(CSRC, "ucac_dev.cuh"), os.path.join(INCLUDE, "ucac.h")]
+    headers = [os.path.join(CSRC, "ucac_dev.cuh"), os.path.join(CSRC, "ucac_part.h"), os.path.join(INCLUDE, "ucac.h")]
     objs = []
     jobs = []
     for src, flags in UNITS.items():
@@ -72,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(lg)
     if force or jobs or _stale(LIB, objs):
         tmp = LIB + f".{os.getpid()}.tmp"
-        r = subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+        r = subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, *LIBS], capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
         os.replace(tmp, LIB)

@@ -13,6 +13,8 @@
 // The outer update lambda <- clip(lambda + beta z) decided at the end of iteration l is
 // applied lazily by the owning thread at the start of its row update in iteration l+1 (the
 // x-steps never read lambda), which saves a full pass over all rows.
+#include <algorithm>
+
 #include "ucac_dev.cuh"
 
 namespace ucac {
@@ -84,7 +86,7 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 #define FX(k, i) d.f[(size_t)(k) * LT + (i)]
 #define FB(k, i) d.fbar[(size_t)(k) * LT + (i)]
 #define XX(k, i) d.x[(size_t)(k) * LT + (i)]
-#define TH(k, i) d.tauh[(size_t)(k) * LT + (i)]
+#define TH(k, i) d.tauh[(size_t)(k) * LTH + (i)]
 
 constexpr int BUS_THREADS = 128;
 constexpr int UBAR_THREADS = 64;
@@ -99,12 +101,13 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t GT = (size_t)d.G * T, LT = (size_t)d.L * T, BT = (size_t)d.B * T;
+    const size_t LTH = (size_t)(d.L + d.Lph) * T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const double rpq = d.rpq, rva = d.rva;
     const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
     const int pending = d.st->pending_outer;
     Acc acc;
-    if (k < d.B * T) {
+    if (k < d.B_own * T) {   // owned buses only; ghost buses are solved by their owner
         const int i = k / T, t = k - i * T;
         const int g0 = d.bg_ptr[i], g1 = d.bg_ptr[i + 1];
         const int e0 = d.be_ptr[i], e1 = d.be_ptr[i + 1];
@@ -203,6 +206,7 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t LT = (size_t)d.L * T, BT = (size_t)d.B * T;
+    const size_t LTH = (size_t)(d.L + d.Lph) * T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const double rpq = d.rpq, rva = d.rva;
     const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
@@ -431,6 +435,42 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
 }
 
 // ------------------------------------------------------------------------- S8 / S9
+// S8 norms, inner test and the outer (lambda, beta) decision from a reduction record (R20-R22)
+__device__ void finalize_status(const Dev &d, const double *rec) {
+    DevStatus *st = d.st;
+    st->primal_inf = rec[R_PINF];
+    st->rz_inf = rec[R_RZINF];
+    st->rz_2 = sqrt(rec[R_RZ2]);
+    st->z_inf = rec[R_ZINF];
+    st->z_2 = sqrt(rec[R_Z2]);
+    st->dual_inf = rec[R_DINF];
+    st->objective = rec[R_OBJ];
+    st->tron_iters += (unsigned long long)rec[R_C0];
+    st->tron_capped += (unsigned long long)rec[R_C1];
+    st->al_active += (unsigned long long)rec[R_C2];
+    st->al_capped += (unsigned long long)rec[R_C3];
+    st->inner_total += 1;
+    st->inner_since += 1;
+    if ((rec[R_BAD] != 0.0 || !isfinite(rec[R_RZ2]) || !isfinite(rec[R_OBJ])) && st->err_kernel == 0) {
+        st->err_kernel = 1 + K_REDUCE;
+        st->err_iter = (int)st->inner_total;
+    }
+    st->pending_outer = 0;
+    if (d.outer_enabled && st->inner_since >= d.inner_min) {
+        const double thr = fmax(d.eps_inner_abs, 1e-2 / (double)st->outer_k);
+        if (st->rz_inf <= thr || st->inner_since >= d.inner_cap) {
+            const double zn = st->z_2;
+            st->pending_outer = 1;
+            st->beta_lam = st->beta;
+            if (st->outer_k > 1 && zn > d.theta * st->znorm_prev) st->beta = fmin(d.tau * st->beta, d.beta_max);
+            st->znorm_prev = zn;
+            st->outer_k += 1;
+            st->inner_since = 0;
+        }
+    }
+    if (st->stop_on_primal && st->primal_inf <= st->primal_target) st->done = 1;
+}
+
 constexpr int RED_THREADS = 1024;
 __global__ void __launch_bounds__(RED_THREADS) k_reduce(Dev d) {
     if (d.st->done) return;
@@ -472,41 +512,82 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(Dev d) {
     }
     __syncthreads();
     if (tid == 0) {
-        DevStatus *st = d.st;
-        st->primal_inf = sh[0][P_PINF];
-        st->rz_inf = sh[0][P_RZINF];
-        st->rz_2 = sqrt(sh[0][P_RZ2]);
-        st->z_inf = sh[0][P_ZINF];
-        st->z_2 = sqrt(sh[0][P_Z2]);
-        st->dual_inf = sh[0][P_DINF];
-        st->objective = sh[0][P_OBJ];
-        st->tron_iters += d.cnt[0];
-        st->tron_capped += d.cnt[1];
-        st->al_active += d.cnt[2];
-        st->al_capped += d.cnt[3];
+        double rec[NREC];
+        rec[R_RZ2] = sh[0][P_RZ2];
+        rec[R_Z2] = sh[0][P_Z2];
+        rec[R_OBJ] = sh[0][P_OBJ];
+        for (int c = 0; c < 4; c++) rec[R_C0 + c] = (double)d.cnt[c];
+        rec[R_PINF] = sh[0][P_PINF];
+        rec[R_RZINF] = sh[0][P_RZINF];
+        rec[R_ZINF] = sh[0][P_ZINF];
+        rec[R_DINF] = sh[0][P_DINF];
+        rec[R_BAD] = sh[0][P_BAD];
         d.cnt[0] = d.cnt[1] = d.cnt[2] = d.cnt[3] = 0;
         d.alq_cnt[0] = 0;
         d.alq_cnt[1] = 0;
-        st->inner_total += 1;
-        st->inner_since += 1;
-        if ((sh[0][P_BAD] != 0.0 || !isfinite(sh[0][P_RZ2]) || !isfinite(sh[0][P_OBJ])) && st->err_kernel == 0) {
-            st->err_kernel = 1 + K_REDUCE;
-            st->err_iter = (int)st->inner_total;
+        if (d.nranks > 1) {
+            for (int c = 0; c < NREC; c++) d.rec[c] = rec[c];   // cross-rank all-reduce, then k_finalize
+        } else {
+            finalize_status(d, rec);
         }
-        st->pending_outer = 0;
-        if (d.outer_enabled && st->inner_since >= d.inner_min) {
-            const double thr = fmax(d.eps_inner_abs, 1e-2 / (double)st->outer_k);
-            if (st->rz_inf <= thr || st->inner_since >= d.inner_cap) {
-                const double zn = st->z_2;
-                st->pending_outer = 1;
-                st->beta_lam = st->beta;
-                if (st->outer_k > 1 && zn > d.theta * st->znorm_prev) st->beta = fmin(d.tau * st->beta, d.beta_max);
-                st->znorm_prev = zn;
-                st->outer_k += 1;
-                st->inner_since = 0;
-            }
-        }
-        if (st->stop_on_primal && st->primal_inf <= st->primal_target) st->done = 1;
+    }
+}
+
+// S8/S9 on the (all-rank) reduction record
+__global__ void k_finalize(Dev d) {
+    if (d.st->done) return;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double rec[NREC];
+        for (int c = 0; c < NREC; c++) rec[c] = d.rec[c];
+        finalize_status(d, rec);
+    }
+}
+
+// ---- halo exchange: pack/unpack of the cut ends' tauhat and of bus results
+__device__ __forceinline__ int to_kind(int kk) { return kk == 0 ? B_FPJI : (kk == 1 ? B_FQJI : (kk == 2 ? B_WJ : B_AJ)); }
+__global__ void k_pack_tau(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t LTH = (size_t)(d.L + d.Lph) * T;
+    const int n = d.ncut * 4 * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, kk = (k / T) % 4, c = k / (4 * T);
+        d.xsend1[k] = TH(to_kind(kk), (size_t)d.cut_local[c] * T + t);
+    }
+}
+__global__ void k_unpack_tau(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t LTH = (size_t)(d.L + d.Lph) * T;
+    const int n = d.Lph * 4 * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, kk = (k / T) % 4, p = k / (4 * T);
+        TH(to_kind(kk), (size_t)(d.L + p) * T + t) = d.xrecv1[((size_t)d.phantom_src[p] * 4 + kk) * T + t];
+    }
+}
+__global__ void k_pack_bus(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t BT = (size_t)d.B * T;
+    const int n = d.nexport * 6 * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, f = (k / T) % 6, e = k / (6 * T);
+        const size_t bk = (size_t)d.export_local[e] * T + t;
+        d.xsend2[k] = f < 4 ? d.bmu[f * BT + bk] : (f == 4 ? d.wbar[bk] : d.thbar[bk]);
+    }
+}
+__global__ void k_unpack_bus(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t BT = (size_t)d.B * T;
+    const int n = d.nghost * 6 * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, f = (k / T) % 6, gb = k / (6 * T);
+        const size_t bk = (size_t)(d.B_own + gb) * T + t;
+        const double v = d.xrecv2[((size_t)d.ghost_src[gb] * 6 + f) * T + t];
+        if (f < 4) d.bmu[f * BT + bk] = v;
+        else if (f == 4) d.wbar[bk] = v;
+        else d.thbar[bk] = v;
     }
 }
 
@@ -534,6 +615,13 @@ void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS,
 void launch_rows(const Dev &d, cudaStream_t s) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d); }
 void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
 void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }
+void launch_reduce_part(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }
+void launch_finalize(const Dev &d, cudaStream_t s) { k_finalize<<<1, 32, 0, s>>>(d); }
+static int xgrid(int n) { return std::max(1, std::min(296, (n + 255) / 256)); }
+void launch_pack_tau(const Dev &d, cudaStream_t s) { k_pack_tau<<<xgrid(d.ncut * 4 * d.T), 256, 0, s>>>(d); }
+void launch_unpack_tau(const Dev &d, cudaStream_t s) { k_unpack_tau<<<xgrid(d.Lph * 4 * d.T), 256, 0, s>>>(d); }
+void launch_pack_bus(const Dev &d, cudaStream_t s) { k_pack_bus<<<xgrid(d.nexport * 6 * d.T), 256, 0, s>>>(d); }
+void launch_unpack_bus(const Dev &d, cudaStream_t s) { k_unpack_bus<<<xgrid(d.nghost * 6 * d.T), 256, 0, s>>>(d); }
 void launch_apply_outer(const Dev &d, cudaStream_t s) {
     k_apply_outer<<<296, 256, 0, s>>>(d);
     k_clear_pending<<<1, 1, 0, s>>>(d);

@@ -1,12 +1,12 @@
 // ucac.cu -- host runtime of libucac.so: the C ABI of include/ucac.h.
 //
-// create: validate -> build the device layout (SoA, CSR incidence in canonical order) ->
-// cold start kernel.  iterate: a CUDA graph of U inner iterations (fork/join so that the
-// branch solves run concurrently with the generator DP/x-update, and the bus update with
-// the ubar update), launched back to back; no host round trip inside the loop.  The device
-// status word carries the inner test, the outer (lambda, beta) decision and the
-// stop-on-primal flag, so the host never has to look at the iterate.
+// create: validate -> build the rank-local problem (the whole problem on one GPU; the bus-graph
+// cut with its halo on several) -> device layout (SoA, CSR incidence in canonical
+// order) -> cold start kernel -> CUDA graphs of 1 and 16 inner iterations.  iterate: graph
+// launches back to back; the device status word carries the inner test, the outer (lambda,
+// beta) decision and the stop-on-primal flag, so the host never looks at the iterate.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -18,6 +18,7 @@
 
 #include "ucac.h"
 #include "ucac_dev.cuh"
+#include "ucac_part.h"
 
 namespace ucac {
 void launch_apply_outer(const Dev &d, cudaStream_t s);
@@ -29,20 +30,154 @@ using namespace ucac;
 
 static thread_local std::string g_create_err;
 
+// ------------------------------------------------------------------------------------------
+// the rank-local problem (host vectors) -- identity for a single GPU
+// ------------------------------------------------------------------------------------------
+struct Local {
+    int B = 0, Bo = 0, G = 0, L = 0, Lp = 0, T = 0, ref = -1;
+    double S = 100.0;
+    std::vector<double> gs, bs, vmin, vmax, pdT, qdT;            // buses (own + ghost)
+    std::vector<int> from, to;                                    // local branches (local bus ids)
+    std::vector<double> ysoa, rate;
+    std::vector<int> gbus, tu, td, u0, hold;                      // local generators
+    std::vector<double> pmin, pmax, qmin, qmax, c2, c1, c0, csu, csd, rup, rdn, sup, sdn, p0;
+    std::vector<int8_t> uinit;                                    // [G*T] or empty
+    std::vector<int> bgp, bgi, bep, bei;                          // CSR for owned buses
+    std::vector<int> gen_global, branch_global, bus_global;      // local -> global (owned buses)
+    // halo
+    std::vector<int> cut_local, export_local, phantom_src, ghost_src;
+    int max_cut = 0, max_export = 0;
+};
+
+static Local build_local(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co, const ucac_uc *uc,
+                         const int32_t *part, int nranks, int rank) {
+    Local P;
+    const int B = net->nbus, G = net->ngen, L = net->nbranch, T = hz->T;
+    P.T = T;
+    P.S = net->base_mva;
+    Halo h;
+    if (nranks > 1) {
+        h = build_halo(B, L, net->br_from, net->br_to, part, nranks, rank);
+    } else {
+        h.own_bus.resize(B);
+        for (int i = 0; i < B; i++) h.own_bus[i] = i;
+        h.local_branch.resize(L);
+        for (int l = 0; l < L; l++) h.local_branch[l] = l;
+        h.bus_local.resize(B);
+        for (int i = 0; i < B; i++) h.bus_local[i] = i;
+        h.br_local.resize(L);
+        for (int l = 0; l < L; l++) h.br_local[l] = l;
+    }
+    P.Bo = (int)h.own_bus.size();
+    P.B = P.Bo + (int)h.ghost_bus.size();
+    P.L = (int)h.local_branch.size();
+    P.Lp = (int)h.phantom.size();
+    std::vector<int> bus_glob(h.own_bus);
+    bus_glob.insert(bus_glob.end(), h.ghost_bus.begin(), h.ghost_bus.end());
+    P.bus_global = h.own_bus;
+    for (int a = 0; a < P.B; a++) {
+        int i = bus_glob[a];
+        P.gs.push_back(net->bus_gs[i]);
+        P.bs.push_back(net->bus_bs[i]);
+        P.vmin.push_back(net->bus_vmin[i]);
+        P.vmax.push_back(net->bus_vmax[i]);
+    }
+    P.ref = h.bus_local[net->ref_bus] >= 0 && h.bus_local[net->ref_bus] < P.Bo ? h.bus_local[net->ref_bus] : -1;
+    P.pdT.assign((size_t)P.B * T, 0.0);
+    P.qdT.assign((size_t)P.B * T, 0.0);
+    for (int a = 0; a < P.Bo; a++)
+        for (int t = 0; t < T; t++) {
+            P.pdT[(size_t)a * T + t] = hz->pd[(size_t)t * B + bus_glob[a]];
+            P.qdT[(size_t)a * T + t] = hz->qd[(size_t)t * B + bus_glob[a]];
+        }
+    P.ysoa.assign((size_t)8 * P.L, 0.0);
+    for (int a = 0; a < P.L; a++) {
+        int l = h.local_branch[a];
+        P.from.push_back(h.bus_local[net->br_from[l]]);
+        P.to.push_back(h.bus_local[net->br_to[l]]);
+        P.rate.push_back(net->br_rate[l]);
+        for (int k = 0; k < 8; k++) P.ysoa[(size_t)k * P.L + a] = net->br_y[(size_t)l * 8 + k];
+    }
+    P.branch_global = h.local_branch;
+    for (int g = 0; g < G; g++) {
+        int lb = h.bus_local[net->gen_bus[g]];
+        if (lb < 0 || lb >= P.Bo) continue;
+        P.gen_global.push_back(g);
+        P.gbus.push_back(lb);
+        P.tu.push_back(uc->min_up[g]);
+        P.td.push_back(uc->min_dn[g]);
+        P.u0.push_back(uc->u0[g]);
+        P.hold.push_back(uc->hold[g]);
+        P.pmin.push_back(net->gen_pmin[g]);
+        P.pmax.push_back(net->gen_pmax[g]);
+        P.qmin.push_back(net->gen_qmin[g]);
+        P.qmax.push_back(net->gen_qmax[g]);
+        P.c2.push_back(co->c2[g]);
+        P.c1.push_back(co->c1[g]);
+        P.c0.push_back(co->c0[g]);
+        P.csu.push_back(co->startup[g]);
+        P.csd.push_back(co->shutdown[g]);
+        P.rup.push_back(uc->ramp_up[g]);
+        P.rdn.push_back(uc->ramp_dn[g]);
+        P.sup.push_back(uc->su_ramp[g]);
+        P.sdn.push_back(uc->sd_ramp[g]);
+        P.p0.push_back(uc->p0[g]);
+        if (uc->u_init)
+            for (int t = 0; t < T; t++) P.uinit.push_back(uc->u_init[(size_t)g * T + t]);
+    }
+    P.G = (int)P.gen_global.size();
+    // CSR of the owned buses in canonical order: generators by global index, then branch ends by
+    // global (l, side) -- local and phantom branches interleaved exactly as on one GPU
+    P.bgp.assign(P.Bo + 1, 0);
+    P.bep.assign(P.Bo + 1, 0);
+    for (int a = 0; a < P.G; a++) P.bgp[P.gbus[a] + 1]++;
+    struct End { int gl, side, bus, code; };
+    std::vector<End> ends;
+    for (int l = 0; l < L; l++) {
+        int lf = h.bus_local[net->br_from[l]], lt = h.bus_local[net->br_to[l]];
+        int ll = h.br_local[l];
+        if (ll < 0) continue;
+        if (lf >= 0 && lf < P.Bo && ll < P.L) ends.push_back({l, 0, lf, 2 * ll});
+        if (lt >= 0 && lt < P.Bo) ends.push_back({l, 1, lt, 2 * ll + 1});
+    }
+    for (auto &e : ends) P.bep[e.bus + 1]++;
+    for (int i = 0; i < P.Bo; i++) {
+        P.bgp[i + 1] += P.bgp[i];
+        P.bep[i + 1] += P.bep[i];
+    }
+    P.bgi.assign(P.G, 0);
+    P.bei.assign(ends.size(), 0);
+    {
+        std::vector<int> fg(P.Bo, 0), fe(P.Bo, 0);
+        for (int a = 0; a < P.G; a++) P.bgi[P.bgp[P.gbus[a]] + fg[P.gbus[a]]++] = a;
+        for (auto &e : ends) P.bei[P.bep[e.bus] + fe[e.bus]++] = e.code;   // ends already in (l, side) order
+    }
+    P.cut_local = h.cut_local;
+    P.export_local = h.export_local;
+    P.phantom_src = h.phantom_src;
+    P.ghost_src = h.ghost_src;
+    P.max_cut = h.max_cut;
+    P.max_export = h.max_export;
+    return P;
+}
+
 struct ucac_ctx {
     Dev d{};
-    int G = 0, L = 0, B = 0, T = 0;
+    Local P;
+    int G = 0, L = 0, B = 0, T = 0;      // local counts (B = owned buses)
+    int nranks = 1, rank = 0, comm_mode = 0;
+    ncclComm_t comm = nullptr;
     cudaStream_t s = nullptr, s2 = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int gunroll[2] = {1, 16};
     std::vector<void *> dalloc;
-    DevStatus *st_host = nullptr;   // pinned mirror
+    DevStatus *st_host = nullptr;        // pinned mirror
     std::string err;
-    std::vector<cudaEvent_t> tev;   // timed-iteration event pool
+    std::vector<cudaEvent_t> tev;        // timed-iteration event pool
     ucac_params prm{};
-    bool ctl_dirty = true;          // device control fields may hold a stop/done state
+    bool ctl_dirty = true;               // device control fields may hold a stop/done state
 };
 
 #define CK(call)                                                                           \
@@ -51,6 +186,14 @@ struct ucac_ctx {
         if (e_ != cudaSuccess) {                                                           \
             ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
             return UCAC_ECUDA;                                                             \
+        }                                                                                  \
+    } while (0)
+#define NK(call)                                                                           \
+    do {                                                                                   \
+        ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess) {                                                           \
+            ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);                \
+            return UCAC_ENCCL;                                                             \
         }                                                                                  \
     } while (0)
 
@@ -78,6 +221,7 @@ static Tp *dnew(ucac_ctx *ctx, size_t n, cudaError_t &e) {
 
 template <class Tp>
 static cudaError_t up(ucac_ctx *ctx, Tp *dst, const Tp *src, size_t n) {
+    if (n == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, n * sizeof(Tp), cudaMemcpyHostToDevice, ctx->s);
 }
 
@@ -142,6 +286,19 @@ static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, con
 
 static ucac_status build_graphs(ucac_ctx *ctx);
 
+extern "C" ucac_status ucac_nccl_unique_id(unsigned char *id) {
+    if (!id) return UCAC_EINVAL;
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) {
+        g_create_err = ncclGetErrorString(r);
+        return UCAC_ENCCL;
+    }
+    static_assert(sizeof(ncclUniqueId) <= 128, "ncclUniqueId size");
+    memcpy(id, &u, sizeof(u));
+    return UCAC_OK;
+}
+
 extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co,
                                    const ucac_uc *uc, const ucac_params *prm, const ucac_dist *dist,
                                    void *cuda_stream, ucac_ctx **out) {
@@ -149,8 +306,12 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     *out = nullptr;
     ucac_status vs = validate(net, hz, co, uc, prm);
     if (vs != UCAC_OK) return vs;
-    if (dist && dist->nranks > 1)
-        return fail(nullptr, UCAC_EUNSUPPORTED, "multi-rank contexts: use the partitioned runtime (DESIGN.md 9)");
+    const int nranks = dist ? dist->nranks : 1;
+    const int rank = dist ? dist->rank : 0;
+    if (nranks < 1 || rank < 0 || rank >= nranks || nranks > net->nbus)
+        return fail(nullptr, UCAC_EINVAL, "bad rank %d / nranks %d", rank, nranks);
+    if (dist && nranks > 1 && dist->comm_mode != 0 && dist->comm_mode != 1)
+        return fail(nullptr, UCAC_EINVAL, "comm_mode must be 0 (NCCL) or 1 (loopback group)");
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
@@ -159,15 +320,36 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "%s", cudaGetErrorString(e));
     if (prop.major != 10) return fail(nullptr, UCAC_ECUDA, "libucac is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
 
+    std::vector<int32_t> part;
+    if (nranks > 1) {
+        part.assign(net->nbus, 0);
+        if (dist->bus_part) {
+            for (int i = 0; i < net->nbus; i++) {
+                if (dist->bus_part[i] < 0 || dist->bus_part[i] >= nranks) return fail(nullptr, UCAC_EINVAL, "bus_part out of range");
+                part[i] = dist->bus_part[i];
+            }
+        } else if (partition_buses(net->nbus, net->nbranch, net->br_from, net->br_to, dist->bus_xy, nranks, part.data())) {
+            return fail(nullptr, UCAC_EINVAL, "partitioner failed");
+        }
+    }
     ucac_ctx *ctx = new ucac_ctx();
     ctx->prm = *prm;
-    const int B = net->nbus, G = net->ngen, L = net->nbranch, T = hz->T;
-    ctx->B = B; ctx->G = G; ctx->L = L; ctx->T = T;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    ctx->comm_mode = dist && nranks > 1 ? dist->comm_mode : 0;
+    ctx->P = build_local(net, hz, co, uc, part.data(), nranks, rank);
+    Local &P = ctx->P;
+    const int B = P.B, G = P.G, L = P.L, T = P.T;
+    ctx->B = P.Bo;
+    ctx->G = G;
+    ctx->L = L;
+    ctx->T = T;
     auto bail = [&](ucac_status s) {
         g_create_err = ctx->err;
         ucac_destroy(ctx);
         return s;
     };
+    if (G == 0 || L == 0) return bail(fail(ctx, UCAC_EUNSUPPORTED, "rank %d owns no generator or no branch; use fewer ranks", rank));
     if (cuda_stream) {
         ctx->s = (cudaStream_t)cuda_stream;
     } else {
@@ -180,11 +362,26 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
     if (cudaMallocHost(&ctx->st_host, sizeof(DevStatus)) != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
     memset(ctx->st_host, 0, sizeof(DevStatus));
+    if (nranks > 1 && ctx->comm_mode == 0) {
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+        if (r != ncclSuccess) return bail(fail(ctx, UCAC_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
 
     Dev &d = ctx->d;
     d.G = G; d.L = L; d.B = B; d.T = T;
-    d.ref_bus = net->ref_bus;
-    d.S = net->base_mva;
+    d.B_own = P.Bo;
+    d.Lph = P.Lp;
+    d.nranks = nranks;
+    d.ncut = (int)P.cut_local.size();
+    d.nexport = (int)P.export_local.size();
+    d.nphantom_src = (int)P.phantom_src.size();
+    d.nghost = B - P.Bo;
+    d.max_cut = P.max_cut;
+    d.max_export = P.max_export;
+    d.ref_bus = P.ref;
+    d.S = P.S;
     d.rpq = prm->rho_pq; d.rva = prm->rho_va; d.ruc = prm->rho_uc;
     d.tau = prm->tau; d.theta = prm->theta; d.lambda_max = prm->lambda_max; d.beta_max = prm->beta_max;
     d.eps_inner_abs = prm->eps_inner_abs;
@@ -193,7 +390,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.tron_maxit = prm->tron_maxit; d.al_maxit = prm->al_maxit;
     d.al_eta_star = prm->al_eta_star; d.al_sigma0_rel = prm->al_sigma0_rel;
     d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
-    d.nblk_bus = nblk_bus(B, T);
+    d.nblk_bus = nblk_bus(P.Bo, T);
     d.nblk_ubar = nblk_ubar(G, T);
     d.nblk_rows = nblk_rows(L, T);
 
@@ -204,81 +401,50 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc %s", #field)); \
         d.field = p_;                                           \
     } while (0)
-#define UPLOAD(field, type, src, n)                             \
+#define UPLOAD(field, type, vec)                                \
     do {                                                        \
-        type *p_ = dnew<type>(ctx, (n), e);                     \
+        type *p_ = dnew<type>(ctx, (vec).size(), e);            \
         if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc %s", #field)); \
-        if (up<type>(ctx, p_, (src), (n)) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "upload %s", #field)); \
+        if (up<type>(ctx, p_, (vec).data(), (vec).size()) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "upload %s", #field)); \
         d.field = p_;                                           \
     } while (0)
-    // static generator data
-    UPLOAD(gbus, int, net->gen_bus, G);
-    UPLOAD(tu, int, uc->min_up, G);
-    UPLOAD(td, int, uc->min_dn, G);
-    UPLOAD(u0, int, uc->u0, G);
-    UPLOAD(hold, int, uc->hold, G);
-    UPLOAD(pmin, double, net->gen_pmin, G);
-    UPLOAD(pmax, double, net->gen_pmax, G);
-    UPLOAD(qmin, double, net->gen_qmin, G);
-    UPLOAD(qmax, double, net->gen_qmax, G);
-    UPLOAD(c2, double, co->c2, G);
-    UPLOAD(c1, double, co->c1, G);
-    UPLOAD(c0, double, co->c0, G);
-    UPLOAD(csu, double, co->startup, G);
-    UPLOAD(csd, double, co->shutdown, G);
-    UPLOAD(rup, double, uc->ramp_up, G);
-    UPLOAD(rdn, double, uc->ramp_dn, G);
-    UPLOAD(sup, double, uc->su_ramp, G);
-    UPLOAD(sdn, double, uc->sd_ramp, G);
-    UPLOAD(p0, double, uc->p0, G);
-    // branch data, admittance as SoA [8][L]
-    std::vector<double> ysoa((size_t)8 * L);
-    for (int l = 0; l < L; l++)
-        for (int k = 0; k < 8; k++) ysoa[(size_t)k * L + l] = net->br_y[(size_t)l * 8 + k];
-    UPLOAD(y, double, ysoa.data(), (size_t)8 * L);
-    UPLOAD(rate, double, net->br_rate, L);
-    UPLOAD(bfrom, int, net->br_from, L);
-    UPLOAD(bto, int, net->br_to, L);
-    // bus data, demand transposed to [B][T]
-    UPLOAD(gs, double, net->bus_gs, B);
-    UPLOAD(bs, double, net->bus_bs, B);
-    UPLOAD(vmin, double, net->bus_vmin, B);
-    UPLOAD(vmax, double, net->bus_vmax, B);
-    std::vector<double> pdT(BT), qdT(BT);
-    for (int t = 0; t < T; t++)
-        for (int i = 0; i < B; i++) {
-            pdT[(size_t)i * T + t] = hz->pd[(size_t)t * B + i];
-            qdT[(size_t)i * T + t] = hz->qd[(size_t)t * B + i];
-        }
-    UPLOAD(pd, double, pdT.data(), BT);
-    UPLOAD(qd, double, qdT.data(), BT);
-    // CSR incidence, canonical order: generators by index, ends by (l, side)
-    std::vector<int> bgp(B + 1, 0), bep(B + 1, 0), bgi(G), bei((size_t)2 * L);
-    for (int g = 0; g < G; g++) bgp[net->gen_bus[g] + 1]++;
-    for (int l = 0; l < L; l++) {
-        bep[net->br_from[l] + 1]++;
-        bep[net->br_to[l] + 1]++;
-    }
-    for (int i = 0; i < B; i++) {
-        bgp[i + 1] += bgp[i];
-        bep[i + 1] += bep[i];
-    }
-    {
-        std::vector<int> fg(B, 0), fe(B, 0);
-        for (int g = 0; g < G; g++) {
-            int i = net->gen_bus[g];
-            bgi[bgp[i] + fg[i]++] = g;
-        }
-        for (int l = 0; l < L; l++) {
-            int i = net->br_from[l], j = net->br_to[l];
-            bei[bep[i] + fe[i]++] = 2 * l;
-            bei[bep[j] + fe[j]++] = 2 * l + 1;
-        }
-    }
-    UPLOAD(bg_ptr, int, bgp.data(), B + 1);
-    UPLOAD(bg_idx, int, bgi.data(), G);
-    UPLOAD(be_ptr, int, bep.data(), B + 1);
-    UPLOAD(be_idx, int, bei.data(), (size_t)2 * L);
+    UPLOAD(gbus, int, P.gbus);
+    UPLOAD(tu, int, P.tu);
+    UPLOAD(td, int, P.td);
+    UPLOAD(u0, int, P.u0);
+    UPLOAD(hold, int, P.hold);
+    UPLOAD(pmin, double, P.pmin);
+    UPLOAD(pmax, double, P.pmax);
+    UPLOAD(qmin, double, P.qmin);
+    UPLOAD(qmax, double, P.qmax);
+    UPLOAD(c2, double, P.c2);
+    UPLOAD(c1, double, P.c1);
+    UPLOAD(c0, double, P.c0);
+    UPLOAD(csu, double, P.csu);
+    UPLOAD(csd, double, P.csd);
+    UPLOAD(rup, double, P.rup);
+    UPLOAD(rdn, double, P.rdn);
+    UPLOAD(sup, double, P.sup);
+    UPLOAD(sdn, double, P.sdn);
+    UPLOAD(p0, double, P.p0);
+    UPLOAD(y, double, P.ysoa);
+    UPLOAD(rate, double, P.rate);
+    UPLOAD(bfrom, int, P.from);
+    UPLOAD(bto, int, P.to);
+    UPLOAD(gs, double, P.gs);
+    UPLOAD(bs, double, P.bs);
+    UPLOAD(vmin, double, P.vmin);
+    UPLOAD(vmax, double, P.vmax);
+    UPLOAD(pd, double, P.pdT);
+    UPLOAD(qd, double, P.qdT);
+    UPLOAD(bg_ptr, int, P.bgp);
+    UPLOAD(bg_idx, int, P.bgi);
+    UPLOAD(be_ptr, int, P.bep);
+    UPLOAD(be_idx, int, P.bei);
+    UPLOAD(cut_local, int, P.cut_local);
+    UPLOAD(export_local, int, P.export_local);
+    UPLOAD(phantom_src, int, P.phantom_src);
+    UPLOAD(ghost_src, int, P.ghost_src);
     // iterate
     ALLOC(u, int8_t, GT);
     ALLOC(p, double, GT);
@@ -304,16 +470,21 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ALLOC(part_bus, double, (size_t)d.nblk_bus * NPART);
     ALLOC(part_ubar, double, (size_t)d.nblk_ubar * NPART);
     ALLOC(part_rows, double, (size_t)d.nblk_rows * NPART);
-    ALLOC(tauh, double, NBROW * LT);
+    ALLOC(tauh, double, (size_t)NBROW * (L + P.Lp) * T);
     ALLOC(bmu, double, 4 * BT);
     ALLOC(cnt, unsigned long long, 4);
     ALLOC(alq, int, LT);
     ALLOC(alq_cnt, unsigned, 2);
+    ALLOC(rec, double, NREC);
+    ALLOC(xsend1, double, (size_t)P.max_cut * 4 * T);
+    ALLOC(xrecv1, double, (size_t)nranks * P.max_cut * 4 * T);
+    ALLOC(xsend2, double, (size_t)P.max_export * 6 * T);
+    ALLOC(xrecv2, double, (size_t)nranks * P.max_export * 6 * T);
     ALLOC(st, DevStatus, 1);
     int8_t *uinit = nullptr;
-    if (uc->u_init) {
+    if (!P.uinit.empty()) {
         uinit = dnew<int8_t>(ctx, GT, e);
-        if (e != cudaSuccess || up<int8_t>(ctx, uinit, uc->u_init, GT) != cudaSuccess)
+        if (e != cudaSuccess || up<int8_t>(ctx, uinit, P.uinit.data(), GT) != cudaSuccess)
             return bail(fail(ctx, UCAC_ECUDA, "u_init upload"));
     }
     // status: beta = beta0, k = 1 (R21)
@@ -329,20 +500,26 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init kernel: %s", cudaGetErrorString(e)));
     e = cudaStreamSynchronize(ctx->s);
     if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init: %s", cudaGetErrorString(e)));
-    ucac_status gs = build_graphs(ctx);
-    if (gs != UCAC_OK) return bail(gs);
+    if (!(nranks > 1 && ctx->comm_mode == 1)) {
+        ucac_status gs = build_graphs(ctx);
+        if (gs != UCAC_OK) return bail(gs);
+    }
     *out = ctx;
     return UCAC_OK;
 #undef ALLOC
 #undef UPLOAD
 }
 
+// ------------------------------------------------------------------------------------------
 // one inner iteration.  Dependency order (also the order of the eager, timed path):
 //   (7a) k_gen -> (7b) k_genx, k_branch, k_branch_al -> (7d) k_bus, k_rows -> (7c) k_ubar -> S8/S9.
 // In the graph the generator chain k_gen -> k_genx -> k_ubar (which never reads a branch
 // result) runs on a second stream, forked AFTER the register-bound fast-path branch kernel
 // (sharing the SMs with it halves its occupancy) and overlapping the latency-bound thermal
-// AL tail; the bus solve joins both chains.
+// AL tail; the bus solve joins both chains.  Several ranks add the halo exchange: the cut
+// ends' tauhat before the bus solve, the bus results before the row update, the reduction
+// record before the inner/outer decision.
+// ------------------------------------------------------------------------------------------
 static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BRANCH_AL, K_BUS, K_ROWS, K_UBAR, K_REDUCE};
 
 static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
@@ -359,6 +536,8 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
 }
 
 static void enqueue_iteration(ucac_ctx *ctx) {
+    const Dev &d = ctx->d;
+    const bool multi = ctx->nranks > 1;
     launch_kernel(ctx, K_BRANCH, ctx->s);
     cudaEventRecord(ctx->ev_fork, ctx->s);
     cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
@@ -367,10 +546,29 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     launch_kernel(ctx, K_UBAR, ctx->s2);
     cudaEventRecord(ctx->ev_join, ctx->s2);
     launch_kernel(ctx, K_BRANCH_AL, ctx->s);
+    if (multi && d.max_cut > 0) {
+        launch_pack_tau(d, ctx->s);
+        ncclAllGather(d.xsend1, d.xrecv1, (size_t)d.max_cut * 4 * d.T, ncclDouble, ctx->comm, ctx->s);
+        launch_unpack_tau(d, ctx->s);
+    }
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
     launch_kernel(ctx, K_BUS, ctx->s);
+    if (multi && d.max_export > 0) {
+        launch_pack_bus(d, ctx->s);
+        ncclAllGather(d.xsend2, d.xrecv2, (size_t)d.max_export * 6 * d.T, ncclDouble, ctx->comm, ctx->s);
+        launch_unpack_bus(d, ctx->s);
+    }
     launch_kernel(ctx, K_ROWS, ctx->s);
-    launch_kernel(ctx, K_REDUCE, ctx->s);
+    if (multi) {
+        launch_reduce_part(d, ctx->s);
+        ncclGroupStart();
+        ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, ctx->s);
+        ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, ctx->s);
+        ncclGroupEnd();
+        launch_finalize(d, ctx->s);
+    } else {
+        launch_kernel(ctx, K_REDUCE, ctx->s);
+    }
 }
 
 static ucac_status build_graphs(ucac_ctx *ctx) {
@@ -412,6 +610,8 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
                                     int32_t *n_done) {
     if (!ctx) return UCAC_EINVAL;
     if (n < 0) return fail(ctx, UCAC_EINVAL, "n < 0");
+    if (ctx->nranks > 1 && ctx->comm_mode == 1)
+        return fail(ctx, UCAC_ESTATE, "loopback-group contexts iterate through ucac_iterate_group");
     long long before = 0;
     if (n_done) {
         ucac_status s = pull_status(ctx);
@@ -434,12 +634,94 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
     return UCAC_OK;
 }
 
+// In-process loopback group: the partition contexts of one problem (comm_mode 1, same device)
+// step through the same phases as the NCCL graph; the exchanges are device-to-device copies
+// driven from the host between phases (no kernel ever waits on another context).
+extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t iters) {
+    if (!ctxs || n < 1 || iters < 0) return UCAC_EINVAL;
+    for (int r = 0; r < n; r++)
+        if (!ctxs[r] || ctxs[r]->nranks != n || ctxs[r]->rank != r || (n > 1 && ctxs[r]->comm_mode != 1))
+            return fail(ctxs[r], UCAC_EINVAL, "group: context %d is not rank %d of a %d-rank loopback group", r, r, n);
+    ucac_ctx *ctx = ctxs[0];
+    auto sync_all = [&]() -> cudaError_t {
+        for (int r = 0; r < n; r++) {
+            cudaError_t e = cudaStreamSynchronize(ctxs[r]->s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    for (int r = 0; r < n; r++) {
+        ucac_status s = set_control(ctxs[r], 0, 0.0);
+        if (s != UCAC_OK) return s;
+    }
+    for (int it = 0; it < iters; it++) {
+        for (int r = 0; r < n; r++) {
+            ucac_ctx *c = ctxs[r];
+            const int ph1[] = {K_BRANCH, K_GEN, K_GENX, K_UBAR, K_BRANCH_AL};
+            for (int k : ph1) launch_kernel(c, k, c->s);
+            if (c->d.max_cut > 0) launch_pack_tau(c->d, c->s);
+        }
+        CK(sync_all());
+        for (int r = 0; r < n; r++)
+            for (int q = 0; q < n; q++) {
+                const Dev &dr = ctxs[r]->d, &dq = ctxs[q]->d;
+                const size_t blk = (size_t)dr.max_cut * 4 * dr.T;
+                if (dq.ncut > 0)
+                    CK(cudaMemcpyAsync(dr.xrecv1 + q * blk, dq.xsend1, (size_t)dq.ncut * 4 * dq.T * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, ctxs[r]->s));
+            }
+        CK(sync_all());
+        for (int r = 0; r < n; r++) {
+            ucac_ctx *c = ctxs[r];
+            if (c->d.max_cut > 0) launch_unpack_tau(c->d, c->s);
+            launch_kernel(c, K_BUS, c->s);
+            if (c->d.max_export > 0) launch_pack_bus(c->d, c->s);
+        }
+        CK(sync_all());
+        for (int r = 0; r < n; r++)
+            for (int q = 0; q < n; q++) {
+                const Dev &dr = ctxs[r]->d, &dq = ctxs[q]->d;
+                const size_t blk = (size_t)dr.max_export * 6 * dr.T;
+                if (dq.nexport > 0)
+                    CK(cudaMemcpyAsync(dr.xrecv2 + q * blk, dq.xsend2, (size_t)dq.nexport * 6 * dq.T * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, ctxs[r]->s));
+            }
+        CK(sync_all());
+        for (int r = 0; r < n; r++) {
+            ucac_ctx *c = ctxs[r];
+            if (c->d.max_export > 0) launch_unpack_bus(c->d, c->s);
+            launch_kernel(c, K_ROWS, c->s);
+            if (n > 1) launch_reduce_part(c->d, c->s);
+            else launch_kernel(c, K_REDUCE, c->s);
+        }
+        CK(sync_all());
+        if (n > 1) {
+            std::vector<double> all((size_t)n * NREC), red(NREC, 0.0);
+            for (int r = 0; r < n; r++)
+                CK(cudaMemcpy(all.data() + (size_t)r * NREC, ctxs[r]->d.rec, NREC * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int c = 0; c < NREC; c++) {
+                double v = all[c];
+                for (int r = 1; r < n; r++) v = c < NREC_SUM ? v + all[(size_t)r * NREC + c] : std::max(v, all[(size_t)r * NREC + c]);
+                red[c] = v;
+            }
+            for (int r = 0; r < n; r++) {
+                CK(cudaMemcpy(ctxs[r]->d.rec, red.data(), NREC * sizeof(double), cudaMemcpyHostToDevice));
+                launch_finalize(ctxs[r]->d, ctxs[r]->s);
+            }
+            CK(sync_all());
+        }
+    }
+    CK(cudaGetLastError());
+    return UCAC_OK;
+}
+
 static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows",
                                     "k_genx"};
 extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
 
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
     if (!ctx || n < 0) return UCAC_EINVAL;
+    if (ctx->nranks > 1) return fail(ctx, UCAC_EUNSUPPORTED, "timed iterations are single-GPU");
     ucac_status s = set_control(ctx, 0, 0.0);
     if (s != UCAC_OK) return s;
     const size_t need = (size_t)n * NKERN * 2;
@@ -501,6 +783,7 @@ extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
 
 template <class Tp>
 static cudaError_t down(ucac_ctx *ctx, Tp *dst, const Tp *src, size_t n) {
+    if (n == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, n * sizeof(Tp), cudaMemcpyDeviceToHost, ctx->s);
 }
 
@@ -522,6 +805,7 @@ static ucac_status aos_to_soa(ucac_ctx *ctx, double *dev, const double *host, si
     return UCAC_OK;
 }
 
+// State of the (rank-local) problem: generators, local branches and OWNED buses.
 extern "C" ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st) {
     if (!ctx || !st) return UCAC_EINVAL;
     launch_apply_outer(ctx->d, ctx->s);
@@ -563,6 +847,7 @@ extern "C" ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st) {
 
 extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     if (!ctx || !st) return UCAC_EINVAL;
+    if (ctx->nranks > 1) return fail(ctx, UCAC_EUNSUPPORTED, "set_state is single-GPU (ghost buses would be stale)");
     const Dev &d = ctx->d;
     const size_t GT = (size_t)ctx->G * ctx->T, LT = (size_t)ctx->L * ctx->T, BT = (size_t)ctx->B * ctx->T;
     CK(cudaStreamSynchronize(ctx->s));
@@ -620,6 +905,14 @@ extern "C" ucac_status ucac_get_solution(ucac_ctx *ctx, ucac_solution *sol) {
         if (s != UCAC_OK) return s;
     }
     CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids, int32_t *count) {
+    if (!ctx || !count || which < 0 || which > 2) return UCAC_EINVAL;
+    const std::vector<int> &v = which == 0 ? ctx->P.gen_global : (which == 1 ? ctx->P.branch_global : ctx->P.bus_global);
+    *count = (int32_t)v.size();
+    if (ids) std::copy(v.begin(), v.end(), ids);
     return UCAC_OK;
 }
 
@@ -689,14 +982,10 @@ extern "C" ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz) {
     // Algorithmic bytes: every array element a kernel must read or write once.
     // k_branch: read fbar(4) z(8) y(8) x(4) al(3) + wbar/thbar of both ends (4); write x(4) f(4) al(3) tauhat(8)
     sz->alg_bytes[K_BRANCH] = LT * 46 * 8 + L * (9 * 8 + 2 * 4);
-    // k_gen: read ubar(3) pbar qbar z,y of 12 rows (24) ; write p q ph (3) + u (1 B)
     // k_gen (DP): read ubar, z, y of the 3 duplicate rows (9); write u (1 B)
     sz->alg_bytes[K_GEN] = GT * (9 * 8 + 1);
     // k_genx: read ubar(3) pbar qbar (2) z,y of 9 rows (18); write p q ph (3)
     sz->alg_bytes[K_GENX] = GT * 26 * 8 + G * 24 * 8;
-    // k_bus: per gen-period: read p q ph z,y,lambda of GP GQ RC (9) pbar qbar (2), write pbar qbar z y (8)
-    //        per branch end-period: read f(2) x(2) z,y,lambda(12) fbar(2), write fbar(2) z,y(8)
-    //        per bus-period: read pd qd wbar thbar, write wbar thbar
     // k_bus: per gen-period read p q ph z,y,lambda of GP GQ RC (9) pbar qbar (2), write pbar qbar z y (8);
     //        per end-period read tauhat (4); per bus-period read pd qd wbar thbar, write wbar thbar + 4 bmu
     sz->alg_bytes[K_BUS] = GT * 19 * 8 + 2 * LT * 4 * 8 + BT * 10 * 8;
@@ -727,6 +1016,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
         if (g) cudaGraphExecDestroy(g);
     for (auto ev : ctx->tev) cudaEventDestroy(ev);
     for (void *p : ctx->dalloc) cudaFree(p);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);

@@ -22,6 +22,8 @@ enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, K_
 // per-block reduction record (S8): max |r|, max |r+z|, sum (r+z)^2, max |z|, sum z^2,
 // max rho |dxbar|, objective, non-finite flag
 enum Part { P_PINF = 0, P_RZINF, P_RZ2, P_ZINF, P_Z2, P_DINF, P_OBJ, P_BAD, NPART };
+// cross-rank reduction record: 7 sums (RZ2, Z2, OBJ, 4 TRON counters) then 5 maxes
+enum Rec { R_RZ2 = 0, R_Z2, R_OBJ, R_C0, R_C1, R_C2, R_C3, NREC_SUM, R_PINF = NREC_SUM, R_RZINF, R_ZINF, R_DINF, R_BAD, NREC };
 
 struct DevStatus {
     double beta;          // current beta^k
@@ -83,7 +85,14 @@ struct Dev {
     double *part_bus;                 // [nblk_bus][NPART]
     double *part_ubar;                // [nblk_ubar][NPART]
     unsigned long long *cnt;          // [4] per-iteration TRON counters (zeroed by reduce)
-    double *tauh;                     // [8][L*T] bus-side targets x + z + y/rho of the branch rows
+    // ---- multi-rank; single GPU: B_own = B, Lph = 0, nothing to exchange
+    int B_own;                        // owned buses [0, B_own); ghosts [B_own, B)
+    int Lph;                          // phantom branches [L, L + Lph) (tauhat only)
+    int ncut, nexport, nphantom_src, nghost, max_cut, max_export, nranks;
+    const int *cut_local, *export_local, *phantom_src, *ghost_src;
+    double *xsend1, *xrecv1, *xsend2, *xrecv2;   // halo exchange buffers
+    double *rec;                      // [NREC] local reduction record (sums then maxes)
+    double *tauh;                     // [8][(L+Lph)*T] bus-side targets x + z + y/rho of the branch rows
     double *bmu;                      // [4][B*T] muP, muQ, wbar - wbar_old, thbar - thbar_old
     double *part_rows;                // [nblk_rows][NPART]
     int *alq;                         // [L*T] queue of thermal-active solves (phase 2)
@@ -104,6 +113,13 @@ void launch_genx(const Dev &d, cudaStream_t s);
 void launch_bus(const Dev &d, cudaStream_t s);
 void launch_rows(const Dev &d, cudaStream_t s);
 int nblk_rows(int L, int T);
+// multi-rank
+void launch_reduce_part(const Dev &d, cudaStream_t s);
+void launch_finalize(const Dev &d, cudaStream_t s);
+void launch_pack_tau(const Dev &d, cudaStream_t s);
+void launch_unpack_tau(const Dev &d, cudaStream_t s);
+void launch_pack_bus(const Dev &d, cudaStream_t s);
+void launch_unpack_bus(const Dev &d, cudaStream_t s);
 void launch_ubar(const Dev &d, cudaStream_t s);
 void launch_reduce(const Dev &d, cudaStream_t s);
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s);

@@ -61,6 +61,11 @@ class Params(C.Structure):
                 ("al_sigma_decay", C.c_double)]
 
 
+class Dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("comm_mode", C.c_int32),
+                ("nccl_id", C.c_ubyte * 128), ("bus_part", ip), ("bus_xy", dp)]
+
+
 class Report(C.Structure):
     _fields_ = [("primal_inf", C.c_double), ("rz_inf", C.c_double), ("rz_2", C.c_double),
                 ("z_inf", C.c_double), ("z_2", C.c_double), ("dual_inf", C.c_double),
@@ -144,11 +149,22 @@ def _declare(L):
     L.ucac_last_error.restype = C.c_char_p
     L.ucac_destroy.argtypes = [C.c_void_p]
     L.ucac_destroy.restype = None
+    L.ucac_partition.argtypes = [C.c_int32, C.c_int32, ip, ip, dp, C.c_int32, ip]
+    L.ucac_partition.restype = C.c_int
+    L.ucac_halo_lists.argtypes = [C.c_int32, C.c_int32, ip, ip, ip, C.c_int32, C.c_int32, ip, ip, ip, ip, ip, ip, ip]
+    L.ucac_halo_lists.restype = C.c_int
+    L.ucac_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte)]
+    L.ucac_nccl_unique_id.restype = C.c_int
+    L.ucac_iterate_group.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_int32]
+    L.ucac_iterate_group.restype = C.c_int
+    L.ucac_local_map.argtypes = [C.c_void_p, C.c_int32, ip, ip]
+    L.ucac_local_map.restype = C.c_int
 
 
 EXPORTED = ["ucac_create", "ucac_iterate", "ucac_iterate_timed", "ucac_kernel_name", "ucac_residuals",
             "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
-            "ucac_stream", "ucac_last_error", "ucac_destroy"]
+            "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
+            "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map"]
 
 
 def _check(rc, h=None):
@@ -167,7 +183,9 @@ def params_struct(pr) -> Params:
 class Context:
     """One ADMM context on the current CUDA device (ucac_create .. ucac_destroy)."""
 
-    def __init__(self, pb, pr, stream: int = 0):
+    def __init__(self, pb, pr, stream: int = 0, dist: dict | None = None):
+        """dist: None (one GPU) or {"rank", "nranks", "comm_mode" (0 NCCL / 1 loopback group),
+        "nccl_id" (bytes, mode 0), "bus_part" (optional), "bus_xy" (optional)}"""
         self.L = lib()
         pb = pb.normalized()
         self.pb, self.pr = pb, pr
@@ -186,11 +204,33 @@ class Context:
         uc = Uc(a(pb.ramp_up), a(pb.ramp_dn), a(pb.su_ramp), a(pb.sd_ramp), a(pb.min_up, ip), a(pb.min_dn, ip),
                 a(pb.u0, ip), a(pb.hold, ip), a(pb.p0), ui)
         prm = params_struct(pr)
+        dist_c = None
+        if dist is not None:
+            dist_c = Dist()
+            dist_c.rank, dist_c.nranks, dist_c.comm_mode = dist["rank"], dist["nranks"], dist.get("comm_mode", 0)
+            if dist.get("nccl_id") is not None:
+                dist_c.nccl_id[:] = list(bytes(dist["nccl_id"]))
+            dist_c.bus_part = a(np.asarray(dist["bus_part"], dtype=np.int32), ip) if dist.get("bus_part") is not None else None
+            xy = dist.get("bus_xy", pb.bus_xy)
+            dist_c.bus_xy = a(np.asarray(xy, dtype=np.float64).reshape(-1)) if xy is not None else None
         h = C.c_void_p()
-        rc = self.L.ucac_create(C.byref(net), C.byref(hz), C.byref(co), C.byref(uc), C.byref(prm), None,
+        rc = self.L.ucac_create(C.byref(net), C.byref(hz), C.byref(co), C.byref(uc), C.byref(prm),
+                                C.byref(dist_c) if dist_c is not None else None,
                                 C.c_void_p(stream) if stream else None, C.byref(h))
         _check(rc, None)
         self.h = h
+        self.dist = dist
+        self._local = {}
+        for which, name in ((0, "gen"), (1, "branch"), (2, "bus")):
+            cnt = C.c_int32(0)
+            _check(self.L.ucac_local_map(self.h, which, None, C.byref(cnt)), self.h)
+            ids = np.zeros(cnt.value, dtype=np.int32)
+            _check(self.L.ucac_local_map(self.h, which, ids.ctypes.data_as(ip), C.byref(cnt)), self.h)
+            self._local[name] = ids
+
+    def local_ids(self, which: str) -> np.ndarray:
+        """global ids of the local generators / branches / owned buses (state layout order)"""
+        return self._local[which]
 
     def close(self):
         if getattr(self, "h", None):
@@ -228,7 +268,8 @@ class Context:
 
     def solution(self) -> dict:
         pb = self.pb
-        GT, LT, BT = pb.ngen * pb.T, pb.nbranch * pb.T, pb.nbus * pb.T
+        GT, LT, BT = (len(self._local["gen"]) * pb.T, len(self._local["branch"]) * pb.T,
+                      len(self._local["bus"]) * pb.T)
         out = {"u_on": np.zeros(GT, np.int8), "p": np.zeros(GT), "q": np.zeros(GT), "wbar": np.zeros(BT),
                "thetabar": np.zeros(BT), "flows": np.zeros(4 * LT)}
         s = Solution(out["u_on"].ctypes.data_as(i8p), *[out[k].ctypes.data_as(dp) for k in
@@ -238,7 +279,8 @@ class Context:
 
     def _sizes(self):
         pb = self.pb
-        GT, LT, BT = pb.ngen * pb.T, pb.nbranch * pb.T, pb.nbus * pb.T
+        GT, LT, BT = (len(self._local["gen"]) * pb.T, len(self._local["branch"]) * pb.T,
+                      len(self._local["bus"]) * pb.T)
         return {"GT": GT, "12GT": 12 * GT, "4LT": 4 * LT, "3LT": 3 * LT, "8LT": 8 * LT, "BT": BT, "8": 8}
 
     def get_state(self) -> dict:
@@ -283,3 +325,71 @@ def dp_batch_device(G, T, L_ptr, tu_ptr, td_ptr, u0_ptr, hold_ptr, sched_ptr, co
     rc = lib().ucac_dp_batch(G, T, L_ptr, tu_ptr, td_ptr, u0_ptr, hold_ptr, sched_ptr, cost_ptr, 1,
                              C.c_void_p(stream) if stream else None)
     _check(rc, None)
+
+
+def partition(pb, nparts: int, use_xy: bool = True) -> np.ndarray:
+    """bus -> rank (ucac_partition: weighted RCB on the bus coordinates, or BFS chunks)"""
+    pb = pb.normalized()
+    part = np.zeros(pb.nbus, dtype=np.int32)
+    xy = np.ascontiguousarray(pb.bus_xy, dtype=np.float64).reshape(-1) if (use_xy and pb.bus_xy is not None) else None
+    rc = lib().ucac_partition(pb.nbus, pb.nbranch, pb.br_from.ctypes.data_as(ip), pb.br_to.ctypes.data_as(ip),
+                              xy.ctypes.data_as(dp) if xy is not None else None, nparts, part.ctypes.data_as(ip))
+    _check(rc, None)
+    return part
+
+
+def halo_lists(pb, part, rank: int) -> dict:
+    """ucac_halo_lists: the rank-local components and halo (global ids)"""
+    pb = pb.normalized()
+    part = np.ascontiguousarray(part, dtype=np.int32)
+    nparts = int(part.max()) + 1
+    sizes = np.zeros(6, dtype=np.int32)
+    args = [pb.nbus, pb.nbranch, pb.br_from.ctypes.data_as(ip), pb.br_to.ctypes.data_as(ip), part.ctypes.data_as(ip),
+            nparts, rank, sizes.ctypes.data_as(ip)]
+    _check(lib().ucac_halo_lists(*args, None, None, None, None, None, None), None)
+    names = ["own_bus", "ghost_bus", "local_branch", "phantom", "cut_branch", "export_bus"]
+    out = {n: np.zeros(int(s), dtype=np.int32) for n, s in zip(names, sizes)}
+    _check(lib().ucac_halo_lists(*args, *[out[n].ctypes.data_as(ip) for n in names]), None)
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(lib().ucac_nccl_unique_id(buf), None)
+    return bytes(buf)
+
+
+def iterate_group(ctxs, iters: int):
+    """ucac_iterate_group over comm_mode-1 contexts (rank order)"""
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    _check(lib().ucac_iterate_group(arr, len(ctxs), iters), ctxs[0].h)
+
+
+def assemble_state(pb, ctxs) -> dict:
+    """global canonical state from the local states of a partition group"""
+    pb = pb.normalized()
+    T, G, L, B = pb.T, pb.ngen, pb.nbranch, pb.nbus
+    out = {n: np.zeros({"GT": G * T, "12GT": 12 * G * T, "4LT": 4 * L * T, "3LT": 3 * L * T, "8LT": 8 * L * T,
+                        "BT": B * T, "8": 8}[s], dtype=t) for n, t, s in STATE_FIELDS}
+    for c in ctxs:
+        st = c.get_state()
+        g, l, b = c.local_ids("gen"), c.local_ids("branch"), c.local_ids("bus")
+        gi = (g[:, None] * T + np.arange(T)).reshape(-1)
+        li = (l[:, None] * T + np.arange(T)).reshape(-1)
+        bi = (b[:, None] * T + np.arange(T)).reshape(-1)
+        for n, t, s in STATE_FIELDS:
+            v = st[n]
+            if s == "GT":
+                out[n][gi] = v
+            elif s == "12GT":
+                out[n].reshape(12, -1)[:, gi] = v.reshape(12, -1)
+            elif s == "8LT":
+                out[n].reshape(8, -1)[:, li] = v.reshape(8, -1)
+            elif s in ("4LT", "3LT"):
+                k = 4 if s == "4LT" else 3
+                out[n].reshape(-1, k)[li] = v.reshape(-1, k)
+            elif s == "BT":
+                out[n][bi] = v
+            else:
+                out[n] = v
+    return out

@@ -39,7 +39,8 @@ def test_struct_layouts_match_header(tmp_path):
     import ctypes as C
     structs = {"ucac_network": ucac.Network, "ucac_horizon": ucac.Horizon, "ucac_costs": ucac.Costs,
                "ucac_uc": ucac.Uc, "ucac_params": ucac.Params, "ucac_report": ucac.Report,
-               "ucac_solution": ucac.Solution, "ucac_state": ucac.State, "ucac_sizes": ucac.Sizes}
+               "ucac_solution": ucac.Solution, "ucac_state": ucac.State, "ucac_sizes": ucac.Sizes,
+               "ucac_dist": ucac.Dist}
     src = ['#include <stdio.h>', '#include <stddef.h>', '#include "ucac.h"', "int main(void){"]
     for cname, py in structs.items():
         src.append(f'printf("{cname} %zu\\n", sizeof({cname}));')

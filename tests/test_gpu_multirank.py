@@ -1,0 +1,49 @@
+"""Multi-rank path on one GPU: a comm_mode-1 loopback group of P partition contexts runs the
+same phases and halo exchanges as the NCCL graph.  Every component is computed
+by exactly the kernel that computes it on one GPU, and the bus sums run in the same canonical
+order, so the assembled iterate must equal the single-GPU iterate BIT FOR BIT (only the
+global 2-norm sums differ in summation order; they feed the outer-update test, which flips
+only at exact ties)."""
+import numpy as np
+import pytest
+
+from paper_2310_13145_b200 import inputs, ucac
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,P,iters", [("case30", 2, 30), ("case118", 3, 25), ("case300", 4, 20),
+                                          ("pegase2869", 8, 6)])
+def test_loopback_group_bitwise_equals_single_gpu(name, P, iters):
+    pb, pr = inputs.build_config(name)
+    one = ucac.Context(pb, pr)
+    one.iterate(iters)
+    ref = one.get_state()
+    part = ucac.partition(pb, P)
+    ctxs = [ucac.Context(pb, pr, dist={"rank": r, "nranks": P, "comm_mode": 1, "bus_part": part}) for r in range(P)]
+    ucac.iterate_group(ctxs, iters)
+    got = ucac.assemble_state(pb, ctxs)
+    for k in ref:
+        if k == "scal":
+            assert np.array_equal(got[k][[0, 2, 3, 4]], ref[k][[0, 2, 3, 4]]), (k, got[k], ref[k])
+            continue
+        assert np.array_equal(got[k], ref[k]), (name, P, k, np.max(np.abs(got[k].astype(float) - ref[k])))
+    r1 = one.report()
+    for c in ctxs:
+        rp = c.report()
+        assert rp["primal_inf"] == r1["primal_inf"] and rp["inner_total"] == iters
+        assert rp["objective"] == pytest.approx(r1["objective"], rel=1e-12)
+    # each rank holds only its part
+    assert sum(len(c.local_ids("bus")) for c in ctxs) == pb.nbus
+    assert sum(len(c.local_ids("branch")) for c in ctxs) == pb.nbranch
+
+
+def test_group_rejects_mismatched_contexts():
+    pb, pr = inputs.build_config("case30")
+    part = ucac.partition(pb, 2)
+    a = ucac.Context(pb, pr, dist={"rank": 0, "nranks": 2, "comm_mode": 1, "bus_part": part})
+    b = ucac.Context(pb, pr, dist={"rank": 1, "nranks": 2, "comm_mode": 1, "bus_part": part})
+    with pytest.raises(ucac.UcacError):
+        ucac.iterate_group([b, a], 1)
+    with pytest.raises(ucac.UcacError):
+        a.iterate(1)   # loopback contexts iterate as a group
