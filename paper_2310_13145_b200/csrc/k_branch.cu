@@ -461,12 +461,13 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
 // the same value the oracle forms.
 __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x, double f0, double f1,
                                             double f2, double f3) {
-    const size_t LTs = (size_t)(d.L + d.Lph) * d.T;   // tauhat kind stride includes phantom branches
+    const size_t LTs = (size_t)d.L * d.T;                // row-state kind stride
+    const size_t LTH = (size_t)(d.L + d.Lph) * d.T;      // tauhat kind stride includes phantom branches
     const double xs[8] = {f0, f1, f2, f3, x[0], x[1], x[2], x[3]};
 #pragma unroll
     for (int r = 0; r < 8; r++) {
         const double rho = r < 4 ? d.rpq : d.rva;
-        d.tauh[r * LTs + k] = xs[r] + d.zb[r * LTs + k] + d.yb[r * LTs + k] / rho;
+        d.tauh[r * LTH + k] = xs[r] + d.zb[r * LTs + k] + d.yb[r * LTs + k] / rho;
     }
 }
 
