@@ -308,6 +308,8 @@ def main():
             "branch_solves_per_s": v * pb.nbranch * pb.T,
             "newton_iters_per_s": newton / (tot_ms * 1e-3),
             "newton_per_solve": newton / max(1, args.steps * pb.nbranch * pb.T),
+            "branch_stats_per_step": {k: (rep1[k] - rep0[k]) / args.steps
+                                      for k in ("tron_capped", "al_active", "al_capped")},
             "primal_inf": rep1["primal_inf"],
             "roofline": roofline,
             "sweep_kernels": sweep,

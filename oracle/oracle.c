@@ -5,7 +5,7 @@
  * TEST INFRASTRUCTURE ONLY (see oracle.h).  Single threaded, fp64, plain loops in the
  * paper's order; compiled with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
  * It shares no code with the CUDA path.  Where the paper is silent the reading taken is
- * the one registered in DESIGN.md section 3 ("R1".."R33", mirroring SURVEY.md c.4).
+ * the one registered in DESIGN.md section 3 ("R1".."R42", mirroring SURVEY.md c.4).
  *
  * Parity pins (tests/test_oracle_*.py) check every function here against something
  * other than itself: brute force over Eq. (3) schedules, exact active-set enumeration
@@ -707,6 +707,94 @@ static void br_eval(void *vc, const double *X, double *fo, double *g, double *H)
     *fo = F;
 }
 
+/* Second-order multiplier update of the method of multipliers (R42).  Near the round's
+ * minimiser X(mu) of the AL Phi on the box, with the active bounds fixed, the constraint values
+ * move as dh/dmu = -M, M = J_F H_FF^{-1} J_F' (J = dh/dX, H = Hessian of Phi, F = the
+ * variables strictly inside their bounds), so the Newton step on h(mu) = 0 is dmu = M^{-1} h.
+ * For sigma -> inf, M -> I/sigma and this is the first-order update dmu = sigma h.
+ * Returns 0 (caller keeps the first-order update) if H_FF or M is not positive definite. */
+#define AL_NEWTON_C 10.0
+static int al_newton_dmu(bctx *c, const double *X, const double *lo, const double *hi,
+                         const double *h, double *dmu) {
+    double F, g[6], H[36], f[4], Jf[16];
+    br_eval(c, X, &F, g, H);
+    orc_branch_flows(c->y, X, f, Jf, NULL);
+    /* J rows: dh_m/dX = 2 (P_m dP_m/dx + Q_m dQ_m/dx) / rbar^2, and 1 for the slack s_m */
+    double J[2][6];
+    for (int m = 0; m < 2; m++) {
+        int kp = 2 * m, kq = 2 * m + 1;
+        for (int a = 0; a < 4; a++) J[m][a] = 2.0 * (f[kp] * Jf[kp * 4 + a] + f[kq] * Jf[kq * 4 + a]) / c->r2;
+        J[m][4] = m == 0 ? 1.0 : 0.0;
+        J[m][5] = m == 1 ? 1.0 : 0.0;
+    }
+    int idx[6], nf = 0;
+    for (int i = 0; i < 6; i++)
+        if (X[i] > lo[i] && X[i] < hi[i]) idx[nf++] = i;
+    /* Cholesky H_FF = L L' (textbook, column by column) */
+    double L[36];
+    for (int j = 0; j < nf; j++) {
+        double d = H[idx[j] * 6 + idx[j]];
+        for (int k = 0; k < j; k++) d = d - L[j * 6 + k] * L[j * 6 + k];
+        if (!(d > 0.0)) return 0;
+        L[j * 6 + j] = sqrt(d);
+        for (int i = j + 1; i < nf; i++) {
+            double v = H[idx[i] * 6 + idx[j]];
+            for (int k = 0; k < j; k++) v = v - L[i * 6 + k] * L[j * 6 + k];
+            L[i * 6 + j] = v / L[j * 6 + j];
+        }
+    }
+    /* V_m = H_FF^{-1} J_m,F by forward and back substitution; M_mn = J_m,F . V_n */
+    double V[2][6];
+    for (int m = 0; m < 2; m++) {
+        double z[6];
+        for (int i = 0; i < nf; i++) {
+            double v = J[m][idx[i]];
+            for (int k = 0; k < i; k++) v = v - L[i * 6 + k] * z[k];
+            z[i] = v / L[i * 6 + i];
+        }
+        for (int i = nf - 1; i >= 0; i--) {
+            double v = z[i];
+            for (int k = i + 1; k < nf; k++) v = v - L[k * 6 + i] * V[m][k];
+            V[m][i] = v / L[i * 6 + i];
+        }
+    }
+    double M[2][2];
+    for (int m = 0; m < 2; m++)
+        for (int n = 0; n < 2; n++) {
+            double v = 0.0;
+            for (int i = 0; i < nf; i++) v = v + J[m][idx[i]] * V[n][i];
+            M[m][n] = v;
+        }
+    /* Spectral safeguard: in each eigen-direction v of M (eigenvalue lam in (0, 1/sigma]) take
+     * the Newton factor 1/lam where lam >= 1/(C sigma), and the first-order factor sigma where M
+     * is nearly singular (both ends of a near-lossless line binding: their multipliers are not
+     * separately determined, and 1/lam would amplify rounding along that direction). */
+    double a = M[0][0], b = 0.5 * (M[0][1] + M[1][0]), d = M[1][1];
+    double mean = 0.5 * (a + d), half = 0.5 * (a - d);
+    double r = sqrt(half * half + b * b);
+    double lam[2] = {mean + r, mean - r};
+    double v[2][2];
+    if (r == 0.0) {
+        v[0][0] = 1.0; v[0][1] = 0.0;
+    } else if (a >= d) {
+        double n = sqrt((lam[0] - d) * (lam[0] - d) + b * b);
+        v[0][0] = (lam[0] - d) / n; v[0][1] = b / n;
+    } else {
+        double n = sqrt(b * b + (lam[0] - a) * (lam[0] - a));
+        v[0][0] = b / n; v[0][1] = (lam[0] - a) / n;
+    }
+    v[1][0] = -v[0][1]; v[1][1] = v[0][0];
+    dmu[0] = 0.0;
+    dmu[1] = 0.0;
+    for (int e = 0; e < 2; e++) {
+        double fac = lam[e] >= 1.0 / (AL_NEWTON_C * c->sig) ? 1.0 / lam[e] : c->sig;
+        double ph = v[e][0] * h[0] + v[e][1] * h[1];
+        dmu[0] = dmu[0] + fac * ph * v[e][0];
+        dmu[1] = dmu[1] + fac * ph * v[e][1];
+    }
+    return 1;
+}
+
 /* One branch solve (R9/R10/R12): TRON on the 4-variable box; if the rate is
  * 0 (unlimited) or both ends satisfy Eq. 2c-2d, done (thermal multipliers 0).  Otherwise
  * method of multipliers on the 6-variable slack form, warm-starting (mu, sigma). */
@@ -746,8 +834,13 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
                 double h2 = (f[2] * f[2] + f[3] * f[3]) / c.r2 - 1.0 + X[5];
                 double hm = dmax(fabs(h1), fabs(h2));
                 if (hm <= pr->al_eta_star) break;
-                c.mu[0] = c.mu[0] + c.sig * h1;
-                c.mu[1] = c.mu[1] + c.sig * h2;
+                double hv[2] = {h1, h2}, dmu[2];
+                if (!al_newton_dmu(&c, X, lo, hi, hv, dmu)) {
+                    dmu[0] = c.sig * h1;
+                    dmu[1] = c.sig * h2;
+                }
+                c.mu[0] = c.mu[0] + dmu[0];
+                c.mu[1] = c.mu[1] + dmu[1];
                 if (hm > 0.25 * hprev) c.sig = dmin(10.0 * c.sig, smax);
                 hprev = hm;
             }

@@ -52,8 +52,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     headers = [os.path.join(CSRC, "ucac_dev.cuh"), os.path.join(CSRC, "ucac_part.h"), os.path.join(INCLUDE, "ucac.h")]
     objs = []
     jobs = []
+    # tuning A/B only: UCAC_SRC_OVERRIDE="k_branch.cu=/path/variant.cu" compiles another file for a unit
+    override = dict(kv.split("=", 1) for kv in os.environ.get("UCAC_SRC_OVERRIDE", "").split(",") if "=" in kv)
     for src, flags in UNITS.items():
-        s = os.path.join(CSRC, src)
+        s = override.get(src, os.path.join(CSRC, src))
         o = os.path.join(OUT, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers + [os.path.abspath(__file__)]):

@@ -210,3 +210,49 @@ def test_branch_binding_limit_grid_search():
         assert feas.any()
         Fg = F[feas].min()
         assert Fx <= Fg + 1e-6 * abs(Fg)
+
+
+def _lagrangian_grad(y, x, s, mu, tau, rpq, rva, r2):
+    """Gradient of F + sum_m mu_m h_m over (x, s) by torch autograd (fp64), h_m the normalised
+    Eq. 2c-2d constraint in slack form (R36)."""
+    xt = torch.tensor(np.concatenate([x, s]), dtype=torch.float64, requires_grad=True)
+    f = flows_torch(y, xt[:4])
+    tt = torch.tensor(tau, dtype=torch.float64)
+    F = 0.5 * rpq * torch.sum((f - tt[:4]) ** 2) + 0.5 * rva * torch.sum((xt[:4] - tt[4:]) ** 2)
+    h0 = (f[0] ** 2 + f[1] ** 2) / r2 - 1.0 + xt[4]
+    h1 = (f[2] ** 2 + f[3] ** 2) / r2 - 1.0 + xt[5]
+    Lg = F + float(mu[0]) * h0 + float(mu[1]) * h1
+    (g,) = torch.autograd.grad(Lg, xt)
+    return g.numpy(), np.array([h0.item(), h1.item()])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_branch_al_kkt_multipliers(seed):
+    """The returned (x, mu) is a KKT point of the thermally constrained branch problem
+    (Eq. 2c-2d): h ~ 0, mu >= 0 on a binding end, mu ~ 0 where the slack is interior, and the
+    Lagrangian gradient vanishes on the free variables (autograd, independent of the oracle's
+    derivative code and of its multiplier update rule).  Second-order multiplier steps (R42)
+    reach it in a few rounds (a first-order update needs about twice as many)."""
+    rng = np.random.default_rng(300 + seed)
+    y = inputs.branch_admittance(rng.uniform(0.005, 0.03), rng.uniform(0.05, 0.2), rng.uniform(0.0, 0.1))
+    rpq, rva = 5e3, 1e4
+    rate = 0.5 + 0.2 * rng.uniform()
+    xs = np.array([1.0, 0.98, 0.12, 0.0]) + rng.normal(size=4) * 0.01
+    tau = np.concatenate([flows_complex(y, xs) * (1.2 + 0.2 * rng.uniform()), xs])
+    lo, hi = np.array([0.81, 0.81]), np.array([1.21, 1.21])
+    x, al, f, st = oracle.branch_solve(y, lo, hi, rate, tau, rpq, rva, PR, xs.copy(), np.zeros(3))
+    assert st[2] == 1 and st[4] == 0
+    r2 = rate ** 2
+    s = np.clip(1.0 - np.array([f[0] ** 2 + f[1] ** 2, f[2] ** 2 + f[3] ** 2]) / r2, 0.0, 1.0)
+    g, h = _lagrangian_grad(y, x, s, al[:2], tau, rpq, rva, r2)
+    assert np.max(np.abs(h)) <= 1e-8
+    scale = rpq * np.max(np.abs(flows_complex(y, x))) ** 2
+    for i in range(4):
+        if lo[min(i, 1)] < x[i] < hi[min(i, 1)] or i >= 2:
+            assert abs(g[i]) <= 1e-6 * scale, (i, g)
+    for m in range(2):
+        if s[m] > 1e-6:
+            assert abs(al[m]) <= 1e-6 * scale
+        else:
+            assert al[m] >= -1e-6 * scale
+    assert st[3] <= 6 and st[0] <= 40, st

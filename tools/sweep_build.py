@@ -11,7 +11,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run(flags, steps=20):
-    env = dict(os.environ, UCAC_EXTRA_NVCC=flags)
+    # a variant is "nvcc flags" or "src:k_branch.cu=path [nvcc flags]" (compile another file for a unit)
+    src = ""
+    if flags.startswith("src:"):
+        src, _, flags = flags[4:].partition(" ")
+    env = dict(os.environ, UCAC_EXTRA_NVCC=flags, UCAC_SRC_OVERRIDE=src)
     subprocess.run([sys.executable, os.path.join(ROOT, "paper_2310_13145_b200", "build.py"), "--force"], env=env,
                    check=True, capture_output=True)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", str(steps), "--warmup", "5",
@@ -20,7 +24,7 @@ def run(flags, steps=20):
     if not line:
         return {"flags": flags, "error": out.stderr[-500:]}
     d = json.loads(line[-1])
-    return {"flags": flags, "value": round(d["value"], 1), "ms_step": round(d["ms_per_step"], 4),
+    return {"flags": (src + " " + flags).strip(), "value": round(d["value"], 1), "ms_step": round(d["ms_per_step"], 4),
             "kernels_ms": {k: round(v, 4) for k, v in d["kernel_ms_per_step"].items()},
             "newton_per_solve": round(d["newton_per_solve"], 3)}
 
