@@ -78,16 +78,43 @@ def test_dp_batch_bit_exact():
             assert c[g] == co
 
 
+FREE_RUN = 10
+
+
 def run_pair(pb, pr, iters, check_every=1):
+    """GPU vs oracle over `iters` inner iterations.
+
+    * every checked iteration, one-step parity: a fresh oracle started from the GPU's previous
+      state takes the same iteration; every field must agree to the tight tolerance;
+    * the first FREE_RUN iterations, free-running parity: both sides iterate on their own
+      state; every field must agree to the same tolerance;
+    * the whole run, free-running: the commitment schedule u and the outer-loop scalars must be
+      identical.
+    Past a few dozen iterations the free-running float fields are not compared element by
+    element: rounding-level differences (FMA contraction in the branch kernel) are amplified by
+    the ADMM map near activity switches of the generator closed form (measured 1e-10 -> 4e-8
+    relative in one iteration, decaying afterwards), which is a property of the iteration, not
+    an error of either side; the one-step check isolates the computation of each iteration."""
     gpu = ucac.Context(pb, pr)
     orc = oracle.Oracle(pb, pr)
     rho_max = max(pr.rho_pq, pr.rho_va, pr.rho_uc)
     compare(gpu.get_state(), orc.get_state(), rho_max, "init")
     for it in range(iters):
+        check = (it + 1) % check_every == 0
+        if check:
+            one = oracle.Oracle(pb, pr)
+            one.set_state(gpu.get_state())
         gpu.iterate(1)
         orc.iterate(1)
-        if (it + 1) % check_every == 0:
-            compare(gpu.get_state(), orc.get_state(), rho_max, f"iteration {it + 1}")
+        gs, os_ = gpu.get_state(), orc.get_state()
+        if check:
+            one.iterate(1)
+            compare(gs, one.get_state(), rho_max, f"one-step iteration {it + 1}")
+            one.close()
+        if it < FREE_RUN:
+            compare(gs, os_, rho_max, f"free-running iteration {it + 1}")
+        assert np.array_equal(gs["u"], os_["u"]), f"free-running schedule, iteration {it + 1}"
+        assert np.array_equal(gs["scal"][[0, 2, 3, 4]], os_["scal"][[0, 2, 3, 4]]), f"scalars, iteration {it + 1}"
     rg, ro = gpu.report(), orc.report()
     assert rg["objective"] == pytest.approx(ro["objective"], rel=1e-9)
     assert rg["primal_inf"] == pytest.approx(ro["primal_inf"], rel=1e-6, abs=1e-12)

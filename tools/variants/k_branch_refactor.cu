@@ -18,6 +18,13 @@
 // search, ratio test) is the one specified in DESIGN.md 5.3; the oracle implements the same
 // algorithm independently (oracle/oracle.c) with a straightforward evaluation.
 #include "ucac_dev.cuh"
+#ifdef UCAC_PROF
+#include <cstdio>
+#endif
+
+#ifndef UCAC_TRON_DIRECT
+#define UCAC_TRON_DIRECT 0   // 1: Newton step by LDL^T when it is interior (tried)
+#endif
 
 namespace ucac {
 namespace {
@@ -203,28 +210,19 @@ struct BrFun {
     }
 };
 
+// pairwise partial sums: half the dependent-FMA chain of a running sum
 template <int N>
 __device__ __forceinline__ double dotn(const double *a, const double *b) {
-    double s = 0.0;
+    double s = a[0] * b[0] + a[1] * b[1];
 #pragma unroll
-    for (int i = 0; i < N; i++) s += a[i] * b[i];
+    for (int i = 2; i + 1 < N; i += 2) s += a[i] * b[i] + a[i + 1] * b[i + 1];
+    if (N & 1) s += a[N - 1] * b[N - 1];
     return s;
 }
 template <int N>
 __device__ __forceinline__ void matvec(const double (*H)[N], const double *v, double *o) {
 #pragma unroll
-    for (int i = 0; i < N; i++) {
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; j++) s += H[i][j] * v[j];
-        o[i] = s;
-    }
-}
-template <int N>
-__device__ __forceinline__ double qmodel(const double *g, const double (*H)[N], const double *s) {
-    double Hs[N];
-    matvec<N>(H, s, Hs);
-    return dotn<N>(g, s) + 0.5 * dotn<N>(s, Hs);
+    for (int i = 0; i < N; i++) o[i] = dotn<N>(H[i], v);
 }
 // compare/select clamp (the oracle's form; cheaper than fmin/fmax with their NaN handling)
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -236,10 +234,6 @@ __device__ __forceinline__ void pstep(const double *x, const double *lo, const d
     for (int i = 0; i < N; i++) s[i] = clampd(x[i] - a * g[i], lo[i], hi[i]) - x[i];
 }
 template <int N>
-__device__ __forceinline__ bool cauchy_ok(const double *g, const double (*H)[N], const double *s, double delta) {
-    return sqrt(dotn<N>(s, s)) <= delta && qmodel<N>(g, H, s) <= TR_MU0 * dotn<N>(g, s);
-}
-template <int N>
 __device__ __forceinline__ double bnd_tau(const double *a, const double *p, double delta) {
     double aa = dotn<N>(a, a), ap = dotn<N>(a, p), pp = dotn<N>(p, p);
     if (pp <= 0.0) return 0.0;
@@ -248,39 +242,77 @@ __device__ __forceinline__ double bnd_tau(const double *a, const double *p, doub
     return ap > 0.0 ? gap / (ap + rad) : (rad - ap) / pp;
 }
 
+// Projected trust-region Newton, split into begin / converged / iterate so a
+// caller can interleave iterations of different solves (the flattened AL loop of k_branch_al).
 template <int N>
-__device__ __forceinline__ void copy_h(const double (*H)[N], double (*o)[N]) {
+struct Tron {
+    double f, g[N], H[N][N], delta, alpha;
+    int it;
+
+    template <class Fun>
+    __device__ __forceinline__ void begin(const Fun &fn, double *x, const double *lo, const double *hi) {
 #pragma unroll
-    for (int i = 0; i < N; i++)
+        for (int i = 0; i < N; i++) x[i] = clampd(x[i], lo[i], hi[i]);
+        fn.template eval<N, true>(x, f, g, H);
+        delta = TR_DELTA0;
+        alpha = 1.0;
+        it = 0;
+        // first Cauchy trial length: the model minimiser along -g (R41)
+        double Hg[N];
+        matvec<N>(H, g, Hg);
+        const double gHg = dotn<N>(g, Hg), gg = dotn<N>(g, g);
+        if (gHg > 0.0 && gg > 0.0) alpha = gg / gHg;
+    }
+    // ||P(x - g) - x||_inf <= gtol
+    __device__ __forceinline__ bool converged(const double *x, const double *lo, const double *hi,
+                                              double gtol) const {
+        double pgn = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; j++) o[i][j] = H[i][j];
+        for (int i = 0; i < N; i++) pgn = fmax(pgn, fabs(clampd(x[i] - g[i], lo[i], hi[i]) - x[i]));
+        return pgn <= gtol;
+    }
+    // one iteration (Cauchy point, CG, projected search, ratio test); true = stall stop
+    template <class Fun>
+    __device__ __forceinline__ bool iterate(const Fun &fn, double *x, const double *lo, const double *hi);
+};
+
+// One Cauchy trial s = P(x - a g) - x: returns whether the sufficient-decrease and trust-region
+// tests hold, and the model value q(s).  While only the coordinates pinned at a bound (gm = 0)
+// are clamped, s = -a gm and q(s) = -a gm.gm + a^2/2 gm'H gm, O(N) instead of a mat-vec.
+template <int N>
+__device__ __forceinline__ bool cauchy_trial(const double *x, const double *lo, const double *hi, const double *g,
+                                             const double *gm, const double (*H)[N], double gg, double gHg,
+                                             double a, double d2, double *s, double &q, bool &simple) {
+    simple = true;
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        const double v = x[i] - a * g[i];
+        s[i] = clampd(v, lo[i], hi[i]) - x[i];
+        simple = simple && (gm[i] == 0.0 || (v >= lo[i] && v <= hi[i]));
+    }
+    double ss, gs;
+    if (simple) {
+        ss = a * a * gg;
+        gs = -a * gg;
+        q = gs + 0.5 * a * a * gHg;
+    } else {
+        double Hs[N];
+        matvec<N>(H, s, Hs);
+        ss = dotn<N>(s, s);
+        gs = dotn<N>(g, s);
+        q = gs + 0.5 * dotn<N>(s, Hs);
+    }
+    return ss <= d2 && q <= TR_MU0 * gs;
 }
 
-// Second-order multiplier update of the thermal AL (R42): dmu = M^{-1} h in the well-conditioned
-// eigen-directions of M = J_F H_FF^{-1} J_F' and sigma h in the others.  H is the AL Hessian at
-// the round's end point x (6 variables); its slack columns are sigma * dh/dx, so
-// J_m = (H[0..3][4+m] / sigma, e_{4+m}).  F = variables strictly inside their bounds; H_FF is
-// factored as L D L' with the fixed rows and columns replaced by the identity.  Returns false
-// (keep the first-order step) if H_FF is not positive definite.
-constexpr double AL_NEWTON_C = 10.0;
-__device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double *x, const double *lo,
-                                              const double *hi, double sig, const double *h, double *dmu) {
-    bool fr[6];
-#pragma unroll
-    for (int i = 0; i < 6; i++) fr[i] = x[i] > lo[i] && x[i] < hi[i];
-    double J[2][6];
-    const double isig = 1.0 / sig;
-#pragma unroll
-    for (int m = 0; m < 2; m++) {
-#pragma unroll
-        for (int a = 0; a < 4; a++) J[m][a] = fr[a] ? H[a][4 + m] * isig : 0.0;
-        J[m][4] = (m == 0 && fr[4]) ? 1.0 : 0.0;
-        J[m][5] = (m == 1 && fr[5]) ? 1.0 : 0.0;
-    }
-    double Lm[6][6], D[6];
+// Newton step on the free set F by an LDL^T factorisation of H_FF (fixed rows/columns
+// replaced by the identity).  Returns false if H_FF is not positive definite.
+template <int N>
+__device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr, const double *r, double *w) {
+    double Lm[N][N], D[N];
     bool pd = true;
 #pragma unroll
-    for (int j = 0; j < 6; j++) {
+    for (int j = 0; j < N; j++) {
         double dj = fr[j] ? H[j][j] : 1.0;
 #pragma unroll
         for (int k = 0; k < j; k++) dj -= Lm[j][k] * Lm[j][k] * D[k];
@@ -288,7 +320,7 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
         D[j] = dj;
         const double inv = 1.0 / dj;
 #pragma unroll
-        for (int i = j + 1; i < 6; i++) {
+        for (int i = j + 1; i < N; i++) {
             double v = (fr[i] && fr[j]) ? H[i][j] : 0.0;
 #pragma unroll
             for (int k = 0; k < j; k++) v -= Lm[i][k] * Lm[j][k] * D[k];
@@ -296,132 +328,105 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
         }
     }
     if (!pd) return false;
-    // V_n = H_FF^{-1} J_n (zero on fixed coordinates), M_mn = J_m . V_n
-    double V[2][6];
+    double z[N];
 #pragma unroll
-    for (int n = 0; n < 2; n++) {
-        double z[6];
+    for (int i = 0; i < N; i++) {
+        double v = r[i];
 #pragma unroll
-        for (int i = 0; i < 6; i++) {
-            double v = J[n][i];
-#pragma unroll
-            for (int k = 0; k < i; k++) v -= Lm[i][k] * z[k];
-            z[i] = v;
-        }
-#pragma unroll
-        for (int i = 5; i >= 0; i--) {
-            double v = z[i] / D[i];
-#pragma unroll
-            for (int k = i + 1; k < 6; k++) v -= Lm[k][i] * V[n][k];
-            V[n][i] = v;
-        }
+        for (int k = 0; k < i; k++) v -= Lm[i][k] * z[k];
+        z[i] = v;
     }
-    const double a = dotn<6>(J[0], V[0]), d = dotn<6>(J[1], V[1]);
-    const double b = 0.5 * (dotn<6>(J[0], V[1]) + dotn<6>(J[1], V[0]));
-    const double mean = 0.5 * (a + d), half = 0.5 * (a - d);
-    const double r = sqrt(half * half + b * b);
-    const double lam0 = mean + r, lam1 = mean - r;
-    double v0, v1;
-    if (r == 0.0) {
-        v0 = 1.0;
-        v1 = 0.0;
-    } else if (a >= d) {
-        const double n = sqrt((lam0 - d) * (lam0 - d) + b * b);
-        v0 = (lam0 - d) / n;
-        v1 = b / n;
-    } else {
-        const double n = sqrt(b * b + (lam0 - a) * (lam0 - a));
-        v0 = b / n;
-        v1 = (lam0 - a) / n;
+#pragma unroll
+    for (int i = N - 1; i >= 0; i--) {
+        double v = z[i] / D[i];
+#pragma unroll
+        for (int k = i + 1; k < N; k++) v -= Lm[k][i] * w[k];
+        w[i] = fr[i] ? v : 0.0;
     }
-    const double thr = 1.0 / (AL_NEWTON_C * sig);
-    const double f0 = lam0 >= thr ? 1.0 / lam0 : sig, f1 = lam1 >= thr ? 1.0 / lam1 : sig;
-    const double p0 = v0 * h[0] + v1 * h[1], p1 = -v1 * h[0] + v0 * h[1];
-    dmu[0] = f0 * p0 * v0 - f1 * p1 * v1;
-    dmu[1] = f0 * p0 * v1 + f1 * p1 * v0;
     return true;
 }
 
-// Projected trust-region Newton.  Returns true when ||P(x-g)-x||_inf <= gtol.
-template <int N, class Fun>
-__device__ bool tron(const Fun &fn, double *x, const double *lo, const double *hi, double gtol,
-                     int maxit, int &iters, double (*Hout)[N] = nullptr) {
-    double f, g[N], H[N][N];
-#pragma unroll
-    for (int i = 0; i < N; i++) x[i] = clampd(x[i], lo[i], hi[i]);
-    fn.template eval<N, true>(x, f, g, H);
-    double delta = TR_DELTA0, alpha = 1.0;
+template <int N>
+template <class Fun>
+__device__ __forceinline__ bool Tron<N>::iterate(const Fun &fn, double *x, const double *lo, const double *hi) {
+    const double d2 = delta * delta;
+    // --- Cauchy point: backtrack (x0.1) or extrapolate (x10) along P(x - a g)
+    double sc[N], qc, gq[N];   // Cauchy step, its model value, model gradient g + H sc
+    bool csimple;
     {
-        // first Cauchy trial length: the model minimiser along -g (R41)
-        double Hg[N];
-        matvec<N>(H, g, Hg);
-        const double gHg = dotn<N>(g, Hg), gg = dotn<N>(g, g);
-        if (gHg > 0.0 && gg > 0.0) alpha = gg / gHg;
-    }
-    int it = 0;
-    for (; it < maxit; it++) {
-        double pgn = 0.0;
+        double gm[N], Hgm[N];
 #pragma unroll
-        for (int i = 0; i < N; i++) pgn = fmax(pgn, fabs(clampd(x[i] - g[i], lo[i], hi[i]) - x[i]));
-        if (pgn <= gtol) {
-            iters = it;
-            if (Hout) copy_h<N>(H, Hout);
-            return true;
+        for (int i = 0; i < N; i++) {
+            const bool pinned = (x[i] <= lo[i] && g[i] > 0.0) || (x[i] >= hi[i] && g[i] < 0.0);
+            gm[i] = pinned ? 0.0 : g[i];
         }
-        // --- Cauchy point: backtrack (x0.1) or extrapolate (x10) along P(x - a g)
-        double sc[N];
-        {
-            double a = alpha;
-            pstep<N>(x, lo, hi, g, a, sc);
-            if (!cauchy_ok<N>(g, H, sc, delta)) {
-                for (int k = 0; k < 60; k++) {
-                    a *= 0.1;
-                    pstep<N>(x, lo, hi, g, a, sc);
-                    if (cauchy_ok<N>(g, H, sc, delta)) break;
-                }
-            } else {
-                for (int k = 0; k < 20; k++) {
-                    double sp[N];
-#pragma unroll
-                    for (int i = 0; i < N; i++) sp[i] = sc[i];
-                    double ap = a;
-                    a *= 10.0;
-                    pstep<N>(x, lo, hi, g, a, sc);
-                    bool same = true;
-#pragma unroll
-                    for (int i = 0; i < N; i++) same = same && (sc[i] == sp[i]);
-                    if (!cauchy_ok<N>(g, H, sc, delta) || same) {
-                        a = ap;
-#pragma unroll
-                        for (int i = 0; i < N; i++) sc[i] = sp[i];
-                        break;
-                    }
-                }
+        matvec<N>(H, gm, Hgm);
+        const double gg = dotn<N>(gm, gm), gHg = dotn<N>(gm, Hgm);
+        double a = alpha;
+        if (!cauchy_trial<N>(x, lo, hi, g, gm, H, gg, gHg, a, d2, sc, qc, csimple)) {
+            for (int k = 0; k < 60; k++) {
+                a *= 0.1;
+                if (cauchy_trial<N>(x, lo, hi, g, gm, H, gg, gHg, a, d2, sc, qc, csimple)) break;
             }
-            alpha = a;
+        } else {
+            for (int k = 0; k < 20; k++) {
+                double sn[N], qn;
+                bool sim;
+                const bool ok = cauchy_trial<N>(x, lo, hi, g, gm, H, gg, gHg, 10.0 * a, d2, sn, qn, sim);
+                bool same = true;
+#pragma unroll
+                for (int i = 0; i < N; i++) same = same && (sn[i] == sc[i]);
+                if (!ok || same) break;
+                a *= 10.0;
+#pragma unroll
+                for (int i = 0; i < N; i++) sc[i] = sn[i];
+                qc = qn;
+                csimple = sim;
+            }
         }
-        // --- Steihaug-Toint CG on the free variables at x + sc, region ||sc + w|| <= delta
-        bool fr[N];
-        double gq[N], w[N];
-        {
+        alpha = a;
+        // gradient of the model at the Cauchy point, gq = g + H sc
+        if (csimple) {
+#pragma unroll
+            for (int i = 0; i < N; i++) gq[i] = g[i] - a * Hgm[i];
+        } else {
             double Hs[N];
             matvec<N>(H, sc, Hs);
 #pragma unroll
-            for (int i = 0; i < N; i++) {
-                double xc = x[i] + sc[i];
-                fr[i] = (xc > lo[i]) && (xc < hi[i]);
-                gq[i] = g[i] + Hs[i];
-                w[i] = 0.0;
-            }
-            double r[N], p[N];
+            for (int i = 0; i < N; i++) gq[i] = g[i] + Hs[i];
+        }
+    }
+    // --- subspace step on the free variables at x + sc, region ||sc + w|| <= delta:
+    // the Newton step when H_FF is positive definite and it lies inside the region (the point
+    // Steihaug-Toint CG converges to), otherwise Steihaug-Toint CG itself
+    bool fr[N];
+    double w[N];
+    {
+        double r[N];
 #pragma unroll
-            for (int i = 0; i < N; i++) {
-                r[i] = fr[i] ? -gq[i] : 0.0;
-                p[i] = r[i];
+        for (int i = 0; i < N; i++) {
+            const double xc = x[i] + sc[i];
+            fr[i] = (xc > lo[i]) && (xc < hi[i]);
+            r[i] = fr[i] ? -gq[i] : 0.0;
+            w[i] = 0.0;
+        }
+        double rr = dotn<N>(r, r);
+        if (rr != 0.0) {
+            bool done = false;
+            if (UCAC_TRON_DIRECT && newton_free<N>(H, fr, r, w)) {
+                double t[N];
+#pragma unroll
+                for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
+                done = dotn<N>(t, t) < d2;
             }
-            double rr = dotn<N>(r, r);
-            if (rr != 0.0) {
-                double tol2 = TR_CGTOL * TR_CGTOL * rr;
+            if (!done) {
+                double p[N];
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    w[i] = 0.0;
+                    p[i] = r[i];
+                }
+                const double tol2 = TR_CGTOL * TR_CGTOL * rr;
                 for (int k = 0; k < N; k++) {
                     double Hp[N], t[N];
                     matvec<N>(H, p, Hp);
@@ -440,7 +445,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                     double tt[N];
 #pragma unroll
                     for (int i = 0; i < N; i++) tt[i] = t[i] + a * p[i];
-                    if (sqrt(dotn<N>(tt, tt)) >= delta) {
+                    if (dotn<N>(tt, tt) >= d2) {
                         double tau = bnd_tau<N>(t, p, delta);
 #pragma unroll
                         for (int i = 0; i < N; i++) w[i] += tau * p[i];
@@ -460,65 +465,80 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                 }
             }
         }
-        // --- projected search along w from the Cauchy point
-        double s[N];
-        {
-            double qc = qmodel<N>(g, H, sc);
-            double b = 1.0;
-            bool found = false;
-            for (int k = 0; k < 20; k++) {
-                double ds[N];
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
-                    ds[i] = s[i] - sc[i];
-                }
-                if (qmodel<N>(g, H, s) <= qc + TR_MU0 * dotn<N>(gq, ds)) {
-                    found = true;
-                    break;
-                }
-                b *= 0.5;
-            }
-            if (!found) {
-#pragma unroll
-                for (int i = 0; i < N; i++) s[i] = sc[i];
-            }
-        }
-        // --- stall: a step at the rounding level of x means the gradient floor is reached
-        {
-            double xm = 0.0;
-#pragma unroll
-            for (int i = 0; i < N; i++) xm = fmax(xm, fabs(x[i]));
-            if (sqrt(dotn<N>(s, s)) <= TR_STALL * (1.0 + xm)) {
-                iters = it;
-                if (Hout) copy_h<N>(H, Hout);
-                return true;
-            }
-        }
-        // --- ratio test
-        double pred = -qmodel<N>(g, H, s);
-        double xn[N], gn[N], fnew;
-#pragma unroll
-        for (int i = 0; i < N; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
-        fn.template eval<N, false>(xn, fnew, gn, nullptr);
-        double ared = f - fnew;
-        if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dotn<N>(g, s) + dotn<N>(gn, s));
-        double ratio = pred > 0.0 ? ared / pred : -1.0;
-        double snorm = sqrt(dotn<N>(s, s));
-        if (ratio > TR_ETA0) {
-#pragma unroll
-            for (int i = 0; i < N; i++) x[i] = xn[i];
-            fn.template eval<N, true>(x, f, g, H);
-        }
-        if (ratio < TR_ETA1) delta = TR_SIG1 * fmin(snorm, delta);
-        else if (ratio > TR_ETA2) delta = fmax(delta, TR_SIG3 * snorm);
     }
-    iters = it;
-    if (Hout) copy_h<N>(H, Hout);
-    double pgn = 0.0;
+    // --- projected search along w from the Cauchy point; q(sc + d) = qc + gq.d + d'Hd/2
+    double s[N], qs = qc;
+    {
+        double b = 1.0;
+        bool found = false;
+        for (int k = 0; k < 20; k++) {
+            double ds[N], Hd[N];
 #pragma unroll
-    for (int i = 0; i < N; i++) pgn = fmax(pgn, fabs(clampd(x[i] - g[i], lo[i], hi[i]) - x[i]));
-    return pgn <= gtol;
+            for (int i = 0; i < N; i++) {
+                s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
+                ds[i] = s[i] - sc[i];
+            }
+            matvec<N>(H, ds, Hd);
+            const double gd = dotn<N>(gq, ds);
+            const double q = qc + gd + 0.5 * dotn<N>(ds, Hd);
+            if (q <= qc + TR_MU0 * gd) {
+                found = true;
+                qs = q;
+                break;
+            }
+            b *= 0.5;
+        }
+        if (!found) {
+#pragma unroll
+            for (int i = 0; i < N; i++) s[i] = sc[i];
+        }
+    }
+    const double ss = dotn<N>(s, s);
+    // --- stall: a step at the rounding level of x means the gradient floor is reached
+    {
+        double xm = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; i++) xm = fmax(xm, fabs(x[i]));
+        const double tol = TR_STALL * (1.0 + xm);
+        if (ss <= tol * tol) return true;
+    }
+    // --- ratio test
+    const double pred = -qs;
+    double xn[N], gn[N], fnew;
+#pragma unroll
+    for (int i = 0; i < N; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
+    fn.template eval<N, false>(xn, fnew, gn, nullptr);
+    double ared = f - fnew;
+    if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dotn<N>(g, s) + dotn<N>(gn, s));
+    const double ratio = pred > 0.0 ? ared / pred : -1.0;
+    const double snorm = sqrt(ss);
+    if (ratio > TR_ETA0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) x[i] = xn[i];
+        fn.template eval<N, true>(x, f, g, H);
+    }
+    if (ratio < TR_ETA1) delta = TR_SIG1 * fmin(snorm, delta);
+    else if (ratio > TR_ETA2) delta = fmax(delta, TR_SIG3 * snorm);
+    it++;
+    return false;
+}
+
+// Whole solve.  Returns true when ||P(x-g)-x||_inf <= gtol (or the step stalled at rounding).
+template <int N, class Fun>
+__device__ __forceinline__ bool tron(const Fun &fn, double *x, const double *lo, const double *hi, double gtol,
+                                     int maxit, int &iters) {
+    Tron<N> S;
+    S.begin(fn, x, lo, hi);
+    for (;;) {
+        if (S.converged(x, lo, hi, gtol)) break;
+        if (S.it >= maxit) {
+            iters = S.it;
+            return false;
+        }
+        if (S.iterate(fn, x, lo, hi)) break;
+    }
+    iters = S.it;
+    return true;
 }
 
 __device__ __forceinline__ void warp_add_u64(unsigned long long *dst, unsigned long long v) {
@@ -574,6 +594,12 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #ifndef UCAC_BRANCH_MINB
 #define UCAC_BRANCH_MINB 3
 #endif
+#ifndef UCAC_AL_DEAL
+#define UCAC_AL_DEAL 0
+#endif
+#ifndef UCAC_AL_FLAT
+#define UCAC_AL_FLAT 0
+#endif
 #ifndef UCAC_AL_BLOCKS_PER_SM
 #define UCAC_AL_BLOCKS_PER_SM 4
 #endif
@@ -619,87 +645,176 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
     warp_add_u64(d.cnt + 1, c_cap);
 }
 
-// Phase 2: the queued thermal-active solves (6-variable slack AL, R36), pulled one at a time
-// by every thread of a persistent grid, so the heavy tail is spread over all SMs.
+// Phase 2: the queued thermal-active solves (6-variable slack AL, R36).
+//
+// The warp executes the union of its lanes' control flow, so a nested "AL round { TRON }" loop
+// costs sum over rounds of the max over lanes.  The loop is therefore FLATTENED: every pass does
+// one TRON iteration of whatever round each lane is in, and a lane whose round ends updates
+// (mu, sigma) -- or finishes its solve and takes the next queued item -- in the same pass.  The
+// per-solve arithmetic is exactly the nested algorithm's (oracle orc_branch_solve).
+//
+// Items are dealt lane-major over all warps of the grid (item = lane * nwarps + warp, then
+// strided by 32 * nwarps), so with a short queue each warp carries only a few solves and the
+// max over its lanes stays close to the single longest solve.
+struct AlItem {
+    BrFun<true> F;
+    double lo[6], hi[6], x[6];
+    double r2, sig0, smax, hprev;
+    int k, kk;
+};
+
+__device__ __forceinline__ void al_begin(const Dev &d, int k, AlItem &A) {
+    const size_t LTs = (size_t)d.L * d.T;
+    {
+        BrFun<false> F4;
+        load_solve(d, k, F4, A.lo, A.hi);
+        A.F.Gii = F4.Gii; A.F.Gij = F4.Gij; A.F.Gji = F4.Gji; A.F.Gjj = F4.Gjj;
+        A.F.Bii = F4.Bii; A.F.Bij = F4.Bij; A.F.Bji = F4.Bji; A.F.Bjj = F4.Bjj;
+#pragma unroll
+        for (int r = 0; r < 8; r++) A.F.tau[r] = F4.tau[r];
+        A.F.rpq = F4.rpq; A.F.rva = F4.rva;
+        A.F.K00 = F4.K00; A.F.K02 = F4.K02; A.F.K03 = F4.K03; A.F.K11 = F4.K11;
+        A.F.K12 = F4.K12; A.F.K13 = F4.K13; A.F.K22 = F4.K22;
+    }
+    A.lo[2] = -TWO_PI; A.hi[2] = TWO_PI; A.lo[3] = -TWO_PI; A.hi[3] = TWO_PI;
+    A.lo[4] = 0.0; A.hi[4] = 1.0; A.lo[5] = 0.0; A.hi[5] = 1.0;
+    const double rate = d.rate[k / d.T];
+    A.r2 = rate * rate;
+    A.sig0 = d.al_sigma0_rel * d.rpq * A.r2;
+    A.F.r2inv = 1.0 / A.r2;
+#pragma unroll
+    for (int m = 0; m < 4; m++) A.x[m] = d.x[m * LTs + k];
+    {
+        const double f0 = d.f[0 * LTs + k], f1 = d.f[1 * LTs + k], f2 = d.f[2 * LTs + k], f3 = d.f[3 * LTs + k];
+        A.x[4] = clampd(1.0 - (f0 * f0 + f1 * f1) / A.r2, 0.0, 1.0);
+        A.x[5] = clampd(1.0 - (f2 * f2 + f3 * f3) / A.r2, 0.0, 1.0);
+    }
+    A.F.mu0 = d.al[0 * LTs + k];
+    A.F.mu1 = d.al[1 * LTs + k];
+    A.F.sig = fmax(A.sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
+    A.smax = d.al_sigma_max_rel * A.sig0;
+    A.hprev = INFINITY;
+    A.k = k;
+    A.kk = 0;
+}
+
+__device__ __forceinline__ void al_finish(const Dev &d, const AlItem &A) {
+    const size_t LTs = (size_t)d.L * d.T;
+    const int k = A.k;
+    double C, S, f0, f1, f2, f3;
+    A.F.flows(A.x, C, S, f0, f1, f2, f3);
+#pragma unroll
+    for (int m = 0; m < 4; m++) d.x[m * LTs + k] = A.x[m];
+    d.f[0 * LTs + k] = f0;
+    d.f[1 * LTs + k] = f1;
+    d.f[2 * LTs + k] = f2;
+    d.f[3 * LTs + k] = f3;
+    d.al[0 * LTs + k] = A.F.mu0;
+    d.al[1 * LTs + k] = A.F.mu1;
+    d.al[2 * LTs + k] = A.F.sig;
+    emit_tauhat(d, k, A.x, f0, f1, f2, f3);
+}
+
 __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
     if (d.st->done) return;
-    const size_t LTs = (size_t)d.L * d.T;
     const unsigned n = *((volatile unsigned *)d.alq_cnt);
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = threadIdx.x & 31, gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+#if UCAC_AL_DEAL
+    unsigned next = lane * nwarps + gwarp;   // lane-major: few solves per warp
+#else
+    unsigned next = gwarp * 32 + lane;       // dense: full warps
+#endif
     unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0;
-    for (;;) {
-        const unsigned idx = atomicAdd(d.alq_cnt + 1, 1u);
-        if (idx >= n) break;
-        const int k = d.alq[idx];
-        BrFun<true> F6;
-        double lo[6], hi[6];
-        {
-            BrFun<false> F4;
-            load_solve(d, k, F4, lo, hi);
-            F6.Gii = F4.Gii; F6.Gij = F4.Gij; F6.Gji = F4.Gji; F6.Gjj = F4.Gjj;
-            F6.Bii = F4.Bii; F6.Bij = F4.Bij; F6.Bji = F4.Bji; F6.Bjj = F4.Bjj;
-#pragma unroll
-            for (int r = 0; r < 8; r++) F6.tau[r] = F4.tau[r];
-            F6.rpq = F4.rpq; F6.rva = F4.rva;
-            F6.K00 = F4.K00; F6.K02 = F4.K02; F6.K03 = F4.K03; F6.K11 = F4.K11;
-            F6.K12 = F4.K12; F6.K13 = F4.K13; F6.K22 = F4.K22;
-        }
-        lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
-        lo[4] = 0.0; hi[4] = 1.0; lo[5] = 0.0; hi[5] = 1.0;
-        const double rate = d.rate[k / d.T];
-        const double r2 = rate * rate;
-        const double sig0 = d.al_sigma0_rel * d.rpq * r2;
-        F6.r2inv = 1.0 / r2;
-        double x[6];
-#pragma unroll
-        for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
-        {
-            const double f0 = d.f[0 * LTs + k], f1 = d.f[1 * LTs + k], f2 = d.f[2 * LTs + k], f3 = d.f[3 * LTs + k];
-            x[4] = clampd(1.0 - (f0 * f0 + f1 * f1) / r2, 0.0, 1.0);
-            x[5] = clampd(1.0 - (f2 * f2 + f3 * f3) / r2, 0.0, 1.0);
-        }
-        double mu0 = d.al[0 * LTs + k], mu1 = d.al[1 * LTs + k];
-        double sig = fmax(sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
-        const double smax = d.al_sigma_max_rel * sig0;
-        double hprev = INFINITY;
-        double C, S, f0, f1, f2, f3;
-        int kk = 0;
+    AlItem A;
+#if !UCAC_AL_FLAT
+    // nested form: AL rounds around whole TRON solves
+    for (; next < n; next += 32 * nwarps) {
+#ifdef UCAC_PROF
+        const long long t0 = clock64();
+        unsigned long long it0 = c_it, cap0 = c_cap;
+#endif
+        al_begin(d, d.alq[next], A);
         c_al += 1;
-        for (; kk < d.al_maxit; kk++) {
-            F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
+        for (;;) {
             int it = 0;
-            double Hx[6][6];
-            bool ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it, Hx);
+            const bool ok = tron<6>(A.F, A.x, A.lo, A.hi, d.tron_gtol, d.tron_maxit, it);
             c_it += it;
             c_cap += !ok;
-            F6.flows(x, C, S, f0, f1, f2, f3);
-            double h1 = (f0 * f0 + f1 * f1) / r2 - 1.0 + x[4];
-            double h2 = (f2 * f2 + f3 * f3) / r2 - 1.0 + x[5];
-            double hm = fmax(fabs(h1), fabs(h2));
+            double C, Sn, f0, f1, f2, f3;
+            A.F.flows(A.x, C, Sn, f0, f1, f2, f3);
+            const double h1 = (f0 * f0 + f1 * f1) / A.r2 - 1.0 + A.x[4];
+            const double h2 = (f2 * f2 + f3 * f3) / A.r2 - 1.0 + A.x[5];
+            const double hm = fmax(fabs(h1), fabs(h2));
             if (hm <= d.al_eta_star) break;
-            const double hv[2] = {h1, h2};
-            double dmu[2];
-            if (!al_newton_dmu(Hx, x, lo, hi, sig, hv, dmu)) {
-                dmu[0] = sig * h1;
-                dmu[1] = sig * h2;
+            A.F.mu0 += A.F.sig * h1;
+            A.F.mu1 += A.F.sig * h2;
+            if (hm > 0.25 * A.hprev) A.F.sig = fmin(10.0 * A.F.sig, A.smax);
+            A.hprev = hm;
+            if (++A.kk >= d.al_maxit) {
+                c_alcap += 1;
+                break;
             }
-            mu0 += dmu[0];
-            mu1 += dmu[1];
-            if (hm > 0.25 * hprev) sig = fmin(10.0 * sig, smax);
-            hprev = hm;
         }
-        c_alcap += kk >= d.al_maxit;
-        F6.flows(x, C, S, f0, f1, f2, f3);
-#pragma unroll
-        for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
-        d.f[0 * LTs + k] = f0;
-        d.f[1 * LTs + k] = f1;
-        d.f[2 * LTs + k] = f2;
-        d.f[3 * LTs + k] = f3;
-        d.al[0 * LTs + k] = mu0;
-        d.al[1 * LTs + k] = mu1;
-        d.al[2 * LTs + k] = sig;
-        emit_tauhat(d, k, x, f0, f1, f2, f3);
+        al_finish(d, A);
+#ifdef UCAC_PROF
+        // diagnostic build only: report solves slower than UCAC_PROF cycles
+        const long long dt = clock64() - t0;
+        if (dt > UCAC_PROF)
+            printf("ALPROF k %d l %d t %d cycles %lld tron_iters %llu rounds %d tron_caps %llu warp %u lane %u\n",
+                   A.k, A.k / d.T, A.k % d.T, dt, c_it - it0, A.kk + 1, c_cap - cap0, gwarp, lane);
+#endif
     }
+#else
+    Tron<6> S;
+    bool busy = false;
+    for (;;) {
+        if (!busy) {
+            if (next >= n) break;
+            al_begin(d, d.alq[next], A);
+            next += 32 * nwarps;
+            c_al += 1;
+            S.begin(A.F, A.x, A.lo, A.hi);
+            busy = true;
+        }
+        // one TRON pass of the current round
+        bool round_done = false, ok = true;
+        if (S.converged(A.x, A.lo, A.hi, d.tron_gtol)) {
+            round_done = true;
+        } else if (S.it >= d.tron_maxit) {
+            round_done = true;
+            ok = false;
+        } else {
+            round_done = S.iterate(A.F, A.x, A.lo, A.hi);
+        }
+        if (!round_done) continue;
+        // round end: the method-of-multipliers update (R9)
+        c_it += S.it;
+        c_cap += !ok;
+        double C, Sn, f0, f1, f2, f3;
+        A.F.flows(A.x, C, Sn, f0, f1, f2, f3);
+        const double h1 = (f0 * f0 + f1 * f1) / A.r2 - 1.0 + A.x[4];
+        const double h2 = (f2 * f2 + f3 * f3) / A.r2 - 1.0 + A.x[5];
+        const double hm = fmax(fabs(h1), fabs(h2));
+        bool fin = hm <= d.al_eta_star;
+        if (!fin) {
+            A.F.mu0 += A.F.sig * h1;
+            A.F.mu1 += A.F.sig * h2;
+            if (hm > 0.25 * A.hprev) A.F.sig = fmin(10.0 * A.F.sig, A.smax);
+            A.hprev = hm;
+            if (++A.kk >= d.al_maxit) {
+                fin = true;
+                c_alcap += 1;
+            }
+        }
+        if (fin) {
+            al_finish(d, A);
+            busy = false;
+        } else {
+            S.begin(A.F, A.x, A.lo, A.hi);
+        }
+    }
+#endif
     if (c_it) atomicAdd(d.cnt + 0, c_it);
     if (c_cap) atomicAdd(d.cnt + 1, c_cap);
     if (c_al) atomicAdd(d.cnt + 2, c_al);
