@@ -161,7 +161,7 @@ ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids, int32_t *
 /* Same iterations launched kernel by kernel with a CUDA event pair around every launch;
  * kernel_ms[k] receives the summed device time of kernel k (order: ucac_kernel_name(k)),
  * launches[k] the number of launches.  Used by the benchmark for per-kernel rooflines. */
-#define UCAC_NKERNELS 8
+#define UCAC_NKERNELS 10
 ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches);
 const char *ucac_kernel_name(int32_t k);
 

@@ -608,6 +608,10 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         if (rate > 0.0 && (f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2)) {
             const unsigned pos = atomicAdd(d.alq_cnt, 1u);
             d.alq[pos] = k;
+            const int l = k / d.T, t = k - l * d.T;
+            const unsigned stamp = mark_stamp(d);
+            d.bmark[(size_t)d.bfrom[l] * d.T + t] = stamp;
+            d.bmark[(size_t)d.bto[l] * d.T + t] = stamp;
         } else {
             d.al[0 * LTs + k] = 0.0;
             d.al[1 * LTs + k] = 0.0;

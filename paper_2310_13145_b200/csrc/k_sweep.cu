@@ -97,7 +97,11 @@ constexpr int ROWS_THREADS = 128;
 // generators' rows (read here) and of its incident branch ends (tauhat, written by k_branch),
 // in canonical CSR order; writes the generator copies (and their rows GP, GQ, RC_{t+1}),
 // wbar, thbar and (muP, muQ, dwbar, dthbar) for k_rows.
-__global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
+//
+// Two launches per iteration: early (late = 0) for the bus-periods with no thermal-AL solve at an
+// incident branch end -- their inputs are final after the fast path, so in the single-GPU graph
+// this runs in the shadow of k_branch_al -- and late (late = 1) for the marked ones.
+__global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d, int late) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t GT = (size_t)d.G * T, LT = (size_t)d.L * T, BT = (size_t)d.B * T;
@@ -107,7 +111,8 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
     const int pending = d.st->pending_outer;
     Acc acc;
-    if (k < d.B_own * T) {   // owned buses only; ghost buses are solved by their owner
+    if (k < d.B_own * T && (d.bmark[k] == mark_stamp(d)) == (late != 0)) {
+        // owned buses only; ghost buses are solved by their owner
         const int i = k / T, t = k - i * T;
         const int g0 = d.bg_ptr[i], g1 = d.bg_ptr[i + 1];
         const int e0 = d.be_ptr[i], e1 = d.be_ptr[i + 1];
@@ -195,14 +200,15 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
         d.bmu[2 * BT + k] = wb - wbo;
         d.bmu[3 * BT + k] = tb - tbo;
     }
-    block_reduce_store(acc, d.part_bus);
+    block_reduce_store(acc, late ? d.part_bus2 : d.part_bus);
     (void)LT;
 }
 
 // k_rows: one thread per (l,t) finishes step (7d) for the two ends of branch l (flow copies
 // fbar = tauhat - mu/rho_pq) and runs (7e)/(7f) for its 8 rows.  Same (l,t) mapping and
 // coalescing as k_branch.
-__global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
+// Early / late launches as for k_bus: a branch-period is late if either end bus is marked.
+__global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d, int late) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t LT = (size_t)d.L * T, BT = (size_t)d.B * T;
@@ -212,8 +218,10 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
     const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
     const int pending = d.st->pending_outer;
     Acc acc;
-    if (k < d.L * T) {
-        const int l = k / T, t = k - l * T;
+    const int l = k / T, t = k - l * T;
+    const unsigned stamp = mark_stamp(d);
+    if (k < d.L * T && (d.bmark[(size_t)d.bfrom[l] * T + t] == stamp || d.bmark[(size_t)d.bto[l] * T + t] == stamp) ==
+                           (late != 0)) {
 #pragma unroll
         for (int side = 0; side < 2; side++) {
             const int bus = side ? d.bto[l] : d.bfrom[l];
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
                    acc);
         }
     }
-    block_reduce_store(acc, d.part_rows);
+    block_reduce_store(acc, late ? d.part_rows2 : d.part_rows);
 }
 
 
@@ -481,9 +489,13 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(Dev d) {
 #pragma unroll
     for (int k = 0; k < NPART; k++) v[k] = 0.0;
     const int nb = d.nblk_bus, nu = d.nblk_ubar, nr = d.nblk_rows;
-    for (int b = tid; b < nb + nu + nr; b += RED_THREADS) {
+    // partial slots in a fixed order: bus early, bus late, ubar, rows early, rows late
+    for (int b = tid; b < 2 * nb + nu + 2 * nr; b += RED_THREADS) {
         const double *pp = b < nb ? d.part_bus + (size_t)b * NPART
-                         : (b < nb + nu ? d.part_ubar + (size_t)(b - nb) * NPART : d.part_rows + (size_t)(b - nb - nu) * NPART);
+                         : b < 2 * nb ? d.part_bus2 + (size_t)(b - nb) * NPART
+                         : b < 2 * nb + nu ? d.part_ubar + (size_t)(b - 2 * nb) * NPART
+                         : b < 2 * nb + nu + nr ? d.part_rows + (size_t)(b - 2 * nb - nu) * NPART
+                                                : d.part_rows2 + (size_t)(b - 2 * nb - nu - nr) * NPART;
 #pragma unroll
         for (int k = 0; k < NPART; k++) {
             const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
@@ -611,8 +623,8 @@ int nblk_bus(int B, int T) { return (B * T + BUS_THREADS - 1) / BUS_THREADS; }
 int nblk_ubar(int G, int T) { return (G * T + UBAR_THREADS - 1) / UBAR_THREADS; }
 int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; }
 
-void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d); }
-void launch_rows(const Dev &d, cudaStream_t s) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d); }
+void launch_bus(const Dev &d, cudaStream_t s, int late) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d, late); }
+void launch_rows(const Dev &d, cudaStream_t s, int late) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d, late); }
 void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
 void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }
 void launch_reduce_part(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }

@@ -167,9 +167,9 @@ struct ucac_ctx {
     int G = 0, L = 0, B = 0, T = 0;      // local counts (B = owned buses)
     int nranks = 1, rank = 0, comm_mode = 0;
     ncclComm_t comm = nullptr;
-    cudaStream_t s = nullptr, s2 = nullptr;
+    cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     bool own_stream = false;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int gunroll[2] = {1, 16};
     std::vector<void *> dalloc;
@@ -357,8 +357,11 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         ctx->own_stream = true;
     }
     if (cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->s3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_genx, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_early, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
     if (cudaMallocHost(&ctx->st_host, sizeof(DevStatus)) != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
     memset(ctx->st_host, 0, sizeof(DevStatus));
@@ -470,6 +473,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ALLOC(part_bus, double, (size_t)d.nblk_bus * NPART);
     ALLOC(part_ubar, double, (size_t)d.nblk_ubar * NPART);
     ALLOC(part_rows, double, (size_t)d.nblk_rows * NPART);
+    ALLOC(part_bus2, double, (size_t)d.nblk_bus * NPART);
+    ALLOC(part_rows2, double, (size_t)d.nblk_rows * NPART);
+    ALLOC(bmark, unsigned, BT);
     ALLOC(tauh, double, (size_t)NBROW * (L + P.Lp) * T);
     ALLOC(bmu, double, 4 * BT);
     ALLOC(cnt, unsigned long long, 4);
@@ -512,15 +518,23 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
 
 // ------------------------------------------------------------------------------------------
 // one inner iteration.  Dependency order (also the order of the eager, timed path):
-//   (7a) k_gen -> (7b) k_genx, k_branch, k_branch_al -> (7d) k_bus, k_rows -> (7c) k_ubar -> S8/S9.
-// In the graph the generator chain k_gen -> k_genx -> k_ubar (which never reads a branch
-// result) runs on a second stream, forked AFTER the register-bound fast-path branch kernel
-// (sharing the SMs with it halves its occupancy) and overlapping the latency-bound thermal
-// AL tail; the bus solve joins both chains.  Several ranks add the halo exchange: the cut
-// ends' tauhat before the bus solve, the bus results before the row update, the reduction
-// record before the inner/outer decision.
+//   (7a) k_gen -> (7b) k_genx, k_branch -> (7d) k_bus, k_rows [early] -> (7b) k_branch_al
+//   -> (7d) k_bus, k_rows [late] -> (7c) k_ubar -> S8/S9.
+// The fast-path branch kernel marks the bus-periods touched by a thermal-AL solve; the bus
+// solve and row update of everything else only need the fast path and the generator x-update
+// (early phase), the marked ones wait for the AL tail (late phase).  In the single-GPU graph:
+//   s : k_branch ---------------------------> k_branch_al --------> [join] k_bus/k_rows late, k_reduce
+//   s2:           k_gen -> k_genx -> k_ubar ---------------------------^
+//   s3:                      `-> k_bus/k_rows early -------------------^
+// i.e. the early sweep (~90 % of the bus/row work) and the generator chain (which never reads a
+// branch result) run in the shadow of the latency-bound AL tail.  The generator chain forks AFTER
+// the register-bound fast path (sharing the SMs with it halves its occupancy).  Several ranks
+// add the halo exchange: the cut ends' tauhat before the bus solve, the bus results
+// before the row update, the reduction record before the inner/outer decision; there both bus
+// phases run after the tauhat exchange and both row phases after the bus exchange.
 // ------------------------------------------------------------------------------------------
-static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BRANCH_AL, K_BUS, K_ROWS, K_UBAR, K_REDUCE};
+static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BUS, K_ROWS, K_BRANCH_AL, K_BUS_LATE, K_ROWS_LATE,
+                                  K_UBAR, K_REDUCE};
 
 static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
     switch (k) {
@@ -528,8 +542,10 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
         case K_BRANCH_AL: launch_branch_al(ctx->d, s); break;
         case K_GEN: launch_gen(ctx->d, s); break;
         case K_GENX: launch_genx(ctx->d, s); break;
-        case K_BUS: launch_bus(ctx->d, s); break;
-        case K_ROWS: launch_rows(ctx->d, s); break;
+        case K_BUS: launch_bus(ctx->d, s, 0); break;
+        case K_BUS_LATE: launch_bus(ctx->d, s, 1); break;
+        case K_ROWS: launch_rows(ctx->d, s, 0); break;
+        case K_ROWS_LATE: launch_rows(ctx->d, s, 1); break;
         case K_UBAR: launch_ubar(ctx->d, s); break;
         default: launch_reduce(ctx->d, s); break;
     }
@@ -543,6 +559,13 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
     launch_kernel(ctx, K_GEN, ctx->s2);
     launch_kernel(ctx, K_GENX, ctx->s2);
+    if (!multi) {
+        cudaEventRecord(ctx->ev_genx, ctx->s2);
+        cudaStreamWaitEvent(ctx->s3, ctx->ev_genx, 0);
+        launch_kernel(ctx, K_BUS, ctx->s3);
+        launch_kernel(ctx, K_ROWS, ctx->s3);
+        cudaEventRecord(ctx->ev_early, ctx->s3);
+    }
     launch_kernel(ctx, K_UBAR, ctx->s2);
     cudaEventRecord(ctx->ev_join, ctx->s2);
     launch_kernel(ctx, K_BRANCH_AL, ctx->s);
@@ -552,23 +575,28 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         launch_unpack_tau(d, ctx->s);
     }
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
+    if (!multi) {
+        cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
+        launch_kernel(ctx, K_BUS_LATE, ctx->s);
+        launch_kernel(ctx, K_ROWS_LATE, ctx->s);
+        launch_kernel(ctx, K_REDUCE, ctx->s);
+        return;
+    }
     launch_kernel(ctx, K_BUS, ctx->s);
-    if (multi && d.max_export > 0) {
+    launch_kernel(ctx, K_BUS_LATE, ctx->s);
+    if (d.max_export > 0) {
         launch_pack_bus(d, ctx->s);
         ncclAllGather(d.xsend2, d.xrecv2, (size_t)d.max_export * 6 * d.T, ncclDouble, ctx->comm, ctx->s);
         launch_unpack_bus(d, ctx->s);
     }
     launch_kernel(ctx, K_ROWS, ctx->s);
-    if (multi) {
-        launch_reduce_part(d, ctx->s);
-        ncclGroupStart();
-        ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, ctx->s);
-        ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, ctx->s);
-        ncclGroupEnd();
-        launch_finalize(d, ctx->s);
-    } else {
-        launch_kernel(ctx, K_REDUCE, ctx->s);
-    }
+    launch_kernel(ctx, K_ROWS_LATE, ctx->s);
+    launch_reduce_part(d, ctx->s);
+    ncclGroupStart();
+    ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, ctx->s);
+    ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, ctx->s);
+    ncclGroupEnd();
+    launch_finalize(d, ctx->s);
 }
 
 static ucac_status build_graphs(ucac_ctx *ctx) {
@@ -675,6 +703,7 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
             ucac_ctx *c = ctxs[r];
             if (c->d.max_cut > 0) launch_unpack_tau(c->d, c->s);
             launch_kernel(c, K_BUS, c->s);
+            launch_kernel(c, K_BUS_LATE, c->s);
             if (c->d.max_export > 0) launch_pack_bus(c->d, c->s);
         }
         CK(sync_all());
@@ -691,6 +720,7 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
             ucac_ctx *c = ctxs[r];
             if (c->d.max_export > 0) launch_unpack_bus(c->d, c->s);
             launch_kernel(c, K_ROWS, c->s);
+            launch_kernel(c, K_ROWS_LATE, c->s);
             if (n > 1) launch_reduce_part(c->d, c->s);
             else launch_kernel(c, K_REDUCE, c->s);
         }
@@ -716,7 +746,7 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
 }
 
 static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows",
-                                    "k_genx"};
+                                    "k_genx", "k_bus_late", "k_rows_late"};
 extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
 
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
@@ -994,7 +1024,13 @@ extern "C" ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz) {
     sz->alg_bytes[K_ROWS] = LT * 72 * 8;
     // k_ubar: per gen-period: read u p q ph ubar(3) z,y,lambda of 9 rows (27); write ubar(3) z,y (18)
     sz->alg_bytes[K_UBAR] = GT * (51 * 8 + 1);
-    sz->alg_bytes[K_REDUCE] = (int64_t)(ctx->d.nblk_bus + ctx->d.nblk_ubar + ctx->d.nblk_rows) * NPART * 8;
+    sz->alg_bytes[K_REDUCE] = (int64_t)(2 * ctx->d.nblk_bus + ctx->d.nblk_ubar + 2 * ctx->d.nblk_rows) * NPART * 8;
+    // the early/late split of k_bus and k_rows is data-dependent: their figures above cover both
+    // launches (plus the marks, 4 B per bus-period and 8 B per branch-period per launch)
+    sz->alg_bytes[K_BUS] += 2 * BT * 4;
+    sz->alg_bytes[K_ROWS] += 2 * LT * 8;
+    sz->alg_bytes[K_BUS_LATE] = 0;
+    sz->alg_bytes[K_ROWS_LATE] = 0;
     sz->alg_bytes[K_BRANCH_AL] = 0;  // data-dependent: 49 doubles per queued (l,t)
     int64_t tot = 0;
     for (int k = 0; k < NKERN; k++) tot += sz->alg_bytes[k];
@@ -1020,7 +1056,10 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->ev_genx) cudaEventDestroy(ctx->ev_genx);
+    if (ctx->ev_early) cudaEventDestroy(ctx->ev_early);
     if (ctx->s2) cudaStreamDestroy(ctx->s2);
+    if (ctx->s3) cudaStreamDestroy(ctx->s3);
     if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);
     delete ctx;
 }

@@ -17,7 +17,7 @@ enum BrRow { B_FPIJ = 0, B_FQIJ, B_FPJI, B_FQJI, B_WI, B_WJ, B_AI, B_AJ, NBROW }
 
 // kernel ids (ucac_kernel_name)
 enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, K_BRANCH_AL = 5, K_ROWS = 6,
-                K_GENX = 7, NKERN = 8 };
+                K_GENX = 7, K_BUS_LATE = 8, K_ROWS_LATE = 9, NKERN = 10 };
 
 // per-block reduction record (S8): max |r|, max |r+z|, sum (r+z)^2, max |z|, sum z^2,
 // max rho |dxbar|, objective, non-finite flag
@@ -96,11 +96,16 @@ struct Dev {
     double *bmu;                      // [4][B*T] muP, muQ, wbar - wbar_old, thbar - thbar_old
     double *part_rows;                // [nblk_rows][NPART]
     int *alq;                         // [L*T] queue of thermal-active solves (phase 2)
+    unsigned *bmark;                  // [B*T] = stamp(iteration) if an incident (l,t) is queued:
+                                      // its bus solve and rows wait for the AL tail (late phase)
+    double *part_bus2, *part_rows2;   // late-phase block partials (same shapes)
     unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
     DevStatus *st;
 };
 
 __host__ __device__ inline size_t gi(const Dev &d, int g, int t) { return (size_t)g * d.T + t; }
+// per-iteration stamp of bmark (read before k_reduce advances inner_total; never 0)
+__device__ __forceinline__ unsigned mark_stamp(const Dev &d) { return (unsigned)(d.st->inner_total + 1); }
 
 }  // namespace ucac
 
@@ -110,8 +115,8 @@ void launch_branch(const Dev &d, cudaStream_t s);
 void launch_branch_al(const Dev &d, cudaStream_t s);
 void launch_gen(const Dev &d, cudaStream_t s);
 void launch_genx(const Dev &d, cudaStream_t s);
-void launch_bus(const Dev &d, cudaStream_t s);
-void launch_rows(const Dev &d, cudaStream_t s);
+void launch_bus(const Dev &d, cudaStream_t s, int late);
+void launch_rows(const Dev &d, cudaStream_t s, int late);
 int nblk_rows(int L, int T);
 // multi-rank
 void launch_reduce_part(const Dev &d, cudaStream_t s);

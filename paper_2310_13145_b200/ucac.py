@@ -20,8 +20,9 @@ ip = C.POINTER(C.c_int32)
 i8p = C.POINTER(C.c_int8)
 i64p = C.POINTER(C.c_int64)
 
-NKERNELS = 8
-KERNELS = ["k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows", "k_genx"]
+NKERNELS = 10
+KERNELS = ["k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows", "k_genx", "k_bus_late",
+           "k_rows_late"]
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ENUMERIC", 6: "ESTATE", 7: "EUNSUPPORTED"}
 
 
