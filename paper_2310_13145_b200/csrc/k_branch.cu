@@ -608,10 +608,20 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         if (rate > 0.0 && (f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2)) {
             const unsigned pos = atomicAdd(d.alq_cnt, 1u);
             d.alq[pos] = k;
+            // mark both end buses and every branch end at them: their bus solve and end rows move
+            // to the late phase, after the AL tail
             const int l = k / d.T, t = k - l * d.T;
             const unsigned stamp = mark_stamp(d);
-            d.bmark[(size_t)d.bfrom[l] * d.T + t] = stamp;
-            d.bmark[(size_t)d.bto[l] * d.T + t] = stamp;
+#pragma unroll
+            for (int side = 0; side < 2; side++) {
+                const int bus = side ? d.bto[l] : d.bfrom[l];
+                d.bmark[(size_t)bus * d.T + t] = stamp;
+                if (bus < d.B_own)
+                    for (int a = d.be_ptr[bus]; a < d.be_ptr[bus + 1]; a++) {
+                        const int code = d.be_idx[a];
+                        d.rmark[code & 1][(size_t)(code >> 1) * d.T + t] = stamp;
+                    }
+            }
         } else {
             d.al[0 * LTs + k] = 0.0;
             d.al[1 * LTs + k] = 0.0;

@@ -52,6 +52,26 @@ __device__ __forceinline__ void zy_row(double r, double rho, double beta, double
     if (!isfinite(r) || !isfinite(zz)) a.v[P_BAD] = 1.0;
 }
 
+// the same update on values (loads hoisted by the caller): returns z, y and lambda in place
+__device__ __forceinline__ void zy_vals(double r, double rho, double beta, double &z, double &y, double &lam,
+                                        int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+    if (pending) {
+        const double v = lam + beta_lam * z;
+        lam = v < -lmax ? -lmax : (v > lmax ? lmax : v);
+    }
+    const double zz = -((lam + y) + rho * r) / (beta + rho);
+    y = y + rho * (r + zz);
+    z = zz;
+    const double rz = r + zz;
+    a.v[P_PINF] = fmax(a.v[P_PINF], fabs(r));
+    a.v[P_RZINF] = fmax(a.v[P_RZINF], fabs(rz));
+    a.v[P_RZ2] = a.v[P_RZ2] + rz * rz;
+    a.v[P_ZINF] = fmax(a.v[P_ZINF], fabs(zz));
+    a.v[P_Z2] = a.v[P_Z2] + zz * zz;
+    a.v[P_DINF] = fmax(a.v[P_DINF], rho * fabs(dxb));
+    if (!isfinite(r) || !isfinite(zz)) a.v[P_BAD] = 1.0;
+}
+
 // deterministic block reduction -> part[blockIdx.x][NPART]
 __device__ void block_reduce_store(Acc &a, double *part) {
     __shared__ double sh[32][NPART];
@@ -91,6 +111,105 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 constexpr int BUS_THREADS = 128;
 constexpr int UBAR_THREADS = 64;
 constexpr int ROWS_THREADS = 128;
+constexpr int LATE_THREADS = 1024;
+
+// ------------------------------------------------------------------------- S8 partials
+// Every kernel that updates rows leaves one partial per block.  The early ones (k_bus, k_ubar,
+// k_rows) are folded by k_fold_early off the critical path (in the shadow of the AL tail); the
+// late kernels fold their own in their LAST block (threadfence + counter), and the last block of
+// the iteration's last kernel folds the three records.  Fixed slots, fixed order: deterministic.
+enum RecKind { RK_EARLY = 0, RK_BUS_LATE, RK_ROWS_LATE, NRK };
+
+// fold slots [0, n) of part into out[NPART]: 32 groups of NPART threads take every 32nd slot
+// (independent loads in flight), then the groups are folded in order
+__device__ __forceinline__ double fold(int k, double a, double b) {
+    return (k == P_RZ2 || k == P_Z2 || k == P_OBJ) ? a + b : fmax(a, b);
+}
+__device__ void fold_slots(const double *part, int n, double *out) {
+    __shared__ double grp[32][NPART];
+    const int ng = min(32, (int)blockDim.x / NPART);   // groups (blockDim is a multiple of NPART)
+    const int k = threadIdx.x % NPART, g = threadIdx.x / NPART;
+    if (g < ng) {
+        double v = 0.0;
+        int j = g;
+        for (; j + 3 * ng < n; j += 4 * ng) {   // four independent loads in flight, folded in slot order
+            const double a0 = __ldcg(part + (size_t)j * NPART + k);
+            const double a1 = __ldcg(part + (size_t)(j + ng) * NPART + k);
+            const double a2 = __ldcg(part + (size_t)(j + 2 * ng) * NPART + k);
+            const double a3 = __ldcg(part + (size_t)(j + 3 * ng) * NPART + k);
+            v = fold(k, fold(k, fold(k, fold(k, v, a0), a1), a2), a3);
+        }
+        for (; j < n; j += ng) v = fold(k, v, __ldcg(part + (size_t)j * NPART + k));
+        grp[g][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NPART) {
+        double v = grp[0][threadIdx.x];
+        for (int q = 1; q < ng; q++) v = fold(threadIdx.x, v, grp[q][threadIdx.x]);
+        out[threadIdx.x] = v;
+    }
+    __syncthreads();
+}
+
+// store this block's partial; true in the last block of the launch (which then folds)
+__device__ bool store_partial_last(Acc &acc, double *part, unsigned *counter) {
+    block_reduce_store(acc, part);
+    __shared__ bool last;
+    if (threadIdx.x < NPART) __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        if (threadIdx.x == 0) *counter = 0;   // ready for the next launch
+    }
+    return last;
+}
+
+__device__ void finalize_status(const Dev &d, const double *rec);
+
+// last block of the iteration: fold the three records (fixed order) -> S8 record -> S9
+__device__ void final_fold(const Dev &d) {
+    __shared__ double fin[NPART];
+    if (threadIdx.x < NPART) {
+        const int k = threadIdx.x;
+        double v = __ldcg(d.rec_part + k);
+        for (int r = 1; r < NRK; r++) v = fold(k, v, __ldcg(d.rec_part + r * NPART + k));
+        fin[k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double rec[NREC];
+        rec[R_RZ2] = fin[P_RZ2];
+        rec[R_Z2] = fin[P_Z2];
+        rec[R_OBJ] = fin[P_OBJ];
+        for (int q = 0; q < 4; q++) rec[R_C0 + q] = (double)__ldcg(d.cnt + q);
+        rec[R_PINF] = fin[P_PINF];
+        rec[R_RZINF] = fin[P_RZINF];
+        rec[R_ZINF] = fin[P_ZINF];
+        rec[R_DINF] = fin[P_DINF];
+        rec[R_BAD] = fin[P_BAD];
+        d.cnt[0] = d.cnt[1] = d.cnt[2] = d.cnt[3] = 0;
+        d.alq_cnt[0] = 0;
+        d.alq_cnt[1] = 0;
+        if (d.nranks > 1) {
+            for (int q = 0; q < NREC; q++) d.rec[q] = rec[q];   // cross-rank all-reduce, then k_finalize
+        } else {
+            finalize_status(d, rec);
+        }
+    }
+}
+
+__device__ __forceinline__ void kernel_tail(const Dev &d, Acc &acc, double *part, int kind, bool final) {
+    if (store_partial_last(acc, part, d.kdone + kind)) {
+        fold_slots(part, gridDim.x, d.rec_part + kind * NPART);
+        if (final) {
+            __threadfence();
+            final_fold(d);
+        }
+    }
+}
+
 
 // ------------------------------------------------------------------------- (7d) bus
 // k_bus: one thread per (i,t) solves the bus 2x2 KKT system from the bus-side targets of its
@@ -98,27 +217,36 @@ constexpr int ROWS_THREADS = 128;
 // in canonical CSR order; writes the generator copies (and their rows GP, GQ, RC_{t+1}),
 // wbar, thbar and (muP, muQ, dwbar, dthbar) for k_rows.
 //
-// Two launches per iteration: early (late = 0) for the bus-periods with no thermal-AL solve at an
+// Split: k_bus (early) takes the bus-periods with no thermal-AL solve at an
 // incident branch end -- their inputs are final after the fast path, so in the single-GPU graph
-// this runs in the shadow of k_branch_al -- and late (late = 1) for the marked ones.
-__global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d, int late) {
-    if (d.st->done) return;
+// it runs in the shadow of k_branch_al -- and k_late the marked ones after the AL tail.
+struct Ctl {
+    double rpq, rva, beta, beta_lam, lmax;
+    int pending;
+    unsigned stamp;
+    __device__ explicit Ctl(const Dev &d)
+        : rpq(d.rpq), rva(d.rva), beta(d.st->beta), beta_lam(d.st->beta_lam), lmax(d.lambda_max),
+          pending(d.st->pending_outer), stamp(mark_stamp(d)) {}
+};
+
+// bus-period k = i*T + t of an owned bus (ghost buses are solved by their owner)
+__device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc &acc) {
     const int T = d.T;
-    const size_t GT = (size_t)d.G * T, LT = (size_t)d.L * T, BT = (size_t)d.B * T;
+    const size_t GT = (size_t)d.G * T, BT = (size_t)d.B * T;
     const size_t LTH = (size_t)(d.L + d.Lph) * T;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const double rpq = d.rpq, rva = d.rva;
-    const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
-    const int pending = d.st->pending_outer;
-    Acc acc;
-    if (k < d.B_own * T && (d.bmark[k] == mark_stamp(d)) == (late != 0)) {
-        // owned buses only; ghost buses are solved by their owner
+    const double rpq = c.rpq, rva = c.rva;
+    const double beta = c.beta, beta_lam = c.beta_lam, lmax = c.lmax;
+    const int pending = c.pending;
+    {
         const int i = k / T, t = k - i * T;
         const int g0 = d.bg_ptr[i], g1 = d.bg_ptr[i + 1];
         const int e0 = d.be_ptr[i], e1 = d.be_ptr[i + 1];
         const int ne = e1 - e0;
         // ---- sums of the 2x2 KKT system, canonical order (gens, ends, wbar)
         double AP = 0.0, AQ = 0.0, C = 0.0, rP = d.pd[k], rQ = d.qd[k];
+        const double wbo = d.wbar[k], tbo = d.thbar[k];
+        // (loops unrolled so the loads of several gens / ends are in flight together)
+#pragma unroll 2
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
             const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) / rpq;
@@ -138,6 +266,7 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d, int late) {
             rQ = rQ - thq;
         }
         double wsum = 0.0, tsum = 0.0;
+#pragma unroll 4
         for (int a = e0; a < e1; a++) {
             const int code = d.be_idx[a];
             const int l = code >> 1, side = code & 1;
@@ -163,13 +292,24 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d, int late) {
         const double det = AP * AQ - C * C;
         const double muP = (rP * AQ - C * rQ) / det;
         const double muQ = (AP * rQ - C * rP) / det;
-        // ---- generator copies and their rows
+        // ---- generator copies and their rows (each gen: all loads, then the updates, then the stores)
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
-            const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) / rpq;
+            const bool rc = t < T - 1;
+            const double pg = d.p[gi], qg = d.q[gi], pbo = d.pbar[gi], qbo = d.qbar[gi];
+            double zp = ZG(G_GP, gi), yp = YG(G_GP, gi), lp = LG(G_GP, gi);
+            double zq = ZG(G_GQ, gi), yq = YG(G_GQ, gi), lq = LG(G_GQ, gi);
+            double phn = 0.0, zr = 0.0, yr = 0.0, lr = 0.0;
+            if (rc) {
+                phn = d.ph[gi + 1];
+                zr = ZG(G_RC, gi + 1);
+                yr = YG(G_RC, gi + 1);
+                lr = LG(G_RC, gi + 1);
+            }
+            const double tgp = pg + zp + yp / rpq;
             double th, aa;
-            if (t < T - 1) {
-                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) / rpq;
+            if (rc) {
+                const double trc = phn + zr + yr / rpq;
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
             } else {
@@ -177,22 +317,29 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d, int late) {
                 aa = rpq;
             }
             const double pb = th + muP / aa;
-            const double thq = d.q[gi] + ZG(G_GQ, gi) + YG(G_GQ, gi) / rpq;
+            const double thq = qg + zq + yq / rpq;
             const double qb = thq + muQ / rpq;
-            const double pbo = d.pbar[gi], qbo = d.qbar[gi];
+            zy_vals(pg - pb, rpq, beta, zp, yp, lp, pending, beta_lam, lmax, pb - pbo, acc);
+            zy_vals(qg - qb, rpq, beta, zq, yq, lq, pending, beta_lam, lmax, qb - qbo, acc);
+            if (rc) zy_vals(phn - pb, rpq, beta, zr, yr, lr, pending, beta_lam, lmax, pb - pbo, acc);
             d.pbar[gi] = pb;
             d.qbar[gi] = qb;
-            zy_row(d.p[gi] - pb, rpq, beta, &ZG(G_GP, gi), &YG(G_GP, gi), &LG(G_GP, gi), pending, beta_lam, lmax,
-                   pb - pbo, acc);
-            zy_row(d.q[gi] - qb, rpq, beta, &ZG(G_GQ, gi), &YG(G_GQ, gi), &LG(G_GQ, gi), pending, beta_lam, lmax,
-                   qb - qbo, acc);
-            if (t < T - 1)
-                zy_row(d.ph[gi + 1] - pb, rpq, beta, &ZG(G_RC, gi + 1), &YG(G_RC, gi + 1), &LG(G_RC, gi + 1),
-                       pending, beta_lam, lmax, pb - pbo, acc);
+            ZG(G_GP, gi) = zp;
+            YG(G_GP, gi) = yp;
+            ZG(G_GQ, gi) = zq;
+            YG(G_GQ, gi) = yq;
+            if (pending) {
+                LG(G_GP, gi) = lp;
+                LG(G_GQ, gi) = lq;
+            }
+            if (rc) {
+                ZG(G_RC, gi + 1) = zr;
+                YG(G_RC, gi + 1) = yr;
+                if (pending) LG(G_RC, gi + 1) = lr;
+            }
         }
         const double wb = thw + (alw * muP + bew * muQ) / aw;
         const double tb = (i == d.ref_bus) ? 0.0 : tsum / (double)ne;
-        const double wbo = d.wbar[k], tbo = d.thbar[k];
         d.wbar[k] = wb;
         d.thbar[k] = tb;
         d.bmu[0 * BT + k] = muP;
@@ -200,53 +347,132 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d, int late) {
         d.bmu[2 * BT + k] = wb - wbo;
         d.bmu[3 * BT + k] = tb - tbo;
     }
-    block_reduce_store(acc, late ? d.part_bus2 : d.part_bus);
-    (void)LT;
 }
 
-// k_rows: one thread per (l,t) finishes step (7d) for the two ends of branch l (flow copies
-// fbar = tauhat - mu/rho_pq) and runs (7e)/(7f) for its 8 rows.  Same (l,t) mapping and
-// coalescing as k_branch.
-// Early / late launches as for k_bus: a branch-period is late if either end bus is marked.
-__global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d, int late) {
+__global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     if (d.st->done) return;
+    const Ctl c(d);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    Acc acc;
+    if (k < d.B_own * d.T && d.bmark[k] != c.stamp) bus_solve(d, c, k, acc);
+    block_reduce_store(acc, d.part_bus);
+}
+
+// The four rows of branch end (l, side) at period t -- flow copies fbar = tauhat - mu/rho_pq,
+// then (7e)/(7f) for FP, FQ, W, A of that end -- need only that end's bus result.
+__device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int t, int side, Acc &acc) {
     const int T = d.T;
     const size_t LT = (size_t)d.L * T, BT = (size_t)d.B * T;
     const size_t LTH = (size_t)(d.L + d.Lph) * T;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const double rpq = d.rpq, rva = d.rva;
-    const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
-    const int pending = d.st->pending_outer;
-    Acc acc;
-    const int l = k / T, t = k - l * T;
-    const unsigned stamp = mark_stamp(d);
-    if (k < d.L * T && (d.bmark[(size_t)d.bfrom[l] * T + t] == stamp || d.bmark[(size_t)d.bto[l] * T + t] == stamp) ==
-                           (late != 0)) {
+    const size_t k = (size_t)l * T + t;
+    const int bus = side ? d.bto[l] : d.bfrom[l];
+    const size_t bk = (size_t)bus * T + t;
+    const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
+    const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
+    const int rows[4] = {kp, kq, kw, ka};
+    // every load first (no store in between: one round of memory latency, not four)
+    const double muP = d.bmu[0 * BT + bk], muQ = d.bmu[1 * BT + bk];
+    const double dwb = d.bmu[2 * BT + bk], dtb = d.bmu[3 * BT + bk];
+    const double wb = d.wbar[bk], tb = d.thbar[bk];
+    const double thp = TH(kp, k), thq = TH(kq, k), pbo = FB(kp, k), qbo = FB(kq, k);
+    const double fp = FX(kp, k), fq = FX(kq, k), xw = XX(side ? 1 : 0, k), xa = XX(side ? 3 : 2, k);
+    double z[4], y[4], lam[4];
 #pragma unroll
-        for (int side = 0; side < 2; side++) {
-            const int bus = side ? d.bto[l] : d.bfrom[l];
-            const size_t bk = (size_t)bus * T + t;
-            const double muP = d.bmu[0 * BT + bk], muQ = d.bmu[1 * BT + bk];
-            const double dwb = d.bmu[2 * BT + bk], dtb = d.bmu[3 * BT + bk];
-            const double wb = d.wbar[bk], tb = d.thbar[bk];
-            const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
-            const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
-            const double pb = TH(kp, k) + (-muP) / rpq;
-            const double qb = TH(kq, k) + (-muQ) / rpq;
-            const double pbo = FB(kp, k), qbo = FB(kq, k);
-            FB(kp, k) = pb;
-            FB(kq, k) = qb;
-            zy_row(FX(kp, k) - pb, rpq, beta, &ZB(kp, k), &YB(kp, k), &LB(kp, k), pending, beta_lam, lmax, pb - pbo, acc);
-            zy_row(FX(kq, k) - qb, rpq, beta, &ZB(kq, k), &YB(kq, k), &LB(kq, k), pending, beta_lam, lmax, qb - qbo, acc);
-            zy_row(XX(side ? 1 : 0, k) - wb, rva, beta, &ZB(kw, k), &YB(kw, k), &LB(kw, k), pending, beta_lam, lmax, dwb,
-                   acc);
-            zy_row(XX(side ? 3 : 2, k) - tb, rva, beta, &ZB(ka, k), &YB(ka, k), &LB(ka, k), pending, beta_lam, lmax, dtb,
-                   acc);
-        }
+    for (int r = 0; r < 4; r++) {
+        z[r] = ZB(rows[r], k);
+        y[r] = YB(rows[r], k);
+        lam[r] = LB(rows[r], k);
     }
-    block_reduce_store(acc, late ? d.part_rows2 : d.part_rows);
+    const double pb = thp + (-muP) / c.rpq;
+    const double qb = thq + (-muQ) / c.rpq;
+    zy_vals(fp - pb, c.rpq, c.beta, z[0], y[0], lam[0], c.pending, c.beta_lam, c.lmax, pb - pbo, acc);
+    zy_vals(fq - qb, c.rpq, c.beta, z[1], y[1], lam[1], c.pending, c.beta_lam, c.lmax, qb - qbo, acc);
+    zy_vals(xw - wb, c.rva, c.beta, z[2], y[2], lam[2], c.pending, c.beta_lam, c.lmax, dwb, acc);
+    zy_vals(xa - tb, c.rva, c.beta, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
+    FB(kp, k) = pb;
+    FB(kq, k) = qb;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        ZB(rows[r], k) = z[r];
+        YB(rows[r], k) = y[r];
+        if (c.pending) LB(rows[r], k) = lam[r];
+    }
+    (void)LTH;
+    (void)LT;
 }
 
+// k_rows (early): one thread per (l,t), the ends whose bus is not marked (coalesced row
+// arrays, as k_branch); the marked ends are done by k_rows_late.
+__global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
+    if (d.st->done) return;
+    const Ctl c(d);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    Acc acc;
+    if (k < d.L * d.T) {
+        const int l = k / d.T, t = k - l * d.T;
+        if (d.rmark[0][k] != c.stamp) end_rows(d, c, l, t, 0, acc);
+        if (d.rmark[1][k] != c.stamp) end_rows(d, c, l, t, 1, acc);
+    }
+    block_reduce_store(acc, d.part_rows);
+}
+
+// Late phase (after the AL tail): k_bus_late solves the marked bus-periods, k_rows_late updates
+// the marked ends (1024-thread blocks: few partial slots, so the final fold is short).
+// Single GPU: k_rows_late is the last kernel of the iteration (final = 1).
+__global__ void __launch_bounds__(LATE_THREADS) k_bus_late(Dev d) {
+    if (d.st->done) return;
+    const Ctl c(d);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    Acc acc;
+    if (k < d.B_own * d.T && d.bmark[k] == c.stamp) bus_solve(d, c, k, acc);
+    kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, false);
+}
+
+// k_fold_early: the block partials of k_bus, k_ubar and k_rows (in that order) -> rec_part[RK_EARLY]
+constexpr int FOLD_BLOCKS = 64, FOLD_THREADS = 256;
+__global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
+    if (d.st->done) return;
+    const int nb = d.nblk_bus, nu = d.nblk_ubar, nr = d.nblk_rows, n = nb + nu + nr;
+    const int chunk = (n + FOLD_BLOCKS - 1) / FOLD_BLOCKS;
+    const int j0 = min(n, (int)blockIdx.x * chunk), j1 = min(n, j0 + chunk);
+    __shared__ double grp[FOLD_THREADS / NPART][NPART];
+    const int k = threadIdx.x % NPART, g = threadIdx.x / NPART, ng = FOLD_THREADS / NPART;
+    double v = 0.0;
+    for (int j = j0 + g; j < j1; j += ng) {
+        const double *p = j < nb ? d.part_bus + (size_t)j * NPART
+                        : j < nb + nu ? d.part_ubar + (size_t)(j - nb) * NPART : d.part_rows + (size_t)(j - nb - nu) * NPART;
+        v = fold(k, v, __ldcg(p + k));
+    }
+    grp[g][k] = v;
+    __syncthreads();
+    if (threadIdx.x < NPART) {
+        double w = grp[0][threadIdx.x];
+        for (int q = 1; q < ng; q++) w = fold(threadIdx.x, w, grp[q][threadIdx.x]);
+        d.part_efold[(size_t)blockIdx.x * NPART + threadIdx.x] = w;
+        __threadfence();
+    }
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(d.kdone + RK_EARLY, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) d.kdone[RK_EARLY] = 0;
+    fold_slots(d.part_efold, gridDim.x, d.rec_part + RK_EARLY * NPART);
+}
+
+__global__ void __launch_bounds__(LATE_THREADS) k_rows_late(Dev d, int final) {
+    if (d.st->done) return;
+    const Ctl c(d);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    Acc acc;
+    if (k < d.L * d.T) {
+        const int l = k / d.T, t = k - l * d.T;
+        if (d.rmark[0][k] == c.stamp) end_rows(d, c, l, t, 0, acc);
+        if (d.rmark[1][k] == c.stamp) end_rows(d, c, l, t, 1, acc);
+    }
+    kernel_tail(d, acc, d.part_lrows, RK_ROWS_LATE, final != 0);
+}
 
 // ------------------------------------------------------------------------- (7c) ubar
 __device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -460,7 +686,7 @@ __device__ void finalize_status(const Dev &d, const double *rec) {
     st->inner_total += 1;
     st->inner_since += 1;
     if ((rec[R_BAD] != 0.0 || !isfinite(rec[R_RZ2]) || !isfinite(rec[R_OBJ])) && st->err_kernel == 0) {
-        st->err_kernel = 1 + K_REDUCE;
+        st->err_kernel = 1 + K_ROWS_LATE;
         st->err_iter = (int)st->inner_total;
     }
     st->pending_outer = 0;
@@ -477,72 +703,6 @@ __device__ void finalize_status(const Dev &d, const double *rec) {
         }
     }
     if (st->stop_on_primal && st->primal_inf <= st->primal_target) st->done = 1;
-}
-
-constexpr int RED_THREADS = 1024;
-__global__ void __launch_bounds__(RED_THREADS) k_reduce(Dev d) {
-    if (d.st->done) return;
-    __shared__ double sw[RED_THREADS / 32][NPART];
-    __shared__ double sh[1][NPART];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double v[NPART];
-#pragma unroll
-    for (int k = 0; k < NPART; k++) v[k] = 0.0;
-    const int nb = d.nblk_bus, nu = d.nblk_ubar, nr = d.nblk_rows;
-    // partial slots in a fixed order: bus early, bus late, ubar, rows early, rows late
-    for (int b = tid; b < 2 * nb + nu + 2 * nr; b += RED_THREADS) {
-        const double *pp = b < nb ? d.part_bus + (size_t)b * NPART
-                         : b < 2 * nb ? d.part_bus2 + (size_t)(b - nb) * NPART
-                         : b < 2 * nb + nu ? d.part_ubar + (size_t)(b - 2 * nb) * NPART
-                         : b < 2 * nb + nu + nr ? d.part_rows + (size_t)(b - 2 * nb - nu) * NPART
-                                                : d.part_rows2 + (size_t)(b - 2 * nb - nu - nr) * NPART;
-#pragma unroll
-        for (int k = 0; k < NPART; k++) {
-            const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
-            v[k] = isum ? v[k] + pp[k] : fmax(v[k], pp[k]);
-        }
-    }
-    // fixed-shape tree: warp butterflies, then warp results in index order
-#pragma unroll
-    for (int k = 0; k < NPART; k++) {
-        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
-        double x = v[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double w = __shfl_down_sync(0xffffffffu, x, o);
-            x = isum ? x + w : fmax(x, w);
-        }
-        if (lane == 0) sw[warp][k] = x;
-    }
-    __syncthreads();
-    if (tid < NPART) {
-        const int k = tid;
-        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
-        double x = sw[0][k];
-        for (int w = 1; w < RED_THREADS / 32; w++) x = isum ? x + sw[w][k] : fmax(x, sw[w][k]);
-        sh[0][k] = x;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double rec[NREC];
-        rec[R_RZ2] = sh[0][P_RZ2];
-        rec[R_Z2] = sh[0][P_Z2];
-        rec[R_OBJ] = sh[0][P_OBJ];
-        for (int c = 0; c < 4; c++) rec[R_C0 + c] = (double)d.cnt[c];
-        rec[R_PINF] = sh[0][P_PINF];
-        rec[R_RZINF] = sh[0][P_RZINF];
-        rec[R_ZINF] = sh[0][P_ZINF];
-        rec[R_DINF] = sh[0][P_DINF];
-        rec[R_BAD] = sh[0][P_BAD];
-        d.cnt[0] = d.cnt[1] = d.cnt[2] = d.cnt[3] = 0;
-        d.alq_cnt[0] = 0;
-        d.alq_cnt[1] = 0;
-        if (d.nranks > 1) {
-            for (int c = 0; c < NREC; c++) d.rec[c] = rec[c];   // cross-rank all-reduce, then k_finalize
-        } else {
-            finalize_status(d, rec);
-        }
-    }
 }
 
 // S8/S9 on the (all-rank) reduction record
@@ -623,11 +783,16 @@ int nblk_bus(int B, int T) { return (B * T + BUS_THREADS - 1) / BUS_THREADS; }
 int nblk_ubar(int G, int T) { return (G * T + UBAR_THREADS - 1) / UBAR_THREADS; }
 int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; }
 
-void launch_bus(const Dev &d, cudaStream_t s, int late) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d, late); }
-void launch_rows(const Dev &d, cudaStream_t s, int late) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d, late); }
+void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d); }
+void launch_rows(const Dev &d, cudaStream_t s) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d); }
+void launch_bus_late(const Dev &d, cudaStream_t s) { k_bus_late<<<d.nblk_lbus, LATE_THREADS, 0, s>>>(d); }
+void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
+    k_rows_late<<<d.nblk_lrows, LATE_THREADS, 0, s>>>(d, final);
+}
+int nblk_late(int n) { return (n + LATE_THREADS - 1) / LATE_THREADS; }
+int fold_blocks() { return FOLD_BLOCKS; }
+void launch_fold_early(const Dev &d, cudaStream_t s) { k_fold_early<<<FOLD_BLOCKS, FOLD_THREADS, 0, s>>>(d); }
 void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
-void launch_reduce(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }
-void launch_reduce_part(const Dev &d, cudaStream_t s) { k_reduce<<<1, RED_THREADS, 0, s>>>(d); }
 void launch_finalize(const Dev &d, cudaStream_t s) { k_finalize<<<1, 32, 0, s>>>(d); }
 static int xgrid(int n) { return std::max(1, std::min(296, (n + 255) / 256)); }
 void launch_pack_tau(const Dev &d, cudaStream_t s) { k_pack_tau<<<xgrid(d.ncut * 4 * d.T), 256, 0, s>>>(d); }

@@ -473,9 +473,22 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ALLOC(part_bus, double, (size_t)d.nblk_bus * NPART);
     ALLOC(part_ubar, double, (size_t)d.nblk_ubar * NPART);
     ALLOC(part_rows, double, (size_t)d.nblk_rows * NPART);
-    ALLOC(part_bus2, double, (size_t)d.nblk_bus * NPART);
-    ALLOC(part_rows2, double, (size_t)d.nblk_rows * NPART);
+    d.nblk_lbus = nblk_late(P.Bo * T);
+    d.nblk_lrows = nblk_late(L * T);
+    ALLOC(part_lbus, double, (size_t)d.nblk_lbus * NPART);
+    ALLOC(part_lrows, double, (size_t)d.nblk_lrows * NPART);
+    ALLOC(part_efold, double, (size_t)fold_blocks() * NPART);
+    ALLOC(rec_part, double, 3 * NPART);
+    ALLOC(kdone, unsigned, 3);
     ALLOC(bmark, unsigned, BT);
+    {
+        auto r0 = dnew<unsigned>(ctx, (size_t)(L + P.Lp) * T, e);
+        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc rmark"));
+        auto r1 = dnew<unsigned>(ctx, (size_t)(L + P.Lp) * T, e);
+        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc rmark"));
+        d.rmark[0] = r0;
+        d.rmark[1] = r1;
+    }
     ALLOC(tauh, double, (size_t)NBROW * (L + P.Lp) * T);
     ALLOC(bmu, double, 4 * BT);
     ALLOC(cnt, unsigned long long, 4);
@@ -519,11 +532,11 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
 // ------------------------------------------------------------------------------------------
 // one inner iteration.  Dependency order (also the order of the eager, timed path):
 //   (7a) k_gen -> (7b) k_genx, k_branch -> (7d) k_bus, k_rows [early] -> (7b) k_branch_al
-//   -> (7d) k_bus, k_rows [late] -> (7c) k_ubar -> S8/S9.
+//   -> (7c) k_ubar -> k_late [(7d) late bus + rows, S8/S9].
 // The fast-path branch kernel marks the bus-periods touched by a thermal-AL solve; the bus
 // solve and row update of everything else only need the fast path and the generator x-update
 // (early phase), the marked ones wait for the AL tail (late phase).  In the single-GPU graph:
-//   s : k_branch ---------------------------> k_branch_al --------> [join] k_bus/k_rows late, k_reduce
+//   s : k_branch ---------------------------> k_branch_al --------> [join] k_late
 //   s2:           k_gen -> k_genx -> k_ubar ---------------------------^
 //   s3:                      `-> k_bus/k_rows early -------------------^
 // i.e. the early sweep (~90 % of the bus/row work) and the generator chain (which never reads a
@@ -533,8 +546,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
 // before the row update, the reduction record before the inner/outer decision; there both bus
 // phases run after the tauhat exchange and both row phases after the bus exchange.
 // ------------------------------------------------------------------------------------------
-static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BUS, K_ROWS, K_BRANCH_AL, K_BUS_LATE, K_ROWS_LATE,
-                                  K_UBAR, K_REDUCE};
+static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BUS, K_ROWS, K_BRANCH_AL, K_UBAR, K_FOLD,
+                                  K_BUS_LATE, K_ROWS_LATE};
 
 static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
     switch (k) {
@@ -542,12 +555,13 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
         case K_BRANCH_AL: launch_branch_al(ctx->d, s); break;
         case K_GEN: launch_gen(ctx->d, s); break;
         case K_GENX: launch_genx(ctx->d, s); break;
-        case K_BUS: launch_bus(ctx->d, s, 0); break;
-        case K_BUS_LATE: launch_bus(ctx->d, s, 1); break;
-        case K_ROWS: launch_rows(ctx->d, s, 0); break;
-        case K_ROWS_LATE: launch_rows(ctx->d, s, 1); break;
+        case K_BUS: launch_bus(ctx->d, s); break;
+        case K_ROWS: launch_rows(ctx->d, s); break;
+        case K_BUS_LATE: launch_bus_late(ctx->d, s); break;
+        case K_ROWS_LATE: launch_rows_late(ctx->d, s, 1); break;
+        case K_FOLD: launch_fold_early(ctx->d, s); break;
         case K_UBAR: launch_ubar(ctx->d, s); break;
-        default: launch_reduce(ctx->d, s); break;
+        default: break;
     }
 }
 
@@ -564,10 +578,14 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         cudaStreamWaitEvent(ctx->s3, ctx->ev_genx, 0);
         launch_kernel(ctx, K_BUS, ctx->s3);
         launch_kernel(ctx, K_ROWS, ctx->s3);
-        cudaEventRecord(ctx->ev_early, ctx->s3);
     }
     launch_kernel(ctx, K_UBAR, ctx->s2);
     cudaEventRecord(ctx->ev_join, ctx->s2);
+    if (!multi) {   // fold the early partials in the shadow of the AL tail
+        cudaStreamWaitEvent(ctx->s3, ctx->ev_join, 0);
+        launch_kernel(ctx, K_FOLD, ctx->s3);
+        cudaEventRecord(ctx->ev_early, ctx->s3);
+    }
     launch_kernel(ctx, K_BRANCH_AL, ctx->s);
     if (multi && d.max_cut > 0) {
         launch_pack_tau(d, ctx->s);
@@ -576,10 +594,9 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     }
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
     if (!multi) {
-        cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_BUS_LATE, ctx->s);
+        cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_ROWS_LATE, ctx->s);
-        launch_kernel(ctx, K_REDUCE, ctx->s);
         return;
     }
     launch_kernel(ctx, K_BUS, ctx->s);
@@ -590,8 +607,8 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         launch_unpack_bus(d, ctx->s);
     }
     launch_kernel(ctx, K_ROWS, ctx->s);
+    launch_kernel(ctx, K_FOLD, ctx->s);
     launch_kernel(ctx, K_ROWS_LATE, ctx->s);
-    launch_reduce_part(d, ctx->s);
     ncclGroupStart();
     ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, ctx->s);
     ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, ctx->s);
@@ -720,9 +737,8 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
             ucac_ctx *c = ctxs[r];
             if (c->d.max_export > 0) launch_unpack_bus(c->d, c->s);
             launch_kernel(c, K_ROWS, c->s);
+            launch_kernel(c, K_FOLD, c->s);
             launch_kernel(c, K_ROWS_LATE, c->s);
-            if (n > 1) launch_reduce_part(c->d, c->s);
-            else launch_kernel(c, K_REDUCE, c->s);
         }
         CK(sync_all());
         if (n > 1) {
@@ -745,8 +761,8 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
     return UCAC_OK;
 }
 
-static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows",
-                                    "k_genx", "k_bus_late", "k_rows_late"};
+static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_bus_late", "k_branch_al", "k_rows",
+                                    "k_genx", "k_rows_late", "k_fold_early"};
 extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
 
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
@@ -1024,13 +1040,14 @@ extern "C" ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz) {
     sz->alg_bytes[K_ROWS] = LT * 72 * 8;
     // k_ubar: per gen-period: read u p q ph ubar(3) z,y,lambda of 9 rows (27); write ubar(3) z,y (18)
     sz->alg_bytes[K_UBAR] = GT * (51 * 8 + 1);
-    sz->alg_bytes[K_REDUCE] = (int64_t)(2 * ctx->d.nblk_bus + ctx->d.nblk_ubar + 2 * ctx->d.nblk_rows) * NPART * 8;
-    // the early/late split of k_bus and k_rows is data-dependent: their figures above cover both
-    // launches (plus the marks, 4 B per bus-period and 8 B per branch-period per launch)
-    sz->alg_bytes[K_BUS] += 2 * BT * 4;
-    sz->alg_bytes[K_ROWS] += 2 * LT * 8;
-    sz->alg_bytes[K_BUS_LATE] = 0;
-    sz->alg_bytes[K_ROWS_LATE] = 0;
+    // the early/late split of the bus solve and row update is data-dependent: the k_bus and k_rows
+    // figures above cover all bus- and branch-periods (plus the marks they read); the late
+    // kernels are charged only their own scan of the marks
+    sz->alg_bytes[K_BUS] += BT * 4;
+    sz->alg_bytes[K_ROWS] += 2 * LT * 4;
+    sz->alg_bytes[K_BUS_LATE] = BT * 4;
+    sz->alg_bytes[K_ROWS_LATE] = 2 * LT * 4;
+    sz->alg_bytes[K_FOLD] = (int64_t)(ctx->d.nblk_bus + ctx->d.nblk_ubar + ctx->d.nblk_rows) * NPART * 8;
     sz->alg_bytes[K_BRANCH_AL] = 0;  // data-dependent: 49 doubles per queued (l,t)
     int64_t tot = 0;
     for (int k = 0; k < NKERN; k++) tot += sz->alg_bytes[k];

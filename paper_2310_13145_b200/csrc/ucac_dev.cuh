@@ -16,8 +16,8 @@ enum GenRow { G_DON = 0, G_DSU, G_DSD, G_PL, G_PU, G_QL, G_QU, G_RD, G_RU, G_GP,
 enum BrRow { B_FPIJ = 0, B_FQIJ, B_FPJI, B_FQJI, B_WI, B_WJ, B_AI, B_AJ, NBROW };
 
 // kernel ids (ucac_kernel_name)
-enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_REDUCE = 4, K_BRANCH_AL = 5, K_ROWS = 6,
-                K_GENX = 7, K_BUS_LATE = 8, K_ROWS_LATE = 9, NKERN = 10 };
+enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_BUS_LATE = 4, K_BRANCH_AL = 5, K_ROWS = 6,
+                K_GENX = 7, K_ROWS_LATE = 8, K_FOLD = 9, NKERN = 10 };
 
 // per-block reduction record (S8): max |r|, max |r+z|, sum (r+z)^2, max |z|, sum z^2,
 // max rho |dxbar|, objective, non-finite flag
@@ -97,8 +97,13 @@ struct Dev {
     double *part_rows;                // [nblk_rows][NPART]
     int *alq;                         // [L*T] queue of thermal-active solves (phase 2)
     unsigned *bmark;                  // [B*T] = stamp(iteration) if an incident (l,t) is queued:
-                                      // its bus solve and rows wait for the AL tail (late phase)
-    double *part_bus2, *part_rows2;   // late-phase block partials (same shapes)
+                                      // its bus solve waits for the AL tail (k_bus_late)
+    unsigned *rmark[2];               // [(L+Lph)*T] per side: = stamp if that end's bus is marked
+    int nblk_lbus, nblk_lrows;        // late-phase grids (1024-thread blocks)
+    double *part_lbus, *part_lrows;   // their block partials
+    double *part_efold;               // [fold_blocks()][NPART] first-level fold of the early partials
+    double *rec_part;                 // [3][NPART] folded records: early, bus late, rows late
+    unsigned *kdone;                  // [3] last-block counters of the kernels producing them
     unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
     DevStatus *st;
 };
@@ -115,18 +120,21 @@ void launch_branch(const Dev &d, cudaStream_t s);
 void launch_branch_al(const Dev &d, cudaStream_t s);
 void launch_gen(const Dev &d, cudaStream_t s);
 void launch_genx(const Dev &d, cudaStream_t s);
-void launch_bus(const Dev &d, cudaStream_t s, int late);
-void launch_rows(const Dev &d, cudaStream_t s, int late);
+void launch_bus(const Dev &d, cudaStream_t s);
+void launch_rows(const Dev &d, cudaStream_t s);
+void launch_bus_late(const Dev &d, cudaStream_t s);
+void launch_rows_late(const Dev &d, cudaStream_t s, int final);
+int nblk_late(int n);
+int fold_blocks();
+void launch_fold_early(const Dev &d, cudaStream_t s);
 int nblk_rows(int L, int T);
 // multi-rank
-void launch_reduce_part(const Dev &d, cudaStream_t s);
 void launch_finalize(const Dev &d, cudaStream_t s);
 void launch_pack_tau(const Dev &d, cudaStream_t s);
 void launch_unpack_tau(const Dev &d, cudaStream_t s);
 void launch_pack_bus(const Dev &d, cudaStream_t s);
 void launch_unpack_bus(const Dev &d, cudaStream_t s);
 void launch_ubar(const Dev &d, cudaStream_t s);
-void launch_reduce(const Dev &d, cudaStream_t s);
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s);
 void launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                      const int *hold, int8_t *sched, double *cost, cudaStream_t s);

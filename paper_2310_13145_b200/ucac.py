@@ -21,8 +21,8 @@ i8p = C.POINTER(C.c_int8)
 i64p = C.POINTER(C.c_int64)
 
 NKERNELS = 10
-KERNELS = ["k_branch", "k_gen", "k_bus", "k_ubar", "k_reduce", "k_branch_al", "k_rows", "k_genx", "k_bus_late",
-           "k_rows_late"]
+KERNELS = ["k_branch", "k_gen", "k_bus", "k_ubar", "k_bus_late", "k_branch_al", "k_rows", "k_genx", "k_rows_late",
+           "k_fold_early"]
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ENUMERIC", 6: "ESTATE", 7: "EUNSUPPORTED"}
 
 
