@@ -19,6 +19,12 @@
 // algorithm independently (oracle/oracle.c) with a straightforward evaluation.
 #include "ucac_dev.cuh"
 
+// Subspace step of TRON for N <= UCAC_TRON_DIRECT_MAXN variables: LDL^T Newton step when H_FF is
+// positive definite and the step is interior, else Steihaug-Toint CG.
+#ifndef UCAC_TRON_DIRECT_MAXN
+#define UCAC_TRON_DIRECT_MAXN 4
+#endif
+
 namespace ucac {
 namespace {
 
@@ -342,6 +348,47 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
     return true;
 }
 
+// Newton step on the free set F by an LDL^T factorisation of H_FF (fixed rows/columns
+// replaced by the identity).  Returns false if H_FF is not positive definite.
+template <int N>
+__device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr, const double *r, double *w) {
+    double Lm[N][N], D[N];
+    bool pd = true;
+#pragma unroll
+    for (int j = 0; j < N; j++) {
+        double dj = fr[j] ? H[j][j] : 1.0;
+#pragma unroll
+        for (int k = 0; k < j; k++) dj -= Lm[j][k] * Lm[j][k] * D[k];
+        pd = pd && dj > 0.0;
+        D[j] = dj;
+        const double inv = 1.0 / dj;
+#pragma unroll
+        for (int i = j + 1; i < N; i++) {
+            double v = (fr[i] && fr[j]) ? H[i][j] : 0.0;
+#pragma unroll
+            for (int k = 0; k < j; k++) v -= Lm[i][k] * Lm[j][k] * D[k];
+            Lm[i][j] = v * inv;
+        }
+    }
+    if (!pd) return false;
+    double z[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        double v = r[i];
+#pragma unroll
+        for (int k = 0; k < i; k++) v -= Lm[i][k] * z[k];
+        z[i] = v;
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; i--) {
+        double v = z[i] / D[i];
+#pragma unroll
+        for (int k = i + 1; k < N; k++) v -= Lm[k][i] * w[k];
+        w[i] = fr[i] ? v : 0.0;
+    }
+    return true;
+}
+
 // Projected trust-region Newton.  Returns true when ||P(x-g)-x||_inf <= gtol.
 template <int N, class Fun>
 __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *hi, double gtol,
@@ -420,7 +467,21 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                 p[i] = r[i];
             }
             double rr = dotn<N>(r, r);
-            if (rr != 0.0) {
+            bool direct = false;
+            if (rr != 0.0 && N <= UCAC_TRON_DIRECT_MAXN) {
+                // the point CG converges to, when it is interior: the Newton step on the free set
+                if (newton_free<N>(H, fr, r, w)) {
+                    double t[N];
+#pragma unroll
+                    for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
+                    direct = dotn<N>(t, t) < delta * delta;
+                }
+                if (!direct) {
+#pragma unroll
+                    for (int i = 0; i < N; i++) w[i] = 0.0;
+                }
+            }
+            if (rr != 0.0 && !direct) {
                 double tol2 = TR_CGTOL * TR_CGTOL * rr;
                 for (int k = 0; k < N; k++) {
                     double Hp[N], t[N];
