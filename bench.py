@@ -29,10 +29,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ADMM iters/sec & branch-subproblem solves/sec; time-to-residual 1e-4, 1/2/4/8 B200"
 UNIT = "ADMM inner iterations/s"
-# FP64 flops per TRON Newton iteration of k_branch, from the ncu SASS instruction counts
-# (DFMA = 2, DADD/DMUL = 1) divided by the Newton iterations the kernel reported for the same
-# launch -- profiles/r01_branch_flops.md.  Used for the FP64 roofline of the branch kernel.
-FLOPS_PER_NEWTON_ITER = 1450.0
+# FP64 flops per TRON Newton iteration of the two branch kernels: lane-level SASS counts of the
+# same launches (2 DFMA + DADD + DMUL) / the Newton iterations the solver counted in them
+# (tools/calibrate_flops.py; profiles/r01/flops_calibration.json).  The AL figure includes the
+# per-round work (Hessian at the round start, multiplier update) amortised over its iterations.
+FLOPS_PER_NEWTON_FAST = 1350.0
+FLOPS_PER_NEWTON_AL = 3034.0
 
 
 def measured_peaks():
@@ -49,49 +51,80 @@ def fp64_peak_tflops(sm_mhz: float) -> float:
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML polled every
+    millisecond from a thread (the timed region lasts tens of ms, shorter than nvidia-smi's own
+    start-up), nvidia-smi -lms 100 if NVML is unavailable."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []          # (sm_mhz, max_mhz, reason mask)
+        self.stop = threading.Event()
+        self.t = None
+        self.src = "none"
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def loop():
+                while not self.stop.is_set():
+                    try:
+                        self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, get_reasons(h)))
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+            self.src = "nvml"
+            self.t = threading.Thread(target=loop, daemon=True)
             self.t.start()
+            time.sleep(0.005)
         except Exception:
-            self.proc = None
+            self._smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+    def _smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_power_cap,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+        try:
+            proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}",
+                                     "--format=csv,noheader,nounits", "-lms", "100"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        self.src = "nvidia-smi"
+        bits = [0x8, 0x4, 0x40, 0x20]
+
+        def read():
+            for line in proc.stdout:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 6 and p[0].replace(".", "").isdigit():
+                    mask = sum(b for b, v in zip(bits, p[2:6]) if v.lower() == "active")
+                    self.rows.append((float(p[0]), float(p[1]), mask))
+                if self.stop.is_set():
+                    break
+            proc.terminate()
+        self.t = threading.Thread(target=read, daemon=True)
+        self.t.start()
+        time.sleep(1.0)   # nvidia-smi start-up
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=5)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0,
+                    "source": self.src}
+        reasons = sorted({n for _, _, m in self.rows for b, n in self.REASONS.items() if m & b})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": self.src}
 
 
 def oracle_sample(pb, pr, steps: int, budget_s: float):
@@ -152,7 +185,7 @@ def problem_bytes(pb) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ucac", choices=["ucac", "reference"])
     ap.add_argument("--config", default="pegase2869")
@@ -238,37 +271,40 @@ def main():
     clocks = clk.summary()
 
     # ---- per-kernel device times (same kernels launched eagerly with an event pair each), 1 GPU
-    roofline, sweep, kms = None, None, None
+    roofline, kernels, kms = None, None, None
     if world == 1:
         kms, klaunch = ctx.iterate_timed(args.steps)
         rep2 = ctx.report()
-        newton_timed = rep2["tron_iters"] - rep1["tron_iters"]
+        n_al = rep2["al_tron_iters"] - rep1["al_tron_iters"]
+        n_fast = rep2["tron_iters"] - rep1["tron_iters"] - n_al
         ksum = sum(kms.values())
-        dom = max(kms, key=kms.get)
-        if dom in ("k_branch", "k_branch_al"):
-            flops = newton_timed * FLOPS_PER_NEWTON_ITER
-            kt = kms["k_branch"] + kms["k_branch_al"]
-            achieved = flops / (kt * 1e-3) / 1e12
-            peak = fp64_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
-            roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                        "traffic": None, "kernel": "k_branch+k_branch_al",
-                        "peak_note": "FP64 non-tensor: 148 SM x 64 DFMA/clk x 2 at sm_max_mhz from MEASURED_PEAKS.json "
-                                     "(derived, DESIGN.md 8); flops = Newton iterations x FLOPS_PER_NEWTON_ITER",
-                        "share_of_step": kt / ksum, "kernel_ms_per_step": kt / args.steps}
-        else:
-            bytes_ = sizes["alg_bytes"][dom] * args.steps
-            achieved = bytes_ / (kms[dom] * 1e-3) / 1e9
-            peak = peaks.get("hbm_gbs", 6650.0)
-            roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                        "traffic": None, "kernel": dom, "share_of_step": kms[dom] / ksum,
-                        "kernel_ms_per_step": kms[dom] / args.steps}
-        sweep = {}
-        for k in ("k_bus", "k_rows", "k_ubar", "k_genx", "k_gen"):
-            b = sizes["alg_bytes"][k] * args.steps
+        fp64 = fp64_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        fp64_note = ("FP64 non-tensor peak derived: 148 SM x 64 DFMA lanes/clk x 2 flop at sm_max_mhz of "
+                     "MEASURED_PEAKS.json (DESIGN.md 8)")
+        kernels = {}
+        for k, n, fpn in (("k_branch", n_fast, FLOPS_PER_NEWTON_FAST), ("k_branch_al", n_al, FLOPS_PER_NEWTON_AL)):
+            a_ = n * fpn / (kms[k] * 1e-3) / 1e12
+            kernels[k] = {"bound": "alu", "achieved": a_, "peak": fp64, "unit": "TFLOP/s", "frac": a_ / fp64,
+                          "newton_iters_per_step": n / args.steps, "flops_per_newton": fpn,
+                          "ms_per_step": kms[k] / args.steps, "share_of_step": kms[k] / ksum}
+        for k in ("k_rows", "k_bus", "k_ubar", "k_genx", "k_gen"):
             t = kms[k] + kms.get(k + "_late", 0.0)       # early + late launches
-            gbs = b / (t * 1e-3) / 1e9
-            sweep[k] = {"alg_GBps": gbs, "frac_hbm": gbs / peaks.get("hbm_gbs", 6650.0),
-                        "ms_per_step": t / args.steps}
+            gbs = sizes["alg_bytes"][k] * args.steps / (t * 1e-3) / 1e9
+            kernels[k + ("+late" if k + "_late" in kms else "")] = {
+                "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                "ms_per_step": t / args.steps, "share_of_step": t / ksum}
+        dom = max(("k_branch", "k_branch_al"), key=lambda k: kms[k])
+        if max(kms, key=kms.get) == dom:
+            roofline = dict(kernels[dom], kernel=dom, traffic=None,
+                            peak_note=fp64_note + "; flops = the kernel's Newton iterations (live counter) x "
+                                      "its FP64 flops per Newton iteration (ncu SASS count, tools/calibrate_flops.py)")
+        else:
+            dom = max(kms, key=kms.get)
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": sizes["alg_bytes"][dom] * args.steps /
+                        (kms[dom] * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s", "traffic": None,
+                        "ms_per_step": kms[dom] / args.steps, "share_of_step": kms[dom] / ksum}
+            roofline["frac"] = roofline["achieved"] / hbm
 
     # ---- e2e: the public API from host buffers (create = H2D of the problem, iterate,
     #      residuals + solution = D2H), per step = one inner iteration, max over ranks
@@ -313,7 +349,7 @@ def main():
                                       for k in ("tron_capped", "al_active", "al_capped")},
             "primal_inf": rep1["primal_inf"],
             "roofline": roofline,
-            "sweep_kernels": sweep,
+            "kernels": kernels,
             "kernel_ms_per_step": {k: v_ / args.steps for k, v_ in kms.items()} if kms else None,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -169,6 +169,7 @@ const char *ucac_kernel_name(int32_t k);
 typedef struct {
     double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective, beta;
     int64_t inner_total, outer_total, tron_iters, tron_capped, al_active, al_capped;
+    int64_t al_tron_iters;            /* TRON iterations inside thermal-AL solves (part of tron_iters) */
     int32_t inner_since_outer, outer_k;
     int32_t err_kernel, err_iter;     /* first non-finite: kernel id + 1 (0 = none), iteration */
 } ucac_report;

@@ -715,7 +715,7 @@ static void br_eval(void *vc, const double *X, double *fo, double *g, double *H)
  * Returns 0 (caller keeps the first-order update) if H_FF or M is not positive definite. */
 #define AL_NEWTON_C 10.0
 static int al_newton_dmu(bctx *c, const double *X, const double *lo, const double *hi,
-                         const double *h, double *dmu) {
+                         const double *h, double *dmu, double *dx) {
     double F, g[6], H[36], f[4], Jf[16];
     br_eval(c, X, &F, g, H);
     orc_branch_flows(c->y, X, f, Jf, NULL);
@@ -792,6 +792,9 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
         dmu[0] = dmu[0] + fac * ph * v[e][0];
         dmu[1] = dmu[1] + fac * ph * v[e][1];
     }
+    /* first-order move of the round's minimiser with mu (R43): dX_F = -H_FF^{-1} J_F' dmu */
+    for (int i = 0; i < 6; i++) dx[i] = 0.0;
+    for (int i = 0; i < nf; i++) dx[idx[i]] = -(V[0][i] * dmu[0] + V[1][i] * dmu[1]);
     return 1;
 }
 
@@ -834,8 +837,12 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
                 double h2 = (f[2] * f[2] + f[3] * f[3]) / c.r2 - 1.0 + X[5];
                 double hm = dmax(fabs(h1), fabs(h2));
                 if (hm <= pr->al_eta_star) break;
-                double hv[2] = {h1, h2}, dmu[2];
-                if (!al_newton_dmu(&c, X, lo, hi, hv, dmu)) {
+                double hv[2] = {h1, h2}, dmu[2], dx[6];
+                if (al_newton_dmu(&c, X, lo, hi, hv, dmu, dx)) {
+#ifndef ORC_NO_PREDICTOR
+                    for (int i = 0; i < 6; i++) X[i] = clampd(X[i] + dx[i], lo[i], hi[i]);
+#endif
+                } else {
                     dmu[0] = c.sig * h1;
                     dmu[1] = c.sig * h2;
                 }

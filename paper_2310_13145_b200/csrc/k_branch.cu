@@ -262,7 +262,8 @@ __device__ __forceinline__ void copy_h(const double (*H)[N], double (*o)[N]) {
         for (int j = 0; j < N; j++) o[i][j] = H[i][j];
 }
 
-// Second-order multiplier update of the thermal AL (R42): dmu = M^{-1} h in the well-conditioned
+// Second-order multiplier update of the thermal AL (R42) with the primal predictor (R43):
+// dmu = M^{-1} h in the well-conditioned
 // eigen-directions of M = J_F H_FF^{-1} J_F' and sigma h in the others.  H is the AL Hessian at
 // the round's end point x (6 variables); its slack columns are sigma * dh/dx, so
 // J_m = (H[0..3][4+m] / sigma, e_{4+m}).  F = variables strictly inside their bounds; H_FF is
@@ -270,7 +271,8 @@ __device__ __forceinline__ void copy_h(const double (*H)[N], double (*o)[N]) {
 // (keep the first-order step) if H_FF is not positive definite.
 constexpr double AL_NEWTON_C = 10.0;
 __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double *x, const double *lo,
-                                              const double *hi, double sig, const double *h, double *dmu) {
+                                              const double *hi, double sig, const double *h, double *dmu,
+                                              double *dx) {
     bool fr[6];
 #pragma unroll
     for (int i = 0; i < 6; i++) fr[i] = x[i] > lo[i] && x[i] < hi[i];
@@ -345,6 +347,9 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
     const double p0 = v0 * h[0] + v1 * h[1], p1 = -v1 * h[0] + v0 * h[1];
     dmu[0] = f0 * p0 * v0 - f1 * p1 * v1;
     dmu[1] = f0 * p0 * v1 + f1 * p1 * v0;
+    // first-order move of the round's minimiser with mu (R43): dx_F = -H_FF^{-1} J_F' dmu
+#pragma unroll
+    for (int i = 0; i < 6; i++) dx[i] = -(V[0][i] * dmu[0] + V[1][i] * dmu[1]);
     return true;
 }
 
@@ -635,6 +640,9 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #ifndef UCAC_BRANCH_MINB
 #define UCAC_BRANCH_MINB 3
 #endif
+#ifndef UCAC_AL_DEAL
+#define UCAC_AL_DEAL 0
+#endif
 #ifndef UCAC_AL_BLOCKS_PER_SM
 #define UCAC_AL_BLOCKS_PER_SM 4
 #endif
@@ -700,10 +708,17 @@ __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
     if (d.st->done) return;
     const size_t LTs = (size_t)d.L * d.T;
     const unsigned n = *((volatile unsigned *)d.alq_cnt);
-    unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0;
+    unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0, c_alit = 0;
+#if UCAC_AL_DEAL
+    // lane-major static dealing: item lane * nwarps + warp, so each warp carries few solves
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    const unsigned gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    for (unsigned idx = lane * nwarps + gwarp; idx < n; idx += 32 * nwarps) {
+#else
     for (;;) {
         const unsigned idx = atomicAdd(d.alq_cnt + 1, 1u);
         if (idx >= n) break;
+#endif
         const int k = d.alq[idx];
         BrFun<true> F6;
         double lo[6], hi[6];
@@ -745,6 +760,7 @@ __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
             double Hx[6][6];
             bool ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it, Hx);
             c_it += it;
+            c_alit += it;
             c_cap += !ok;
             F6.flows(x, C, S, f0, f1, f2, f3);
             double h1 = (f0 * f0 + f1 * f1) / r2 - 1.0 + x[4];
@@ -752,8 +768,11 @@ __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
             double hm = fmax(fabs(h1), fabs(h2));
             if (hm <= d.al_eta_star) break;
             const double hv[2] = {h1, h2};
-            double dmu[2];
-            if (!al_newton_dmu(Hx, x, lo, hi, sig, hv, dmu)) {
+            double dmu[2], dx[6];
+            if (al_newton_dmu(Hx, x, lo, hi, sig, hv, dmu, dx)) {
+#pragma unroll
+                for (int i = 0; i < 6; i++) x[i] = clampd(x[i] + dx[i], lo[i], hi[i]);
+            } else {
                 dmu[0] = sig * h1;
                 dmu[1] = sig * h2;
             }
@@ -779,6 +798,7 @@ __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
     if (c_cap) atomicAdd(d.cnt + 1, c_cap);
     if (c_al) atomicAdd(d.cnt + 2, c_al);
     if (c_alcap) atomicAdd(d.cnt + 3, c_alcap);
+    if (c_alit) atomicAdd(d.cnt + 4, c_alit);
 }
 
 }  // namespace

@@ -183,13 +183,13 @@ __device__ void final_fold(const Dev &d) {
         rec[R_RZ2] = fin[P_RZ2];
         rec[R_Z2] = fin[P_Z2];
         rec[R_OBJ] = fin[P_OBJ];
-        for (int q = 0; q < 4; q++) rec[R_C0 + q] = (double)__ldcg(d.cnt + q);
+        for (int q = 0; q < NCNT; q++) rec[R_C0 + q] = (double)__ldcg(d.cnt + q);
         rec[R_PINF] = fin[P_PINF];
         rec[R_RZINF] = fin[P_RZINF];
         rec[R_ZINF] = fin[P_ZINF];
         rec[R_DINF] = fin[P_DINF];
         rec[R_BAD] = fin[P_BAD];
-        d.cnt[0] = d.cnt[1] = d.cnt[2] = d.cnt[3] = 0;
+        for (int q = 0; q < NCNT; q++) d.cnt[q] = 0;
         d.alq_cnt[0] = 0;
         d.alq_cnt[1] = 0;
         if (d.nranks > 1) {
@@ -683,6 +683,7 @@ __device__ void finalize_status(const Dev &d, const double *rec) {
     st->tron_capped += (unsigned long long)rec[R_C1];
     st->al_active += (unsigned long long)rec[R_C2];
     st->al_capped += (unsigned long long)rec[R_C3];
+    st->al_tron_iters += (unsigned long long)rec[R_C4];
     st->inner_total += 1;
     st->inner_since += 1;
     if ((rec[R_BAD] != 0.0 || !isfinite(rec[R_RZ2]) || !isfinite(rec[R_OBJ])) && st->err_kernel == 0) {

@@ -491,7 +491,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     }
     ALLOC(tauh, double, (size_t)NBROW * (L + P.Lp) * T);
     ALLOC(bmu, double, 4 * BT);
-    ALLOC(cnt, unsigned long long, 4);
+    ALLOC(cnt, unsigned long long, NCNT);
     ALLOC(alq, int, LT);
     ALLOC(alq_cnt, unsigned, 2);
     ALLOC(rec, double, NREC);
@@ -819,6 +819,7 @@ extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
     r->tron_capped = (int64_t)h->tron_capped;
     r->al_active = (int64_t)h->al_active;
     r->al_capped = (int64_t)h->al_capped;
+    r->al_tron_iters = (int64_t)h->al_tron_iters;
     r->inner_since_outer = (int32_t)h->inner_since;
     r->outer_k = (int32_t)h->outer_k;
     r->err_kernel = h->err_kernel;
@@ -931,7 +932,7 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     h->done = 0;
     h->err_kernel = 0;
     CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
-    CK(cudaMemsetAsync(d.cnt, 0, 4 * sizeof(unsigned long long), ctx->s));
+    CK(cudaMemsetAsync(d.cnt, 0, NCNT * sizeof(unsigned long long), ctx->s));
     CK(cudaMemsetAsync(d.alq_cnt, 0, 2 * sizeof(unsigned), ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     return UCAC_OK;

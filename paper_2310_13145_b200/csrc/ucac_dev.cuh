@@ -23,7 +23,9 @@ enum KernelId { K_BRANCH = 0, K_GEN = 1, K_BUS = 2, K_UBAR = 3, K_BUS_LATE = 4, 
 // max rho |dxbar|, objective, non-finite flag
 enum Part { P_PINF = 0, P_RZINF, P_RZ2, P_ZINF, P_Z2, P_DINF, P_OBJ, P_BAD, NPART };
 // cross-rank reduction record: 7 sums (RZ2, Z2, OBJ, 4 TRON counters) then 5 maxes
-enum Rec { R_RZ2 = 0, R_Z2, R_OBJ, R_C0, R_C1, R_C2, R_C3, NREC_SUM, R_PINF = NREC_SUM, R_RZINF, R_ZINF, R_DINF, R_BAD, NREC };
+enum Rec { R_RZ2 = 0, R_Z2, R_OBJ, R_C0, R_C1, R_C2, R_C3, R_C4, NREC_SUM, R_PINF = NREC_SUM, R_RZINF, R_ZINF, R_DINF, R_BAD,
+           NREC };
+constexpr int NCNT = 5;   // TRON iterations, TRON caps, AL solves, AL caps, TRON iterations inside the AL
 
 struct DevStatus {
     double beta;          // current beta^k
@@ -39,7 +41,7 @@ struct DevStatus {
     int pad_;
     double primal_target;
     double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective;
-    unsigned long long tron_iters, tron_capped, al_active, al_capped;
+    unsigned long long tron_iters, tron_capped, al_active, al_capped, al_tron_iters;
 };
 
 struct Dev {
@@ -84,7 +86,7 @@ struct Dev {
     // ---- reduction scratch
     double *part_bus;                 // [nblk_bus][NPART]
     double *part_ubar;                // [nblk_ubar][NPART]
-    unsigned long long *cnt;          // [4] per-iteration TRON counters (zeroed by reduce)
+    unsigned long long *cnt;          // [NCNT] per-iteration solver counters (zeroed by the final fold)
     // ---- multi-rank; single GPU: B_own = B, Lph = 0, nothing to exchange
     int B_own;                        // owned buses [0, B_own); ghosts [B_own, B)
     int Lph;                          // phantom branches [L, L + Lph) (tauhat only)

@@ -73,6 +73,7 @@ class Report(C.Structure):
                 ("objective", C.c_double), ("beta", C.c_double),
                 ("inner_total", C.c_int64), ("outer_total", C.c_int64), ("tron_iters", C.c_int64),
                 ("tron_capped", C.c_int64), ("al_active", C.c_int64), ("al_capped", C.c_int64),
+                ("al_tron_iters", C.c_int64),
                 ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32),
                 ("err_kernel", C.c_int32), ("err_iter", C.c_int32)]
 
