@@ -26,6 +26,10 @@
 #endif
 
 namespace ucac {
+#ifdef UCAC_PROF
+// diagnostic builds only: per queued AL solve (k, start ns, end ns, Newton its, rounds, warp<<8|lane)
+__device__ unsigned long long g_prof[6 << 16];
+#endif
 namespace {
 
 constexpr double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
@@ -720,6 +724,11 @@ __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
         if (idx >= n) break;
 #endif
         const int k = d.alq[idx];
+#ifdef UCAC_PROF
+        unsigned long long t_start;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        const unsigned long long it0 = c_it;
+#endif
         BrFun<true> F6;
         double lo[6], hi[6];
         {
@@ -793,6 +802,17 @@ __global__ void __launch_bounds__(64) k_branch_al(Dev d) {
         d.al[1 * LTs + k] = mu1;
         d.al[2 * LTs + k] = sig;
         emit_tauhat(d, k, x, f0, f1, f2, f3);
+#ifdef UCAC_PROF
+        {
+            unsigned long long t_end;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            if (idx < (1u << 16)) {
+                unsigned long long *r = g_prof + 6ull * idx;
+                r[0] = k; r[1] = t_start; r[2] = t_end; r[3] = c_it - it0; r[4] = kk + 1;
+                r[5] = ((unsigned long long)(blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 8 | (threadIdx.x & 31);
+            }
+        }
+#endif
     }
     if (c_it) atomicAdd(d.cnt + 0, c_it);
     if (c_cap) atomicAdd(d.cnt + 1, c_cap);
@@ -810,3 +830,9 @@ void launch_branch(const Dev &d, cudaStream_t s) {
 void launch_branch_al(const Dev &d, cudaStream_t s) { k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, 64, 0, s>>>(d); }
 
 }  // namespace ucac
+
+#ifdef UCAC_PROF
+extern "C" int ucac_debug_prof(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, ucac::g_prof, bytes < sizeof(ucac::g_prof) ? bytes : sizeof(ucac::g_prof));
+}
+#endif
