@@ -644,6 +644,9 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #ifndef UCAC_BRANCH_MINB
 #define UCAC_BRANCH_MINB 3
 #endif
+#ifndef UCAC_AL_TPB
+#define UCAC_AL_TPB 64
+#endif
 #ifndef UCAC_AL_DEAL
 #define UCAC_AL_DEAL 0
 #endif
@@ -708,7 +711,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
 
 // Phase 2: the queued thermal-active solves (6-variable slack AL, R36), pulled one at a time
 // by every thread of a persistent grid, so the heavy tail is spread over all SMs.
-__global__ void __launch_bounds__(64) k_branch_al(Dev d) {
+__global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
     if (d.st->done) return;
     const size_t LTs = (size_t)d.L * d.T;
     const unsigned n = *((volatile unsigned *)d.alq_cnt);
@@ -827,7 +830,7 @@ void launch_branch(const Dev &d, cudaStream_t s) {
     const int n = d.L * d.T;
     k_branch<<<(n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB, UCAC_BRANCH_TPB, 0, s>>>(d);
 }
-void launch_branch_al(const Dev &d, cudaStream_t s) { k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, 64, 0, s>>>(d); }
+void launch_branch_al(const Dev &d, cudaStream_t s) { k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, 0, s>>>(d); }
 
 }  // namespace ucac
 

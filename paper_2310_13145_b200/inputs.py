@@ -579,3 +579,26 @@ def build_config(name: str, T: Optional[int] = None):
                             clusters=c.get("clusters", 1), vhi_thresh=c.get("vhi", 1.05), name=name)
     rp, rv, ru = c["rho"]
     return pb, Params(rho_pq=rp, rho_va=rv, rho_uc=ru)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-1 workload (Fig. 1 shape): batches of independent UC DP instances with random
+# stage costs.  Per generator and period, L(a, b) is the cost of being in state b at t after
+# state a at t-1: L(0,0) = 0, L(1,1) = on-cost, L(0,1) = on-cost + start-up cost,
+# L(1,0) = shut-down cost; min up/down times in [1, 8], initial state, held prefix in [0, 3].
+# Plain data generation: no DP arithmetic here.
+def dp_workload(G: int, T: int, seed: int = 1):
+    rng = np.random.default_rng(seed)
+    on = rng.uniform(-1.0, 1.0, (G, T)) + 0.3 * np.sin(np.linspace(0, 4 * np.pi, T))[None, :]
+    csu = rng.uniform(0.0, 2.0, (G, 1))
+    csd = rng.uniform(0.0, 0.5, (G, 1))
+    L = np.zeros((G, T, 2, 2))
+    L[:, :, 1, 1] = on
+    L[:, :, 0, 1] = on + csu
+    L[:, :, 1, 0] = csd
+    tu = rng.integers(1, 9, G).astype(np.int32)
+    td = rng.integers(1, 9, G).astype(np.int32)
+    u0 = rng.integers(0, 2, G).astype(np.int32)
+    hold = rng.integers(0, 4, G).astype(np.int32)
+    hold = np.minimum(hold, T).astype(np.int32)
+    return L, tu, td, u0, hold

@@ -81,6 +81,17 @@ def test_dp_batch_bit_exact():
 FREE_RUN = 10
 
 
+@pytest.mark.parametrize("G,T", [(1000, 168), (10000, 24), (10000, 168)])
+def test_dp_batch_next1_sizes_bit_exact(G, T):
+    """NEXT-1 (Fig. 1 shape): every schedule and cost of a 1e3/1e4-generator batch equals the
+    oracle's DP bit for bit, on the bench's workload generator."""
+    L, tu, td, u0, hold = inputs.dp_workload(G, T, seed=G + T)
+    s, c = ucac.dp_batch(L, tu, td, u0, hold)
+    for g in range(G):
+        so, co = oracle.dp_solve(L[g], int(tu[g]), int(td[g]), int(u0[g]), int(hold[g]))
+        assert np.array_equal(s[g], so) and c[g] == co, (G, T, g)
+
+
 def run_pair(pb, pr, iters, check_every=1):
     """GPU vs oracle over `iters` inner iterations.
 
