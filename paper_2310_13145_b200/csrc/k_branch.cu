@@ -598,7 +598,9 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long *dst, unsigned l
 }
 
 // load the data of solve k = l*T + t: admittances, targets tau = xbar - z - y/rho (5.1), w bounds
-__device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F, double *wlo, double *whi) {
+// zs/ys (optional, stride `ss`): keep z and y/rho of the 8 rows for the tauhat emission
+__device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F, double *wlo, double *whi,
+                                           double *zs = nullptr, double *ys = nullptr, int ss = 0) {
     const size_t LTs = (size_t)d.L * d.T;
     const int l = k / d.T, t = k - l * d.T;
     const int bi = d.bfrom[l], bj = d.bto[l];
@@ -606,13 +608,18 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
     F.Bii = d.y[4 * d.L + l]; F.Bij = d.y[5 * d.L + l]; F.Bji = d.y[6 * d.L + l]; F.Bjj = d.y[7 * d.L + l];
     F.rpq = d.rpq;
     F.rva = d.rva;
-#pragma unroll
-    for (int r = 0; r < 4; r++) F.tau[r] = d.fbar[r * LTs + k] - d.zb[r * LTs + k] - d.yb[r * LTs + k] / d.rpq;
     const size_t wi = (size_t)bi * d.T + t, wj = (size_t)bj * d.T + t;
-    F.tau[4] = d.wbar[wi] - d.zb[B_WI * LTs + k] - d.yb[B_WI * LTs + k] / d.rva;
-    F.tau[5] = d.wbar[wj] - d.zb[B_WJ * LTs + k] - d.yb[B_WJ * LTs + k] / d.rva;
-    F.tau[6] = d.thbar[wi] - d.zb[B_AI * LTs + k] - d.yb[B_AI * LTs + k] / d.rva;
-    F.tau[7] = d.thbar[wj] - d.zb[B_AJ * LTs + k] - d.yb[B_AJ * LTs + k] / d.rva;
+    const double xb[8] = {d.fbar[0 * LTs + k], d.fbar[1 * LTs + k], d.fbar[2 * LTs + k], d.fbar[3 * LTs + k],
+                          d.wbar[wi], d.wbar[wj], d.thbar[wi], d.thbar[wj]};
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const double z = d.zb[r * LTs + k], yr = d.yb[r * LTs + k] / (r < 4 ? d.rpq : d.rva);
+        F.tau[r] = xb[r] - z - yr;
+        if (zs) {
+            zs[r * ss] = z;
+            ys[r * ss] = yr;
+        }
+    }
     F.setup();
     wlo[0] = d.vmin[bi] * d.vmin[bi];
     whi[0] = d.vmax[bi] * d.vmax[bi];
@@ -626,6 +633,13 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
 // (DESIGN.md 5.5), written right after the solve so the bus kernel reads 4 values per incident
 // end instead of the row state.  (x + z) + y/rho has no multiply-add to contract, so this is
 // the same value the oracle forms.
+__device__ __forceinline__ void emit_tauhat_zy(const Dev &d, int k, const double *x, double f0, double f1,
+                                               double f2, double f3, const double *zs, const double *ys, int ss) {
+    const size_t LTH = (size_t)(d.L + d.Lph) * d.T;      // tauhat kind stride includes phantom branches
+    const double xs[8] = {f0, f1, f2, f3, x[0], x[1], x[2], x[3]};
+#pragma unroll
+    for (int r = 0; r < 8; r++) d.tauh[r * LTH + k] = xs[r] + zs[r * ss] + ys[r * ss];
+}
 __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x, double f0, double f1,
                                             double f2, double f3) {
     const size_t LTs = (size_t)d.L * d.T;                // row-state kind stride
@@ -662,7 +676,9 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         const size_t LTs = (size_t)LT;
         BrFun<false> F4;
         double lo[4], hi[4];
-        load_solve(d, k, F4, lo, hi);
+        // z and y/rho of the 8 rows, kept in shared memory for the tauhat emission
+        __shared__ double s_z[8][UCAC_BRANCH_TPB], s_y[8][UCAC_BRANCH_TPB];
+        load_solve(d, k, F4, lo, hi, &s_z[0][threadIdx.x], &s_y[0][threadIdx.x], UCAC_BRANCH_TPB);
         lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
         double x[4];
 #pragma unroll
@@ -702,7 +718,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
             d.al[0 * LTs + k] = 0.0;
             d.al[1 * LTs + k] = 0.0;
             d.al[2 * LTs + k] = d.al_sigma0_rel * d.rpq * r2;
-            emit_tauhat(d, k, x, f0, f1, f2, f3);
+            emit_tauhat_zy(d, k, x, f0, f1, f2, f3, &s_z[0][threadIdx.x], &s_y[0][threadIdx.x], UCAC_BRANCH_TPB);
         }
     }
     warp_add_u64(d.cnt + 0, c_it);
