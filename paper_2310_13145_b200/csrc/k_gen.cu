@@ -380,11 +380,12 @@ void launch_gen(const Dev &d, cudaStream_t s) {
 }
 void launch_genx(const Dev &d, cudaStream_t s) { k_genx<<<(d.G * d.T + 127) / 128, 128, 0, s>>>(d); }
 
-void launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
-                     const int *hold, int8_t *sched, double *cost, cudaStream_t s) {
+cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
+                            const int *hold, int8_t *sched, double *cost, cudaStream_t s) {
     const int warps = 4;
     k_dp_batch<<<(G + warps - 1) / warps, warps * 32, gen_smem(T, warps), s>>>(G, T, L, tu, td, u0, hold,
                                                                                 sched, cost);
+    return cudaGetLastError();
 }
 
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s) {

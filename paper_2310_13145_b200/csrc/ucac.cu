@@ -976,8 +976,7 @@ extern "C" ucac_status ucac_dp_batch(int32_t ngen, int32_t T, const double *L, c
         return UCAC_ECUDA;
     }
     if (on_device) {
-        launch_dp_batch(ngen, T, L, min_up, min_dn, u0, hold, sched, cost, s);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_dp_batch(ngen, T, L, min_up, min_dn, u0, hold, sched, cost, s);
         if (e != cudaSuccess) {
             g_create_err = cudaGetErrorString(e);
             return UCAC_ECUDA;
@@ -1005,10 +1004,11 @@ extern "C" ucac_status ucac_dp_batch(int32_t ngen, int32_t T, const double *L, c
         cudaMemcpyAsync(dtd, min_dn, ngen * 4, cudaMemcpyHostToDevice, s);
         cudaMemcpyAsync(du0, u0, ngen * 4, cudaMemcpyHostToDevice, s);
         cudaMemcpyAsync(dh, hold, ngen * 4, cudaMemcpyHostToDevice, s);
-        launch_dp_batch(ngen, T, dL, dtu, dtd, du0, dh, ds, dc, s);
+        e = launch_dp_batch(ngen, T, dL, dtu, dtd, du0, dh, ds, dc, s);
         cudaMemcpyAsync(sched, ds, GT, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(cost, dc, ngen * 8, cudaMemcpyDeviceToHost, s);
-        e = cudaStreamSynchronize(s);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = e2;
     }
     cudaFree(dL); cudaFree(dc); cudaFree(dtu); cudaFree(dtd); cudaFree(du0); cudaFree(dh); cudaFree(ds);
     if (e != cudaSuccess) {

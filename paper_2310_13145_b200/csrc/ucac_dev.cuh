@@ -138,8 +138,8 @@ void launch_pack_bus(const Dev &d, cudaStream_t s);
 void launch_unpack_bus(const Dev &d, cudaStream_t s);
 void launch_ubar(const Dev &d, cudaStream_t s);
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s);
-void launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
-                     const int *hold, int8_t *sched, double *cost, cudaStream_t s);
+cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
+                            const int *hold, int8_t *sched, double *cost, cudaStream_t s);
 int nblk_bus(int B, int T);
 int nblk_ubar(int G, int T);
 }  // namespace ucac
