@@ -247,7 +247,7 @@ __device__ __forceinline__ void pstep(const double *x, const double *lo, const d
 }
 template <int N>
 __device__ __forceinline__ bool cauchy_ok(const double *g, const double (*H)[N], const double *s, double delta) {
-    return sqrt(dotn<N>(s, s)) <= delta && qmodel<N>(g, H, s) <= TR_MU0 * dotn<N>(g, s);
+    return dotn<N>(s, s) <= delta * delta && qmodel<N>(g, H, s) <= TR_MU0 * dotn<N>(g, s);
 }
 template <int N>
 __device__ __forceinline__ double bnd_tau(const double *a, const double *p, double delta) {
@@ -510,7 +510,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                     double tt[N];
 #pragma unroll
                     for (int i = 0; i < N; i++) tt[i] = t[i] + a * p[i];
-                    if (sqrt(dotn<N>(tt, tt)) >= delta) {
+                    if (dotn<N>(tt, tt) >= delta * delta) {
                         double tau = bnd_tau<N>(t, p, delta);
 #pragma unroll
                         for (int i = 0; i < N; i++) w[i] += tau * p[i];
@@ -531,9 +531,9 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
             }
         }
         // --- projected search along w from the Cauchy point
-        double s[N];
+        double s[N], qs;   // step and its model value (reused by the ratio test)
         {
-            double qc = qmodel<N>(g, H, sc);
+            const double qc = qmodel<N>(g, H, sc);
             double b = 1.0;
             bool found = false;
             for (int k = 0; k < 20; k++) {
@@ -543,7 +543,8 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                     s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
                     ds[i] = s[i] - sc[i];
                 }
-                if (qmodel<N>(g, H, s) <= qc + TR_MU0 * dotn<N>(gq, ds)) {
+                qs = qmodel<N>(g, H, s);
+                if (qs <= qc + TR_MU0 * dotn<N>(gq, ds)) {
                     found = true;
                     break;
                 }
@@ -552,21 +553,24 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
             if (!found) {
 #pragma unroll
                 for (int i = 0; i < N; i++) s[i] = sc[i];
+                qs = qc;
             }
         }
+        const double ss = dotn<N>(s, s);
         // --- stall: a step at the rounding level of x means the gradient floor is reached
         {
             double xm = 0.0;
 #pragma unroll
             for (int i = 0; i < N; i++) xm = fmax(xm, fabs(x[i]));
-            if (sqrt(dotn<N>(s, s)) <= TR_STALL * (1.0 + xm)) {
+            const double tol = TR_STALL * (1.0 + xm);
+            if (ss <= tol * tol) {
                 iters = it;
                 if (Hout) copy_h<N>(H, Hout);
                 return true;
             }
         }
         // --- ratio test
-        double pred = -qmodel<N>(g, H, s);
+        double pred = -qs;
         double xn[N], gn[N], fnew;
 #pragma unroll
         for (int i = 0; i < N; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
@@ -574,7 +578,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
         double ared = f - fnew;
         if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dotn<N>(g, s) + dotn<N>(gn, s));
         double ratio = pred > 0.0 ? ared / pred : -1.0;
-        double snorm = sqrt(dotn<N>(s, s));
+        double snorm = sqrt(ss);
         if (ratio > TR_ETA0) {
 #pragma unroll
             for (int i = 0; i < N; i++) x[i] = xn[i];
