@@ -574,7 +574,10 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
         double xn[N], gn[N], fnew;
 #pragma unroll
         for (int i = 0; i < N; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
-        fn.template eval<N, false>(xn, fnew, gn, nullptr);
+        // one evaluation with the Hessian at the trial point, adopted if the step is accepted
+        // (accepted steps are the common case: this saves the second flow evaluation)
+        double Hn[N][N];
+        fn.template eval<N, true>(xn, fnew, gn, Hn);
         double ared = f - fnew;
         if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dotn<N>(g, s) + dotn<N>(gn, s));
         double ratio = pred > 0.0 ? ared / pred : -1.0;
@@ -582,7 +585,13 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
         if (ratio > TR_ETA0) {
 #pragma unroll
             for (int i = 0; i < N; i++) x[i] = xn[i];
-            fn.template eval<N, true>(x, f, g, H);
+            f = fnew;
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                g[i] = gn[i];
+#pragma unroll
+                for (int j = 0; j < N; j++) H[i][j] = Hn[i][j];
+            }
         }
         if (ratio < TR_ETA1) delta = TR_SIG1 * fmin(snorm, delta);
         else if (ratio > TR_ETA2) delta = fmax(delta, TR_SIG3 * snorm);
