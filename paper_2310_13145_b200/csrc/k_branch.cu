@@ -145,7 +145,8 @@ struct BrFun {
                 k01 += sig * (dh0[0] * dh0[1] + dh1[0] * dh1[1]);
             }
         }
-        double i2wi = 0.5 / x[0], i2wj = 0.5 / x[1];
+        const double ixx = 0.5 / (x[0] * x[1]);   // one division for both 1/(2 w)
+        double i2wi = x[1] * ixx, i2wj = x[0] * ixx;
         double dC[4] = {C * i2wi, C * i2wj, -S, S};
         double dS[4] = {S * i2wi, S * i2wj, C, -C};
 #pragma unroll
