@@ -22,7 +22,7 @@
 // Subspace step of TRON for N <= UCAC_TRON_DIRECT_MAXN variables: LDL^T Newton step when H_FF is
 // positive definite and the step is interior, else Steihaug-Toint CG.
 #ifndef UCAC_TRON_DIRECT_MAXN
-#define UCAC_TRON_DIRECT_MAXN 4
+#define UCAC_TRON_DIRECT_MAXN 6
 #endif
 
 namespace ucac {
@@ -362,21 +362,23 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
 // replaced by the identity).  Returns false if H_FF is not positive definite.
 template <int N>
 __device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr, const double *r, double *w) {
-    double Lm[N][N], D[N];
+    // L D L' with LD[i][j] = L[i][j] D[j] kept (no triple products) and the pivots inverted once
+    double Lm[N][N], LD[N][N], iD[N];
     bool pd = true;
 #pragma unroll
     for (int j = 0; j < N; j++) {
         double dj = fr[j] ? H[j][j] : 1.0;
 #pragma unroll
-        for (int k = 0; k < j; k++) dj -= Lm[j][k] * Lm[j][k] * D[k];
+        for (int k = 0; k < j; k++) dj -= Lm[j][k] * LD[j][k];
         pd = pd && dj > 0.0;
-        D[j] = dj;
         const double inv = 1.0 / dj;
+        iD[j] = inv;
 #pragma unroll
         for (int i = j + 1; i < N; i++) {
             double v = (fr[i] && fr[j]) ? H[i][j] : 0.0;
 #pragma unroll
-            for (int k = 0; k < j; k++) v -= Lm[i][k] * Lm[j][k] * D[k];
+            for (int k = 0; k < j; k++) v -= Lm[i][k] * LD[j][k];
+            LD[i][j] = v;
             Lm[i][j] = v * inv;
         }
     }
@@ -391,7 +393,7 @@ __device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr
     }
 #pragma unroll
     for (int i = N - 1; i >= 0; i--) {
-        double v = z[i] / D[i];
+        double v = z[i] * iD[i];
 #pragma unroll
         for (int k = i + 1; k < N; k++) v -= Lm[k][i] * w[k];
         w[i] = fr[i] ? v : 0.0;
