@@ -681,7 +681,7 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #define UCAC_AL_DEAL 0
 #endif
 #ifndef UCAC_AL_BLOCKS_PER_SM
-#define UCAC_AL_BLOCKS_PER_SM 4
+#define UCAC_AL_BLOCKS_PER_SM 2
 #endif
 __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(Dev d) {
     if (d.st->done) return;
