@@ -579,14 +579,20 @@ static double pgnorm(int n, const double *x, const double *g, const double *lo,
     }
     return m;
 }
+static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn ev, void *ctx,
+                  double gtol, int maxit, int *iters, double delta0);
 static int tron(int n, double *x, const double *lo, const double *hi, eval_fn ev, void *ctx,
                 double gtol, int maxit, int *iters) {
+    return tron_r(n, x, lo, hi, ev, ctx, gtol, maxit, iters, TR_DELTA0);
+}
+static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn ev, void *ctx,
+                  double gtol, int maxit, int *iters, double delta0) {
     double f, g[MAXN], H[MAXN * MAXN], fn, gn[MAXN], Hn[MAXN * MAXN];
     double sc[MAXN], w[MAXN], s[MAXN], xn[MAXN], gq[MAXN], Hs[MAXN];
     int fr[MAXN];
     for (int i = 0; i < n; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     ev(ctx, x, &f, g, H);
-    double delta = TR_DELTA0, alpha = 1.0;
+    double delta = delta0, alpha = 1.0;
     {
         /* first Cauchy trial length: the model minimiser along -g (R41) */
         double Hg[MAXN];
@@ -714,6 +720,7 @@ static void br_eval(void *vc, const double *X, double *fo, double *g, double *H)
  * For sigma -> inf, M -> I/sigma and this is the first-order update dmu = sigma h.
  * Returns 0 (caller keeps the first-order update) if H_FF or M is not positive definite. */
 #define AL_NEWTON_C 10.0
+#define AL_R1_DELTA0 0.03
 static int al_newton_dmu(bctx *c, const double *X, const double *lo, const double *hi,
                          const double *h, double *dmu, double *dx) {
     double F, g[6], H[36], f[4], Jf[16];
@@ -829,7 +836,9 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
             int k;
             stats[2] = 1;
             for (k = 0; k < pr->al_maxit; k++) {
-                ok = tron(6, X, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it);
+                /* round 1 starts at the fast-path point, which violates Eq. 2c-2d: a small first
+                 * trust region (R44) keeps the first model step where sigma h^2 is modelled well */
+                ok = tron_r(6, X, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it, k == 0 ? AL_R1_DELTA0 : TR_DELTA0);
                 stats[0] += it;
                 stats[1] += !ok;
                 orc_branch_flows(y, X, f, NULL, NULL);

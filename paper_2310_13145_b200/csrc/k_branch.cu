@@ -275,6 +275,7 @@ __device__ __forceinline__ void copy_h(const double (*H)[N], double (*o)[N]) {
 // factored as L D L' with the fixed rows and columns replaced by the identity.  Returns false
 // (keep the first-order step) if H_FF is not positive definite.
 constexpr double AL_NEWTON_C = 10.0;
+constexpr double AL_R1_DELTA0 = 0.03;
 __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double *x, const double *lo,
                                               const double *hi, double sig, const double *h, double *dmu,
                                               double *dx) {
@@ -404,12 +405,12 @@ __device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr
 // Projected trust-region Newton.  Returns true when ||P(x-g)-x||_inf <= gtol.
 template <int N, class Fun>
 __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *hi, double gtol,
-                     int maxit, int &iters, double (*Hout)[N] = nullptr) {
+                     int maxit, int &iters, double (*Hout)[N] = nullptr, double delta0 = TR_DELTA0) {
     double f, g[N], H[N][N];
 #pragma unroll
     for (int i = 0; i < N; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     fn.template eval<N, true>(x, f, g, H);
-    double delta = TR_DELTA0, alpha = 1.0;
+    double delta = delta0, alpha = 1.0;
     {
         // first Cauchy trial length: the model minimiser along -g (R41)
         double Hg[N];
@@ -802,7 +803,8 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
             F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
             int it = 0;
             double Hx[6][6];
-            bool ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it, Hx);
+            // round 1 starts at the fast-path point, which violates Eq. 2c-2d: small first radius (R44)
+            bool ok = tron<6>(F6, x, lo, hi, d.tron_gtol, d.tron_maxit, it, Hx, kk == 0 ? AL_R1_DELTA0 : TR_DELTA0);
             c_it += it;
             c_alit += it;
             c_cap += !ok;
