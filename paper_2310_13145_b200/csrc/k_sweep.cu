@@ -618,30 +618,58 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
             n = 3;
         }
 #undef ROW
+        // z, y, lambda of the group's rows, all loaded before any store (a store to one row array
+        // would otherwise order every later row's loads behind it)
+        const int rk[7] = {G_DON, G_DSD, G_PL, G_PU, G_QL, G_QU, G_RD};
+        double zr[9], yr[9], lr[9];
+#pragma unroll
+        for (int q2 = 0; q2 < 7; q2++) {
+            zr[q2] = ZG(rk[q2], i);
+            yr[q2] = YG(rk[q2], i);
+            lr[q2] = LG(rk[q2], i);
+        }
+        const bool nxt = t < T - 1;
+        if (nxt) {
+            zr[7] = ZG(G_DSU, i + 1); yr[7] = YG(G_DSU, i + 1); lr[7] = LG(G_DSU, i + 1);
+            zr[8] = ZG(G_RU, i + 1);  yr[8] = YG(G_RU, i + 1);  lr[8] = LG(G_RU, i + 1);
+        }
         double v[3];
         boxqp3(n, m, cm, e, v);
         const double on_n = v[0], sd_n = v[1];
-        d.ub_on[i] = on_n;
-        d.ub_sd[i] = sd_n;
         // rows of the group with the new ubar (r = x-part - c'ubar)
         const double don = on_n - on_o, dsd = sd_n - sd_o;
-        zy_row((double)ut - on_n, ruc, beta, &ZG(G_DON, i), &YG(G_DON, i), &LG(G_DON, i), pending, beta_lam, lmax, don, acc);
-        zy_row((double)sdt - sd_n, ruc, beta, &ZG(G_DSD, i), &YG(G_DSD, i), &LG(G_DSD, i), pending, beta_lam, lmax, dsd, acc);
-        zy_row((p - spl) - Pm * on_n, ruc, beta, &ZG(G_PL, i), &YG(G_PL, i), &LG(G_PL, i), pending, beta_lam, lmax, Pm * don, acc);
-        zy_row((p + spu) - PM * on_n, ruc, beta, &ZG(G_PU, i), &YG(G_PU, i), &LG(G_PU, i), pending, beta_lam, lmax, PM * don, acc);
-        zy_row((q - sql) - Qm * on_n, ruc, beta, &ZG(G_QL, i), &YG(G_QL, i), &LG(G_QL, i), pending, beta_lam, lmax, Qm * don, acc);
-        zy_row((q + squ) - QM * on_n, ruc, beta, &ZG(G_QU, i), &YG(G_QU, i), &LG(G_QU, i), pending, beta_lam, lmax, QM * don, acc);
-        zy_row((dd - srd) + RDn * on_n + SDn * sd_n, ruc, beta, &ZG(G_RD, i), &YG(G_RD, i), &LG(G_RD, i), pending, beta_lam,
-               lmax, RDn * don + SDn * dsd, acc);
-        if (t < T - 1) {
-            const size_t j = i + 1;
-            const double su_n = v[2];
-            d.ub_su[j] = su_n;
+        zy_vals((double)ut - on_n, ruc, beta, zr[0], yr[0], lr[0], pending, beta_lam, lmax, don, acc);
+        zy_vals((double)sdt - sd_n, ruc, beta, zr[1], yr[1], lr[1], pending, beta_lam, lmax, dsd, acc);
+        zy_vals((p - spl) - Pm * on_n, ruc, beta, zr[2], yr[2], lr[2], pending, beta_lam, lmax, Pm * don, acc);
+        zy_vals((p + spu) - PM * on_n, ruc, beta, zr[3], yr[3], lr[3], pending, beta_lam, lmax, PM * don, acc);
+        zy_vals((q - sql) - Qm * on_n, ruc, beta, zr[4], yr[4], lr[4], pending, beta_lam, lmax, Qm * don, acc);
+        zy_vals((q + squ) - QM * on_n, ruc, beta, zr[5], yr[5], lr[5], pending, beta_lam, lmax, QM * don, acc);
+        zy_vals((dd - srd) + RDn * on_n + SDn * sd_n, ruc, beta, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
+                RDn * don + SDn * dsd, acc);
+        double su_n = 0.0;
+        if (nxt) {
+            su_n = v[2];
             const double dsu = su_n - su_on;
-            zy_row((double)sun - su_n, ruc, beta, &ZG(G_DSU, j), &YG(G_DSU, j), &LG(G_DSU, j), pending, beta_lam, lmax, dsu,
-                   acc);
-            zy_row(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, beta, &ZG(G_RU, j), &YG(G_RU, j), &LG(G_RU, j),
-                   pending, beta_lam, lmax, RUp * don + SUp * dsu, acc);
+            zy_vals((double)sun - su_n, ruc, beta, zr[7], yr[7], lr[7], pending, beta_lam, lmax, dsu, acc);
+            zy_vals(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, beta, zr[8], yr[8], lr[8], pending, beta_lam,
+                    lmax, RUp * don + SUp * dsu, acc);
+        }
+        d.ub_on[i] = on_n;
+        d.ub_sd[i] = sd_n;
+#pragma unroll
+        for (int q2 = 0; q2 < 7; q2++) {
+            ZG(rk[q2], i) = zr[q2];
+            YG(rk[q2], i) = yr[q2];
+            if (pending) LG(rk[q2], i) = lr[q2];
+        }
+        if (nxt) {
+            d.ub_su[i + 1] = su_n;
+            ZG(G_DSU, i + 1) = zr[7]; YG(G_DSU, i + 1) = yr[7];
+            ZG(G_RU, i + 1) = zr[8];  YG(G_RU, i + 1) = yr[8];
+            if (pending) {
+                LG(G_DSU, i + 1) = lr[7];
+                LG(G_RU, i + 1) = lr[8];
+            }
         }
         if (t == 0) {
             // group 0 = (ubar^su_1): rows D_SU_1, RU_1 (ubar^on_0 := u0, R4)
