@@ -685,6 +685,7 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #define UCAC_AL_BLOCKS_PER_SM 2
 #endif
 __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(Dev d) {
+    TL_KERNEL(K_BRANCH);
     if (d.st->done) return;
     const int LT = d.L * d.T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -745,6 +746,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
 // Phase 2: the queued thermal-active solves (6-variable slack AL, R36), pulled one at a time
 // by every thread of a persistent grid, so the heavy tail is spread over all SMs.
 __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
+    TL_KERNEL(K_BRANCH_AL);
     if (d.st->done) return;
     const size_t LTs = (size_t)d.L * d.T;
     const unsigned n = *((volatile unsigned *)d.alq_cnt);

@@ -232,6 +232,7 @@ __device__ void gen_solve(const GenIn &g, double &po, double &qo, double &pho) {
 #define YG(k, i) d.yg[(size_t)(k) * GT + (i)]
 
 __global__ void __launch_bounds__(128) k_gen(Dev d) {
+    TL_KERNEL(K_GEN);
     if (d.st->done) return;
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(128) k_gen(Dev d) {
 
 // (7b) generator part on iterate l: one thread per (g,t) (S2)
 __global__ void __launch_bounds__(128) k_genx(Dev d) {
+    TL_KERNEL(K_GENX);
     if (d.st->done) return;
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;

@@ -350,6 +350,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
 }
 
 __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
+    TL_KERNEL(K_BUS);
     if (d.st->done) return;
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -404,6 +405,7 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
 // k_rows (early): one thread per (l,t), the ends whose bus is not marked (coalesced row
 // arrays, as k_branch); the marked ends are done by k_rows_late.
 __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
+    TL_KERNEL(K_ROWS);
     if (d.st->done) return;
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -420,6 +422,7 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
 // the marked ends (1024-thread blocks: few partial slots, so the final fold is short).
 // Single GPU: k_rows_late is the last kernel of the iteration (final = 1).
 __global__ void __launch_bounds__(LATE_THREADS) k_bus_late(Dev d) {
+    TL_KERNEL(K_BUS_LATE);
     if (d.st->done) return;
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -431,6 +434,7 @@ __global__ void __launch_bounds__(LATE_THREADS) k_bus_late(Dev d) {
 // k_fold_early: the block partials of k_bus, k_ubar and k_rows (in that order) -> rec_part[RK_EARLY]
 constexpr int FOLD_BLOCKS = 64, FOLD_THREADS = 256;
 __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
+    TL_KERNEL(K_FOLD);
     if (d.st->done) return;
     const int nb = d.nblk_bus, nu = d.nblk_ubar, nr = d.nblk_rows, n = nb + nu + nr;
     const int chunk = (n + FOLD_BLOCKS - 1) / FOLD_BLOCKS;
@@ -462,6 +466,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
 }
 
 __global__ void __launch_bounds__(LATE_THREADS) k_rows_late(Dev d, int final) {
+    TL_KERNEL(K_ROWS_LATE);
     if (d.st->done) return;
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -555,6 +560,7 @@ __device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, doub
 }
 
 __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
+    TL_KERNEL(K_UBAR);
     if (d.st->done) return;
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;

@@ -495,6 +495,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ALLOC(alq, int, LT);
     ALLOC(alq_cnt, unsigned, 2);
     ALLOC(rec, double, NREC);
+    ALLOC(tl, unsigned long long, 2 * NKERN);
     ALLOC(xsend1, double, (size_t)P.max_cut * 4 * T);
     ALLOC(xrecv1, double, (size_t)nranks * P.max_cut * 4 * T);
     ALLOC(xsend2, double, (size_t)P.max_export * 6 * T);
@@ -592,13 +593,16 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         ncclAllGather(d.xsend1, d.xrecv1, (size_t)d.max_cut * 4 * d.T, ncclDouble, ctx->comm, ctx->s);
         launch_unpack_tau(d, ctx->s);
     }
-    cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
     if (!multi) {
+        // the late bus solve needs the AL results and the generator x-update only (not k_ubar);
+        // the late rows' final fold needs every early partial (k_fold_early, after k_ubar)
+        cudaStreamWaitEvent(ctx->s, ctx->ev_genx, 0);
         launch_kernel(ctx, K_BUS_LATE, ctx->s);
         cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_ROWS_LATE, ctx->s);
         return;
     }
+    cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
     launch_kernel(ctx, K_BUS, ctx->s);
     launch_kernel(ctx, K_BUS_LATE, ctx->s);
     if (d.max_export > 0) {
@@ -1081,3 +1085,18 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);
     delete ctx;
 }
+
+#ifdef UCAC_PROF
+// diagnostic builds only: reset / read the kernel timeline (2*NKERN u64: first start, last exit)
+extern "C" int ucac_debug_timeline(ucac_ctx *ctx, unsigned long long *host, int reset) {
+    if (reset) {
+        std::vector<unsigned long long> v(2 * NKERN);
+        for (int k = 0; k < NKERN; k++) {
+            v[2 * k] = ~0ull;
+            v[2 * k + 1] = 0ull;
+        }
+        return (int)cudaMemcpy(ctx->d.tl, v.data(), v.size() * 8, cudaMemcpyHostToDevice);
+    }
+    return (int)cudaMemcpy(host, ctx->d.tl, 2 * NKERN * 8, cudaMemcpyDeviceToHost);
+}
+#endif

@@ -108,7 +108,35 @@ struct Dev {
     unsigned *kdone;                  // [3] last-block counters of the kernels producing them
     unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
     DevStatus *st;
+    unsigned long long *tl;           // [2*NKERN] diagnostic timeline (UCAC_PROF builds only)
 };
+
+// UCAC_PROF builds: per kernel, the earliest block start and the latest block-thread-0 exit on the
+// global timer (ns), for graph timelines (tools/timeline.py).  Empty otherwise.
+#ifdef UCAC_PROF
+struct TlGuard {
+    unsigned long long *p;
+    __device__ TlGuard(unsigned long long *tl, int kid) : p(tl + 2 * kid) {
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMin(p, t);
+        }
+    }
+    __device__ ~TlGuard() {
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(p + 1, t);
+        }
+    }
+};
+#define TL_KERNEL(kid) TlGuard tl_guard_(d.tl, (kid))
+#else
+#define TL_KERNEL(kid) \
+    do {               \
+    } while (0)
+#endif
 
 __host__ __device__ inline size_t gi(const Dev &d, int g, int t) { return (size_t)g * d.T + t; }
 // per-iteration stamp of bmark (read before k_reduce advances inner_total; never 0)
