@@ -676,13 +676,13 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #define UCAC_BRANCH_MINB 3
 #endif
 #ifndef UCAC_AL_TPB
-#define UCAC_AL_TPB 64
+#define UCAC_AL_TPB 256
 #endif
 #ifndef UCAC_AL_DEAL
-#define UCAC_AL_DEAL 0
+#define UCAC_AL_DEAL 2
 #endif
 #ifndef UCAC_AL_BLOCKS_PER_SM
-#define UCAC_AL_BLOCKS_PER_SM 2
+#define UCAC_AL_BLOCKS_PER_SM 1
 #endif
 __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(Dev d) {
     TL_KERNEL(K_BRANCH);
@@ -751,7 +751,11 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
     const size_t LTs = (size_t)d.L * d.T;
     const unsigned n = *((volatile unsigned *)d.alq_cnt);
     unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0, c_alit = 0;
-#if UCAC_AL_DEAL
+#if UCAC_AL_DEAL == 2
+    // block-major static dealing: the queue fills the first blocks, so the AL work sits on few SMs
+    // (with full-register-file blocks, exclusively) and the other SMs run the concurrent sweeps
+    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+#elif UCAC_AL_DEAL == 1
     // lane-major static dealing: item lane * nwarps + warp, so each warp carries few solves
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     const unsigned gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -866,7 +870,13 @@ void launch_branch(const Dev &d, cudaStream_t s) {
     const int n = d.L * d.T;
     k_branch<<<(n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB, UCAC_BRANCH_TPB, 0, s>>>(d);
 }
-void launch_branch_al(const Dev &d, cudaStream_t s) { k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, 0, s>>>(d); }
+#ifndef UCAC_AL_SMEM
+#define UCAC_AL_SMEM 0   // dynamic shared memory per AL block (bytes): > 0 reserves SMs for the AL work
+#endif
+void launch_branch_al(const Dev &d, cudaStream_t s) {
+    if (UCAC_AL_SMEM > 48 * 1024) cudaFuncSetAttribute(k_branch_al, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
+    k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, UCAC_AL_SMEM, s>>>(d);
+}
 
 }  // namespace ucac
 

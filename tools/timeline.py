@@ -21,18 +21,24 @@ def main(name="pegase2869", warm=10):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     L = ucac.lib()
     buf = np.zeros(2 * ucac.NKERNELS, dtype=np.uint64)
-    rows = []
+    rows, ev_ms = [], []
+    st = torch.cuda.ExternalStream(c.stream)
     for rep in range(5):
         flush.zero_()
         torch.cuda.synchronize()
         L.ucac_debug_timeline(c.h, None, 1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
         c.iterate(1)
+        b.record(st)
         c.report()
+        ev_ms.append(a.elapsed_time(b))
         L.ucac_debug_timeline(c.h, buf.ctypes.data_as(C.c_void_p), 0)
         rows.append(buf.astype(np.int64).reshape(-1, 2).copy())
     r = np.median(np.stack(rows), axis=0)
     t0 = r[:, 0].min()
     order = np.argsort(r[:, 0])
+    print(f"event-timed step {np.median(ev_ms) * 1e3:.1f} us; kernels span {(r[:, 1].max() - t0) / 1e3:.1f} us")
     for k in order:
         print(f"{ucac.KERNELS[k]:14s} start {(r[k, 0] - t0) / 1e3:8.1f} us  end {(r[k, 1] - t0) / 1e3:8.1f} us  "
               f"span {(r[k, 1] - r[k, 0]) / 1e3:7.1f} us")
