@@ -111,7 +111,10 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 constexpr int BUS_THREADS = 128;
 constexpr int UBAR_THREADS = 64;
 constexpr int ROWS_THREADS = 128;
-constexpr int LATE_THREADS = 1024;
+#ifndef UCAC_LATE_THREADS
+#define UCAC_LATE_THREADS 1024
+#endif
+constexpr int LATE_THREADS = UCAC_LATE_THREADS;
 
 // ------------------------------------------------------------------------- S8 partials
 // Every kernel that updates rows leaves one partial per block.  The early ones (k_bus, k_ubar,
