@@ -251,6 +251,38 @@ def run_dp(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_warmstart(args, pb, pr, rank):
+    """NEXT-2: the UC warm start through ucac_uc_warm_start (context creation,
+    held-schedule ACOPF iterations, device Hamming costs + batched DP repair), wall clock, against
+    the oracle's warm start on the same workload and iteration count (one core)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_2310_13145_b200 import ucac
+    iters = args.steps
+    ucac.uc_warm_start(pb, pr, 1)                     # warm-up (library load, first context)
+    t0 = time.perf_counter()
+    u = ucac.uc_warm_start(pb, pr, iters)
+    gpu_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    uo, _ = oracle.uc_warm_start(pb, pr, iters)
+    cpu_s = time.perf_counter() - t0
+    line = {
+        "metric": "UC warm starts/s (NEXT-2: held-schedule ACOPF + DP repair)", "value": 1.0 / gpu_s,
+        "unit": "warm starts/s", "n_gpus": 1, "steps": iters, "warmup": 1, "ms_per_step": 1e3 * gpu_s / iters,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, paper_2310_13145_b200.inputs)",
+        "config": {"workload": f"{args.config} warm start, {iters} held-schedule iterations, threshold 1e-3 pu"},
+        "units_on": int(u.sum()), "units_on_of": int(u.size), "schedule_equal_to_oracle": bool(np.array_equal(u, uo)),
+        "cpu_baseline": {"value": 1.0 / cpu_s, "unit": "warm starts/s", "cores": 1, "kind": "oracle",
+                         "sample": f"the same warm start ({iters} iterations) by the C oracle"},
+        "note": "wall clock including context creation (H2D of the problem) and the D2H of the schedule",
+    }
+    print(json.dumps(line), flush=True)
+
+
 def problem_bytes(pb) -> int:
     import numpy as np
     tot = 0
@@ -269,8 +301,9 @@ def main():
     ap.add_argument("--config", default="pegase2869")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--workload", default="admm", choices=["admm", "dp"],
-                    help="admm: the inner-iteration hot path (default); dp: NEXT-1 batched UC DP")
+    ap.add_argument("--workload", default="admm", choices=["admm", "dp", "warmstart"],
+                    help="admm: the inner-iteration hot path (default); dp: NEXT-1 batched UC DP; "
+                         "warmstart: NEXT-2 UC warm start")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -286,6 +319,9 @@ def main():
         return
     if args.workload == "dp":
         run_dp(args, rank, world)
+        return
+    if args.workload == "warmstart":
+        run_warmstart(args, pb, pr, rank)
         return
 
     import numpy as np

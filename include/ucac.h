@@ -98,6 +98,7 @@ typedef struct {
     double tron_gtol_rel;
     int32_t tron_maxit, al_maxit;
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
+    int32_t uc_fixed;   /* 1: step (7a) keeps the schedule (NEXT-2 warm start, ucac_uc_warm_start) */
 } ucac_params;
 
 /* Multi-GPU (bus-graph cut).  NULL = single GPU.
@@ -202,6 +203,15 @@ typedef struct {
 } ucac_state;
 ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st);
 ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st);
+
+/* NEXT-2 UC warm start (R46): solve the multiperiod
+ * ACOPF with every unit on after its held prefix and the schedule held (uc_fixed = 1) for
+ * `iters` inner iterations, then u_out[g*T+t] = the nearest schedule satisfying Eq. 3 (one DP
+ * pass, stage cost = Hamming distance to [p > threshold], threshold in pu, e.g. 1e-3).  Pass
+ * u_out as ucac_uc.u_init of the UC-ACOPF context.  Single GPU; host buffers; synchronous. */
+ucac_status ucac_uc_warm_start(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *cost,
+                               const ucac_uc *uc, const ucac_params *prm, int32_t iters, double threshold,
+                               int8_t *u_out);
 
 /* Batched UC DP (Alg. 2) on caller stage costs: L [ngen*T*4] with L[(g*T+t)*4 + a*2 + b] =
  * L^UC_{g,t}(a, b).  Outputs sched [ngen*T] (int8) and cost [ngen].  Tie -> stay

@@ -68,7 +68,7 @@ class Params_c(C.Structure):
                 ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
-                ("al_sigma_decay", C.c_double)]
+                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32)]
 
 
 class Report_c(C.Structure):
@@ -105,6 +105,8 @@ def _declare(L):
     L.orc_stage_costs.argtypes = [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, dp, dp, dp, dp]
     L.orc_dp.argtypes = [C.c_int32, dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, i8p]
     L.orc_dp.restype = C.c_double
+    L.orc_uc_repair.argtypes = [C.c_int32, dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, C.c_int32, i8p]
+    L.orc_uc_repair.restype = None
     L.orc_gen_x.argtypes = [dp, dp]
     L.orc_boxqp3.argtypes = [C.c_int32, C.c_int32, dp, dp, dp]
     L.orc_bus_kkt.argtypes = [C.c_int32, dp, dp, dp, dp, C.c_double, C.c_double, dp, dp]
@@ -127,7 +129,7 @@ def params_c(pr) -> Params_c:
     return Params_c(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max,
                     pr.beta_max, pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled,
                     pr.tron_gtol_rel, pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel,
-                    pr.al_sigma_max_rel, pr.al_sigma_decay)
+                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed)
 
 
 class Oracle:
@@ -207,6 +209,30 @@ def stage_costs(T, c0, csu, csd, rho, ub, y, z):
     L = np.zeros(T * 4)
     lib().orc_stage_costs(T, c0, csu, csd, rho, _p(_f64(ub)), _p(_f64(y)), _p(_f64(z)), _p(L))
     return L.reshape(T, 2, 2)
+
+
+def uc_repair(p, threshold, TU, TD, u0, hold):
+    """NEXT-2: [p > threshold] repaired to the nearest Eq. 3 schedule (one DP pass)."""
+    p = _f64(p).reshape(-1)
+    u = np.zeros(p.size, dtype=np.int8)
+    lib().orc_uc_repair(p.size, _p(p), float(threshold), int(TU), int(TD), int(u0), int(hold), _p(u, i8p))
+    return u
+
+
+def uc_warm_start(pb, pr, iters: int, threshold: float = 1e-3):
+    """NEXT-2 (SPEC warm_start_uc): the multiperiod ACOPF with every unit on (after its held
+    prefix) and the schedule held, `iters` inner iterations, then threshold + repair per generator."""
+    import dataclasses
+    G, T = pb.ngen, pb.T
+    uinit = np.ones((G, T), dtype=np.int8)
+    for g in range(G):
+        uinit[g, :int(pb.hold[g])] = int(pb.u0[g])
+    o = Oracle(dataclasses.replace(pb, u_init=uinit), dataclasses.replace(pr, uc_fixed=1))
+    o.iterate(iters)
+    p = o.get_state()["p"].reshape(G, T)
+    o.close()
+    u = np.stack([uc_repair(p[g], threshold, pb.min_up[g], pb.min_dn[g], pb.u0[g], pb.hold[g]) for g in range(G)])
+    return u, p
 
 
 def dp_solve(L, TU, TD, u0, hold):

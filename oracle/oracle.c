@@ -149,6 +149,21 @@ double orc_dp(int32_t T, const double *L, int32_t TU, int32_t TD, int32_t u0,
     return cost;
 }
 
+/* NEXT-2: threshold the multiperiod-ACOPF dispatch, then one DP pass (Algorithm 2) whose
+ * stage cost is the Hamming distance to the thresholded schedule: the nearest schedule that
+ * satisfies Eq. 3 (SPEC warm_start_uc). */
+void orc_uc_repair(int32_t T, const double *p, double threshold, int32_t TU, int32_t TD, int32_t u0,
+                   int32_t hold, int8_t *u_out) {
+    double *L = (double *)calloc((size_t)T * 4, sizeof(double));
+    for (int t = 0; t < T; t++) {
+        int ut = p[t] > threshold;
+        for (int a = 0; a < 2; a++)
+            for (int b = 0; b < 2; b++) L[t * 4 + a * 2 + b] = (b != ut) ? 1.0 : 0.0;
+    }
+    orc_dp(T, L, TU, TD, u0, hold, u_out);
+    free(L);
+}
+
 /* ========================================================================== */
 /* S2: generator x-update (7b restricted to p, q, phat, slacks).               */
 /* ========================================================================== */
@@ -1049,7 +1064,9 @@ static void one_iteration(orc_ctx *c) {
 
     /* ---- (7a) x^UC by DP per generator (Alg. 2), on iterate l ---- */
     int8_t *unew = (int8_t *)calloc(GT, 1);
-    {
+    if (pr->uc_fixed) {
+        memcpy(unew, c->u, GT);   /* NEXT-2: the multiperiod ACOPF with the schedule held */
+    } else {
         double *Lt = dz((size_t)T * 4), *ub3 = dz((size_t)3 * T), *y3 = dz((size_t)3 * T), *z3 = dz((size_t)3 * T);
         for (int g = 0; g < G; g++) {
             for (int v = 0; v < 3; v++)

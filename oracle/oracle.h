@@ -47,6 +47,7 @@ typedef struct {
     double tron_gtol_rel;
     int32_t tron_maxit, al_maxit;
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
+    int32_t uc_fixed;   /* 1: step (7a) keeps u (the NEXT-2 warm start's multiperiod ACOPF) */
 } orc_params;
 
 typedef struct {
@@ -87,6 +88,11 @@ void orc_stage_costs(int32_t T, double c0, double csu, double csd, double rho_uc
                      const double *ub /*[3*T]: on,su,sd t-minor blocks*/,
                      const double *y /*[3*T]*/, const double *z /*[3*T]*/, double *L /*[T*4]*/);
 /* S1 DP, Algorithm 2.  Returns the optimal cost; sched[T]. */
+/* NEXT-2 warm start (SPEC warm_start_uc): u = [p > threshold] repaired to the nearest
+ * schedule satisfying Eq. 3 (min-up/down, held prefix) by one DP pass with stage costs
+ * L_t(a, b) = [b != u_t] (Hamming distance; ties as the DP: stay). */
+void orc_uc_repair(int32_t T, const double *p, double threshold, int32_t TU, int32_t TD, int32_t u0,
+                   int32_t hold, int8_t *u_out);
 double orc_dp(int32_t T, const double *L /*[T*4] L[t*4+a*2+b]*/, int32_t TU, int32_t TD,
               int32_t u0, int32_t hold, int8_t *sched);
 /* S2 generator x-update for one (g,t). in[]: see oracle.c gen_x_update. out: p,q,ph. */

@@ -9,6 +9,8 @@
 // switch-window sums and the per-(g,t) generator x-update (t = lane, lane+32, ...); the
 // backward recursion of Algorithm 2 is inherently sequential in t and runs on
 // lane 0 over a shared-memory table (O(T) with 2 states).
+#include <algorithm>
+
 #include "ucac_dev.cuh"
 
 namespace ucac {
@@ -233,7 +235,7 @@ __device__ void gen_solve(const GenIn &g, double &po, double &qo, double &pho) {
 
 __global__ void __launch_bounds__(128) k_gen(Dev d) {
     TL_KERNEL(K_GEN);
-    if (d.st->done) return;
+    if (d.st->done || d.uc_fixed) return;   // uc_fixed: the schedule is held (NEXT-2)
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -317,6 +319,18 @@ __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const i
     if (lane == 0) cost[g] = c;
 }
 
+// NEXT-2: stage costs of the repair DP, L_t(a, b) = [b != (p_t > threshold)] -- the
+// Hamming distance to the thresholded multiperiod-ACOPF dispatch (SPEC warm_start_uc)
+__global__ void k_hamming_costs(int n, const double *p, double threshold, double *L) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int ut = p[k] > threshold;
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) L[(size_t)k * 4 + a * 2 + b] = (b != ut) ? 1.0 : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------- cold start (S0)
 __global__ void k_init(Dev d, const int8_t *u_init) {
     const int T = d.T;
@@ -388,6 +402,10 @@ cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const 
     k_dp_batch<<<(G + warps - 1) / warps, warps * 32, gen_smem(T, warps), s>>>(G, T, L, tu, td, u0, hold,
                                                                                 sched, cost);
     return cudaGetLastError();
+}
+
+void launch_hamming_costs(int n, const double *p, double threshold, double *L, cudaStream_t s) {
+    k_hamming_costs<<<std::max(1, std::min(592, (n + 255) / 256)), 256, 0, s>>>(n, p, threshold, L);
 }
 
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s) {

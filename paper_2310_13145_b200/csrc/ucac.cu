@@ -393,6 +393,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.tron_maxit = prm->tron_maxit; d.al_maxit = prm->al_maxit;
     d.al_eta_star = prm->al_eta_star; d.al_sigma0_rel = prm->al_sigma0_rel;
     d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
+    d.uc_fixed = prm->uc_fixed;
     d.nblk_bus = nblk_bus(P.Bo, T);
     d.nblk_ubar = nblk_ubar(G, T);
     d.nblk_rows = nblk_rows(L, T);
@@ -957,6 +958,56 @@ extern "C" ucac_status ucac_get_solution(ucac_ctx *ctx, ucac_solution *sol) {
     }
     CK(cudaStreamSynchronize(ctx->s));
     return UCAC_OK;
+}
+
+// NEXT-2: the UC warm start.  The multiperiod ACOPF with every unit on
+// after its held prefix and the schedule held (uc_fixed), `iters` inner iterations; then on the
+// device the Hamming stage costs to [p > threshold] and one batched DP pass (Algorithm 2) give the
+// nearest schedule satisfying Eq. 3.  Single GPU.
+extern "C" ucac_status ucac_uc_warm_start(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *cost,
+                                          const ucac_uc *uc, const ucac_params *prm, int32_t iters,
+                                          double threshold, int8_t *u_out) {
+    if (!net || !hz || !cost || !uc || !prm || !u_out || iters < 0) {
+        g_create_err = "ucac_uc_warm_start: bad arguments";
+        return UCAC_EINVAL;
+    }
+    const int G = net->ngen, T = hz->T;
+    std::vector<int8_t> uinit((size_t)G * T);
+    for (int g = 0; g < G; g++)
+        for (int t = 0; t < T; t++) uinit[(size_t)g * T + t] = t < uc->hold[g] ? (int8_t)uc->u0[g] : (int8_t)1;
+    ucac_uc uc2 = *uc;
+    uc2.u_init = uinit.data();
+    ucac_params p2 = *prm;
+    p2.uc_fixed = 1;
+    ucac_ctx *ctx = nullptr;
+    ucac_status s = ucac_create(net, hz, cost, &uc2, &p2, nullptr, nullptr, &ctx);
+    if (s != UCAC_OK) return s;
+    s = ucac_iterate(ctx, iters, 0, 0.0, nullptr);
+    double *L = nullptr, *c = nullptr;
+    int8_t *sched = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (s == UCAC_OK) {
+        const Dev &d = ctx->d;
+        const size_t GT = (size_t)G * T;
+        if ((e = cudaMallocAsync((void **)&L, GT * 4 * sizeof(double), ctx->s)) == cudaSuccess &&
+            (e = cudaMallocAsync((void **)&c, G * sizeof(double), ctx->s)) == cudaSuccess &&
+            (e = cudaMallocAsync((void **)&sched, GT, ctx->s)) == cudaSuccess) {
+            launch_hamming_costs((int)GT, d.p, threshold, L, ctx->s);
+            e = launch_dp_batch(G, T, L, d.tu, d.td, d.u0, d.hold, sched, c, ctx->s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(u_out, sched, GT, cudaMemcpyDeviceToHost, ctx->s);
+            cudaFreeAsync(L, ctx->s);
+            cudaFreeAsync(c, ctx->s);
+            cudaFreeAsync(sched, ctx->s);
+            cudaError_t e2 = cudaStreamSynchronize(ctx->s);
+            if (e == cudaSuccess) e = e2;
+        }
+        if (e != cudaSuccess) {
+            g_create_err = cudaGetErrorString(e);
+            s = UCAC_ECUDA;
+        }
+    }
+    ucac_destroy(ctx);
+    return s;
 }
 
 extern "C" ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids, int32_t *count) {

@@ -55,6 +55,7 @@ struct Dev {
     double tron_gtol;                 // absolute: tron_gtol_rel * max(rho_pq, rho_va)
     int tron_maxit, al_maxit;
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
+    int uc_fixed;                     // 1: k_gen keeps u (NEXT-2)
 
     // ---- static generator data [G]
     const int *gbus, *tu, *td, *u0, *hold;
@@ -166,6 +167,7 @@ void launch_pack_bus(const Dev &d, cudaStream_t s);
 void launch_unpack_bus(const Dev &d, cudaStream_t s);
 void launch_ubar(const Dev &d, cudaStream_t s);
 void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s);
+void launch_hamming_costs(int n, const double *p, double threshold, double *L, cudaStream_t s);
 cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                             const int *hold, int8_t *sched, double *cost, cudaStream_t s);
 int nblk_bus(int B, int T);

@@ -185,6 +185,7 @@ class Params:
     al_sigma0_rel: float = 10.0
     al_sigma_max_rel: float = 1e3
     al_sigma_decay: float = 0.1
+    uc_fixed: int = 0          # 1: step (7a) keeps u (NEXT-2 warm start's multiperiod ACOPF)
 
 
 # --------------------------------------------------------------------------------------

@@ -59,7 +59,7 @@ class Params(C.Structure):
                 ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
-                ("al_sigma_decay", C.c_double)]
+                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32)]
 
 
 class Dist(C.Structure):
@@ -126,6 +126,9 @@ def _declare(L):
     L.ucac_create.argtypes = [C.POINTER(Network), C.POINTER(Horizon), C.POINTER(Costs), C.POINTER(Uc),
                               C.POINTER(Params), C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
     L.ucac_create.restype = C.c_int
+    L.ucac_uc_warm_start.argtypes = [C.POINTER(Network), C.POINTER(Horizon), C.POINTER(Costs), C.POINTER(Uc),
+                                     C.POINTER(Params), C.c_int32, C.c_double, i8p]
+    L.ucac_uc_warm_start.restype = C.c_int
     L.ucac_iterate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_int32)]
     L.ucac_iterate.restype = C.c_int
     L.ucac_iterate_timed.argtypes = [C.c_void_p, C.c_int32, dp, i64p]
@@ -166,7 +169,7 @@ def _declare(L):
 EXPORTED = ["ucac_create", "ucac_iterate", "ucac_iterate_timed", "ucac_kernel_name", "ucac_residuals",
             "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
-            "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map"]
+            "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start"]
 
 
 def _check(rc, h=None):
@@ -179,7 +182,36 @@ def params_struct(pr) -> Params:
     return Params(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max, pr.beta_max,
                   pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled, pr.tron_gtol_rel,
                   pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel, pr.al_sigma_max_rel,
-                  pr.al_sigma_decay)
+                  pr.al_sigma_decay, pr.uc_fixed)
+
+
+def problem_structs(pb, keep: list):
+    """ucac_network / horizon / costs / uc of a normalized Problem (arrays kept alive in `keep`)."""
+    def a(x, t=dp):
+        x = np.ascontiguousarray(x)
+        keep.append(x)
+        return x.ctypes.data_as(t)
+    net = Network(pb.nbus, pb.ngen, pb.nbranch, pb.ref_bus, pb.base_mva, a(pb.bus_gs), a(pb.bus_bs),
+                  a(pb.bus_vmin), a(pb.bus_vmax), a(pb.br_from, ip), a(pb.br_to, ip), a(pb.br_y.reshape(-1)),
+                  a(pb.br_rate), a(pb.gen_bus, ip), a(pb.pmin), a(pb.pmax), a(pb.qmin), a(pb.qmax))
+    hz = Horizon(pb.T, a(pb.pd.reshape(-1)), a(pb.qd.reshape(-1)))
+    co = Costs(a(pb.c2), a(pb.c1), a(pb.c0), a(pb.csu), a(pb.csd))
+    ui = a(np.ascontiguousarray(pb.u_init, dtype=np.int8).reshape(-1), i8p) if pb.u_init is not None else None
+    uc = Uc(a(pb.ramp_up), a(pb.ramp_dn), a(pb.su_ramp), a(pb.sd_ramp), a(pb.min_up, ip), a(pb.min_dn, ip),
+            a(pb.u0, ip), a(pb.hold, ip), a(pb.p0), ui)
+    return net, hz, co, uc
+
+
+def uc_warm_start(pb, pr, iters: int, threshold: float = 1e-3) -> np.ndarray:
+    """NEXT-2 UC warm start (ucac_uc_warm_start): the schedule [ngen, T] to pass as u_init."""
+    pb = pb.normalized()
+    keep = []
+    net, hz, co, uc = problem_structs(pb, keep)
+    prm = params_struct(pr)
+    u = np.zeros(pb.ngen * pb.T, dtype=np.int8)
+    _check(lib().ucac_uc_warm_start(C.byref(net), C.byref(hz), C.byref(co), C.byref(uc), C.byref(prm), int(iters),
+                                    float(threshold), u.ctypes.data_as(i8p)), None)
+    return u.reshape(pb.ngen, pb.T)
 
 
 class Context:
@@ -197,14 +229,7 @@ class Context:
             x = np.ascontiguousarray(x)
             keep.append(x)
             return x.ctypes.data_as(t)
-        net = Network(pb.nbus, pb.ngen, pb.nbranch, pb.ref_bus, pb.base_mva, a(pb.bus_gs), a(pb.bus_bs),
-                      a(pb.bus_vmin), a(pb.bus_vmax), a(pb.br_from, ip), a(pb.br_to, ip), a(pb.br_y.reshape(-1)),
-                      a(pb.br_rate), a(pb.gen_bus, ip), a(pb.pmin), a(pb.pmax), a(pb.qmin), a(pb.qmax))
-        hz = Horizon(pb.T, a(pb.pd.reshape(-1)), a(pb.qd.reshape(-1)))
-        co = Costs(a(pb.c2), a(pb.c1), a(pb.c0), a(pb.csu), a(pb.csd))
-        ui = a(np.ascontiguousarray(pb.u_init, dtype=np.int8).reshape(-1), i8p) if pb.u_init is not None else None
-        uc = Uc(a(pb.ramp_up), a(pb.ramp_dn), a(pb.su_ramp), a(pb.sd_ramp), a(pb.min_up, ip), a(pb.min_dn, ip),
-                a(pb.u0, ip), a(pb.hold, ip), a(pb.p0), ui)
+        net, hz, co, uc = problem_structs(pb, keep)
         prm = params_struct(pr)
         dist_c = None
         if dist is not None:

@@ -240,3 +240,18 @@ def test_edge_cases():
         ucac.Context(bad, pr)
     with pytest.raises(ucac.UcacError):
         ucac.Context(inputs.case9(T=4), inputs.Params(rho_pq=-1, rho_va=1, rho_uc=1))
+
+
+@pytest.mark.parametrize("name,iters", [("case9", 40), ("case30", 60), ("case118", 40)])
+def test_uc_warm_start_next2(name, iters):
+    """NEXT-2: ucac_uc_warm_start (held-schedule ACOPF on the GPU, device Hamming costs,
+    batched DP) gives the oracle's repaired schedule bit for bit (thresholds taken on p within
+    rounding of the threshold excepted), and the UC-ACOPF run from it keeps parity."""
+    import dataclasses
+    pb, pr = inputs.build_config(name)
+    ug = ucac.uc_warm_start(pb, pr, iters)
+    uo, po = oracle.uc_warm_start(pb, pr, iters)
+    ambiguous = np.abs(po - 1e-3) < 1e-9
+    mism = ug != uo
+    assert not mism.any() or ambiguous.any(), np.argwhere(mism)[:5]
+    run_pair(dataclasses.replace(pb, u_init=ug), pr, 10)
