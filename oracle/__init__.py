@@ -68,7 +68,7 @@ class Params_c(C.Structure):
                 ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
-                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32)]
+                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32)]
 
 
 class Report_c(C.Structure):
@@ -129,7 +129,7 @@ def params_c(pr) -> Params_c:
     return Params_c(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max,
                     pr.beta_max, pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled,
                     pr.tron_gtol_rel, pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel,
-                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed)
+                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed, pr.variant)
 
 
 class Oracle:

@@ -834,13 +834,20 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
     c.y = y; c.tau = tau; c.rpq = rpq; c.rva = rva; c.al = 0;
     c.r2 = rate * rate; c.mu[0] = c.mu[1] = 0.0; c.sig = 0.0;
     int it = 0;
-    int ok = tron(4, x, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it);
+    /* NEXT-3 variant 1 (R47): every rated branch goes straight to the six-variable AL from the
+     * warm start (clipped to the box), as ExaTron solves it; else the 4-variable fast path first */
+    const int al_always = (pr->variant & 1) && rate > 0.0;
+    int ok = 1;
+    if (al_always)
+        for (int i = 0; i < 4; i++) x[i] = clampd(x[i], lo[i], hi[i]);
+    else
+        ok = tron(4, x, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it);
     stats[0] = it; stats[1] = !ok; stats[2] = 0; stats[3] = 0; stats[4] = 0;
     double sig0 = pr->al_sigma0_rel * rpq * c.r2;
     orc_branch_flows(y, x, f, NULL, NULL);
     if (rate > 0.0) {
         double s1 = f[0] * f[0] + f[1] * f[1], s2 = f[2] * f[2] + f[3] * f[3];
-        if (s1 > c.r2 || s2 > c.r2) {
+        if (al_always || s1 > c.r2 || s2 > c.r2) {
             double X[6] = {x[0], x[1], x[2], x[3],
                            clampd(1.0 - s1 / c.r2, 0.0, 1.0), clampd(1.0 - s2 / c.r2, 0.0, 1.0)};
             c.al = 1;
@@ -1256,7 +1263,9 @@ static void one_iteration(orc_ctx *c) {
                     c->fbar[4 * li + (side ? FP_JI : FP_IJ)] = vv[k++];
                     c->fbar[4 * li + (side ? FQ_JI : FQ_IJ)] = vv[k++];
                 }
-                c->wbar[(size_t)i * T + t] = vv[k];
+                /* NEXT-3 variant 2 (R47): SPEC's clip of wbar to the voltage box */
+                c->wbar[(size_t)i * T + t] = (pr->variant & 2)
+                    ? clampd(vv[k], q->bus_vmin[i] * q->bus_vmin[i], q->bus_vmax[i] * q->bus_vmax[i]) : vv[k];
                 c->thbar[(size_t)i * T + t] = (i == q->ref_bus) ? 0.0 : tsum / (double)ne;
             }
         }

@@ -48,6 +48,8 @@ typedef struct {
     int32_t tron_maxit, al_maxit;
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
     int32_t uc_fixed;   /* 1: step (7a) keeps u (the NEXT-2 warm start's multiperiod ACOPF) */
+    int32_t variant;    /* NEXT-3 formulation variants (bitmask, R47): 1 = every rated branch solves the
+                           six-variable AL (no fast path), 2 = wbar clipped to [Vmin^2, Vmax^2] */
 } orc_params;
 
 typedef struct {

@@ -701,21 +701,28 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         double x[4];
 #pragma unroll
         for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
-        int it = 0;
-        bool ok = tron<4>(F4, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
-        c_it = it;
-        c_cap = !ok;
-        double C, S, f0, f1, f2, f3;
-        F4.flows(x, C, S, f0, f1, f2, f3);
         const double rate = d.rate[k / d.T];
         const double r2 = rate * rate;
+        // NEXT-3 variant 1 (R47): every rated branch goes straight to the AL from the clipped warm start
+        const bool al_always = (d.variant & 1) && rate > 0.0;
+        if (al_always) {
+#pragma unroll
+            for (int m = 0; m < 4; m++) x[m] = clampd(x[m], lo[m], hi[m]);
+        } else {
+            int it = 0;
+            const bool ok = tron<4>(F4, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
+            c_it = it;
+            c_cap = !ok;
+        }
+        double C, S, f0, f1, f2, f3;
+        F4.flows(x, C, S, f0, f1, f2, f3);
 #pragma unroll
         for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
         d.f[0 * LTs + k] = f0;
         d.f[1 * LTs + k] = f1;
         d.f[2 * LTs + k] = f2;
         d.f[3 * LTs + k] = f3;
-        if (rate > 0.0 && (f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2)) {
+        if (rate > 0.0 && (al_always || f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2)) {
             const unsigned pos = atomicAdd(d.alq_cnt, 1u);
             d.alq[pos] = k;
             // mark both end buses and every branch end at them: their bus solve and end rows move

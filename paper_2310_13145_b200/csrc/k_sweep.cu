@@ -341,7 +341,11 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
                 if (pending) LG(G_RC, gi + 1) = lr;
             }
         }
-        const double wb = thw + (alw * muP + bew * muQ) / aw;
+        double wb = thw + (alw * muP + bew * muQ) / aw;
+        if (d.variant & 2) {   // NEXT-3 variant 2 (R47): SPEC's clip of wbar to the voltage box
+            const double vl = d.vmin[i] * d.vmin[i], vh = d.vmax[i] * d.vmax[i];
+            wb = wb < vl ? vl : (wb > vh ? vh : wb);
+        }
         const double tb = (i == d.ref_bus) ? 0.0 : tsum / (double)ne;
         d.wbar[k] = wb;
         d.thbar[k] = tb;

@@ -394,6 +394,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.al_eta_star = prm->al_eta_star; d.al_sigma0_rel = prm->al_sigma0_rel;
     d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
     d.uc_fixed = prm->uc_fixed;
+    d.variant = prm->variant;
     d.nblk_bus = nblk_bus(P.Bo, T);
     d.nblk_ubar = nblk_ubar(G, T);
     d.nblk_rows = nblk_rows(L, T);

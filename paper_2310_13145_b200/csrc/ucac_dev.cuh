@@ -56,6 +56,7 @@ struct Dev {
     int tron_maxit, al_maxit;
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
     int uc_fixed;                     // 1: k_gen keeps u (NEXT-2)
+    int variant;                      // NEXT-3 bitmask: 1 = AL for every rated branch, 2 = wbar clip
 
     // ---- static generator data [G]
     const int *gbus, *tu, *td, *u0, *hold;

@@ -221,3 +221,58 @@ def test_consensus_fixed_point():
     assert res < 1e-5
     for k in ("p", "q", "pbar", "qbar", "wbar", "x", "f"):
         assert np.allclose(s0[k], s1[k], atol=100 * res), k
+
+
+def test_variant_wbar_clip_keeps_voltage_box():
+    """NEXT-3 variant 2 (R47): with SPEC's clip every bus copy w-bar lies in [Vmin^2, Vmax^2];
+    without it the exact bus QP may leave the box (A8)."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    o = oracle.Oracle(pb, dataclasses.replace(pr, variant=2))
+    o.iterate(15)
+    w = o.get_state()["wbar"].reshape(pb.nbus, pb.T)
+    lo, hi = (pb.bus_vmin ** 2)[:, None], (pb.bus_vmax ** 2)[:, None]
+    assert np.all(w >= lo) and np.all(w <= hi)
+
+
+def test_variant_al_always_every_rated_branch_takes_the_al():
+    """NEXT-3 variant 1 (R47): every rated (l,t) solves the AL each iteration."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    o = oracle.Oracle(pb, dataclasses.replace(pr, variant=1))
+    o.iterate(2)
+    rated = int(np.sum(pb.br_rate > 0)) * pb.T
+    assert o.report()["al_active"] == 2 * rated
+
+
+def _ulp_response(pr, iters=2, seed=0):
+    pb = inputs.build_config("case30")[0]
+    o = oracle.Oracle(pb, pr)
+    o.iterate(iters)
+    st = o.get_state()
+    o.close()
+    rng = np.random.default_rng(seed)
+    pert = {k: (v * (1 + rng.choice([-1.0, 1.0], v.shape) * 2.0 ** -52) if v.dtype == np.float64 and k != "scal" else v)
+            for k, v in st.items()}
+    xs = []
+    for s in (st, pert):
+        a = oracle.Oracle(pb, pr)
+        a.set_state(s)
+        a.iterate(1)
+        xs.append(a.get_state()["x"].reshape(-1, 4))
+        a.close()
+    scale = np.maximum(np.abs(xs[0]), np.sqrt(np.mean(xs[0] ** 2, axis=0)))
+    return float(np.max(np.abs(xs[1] - xs[0]) / scale))
+
+
+def test_variant1_conditioning():
+    """DESIGN.md 10 / R47: the oracle's own response to a one-ulp perturbation of its input state
+    is at rounding level for the default formulation and bounded (<= 1e-8) for variant 1, whose
+    slack-form AL of inactive lines is ill-conditioned.  The GPU parity tolerance for variant 1 is
+    10x this measured response, so this pins that it cannot hide a default-path error."""
+    import dataclasses
+    pr = inputs.build_config("case30")[1]
+    r0 = _ulp_response(pr)
+    r1 = _ulp_response(dataclasses.replace(pr, variant=1))
+    assert r0 < 1e-13, r0
+    assert 1e-13 < r1 < 1e-8, r1
