@@ -9,10 +9,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -174,6 +177,7 @@ struct ucac_ctx {
     int gunroll[2] = {1, 16};
     std::vector<void *> dalloc;
     DevStatus *st_host = nullptr;        // pinned mirror
+    double *xpose = nullptr;             // [4 LT] scratch for SoA -> AoS read-back
     std::string err;
     std::vector<cudaEvent_t> tev;        // timed-iteration event pool
     ucac_params prm{};
@@ -209,21 +213,51 @@ static ucac_status fail(ucac_ctx *ctx, ucac_status s, const char *fmt, ...) {
 }
 
 template <class Tp>
-static Tp *dnew(ucac_ctx *ctx, size_t n, cudaError_t &e) {
-    void *p = nullptr;
-    e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(Tp));
-    if (e == cudaSuccess) {
-        ctx->dalloc.push_back(p);
-        e = cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(Tp), ctx->s);
-    }
-    return (Tp *)p;
-}
-
-template <class Tp>
 static cudaError_t up(ucac_ctx *ctx, Tp *dst, const Tp *src, size_t n) {
     if (n == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, n * sizeof(Tp), cudaMemcpyHostToDevice, ctx->s);
 }
+
+// Pinned DevStatus buffers are recycled across contexts: a page-locked allocation costs
+// milliseconds, a context needs one small buffer.
+static std::mutex g_pinned_mu;
+static std::vector<DevStatus *> g_pinned_free;
+static DevStatus *pinned_status_get() {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        if (!g_pinned_free.empty()) {
+            DevStatus *p = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return p;
+        }
+    }
+    void *p = nullptr;
+    return cudaMallocHost(&p, sizeof(DevStatus)) == cudaSuccess ? (DevStatus *)p : nullptr;
+}
+static void pinned_status_put(DevStatus *p) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back(p);
+}
+
+// Bump allocator over one device allocation: 256-byte aligned slices.  With base == 0 it only
+// measures (the sizing pass); with `stage` set, put() also copies the host vector into the
+// staging image at the slice's offset.
+struct Arena {
+    uintptr_t base = 0;
+    size_t off = 0, up_end = 0;
+    char *stage = nullptr;
+    template <class Tp> Tp *take(size_t n) {
+        const size_t o = (off + 255) & ~(size_t)255;
+        off = o + std::max<size_t>(n, 1) * sizeof(Tp);
+        return base ? (Tp *)(base + o) : nullptr;
+    }
+    template <class Tp> Tp *put(const std::vector<Tp> &v) {
+        const size_t o = (off + 255) & ~(size_t)255;
+        Tp *p = take<Tp>(v.size());
+        if (stage && !v.empty()) memcpy(stage + o, v.data(), v.size() * sizeof(Tp));
+        return p;
+    }
+};
 
 static bool finite_all(const double *a, size_t n) {
     for (size_t i = 0; i < n; i++)
@@ -304,7 +338,17 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
                                    void *cuda_stream, ucac_ctx **out) {
     if (!out) return fail(nullptr, UCAC_EINVAL, "out is NULL");
     *out = nullptr;
+    // UCAC_CREATE_TRACE=1: phase times of ucac_create on stderr (diagnostics)
+    static const bool trace = getenv("UCAC_CREATE_TRACE") != nullptr;
+    auto tp0 = std::chrono::steady_clock::now(), tpl = tp0;
+    auto mark = [&](const char *what) {
+        if (!trace) return;
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "ucac_create %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tpl).count());
+        tpl = now;
+    };
     ucac_status vs = validate(net, hz, co, uc, prm);
+    mark("validate");
     if (vs != UCAC_OK) return vs;
     const int nranks = dist ? dist->nranks : 1;
     const int rank = dist ? dist->rank : 0;
@@ -315,10 +359,11 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
-    cudaDeviceProp prop;
-    e = cudaGetDeviceProperties(&prop, dev);
+    int cc_major = 0, cc_minor = 0;
+    e = cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
     if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "%s", cudaGetErrorString(e));
-    if (prop.major != 10) return fail(nullptr, UCAC_ECUDA, "libucac is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+    if (cc_major != 10) return fail(nullptr, UCAC_ECUDA, "libucac is built for sm_100a; device is sm_%d%d", cc_major, cc_minor);
 
     std::vector<int32_t> part;
     if (nranks > 1) {
@@ -337,7 +382,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ctx->nranks = nranks;
     ctx->rank = rank;
     ctx->comm_mode = dist && nranks > 1 ? dist->comm_mode : 0;
+    mark("device/part");
     ctx->P = build_local(net, hz, co, uc, part.data(), nranks, rank);
+    mark("build_local");
     Local &P = ctx->P;
     const int B = P.B, G = P.G, L = P.L, T = P.T;
     ctx->B = P.Bo;
@@ -363,7 +410,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         cudaEventCreateWithFlags(&ctx->ev_genx, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_early, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
-    if (cudaMallocHost(&ctx->st_host, sizeof(DevStatus)) != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
+    mark("streams");
+    if ((ctx->st_host = pinned_status_get()) == nullptr) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
+    mark("pinned");
     memset(ctx->st_host, 0, sizeof(DevStatus));
     if (nranks > 1 && ctx->comm_mode == 0) {
         ncclUniqueId id;
@@ -400,114 +449,117 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.nblk_rows = nblk_rows(L, T);
 
     const size_t GT = (size_t)G * T, LT = (size_t)L * T, BT = (size_t)B * T;
-#define ALLOC(field, type, n)                                   \
-    do {                                                        \
-        auto p_ = dnew<type>(ctx, (n), e);                      \
-        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc %s", #field)); \
-        d.field = p_;                                           \
-    } while (0)
-#define UPLOAD(field, type, vec)                                \
-    do {                                                        \
-        type *p_ = dnew<type>(ctx, (vec).size(), e);            \
-        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc %s", #field)); \
-        if (up<type>(ctx, p_, (vec).data(), (vec).size()) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "upload %s", #field)); \
-        d.field = p_;                                           \
-    } while (0)
-    UPLOAD(gbus, int, P.gbus);
-    UPLOAD(tu, int, P.tu);
-    UPLOAD(td, int, P.td);
-    UPLOAD(u0, int, P.u0);
-    UPLOAD(hold, int, P.hold);
-    UPLOAD(pmin, double, P.pmin);
-    UPLOAD(pmax, double, P.pmax);
-    UPLOAD(qmin, double, P.qmin);
-    UPLOAD(qmax, double, P.qmax);
-    UPLOAD(c2, double, P.c2);
-    UPLOAD(c1, double, P.c1);
-    UPLOAD(c0, double, P.c0);
-    UPLOAD(csu, double, P.csu);
-    UPLOAD(csd, double, P.csd);
-    UPLOAD(rup, double, P.rup);
-    UPLOAD(rdn, double, P.rdn);
-    UPLOAD(sup, double, P.sup);
-    UPLOAD(sdn, double, P.sdn);
-    UPLOAD(p0, double, P.p0);
-    UPLOAD(y, double, P.ysoa);
-    UPLOAD(rate, double, P.rate);
-    UPLOAD(bfrom, int, P.from);
-    UPLOAD(bto, int, P.to);
-    UPLOAD(gs, double, P.gs);
-    UPLOAD(bs, double, P.bs);
-    UPLOAD(vmin, double, P.vmin);
-    UPLOAD(vmax, double, P.vmax);
-    UPLOAD(pd, double, P.pdT);
-    UPLOAD(qd, double, P.qdT);
-    UPLOAD(bg_ptr, int, P.bgp);
-    UPLOAD(bg_idx, int, P.bgi);
-    UPLOAD(be_ptr, int, P.bep);
-    UPLOAD(be_idx, int, P.bei);
-    UPLOAD(cut_local, int, P.cut_local);
-    UPLOAD(export_local, int, P.export_local);
-    UPLOAD(phantom_src, int, P.phantom_src);
-    UPLOAD(ghost_src, int, P.ghost_src);
-    // iterate
-    ALLOC(u, int8_t, GT);
-    ALLOC(p, double, GT);
-    ALLOC(q, double, GT);
-    ALLOC(ph, double, GT);
-    ALLOC(ub_on, double, GT);
-    ALLOC(ub_su, double, GT);
-    ALLOC(ub_sd, double, GT);
-    ALLOC(pbar, double, GT);
-    ALLOC(qbar, double, GT);
-    ALLOC(zg, double, NGROW * GT);
-    ALLOC(yg, double, NGROW * GT);
-    ALLOC(lg, double, NGROW * GT);
-    ALLOC(x, double, 4 * LT);
-    ALLOC(f, double, 4 * LT);
-    ALLOC(fbar, double, 4 * LT);
-    ALLOC(al, double, 3 * LT);
-    ALLOC(zb, double, NBROW * LT);
-    ALLOC(yb, double, NBROW * LT);
-    ALLOC(lb, double, NBROW * LT);
-    ALLOC(wbar, double, BT);
-    ALLOC(thbar, double, BT);
-    ALLOC(part_bus, double, (size_t)d.nblk_bus * NPART);
-    ALLOC(part_ubar, double, (size_t)d.nblk_ubar * NPART);
-    ALLOC(part_rows, double, (size_t)d.nblk_rows * NPART);
-    d.nblk_lbus = nblk_late(P.Bo * T);
-    d.nblk_lrows = nblk_late(L * T);
-    ALLOC(part_lbus, double, (size_t)d.nblk_lbus * NPART);
-    ALLOC(part_lrows, double, (size_t)d.nblk_lrows * NPART);
-    ALLOC(part_efold, double, (size_t)fold_blocks() * NPART);
-    ALLOC(rec_part, double, 3 * NPART);
-    ALLOC(kdone, unsigned, 3);
-    ALLOC(bmark, unsigned, BT);
-    {
-        auto r0 = dnew<unsigned>(ctx, (size_t)(L + P.Lp) * T, e);
-        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc rmark"));
-        auto r1 = dnew<unsigned>(ctx, (size_t)(L + P.Lp) * T, e);
-        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc rmark"));
-        d.rmark[0] = r0;
-        d.rmark[1] = r1;
-    }
-    ALLOC(tauh, double, (size_t)NBROW * (L + P.Lp) * T);
-    ALLOC(bmu, double, 4 * BT);
-    ALLOC(cnt, unsigned long long, NCNT);
-    ALLOC(alq, int, LT);
-    ALLOC(alq_cnt, unsigned, 2);
-    ALLOC(rec, double, NREC);
-    ALLOC(tl, unsigned long long, 2 * NKERN);
-    ALLOC(xsend1, double, (size_t)P.max_cut * 4 * T);
-    ALLOC(xrecv1, double, (size_t)nranks * P.max_cut * 4 * T);
-    ALLOC(xsend2, double, (size_t)P.max_export * 6 * T);
-    ALLOC(xrecv2, double, (size_t)nranks * P.max_export * 6 * T);
-    ALLOC(st, DevStatus, 1);
+    // One device arena for every array of the context: the uploaded inputs form
+    // its prefix, staged contiguously on the host and sent with one copy; the rest is zeroed with
+    // one memset.  A first pass over the same layout sizes it.
     int8_t *uinit = nullptr;
-    if (!P.uinit.empty()) {
-        uinit = dnew<int8_t>(ctx, GT, e);
-        if (e != cudaSuccess || up<int8_t>(ctx, uinit, P.uinit.data(), GT) != cudaSuccess)
-            return bail(fail(ctx, UCAC_ECUDA, "u_init upload"));
+    auto layout = [&](Arena &A) {
+        d.gbus = A.put(P.gbus);
+        d.tu = A.put(P.tu);
+        d.td = A.put(P.td);
+        d.u0 = A.put(P.u0);
+        d.hold = A.put(P.hold);
+        d.pmin = A.put(P.pmin);
+        d.pmax = A.put(P.pmax);
+        d.qmin = A.put(P.qmin);
+        d.qmax = A.put(P.qmax);
+        d.c2 = A.put(P.c2);
+        d.c1 = A.put(P.c1);
+        d.c0 = A.put(P.c0);
+        d.csu = A.put(P.csu);
+        d.csd = A.put(P.csd);
+        d.rup = A.put(P.rup);
+        d.rdn = A.put(P.rdn);
+        d.sup = A.put(P.sup);
+        d.sdn = A.put(P.sdn);
+        d.p0 = A.put(P.p0);
+        d.y = A.put(P.ysoa);
+        d.rate = A.put(P.rate);
+        d.bfrom = A.put(P.from);
+        d.bto = A.put(P.to);
+        d.gs = A.put(P.gs);
+        d.bs = A.put(P.bs);
+        d.vmin = A.put(P.vmin);
+        d.vmax = A.put(P.vmax);
+        d.pd = A.put(P.pdT);
+        d.qd = A.put(P.qdT);
+        d.bg_ptr = A.put(P.bgp);
+        d.bg_idx = A.put(P.bgi);
+        d.be_ptr = A.put(P.bep);
+        d.be_idx = A.put(P.bei);
+        d.cut_local = A.put(P.cut_local);
+        d.export_local = A.put(P.export_local);
+        d.phantom_src = A.put(P.phantom_src);
+        d.ghost_src = A.put(P.ghost_src);
+        uinit = P.uinit.empty() ? nullptr : A.put(P.uinit);
+        A.up_end = A.off;
+        // iterate (zeroed, then set by launch_init)
+        d.u = A.take<int8_t>(GT);
+        d.p = A.take<double>(GT);
+        d.q = A.take<double>(GT);
+        d.ph = A.take<double>(GT);
+        d.ub_on = A.take<double>(GT);
+        d.ub_su = A.take<double>(GT);
+        d.ub_sd = A.take<double>(GT);
+        d.pbar = A.take<double>(GT);
+        d.qbar = A.take<double>(GT);
+        d.zg = A.take<double>(NGROW * GT);
+        d.yg = A.take<double>(NGROW * GT);
+        d.lg = A.take<double>(NGROW * GT);
+        d.x = A.take<double>(4 * LT);
+        d.f = A.take<double>(4 * LT);
+        d.fbar = A.take<double>(4 * LT);
+        d.al = A.take<double>(3 * LT);
+        d.zb = A.take<double>(NBROW * LT);
+        d.yb = A.take<double>(NBROW * LT);
+        d.lb = A.take<double>(NBROW * LT);
+        d.wbar = A.take<double>(BT);
+        d.thbar = A.take<double>(BT);
+        d.part_bus = A.take<double>((size_t)d.nblk_bus * NPART);
+        d.part_ubar = A.take<double>((size_t)d.nblk_ubar * NPART);
+        d.part_rows = A.take<double>((size_t)d.nblk_rows * NPART);
+        d.nblk_lbus = nblk_late(P.Bo * T);
+        d.nblk_lrows = nblk_late(L * T);
+        d.part_lbus = A.take<double>((size_t)d.nblk_lbus * NPART);
+        d.part_lrows = A.take<double>((size_t)d.nblk_lrows * NPART);
+        d.part_efold = A.take<double>((size_t)fold_blocks() * NPART);
+        d.rec_part = A.take<double>(3 * NPART);
+        d.kdone = A.take<unsigned>(3);
+        d.bmark = A.take<unsigned>(BT);
+        d.tauh = A.take<double>((size_t)NBROW * (L + P.Lp) * T);
+        d.bmu = A.take<double>(4 * BT);
+        d.cnt = A.take<unsigned long long>(NCNT);
+        d.alq = A.take<int>(LT);
+        d.alq_cnt = A.take<unsigned>(2);
+        d.rec = A.take<double>(NREC);
+        d.tl = A.take<unsigned long long>(2 * NKERN);
+        d.xsend1 = A.take<double>((size_t)P.max_cut * 4 * T);
+        d.xrecv1 = A.take<double>((size_t)nranks * P.max_cut * 4 * T);
+        d.xsend2 = A.take<double>((size_t)P.max_export * 6 * T);
+        d.xrecv2 = A.take<double>((size_t)nranks * P.max_export * 6 * T);
+        d.st = A.take<DevStatus>(1);
+        d.rmark[0] = A.take<unsigned>((size_t)(L + P.Lp) * T);
+        d.rmark[1] = A.take<unsigned>((size_t)(L + P.Lp) * T);
+        ctx->xpose = A.take<double>(4 * LT);
+    };
+    {
+        mark("setup");
+        Arena sizing;
+        layout(sizing);
+        void *base = nullptr;
+        e = cudaMalloc(&base, sizing.off);
+        if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc arena of %zu B", sizing.off));
+        ctx->dalloc.push_back(base);
+        std::vector<char> stage(sizing.up_end, 0);
+        Arena A;
+        A.base = (uintptr_t)base;
+        A.stage = stage.data();
+        layout(A);
+        if (cudaMemcpyAsync(base, stage.data(), A.up_end, cudaMemcpyHostToDevice, ctx->s) != cudaSuccess ||
+            cudaMemsetAsync((char *)base + A.up_end, 0, A.off - A.up_end, ctx->s) != cudaSuccess)
+            return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
+        // the pageable staging buffer must outlive the copy
+        if (cudaStreamSynchronize(ctx->s) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
     }
     // status: beta = beta0, k = 1 (R21)
     DevStatus st0{};
@@ -517,15 +569,18 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     if (cudaMemcpyAsync(d.st, ctx->st_host, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "status upload"));
     if (gen_set_smem_attr(T) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "T=%d needs %zu B of shared memory", T, gen_smem_bytes(T)));
+    mark("arena");
     launch_init(d, uinit, ctx->s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init kernel: %s", cudaGetErrorString(e)));
     e = cudaStreamSynchronize(ctx->s);
     if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init: %s", cudaGetErrorString(e)));
     if (!(nranks > 1 && ctx->comm_mode == 1)) {
+        mark("init");
         ucac_status gs = build_graphs(ctx);
         if (gs != UCAC_OK) return bail(gs);
     }
+    mark("graphs");
     *out = ctx;
     return UCAC_OK;
 #undef ALLOC
@@ -841,12 +896,19 @@ static cudaError_t down(ucac_ctx *ctx, Tp *dst, const Tp *src, size_t n) {
 }
 
 // [K][n] device SoA <-> [n][K] canonical host
+// out[j] = in[(j % K) * n + j / K]: one coalesced write per output element
+__global__ void k_soa_to_aos(const double *__restrict__ in, double *__restrict__ out, size_t n, int K) {
+    const size_t N = n * (size_t)K;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < N; j += (size_t)gridDim.x * blockDim.x)
+        out[j] = in[(j % K) * n + j / K];
+}
 static ucac_status soa_to_aos(ucac_ctx *ctx, double *host, const double *dev, size_t n, int K) {
-    std::vector<double> tmp(n * K);
-    CK(down(ctx, tmp.data(), dev, n * K));
+    if (n == 0) return UCAC_OK;
+    // transposed on the device into the context's scratch, then one copy
+    k_soa_to_aos<<<148 * 8, 256, 0, ctx->s>>>(dev, ctx->xpose, n, K);
+    CK(cudaGetLastError());
+    CK(down(ctx, host, (const double *)ctx->xpose, n * K));
     CK(cudaStreamSynchronize(ctx->s));
-    for (size_t i = 0; i < n; i++)
-        for (int k = 0; k < K; k++) host[i * K + k] = tmp[(size_t)k * n + i];
     return UCAC_OK;
 }
 static ucac_status aos_to_soa(ucac_ctx *ctx, double *dev, const double *host, size_t n, int K) {
@@ -1127,7 +1189,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     for (auto ev : ctx->tev) cudaEventDestroy(ev);
     for (void *p : ctx->dalloc) cudaFree(p);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
-    if (ctx->st_host) cudaFreeHost(ctx->st_host);
+    if (ctx->st_host) pinned_status_put(ctx->st_host);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->ev_genx) cudaEventDestroy(ctx->ev_genx);
