@@ -454,20 +454,29 @@ def main():
 
     # ---- e2e: the public API from host buffers (create = H2D of the problem, iterate,
     #      residuals + solution = D2H), per step = one inner iteration, max over ranks
-    barrier()
-    t0 = time.perf_counter()
-    ctx2 = ucac.Context(pb, pr, dist=make_dist())
-    ctx2.iterate(args.steps)
-    _ = ctx2.report()
-    sol = ctx2.solution()
-    t1 = time.perf_counter()
-    ctx2.close()
-    e2e_s = allmax(t1 - t0)
+    def e2e_run():
+        barrier()
+        t0 = time.perf_counter()
+        c2 = ucac.Context(pb, pr, dist=make_dist())
+        ta = time.perf_counter()
+        c2.iterate(args.steps)
+        _ = c2.report()
+        tb = time.perf_counter()
+        sol_ = c2.solution()
+        t1 = time.perf_counter()
+        c2.close()
+        return t1 - t0, sol_, {"create_ms": 1e3 * (ta - t0), "iterate_report_ms": 1e3 * (tb - ta),
+                               "solution_ms": 1e3 * (t1 - tb)}
+
+    e2e_run()   # untimed warm-up of the public-API path (first-call driver work)
+    dt, sol, parts = e2e_run()
+    e2e_s = allmax(dt)
     h2d = problem_bytes(pb.normalized()) * world
     d2h = allsum(sum(v.nbytes for v in sol.values()) + 200)
     e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
            "d2h_bytes_per_step": int(d2h / args.steps),
-           "note": "ucac_create(host arrays) + ucac_iterate(K) + ucac_residuals + ucac_get_solution, wall clock"}
+           "note": "ucac_create(host arrays) + ucac_iterate(K) + ucac_residuals + ucac_get_solution, wall clock, "
+                   "after one untimed warm-up run of the same calls", "parts_rank0": parts}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

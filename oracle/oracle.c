@@ -479,7 +479,7 @@ static double qmodel(int n, const double *g, const double *H, const double *s) {
  * specified in DESIGN.md 5.3 (constants R10).  Returns 1 if ||P(x-g)-x||_inf <= gtol. */
 static const double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
 static const double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-12;
-static const double TR_EPSF = 1e-10, TR_STALL = 1e-14;
+static const double TR_EPSF = 1e-10, TR_STALL = 1e-13;   /* R48 */
 
 static void pstep(int n, const double *x, const double *lo, const double *hi,
                   const double *d, double a, double *s) {
@@ -627,7 +627,8 @@ static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn 
         for (int i = 0; i < n; i++) gq[i] = g[i] + Hs[i];
         steihaug(n, H, gq, fr, sc, delta, w);
         prsrch(n, x, lo, hi, g, H, sc, w, s);
-        /* stall: a step at the rounding level of x means the gradient floor is reached */
+        /* stall: a step below 1e-13 (1 + |x|) means the rounding floor of the gradient is reached;
+         * for the AL's sigma J'J curvature that floor lies above gtol (R48) */
         {
             double xm = 0.0;
             for (int i = 0; i < n; i++) xm = dmax(xm, fabs(x[i]));
@@ -838,6 +839,9 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
      * warm start (clipped to the box), as ExaTron solves it; else the 4-variable fast path first */
     const int al_always = (pr->variant & 1) && rate > 0.0;
     int ok = 1;
+    /* the previous iterate, clipped to the box: the second candidate start of the AL (R49) */
+    double xprev[4];
+    for (int i = 0; i < 4; i++) xprev[i] = clampd(x[i], lo[i], hi[i]);
     if (al_always)
         for (int i = 0; i < 4; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     else
@@ -857,6 +861,19 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
             double hprev = INFINITY;
             int k;
             stats[2] = 1;
+            {
+                /* R49: round 1 starts from whichever of the fast-path point and the previous
+                 * iterate (each with its slacks from its flows) has the lower AL value */
+                double fp[4], Xp[6], Fa, Fb, gs[6], Hs[36];
+                orc_branch_flows(y, xprev, fp, NULL, NULL);
+                for (int i = 0; i < 4; i++) Xp[i] = xprev[i];
+                Xp[4] = clampd(1.0 - (fp[0] * fp[0] + fp[1] * fp[1]) / c.r2, 0.0, 1.0);
+                Xp[5] = clampd(1.0 - (fp[2] * fp[2] + fp[3] * fp[3]) / c.r2, 0.0, 1.0);
+                br_eval(&c, X, &Fa, gs, Hs);
+                br_eval(&c, Xp, &Fb, gs, Hs);
+                if (Fb < Fa)
+                    for (int i = 0; i < 6; i++) X[i] = Xp[i];
+            }
             for (k = 0; k < pr->al_maxit; k++) {
                 /* round 1 starts at the fast-path point, which violates Eq. 2c-2d: a small first
                  * trust region (R44) keeps the first model step where sigma h^2 is modelled well */

@@ -34,7 +34,7 @@ namespace {
 
 constexpr double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
 constexpr double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-12;
-constexpr double TR_EPSF = 1e-10, TR_STALL = 1e-14;
+constexpr double TR_EPSF = 1e-10, TR_STALL = 1e-13;   // R48
 constexpr double TWO_PI = 6.283185307179586;
 
 template <bool AL>
@@ -716,15 +716,22 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         }
         double C, S, f0, f1, f2, f3;
         F4.flows(x, C, S, f0, f1, f2, f3);
+        const bool queue = rate > 0.0 && (al_always || f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2);
+        unsigned pos = 0;
+        if (queue) {
+            pos = atomicAdd(d.alq_cnt, 1u);
+            d.alq[pos] = k;
+            // the previous iterate (still in d.x): the AL's second candidate start (R49)
+#pragma unroll
+            for (int m = 0; m < 4; m++) d.alq_x[m * LTs + pos] = d.x[m * LTs + k];
+        }
 #pragma unroll
         for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
         d.f[0 * LTs + k] = f0;
         d.f[1 * LTs + k] = f1;
         d.f[2 * LTs + k] = f2;
         d.f[3 * LTs + k] = f3;
-        if (rate > 0.0 && (al_always || f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2)) {
-            const unsigned pos = atomicAdd(d.alq_cnt, 1u);
-            d.alq[pos] = k;
+        if (queue) {
             // mark both end buses and every branch end at them: their bus solve and end rows move
             // to the late phase, after the AL tail
             const int l = k / d.T, t = k - l * d.T;
@@ -807,6 +814,21 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
         }
         double mu0 = d.al[0 * LTs + k], mu1 = d.al[1 * LTs + k];
         double sig = fmax(sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
+        {
+            // R49: round 1 starts from whichever of the fast-path point and the previous iterate
+            // (each with its slacks from its flows) has the lower AL value
+            double xp[6], C0, S0, p0, p1, p2, p3;
+#pragma unroll
+            for (int m = 0; m < 4; m++) xp[m] = clampd(d.alq_x[m * LTs + idx], lo[m], hi[m]);
+            F6.flows(xp, C0, S0, p0, p1, p2, p3);
+            xp[4] = clampd(1.0 - (p0 * p0 + p1 * p1) / r2, 0.0, 1.0);
+            xp[5] = clampd(1.0 - (p2 * p2 + p3 * p3) / r2, 0.0, 1.0);
+            F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
+            if (F6.value(xp) < F6.value(x)) {
+#pragma unroll
+                for (int m = 0; m < 6; m++) x[m] = xp[m];
+            }
+        }
         const double smax = d.al_sigma_max_rel * sig0;
         double hprev = INFINITY;
         double C, S, f0, f1, f2, f3;

@@ -531,6 +531,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.cnt = A.take<unsigned long long>(NCNT);
         d.alq = A.take<int>(LT);
         d.alq_cnt = A.take<unsigned>(2);
+        d.alq_x = A.take<double>(4 * LT);
         d.rec = A.take<double>(NREC);
         d.tl = A.take<unsigned long long>(2 * NKERN);
         d.xsend1 = A.take<double>((size_t)P.max_cut * 4 * T);

@@ -109,6 +109,7 @@ struct Dev {
     double *rec_part;                 // [3][NPART] folded records: early, bus late, rows late
     unsigned *kdone;                  // [3] last-block counters of the kernels producing them
     unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
+    double *alq_x;                    // [4][L*T] by queue position: the previous x of a queued solve (R49)
     DevStatus *st;
     unsigned long long *tl;           // [2*NKERN] diagnostic timeline (UCAC_PROF builds only)
 };
