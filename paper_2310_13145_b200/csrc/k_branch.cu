@@ -630,7 +630,9 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
                           d.wbar[wi], d.wbar[wj], d.thbar[wi], d.thbar[wj]};
 #pragma unroll
     for (int r = 0; r < 8; r++) {
-        const double z = d.zb[r * LTs + k], yr = d.yb[r * LTs + k] / (r < 4 ? d.rpq : d.rva);
+        // y * (1/rho) instead of y / rho: within one ulp of the oracle's quotient, and no division
+        // (whose slow-path call made the compiler spill around each of the eight loads)
+        const double z = d.zb[r * LTs + k], yr = d.yb[r * LTs + k] * (r < 4 ? d.irpq : d.irva);
         F.tau[r] = xb[r] - z - yr;
         if (zs) {
             zs[r * ss] = z;
@@ -648,8 +650,8 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
 // appended to the AL queue and finished by k_branch_al (R9); the rest are final here.
 // Bus-side targets of the 8 rows of solve k for step (7d): tauhat = x-part + z + y/rho
 // (DESIGN.md 5.5), written right after the solve so the bus kernel reads 4 values per incident
-// end instead of the row state.  (x + z) + y/rho has no multiply-add to contract, so this is
-// the same value the oracle forms.
+// end instead of the row state.  y/rho is formed as y * (1/rho) (within one ulp of the
+// oracle's quotient).
 __device__ __forceinline__ void emit_tauhat_zy(const Dev &d, int k, const double *x, double f0, double f1,
                                                double f2, double f3, const double *zs, const double *ys, int ss) {
     const size_t LTH = (size_t)(d.L + d.Lph) * d.T;      // tauhat kind stride includes phantom branches
@@ -664,8 +666,7 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
     const double xs[8] = {f0, f1, f2, f3, x[0], x[1], x[2], x[3]};
 #pragma unroll
     for (int r = 0; r < 8; r++) {
-        const double rho = r < 4 ? d.rpq : d.rva;
-        d.tauh[r * LTH + k] = xs[r] + d.zb[r * LTs + k] + d.yb[r * LTs + k] / rho;
+        d.tauh[r * LTH + k] = xs[r] + d.zb[r * LTs + k] + d.yb[r * LTs + k] * (r < 4 ? d.irpq : d.irva);
     }
 }
 

@@ -435,6 +435,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.ref_bus = P.ref;
     d.S = P.S;
     d.rpq = prm->rho_pq; d.rva = prm->rho_va; d.ruc = prm->rho_uc;
+    d.irpq = 1.0 / prm->rho_pq; d.irva = 1.0 / prm->rho_va;
     d.tau = prm->tau; d.theta = prm->theta; d.lambda_max = prm->lambda_max; d.beta_max = prm->beta_max;
     d.eps_inner_abs = prm->eps_inner_abs;
     d.inner_min = prm->inner_min; d.inner_cap = prm->inner_cap; d.outer_enabled = prm->outer_enabled;

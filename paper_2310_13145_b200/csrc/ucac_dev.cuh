@@ -50,6 +50,7 @@ struct Dev {
     int nblk_bus, nblk_ubar, nblk_rows;
     double S;                         // base MVA
     double rpq, rva, ruc;             // rho classes
+    double irpq, irva;                // 1/rho_pq, 1/rho_va: the branch kernels form y/rho as y * (1/rho)
     double tau, theta, lambda_max, beta_max, eps_inner_abs;
     int inner_min, inner_cap, outer_enabled;
     double tron_gtol;                 // absolute: tron_gtol_rel * max(rho_pq, rho_va)
