@@ -289,15 +289,15 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
     const double on = d.ub_on[i], su = d.ub_su[i], sd = d.ub_sd[i];
     const double onp = t == 0 ? u0 : d.ub_on[i - 1];
     in.first = t == 0;
-    in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) / rpq;
-    in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) / rpq;
-    in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / rpq;
-    in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) / ruc;
-    in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) / ruc;
-    in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) / ruc;
-    in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) / ruc;
-    in.brl = -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) / ruc;
-    in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) / ruc;
+    in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) * d.irpq;
+    in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) * d.irpq;
+    in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) * d.irpq;
+    in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) * d.iruc;
+    in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) * d.iruc;
+    in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) * d.iruc;
+    in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) * d.iruc;
+    in.brl = -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) * d.iruc;
+    in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) * d.iruc;
     double po, qo, pho;
     gen_solve(in, po, qo, pho);
     d.p[i] = po;
@@ -392,9 +392,9 @@ static size_t gen_smem(int T, int warps) { return dp_smem_bytes(T) * warps; }
 
 void launch_gen(const Dev &d, cudaStream_t s) {
     const int warps = 4;
-    k_gen<<<(d.G + warps - 1) / warps, warps * 32, gen_smem(d.T, warps), s>>>(d);
+    launch_hi_prio(k_gen, dim3((d.G + warps - 1) / warps), dim3(warps * 32), gen_smem(d.T, warps), s, d);
 }
-void launch_genx(const Dev &d, cudaStream_t s) { k_genx<<<(d.G * d.T + 127) / 128, 128, 0, s>>>(d); }
+void launch_genx(const Dev &d, cudaStream_t s) { launch_hi_prio(k_genx, dim3((d.G * d.T + 127) / 128), dim3(128), 0, s, d); }
 
 cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                             const int *hold, int8_t *sched, double *cost, cudaStream_t s) {

@@ -28,8 +28,10 @@ struct Acc {
     }
 };
 
-// (7e) z = -(lambda + y + rho r)/(beta + rho), (7f) y += rho (r + z); S8 terms
-__device__ __forceinline__ void zy_row(double r, double rho, double beta, double *zp, double *yp, double *lp,
+// (7e) z = -(lambda + y + rho r)/(beta + rho), (7f) y += rho (r + z); S8 terms.
+// ib = 1/(beta + rho), formed once per thread: the quotient becomes a product (within one ulp of
+// the oracle's), with no division slow path to spill around.
+__device__ __forceinline__ void zy_row(double r, double rho, double ib, double *zp, double *yp, double *lp,
                                        int pending, double beta_lam, double lmax, double dxb, Acc &a) {
     double lam = *lp;
     double zo = *zp;
@@ -39,7 +41,7 @@ __device__ __forceinline__ void zy_row(double r, double rho, double beta, double
         *lp = lam;
     }
     double y = *yp;
-    double zz = -((lam + y) + rho * r) / (beta + rho);
+    double zz = -((lam + y) + rho * r) * ib;
     *zp = zz;
     *yp = y + rho * (r + zz);
     double rz = r + zz;
@@ -53,13 +55,13 @@ __device__ __forceinline__ void zy_row(double r, double rho, double beta, double
 }
 
 // the same update on values (loads hoisted by the caller): returns z, y and lambda in place
-__device__ __forceinline__ void zy_vals(double r, double rho, double beta, double &z, double &y, double &lam,
+__device__ __forceinline__ void zy_vals(double r, double rho, double ib, double &z, double &y, double &lam,
                                         int pending, double beta_lam, double lmax, double dxb, Acc &a) {
     if (pending) {
         const double v = lam + beta_lam * z;
         lam = v < -lmax ? -lmax : (v > lmax ? lmax : v);
     }
-    const double zz = -((lam + y) + rho * r) / (beta + rho);
+    const double zz = -((lam + y) + rho * r) * ib;
     y = y + rho * (r + zz);
     z = zz;
     const double rz = r + zz;
@@ -111,10 +113,16 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 constexpr int BUS_THREADS = 128;
 constexpr int UBAR_THREADS = 64;
 constexpr int ROWS_THREADS = 128;
-#ifndef UCAC_LATE_THREADS
-#define UCAC_LATE_THREADS 1024
+// late kernels: most threads skip (unmarked rows), so the block waits on its slowest chain.
+// The bus kernel keeps 1024-thread blocks; the rows kernel, whose row updates need more than the
+// 64 registers of a 1024-thread block, runs 256-thread blocks (measured)
+#ifndef UCAC_LBUS_THREADS
+#define UCAC_LBUS_THREADS 1024
 #endif
-constexpr int LATE_THREADS = UCAC_LATE_THREADS;
+#ifndef UCAC_LROWS_THREADS
+#define UCAC_LROWS_THREADS 256
+#endif
+constexpr int LBUS_THREADS = UCAC_LBUS_THREADS, LROWS_THREADS = UCAC_LROWS_THREADS;
 
 // ------------------------------------------------------------------------- S8 partials
 // Every kernel that updates rows leaves one partial per block.  The early ones (k_bus, k_ubar,
@@ -224,12 +232,12 @@ __device__ __forceinline__ void kernel_tail(const Dev &d, Acc &acc, double *part
 // incident branch end -- their inputs are final after the fast path, so in the single-GPU graph
 // it runs in the shadow of k_branch_al -- and k_late the marked ones after the AL tail.
 struct Ctl {
-    double rpq, rva, beta, beta_lam, lmax;
+    double rpq, rva, irpq, beta, beta_lam, lmax, ibpq, ibva;
     int pending;
     unsigned stamp;
     __device__ explicit Ctl(const Dev &d)
-        : rpq(d.rpq), rva(d.rva), beta(d.st->beta), beta_lam(d.st->beta_lam), lmax(d.lambda_max),
-          pending(d.st->pending_outer), stamp(mark_stamp(d)) {}
+        : rpq(d.rpq), rva(d.rva), irpq(d.irpq), beta(d.st->beta), beta_lam(d.st->beta_lam), lmax(d.lambda_max),
+          ibpq(1.0 / (beta + d.rpq)), ibva(1.0 / (beta + d.rva)), pending(d.st->pending_outer), stamp(mark_stamp(d)) {}
 };
 
 // bus-period k = i*T + t of an owned bus (ghost buses are solved by their owner)
@@ -238,7 +246,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
     const size_t GT = (size_t)d.G * T, BT = (size_t)d.B * T;
     const size_t LTH = (size_t)(d.L + d.Lph) * T;
     const double rpq = c.rpq, rva = c.rva;
-    const double beta = c.beta, beta_lam = c.beta_lam, lmax = c.lmax;
+    const double irpq = c.irpq, ibpq = c.ibpq, beta_lam = c.beta_lam, lmax = c.lmax;
     const int pending = c.pending;
     {
         const int i = k / T, t = k - i * T;
@@ -252,10 +260,10 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
 #pragma unroll 2
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
-            const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) / rpq;
+            const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) * irpq;
             double th, aa;
             if (t < T - 1) {
-                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) / rpq;
+                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) * irpq;
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
             } else {
@@ -264,8 +272,8 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
             }
             AP = AP + 1.0 / aa;
             rP = rP - th;
-            const double thq = d.q[gi] + ZG(G_GQ, gi) + YG(G_GQ, gi) / rpq;
-            AQ = AQ + 1.0 / rpq;
+            const double thq = d.q[gi] + ZG(G_GQ, gi) + YG(G_GQ, gi) * irpq;
+            AQ = AQ + irpq;
             rQ = rQ - thq;
         }
         double wsum = 0.0, tsum = 0.0;
@@ -277,9 +285,9 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
             const int kp = side ? B_FPJI : B_FPIJ, kq = side ? B_FQJI : B_FQIJ;
             const int kw = side ? B_WJ : B_WI, ka = side ? B_AJ : B_AI;
             const double thp = TH(kp, li), thq = TH(kq, li), thw = TH(kw, li), tha = TH(ka, li);
-            AP = AP + 1.0 / rpq;
+            AP = AP + irpq;
             rP = rP + thp;
-            AQ = AQ + 1.0 / rpq;
+            AQ = AQ + irpq;
             rQ = rQ + thq;
             wsum = wsum + thw;
             tsum = tsum + tha;
@@ -309,10 +317,10 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
                 yr = YG(G_RC, gi + 1);
                 lr = LG(G_RC, gi + 1);
             }
-            const double tgp = pg + zp + yp / rpq;
+            const double tgp = pg + zp + yp * irpq;
             double th, aa;
             if (rc) {
-                const double trc = phn + zr + yr / rpq;
+                const double trc = phn + zr + yr * irpq;
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
             } else {
@@ -320,11 +328,11 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
                 aa = rpq;
             }
             const double pb = th + muP / aa;
-            const double thq = qg + zq + yq / rpq;
-            const double qb = thq + muQ / rpq;
-            zy_vals(pg - pb, rpq, beta, zp, yp, lp, pending, beta_lam, lmax, pb - pbo, acc);
-            zy_vals(qg - qb, rpq, beta, zq, yq, lq, pending, beta_lam, lmax, qb - qbo, acc);
-            if (rc) zy_vals(phn - pb, rpq, beta, zr, yr, lr, pending, beta_lam, lmax, pb - pbo, acc);
+            const double thq = qg + zq + yq * irpq;
+            const double qb = thq + muQ * irpq;
+            zy_vals(pg - pb, rpq, ibpq, zp, yp, lp, pending, beta_lam, lmax, pb - pbo, acc);
+            zy_vals(qg - qb, rpq, ibpq, zq, yq, lq, pending, beta_lam, lmax, qb - qbo, acc);
+            if (rc) zy_vals(phn - pb, rpq, ibpq, zr, yr, lr, pending, beta_lam, lmax, pb - pbo, acc);
             d.pbar[gi] = pb;
             d.qbar[gi] = qb;
             ZG(G_GP, gi) = zp;
@@ -391,12 +399,12 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
         y[r] = YB(rows[r], k);
         lam[r] = LB(rows[r], k);
     }
-    const double pb = thp + (-muP) / c.rpq;
-    const double qb = thq + (-muQ) / c.rpq;
-    zy_vals(fp - pb, c.rpq, c.beta, z[0], y[0], lam[0], c.pending, c.beta_lam, c.lmax, pb - pbo, acc);
-    zy_vals(fq - qb, c.rpq, c.beta, z[1], y[1], lam[1], c.pending, c.beta_lam, c.lmax, qb - qbo, acc);
-    zy_vals(xw - wb, c.rva, c.beta, z[2], y[2], lam[2], c.pending, c.beta_lam, c.lmax, dwb, acc);
-    zy_vals(xa - tb, c.rva, c.beta, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
+    const double pb = thp + (-muP) * c.irpq;
+    const double qb = thq + (-muQ) * c.irpq;
+    zy_vals(fp - pb, c.rpq, c.ibpq, z[0], y[0], lam[0], c.pending, c.beta_lam, c.lmax, pb - pbo, acc);
+    zy_vals(fq - qb, c.rpq, c.ibpq, z[1], y[1], lam[1], c.pending, c.beta_lam, c.lmax, qb - qbo, acc);
+    zy_vals(xw - wb, c.rva, c.ibva, z[2], y[2], lam[2], c.pending, c.beta_lam, c.lmax, dwb, acc);
+    zy_vals(xa - tb, c.rva, c.ibva, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
     FB(kp, k) = pb;
     FB(kq, k) = qb;
 #pragma unroll
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
 // Late phase (after the AL tail): k_bus_late solves the marked bus-periods, k_rows_late updates
 // the marked ends (1024-thread blocks: few partial slots, so the final fold is short).
 // Single GPU: k_rows_late is the last kernel of the iteration (final = 1).
-__global__ void __launch_bounds__(LATE_THREADS) k_bus_late(Dev d) {
+__global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
     TL_KERNEL(K_BUS_LATE);
     if (d.st->done) return;
     const Ctl c(d);
@@ -472,7 +480,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
     fold_slots(d.part_efold, gridDim.x, d.rec_part + RK_EARLY * NPART);
 }
 
-__global__ void __launch_bounds__(LATE_THREADS) k_rows_late(Dev d, int final) {
+__global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
     TL_KERNEL(K_ROWS_LATE);
     if (d.st->done) return;
     const Ctl c(d);
@@ -572,8 +580,8 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const double ruc = d.ruc;
-    const double beta = d.st->beta, beta_lam = d.st->beta_lam, lmax = d.lambda_max;
+    const double ruc = d.ruc, iruc = d.iruc;
+    const double beta_lam = d.st->beta_lam, lmax = d.lambda_max, ibuc = 1.0 / (d.st->beta + ruc);
     const int pending = d.st->pending_outer;
     Acc acc;
     if (k < d.G * T) {
@@ -589,11 +597,11 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         const int sdt = up > ut, sut = ut > up;
         const double p = d.p[i], q = d.q[i], ph = d.ph[i];
         // slacks (x-variables of 7b) recomputed exactly as the x-step defines them
-        const double bpl = Pm * on_o - ZG(G_PL, i) - YG(G_PL, i) / ruc;
-        const double bpu = PM * on_o - ZG(G_PU, i) - YG(G_PU, i) / ruc;
-        const double bql = Qm * on_o - ZG(G_QL, i) - YG(G_QL, i) / ruc;
-        const double bqu = QM * on_o - ZG(G_QU, i) - YG(G_QU, i) / ruc;
-        const double brl = -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) / ruc;
+        const double bpl = Pm * on_o - ZG(G_PL, i) - YG(G_PL, i) * iruc;
+        const double bpu = PM * on_o - ZG(G_PU, i) - YG(G_PU, i) * iruc;
+        const double bql = Qm * on_o - ZG(G_QL, i) - YG(G_QL, i) * iruc;
+        const double bqu = QM * on_o - ZG(G_QU, i) - YG(G_QU, i) * iruc;
+        const double brl = -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) * iruc;
         const double dd = p - ph;
         const double spl = fmax(0.0, p - bpl), spu = fmax(0.0, bpu - p);
         const double sql = fmax(0.0, q - bql), squ = fmax(0.0, bqu - q);
@@ -607,13 +615,13 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         cm[m][2] = (a2);      \
         e[m++] = (ev);        \
     } while (0)
-        ROW(1.0, 0.0, 0.0, (double)ut + ZG(G_DON, i) + YG(G_DON, i) / ruc);
-        ROW(0.0, 1.0, 0.0, (double)sdt + ZG(G_DSD, i) + YG(G_DSD, i) / ruc);
-        ROW(Pm, 0.0, 0.0, (p - spl) + ZG(G_PL, i) + YG(G_PL, i) / ruc);
-        ROW(PM, 0.0, 0.0, (p + spu) + ZG(G_PU, i) + YG(G_PU, i) / ruc);
-        ROW(Qm, 0.0, 0.0, (q - sql) + ZG(G_QL, i) + YG(G_QL, i) / ruc);
-        ROW(QM, 0.0, 0.0, (q + squ) + ZG(G_QU, i) + YG(G_QU, i) / ruc);
-        ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) / ruc);
+        ROW(1.0, 0.0, 0.0, (double)ut + ZG(G_DON, i) + YG(G_DON, i) * iruc);
+        ROW(0.0, 1.0, 0.0, (double)sdt + ZG(G_DSD, i) + YG(G_DSD, i) * iruc);
+        ROW(Pm, 0.0, 0.0, (p - spl) + ZG(G_PL, i) + YG(G_PL, i) * iruc);
+        ROW(PM, 0.0, 0.0, (p + spu) + ZG(G_PU, i) + YG(G_PU, i) * iruc);
+        ROW(Qm, 0.0, 0.0, (q - sql) + ZG(G_QL, i) + YG(G_QL, i) * iruc);
+        ROW(QM, 0.0, 0.0, (q + squ) + ZG(G_QU, i) + YG(G_QU, i) * iruc);
+        ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) * iruc);
         int n = 2;
         int sun = 0;
         double pn = 0.0, phn = 0.0, sru_n = 0.0, su_on = 0.0;
@@ -624,10 +632,10 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
             pn = d.p[j];
             phn = d.ph[j];
             su_on = d.ub_su[j];
-            const double bru_n = RUp * on_o + SUp * su_on - ZG(G_RU, j) - YG(G_RU, j) / ruc;
+            const double bru_n = RUp * on_o + SUp * su_on - ZG(G_RU, j) - YG(G_RU, j) * iruc;
             sru_n = fmax(0.0, bru_n - (pn - phn));
-            ROW(0.0, 0.0, 1.0, (double)sun + ZG(G_DSU, j) + YG(G_DSU, j) / ruc);
-            ROW(RUp, 0.0, SUp, ((pn - phn) + sru_n) + ZG(G_RU, j) + YG(G_RU, j) / ruc);
+            ROW(0.0, 0.0, 1.0, (double)sun + ZG(G_DSU, j) + YG(G_DSU, j) * iruc);
+            ROW(RUp, 0.0, SUp, ((pn - phn) + sru_n) + ZG(G_RU, j) + YG(G_RU, j) * iruc);
             n = 3;
         }
 #undef ROW
@@ -651,20 +659,20 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         const double on_n = v[0], sd_n = v[1];
         // rows of the group with the new ubar (r = x-part - c'ubar)
         const double don = on_n - on_o, dsd = sd_n - sd_o;
-        zy_vals((double)ut - on_n, ruc, beta, zr[0], yr[0], lr[0], pending, beta_lam, lmax, don, acc);
-        zy_vals((double)sdt - sd_n, ruc, beta, zr[1], yr[1], lr[1], pending, beta_lam, lmax, dsd, acc);
-        zy_vals((p - spl) - Pm * on_n, ruc, beta, zr[2], yr[2], lr[2], pending, beta_lam, lmax, Pm * don, acc);
-        zy_vals((p + spu) - PM * on_n, ruc, beta, zr[3], yr[3], lr[3], pending, beta_lam, lmax, PM * don, acc);
-        zy_vals((q - sql) - Qm * on_n, ruc, beta, zr[4], yr[4], lr[4], pending, beta_lam, lmax, Qm * don, acc);
-        zy_vals((q + squ) - QM * on_n, ruc, beta, zr[5], yr[5], lr[5], pending, beta_lam, lmax, QM * don, acc);
-        zy_vals((dd - srd) + RDn * on_n + SDn * sd_n, ruc, beta, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
+        zy_vals((double)ut - on_n, ruc, ibuc, zr[0], yr[0], lr[0], pending, beta_lam, lmax, don, acc);
+        zy_vals((double)sdt - sd_n, ruc, ibuc, zr[1], yr[1], lr[1], pending, beta_lam, lmax, dsd, acc);
+        zy_vals((p - spl) - Pm * on_n, ruc, ibuc, zr[2], yr[2], lr[2], pending, beta_lam, lmax, Pm * don, acc);
+        zy_vals((p + spu) - PM * on_n, ruc, ibuc, zr[3], yr[3], lr[3], pending, beta_lam, lmax, PM * don, acc);
+        zy_vals((q - sql) - Qm * on_n, ruc, ibuc, zr[4], yr[4], lr[4], pending, beta_lam, lmax, Qm * don, acc);
+        zy_vals((q + squ) - QM * on_n, ruc, ibuc, zr[5], yr[5], lr[5], pending, beta_lam, lmax, QM * don, acc);
+        zy_vals((dd - srd) + RDn * on_n + SDn * sd_n, ruc, ibuc, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
                 RDn * don + SDn * dsd, acc);
         double su_n = 0.0;
         if (nxt) {
             su_n = v[2];
             const double dsu = su_n - su_on;
-            zy_vals((double)sun - su_n, ruc, beta, zr[7], yr[7], lr[7], pending, beta_lam, lmax, dsu, acc);
-            zy_vals(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, beta, zr[8], yr[8], lr[8], pending, beta_lam,
+            zy_vals((double)sun - su_n, ruc, ibuc, zr[7], yr[7], lr[7], pending, beta_lam, lmax, dsu, acc);
+            zy_vals(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, ibuc, zr[8], yr[8], lr[8], pending, beta_lam,
                     lmax, RUp * don + SUp * dsu, acc);
         }
         d.ub_on[i] = on_n;
@@ -686,19 +694,19 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         }
         if (t == 0) {
             // group 0 = (ubar^su_1): rows D_SU_1, RU_1 (ubar^on_0 := u0, R4)
-            const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) / ruc;
+            const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) * iruc;
             const double sru = fmax(0.0, bru - dd);
             double c1[2][3] = {{1.0, 0.0, 0.0}, {SUp, 0.0, 0.0}};
             double e1[2];
-            e1[0] = (double)sut + ZG(G_DSU, i) + YG(G_DSU, i) / ruc;
-            e1[1] = (dd + sru) - RUp * (double)u0 + ZG(G_RU, i) + YG(G_RU, i) / ruc;
+            e1[0] = (double)sut + ZG(G_DSU, i) + YG(G_DSU, i) * iruc;
+            e1[1] = (dd + sru) - RUp * (double)u0 + ZG(G_RU, i) + YG(G_RU, i) * iruc;
             double v1[3];
             boxqp3(1, 2, c1, e1, v1);
             d.ub_su[i] = v1[0];
             const double dsu = v1[0] - su_o;
-            zy_row((double)sut - v1[0], ruc, beta, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
+            zy_row((double)sut - v1[0], ruc, ibuc, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
                    acc);
-            zy_row((dd + sru) - RUp * (double)u0 - SUp * v1[0], ruc, beta, &ZG(G_RU, i), &YG(G_RU, i), &LG(G_RU, i),
+            zy_row((dd + sru) - RUp * (double)u0 - SUp * v1[0], ruc, ibuc, &ZG(G_RU, i), &YG(G_RU, i), &LG(G_RU, i),
                    pending, beta_lam, lmax, SUp * dsu, acc);
         }
         // objective, Eq. 1a with f^OPF = c2 (S p)^2 + c1 S p and f^UC (R13)
@@ -827,14 +835,15 @@ int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; 
 
 void launch_bus(const Dev &d, cudaStream_t s) { k_bus<<<d.nblk_bus, BUS_THREADS, 0, s>>>(d); }
 void launch_rows(const Dev &d, cudaStream_t s) { k_rows<<<d.nblk_rows, ROWS_THREADS, 0, s>>>(d); }
-void launch_bus_late(const Dev &d, cudaStream_t s) { k_bus_late<<<d.nblk_lbus, LATE_THREADS, 0, s>>>(d); }
+void launch_bus_late(const Dev &d, cudaStream_t s) { k_bus_late<<<d.nblk_lbus, LBUS_THREADS, 0, s>>>(d); }
 void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
-    k_rows_late<<<d.nblk_lrows, LATE_THREADS, 0, s>>>(d, final);
+    k_rows_late<<<d.nblk_lrows, LROWS_THREADS, 0, s>>>(d, final);
 }
-int nblk_late(int n) { return (n + LATE_THREADS - 1) / LATE_THREADS; }
+int nblk_lbus(int n) { return (n + LBUS_THREADS - 1) / LBUS_THREADS; }
+int nblk_lrows(int n) { return (n + LROWS_THREADS - 1) / LROWS_THREADS; }
 int fold_blocks() { return FOLD_BLOCKS; }
 void launch_fold_early(const Dev &d, cudaStream_t s) { k_fold_early<<<FOLD_BLOCKS, FOLD_THREADS, 0, s>>>(d); }
-void launch_ubar(const Dev &d, cudaStream_t s) { k_ubar<<<d.nblk_ubar, UBAR_THREADS, 0, s>>>(d); }
+void launch_ubar(const Dev &d, cudaStream_t s) { launch_hi_prio(k_ubar, dim3(d.nblk_ubar), dim3(UBAR_THREADS), 0, s, d); }
 void launch_finalize(const Dev &d, cudaStream_t s) { k_finalize<<<1, 32, 0, s>>>(d); }
 static int xgrid(int n) { return std::max(1, std::min(296, (n + 255) / 256)); }
 void launch_pack_tau(const Dev &d, cudaStream_t s) { k_pack_tau<<<xgrid(d.ncut * 4 * d.T), 256, 0, s>>>(d); }

@@ -20,6 +20,15 @@
 #include <vector>
 
 #include "ucac.h"
+
+// graph shape: the generator chain forks at the start of the iteration, on a
+// higher-priority stream
+#ifndef UCAC_EARLY_FORK
+#define UCAC_EARLY_FORK 1
+#endif
+#ifndef UCAC_S2_PRIO
+#define UCAC_S2_PRIO 1
+#endif
 #include "ucac_dev.cuh"
 #include "ucac_part.h"
 
@@ -172,7 +181,7 @@ struct ucac_ctx {
     ncclComm_t comm = nullptr;
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     bool own_stream = false;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr, ev_branch = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int gunroll[2] = {1, 16};
     std::vector<void *> dalloc;
@@ -403,12 +412,15 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         if (cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "stream"));
         ctx->own_stream = true;
     }
-    if (cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking) != cudaSuccess ||
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&ctx->s2, cudaStreamNonBlocking, UCAC_S2_PRIO ? prio_hi : prio_lo) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->s3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_genx, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_early, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ctx->ev_early, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_branch, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
     mark("streams");
     if ((ctx->st_host = pinned_status_get()) == nullptr) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
@@ -435,7 +447,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.ref_bus = P.ref;
     d.S = P.S;
     d.rpq = prm->rho_pq; d.rva = prm->rho_va; d.ruc = prm->rho_uc;
-    d.irpq = 1.0 / prm->rho_pq; d.irva = 1.0 / prm->rho_va;
+    d.irpq = 1.0 / prm->rho_pq; d.irva = 1.0 / prm->rho_va; d.iruc = 1.0 / prm->rho_uc;
     d.tau = prm->tau; d.theta = prm->theta; d.lambda_max = prm->lambda_max; d.beta_max = prm->beta_max;
     d.eps_inner_abs = prm->eps_inner_abs;
     d.inner_min = prm->inner_min; d.inner_cap = prm->inner_cap; d.outer_enabled = prm->outer_enabled;
@@ -519,8 +531,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.part_bus = A.take<double>((size_t)d.nblk_bus * NPART);
         d.part_ubar = A.take<double>((size_t)d.nblk_ubar * NPART);
         d.part_rows = A.take<double>((size_t)d.nblk_rows * NPART);
-        d.nblk_lbus = nblk_late(P.Bo * T);
-        d.nblk_lrows = nblk_late(L * T);
+        d.nblk_lbus = nblk_lbus(P.Bo * T);
+        d.nblk_lrows = nblk_lrows(L * T);
         d.part_lbus = A.take<double>((size_t)d.nblk_lbus * NPART);
         d.part_lrows = A.take<double>((size_t)d.nblk_lrows * NPART);
         d.part_efold = A.take<double>((size_t)fold_blocks() * NPART);
@@ -628,14 +640,25 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
 static void enqueue_iteration(ucac_ctx *ctx) {
     const Dev &d = ctx->d;
     const bool multi = ctx->nranks > 1;
-    launch_kernel(ctx, K_BRANCH, ctx->s);
-    cudaEventRecord(ctx->ev_fork, ctx->s);
-    cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
+    const bool early_fork = !multi && UCAC_EARLY_FORK;
+    if (early_fork) {
+        // the generator chain (7a, 7b gens, 7c) reads only the previous iterate: it runs beside the
+        // branch fast path, on a higher-priority stream
+        cudaEventRecord(ctx->ev_fork, ctx->s);
+        cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
+        launch_kernel(ctx, K_BRANCH, ctx->s);
+        cudaEventRecord(ctx->ev_branch, ctx->s);
+    } else {
+        launch_kernel(ctx, K_BRANCH, ctx->s);
+        cudaEventRecord(ctx->ev_fork, ctx->s);
+        cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
+    }
     launch_kernel(ctx, K_GEN, ctx->s2);
     launch_kernel(ctx, K_GENX, ctx->s2);
     if (!multi) {
         cudaEventRecord(ctx->ev_genx, ctx->s2);
         cudaStreamWaitEvent(ctx->s3, ctx->ev_genx, 0);
+        if (early_fork) cudaStreamWaitEvent(ctx->s3, ctx->ev_branch, 0);
         launch_kernel(ctx, K_BUS, ctx->s3);
         launch_kernel(ctx, K_ROWS, ctx->s3);
     }
@@ -1196,6 +1219,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->ev_genx) cudaEventDestroy(ctx->ev_genx);
     if (ctx->ev_early) cudaEventDestroy(ctx->ev_early);
+    if (ctx->ev_branch) cudaEventDestroy(ctx->ev_branch);
     if (ctx->s2) cudaStreamDestroy(ctx->s2);
     if (ctx->s3) cudaStreamDestroy(ctx->s3);
     if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);

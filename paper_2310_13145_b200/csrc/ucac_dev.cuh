@@ -50,7 +50,7 @@ struct Dev {
     int nblk_bus, nblk_ubar, nblk_rows;
     double S;                         // base MVA
     double rpq, rva, ruc;             // rho classes
-    double irpq, irva;                // 1/rho_pq, 1/rho_va: the branch kernels form y/rho as y * (1/rho)
+    double irpq, irva, iruc;          // 1/rho: every kernel forms y/rho as y * (1/rho)
     double tau, theta, lambda_max, beta_max, eps_inner_abs;
     int inner_min, inner_cap, outer_enabled;
     double tron_gtol;                 // absolute: tron_gtol_rel * max(rho_pq, rho_va)
@@ -152,13 +152,32 @@ __device__ __forceinline__ unsigned mark_stamp(const Dev &d) { return (unsigned)
 namespace ucac {
 void launch_branch(const Dev &d, cudaStream_t s);
 void launch_branch_al(const Dev &d, cudaStream_t s);
+// Launch with the device's highest execution priority (a launch attribute, kept by graph capture):
+// the generator chain (k_gen, k_genx, k_ubar) forks at the start of the iteration and should take
+// SM slots as k_branch blocks retire rather than queue behind them.
+template <typename... KArgs>
+inline cudaError_t launch_hi_prio(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, KArgs... args) {
+    static int prio = [] { int lo = 0, hi = 0; cudaDeviceGetStreamPriorityRange(&lo, &hi); return hi; }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = prio;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
 void launch_gen(const Dev &d, cudaStream_t s);
 void launch_genx(const Dev &d, cudaStream_t s);
 void launch_bus(const Dev &d, cudaStream_t s);
 void launch_rows(const Dev &d, cudaStream_t s);
 void launch_bus_late(const Dev &d, cudaStream_t s);
 void launch_rows_late(const Dev &d, cudaStream_t s, int final);
-int nblk_late(int n);
+int nblk_lbus(int n);
+int nblk_lrows(int n);
 int fold_blocks();
 void launch_fold_early(const Dev &d, cudaStream_t s);
 int nblk_rows(int L, int T);
