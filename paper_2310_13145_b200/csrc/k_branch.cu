@@ -37,6 +37,19 @@ constexpr double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-1
 constexpr double TR_EPSF = 1e-10, TR_STALL = 1e-13;   // R48
 constexpr double TWO_PI = 6.283185307179586;
 
+// 1/x for normal x: the MUFU reciprocal approximation refined by two Newton steps (relative error
+// 2^-22 -> 2^-44 -> rounding), i.e. within an ulp of the IEEE quotient the oracle forms, without
+// the division's slow-path call (and the register spills around it).  Callers guarantee a normal
+// x; a subnormal x flushes to zero (result inf), where the quotient would be large but finite.
+__device__ __forceinline__ double rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 template <bool AL>
 struct BrFun {
     double Gii, Gij, Gji, Gjj, Bii, Bij, Bji, Bjj;
@@ -145,7 +158,7 @@ struct BrFun {
                 k01 += sig * (dh0[0] * dh0[1] + dh1[0] * dh1[1]);
             }
         }
-        const double ixx = 0.5 / (x[0] * x[1]);   // one division for both 1/(2 w)
+        const double ixx = 0.5 * rcp(x[0] * x[1]);   // one reciprocal for both 1/(2 w)
         double i2wi = x[1] * ixx, i2wj = x[0] * ixx;
         double dC[4] = {C * i2wi, C * i2wj, -S, S};
         double dS[4] = {S * i2wi, S * i2wj, C, -C};
@@ -240,6 +253,7 @@ __device__ __forceinline__ double qmodel(const double *g, const double (*H)[N], 
 // compare/select clamp (the oracle's form; cheaper than fmin/fmax with their NaN handling)
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+
 template <int N>
 __device__ __forceinline__ void pstep(const double *x, const double *lo, const double *hi,
                                       const double *g, double a, double *s) {
@@ -256,7 +270,7 @@ __device__ __forceinline__ double bnd_tau(const double *a, const double *p, doub
     if (pp <= 0.0) return 0.0;
     double gap = fmax(delta * delta - aa, 0.0);
     double rad = sqrt(ap * ap + pp * gap);
-    return ap > 0.0 ? gap / (ap + rad) : (rad - ap) / pp;
+    return ap > 0.0 ? gap * rcp(ap + rad) : (rad - ap) * rcp(pp);
 }
 
 template <int N>
@@ -283,7 +297,7 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
 #pragma unroll
     for (int i = 0; i < 6; i++) fr[i] = x[i] > lo[i] && x[i] < hi[i];
     double J[2][6];
-    const double isig = 1.0 / sig;
+    const double isig = rcp(sig);
 #pragma unroll
     for (int m = 0; m < 2; m++) {
 #pragma unroll
@@ -298,9 +312,9 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
         double dj = fr[j] ? H[j][j] : 1.0;
 #pragma unroll
         for (int k = 0; k < j; k++) dj -= Lm[j][k] * Lm[j][k] * D[k];
-        pd = pd && dj > 0.0;
+        pd = pd && dj > 1e-300;
         D[j] = dj;
-        const double inv = 1.0 / dj;
+        const double inv = rcp(dj);
 #pragma unroll
         for (int i = j + 1; i < 6; i++) {
             double v = (fr[i] && fr[j]) ? H[i][j] : 0.0;
@@ -324,7 +338,7 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
         }
 #pragma unroll
         for (int i = 5; i >= 0; i--) {
-            double v = z[i] / D[i];
+            double v = z[i] * rcp(D[i]);
 #pragma unroll
             for (int k = i + 1; k < 6; k++) v -= Lm[k][i] * V[n][k];
             V[n][i] = v;
@@ -340,16 +354,16 @@ __device__ __forceinline__ bool al_newton_dmu(const double (*H)[6], const double
         v0 = 1.0;
         v1 = 0.0;
     } else if (a >= d) {
-        const double n = sqrt((lam0 - d) * (lam0 - d) + b * b);
-        v0 = (lam0 - d) / n;
-        v1 = b / n;
+        const double in = rcp(sqrt((lam0 - d) * (lam0 - d) + b * b));
+        v0 = (lam0 - d) * in;
+        v1 = b * in;
     } else {
-        const double n = sqrt(b * b + (lam0 - a) * (lam0 - a));
-        v0 = b / n;
-        v1 = (lam0 - a) / n;
+        const double in = rcp(sqrt(b * b + (lam0 - a) * (lam0 - a)));
+        v0 = b * in;
+        v1 = (lam0 - a) * in;
     }
-    const double thr = 1.0 / (AL_NEWTON_C * sig);
-    const double f0 = lam0 >= thr ? 1.0 / lam0 : sig, f1 = lam1 >= thr ? 1.0 / lam1 : sig;
+    const double thr = rcp(AL_NEWTON_C * sig);
+    const double f0 = lam0 >= thr ? rcp(lam0) : sig, f1 = lam1 >= thr ? rcp(lam1) : sig;
     const double p0 = v0 * h[0] + v1 * h[1], p1 = -v1 * h[0] + v0 * h[1];
     dmu[0] = f0 * p0 * v0 - f1 * p1 * v1;
     dmu[1] = f0 * p0 * v1 + f1 * p1 * v0;
@@ -371,8 +385,8 @@ __device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr
         double dj = fr[j] ? H[j][j] : 1.0;
 #pragma unroll
         for (int k = 0; k < j; k++) dj -= Lm[j][k] * LD[j][k];
-        pd = pd && dj > 0.0;
-        const double inv = 1.0 / dj;
+        pd = pd && dj > 1e-300;
+        const double inv = rcp(dj);
         iD[j] = inv;
 #pragma unroll
         for (int i = j + 1; i < N; i++) {
@@ -416,7 +430,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
         double Hg[N];
         matvec<N>(H, g, Hg);
         const double gHg = dotn<N>(g, Hg), gg = dotn<N>(g, g);
-        if (gHg > 0.0 && gg > 0.0) alpha = gg / gHg;
+        if (gHg > 0.0 && gg > 0.0) alpha = gg * rcp(gHg);
     }
     int it = 0;
     for (; it < maxit; it++) {
@@ -510,7 +524,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                         for (int i = 0; i < N; i++) w[i] += tau * p[i];
                         break;
                     }
-                    double a = rr / kap;
+                    double a = rr * rcp(kap);
                     double tt[N];
 #pragma unroll
                     for (int i = 0; i < N; i++) tt[i] = t[i] + a * p[i];
@@ -527,7 +541,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
                     }
                     double rn = dotn<N>(r, r);
                     if (rn <= tol2) break;
-                    double b = rn / rr;
+                    double b = rn * rcp(rr);
 #pragma unroll
                     for (int i = 0; i < N; i++) p[i] = r[i] + b * p[i];
                     rr = rn;
@@ -584,7 +598,7 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
         fn.template eval<N, true>(xn, fnew, gn, Hn);
         double ared = f - fnew;
         if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dotn<N>(g, s) + dotn<N>(gn, s));
-        double ratio = pred > 0.0 ? ared / pred : -1.0;
+        double ratio = pred > 0.0 ? ared * rcp(pred) : -1.0;
         double snorm = sqrt(ss);
         if (ratio > TR_ETA0) {
 #pragma unroll
@@ -804,14 +818,14 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
         const double rate = d.rate[k / d.T];
         const double r2 = rate * rate;
         const double sig0 = d.al_sigma0_rel * d.rpq * r2;
-        F6.r2inv = 1.0 / r2;
+        F6.r2inv = rcp(r2);
         double x[6];
 #pragma unroll
         for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
         {
             const double f0 = d.f[0 * LTs + k], f1 = d.f[1 * LTs + k], f2 = d.f[2 * LTs + k], f3 = d.f[3 * LTs + k];
-            x[4] = clampd(1.0 - (f0 * f0 + f1 * f1) / r2, 0.0, 1.0);
-            x[5] = clampd(1.0 - (f2 * f2 + f3 * f3) / r2, 0.0, 1.0);
+            x[4] = clampd(1.0 - (f0 * f0 + f1 * f1) * F6.r2inv, 0.0, 1.0);
+            x[5] = clampd(1.0 - (f2 * f2 + f3 * f3) * F6.r2inv, 0.0, 1.0);
         }
         double mu0 = d.al[0 * LTs + k], mu1 = d.al[1 * LTs + k];
         double sig = fmax(sig0, d.al[2 * LTs + k] * d.al_sigma_decay);
@@ -822,8 +836,8 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
 #pragma unroll
             for (int m = 0; m < 4; m++) xp[m] = clampd(d.alq_x[m * LTs + idx], lo[m], hi[m]);
             F6.flows(xp, C0, S0, p0, p1, p2, p3);
-            xp[4] = clampd(1.0 - (p0 * p0 + p1 * p1) / r2, 0.0, 1.0);
-            xp[5] = clampd(1.0 - (p2 * p2 + p3 * p3) / r2, 0.0, 1.0);
+            xp[4] = clampd(1.0 - (p0 * p0 + p1 * p1) * F6.r2inv, 0.0, 1.0);
+            xp[5] = clampd(1.0 - (p2 * p2 + p3 * p3) * F6.r2inv, 0.0, 1.0);
             F6.mu0 = mu0; F6.mu1 = mu1; F6.sig = sig;
             if (F6.value(xp) < F6.value(x)) {
 #pragma unroll
@@ -845,8 +859,8 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
             c_alit += it;
             c_cap += !ok;
             F6.flows(x, C, S, f0, f1, f2, f3);
-            double h1 = (f0 * f0 + f1 * f1) / r2 - 1.0 + x[4];
-            double h2 = (f2 * f2 + f3 * f3) / r2 - 1.0 + x[5];
+            double h1 = (f0 * f0 + f1 * f1) * F6.r2inv - 1.0 + x[4];
+            double h2 = (f2 * f2 + f3 * f3) * F6.r2inv - 1.0 + x[5];
             double hm = fmax(fabs(h1), fabs(h2));
             if (hm <= d.al_eta_star) break;
             const double hv[2] = {h1, h2};
