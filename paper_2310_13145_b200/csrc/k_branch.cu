@@ -703,8 +703,11 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
     TL_KERNEL(K_BRANCH);
     if (d.st->done) return;
     const int LT = d.L * d.T;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long c_it = 0, c_cap = 0;
+    // grid-stride over 128-solve chunks: the grid is sized to leave SM slots free for the
+    // generator chain that runs beside this kernel (launch_branch)
+    for (int base = blockIdx.x * blockDim.x; base < LT; base += gridDim.x * blockDim.x) {
+    const int k = base + threadIdx.x;
     if (k < LT) {
         const size_t LTs = (size_t)LT;
         BrFun<false> F4;
@@ -726,8 +729,8 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         } else {
             int it = 0;
             const bool ok = tron<4>(F4, x, lo, hi, d.tron_gtol, d.tron_maxit, it);
-            c_it = it;
-            c_cap = !ok;
+            c_it += it;
+            c_cap += !ok;
         }
         double C, S, f0, f1, f2, f3;
         F4.flows(x, C, S, f0, f1, f2, f3);
@@ -767,6 +770,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
             d.al[2 * LTs + k] = d.al_sigma0_rel * d.rpq * r2;
             emit_tauhat_zy(d, k, x, f0, f1, f2, f3, &s_z[0][threadIdx.x], &s_y[0][threadIdx.x], UCAC_BRANCH_TPB);
         }
+    }
     }
     warp_add_u64(d.cnt + 0, c_it);
     warp_add_u64(d.cnt + 1, c_cap);
@@ -910,9 +914,25 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
 
 }  // namespace
 
+#ifndef UCAC_BRANCH_FREE_SLOTS
+#define UCAC_BRANCH_FREE_SLOTS 24
+#endif
+#ifndef UCAC_BRANCH_CARVEOUT
+#define UCAC_BRANCH_CARVEOUT -1   // driver default; 50 and 100 measured slower
+#endif
 void launch_branch(const Dev &d, cudaStream_t s) {
-    const int n = d.L * d.T;
-    k_branch<<<(n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB, UCAC_BRANCH_TPB, 0, s>>>(d);
+    // shared-memory carveout: 3 k_branch blocks need 52 KB; a larger carveout lets the generator
+    // chain's blocks (k_gen: ~16 KB each) co-reside in the free slots instead of waiting for the
+    // SM to drain
+    static const bool carve = [] {
+        return UCAC_BRANCH_CARVEOUT < 0 ||
+               cudaFuncSetAttribute(k_branch, cudaFuncAttributePreferredSharedMemoryCarveout, UCAC_BRANCH_CARVEOUT) == cudaSuccess;
+    }();
+    (void)carve;
+    const int n = d.L * d.T, chunks = (n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB;
+    // 148 SMs x UCAC_BRANCH_MINB resident blocks, minus the slots left to the generator chain
+    const int grid = std::max(1, std::min(chunks, 148 * UCAC_BRANCH_MINB - UCAC_BRANCH_FREE_SLOTS));
+    k_branch<<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
 }
 #ifndef UCAC_AL_SMEM
 #define UCAC_AL_SMEM 0   // dynamic shared memory per AL block (bytes): > 0 reserves SMs for the AL work

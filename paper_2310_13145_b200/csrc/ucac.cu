@@ -643,18 +643,23 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     const bool early_fork = !multi && UCAC_EARLY_FORK;
     if (early_fork) {
         // the generator chain (7a, 7b gens, 7c) reads only the previous iterate: it runs beside the
-        // branch fast path, on a higher-priority stream
+        // branch fast path at high launch priority, in the SM slots k_branch's grid leaves free
+        //
+        // (enqueuing the chain before k_branch, or a larger shared-memory carveout for k_branch
+        // so k_gen co-resides from the start, measured slower: k_branch is throughput-bound)
         cudaEventRecord(ctx->ev_fork, ctx->s);
         cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
         launch_kernel(ctx, K_BRANCH, ctx->s);
         cudaEventRecord(ctx->ev_branch, ctx->s);
+        launch_kernel(ctx, K_GEN, ctx->s2);
+        launch_kernel(ctx, K_GENX, ctx->s2);
     } else {
         launch_kernel(ctx, K_BRANCH, ctx->s);
         cudaEventRecord(ctx->ev_fork, ctx->s);
         cudaStreamWaitEvent(ctx->s2, ctx->ev_fork, 0);
+        launch_kernel(ctx, K_GEN, ctx->s2);
+        launch_kernel(ctx, K_GENX, ctx->s2);
     }
-    launch_kernel(ctx, K_GEN, ctx->s2);
-    launch_kernel(ctx, K_GENX, ctx->s2);
     if (!multi) {
         cudaEventRecord(ctx->ev_genx, ctx->s2);
         cudaStreamWaitEvent(ctx->s3, ctx->ev_genx, 0);
