@@ -101,7 +101,9 @@ typedef struct {
     int32_t uc_fixed;   /* 1: step (7a) keeps the schedule (NEXT-2 warm start, ucac_uc_warm_start) */
     int32_t variant;    /* NEXT-3 formulation variants (bitmask, R47): 1 = every rated branch
                            solves the six-variable thermal AL (no 4-variable fast path, as ExaTron),
-                           2 = wbar clipped to [Vmin^2, Vmax^2] after the bus solve (SPEC) */
+                           2 = wbar clipped to [Vmin^2, Vmax^2] after the bus solve (SPEC),
+                           4 = ramp-aware DP (NEXT-4(a), R50): no shutdown at t while the current
+                           dispatch p_{t-1} (p0 at t = 1) exceeds the shutdown ramp S^D */
 } ucac_params;
 
 /* Multi-GPU (bus-graph cut).  NULL = single GPU.

@@ -1101,6 +1101,14 @@ static void one_iteration(orc_ctx *c) {
                     z3[v * T + t] = ZG(D_ON + v, i);
                 }
             orc_stage_costs(T, q->c0[g], q->csu[g], q->csd[g], ruc, ub3, y3, z3, Lt);
+            if (pr->variant & 4) {
+                /* NEXT-4(a), R50: a shutdown at t (u_{t-1} = 1, u_t = 0) needs p_{t-1} <= S^D by
+                 * Eq. 4d; with the current dispatch above S^D that transition is excluded */
+                for (int t = 0; t < T; t++) {
+                    double pprev = t == 0 ? q->p0[g] : c->p[(size_t)g * T + t - 1];
+                    if (pprev > q->sd_ramp[g]) Lt[t * 4 + 1 * 2 + 0] = INFINITY;
+                }
+            }
             orc_dp(T, Lt, q->min_up[g], q->min_dn[g], q->u0[g], q->hold[g], unew + (size_t)g * T);
         }
         free(Lt); free(ub3); free(y3); free(z3);

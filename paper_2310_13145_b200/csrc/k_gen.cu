@@ -255,6 +255,12 @@ __global__ void __launch_bounds__(128) k_gen(Dev d) {
         for (int a = 0; a < 2; a++)
 #pragma unroll
             for (int b = 0; b < 2; b++) s.L[t * 4 + a * 2 + b] = stage_cost(a, b, c0, csu, csd, ruc, ub, yy, zz);
+        // NEXT-4(a) ramp-aware DP (variant bit 4, R50): no shutdown at t while the current dispatch
+        // p_{t-1} exceeds the shutdown ramp S^D (Eq. 4d would be infeasible)
+        if (d.variant & 4) {
+            const double pprev = t == 0 ? d.p0[g] : d.p[i - 1];
+            if (pprev > d.sdn[g]) s.L[t * 4 + 1 * 2 + 0] = INFINITY;
+        }
     }
     __syncwarp();
     dp_warp(s, T, d.tu[g], d.td[g], d.u0[g], d.hold[g]);

@@ -288,18 +288,22 @@ def test_uc_warm_start_next2(name, iters):
     run_pair(dataclasses.replace(pb, u_init=ug), pr, 10)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6])
 def test_formulation_variants_next3(variant):
-    """NEXT-3 (R47): the AL for every rated branch (1), SPEC's w-bar clip (2), both (3) -- each
-    keeps GPU/oracle parity."""
+    """NEXT-3 (R47): the AL for every rated branch (1), SPEC's w-bar clip (2), both (3);
+    NEXT-4(a) (R50): the ramp-aware DP (4), on a case30 variant with S^D = Pmin/2 so the excluded
+    shutdowns occur -- each keeps GPU/oracle parity, schedules bit-exact."""
     import dataclasses
     pb, pr = inputs.build_config("case30")
+    if variant & 4:
+        pb = dataclasses.replace(pb, sd_ramp=pb.pmin * 0.5)
     # variant 1 solves every rated branch by the slack-form AL; for an inactive line its Hessian
     # H_F + sigma J'J is far worse conditioned than the fast path's H_F, so a one-ulp change of
     # the input state moves x by up to ~1e-9 relative in the oracle itself (R47).  Each
     # iteration is checked one step at a time against a tolerance of 10x that measured
     # response; schedules, scalars and counters stay exact over the whole run.
+    iters = 150 if variant & 4 else 20   # the excluded shutdowns start after a few dozen iterations
     if variant & 1:
-        run_pair(pb, dataclasses.replace(pr, variant=variant), 20, free_run=1, sensitivity=True)
+        run_pair(pb, dataclasses.replace(pr, variant=variant), iters, free_run=1, sensitivity=True)
     else:
-        run_pair(pb, dataclasses.replace(pr, variant=variant), 20)
+        run_pair(pb, dataclasses.replace(pr, variant=variant), iters, check_every=1 if iters <= 20 else 3)

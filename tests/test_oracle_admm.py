@@ -276,3 +276,39 @@ def test_variant1_conditioning():
     r1 = _ulp_response(dataclasses.replace(pr, variant=1))
     assert r0 < 1e-13, r0
     assert 1e-13 < r1 < 1e-8, r1
+
+
+def _shutdowns_above_sd(pb, pr, iters):
+    """(violations, shutdowns): shutdowns at t whose previous-iterate dispatch p_{t-1} exceeds S^D."""
+    import dataclasses  # noqa: F401
+    q = pb.normalized()
+    G, T = q.ngen, q.T
+    o = oracle.Oracle(pb, pr)
+    viol = shut = 0
+    for _ in range(iters):
+        p = o.get_state()["p"].reshape(G, T).copy()
+        o.iterate(1)
+        u = o.get_state()["u"].reshape(G, T)
+        for g in range(G):
+            for t in range(T):
+                prev_on = q.u0[g] if t == 0 else u[g, t - 1]
+                if prev_on == 1 and u[g, t] == 0:
+                    shut += 1
+                    pprev = q.p0[g] if t == 0 else p[g, t - 1]
+                    viol += pprev > q.sd_ramp[g]
+    o.close()
+    return viol, shut
+
+
+def test_ramp_aware_dp_next4():
+    """NEXT-4(a), R50 (variant bit 4): no DP schedule shuts a unit down at t while its current
+    dispatch p_{t-1} (or p_0) exceeds the shutdown ramp S^D -- the Eq. 4d-infeasible transition
+    of SURVEY A5.  Scenario: case30 with S^D = Pmin/2, where the default formulation takes such
+    transitions (71 in 300 iterations) and the ramp-aware DP takes none but still shuts units down."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    pb = dataclasses.replace(pb, sd_ramp=pb.pmin * 0.5)
+    v4, s4 = _shutdowns_above_sd(pb, dataclasses.replace(pr, variant=4), 300)
+    v0, s0 = _shutdowns_above_sd(pb, pr, 300)
+    assert v4 == 0 and s4 > 0, (v4, s4)
+    assert v0 > 0, (v0, s0)
