@@ -103,7 +103,9 @@ typedef struct {
                            solves the six-variable thermal AL (no 4-variable fast path, as ExaTron),
                            2 = wbar clipped to [Vmin^2, Vmax^2] after the bus solve (SPEC),
                            4 = ramp-aware DP (NEXT-4(a), R50): no shutdown at t while the current
-                           dispatch p_{t-1} (p0 at t = 1) exceeds the shutdown ramp S^D */
+                           dispatch p_{t-1} (p0 at t = 1) exceeds the shutdown ramp S^D,
+                           8 = no angle consensus rows (SPEC, R51): each line keeps theta_i = 0 and
+                           its own angle difference; thetabar is not updated */
 } ucac_params;
 
 /* Multi-GPU (bus-graph cut).  NULL = single GPU.

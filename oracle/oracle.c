@@ -680,6 +680,7 @@ typedef struct {
     const double *y, *tau;
     double rpq, rva, r2, mu[2], sig;
     int al;
+    int nva;   /* 4 (w and theta rows) or 2 (no angle rows, R51) */
 } bctx;
 static void br_eval(void *vc, const double *X, double *fo, double *g, double *H) {
     bctx *c = (bctx *)vc;
@@ -698,7 +699,7 @@ static void br_eval(void *vc, const double *X, double *fo, double *g, double *H)
                 H[a * n + b] = H[a * n + b] + c->rpq * (J[k * 4 + a] * J[k * 4 + b] + e * Hf[k * 16 + a * 4 + b]);
         }
     }
-    for (int m = 0; m < 4; m++) {
+    for (int m = 0; m < c->nva; m++) {   /* nva = 2 without the angle rows (R51) */
         double e = X[m] - c->tau[4 + m];
         F = F + 0.5 * c->rva * e * e;
         g[m] = g[m] + c->rva * e;
@@ -830,9 +831,13 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
     const double TWO_PI = 6.283185307179586;
     double lo[6] = {wlo[0], wlo[1], -TWO_PI, -TWO_PI, 0.0, 0.0};
     double hi[6] = {whi[0], whi[1], TWO_PI, TWO_PI, 1.0, 1.0};
+    /* NEXT-3 variant 8 (R51): no angle consensus rows; the line's angles are local,
+     * with its own reference theta_i = 0 (only theta_i - theta_j enters the flows) */
+    if (pr->variant & 8) lo[2] = hi[2] = 0.0;
     double gtol = pr->tron_gtol_rel * dmax(rpq, rva);
     bctx c;
     c.y = y; c.tau = tau; c.rpq = rpq; c.rva = rva; c.al = 0;
+    c.nva = (pr->variant & 8) ? 2 : 4;
     c.r2 = rate * rate; c.mu[0] = c.mu[1] = 0.0; c.sig = 0.0;
     int it = 0;
     /* NEXT-3 variant 1 (R47): every rated branch goes straight to the six-variable AL from the
@@ -1291,7 +1296,9 @@ static void one_iteration(orc_ctx *c) {
                 /* NEXT-3 variant 2 (R47): SPEC's clip of wbar to the voltage box */
                 c->wbar[(size_t)i * T + t] = (pr->variant & 2)
                     ? clampd(vv[k], q->bus_vmin[i] * q->bus_vmin[i], q->bus_vmax[i] * q->bus_vmax[i]) : vv[k];
-                c->thbar[(size_t)i * T + t] = (i == q->ref_bus) ? 0.0 : tsum / (double)ne;
+                /* R51: without angle rows thetabar is not a variable (kept at its start value) */
+                if (!(pr->variant & 8))
+                    c->thbar[(size_t)i * T + t] = (i == q->ref_bus) ? 0.0 : tsum / (double)ne;
             }
         }
         free(al_); free(be_); free(aa); free(th); free(vv);
@@ -1353,6 +1360,7 @@ static void one_iteration(orc_ctx *c) {
             r[A_I] = c->x[4 * i + 2] - c->thbar[wi];  dx[A_I] = c->thbar[wi] - tbo[wi];
             r[A_J] = c->x[4 * i + 3] - c->thbar[wj];  dx[A_J] = c->thbar[wj] - tbo[wj];
             for (int k = 0; k < NBR; k++) {
+                if ((pr->variant & 8) && (k == A_I || k == A_J)) continue;   /* R51 */
                 double rho = (k < W_I) ? rpq : rva;
                 zy_row(r[k], rho, beta, &ZB(k, i), &YB(k, i), &LB(k, i), dx[k], &nm);
             }

@@ -54,7 +54,7 @@ template <bool AL>
 struct BrFun {
     double Gii, Gij, Gji, Gjj, Bii, Bij, Bji, Bjj;
     double tau[8];
-    double rpq, rva;
+    double rpq, rva, rvt;                       // rvt: rho of the angle rows (0 without them, R51)
     double K00, K02, K03, K11, K12, K13, K22;   // rho_pq M^T M (K01 = K23 = 0, K33 = K22)
     double mu0, mu1, sig, r2inv;                // AL only
 
@@ -87,13 +87,8 @@ struct BrFun {
         flows(x, C, S, f0, f1, f2, f3);
         double e0 = f0 - tau[0], e1 = f1 - tau[1], e2 = f2 - tau[2], e3 = f3 - tau[3];
         double F = 0.5 * rpq * (e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
-        double v = 0.0;
-#pragma unroll
-        for (int m = 0; m < 4; m++) {
-            double d = x[m] - tau[4 + m];
-            v += d * d;
-        }
-        F += 0.5 * rva * v;
+        const double d0 = x[0] - tau[4], d1 = x[1] - tau[5], d2 = x[2] - tau[6], d3 = x[3] - tau[7];
+        F += 0.5 * (rva * (d0 * d0 + d1 * d1) + rvt * (d2 * d2 + d3 * d3));
         if (AL) {
             double h0 = (f0 * f0 + f1 * f1) * r2inv - 1.0 + x[4];
             double h1 = (f2 * f2 + f3 * f3) * r2inv - 1.0 + x[5];
@@ -109,13 +104,8 @@ struct BrFun {
         flows(x, C, S, f0, f1, f2, f3);
         double e0 = f0 - tau[0], e1 = f1 - tau[1], e2 = f2 - tau[2], e3 = f3 - tau[3];
         F = 0.5 * rpq * (e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
-        double v = 0.0;
-#pragma unroll
-        for (int m = 0; m < 4; m++) {
-            double d = x[m] - tau[4 + m];
-            v += d * d;
-        }
-        F += 0.5 * rva * v;
+        const double d0 = x[0] - tau[4], d1 = x[1] - tau[5], d2 = x[2] - tau[6], d3 = x[3] - tau[7];
+        F += 0.5 * (rva * (d0 * d0 + d1 * d1) + rvt * (d2 * d2 + d3 * d3));
         // phi-space gradient rho_pq M^T e
         double Gw0 = rpq * (e0 * Gii - e1 * Bii);
         double Gw1 = rpq * (e2 * Gjj - e3 * Bjj);
@@ -163,7 +153,7 @@ struct BrFun {
         double dC[4] = {C * i2wi, C * i2wj, -S, S};
         double dS[4] = {S * i2wi, S * i2wj, C, -C};
 #pragma unroll
-        for (int m = 0; m < 4; m++) g[m] = GC * dC[m] + GS * dS[m] + rva * (x[m] - tau[4 + m]);
+        for (int m = 0; m < 4; m++) g[m] = GC * dC[m] + GS * dS[m] + (m < 2 ? rva : rvt) * (x[m] - tau[4 + m]);
         g[0] += Gw0;
         g[1] += Gw1;
         if (AL) {
@@ -205,7 +195,7 @@ struct BrFun {
         H[3][3] += -A;
         H[2][3] += A;
 #pragma unroll
-        for (int m = 0; m < 4; m++) H[m][m] += rva;
+        for (int m = 0; m < 4; m++) H[m][m] += m < 2 ? rva : rvt;
         if (AL) {
 #pragma unroll
             for (int m = 0; m < 4; m++) {
@@ -639,6 +629,7 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
     F.Bii = d.y[4 * d.L + l]; F.Bij = d.y[5 * d.L + l]; F.Bji = d.y[6 * d.L + l]; F.Bjj = d.y[7 * d.L + l];
     F.rpq = d.rpq;
     F.rva = d.rva;
+    F.rvt = (d.variant & 8) ? 0.0 : d.rva;   // NEXT-3 variant 8 (R51): no angle consensus rows
     const size_t wi = (size_t)bi * d.T + t, wj = (size_t)bj * d.T + t;
     const double xb[8] = {d.fbar[0 * LTs + k], d.fbar[1 * LTs + k], d.fbar[2 * LTs + k], d.fbar[3 * LTs + k],
                           d.wbar[wi], d.wbar[wj], d.thbar[wi], d.thbar[wj]};
@@ -716,6 +707,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         __shared__ double s_z[8][UCAC_BRANCH_TPB], s_y[8][UCAC_BRANCH_TPB];
         load_solve(d, k, F4, lo, hi, &s_z[0][threadIdx.x], &s_y[0][threadIdx.x], UCAC_BRANCH_TPB);
         lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
+        if (d.variant & 8) lo[2] = hi[2] = 0.0;   // R51: the line's own angle reference
         double x[4];
 #pragma unroll
         for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
@@ -813,11 +805,12 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
             F6.Bii = F4.Bii; F6.Bij = F4.Bij; F6.Bji = F4.Bji; F6.Bjj = F4.Bjj;
 #pragma unroll
             for (int r = 0; r < 8; r++) F6.tau[r] = F4.tau[r];
-            F6.rpq = F4.rpq; F6.rva = F4.rva;
+            F6.rpq = F4.rpq; F6.rva = F4.rva; F6.rvt = F4.rvt;
             F6.K00 = F4.K00; F6.K02 = F4.K02; F6.K03 = F4.K03; F6.K11 = F4.K11;
             F6.K12 = F4.K12; F6.K13 = F4.K13; F6.K22 = F4.K22;
         }
         lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
+        if (d.variant & 8) lo[2] = hi[2] = 0.0;   // R51
         lo[4] = 0.0; hi[4] = 1.0; lo[5] = 0.0; hi[5] = 1.0;
         const double rate = d.rate[k / d.T];
         const double r2 = rate * rate;

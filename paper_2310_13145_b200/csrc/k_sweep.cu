@@ -354,7 +354,8 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
             const double vl = d.vmin[i] * d.vmin[i], vh = d.vmax[i] * d.vmax[i];
             wb = wb < vl ? vl : (wb > vh ? vh : wb);
         }
-        const double tb = (i == d.ref_bus) ? 0.0 : tsum / (double)ne;
+        // NEXT-3 variant 8 (R51): no angle rows, thetabar is not a variable (kept at its start value)
+        const double tb = (d.variant & 8) ? tbo : ((i == d.ref_bus) ? 0.0 : tsum / (double)ne);
         d.wbar[k] = wb;
         d.thbar[k] = tb;
         d.bmu[0 * BT + k] = muP;
@@ -404,7 +405,8 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
     zy_vals(fp - pb, c.rpq, c.ibpq, z[0], y[0], lam[0], c.pending, c.beta_lam, c.lmax, pb - pbo, acc);
     zy_vals(fq - qb, c.rpq, c.ibpq, z[1], y[1], lam[1], c.pending, c.beta_lam, c.lmax, qb - qbo, acc);
     zy_vals(xw - wb, c.rva, c.ibva, z[2], y[2], lam[2], c.pending, c.beta_lam, c.lmax, dwb, acc);
-    zy_vals(xa - tb, c.rva, c.ibva, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
+    if (!(d.variant & 8))   // R51: without angle rows their z, y, lambda stay 0
+        zy_vals(xa - tb, c.rva, c.ibva, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
     FB(kp, k) = pb;
     FB(kq, k) = qb;
 #pragma unroll

@@ -288,11 +288,12 @@ def test_uc_warm_start_next2(name, iters):
     run_pair(dataclasses.replace(pb, u_init=ug), pr, 10)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6, 8, 9])
 def test_formulation_variants_next3(variant):
-    """NEXT-3 (R47): the AL for every rated branch (1), SPEC's w-bar clip (2), both (3);
-    NEXT-4(a) (R50): the ramp-aware DP (4), on a case30 variant with S^D = Pmin/2 so the excluded
-    shutdowns occur -- each keeps GPU/oracle parity, schedules bit-exact."""
+    """NEXT-3 (R47, R51): the AL for every rated branch (1), SPEC's w-bar clip (2), no angle
+    consensus rows (8), and combinations; NEXT-4(a) (R50): the ramp-aware DP (4), on a case30
+    variant with S^D = Pmin/2 so the excluded shutdowns occur -- each keeps GPU/oracle parity,
+    schedules bit-exact."""
     import dataclasses
     pb, pr = inputs.build_config("case30")
     if variant & 4:

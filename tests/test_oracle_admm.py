@@ -312,3 +312,36 @@ def test_ramp_aware_dp_next4():
     v0, s0 = _shutdowns_above_sd(pb, pr, 300)
     assert v4 == 0 and s4 > 0, (v4, s4)
     assert v0 > 0, (v0, s0)
+
+
+def test_no_angle_consensus_variant_next3():
+    """NEXT-3 variant 8 (R51): without angle consensus rows the A_I/A_J rows keep
+    z = y = lambda = 0, thetabar stays at its start value, every line keeps its own reference
+    theta_i = 0, and a line's solution does not depend on the angle targets tau_6, tau_7."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    pr8 = dataclasses.replace(pr, variant=8)
+    o = oracle.Oracle(pb, pr8)
+    o.iterate(60)
+    st = o.get_state()
+    LT = pb.nbranch * pb.T
+    zb, yb, lb = (st[k].reshape(8, LT) for k in ("zb", "yb", "lb"))
+    assert np.all(zb[6:] == 0) and np.all(yb[6:] == 0) and np.all(lb[6:] == 0)
+    assert np.all(st["thbar"] == 0)
+    x = st["x"].reshape(LT, 4)
+    assert np.all(x[:, 2] == 0) and np.any(x[:, 3] != 0)
+    assert o.report()["outer_total"] >= 1
+    o.close()
+    # angle targets do not enter the line problem
+    rng = np.random.default_rng(5)
+    y = pb.br_y[0]
+    xs = np.array([1.0, 0.98, 0.0, -0.05])
+    tau = np.concatenate([oracle.branch_flows(y, xs)[0] * 1.1, xs])
+    tau2 = tau.copy()
+    tau2[6:] += rng.normal(size=2)
+    a = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 0.0, tau, pr.rho_pq, pr.rho_va, pr8, xs.copy(), np.zeros(3))
+    b = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 0.0, tau2, pr.rho_pq, pr.rho_va, pr8, xs.copy(), np.zeros(3))
+    assert np.array_equal(a[0], b[0]) and a[0][2] == 0.0
+    c = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 0.0, tau2, pr.rho_pq, pr.rho_va, pr, xs.copy(), np.zeros(3))
+    assert not np.array_equal(a[0], c[0])
+
