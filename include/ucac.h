@@ -105,7 +105,9 @@ typedef struct {
                            4 = ramp-aware DP (NEXT-4(a), R50): no shutdown at t while the current
                            dispatch p_{t-1} (p0 at t = 1) exceeds the shutdown ramp S^D,
                            8 = no angle consensus rows (SPEC, R51): each line keeps theta_i = 0 and
-                           its own angle difference; thetabar is not updated */
+                           its own angle difference; thetabar is not updated,
+                           16 = the literal Eq. 5f ramp-down row R_D ubar^on_{t-1} + S_D ubar^su_t
+                           (R52) instead of Eq. 4d's R_D ubar^on_t + S_D ubar^sd_t */
 } ucac_params;
 
 /* Multi-GPU (bus-graph cut).  NULL = single GPU.

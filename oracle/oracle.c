@@ -1140,7 +1140,11 @@ static void one_iteration(orc_ctx *c) {
             in[10] = q->pmax[g] * on - ZG(PU, i) - YG(PU, i) / ruc;
             in[11] = q->qmin[g] * on - ZG(QL, i) - YG(QL, i) / ruc;
             in[12] = q->qmax[g] * on - ZG(QU, i) - YG(QU, i) / ruc;
-            in[13] = -q->ramp_dn[g] * on - q->sd_ramp[g] * sd - ZG(RD, i) - YG(RD, i) / ruc;
+            /* RD row: Eq. 4d (R_D ubar^on_t + S_D ubar^sd_t), or the literal Eq. 5f
+             * (R_D ubar^on_{t-1} + S_D ubar^su_t) with variant bit 16 (R52) */
+            in[13] = (pr->variant & 16)
+                ? -q->ramp_dn[g] * onp - q->sd_ramp[g] * su - ZG(RD, i) - YG(RD, i) / ruc
+                : -q->ramp_dn[g] * on - q->sd_ramp[g] * sd - ZG(RD, i) - YG(RD, i) / ruc;
             in[14] = q->ramp_up[g] * onp + q->su_ramp[g] * su - ZG(RU, i) - YG(RU, i) / ruc;
             in[15] = pL; in[16] = pU; in[17] = qL; in[18] = qU;
             double o[3];
@@ -1183,6 +1187,7 @@ static void one_iteration(orc_ctx *c) {
     free(unew);
 
     /* ---- (7c) xbar^UC: ubar per (g, group) on x^{l+1}, u^{l+1} (R19) ---- */
+    const int lit5f = (pr->variant & 16) != 0;
     for (int g = 0; g < G; g++) {
         double Pm = q->pmin[g], PM = q->pmax[g], Qm = q->qmin[g], QM = q->qmax[g];
         double RDn = q->ramp_dn[g], SDn = q->sd_ramp[g], RUp = q->ramp_up[g], SUp = q->su_ramp[g];
@@ -1198,6 +1203,10 @@ static void one_iteration(orc_ctx *c) {
                 e[m++] = (double)su1 + ZG(D_SU, i) + YG(D_SU, i) / ruc;
                 cm[m * 3 + 0] = SUp; cm[m * 3 + 1] = 0; cm[m * 3 + 2] = 0;
                 e[m++] = (c->p[i] - c->ph[i]) + c->sl[6 * i + 5] - RUp * (double)q->u0[g] + ZG(RU, i) + YG(RU, i) / ruc;
+                if (lit5f) {   /* R52: RD_1 = (d - s) + R_D u0 + S_D ubar^su_1 */
+                    cm[m * 3 + 0] = -SDn; cm[m * 3 + 1] = 0; cm[m * 3 + 2] = 0;
+                    e[m++] = ((c->p[i] - c->ph[i]) - c->sl[6 * i + 4]) + RDn * (double)q->u0[g] + ZG(RD, i) + YG(RD, i) / ruc;
+                }
                 double v[3];
                 orc_boxqp3(n, m, cm, e, v);
                 c->ub[1][i] = v[0];
@@ -1215,12 +1224,15 @@ static void one_iteration(orc_ctx *c) {
             ROW(PM, 0.0, 0.0, (c->p[i] + c->sl[6 * i + 1]) + ZG(PU, i) + YG(PU, i) / ruc);
             ROW(Qm, 0.0, 0.0, (c->q[i] - c->sl[6 * i + 2]) + ZG(QL, i) + YG(QL, i) / ruc);
             ROW(QM, 0.0, 0.0, (c->q[i] + c->sl[6 * i + 3]) + ZG(QU, i) + YG(QU, i) / ruc);
-            ROW(-RDn, -SDn, 0.0, ((c->p[i] - c->ph[i]) - c->sl[6 * i + 4]) + ZG(RD, i) + YG(RD, i) / ruc);
+            if (!lit5f)
+                ROW(-RDn, -SDn, 0.0, ((c->p[i] - c->ph[i]) - c->sl[6 * i + 4]) + ZG(RD, i) + YG(RD, i) / ruc);
             if (t < T - 1) {
                 size_t j = i + 1;
                 int sun = c->u[j] > ut;
                 ROW(0.0, 0.0, 1.0, (double)sun + ZG(D_SU, j) + YG(D_SU, j) / ruc);
                 ROW(RUp, 0.0, SUp, ((c->p[j] - c->ph[j]) + c->sl[6 * j + 5]) + ZG(RU, j) + YG(RU, j) / ruc);
+                if (lit5f)   /* R52: RD_{t+1} = (d - s) + R_D ubar^on_t + S_D ubar^su_{t+1} */
+                    ROW(-RDn, 0.0, -SDn, ((c->p[j] - c->ph[j]) - c->sl[6 * j + 4]) + ZG(RD, j) + YG(RD, j) / ruc);
             }
 #undef ROW
             double v[3];
@@ -1327,8 +1339,13 @@ static void one_iteration(orc_ctx *c) {
             r[PU] = (p + s[1]) - PM * on;         dx[PU] = PM * don;
             r[QL] = (qq - s[2]) - Qm * on;        dx[QL] = Qm * don;
             r[QU] = (qq + s[3]) - QM * on;        dx[QU] = QM * don;
-            r[RD] = (d - s[4]) + q->ramp_dn[g] * on + q->sd_ramp[g] * ubsd;
-            dx[RD] = q->ramp_dn[g] * don + q->sd_ramp[g] * dsd;
+            if (pr->variant & 16) {   /* literal Eq. 5f (R52) */
+                r[RD] = (d - s[4]) + q->ramp_dn[g] * onp + q->sd_ramp[g] * ubsu;
+                dx[RD] = q->ramp_dn[g] * donp + q->sd_ramp[g] * dsu;
+            } else {
+                r[RD] = (d - s[4]) + q->ramp_dn[g] * on + q->sd_ramp[g] * ubsd;
+                dx[RD] = q->ramp_dn[g] * don + q->sd_ramp[g] * dsd;
+            }
             r[RU] = (d + s[5]) - q->ramp_up[g] * onp - q->su_ramp[g] * ubsu;
             dx[RU] = q->ramp_up[g] * donp + q->su_ramp[g] * dsu;
             r[GP] = p - c->pbar[i];               dx[GP] = c->pbar[i] - pbo[i];

@@ -50,11 +50,13 @@ __device__ __forceinline__ double rcp(double x) {
     return fma(r, e, r);
 }
 
-template <bool AL>
+// NOANG: no angle consensus rows (variant bit 8, R51) -- a separate instantiation, so the default
+// kernels carry none of its code
+template <bool AL, bool NOANG = false>
 struct BrFun {
     double Gii, Gij, Gji, Gjj, Bii, Bij, Bji, Bjj;
     double tau[8];
-    double rpq, rva, rvt;                       // rvt: rho of the angle rows (0 without them, R51)
+    double rpq, rva;
     double K00, K02, K03, K11, K12, K13, K22;   // rho_pq M^T M (K01 = K23 = 0, K33 = K22)
     double mu0, mu1, sig, r2inv;                // AL only
 
@@ -87,8 +89,13 @@ struct BrFun {
         flows(x, C, S, f0, f1, f2, f3);
         double e0 = f0 - tau[0], e1 = f1 - tau[1], e2 = f2 - tau[2], e3 = f3 - tau[3];
         double F = 0.5 * rpq * (e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
-        const double d0 = x[0] - tau[4], d1 = x[1] - tau[5], d2 = x[2] - tau[6], d3 = x[3] - tau[7];
-        F += 0.5 * (rva * (d0 * d0 + d1 * d1) + rvt * (d2 * d2 + d3 * d3));
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < (NOANG ? 2 : 4); m++) {
+            double d = x[m] - tau[4 + m];
+            v += d * d;
+        }
+        F += 0.5 * rva * v;
         if (AL) {
             double h0 = (f0 * f0 + f1 * f1) * r2inv - 1.0 + x[4];
             double h1 = (f2 * f2 + f3 * f3) * r2inv - 1.0 + x[5];
@@ -104,8 +111,13 @@ struct BrFun {
         flows(x, C, S, f0, f1, f2, f3);
         double e0 = f0 - tau[0], e1 = f1 - tau[1], e2 = f2 - tau[2], e3 = f3 - tau[3];
         F = 0.5 * rpq * (e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
-        const double d0 = x[0] - tau[4], d1 = x[1] - tau[5], d2 = x[2] - tau[6], d3 = x[3] - tau[7];
-        F += 0.5 * (rva * (d0 * d0 + d1 * d1) + rvt * (d2 * d2 + d3 * d3));
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < (NOANG ? 2 : 4); m++) {
+            double d = x[m] - tau[4 + m];
+            v += d * d;
+        }
+        F += 0.5 * rva * v;
         // phi-space gradient rho_pq M^T e
         double Gw0 = rpq * (e0 * Gii - e1 * Bii);
         double Gw1 = rpq * (e2 * Gjj - e3 * Bjj);
@@ -153,7 +165,7 @@ struct BrFun {
         double dC[4] = {C * i2wi, C * i2wj, -S, S};
         double dS[4] = {S * i2wi, S * i2wj, C, -C};
 #pragma unroll
-        for (int m = 0; m < 4; m++) g[m] = GC * dC[m] + GS * dS[m] + (m < 2 ? rva : rvt) * (x[m] - tau[4 + m]);
+        for (int m = 0; m < 4; m++) g[m] = GC * dC[m] + GS * dS[m] + ((NOANG && m >= 2) ? 0.0 : rva * (x[m] - tau[4 + m]));
         g[0] += Gw0;
         g[1] += Gw1;
         if (AL) {
@@ -195,7 +207,7 @@ struct BrFun {
         H[3][3] += -A;
         H[2][3] += A;
 #pragma unroll
-        for (int m = 0; m < 4; m++) H[m][m] += m < 2 ? rva : rvt;
+        for (int m = 0; m < (NOANG ? 2 : 4); m++) H[m][m] += rva;
         if (AL) {
 #pragma unroll
             for (int m = 0; m < 4; m++) {
@@ -620,7 +632,8 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long *dst, unsigned l
 
 // load the data of solve k = l*T + t: admittances, targets tau = xbar - z - y/rho (5.1), w bounds
 // zs/ys (optional, stride `ss`): keep z and y/rho of the 8 rows for the tauhat emission
-__device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F, double *wlo, double *whi,
+template <bool NOANG>
+__device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false, NOANG> &F, double *wlo, double *whi,
                                            double *zs = nullptr, double *ys = nullptr, int ss = 0) {
     const size_t LTs = (size_t)d.L * d.T;
     const int l = k / d.T, t = k - l * d.T;
@@ -629,7 +642,6 @@ __device__ __forceinline__ void load_solve(const Dev &d, int k, BrFun<false> &F,
     F.Bii = d.y[4 * d.L + l]; F.Bij = d.y[5 * d.L + l]; F.Bji = d.y[6 * d.L + l]; F.Bjj = d.y[7 * d.L + l];
     F.rpq = d.rpq;
     F.rva = d.rva;
-    F.rvt = (d.variant & 8) ? 0.0 : d.rva;   // NEXT-3 variant 8 (R51): no angle consensus rows
     const size_t wi = (size_t)bi * d.T + t, wj = (size_t)bj * d.T + t;
     const double xb[8] = {d.fbar[0 * LTs + k], d.fbar[1 * LTs + k], d.fbar[2 * LTs + k], d.fbar[3 * LTs + k],
                           d.wbar[wi], d.wbar[wj], d.thbar[wi], d.thbar[wj]};
@@ -690,6 +702,7 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #ifndef UCAC_AL_BLOCKS_PER_SM
 #define UCAC_AL_BLOCKS_PER_SM 1
 #endif
+template <bool NOANG>
 __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(Dev d) {
     TL_KERNEL(K_BRANCH);
     if (d.st->done) return;
@@ -701,13 +714,13 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
     const int k = base + threadIdx.x;
     if (k < LT) {
         const size_t LTs = (size_t)LT;
-        BrFun<false> F4;
+        BrFun<false, NOANG> F4;
         double lo[4], hi[4];
         // z and y/rho of the 8 rows, kept in shared memory for the tauhat emission
         __shared__ double s_z[8][UCAC_BRANCH_TPB], s_y[8][UCAC_BRANCH_TPB];
         load_solve(d, k, F4, lo, hi, &s_z[0][threadIdx.x], &s_y[0][threadIdx.x], UCAC_BRANCH_TPB);
         lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
-        if (d.variant & 8) lo[2] = hi[2] = 0.0;   // R51: the line's own angle reference
+        if (NOANG) lo[2] = hi[2] = 0.0;   // R51: the line's own angle reference
         double x[4];
 #pragma unroll
         for (int m = 0; m < 4; m++) x[m] = d.x[m * LTs + k];
@@ -770,6 +783,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
 
 // Phase 2: the queued thermal-active solves (6-variable slack AL, R36), pulled one at a time
 // by every thread of a persistent grid, so the heavy tail is spread over all SMs.
+template <bool NOANG>
 __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
     TL_KERNEL(K_BRANCH_AL);
     if (d.st->done) return;
@@ -796,21 +810,21 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         const unsigned long long it0 = c_it;
 #endif
-        BrFun<true> F6;
+        BrFun<true, NOANG> F6;
         double lo[6], hi[6];
         {
-            BrFun<false> F4;
+            BrFun<false, NOANG> F4;
             load_solve(d, k, F4, lo, hi);
             F6.Gii = F4.Gii; F6.Gij = F4.Gij; F6.Gji = F4.Gji; F6.Gjj = F4.Gjj;
             F6.Bii = F4.Bii; F6.Bij = F4.Bij; F6.Bji = F4.Bji; F6.Bjj = F4.Bjj;
 #pragma unroll
             for (int r = 0; r < 8; r++) F6.tau[r] = F4.tau[r];
-            F6.rpq = F4.rpq; F6.rva = F4.rva; F6.rvt = F4.rvt;
+            F6.rpq = F4.rpq; F6.rva = F4.rva;
             F6.K00 = F4.K00; F6.K02 = F4.K02; F6.K03 = F4.K03; F6.K11 = F4.K11;
             F6.K12 = F4.K12; F6.K13 = F4.K13; F6.K22 = F4.K22;
         }
         lo[2] = -TWO_PI; hi[2] = TWO_PI; lo[3] = -TWO_PI; hi[3] = TWO_PI;
-        if (d.variant & 8) lo[2] = hi[2] = 0.0;   // R51
+        if (NOANG) lo[2] = hi[2] = 0.0;   // R51
         lo[4] = 0.0; hi[4] = 1.0; lo[5] = 0.0; hi[5] = 1.0;
         const double rate = d.rate[k / d.T];
         const double r2 = rate * rate;
@@ -919,20 +933,25 @@ void launch_branch(const Dev &d, cudaStream_t s) {
     // SM to drain
     static const bool carve = [] {
         return UCAC_BRANCH_CARVEOUT < 0 ||
-               cudaFuncSetAttribute(k_branch, cudaFuncAttributePreferredSharedMemoryCarveout, UCAC_BRANCH_CARVEOUT) == cudaSuccess;
+               cudaFuncSetAttribute(k_branch<false>, cudaFuncAttributePreferredSharedMemoryCarveout, UCAC_BRANCH_CARVEOUT) == cudaSuccess;
     }();
     (void)carve;
     const int n = d.L * d.T, chunks = (n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB;
     // 148 SMs x UCAC_BRANCH_MINB resident blocks, minus the slots left to the generator chain
     const int grid = std::max(1, std::min(chunks, 148 * UCAC_BRANCH_MINB - UCAC_BRANCH_FREE_SLOTS));
-    k_branch<<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
+    if (d.variant & 8) k_branch<true><<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
+    else k_branch<false><<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
 }
 #ifndef UCAC_AL_SMEM
 #define UCAC_AL_SMEM 0   // dynamic shared memory per AL block (bytes): > 0 reserves SMs for the AL work
 #endif
 void launch_branch_al(const Dev &d, cudaStream_t s) {
-    if (UCAC_AL_SMEM > 48 * 1024) cudaFuncSetAttribute(k_branch_al, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
-    k_branch_al<<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, UCAC_AL_SMEM, s>>>(d);
+    if (UCAC_AL_SMEM > 48 * 1024) {
+        cudaFuncSetAttribute(k_branch_al<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
+        cudaFuncSetAttribute(k_branch_al<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
+    }
+    if (d.variant & 8) k_branch_al<true><<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, UCAC_AL_SMEM, s>>>(d);
+    else k_branch_al<false><<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, UCAC_AL_SMEM, s>>>(d);
 }
 
 }  // namespace ucac

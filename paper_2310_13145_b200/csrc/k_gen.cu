@@ -302,7 +302,9 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
     in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) * d.iruc;
     in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) * d.iruc;
     in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) * d.iruc;
-    in.brl = -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) * d.iruc;
+    // RD row: Eq. 4d, or the literal Eq. 5f with variant bit 16 (R52)
+    in.brl = (d.variant & 16) ? -rdn * onp - sdn * su - ZG(G_RD, i) - YG(G_RD, i) * d.iruc
+                              : -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) * d.iruc;
     in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) * d.iruc;
     double po, qo, pho;
     gen_solve(in, po, qo, pho);

@@ -576,6 +576,9 @@ __device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, doub
     }
 }
 
+// LIT: the literal Eq. 5f ramp-down row (variant bit 16, R52), a separate instantiation so the
+// default kernel carries none of its code
+template <bool LIT>
 __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
     TL_KERNEL(K_UBAR);
     if (d.st->done) return;
@@ -603,7 +606,10 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         const double bpu = PM * on_o - ZG(G_PU, i) - YG(G_PU, i) * iruc;
         const double bql = Qm * on_o - ZG(G_QL, i) - YG(G_QL, i) * iruc;
         const double bqu = QM * on_o - ZG(G_QU, i) - YG(G_QU, i) * iruc;
-        const double brl = -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) * iruc;
+        // NEXT-3 variant 16 (R52): the literal Eq. 5f ramp-down row R_D ubar^on_{t-1} + S_D ubar^su_t
+        constexpr bool lit = LIT;
+        const double brl = lit ? -RDn * onp_o - SDn * su_o - ZG(G_RD, i) - YG(G_RD, i) * iruc
+                               : -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) * iruc;
         const double dd = p - ph;
         const double spl = fmax(0.0, p - bpl), spu = fmax(0.0, bpu - p);
         const double sql = fmax(0.0, q - bql), squ = fmax(0.0, bqu - q);
@@ -623,10 +629,10 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         ROW(PM, 0.0, 0.0, (p + spu) + ZG(G_PU, i) + YG(G_PU, i) * iruc);
         ROW(Qm, 0.0, 0.0, (q - sql) + ZG(G_QL, i) + YG(G_QL, i) * iruc);
         ROW(QM, 0.0, 0.0, (q + squ) + ZG(G_QU, i) + YG(G_QU, i) * iruc);
-        ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) * iruc);
+        if (!lit) ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) * iruc);
         int n = 2;
         int sun = 0;
-        double pn = 0.0, phn = 0.0, sru_n = 0.0, su_on = 0.0;
+        double pn = 0.0, phn = 0.0, sru_n = 0.0, su_on = 0.0, srd_n = 0.0;
         if (t < T - 1) {
             const size_t j = i + 1;
             const int un = d.u[j];
@@ -638,13 +644,18 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
             sru_n = fmax(0.0, bru_n - (pn - phn));
             ROW(0.0, 0.0, 1.0, (double)sun + ZG(G_DSU, j) + YG(G_DSU, j) * iruc);
             ROW(RUp, 0.0, SUp, ((pn - phn) + sru_n) + ZG(G_RU, j) + YG(G_RU, j) * iruc);
+            if (lit) {   // RD_{t+1} = (d - s) + R_D ubar^on_t + S_D ubar^su_{t+1}: this group's row
+                const double brl_n = -RDn * on_o - SDn * su_on - ZG(G_RD, j) - YG(G_RD, j) * iruc;
+                srd_n = fmax(0.0, (pn - phn) - brl_n);
+                ROW(-RDn, 0.0, -SDn, ((pn - phn) - srd_n) + ZG(G_RD, j) + YG(G_RD, j) * iruc);
+            }
             n = 3;
         }
 #undef ROW
         // z, y, lambda of the group's rows, all loaded before any store (a store to one row array
         // would otherwise order every later row's loads behind it)
         const int rk[7] = {G_DON, G_DSD, G_PL, G_PU, G_QL, G_QU, G_RD};
-        double zr[9], yr[9], lr[9];
+        double zr[10], yr[10], lr[10];
 #pragma unroll
         for (int q2 = 0; q2 < 7; q2++) {
             zr[q2] = ZG(rk[q2], i);
@@ -655,6 +666,7 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         if (nxt) {
             zr[7] = ZG(G_DSU, i + 1); yr[7] = YG(G_DSU, i + 1); lr[7] = LG(G_DSU, i + 1);
             zr[8] = ZG(G_RU, i + 1);  yr[8] = YG(G_RU, i + 1);  lr[8] = LG(G_RU, i + 1);
+            if (lit) { zr[9] = ZG(G_RD, i + 1); yr[9] = YG(G_RD, i + 1); lr[9] = LG(G_RD, i + 1); }
         }
         double v[3];
         boxqp3(n, m, cm, e, v);
@@ -667,8 +679,9 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         zy_vals((p + spu) - PM * on_n, ruc, ibuc, zr[3], yr[3], lr[3], pending, beta_lam, lmax, PM * don, acc);
         zy_vals((q - sql) - Qm * on_n, ruc, ibuc, zr[4], yr[4], lr[4], pending, beta_lam, lmax, Qm * don, acc);
         zy_vals((q + squ) - QM * on_n, ruc, ibuc, zr[5], yr[5], lr[5], pending, beta_lam, lmax, QM * don, acc);
-        zy_vals((dd - srd) + RDn * on_n + SDn * sd_n, ruc, ibuc, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
-                RDn * don + SDn * dsd, acc);
+        if (!lit)
+            zy_vals((dd - srd) + RDn * on_n + SDn * sd_n, ruc, ibuc, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
+                    RDn * don + SDn * dsd, acc);
         double su_n = 0.0;
         if (nxt) {
             su_n = v[2];
@@ -676,11 +689,16 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
             zy_vals((double)sun - su_n, ruc, ibuc, zr[7], yr[7], lr[7], pending, beta_lam, lmax, dsu, acc);
             zy_vals(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, ibuc, zr[8], yr[8], lr[8], pending, beta_lam,
                     lmax, RUp * don + SUp * dsu, acc);
+            if (lit)
+                zy_vals(((pn - phn) - srd_n) + RDn * on_n + SDn * su_n, ruc, ibuc, zr[9], yr[9], lr[9], pending,
+                        beta_lam, lmax, RDn * don + SDn * dsu, acc);
         }
         d.ub_on[i] = on_n;
         d.ub_sd[i] = sd_n;
+        // (literal Eq. 5f: RD_t belongs to group t-1, whose thread stores it; not stored here)
 #pragma unroll
         for (int q2 = 0; q2 < 7; q2++) {
+            if (lit && q2 == 6) continue;
             ZG(rk[q2], i) = zr[q2];
             YG(rk[q2], i) = yr[q2];
             if (pending) LG(rk[q2], i) = lr[q2];
@@ -693,23 +711,32 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
                 LG(G_DSU, i + 1) = lr[7];
                 LG(G_RU, i + 1) = lr[8];
             }
+            if (lit) {
+                ZG(G_RD, i + 1) = zr[9]; YG(G_RD, i + 1) = yr[9];
+                if (pending) LG(G_RD, i + 1) = lr[9];
+            }
         }
         if (t == 0) {
             // group 0 = (ubar^su_1): rows D_SU_1, RU_1 (ubar^on_0 := u0, R4)
             const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) * iruc;
             const double sru = fmax(0.0, bru - dd);
-            double c1[2][3] = {{1.0, 0.0, 0.0}, {SUp, 0.0, 0.0}};
-            double e1[2];
+            double c1[3][3] = {{1.0, 0.0, 0.0}, {SUp, 0.0, 0.0}, {-SDn, 0.0, 0.0}};
+            double e1[3];
             e1[0] = (double)sut + ZG(G_DSU, i) + YG(G_DSU, i) * iruc;
             e1[1] = (dd + sru) - RUp * (double)u0 + ZG(G_RU, i) + YG(G_RU, i) * iruc;
+            // literal Eq. 5f (R52): RD_1 = (d - s) + R_D u0 + S_D ubar^su_1 joins this group
+            e1[2] = ((dd - srd) + RDn * (double)u0) + ZG(G_RD, i) + YG(G_RD, i) * iruc;
             double v1[3];
-            boxqp3(1, 2, c1, e1, v1);
+            boxqp3(1, lit ? 3 : 2, c1, e1, v1);
             d.ub_su[i] = v1[0];
             const double dsu = v1[0] - su_o;
             zy_row((double)sut - v1[0], ruc, ibuc, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
                    acc);
             zy_row((dd + sru) - RUp * (double)u0 - SUp * v1[0], ruc, ibuc, &ZG(G_RU, i), &YG(G_RU, i), &LG(G_RU, i),
                    pending, beta_lam, lmax, SUp * dsu, acc);
+            if (lit)
+                zy_row((dd - srd) + RDn * (double)u0 + SDn * v1[0], ruc, ibuc, &ZG(G_RD, i), &YG(G_RD, i), &LG(G_RD, i),
+                       pending, beta_lam, lmax, SDn * dsu, acc);
         }
         // objective, Eq. 1a with f^OPF = c2 (S p)^2 + c1 S p and f^UC (R13)
         const double Sp = d.S * p;
@@ -845,7 +872,10 @@ int nblk_lbus(int n) { return (n + LBUS_THREADS - 1) / LBUS_THREADS; }
 int nblk_lrows(int n) { return (n + LROWS_THREADS - 1) / LROWS_THREADS; }
 int fold_blocks() { return FOLD_BLOCKS; }
 void launch_fold_early(const Dev &d, cudaStream_t s) { k_fold_early<<<FOLD_BLOCKS, FOLD_THREADS, 0, s>>>(d); }
-void launch_ubar(const Dev &d, cudaStream_t s) { launch_hi_prio(k_ubar, dim3(d.nblk_ubar), dim3(UBAR_THREADS), 0, s, d); }
+void launch_ubar(const Dev &d, cudaStream_t s) {
+    if (d.variant & 16) launch_hi_prio(k_ubar<true>, dim3(d.nblk_ubar), dim3(UBAR_THREADS), 0, s, d);
+    else launch_hi_prio(k_ubar<false>, dim3(d.nblk_ubar), dim3(UBAR_THREADS), 0, s, d);
+}
 void launch_finalize(const Dev &d, cudaStream_t s) { k_finalize<<<1, 32, 0, s>>>(d); }
 static int xgrid(int n) { return std::max(1, std::min(296, (n + 255) / 256)); }
 void launch_pack_tau(const Dev &d, cudaStream_t s) { k_pack_tau<<<xgrid(d.ncut * 4 * d.T), 256, 0, s>>>(d); }

@@ -288,7 +288,7 @@ def test_uc_warm_start_next2(name, iters):
     run_pair(dataclasses.replace(pb, u_init=ug), pr, 10)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6, 8, 9])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6, 8, 9, 16, 17])
 def test_formulation_variants_next3(variant):
     """NEXT-3 (R47, R51): the AL for every rated branch (1), SPEC's w-bar clip (2), no angle
     consensus rows (8), and combinations; NEXT-4(a) (R50): the ramp-aware DP (4), on a case30

@@ -345,3 +345,46 @@ def test_no_angle_consensus_variant_next3():
     c = oracle.branch_solve(y, [0.81, 0.81], [1.21, 1.21], 0.0, tau2, pr.rho_pq, pr.rho_va, pr, xs.copy(), np.zeros(3))
     assert not np.array_equal(a[0], c[0])
 
+
+
+def test_literal_eq5f_ramp_down_next3():
+    """NEXT-3 variant 16 (R52): the ramp-down row is the literal Eq. 5f,
+    (p_t - p^_t) - s + R_D ubar^on_{t-1} + S_D ubar^su_t, instead of Eq. 4d.
+    Pins, one iteration from a mid-run state:
+    * the RD row residual recovered from the y update, r = (y+ - y)/rho - z+, equals the
+      literal row evaluated on the new iterate (slack from the x-step's bound on the old ubar);
+    * ubar^sd is in no physical row any more, so (7c) gives it the projection of its duplicate
+      row's target: clip(u^sd + z + y/rho, 0, 1)."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    pr16 = dataclasses.replace(pr, variant=16, outer_enabled=0)
+    q = pb.normalized()
+    G, T = q.ngen, q.T
+    o = oracle.Oracle(pb, pr16)
+    o.iterate(25)
+    s0 = o.get_state()
+    o.iterate(1)
+    s1 = o.get_state()
+    o.close()
+    ruc = pr.rho_uc
+    RD, DSD = 7, 2
+    z0, y0 = s0["zg"].reshape(12, G, T), s0["yg"].reshape(12, G, T)
+    z1, y1 = s1["zg"].reshape(12, G, T), s1["yg"].reshape(12, G, T)
+    on0, su0 = s0["ub_on"].reshape(G, T), s0["ub_su"].reshape(G, T)
+    on1, su1, sd1 = (s1[k].reshape(G, T) for k in ("ub_on", "ub_su", "ub_sd"))
+    u1 = s1["u"].reshape(G, T)
+    dd = (s1["p"] - s1["ph"]).reshape(G, T)
+    worst = 0.0
+    for g in range(G):
+        for t in range(T):
+            onp0 = q.u0[g] if t == 0 else on0[g, t - 1]
+            onp1 = q.u0[g] if t == 0 else on1[g, t - 1]
+            brl = -q.ramp_dn[g] * onp0 - q.sd_ramp[g] * su0[g, t] - z0[RD, g, t] - y0[RD, g, t] / ruc
+            s4 = max(0.0, dd[g, t] - brl)
+            r_lit = (dd[g, t] - s4) + q.ramp_dn[g] * onp1 + q.sd_ramp[g] * su1[g, t]
+            r_y = (y1[RD, g, t] - y0[RD, g, t]) / ruc - z1[RD, g, t]
+            worst = max(worst, abs(r_lit - r_y))
+            up = q.u0[g] if t == 0 else u1[g, t - 1]
+            sd = float(up > u1[g, t])
+            assert abs(sd1[g, t] - np.clip(sd + z0[DSD, g, t] + y0[DSD, g, t] / ruc, 0.0, 1.0)) <= 1e-12
+    assert worst <= 1e-9, worst
