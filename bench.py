@@ -283,6 +283,18 @@ def run_warmstart(args, pb, pr, rank):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic() -> dict:
+    """DRAM bytes per launch (read + write) of the dominant kernels from the committed ncu
+    --set full capture (profiles/r01/ncu_traffic.json; cold-cache, one launch each)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")))
+        out = {k: v["traffic"] for k, v in d["kernels"].items()}
+        out["_note"] = "dram bytes per launch, " + d["source"]
+        return out
+    except (OSError, ValueError, KeyError):
+        return {}
+
+
 def time_to_residual(target: float = 1e-4, cap: int = 5000, chunk: int = 25):
     """The "time-to-residual 1e-4" part of the metric on BASELINE configs[0] (case9, T=4, Table I
     rho): cold start, the GPU iterates in chunks with the on-device primal stop until primal
@@ -441,14 +453,16 @@ def main():
                 "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                 "ms_per_step": t / args.steps, "share_of_step": t / ksum}
         dom = max(("k_branch", "k_branch_al"), key=lambda k: kms[k])
+        traffic = ncu_traffic()
         if max(kms, key=kms.get) == dom:
-            roofline = dict(kernels[dom], kernel=dom, traffic=None,
+            roofline = dict(kernels[dom], kernel=dom, traffic=traffic.get(dom),
+                            traffic_note=traffic.get("_note"),
                             peak_note=fp64_note + "; flops = the kernel's Newton iterations (live counter) x "
                                       "its FP64 flops per Newton iteration (ncu SASS count, tools/calibrate_flops.py)")
         else:
             dom = max(kms, key=kms.get)
             roofline = {"bound": "hbm", "kernel": dom, "achieved": sizes["alg_bytes"][dom] * args.steps /
-                        (kms[dom] * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s", "traffic": None,
+                        (kms[dom] * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s", "traffic": traffic.get(dom),
                         "ms_per_step": kms[dom] / args.steps, "share_of_step": kms[dom] / ksum}
             roofline["frac"] = roofline["achieved"] / hbm
 

@@ -14,13 +14,16 @@ if [ -z "${SKIP_TESTS:-}" ]; then
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?"
 fi
 timeout 600 python bench.py > "$OUT/bench.jsonl" 2> "$OUT/bench.err"; rc=$?
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > "$OUT/bench_reference.jsonl" 2> "$OUT/bench_reference.err"
+echo "reference rc=$?"; tail -c 600 "$OUT/bench_reference.jsonl"
 echo "bench rc=$rc"; tail -c 3000 "$OUT/bench.jsonl"
 [ $rc -eq 0 ] || { tail -20 "$OUT/bench.err"; exit 1; }
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1
 echo "ncu launches rc=$?"
 for k in "$@"; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k "$k" -s 3 -c 1 \
+  # kernel names match as a regex on the function name (k_branch is a template: k_branch<false>)
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^${k}(<|\$)" -s 3 -c 1 \
     -o "$OUT/full_$k" python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_full_$k.log" 2>&1
   echo "ncu full $k rc=$?"
 done

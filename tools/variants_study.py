@@ -14,7 +14,7 @@ from paper_2310_13145_b200 import inputs, ucac  # noqa: E402
 
 NAMES = {0: "paper reading (fast path + AL when violated)", 1: "AL for every rated branch (ExaTron-faithful)",
          2: "w-bar clipped to the voltage box (SPEC)", 3: "1 + 2", 4: "ramp-aware DP (NEXT-4a)",
-         8: "no angle consensus rows (SPEC)"}
+         8: "no angle consensus rows (SPEC)", 16: "literal Eq. 5f ramp-down (A3)"}
 
 
 def main(out=None):
@@ -22,7 +22,7 @@ def main(out=None):
     rows = []
     for name in ("case30", "case118", "case300"):
         pb, pr = inputs.build_config(name)
-        for v in (0, 1, 2, 3, 4, 8):
+        for v in (0, 1, 2, 3, 4, 8, 16):
             c = ucac.Context(pb, dataclasses.replace(pr, variant=v))
             torch.cuda.synchronize()
             t0 = time.perf_counter()
