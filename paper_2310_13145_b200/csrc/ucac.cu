@@ -561,7 +561,18 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         Arena sizing;
         layout(sizing);
         void *base = nullptr;
-        e = cudaMalloc(&base, sizing.off);
+        // stream-ordered from the device's default pool, whose release threshold is raised once:
+        // a context created after another was destroyed reuses its pages instead of mapping new
+        // ones (create/destroy cycles of the public API, the e2e path)
+        static const bool pool_ready = [] {
+            int dv = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dv) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dv) != cudaSuccess) return false;
+            unsigned long long keep = ~0ull;
+            return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) == cudaSuccess;
+        }();
+        (void)pool_ready;
+        e = cudaMallocAsync(&base, sizing.off, ctx->s);
         if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc arena of %zu B", sizing.off));
         ctx->dalloc.push_back(base);
         std::vector<char> stage(sizing.up_end, 0);
@@ -1217,7 +1228,8 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     for (auto &g : ctx->gexec)
         if (g) cudaGraphExecDestroy(g);
     for (auto ev : ctx->tev) cudaEventDestroy(ev);
-    for (void *p : ctx->dalloc) cudaFree(p);
+    for (void *p : ctx->dalloc) cudaFreeAsync(p, ctx->s);
+    if (ctx->s && !ctx->dalloc.empty()) cudaStreamSynchronize(ctx->s);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->st_host) pinned_status_put(ctx->st_host);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
