@@ -525,7 +525,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "time_to_residual": ttr,
-            "gpu_launches": (10 if world == 1 else 15) * args.steps,
+            "gpu_launches": (11 if world == 1 else 15) * args.steps,   # 1 GPU: 10 kernels + the tail DP
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

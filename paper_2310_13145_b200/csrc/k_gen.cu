@@ -233,9 +233,15 @@ __device__ void gen_solve(const GenIn &g, double &po, double &qo, double &pho) {
 #define ZG(k, i) d.zg[(size_t)(k) * GT + (i)]
 #define YG(k, i) d.yg[(size_t)(k) * GT + (i)]
 
-__global__ void __launch_bounds__(128) k_gen(Dev d) {
+// tail = 0: the iteration's own (7a), skipped when the previous iteration's tail launch already
+// computed it (u_next valid).  tail = 1: launched right after k_ubar, it computes the NEXT
+// iteration's (7a) -- its inputs (ubar, y, z of the duplicate rows, p) are final once k_ubar has
+// run -- so the DP overlaps the rest of this iteration.  The schedule becomes state
+// only when k_genx adopts u_next, after the done check, so a stopped run is unchanged.
+__global__ void __launch_bounds__(128) k_gen(Dev d, int tail) {
     TL_KERNEL(K_GEN);
     if (d.st->done || d.uc_fixed) return;   // uc_fixed: the schedule is held (NEXT-2)
+    if (!tail && *((volatile unsigned *)d.unext_ok)) return;
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -264,7 +270,8 @@ __global__ void __launch_bounds__(128) k_gen(Dev d) {
     }
     __syncwarp();
     dp_warp(s, T, d.tu[g], d.td[g], d.u0[g], d.hold[g]);
-    for (int t = lane; t < T; t += 32) d.u[(size_t)g * T + t] = s.u[t];
+    for (int t = lane; t < T; t += 32) d.u_next[(size_t)g * T + t] = s.u[t];
+    if (tail && g == 0 && lane == 0) *d.unext_ok = 1u;   // read only by later launches (stream order)
 }
 
 // (7b) generator part on iterate l: one thread per (g,t) (S2)
@@ -275,6 +282,8 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
     const size_t GT = (size_t)d.G * T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= d.G * T) return;
+    if (!d.uc_fixed) d.u[k] = d.u_next[k];   // adopt this iteration's (7a) schedule
+    if (k == 0) *d.unext_ok = 0u;              // u_next is consumed: stale for the next state
     const int g = k / T, t = k - g * T;
     const double ruc = d.ruc, rpq = d.rpq;
     const double S = d.S;
@@ -398,9 +407,9 @@ __global__ void k_init(Dev d, const int8_t *u_init) {
 
 static size_t gen_smem(int T, int warps) { return dp_smem_bytes(T) * warps; }
 
-void launch_gen(const Dev &d, cudaStream_t s) {
+void launch_gen(const Dev &d, cudaStream_t s, int tail) {
     const int warps = 4;
-    launch_hi_prio(k_gen, dim3((d.G + warps - 1) / warps), dim3(warps * 32), gen_smem(d.T, warps), s, d);
+    launch_hi_prio(k_gen, dim3((d.G + warps - 1) / warps), dim3(warps * 32), gen_smem(d.T, warps), s, d, tail);
 }
 void launch_genx(const Dev &d, cudaStream_t s) { launch_hi_prio(k_genx, dim3((d.G * d.T + 127) / 128), dim3(128), 0, s, d); }
 

@@ -26,6 +26,9 @@
 #ifndef UCAC_EARLY_FORK
 #define UCAC_EARLY_FORK 1
 #endif
+#ifndef UCAC_PIPE_DP
+#define UCAC_PIPE_DP 1
+#endif
 #ifndef UCAC_S2_PRIO
 #define UCAC_S2_PRIO 1
 #endif
@@ -181,7 +184,8 @@ struct ucac_ctx {
     ncclComm_t comm = nullptr;
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     bool own_stream = false;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr, ev_branch = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr, ev_branch = nullptr,
+                ev_tail = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int gunroll[2] = {1, 16};
     std::vector<void *> dalloc;
@@ -420,7 +424,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_genx, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_early, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_branch, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ctx->ev_branch, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_tail, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
     mark("streams");
     if ((ctx->st_host = pinned_status_get()) == nullptr) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
@@ -545,6 +550,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.alq = A.take<int>(LT);
         d.alq_cnt = A.take<unsigned>(2);
         d.alq_x = A.take<double>(4 * LT);
+        d.u_next = A.take<int8_t>(GT);
+        d.unext_ok = A.take<unsigned>(1);
         d.rec = A.take<double>(NREC);
         d.tl = A.take<unsigned long long>(2 * NKERN);
         d.xsend1 = A.take<double>((size_t)P.max_cut * 4 * T);
@@ -680,6 +687,11 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     }
     launch_kernel(ctx, K_UBAR, ctx->s2);
     cudaEventRecord(ctx->ev_join, ctx->s2);
+    if (early_fork && UCAC_PIPE_DP) {
+        // the next iteration's (7a) DP, overlapping the rest of this one (k_gen tail launch)
+        launch_gen(d, ctx->s2, 1);
+        cudaEventRecord(ctx->ev_tail, ctx->s2);
+    }
     if (!multi) {   // fold the early partials in the shadow of the AL tail
         cudaStreamWaitEvent(ctx->s3, ctx->ev_join, 0);
         launch_kernel(ctx, K_FOLD, ctx->s3);
@@ -698,6 +710,7 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         launch_kernel(ctx, K_BUS_LATE, ctx->s);
         cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_ROWS_LATE, ctx->s);
+        if (early_fork && UCAC_PIPE_DP) cudaStreamWaitEvent(ctx->s, ctx->ev_tail, 0);
         return;
     }
     cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0);
@@ -872,6 +885,8 @@ extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kern
     if (ctx->nranks > 1) return fail(ctx, UCAC_EUNSUPPORTED, "timed iterations are single-GPU");
     ucac_status s = set_control(ctx, 0, 0.0);
     if (s != UCAC_OK) return s;
+    // eager iterations have no tail DP launch: every k_gen computes its own (7a)
+    CK(cudaMemsetAsync(ctx->d.unext_ok, 0, sizeof(unsigned), ctx->s));
     const size_t need = (size_t)n * NKERN * 2;
     while (ctx->tev.size() < need) {
         cudaEvent_t ev;
@@ -1042,6 +1057,7 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     h->err_kernel = 0;
     CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
     CK(cudaMemsetAsync(d.cnt, 0, NCNT * sizeof(unsigned long long), ctx->s));
+    CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));   // the pipelined DP result is stale
     CK(cudaMemsetAsync(d.alq_cnt, 0, 2 * sizeof(unsigned), ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     return UCAC_OK;
@@ -1237,6 +1253,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (ctx->ev_genx) cudaEventDestroy(ctx->ev_genx);
     if (ctx->ev_early) cudaEventDestroy(ctx->ev_early);
     if (ctx->ev_branch) cudaEventDestroy(ctx->ev_branch);
+    if (ctx->ev_tail) cudaEventDestroy(ctx->ev_tail);
     if (ctx->s2) cudaStreamDestroy(ctx->s2);
     if (ctx->s3) cudaStreamDestroy(ctx->s3);
     if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);

@@ -111,6 +111,8 @@ struct Dev {
     unsigned *kdone;                  // [3] last-block counters of the kernels producing them
     unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
     double *alq_x;                    // [4][L*T] by queue position: the previous x of a queued solve (R49)
+    int8_t *u_next;                   // [G*T] the DP's schedule for the next (7b): written by k_gen, adopted by k_genx
+    unsigned *unext_ok;               // 1: u_next holds the DP of the current state (set by the tail k_gen)
     DevStatus *st;
     unsigned long long *tl;           // [2*NKERN] diagnostic timeline (UCAC_PROF builds only)
 };
@@ -170,7 +172,7 @@ inline cudaError_t launch_hi_prio(void (*k)(KArgs...), dim3 grid, dim3 block, si
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
-void launch_gen(const Dev &d, cudaStream_t s);
+void launch_gen(const Dev &d, cudaStream_t s, int tail = 0);
 void launch_genx(const Dev &d, cudaStream_t s);
 void launch_bus(const Dev &d, cudaStream_t s);
 void launch_rows(const Dev &d, cudaStream_t s);
