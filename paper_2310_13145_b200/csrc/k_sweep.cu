@@ -365,13 +365,29 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
     }
 }
 
+// Single GPU (d.fuse_rows): after its bus solve, the (i,t) thread also updates the rows of every
+// branch end at bus i (they need only this bus's result; a bus is marked iff all its ends are),
+// so the end rows need no kernel of their own.  Consecutive threads are consecutive t of one bus,
+// so each end's row accesses stay coalesced.
+__device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int t, int side, Acc &acc);
+__device__ __forceinline__ void bus_end_rows(const Dev &d, const Ctl &c, int k, Acc &acc) {
+    const int i = k / d.T, t = k - i * d.T;
+    for (int a = d.be_ptr[i]; a < d.be_ptr[i + 1]; a++) {
+        const int code = d.be_idx[a];
+        end_rows(d, c, code >> 1, t, code & 1, acc);
+    }
+}
+
 __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     TL_KERNEL(K_BUS);
     if (d.st->done) return;
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc;
-    if (k < d.B_own * d.T && d.bmark[k] != c.stamp) bus_solve(d, c, k, acc);
+    if (k < d.B_own * d.T && d.bmark[k] != c.stamp) {
+        bus_solve(d, c, k, acc);
+        if (d.fuse_rows) bus_end_rows(d, c, k, acc);
+    }
     block_reduce_store(acc, d.part_bus);
 }
 
@@ -444,8 +460,12 @@ __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc;
-    if (k < d.B_own * d.T && d.bmark[k] == c.stamp) bus_solve(d, c, k, acc);
-    kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, false);
+    if (k < d.B_own * d.T && d.bmark[k] == c.stamp) {
+        bus_solve(d, c, k, acc);
+        if (d.fuse_rows) bus_end_rows(d, c, k, acc);
+    }
+    // fused rows: this is the iteration's last kernel and does the final fold
+    kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, d.fuse_rows != 0);
 }
 
 // k_fold_early: the block partials of k_bus, k_ubar and k_rows (in that order) -> rec_part[RK_EARLY]

@@ -26,6 +26,9 @@
 #ifndef UCAC_EARLY_FORK
 #define UCAC_EARLY_FORK 1
 #endif
+#ifndef UCAC_FUSE_ROWS
+#define UCAC_FUSE_ROWS 0   // measured slower: 0.203 vs 0.182 ms (per-thread end loops lengthen the late chains)
+#endif
 #ifndef UCAC_PIPE_DP
 #define UCAC_PIPE_DP 1
 #endif
@@ -461,6 +464,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.al_eta_star = prm->al_eta_star; d.al_sigma0_rel = prm->al_sigma0_rel;
     d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
     d.uc_fixed = prm->uc_fixed;
+    d.fuse_rows = (nranks == 1 && UCAC_FUSE_ROWS) ? 1 : 0;
     d.variant = prm->variant;
     d.nblk_bus = nblk_bus(P.Bo, T);
     d.nblk_ubar = nblk_ubar(G, T);
@@ -646,9 +650,9 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
         case K_GEN: launch_gen(ctx->d, s); break;
         case K_GENX: launch_genx(ctx->d, s); break;
         case K_BUS: launch_bus(ctx->d, s); break;
-        case K_ROWS: launch_rows(ctx->d, s); break;
+        case K_ROWS: if (!ctx->d.fuse_rows) launch_rows(ctx->d, s); break;   // fused: inside k_bus
         case K_BUS_LATE: launch_bus_late(ctx->d, s); break;
-        case K_ROWS_LATE: launch_rows_late(ctx->d, s, 1); break;
+        case K_ROWS_LATE: if (!ctx->d.fuse_rows) launch_rows_late(ctx->d, s, 1); break;
         case K_FOLD: launch_fold_early(ctx->d, s); break;
         case K_UBAR: launch_ubar(ctx->d, s); break;
         default: break;
@@ -707,6 +711,8 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         // the late bus solve needs the AL results and the generator x-update only (not k_ubar);
         // the late rows' final fold needs every early partial (k_fold_early, after k_ubar)
         cudaStreamWaitEvent(ctx->s, ctx->ev_genx, 0);
+        // fused rows: k_bus_late does the final fold, so it needs the folded early partials
+        if (d.fuse_rows) cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_BUS_LATE, ctx->s);
         cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_ROWS_LATE, ctx->s);

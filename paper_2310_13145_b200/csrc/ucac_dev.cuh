@@ -111,6 +111,7 @@ struct Dev {
     unsigned *kdone;                  // [3] last-block counters of the kernels producing them
     unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
     double *alq_x;                    // [4][L*T] by queue position: the previous x of a queued solve (R49)
+    int fuse_rows;                    // 1 GPU: the end rows of a bus are updated by its bus thread (no k_rows)
     int8_t *u_next;                   // [G*T] the DP's schedule for the next (7b): written by k_gen, adopted by k_genx
     unsigned *unext_ok;               // 1: u_next holds the DP of the current state (set by the tail k_gen)
     DevStatus *st;
