@@ -308,3 +308,23 @@ def test_formulation_variants_next3(variant):
         run_pair(pb, dataclasses.replace(pr, variant=variant), iters, free_run=1, sensitivity=True)
     else:
         run_pair(pb, dataclasses.replace(pr, variant=variant), iters, check_every=1 if iters <= 20 else 3)
+
+
+def test_time_to_residual_configs0_matches_oracle():
+    """The metric's time-to-residual part on BASELINE configs[0] (case9, T=4, Table I rho, cold
+    start): the GPU stops on primal <= 1e-4 at the same inner iteration as the oracle, with the
+    same outer count and the objective within 1e-6 (bench.py's time_to_residual)."""
+    pb, pr = inputs.build_config("case9")
+    c = ucac.Context(pb, pr)
+    n = c.iterate(5000, stop_on_primal=1e-4)
+    rg = c.report()
+    assert 0 < n < 5000 and rg["primal_inf"] <= 1e-4
+    o = oracle.Oracle(pb, pr)
+    k = 0
+    while o.report()["primal_inf"] > 1e-4 or k == 0:
+        o.iterate(1)
+        k += 1
+        assert k < 5000
+    ro = o.report()
+    assert k == n and ro["outer_total"] == rg["outer_total"], (k, n)
+    assert rg["objective"] == pytest.approx(ro["objective"], rel=1e-6)
