@@ -159,6 +159,13 @@ ucac_status ucac_create(const ucac_network *net, const ucac_horizon *hz, const u
 ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_primal, double primal_target,
                          int32_t *n_done);
 
+/* NEXT-4(b) adaptive rho ("future work", R53): replace the three penalty classes
+ * rho_pq, rho_va, rho_uc between iterations.  Synchronises the context stream, updates
+ * every rho-derived constant (1/rho, the TRON tolerance gtol_rel * max(rho_pq, rho_va), the AL's
+ * sigma_0) and re-instantiates the iteration graphs (~2 ms).  The iterate (x, xbar, z, y,
+ * lambda, beta) is kept as is.  EINVAL for a non-positive or non-finite rho. */
+ucac_status ucac_set_rho(ucac_ctx *ctx, double rho_pq, double rho_va, double rho_uc);
+
 /* n inner iterations of a comm_mode-1 loopback group: ctxs[r] is rank r of nranks = n contexts
  * of one problem on the current device.  Synchronous. */
 ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t iters);

@@ -99,6 +99,8 @@ def _declare(L):
     L.orc_create.restype = C.c_int
     L.orc_destroy.argtypes = [C.c_void_p]
     L.orc_iterate.argtypes = [C.c_void_p, C.c_int32]
+    L.orc_set_rho.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
+    L.orc_set_rho.restype = None
     L.orc_report_get.argtypes = [C.c_void_p, C.POINTER(Report_c)]
     L.orc_get_state.argtypes = [C.c_void_p, C.POINTER(State_c)]
     L.orc_set_state.argtypes = [C.c_void_p, C.POINTER(State_c)]
@@ -177,6 +179,10 @@ class Oracle:
 
     def iterate(self, n: int = 1):
         self.L.orc_iterate(self.h, n)
+
+    def set_rho(self, rho_pq: float, rho_va: float, rho_uc: float):
+        """NEXT-4(b), R53: new penalty classes between iterations (the iterate is kept)."""
+        self.L.orc_set_rho(self.h, rho_pq, rho_va, rho_uc)
 
     def report(self) -> dict:
         r = Report_c()

@@ -1423,6 +1423,14 @@ int orc_iterate(orc_ctx *c, int32_t n) {
 
 void orc_report_get(const orc_ctx *c, orc_report *r) { *r = c->rep; }
 
+/* NEXT-4(b), R53: new penalty classes between iterations; every rho-derived quantity of the
+ * steps is formed from c->pr at its use, and the iterate is kept. */
+void orc_set_rho(orc_ctx *c, double rho_pq, double rho_va, double rho_uc) {
+    c->pr.rho_pq = rho_pq;
+    c->pr.rho_va = rho_va;
+    c->pr.rho_uc = rho_uc;
+}
+
 void orc_get_state(const orc_ctx *c, orc_state *s) {
     size_t GT = (size_t)c->pb.ngen * c->pb.T, LT = (size_t)c->pb.nbranch * c->pb.T;
     size_t BT = (size_t)c->pb.nbus * c->pb.T, D = sizeof(double);

@@ -80,6 +80,7 @@ typedef struct orc_ctx orc_ctx;
 int  orc_create(const orc_problem *pb, const orc_params *pr, orc_ctx **out);
 void orc_destroy(orc_ctx *c);
 int  orc_iterate(orc_ctx *c, int32_t n);                 /* n inner iterations */
+void orc_set_rho(orc_ctx *c, double rho_pq, double rho_va, double rho_uc);   /* NEXT-4(b), R53 */
 void orc_report_get(const orc_ctx *c, orc_report *r);
 void orc_get_state(const orc_ctx *c, orc_state *s);
 void orc_set_state(orc_ctx *c, const orc_state *s);

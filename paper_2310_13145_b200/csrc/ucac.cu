@@ -800,6 +800,30 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
     return UCAC_OK;
 }
 
+extern "C" ucac_status ucac_set_rho(ucac_ctx *ctx, double rho_pq, double rho_va, double rho_uc) {
+    if (!ctx) return UCAC_EINVAL;
+    if (!(rho_pq > 0.0 && rho_va > 0.0 && rho_uc > 0.0) || !std::isfinite(rho_pq) || !std::isfinite(rho_va) ||
+        !std::isfinite(rho_uc))
+        return fail(ctx, UCAC_EINVAL, "rho must be positive and finite");
+    CK(cudaStreamSynchronize(ctx->s));
+    ucac_params &prm = ctx->prm;
+    prm.rho_pq = rho_pq;
+    prm.rho_va = rho_va;
+    prm.rho_uc = rho_uc;
+    Dev &d = ctx->d;
+    d.rpq = rho_pq; d.rva = rho_va; d.ruc = rho_uc;
+    d.irpq = 1.0 / rho_pq; d.irva = 1.0 / rho_va; d.iruc = 1.0 / rho_uc;
+    d.tron_gtol = prm.tron_gtol_rel * std::max(rho_pq, rho_va);
+    // the graphs captured the old Dev by value: re-instantiate them
+    for (auto &g : ctx->gexec)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    if (!(ctx->nranks > 1 && ctx->comm_mode == 1)) return build_graphs(ctx);
+    return UCAC_OK;
+}
+
 // In-process loopback group: the partition contexts of one problem (comm_mode 1, same device)
 // step through the same phases as the NCCL graph; the exchanges are device-to-device copies
 // driven from the host between phases (no kernel ever waits on another context).

@@ -130,6 +130,7 @@ def _declare(L):
                                      C.POINTER(Params), C.c_int32, C.c_double, i8p]
     L.ucac_uc_warm_start.restype = C.c_int
     L.ucac_iterate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_int32)]
+    L.ucac_set_rho.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
     L.ucac_iterate.restype = C.c_int
     L.ucac_iterate_timed.argtypes = [C.c_void_p, C.c_int32, dp, i64p]
     L.ucac_iterate_timed.restype = C.c_int
@@ -166,7 +167,7 @@ def _declare(L):
     L.ucac_local_map.restype = C.c_int
 
 
-EXPORTED = ["ucac_create", "ucac_iterate", "ucac_iterate_timed", "ucac_kernel_name", "ucac_residuals",
+EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed", "ucac_kernel_name", "ucac_residuals",
             "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
             "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start"]
@@ -281,6 +282,10 @@ class Context:
             return None
         _check(self.L.ucac_iterate(self.h, n, 1, float(stop_on_primal), C.byref(done)), self.h)
         return done.value
+
+    def set_rho(self, rho_pq: float, rho_va: float, rho_uc: float):
+        """NEXT-4(b), R53: new penalty classes between iterations (ucac_set_rho)."""
+        _check(self.L.ucac_set_rho(self.h, float(rho_pq), float(rho_va), float(rho_uc)), self.h)
 
     def iterate_timed(self, n: int):
         ms = np.zeros(NKERNELS)

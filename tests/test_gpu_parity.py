@@ -328,3 +328,33 @@ def test_time_to_residual_configs0_matches_oracle():
     ro = o.report()
     assert k == n and ro["outer_total"] == rg["outer_total"], (k, n)
     assert rg["objective"] == pytest.approx(ro["objective"], rel=1e-6)
+
+
+def test_set_rho_mid_run_next4():
+    """NEXT-4(b), R53: ucac_set_rho between iterations keeps GPU/oracle parity (one-step checks
+    on every iteration after the change; schedules and scalars exact)."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    gpu = ucac.Context(pb, pr)
+    orc = oracle.Oracle(pb, pr)
+    gpu.iterate(8)
+    orc.iterate(8)
+    new = dict(rho_pq=2 * pr.rho_pq, rho_va=0.5 * pr.rho_va, rho_uc=3 * pr.rho_uc)
+    gpu.set_rho(new["rho_pq"], new["rho_va"], new["rho_uc"])
+    orc.set_rho(new["rho_pq"], new["rho_va"], new["rho_uc"])
+    pr2 = dataclasses.replace(pr, **new)
+    rho_max = max(new.values())
+    for it in range(10):
+        one = oracle.Oracle(pb, pr2)
+        one.set_state(gpu.get_state())
+        gpu.iterate(1)
+        orc.iterate(1)
+        one.iterate(1)
+        gs = gpu.get_state()
+        compare(gs, one.get_state(), rho_max, f"one-step after set_rho, iteration {it + 1}")
+        one.close()
+        os_ = orc.get_state()
+        assert np.array_equal(gs["u"], os_["u"])
+        assert np.array_equal(gs["scal"][[0, 2, 3, 4]], os_["scal"][[0, 2, 3, 4]])
+    with pytest.raises(ucac.UcacError):
+        gpu.set_rho(-1.0, 1.0, 1.0)

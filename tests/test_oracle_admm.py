@@ -388,3 +388,23 @@ def test_literal_eq5f_ramp_down_next3():
             sd = float(up > u1[g, t])
             assert abs(sd1[g, t] - np.clip(sd + z0[DSD, g, t] + y0[DSD, g, t] / ruc, 0.0, 1.0)) <= 1e-12
     assert worst <= 1e-9, worst
+
+
+def test_set_rho_equals_fresh_context_next4():
+    """NEXT-4(b), R53: orc_set_rho between iterations is the same as a context created with the
+    new rho and handed the current state (every rho-derived quantity is formed at its use)."""
+    import dataclasses
+    pb, pr = inputs.build_config("case30")
+    a = oracle.Oracle(pb, pr)
+    a.iterate(7)
+    st = a.get_state()
+    a.set_rho(2 * pr.rho_pq, 0.5 * pr.rho_va, 3 * pr.rho_uc)
+    a.iterate(3)
+    b = oracle.Oracle(pb, dataclasses.replace(pr, rho_pq=2 * pr.rho_pq, rho_va=0.5 * pr.rho_va, rho_uc=3 * pr.rho_uc))
+    b.set_state(st)
+    b.iterate(3)
+    sa, sb = a.get_state(), b.get_state()
+    for k in sa:
+        assert np.array_equal(sa[k], sb[k]), k
+    a.close()
+    b.close()
