@@ -26,6 +26,9 @@
 #ifndef UCAC_EARLY_FORK
 #define UCAC_EARLY_FORK 1
 #endif
+#ifndef UCAC_UBAR_AFTER_BUS
+#define UCAC_UBAR_AFTER_BUS 0   // 1 measured slower (0.186 vs 0.181 ms): k_ubar then delays the early fold
+#endif
 #ifndef UCAC_FUSE_ROWS
 #define UCAC_FUSE_ROWS 0   // measured slower: 0.203 vs 0.182 ms (per-thread end loops lengthen the late chains)
 #endif
@@ -188,7 +191,7 @@ struct ucac_ctx {
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr, ev_branch = nullptr,
-                ev_tail = nullptr;
+                ev_tail = nullptr, ev_bus = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int gunroll[2] = {1, 16};
     std::vector<void *> dalloc;
@@ -428,7 +431,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         cudaEventCreateWithFlags(&ctx->ev_genx, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_early, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_branch, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_tail, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ctx->ev_tail, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_bus, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "stream/event creation failed"));
     mark("streams");
     if ((ctx->st_host = pinned_status_get()) == nullptr) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
@@ -687,8 +691,12 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         cudaStreamWaitEvent(ctx->s3, ctx->ev_genx, 0);
         if (early_fork) cudaStreamWaitEvent(ctx->s3, ctx->ev_branch, 0);
         launch_kernel(ctx, K_BUS, ctx->s3);
+        if (UCAC_UBAR_AFTER_BUS) cudaEventRecord(ctx->ev_bus, ctx->s3);
         launch_kernel(ctx, K_ROWS, ctx->s3);
     }
+    // k_ubar is off the critical path (it only has to finish before the early fold): after
+    // k_bus it no longer competes with it for SMs (UCAC_UBAR_AFTER_BUS)
+    if (!multi && UCAC_UBAR_AFTER_BUS) cudaStreamWaitEvent(ctx->s2, ctx->ev_bus, 0);
     launch_kernel(ctx, K_UBAR, ctx->s2);
     cudaEventRecord(ctx->ev_join, ctx->s2);
     if (early_fork && UCAC_PIPE_DP) {
@@ -1284,6 +1292,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (ctx->ev_early) cudaEventDestroy(ctx->ev_early);
     if (ctx->ev_branch) cudaEventDestroy(ctx->ev_branch);
     if (ctx->ev_tail) cudaEventDestroy(ctx->ev_tail);
+    if (ctx->ev_bus) cudaEventDestroy(ctx->ev_bus);
     if (ctx->s2) cudaStreamDestroy(ctx->s2);
     if (ctx->s3) cudaStreamDestroy(ctx->s3);
     if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);
