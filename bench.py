@@ -338,6 +338,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ucac", choices=["ucac", "reference"])
     ap.add_argument("--config", default="pegase2869")
+    ap.add_argument("--T", type=int, default=None, help="override the config's horizon (SURVEY 8(a) stress: pegase T=168)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--workload", default="admm", choices=["admm", "dp", "warmstart"],
@@ -351,7 +352,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     from paper_2310_13145_b200 import inputs
-    pb, pr = inputs.build_config(args.config)
+    pb, pr = inputs.build_config(args.config, args.T)
 
     if args.impl == "reference":
         run_reference(args, pb, pr, rank, world)

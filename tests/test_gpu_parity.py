@@ -358,3 +358,17 @@ def test_set_rho_mid_run_next4():
         assert np.array_equal(gs["scal"][[0, 2, 3, 4]], os_["scal"][[0, 2, 3, 4]])
     with pytest.raises(ucac.UcacError):
         gpu.set_rho(-1.0, 1.0, 1.0)
+
+
+def test_pegase_t168_stress_one_iteration():
+    """SURVEY 8(a) stress row: pegase-shaped T=168 (770 k branch solves, 7.2 M rows per
+    iteration) -- a GPU state after 3 iterations, one more iteration on both sides."""
+    pb, pr = inputs.build_config("pegase2869", 168)
+    gpu = ucac.Context(pb, pr)
+    gpu.iterate(3)
+    st = gpu.get_state()
+    orc = oracle.Oracle(pb, pr)
+    orc.set_state(st)
+    gpu.iterate(1)
+    orc.iterate(1)
+    compare(gpu.get_state(), orc.get_state(), max(pr.rho_pq, pr.rho_va, pr.rho_uc), "pegase T=168")
