@@ -459,12 +459,11 @@ __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
     if (d.st->done) return;
     const Ctl c(d);
     Acc acc;
-    // grid-stride (UCAC_LBUS_GRID > 0 caps the grid: fewer block partials to fold, smaller blocks)
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d.B_own * d.T; k += gridDim.x * blockDim.x)
-        if (d.bmark[k] == c.stamp) {
-            bus_solve(d, c, k, acc);
-            if (d.fuse_rows) bus_end_rows(d, c, k, acc);
-        }
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < d.B_own * d.T && d.bmark[k] == c.stamp) {
+        bus_solve(d, c, k, acc);
+        if (d.fuse_rows) bus_end_rows(d, c, k, acc);
+    }
     // fused rows: this is the iteration's last kernel and does the final fold
     kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, d.fuse_rows != 0);
 }
@@ -909,13 +908,7 @@ void launch_bus_late(const Dev &d, cudaStream_t s) {
 void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
     launch_sweep(UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, k_rows_late, dim3(d.nblk_lrows), dim3(LROWS_THREADS), s, d, final);
 }
-#ifndef UCAC_LBUS_GRID
-#define UCAC_LBUS_GRID 0
-#endif
-int nblk_lbus(int n) {
-    const int b = (n + LBUS_THREADS - 1) / LBUS_THREADS;
-    return UCAC_LBUS_GRID > 0 ? std::min(b, UCAC_LBUS_GRID) : b;
-}
+int nblk_lbus(int n) { return (n + LBUS_THREADS - 1) / LBUS_THREADS; }
 int nblk_lrows(int n) { return (n + LROWS_THREADS - 1) / LROWS_THREADS; }
 int fold_blocks() { return FOLD_BLOCKS; }
 void launch_fold_early(const Dev &d, cudaStream_t s) { k_fold_early<<<FOLD_BLOCKS, FOLD_THREADS, 0, s>>>(d); }
