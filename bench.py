@@ -33,8 +33,8 @@ UNIT = "ADMM inner iterations/s"
 # same launches (2 DFMA + DADD + DMUL) / the Newton iterations the solver counted in them
 # (tools/calibrate_flops.py; profiles/r01/flops_calibration.json).  The AL figure includes the
 # per-round work (Hessian at the round start, multiplier update) amortised over its iterations.
-FLOPS_PER_NEWTON_FAST = 1350.0
-FLOPS_PER_NEWTON_AL = 3034.0
+FLOPS_PER_NEWTON_FAST = 717.0    # profiles/r01/flops_calibration.json (ncu SASS count, current code)
+FLOPS_PER_NEWTON_AL = 2147.0
 
 
 def measured_peaks():

@@ -418,6 +418,9 @@ __device__ __forceinline__ bool newton_free(const double (*H)[N], const bool *fr
     return true;
 }
 
+#ifndef UCAC_NEWTON_FIRST
+#define UCAC_NEWTON_FIRST 1
+#endif
 // Projected trust-region Newton.  Returns true when ||P(x-g)-x||_inf <= gtol.
 template <int N, class Fun>
 __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *hi, double gtol,
@@ -444,136 +447,168 @@ __device__ bool tron(const Fun &fn, double *x, const double *lo, const double *h
             if (Hout) copy_h<N>(H, Hout);
             return true;
         }
-        // --- Cauchy point: backtrack (x0.1) or extrapolate (x10) along P(x - a g)
-        double sc[N];
-        {
-            double a = alpha;
-            pstep<N>(x, lo, hi, g, a, sc);
-            if (!cauchy_ok<N>(g, H, sc, delta)) {
-                for (int k = 0; k < 60; k++) {
-                    a *= 0.1;
-                    pstep<N>(x, lo, hi, g, a, sc);
-                    if (cauchy_ok<N>(g, H, sc, delta)) break;
-                }
-            } else {
-                for (int k = 0; k < 20; k++) {
-                    double sp[N];
-#pragma unroll
-                    for (int i = 0; i < N; i++) sp[i] = sc[i];
-                    double ap = a;
-                    a *= 10.0;
-                    pstep<N>(x, lo, hi, g, a, sc);
-                    bool same = true;
-#pragma unroll
-                    for (int i = 0; i < N; i++) same = same && (sc[i] == sp[i]);
-                    if (!cauchy_ok<N>(g, H, sc, delta) || same) {
-                        a = ap;
-#pragma unroll
-                        for (int i = 0; i < N; i++) sc[i] = sp[i];
-                        break;
-                    }
-                }
-            }
-            alpha = a;
-        }
-        // --- Steihaug-Toint CG on the free variables at x + sc, region ||sc + w|| <= delta
-        bool fr[N];
-        double gq[N], w[N];
-        {
-            double Hs[N];
-            matvec<N>(H, sc, Hs);
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                double xc = x[i] + sc[i];
-                fr[i] = (xc > lo[i]) && (xc < hi[i]);
-                gq[i] = g[i] + Hs[i];
-                w[i] = 0.0;
-            }
-            double r[N], p[N];
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                r[i] = fr[i] ? -gq[i] : 0.0;
-                p[i] = r[i];
-            }
-            double rr = dotn<N>(r, r);
-            bool direct = false;
-            if (rr != 0.0 && N <= UCAC_TRON_DIRECT_MAXN) {
-                // the point CG converges to, when it is interior: the Newton step on the free set
-                if (newton_free<N>(H, fr, r, w)) {
-                    double t[N];
-#pragma unroll
-                    for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
-                    direct = dotn<N>(t, t) < delta * delta;
-                }
-                if (!direct) {
-#pragma unroll
-                    for (int i = 0; i < N; i++) w[i] = 0.0;
-                }
-            }
-            if (rr != 0.0 && !direct) {
-                double tol2 = TR_CGTOL * TR_CGTOL * rr;
-                for (int k = 0; k < N; k++) {
-                    double Hp[N], t[N];
-                    matvec<N>(H, p, Hp);
-#pragma unroll
-                    for (int i = 0; i < N; i++) if (!fr[i]) Hp[i] = 0.0;
-                    double kap = dotn<N>(p, Hp);
-#pragma unroll
-                    for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
-                    if (kap <= 0.0) {
-                        double tau = bnd_tau<N>(t, p, delta);
-#pragma unroll
-                        for (int i = 0; i < N; i++) w[i] += tau * p[i];
-                        break;
-                    }
-                    double a = rr * rcp(kap);
-                    double tt[N];
-#pragma unroll
-                    for (int i = 0; i < N; i++) tt[i] = t[i] + a * p[i];
-                    if (dotn<N>(tt, tt) >= delta * delta) {
-                        double tau = bnd_tau<N>(t, p, delta);
-#pragma unroll
-                        for (int i = 0; i < N; i++) w[i] += tau * p[i];
-                        break;
-                    }
-#pragma unroll
-                    for (int i = 0; i < N; i++) {
-                        w[i] += a * p[i];
-                        r[i] -= a * Hp[i];
-                    }
-                    double rn = dotn<N>(r, r);
-                    if (rn <= tol2) break;
-                    double b = rn * rcp(rr);
-#pragma unroll
-                    for (int i = 0; i < N; i++) p[i] = r[i] + b * p[i];
-                    rr = rn;
-                }
-            }
-        }
-        // --- projected search along w from the Cauchy point
         double s[N], qs;   // step and its model value (reused by the ratio test)
-        {
-            const double qc = qmodel<N>(g, H, sc);
-            double b = 1.0;
-            bool found = false;
-            for (int k = 0; k < 20; k++) {
-                double ds[N];
+        bool have_step = false;
+        if (UCAC_NEWTON_FIRST && N == 4) {   // fast path only: in the 6-variable AL it cost spills
+            // Newton first: with x strictly inside the box and H positive definite, TRON's step
+            // from the Cauchy point sc is sc + w = -H^{-1} g whenever every coordinate stays free
+            // (w solves H w = -(g + H sc)).  So when -H^{-1} g is interior and inside the trust
+            // region it is taken directly, without computing sc; else the full step.
+            bool inside = true;
+#pragma unroll
+            for (int i = 0; i < N; i++) inside = inside && x[i] > lo[i] && x[i] < hi[i];
+            if (inside) {
+                bool fr[N];
+                double r[N], w[N];
 #pragma unroll
                 for (int i = 0; i < N; i++) {
-                    s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
-                    ds[i] = s[i] - sc[i];
+                    fr[i] = true;
+                    r[i] = -g[i];
                 }
-                qs = qmodel<N>(g, H, s);
-                if (qs <= qc + TR_MU0 * dotn<N>(gq, ds)) {
-                    found = true;
-                    break;
-                }
-                b *= 0.5;
-            }
-            if (!found) {
+                if (newton_free<N>(H, fr, r, w) && dotn<N>(w, w) < delta * delta) {
+                    bool in2 = true;
 #pragma unroll
-                for (int i = 0; i < N; i++) s[i] = sc[i];
-                qs = qc;
+                    for (int i = 0; i < N; i++) in2 = in2 && x[i] + w[i] > lo[i] && x[i] + w[i] < hi[i];
+                    if (in2) {
+#pragma unroll
+                        for (int i = 0; i < N; i++) s[i] = w[i];
+                        qs = qmodel<N>(g, H, s);
+                        have_step = qs < 0.0;
+                    }
+                }
+            }
+        }
+        if (!have_step) {
+            // --- Cauchy point: backtrack (x0.1) or extrapolate (x10) along P(x - a g)
+            double sc[N];
+            {
+                double a = alpha;
+                pstep<N>(x, lo, hi, g, a, sc);
+                if (!cauchy_ok<N>(g, H, sc, delta)) {
+                    for (int k = 0; k < 60; k++) {
+                        a *= 0.1;
+                        pstep<N>(x, lo, hi, g, a, sc);
+                        if (cauchy_ok<N>(g, H, sc, delta)) break;
+                    }
+                } else {
+                    for (int k = 0; k < 20; k++) {
+                        double sp[N];
+    #pragma unroll
+                        for (int i = 0; i < N; i++) sp[i] = sc[i];
+                        double ap = a;
+                        a *= 10.0;
+                        pstep<N>(x, lo, hi, g, a, sc);
+                        bool same = true;
+    #pragma unroll
+                        for (int i = 0; i < N; i++) same = same && (sc[i] == sp[i]);
+                        if (!cauchy_ok<N>(g, H, sc, delta) || same) {
+                            a = ap;
+    #pragma unroll
+                            for (int i = 0; i < N; i++) sc[i] = sp[i];
+                            break;
+                        }
+                    }
+                }
+                alpha = a;
+            }
+            // --- Steihaug-Toint CG on the free variables at x + sc, region ||sc + w|| <= delta
+            bool fr[N];
+            double gq[N], w[N];
+            {
+                double Hs[N];
+                matvec<N>(H, sc, Hs);
+    #pragma unroll
+                for (int i = 0; i < N; i++) {
+                    double xc = x[i] + sc[i];
+                    fr[i] = (xc > lo[i]) && (xc < hi[i]);
+                    gq[i] = g[i] + Hs[i];
+                    w[i] = 0.0;
+                }
+                double r[N], p[N];
+    #pragma unroll
+                for (int i = 0; i < N; i++) {
+                    r[i] = fr[i] ? -gq[i] : 0.0;
+                    p[i] = r[i];
+                }
+                double rr = dotn<N>(r, r);
+                bool direct = false;
+                if (rr != 0.0 && N <= UCAC_TRON_DIRECT_MAXN) {
+                    // the point CG converges to, when it is interior: the Newton step on the free set
+                    if (newton_free<N>(H, fr, r, w)) {
+                        double t[N];
+    #pragma unroll
+                        for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
+                        direct = dotn<N>(t, t) < delta * delta;
+                    }
+                    if (!direct) {
+    #pragma unroll
+                        for (int i = 0; i < N; i++) w[i] = 0.0;
+                    }
+                }
+                if (rr != 0.0 && !direct) {
+                    double tol2 = TR_CGTOL * TR_CGTOL * rr;
+                    for (int k = 0; k < N; k++) {
+                        double Hp[N], t[N];
+                        matvec<N>(H, p, Hp);
+    #pragma unroll
+                        for (int i = 0; i < N; i++) if (!fr[i]) Hp[i] = 0.0;
+                        double kap = dotn<N>(p, Hp);
+    #pragma unroll
+                        for (int i = 0; i < N; i++) t[i] = sc[i] + w[i];
+                        if (kap <= 0.0) {
+                            double tau = bnd_tau<N>(t, p, delta);
+    #pragma unroll
+                            for (int i = 0; i < N; i++) w[i] += tau * p[i];
+                            break;
+                        }
+                        double a = rr * rcp(kap);
+                        double tt[N];
+    #pragma unroll
+                        for (int i = 0; i < N; i++) tt[i] = t[i] + a * p[i];
+                        if (dotn<N>(tt, tt) >= delta * delta) {
+                            double tau = bnd_tau<N>(t, p, delta);
+    #pragma unroll
+                            for (int i = 0; i < N; i++) w[i] += tau * p[i];
+                            break;
+                        }
+    #pragma unroll
+                        for (int i = 0; i < N; i++) {
+                            w[i] += a * p[i];
+                            r[i] -= a * Hp[i];
+                        }
+                        double rn = dotn<N>(r, r);
+                        if (rn <= tol2) break;
+                        double b = rn * rcp(rr);
+    #pragma unroll
+                        for (int i = 0; i < N; i++) p[i] = r[i] + b * p[i];
+                        rr = rn;
+                    }
+                }
+            }
+            // --- projected search along w from the Cauchy point
+            {
+                const double qc = qmodel<N>(g, H, sc);
+                double b = 1.0;
+                bool found = false;
+                for (int k = 0; k < 20; k++) {
+                    double ds[N];
+    #pragma unroll
+                    for (int i = 0; i < N; i++) {
+                        s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
+                        ds[i] = s[i] - sc[i];
+                    }
+                    qs = qmodel<N>(g, H, s);
+                    if (qs <= qc + TR_MU0 * dotn<N>(gq, ds)) {
+                        found = true;
+                        break;
+                    }
+                    b *= 0.5;
+                }
+                if (!found) {
+    #pragma unroll
+                    for (int i = 0; i < N; i++) s[i] = sc[i];
+                    qs = qc;
+                }
             }
         }
         const double ss = dotn<N>(s, s);

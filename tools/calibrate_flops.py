@@ -43,7 +43,8 @@ def reduce(csv_path, json_path):
     per = {}
     for r in rows[i + 1:]:
         d = dict(zip(h, r))
-        key = (int(d["ID"]), d["Kernel Name"].split("(")[0].split("::")[-1])
+        # "void (anonymous namespace)::k_branch<0>(Dev)" -> "k_branch" (template instantiations)
+        key = (int(d["ID"]), d["Kernel Name"].split("(")[0].split("::")[-1].split("<")[0])
         per.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     launches = {"k_branch": [], "k_branch_al": []}
     for (lid, name), m in sorted(per.items()):
