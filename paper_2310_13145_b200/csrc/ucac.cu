@@ -26,6 +26,9 @@
 #ifndef UCAC_EARLY_FORK
 #define UCAC_EARLY_FORK 1
 #endif
+#ifndef UCAC_NODE_PRIO
+#define UCAC_NODE_PRIO 0   // honouring node priorities measured neutral (0.1700-0.1712 ms)
+#endif
 #ifndef UCAC_UBAR_AFTER_BUS
 #define UCAC_UBAR_AFTER_BUS 0   // 1 measured slower (0.186 vs 0.181 ms): k_ubar then delays the early fold
 #endif
@@ -751,7 +754,8 @@ static ucac_status build_graphs(ucac_ctx *ctx) {
         CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < ctx->gunroll[gi]; k++) enqueue_iteration(ctx);
         CK(cudaStreamEndCapture(ctx->s, &g));
-        cudaError_t e = cudaGraphInstantiate(&ctx->gexec[gi], g, 0);
+        // per-node launch priorities (launch_hi_prio) are honoured only with this flag
+        cudaError_t e = cudaGraphInstantiate(&ctx->gexec[gi], g, UCAC_NODE_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
         cudaGraphDestroy(g);
         CK(e);
     }
