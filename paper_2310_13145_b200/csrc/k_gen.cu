@@ -304,17 +304,17 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
     const double on = d.ub_on[i], su = d.ub_su[i], sd = d.ub_sd[i];
     const double onp = t == 0 ? u0 : d.ub_on[i - 1];
     in.first = t == 0;
-    in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) * d.irpq;
-    in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) * d.irpq;
-    in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) * d.irpq;
-    in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) * d.iruc;
-    in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) * d.iruc;
-    in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) * d.iruc;
-    in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) * d.iruc;
+    in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) / d.rpq;
+    in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) / d.rpq;
+    in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / d.rpq;
+    in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) / d.ruc;
+    in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) / d.ruc;
+    in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) / d.ruc;
+    in.bqu = qmax * on - ZG(G_QU, i) - YG(G_QU, i) / d.ruc;
     // RD row: Eq. 4d, or the literal Eq. 5f with variant bit 16 (R52)
-    in.brl = (d.variant & 16) ? -rdn * onp - sdn * su - ZG(G_RD, i) - YG(G_RD, i) * d.iruc
-                              : -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) * d.iruc;
-    in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) * d.iruc;
+    in.brl = (d.variant & 16) ? -rdn * onp - sdn * su - ZG(G_RD, i) - YG(G_RD, i) / d.ruc
+                              : -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) / d.ruc;
+    in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) / d.ruc;
     double po, qo, pho;
     gen_solve(in, po, qo, pho);
     d.p[i] = po;

@@ -32,7 +32,8 @@ struct Acc {
 // ib = 1/(beta + rho), formed once per thread: the quotient becomes a product (within one ulp of
 // the oracle's), with no division slow path to spill around.
 __device__ __forceinline__ void zy_row(double r, double rho, double ib, double *zp, double *yp, double *lp,
-                                       int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+                                       int pending, double beta_lam, double lmax, double dxb, Acc &a,
+                                       double bpr = 0.0) {
     double lam = *lp;
     double zo = *zp;
     if (pending) {
@@ -41,7 +42,7 @@ __device__ __forceinline__ void zy_row(double r, double rho, double ib, double *
         *lp = lam;
     }
     double y = *yp;
-    double zz = -((lam + y) + rho * r) * ib;
+    double zz = (bpr > 0.0 ? -((lam + y) + rho * r) / bpr : -((lam + y) + rho * r) * ib);
     *zp = zz;
     *yp = y + rho * (r + zz);
     double rz = r + zz;
@@ -56,12 +57,13 @@ __device__ __forceinline__ void zy_row(double r, double rho, double ib, double *
 
 // the same update on values (loads hoisted by the caller): returns z, y and lambda in place
 __device__ __forceinline__ void zy_vals(double r, double rho, double ib, double &z, double &y, double &lam,
-                                        int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+                                        int pending, double beta_lam, double lmax, double dxb, Acc &a,
+                                        double bpr = 0.0) {
     if (pending) {
         const double v = lam + beta_lam * z;
         lam = v < -lmax ? -lmax : (v > lmax ? lmax : v);
     }
-    const double zz = -((lam + y) + rho * r) * ib;
+    const double zz = (bpr > 0.0 ? -((lam + y) + rho * r) / bpr : -((lam + y) + rho * r) * ib);
     y = y + rho * (r + zz);
     z = zz;
     const double rz = r + zz;
@@ -72,6 +74,17 @@ __device__ __forceinline__ void zy_vals(double r, double rho, double ib, double 
     a.v[P_Z2] = a.v[P_Z2] + zz * zz;
     a.v[P_DINF] = fmax(a.v[P_DINF], rho * fabs(dxb));
     if (!isfinite(r) || !isfinite(zz)) a.v[P_BAD] = 1.0;
+}
+
+// k_ubar's twins of zy_row / zy_vals with the oracle's exact quotient (bpr = beta + rho): the
+// (7c) box-QP can be ill-conditioned, and k_ubar/k_genx keep the oracle's bits
+__device__ __forceinline__ void zy_row_div(double r, double rho, double bpr, double *zp, double *yp, double *lp,
+                                           int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+    zy_row(r, rho, 0.0, zp, yp, lp, pending, beta_lam, lmax, dxb, a, bpr);
+}
+__device__ __forceinline__ void zy_vals_div(double r, double rho, double bpr, double &z, double &y, double &lam,
+                                            int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+    zy_vals(r, rho, 0.0, z, y, lam, pending, beta_lam, lmax, dxb, a, bpr);
 }
 
 // deterministic block reduction -> part[blockIdx.x][NPART]
@@ -605,8 +618,8 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const double ruc = d.ruc, iruc = d.iruc;
-    const double beta_lam = d.st->beta_lam, lmax = d.lambda_max, ibuc = 1.0 / (d.st->beta + ruc);
+    const double ruc = d.ruc;
+    const double beta_lam = d.st->beta_lam, lmax = d.lambda_max, bpr = d.st->beta + ruc;
     const int pending = d.st->pending_outer;
     Acc acc;
     if (k < d.G * T) {
@@ -622,14 +635,14 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         const int sdt = up > ut, sut = ut > up;
         const double p = d.p[i], q = d.q[i], ph = d.ph[i];
         // slacks (x-variables of 7b) recomputed exactly as the x-step defines them
-        const double bpl = Pm * on_o - ZG(G_PL, i) - YG(G_PL, i) * iruc;
-        const double bpu = PM * on_o - ZG(G_PU, i) - YG(G_PU, i) * iruc;
-        const double bql = Qm * on_o - ZG(G_QL, i) - YG(G_QL, i) * iruc;
-        const double bqu = QM * on_o - ZG(G_QU, i) - YG(G_QU, i) * iruc;
+        const double bpl = Pm * on_o - ZG(G_PL, i) - YG(G_PL, i) / ruc;
+        const double bpu = PM * on_o - ZG(G_PU, i) - YG(G_PU, i) / ruc;
+        const double bql = Qm * on_o - ZG(G_QL, i) - YG(G_QL, i) / ruc;
+        const double bqu = QM * on_o - ZG(G_QU, i) - YG(G_QU, i) / ruc;
         // NEXT-3 variant 16 (R52): the literal Eq. 5f ramp-down row R_D ubar^on_{t-1} + S_D ubar^su_t
         constexpr bool lit = LIT;
-        const double brl = lit ? -RDn * onp_o - SDn * su_o - ZG(G_RD, i) - YG(G_RD, i) * iruc
-                               : -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) * iruc;
+        const double brl = lit ? -RDn * onp_o - SDn * su_o - ZG(G_RD, i) - YG(G_RD, i) / ruc
+                               : -RDn * on_o - SDn * sd_o - ZG(G_RD, i) - YG(G_RD, i) / ruc;
         const double dd = p - ph;
         const double spl = fmax(0.0, p - bpl), spu = fmax(0.0, bpu - p);
         const double sql = fmax(0.0, q - bql), squ = fmax(0.0, bqu - q);
@@ -643,13 +656,13 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         cm[m][2] = (a2);      \
         e[m++] = (ev);        \
     } while (0)
-        ROW(1.0, 0.0, 0.0, (double)ut + ZG(G_DON, i) + YG(G_DON, i) * iruc);
-        ROW(0.0, 1.0, 0.0, (double)sdt + ZG(G_DSD, i) + YG(G_DSD, i) * iruc);
-        ROW(Pm, 0.0, 0.0, (p - spl) + ZG(G_PL, i) + YG(G_PL, i) * iruc);
-        ROW(PM, 0.0, 0.0, (p + spu) + ZG(G_PU, i) + YG(G_PU, i) * iruc);
-        ROW(Qm, 0.0, 0.0, (q - sql) + ZG(G_QL, i) + YG(G_QL, i) * iruc);
-        ROW(QM, 0.0, 0.0, (q + squ) + ZG(G_QU, i) + YG(G_QU, i) * iruc);
-        if (!lit) ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) * iruc);
+        ROW(1.0, 0.0, 0.0, (double)ut + ZG(G_DON, i) + YG(G_DON, i) / ruc);
+        ROW(0.0, 1.0, 0.0, (double)sdt + ZG(G_DSD, i) + YG(G_DSD, i) / ruc);
+        ROW(Pm, 0.0, 0.0, (p - spl) + ZG(G_PL, i) + YG(G_PL, i) / ruc);
+        ROW(PM, 0.0, 0.0, (p + spu) + ZG(G_PU, i) + YG(G_PU, i) / ruc);
+        ROW(Qm, 0.0, 0.0, (q - sql) + ZG(G_QL, i) + YG(G_QL, i) / ruc);
+        ROW(QM, 0.0, 0.0, (q + squ) + ZG(G_QU, i) + YG(G_QU, i) / ruc);
+        if (!lit) ROW(-RDn, -SDn, 0.0, (dd - srd) + ZG(G_RD, i) + YG(G_RD, i) / ruc);
         int n = 2;
         int sun = 0;
         double pn = 0.0, phn = 0.0, sru_n = 0.0, su_on = 0.0, srd_n = 0.0;
@@ -660,14 +673,14 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
             pn = d.p[j];
             phn = d.ph[j];
             su_on = d.ub_su[j];
-            const double bru_n = RUp * on_o + SUp * su_on - ZG(G_RU, j) - YG(G_RU, j) * iruc;
+            const double bru_n = RUp * on_o + SUp * su_on - ZG(G_RU, j) - YG(G_RU, j) / ruc;
             sru_n = fmax(0.0, bru_n - (pn - phn));
-            ROW(0.0, 0.0, 1.0, (double)sun + ZG(G_DSU, j) + YG(G_DSU, j) * iruc);
-            ROW(RUp, 0.0, SUp, ((pn - phn) + sru_n) + ZG(G_RU, j) + YG(G_RU, j) * iruc);
+            ROW(0.0, 0.0, 1.0, (double)sun + ZG(G_DSU, j) + YG(G_DSU, j) / ruc);
+            ROW(RUp, 0.0, SUp, ((pn - phn) + sru_n) + ZG(G_RU, j) + YG(G_RU, j) / ruc);
             if (lit) {   // RD_{t+1} = (d - s) + R_D ubar^on_t + S_D ubar^su_{t+1}: this group's row
-                const double brl_n = -RDn * on_o - SDn * su_on - ZG(G_RD, j) - YG(G_RD, j) * iruc;
+                const double brl_n = -RDn * on_o - SDn * su_on - ZG(G_RD, j) - YG(G_RD, j) / ruc;
                 srd_n = fmax(0.0, (pn - phn) - brl_n);
-                ROW(-RDn, 0.0, -SDn, ((pn - phn) - srd_n) + ZG(G_RD, j) + YG(G_RD, j) * iruc);
+                ROW(-RDn, 0.0, -SDn, ((pn - phn) - srd_n) + ZG(G_RD, j) + YG(G_RD, j) / ruc);
             }
             n = 3;
         }
@@ -693,24 +706,24 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         const double on_n = v[0], sd_n = v[1];
         // rows of the group with the new ubar (r = x-part - c'ubar)
         const double don = on_n - on_o, dsd = sd_n - sd_o;
-        zy_vals((double)ut - on_n, ruc, ibuc, zr[0], yr[0], lr[0], pending, beta_lam, lmax, don, acc);
-        zy_vals((double)sdt - sd_n, ruc, ibuc, zr[1], yr[1], lr[1], pending, beta_lam, lmax, dsd, acc);
-        zy_vals((p - spl) - Pm * on_n, ruc, ibuc, zr[2], yr[2], lr[2], pending, beta_lam, lmax, Pm * don, acc);
-        zy_vals((p + spu) - PM * on_n, ruc, ibuc, zr[3], yr[3], lr[3], pending, beta_lam, lmax, PM * don, acc);
-        zy_vals((q - sql) - Qm * on_n, ruc, ibuc, zr[4], yr[4], lr[4], pending, beta_lam, lmax, Qm * don, acc);
-        zy_vals((q + squ) - QM * on_n, ruc, ibuc, zr[5], yr[5], lr[5], pending, beta_lam, lmax, QM * don, acc);
+        zy_vals_div((double)ut - on_n, ruc, bpr, zr[0], yr[0], lr[0], pending, beta_lam, lmax, don, acc);
+        zy_vals_div((double)sdt - sd_n, ruc, bpr, zr[1], yr[1], lr[1], pending, beta_lam, lmax, dsd, acc);
+        zy_vals_div((p - spl) - Pm * on_n, ruc, bpr, zr[2], yr[2], lr[2], pending, beta_lam, lmax, Pm * don, acc);
+        zy_vals_div((p + spu) - PM * on_n, ruc, bpr, zr[3], yr[3], lr[3], pending, beta_lam, lmax, PM * don, acc);
+        zy_vals_div((q - sql) - Qm * on_n, ruc, bpr, zr[4], yr[4], lr[4], pending, beta_lam, lmax, Qm * don, acc);
+        zy_vals_div((q + squ) - QM * on_n, ruc, bpr, zr[5], yr[5], lr[5], pending, beta_lam, lmax, QM * don, acc);
         if (!lit)
-            zy_vals((dd - srd) + RDn * on_n + SDn * sd_n, ruc, ibuc, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
+            zy_vals_div((dd - srd) + RDn * on_n + SDn * sd_n, ruc, bpr, zr[6], yr[6], lr[6], pending, beta_lam, lmax,
                     RDn * don + SDn * dsd, acc);
         double su_n = 0.0;
         if (nxt) {
             su_n = v[2];
             const double dsu = su_n - su_on;
-            zy_vals((double)sun - su_n, ruc, ibuc, zr[7], yr[7], lr[7], pending, beta_lam, lmax, dsu, acc);
-            zy_vals(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, ibuc, zr[8], yr[8], lr[8], pending, beta_lam,
+            zy_vals_div((double)sun - su_n, ruc, bpr, zr[7], yr[7], lr[7], pending, beta_lam, lmax, dsu, acc);
+            zy_vals_div(((pn - phn) + sru_n) - RUp * on_n - SUp * su_n, ruc, bpr, zr[8], yr[8], lr[8], pending, beta_lam,
                     lmax, RUp * don + SUp * dsu, acc);
             if (lit)
-                zy_vals(((pn - phn) - srd_n) + RDn * on_n + SDn * su_n, ruc, ibuc, zr[9], yr[9], lr[9], pending,
+                zy_vals_div(((pn - phn) - srd_n) + RDn * on_n + SDn * su_n, ruc, bpr, zr[9], yr[9], lr[9], pending,
                         beta_lam, lmax, RDn * don + SDn * dsu, acc);
         }
         d.ub_on[i] = on_n;
@@ -738,24 +751,24 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         }
         if (t == 0) {
             // group 0 = (ubar^su_1): rows D_SU_1, RU_1 (ubar^on_0 := u0, R4)
-            const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) * iruc;
+            const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) / ruc;
             const double sru = fmax(0.0, bru - dd);
             double c1[3][3] = {{1.0, 0.0, 0.0}, {SUp, 0.0, 0.0}, {-SDn, 0.0, 0.0}};
             double e1[3];
-            e1[0] = (double)sut + ZG(G_DSU, i) + YG(G_DSU, i) * iruc;
-            e1[1] = (dd + sru) - RUp * (double)u0 + ZG(G_RU, i) + YG(G_RU, i) * iruc;
+            e1[0] = (double)sut + ZG(G_DSU, i) + YG(G_DSU, i) / ruc;
+            e1[1] = (dd + sru) - RUp * (double)u0 + ZG(G_RU, i) + YG(G_RU, i) / ruc;
             // literal Eq. 5f (R52): RD_1 = (d - s) + R_D u0 + S_D ubar^su_1 joins this group
-            e1[2] = ((dd - srd) + RDn * (double)u0) + ZG(G_RD, i) + YG(G_RD, i) * iruc;
+            e1[2] = ((dd - srd) + RDn * (double)u0) + ZG(G_RD, i) + YG(G_RD, i) / ruc;
             double v1[3];
             boxqp3(1, lit ? 3 : 2, c1, e1, v1);
             d.ub_su[i] = v1[0];
             const double dsu = v1[0] - su_o;
-            zy_row((double)sut - v1[0], ruc, ibuc, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
+            zy_row_div((double)sut - v1[0], ruc, bpr, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
                    acc);
-            zy_row((dd + sru) - RUp * (double)u0 - SUp * v1[0], ruc, ibuc, &ZG(G_RU, i), &YG(G_RU, i), &LG(G_RU, i),
+            zy_row_div((dd + sru) - RUp * (double)u0 - SUp * v1[0], ruc, bpr, &ZG(G_RU, i), &YG(G_RU, i), &LG(G_RU, i),
                    pending, beta_lam, lmax, SUp * dsu, acc);
             if (lit)
-                zy_row((dd - srd) + RDn * (double)u0 + SDn * v1[0], ruc, ibuc, &ZG(G_RD, i), &YG(G_RD, i), &LG(G_RD, i),
+                zy_row_div((dd - srd) + RDn * (double)u0 + SDn * v1[0], ruc, bpr, &ZG(G_RD, i), &YG(G_RD, i), &LG(G_RD, i),
                        pending, beta_lam, lmax, SDn * dsu, acc);
         }
         // objective, Eq. 1a with f^OPF = c2 (S p)^2 + c1 S p and f^UC (R13)

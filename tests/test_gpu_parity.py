@@ -170,7 +170,7 @@ def test_case9_config_50_iterations():
     run_pair(pb, pr, 50)
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
 def test_random_grids_ragged(seed):
     """synthetic grids whose (l,t), (i,t), (g,t) counts span several blocks with ragged tails."""
     rng = np.random.default_rng(seed)
@@ -372,3 +372,10 @@ def test_pegase_t168_stress_one_iteration():
     gpu.iterate(1)
     orc.iterate(1)
     compare(gpu.get_state(), orc.get_state(), max(pr.rho_pq, pr.rho_va, pr.rho_uc), "pegase T=168")
+
+
+def test_case300_config_one_step_every_third():
+    """BASELINE configs[3] shape (case300, T=24) on one GPU: 45 iterations, one-step parity on
+    every third, free-running schedules and scalars exact throughout."""
+    pb, pr = inputs.build_config("case300")
+    run_pair(pb, pr, 45, check_every=3)
