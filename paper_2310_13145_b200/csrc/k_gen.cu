@@ -230,6 +230,104 @@ __device__ void gen_solve(const GenIn &g, double &po, double &qo, double &pho) {
     pho = bph;
 }
 
+// The same enumeration split over GENX_LANES consecutive lanes: lane `sub` evaluates the
+// candidates with index = sub (mod GENX_LANES), each exactly as gen_solve does, and the lanes
+// combine (value, index) keeping the smallest value and, on ties, the smallest index -- which is
+// the candidate gen_solve's sequential "if (v < best)" keeps.  Bitwise the same result with
+// GENX_LANES x the threads per (g,t).
+#ifndef UCAC_GENX_LANES
+#define UCAC_GENX_LANES 2   // measured: 1 lane 20.8 us, 2 lanes 16.8, 4 lanes 20.9, 8 lanes 25.1 (eager)
+#endif
+constexpr int GENX_LANES = UCAC_GENX_LANES;
+__device__ __forceinline__ void lane_min(double &v, int &idx, double &a, double &b) {
+    const unsigned m = __activemask();   // whole lane groups: past the end of the grid they left together
+#pragma unroll
+    for (int o = 1; o < GENX_LANES; o <<= 1) {
+        const double v2 = __shfl_xor_sync(m, v, o, GENX_LANES);
+        const int i2 = __shfl_xor_sync(m, idx, o, GENX_LANES);
+        const double a2 = __shfl_xor_sync(m, a, o, GENX_LANES);
+        const double b2 = __shfl_xor_sync(m, b, o, GENX_LANES);
+        if (v2 < v || (v2 == v && i2 < idx)) { v = v2; idx = i2; a = a2; b = b2; }
+    }
+}
+__device__ void gen_solve_lanes(const GenIn &g, int sub, double &po, double &qo, double &pho) {
+    // candidate index: 0..15 the interior patterns, then the bound candidates in gen_solve's order
+    double best = INFINITY, bp = g.pL, bph = g.first ? g.p0 : g.tph;
+    int bidx = 1 << 30;
+    const int ncand = g.first ? 18 : 24;
+    for (int c = sub; c < ncand; c += GENX_LANES) {
+        double v = NAN, p = 0.0, ph = 0.0;
+        bool ok = false;
+        if (c < 16) {
+            const int pat = c;
+            const int alo = pat & 1, ahi = (pat >> 1) & 1, rlo = (pat >> 2) & 1, rhi = (pat >> 3) & 1;
+            if (g.first) {
+                double den = 2.0 * g.c2S2 + g.rpq;
+                double num = -g.c1S + g.rpq * g.tp;
+                if (alo) { den = den + g.ruc; num = num + g.ruc * g.bpl; }
+                if (ahi) { den = den + g.ruc; num = num + g.ruc * g.bpu; }
+                if (rlo) { den = den + g.ruc; num = num + g.ruc * (g.brl + g.p0); }
+                if (rhi) { den = den + g.ruc; num = num + g.ruc * (g.bru + g.p0); }
+                p = num / den;
+                ph = g.p0;
+            } else {
+                double A = 2.0 * g.c2S2 + g.rpq;
+                double b1 = -g.c1S + g.rpq * g.tp;
+                if (alo) { A = A + g.ruc; b1 = b1 + g.ruc * g.bpl; }
+                if (ahi) { A = A + g.ruc; b1 = b1 + g.ruc * g.bpu; }
+                double R = 0.0, rb = 0.0;
+                if (rlo) { R = R + g.ruc; rb = rb + g.ruc * g.brl; }
+                if (rhi) { R = R + g.ruc; rb = rb + g.ruc * g.bru; }
+                b1 = b1 + rb;
+                double b2 = g.rpq * g.tph - rb;
+                double det = (A + R) * (g.rpq + R) - R * R;
+                p = (b1 * (g.rpq + R) + R * b2) / det;
+                ph = ((A + R) * b2 + R * b1) / det;
+            }
+            ok = p >= g.pL && p <= g.pU;
+        } else if (g.first) {
+            p = c == 16 ? g.pL : g.pU;
+            ph = g.p0;
+            ok = true;
+        } else {
+            const int kb = (c - 16) >> 2, pat = (c - 16) & 3;
+            p = kb ? g.pU : g.pL;
+            const int rlo = pat & 1, rhi = (pat >> 1) & 1;
+            double R = 0.0, rb = 0.0;
+            if (rlo) { R = R + g.ruc; rb = rb + g.ruc * g.brl; }
+            if (rhi) { R = R + g.ruc; rb = rb + g.ruc * g.bru; }
+            ph = (g.rpq * g.tph - rb + R * p) / (g.rpq + R);
+            ok = true;
+        }
+        if (ok) v = gen_obj_p(g, p, ph);
+        if (v < best) { best = v; bidx = c; bp = p; bph = ph; }
+    }
+    lane_min(best, bidx, bp, bph);
+    if (g.first) bph = g.p0;
+    double bestq = INFINITY, bq = g.qL;
+    int qidx = 1 << 30;
+    for (int c = sub; c < 6; c += GENX_LANES) {
+        double qq, v = NAN;
+        if (c < 4) {
+            const int lo = c & 1, hi = (c >> 1) & 1;
+            double den = g.rpq, num = g.rpq * g.tq;
+            if (lo) { den = den + g.ruc; num = num + g.ruc * g.bql; }
+            if (hi) { den = den + g.ruc; num = num + g.ruc * g.bqu; }
+            qq = num / den;
+            if (qq >= g.qL && qq <= g.qU) v = gen_obj_q(g, qq);
+        } else {
+            qq = c == 4 ? g.qL : g.qU;
+            v = gen_obj_q(g, qq);
+        }
+        if (v < bestq) { bestq = v; qidx = c; bq = qq; }
+    }
+    double dummy = 0.0;
+    lane_min(bestq, qidx, bq, dummy);
+    po = bp;
+    qo = bq;
+    pho = bph;
+}
+
 #define ZG(k, i) d.zg[(size_t)(k) * GT + (i)]
 #define YG(k, i) d.yg[(size_t)(k) * GT + (i)]
 
@@ -280,10 +378,15 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    // GENX_LANES consecutive lanes per (g,t): a group never straddles the end of the range, so
+    // whole groups past it leave together and the shuffles stay within the active groups
+    const int k4 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = k4 / GENX_LANES, sub = k4 % GENX_LANES;
     if (k >= d.G * T) return;
-    if (!d.uc_fixed) d.u[k] = d.u_next[k];   // adopt this iteration's (7a) schedule
-    if (k == 0) *d.unext_ok = 0u;              // u_next is consumed: stale for the next state
+    if (sub == 0) {
+        if (!d.uc_fixed) d.u[k] = d.u_next[k];   // adopt this iteration's (7a) schedule
+        if (k == 0) *d.unext_ok = 0u;              // u_next is consumed: stale for the next state
+    }
     const int g = k / T, t = k - g * T;
     const double ruc = d.ruc, rpq = d.rpq;
     const double S = d.S;
@@ -316,10 +419,12 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
                               : -rdn * on - sdn * sd - ZG(G_RD, i) - YG(G_RD, i) / d.ruc;
     in.bru = rup * onp + sup * su - ZG(G_RU, i) - YG(G_RU, i) / d.ruc;
     double po, qo, pho;
-    gen_solve(in, po, qo, pho);
-    d.p[i] = po;
-    d.q[i] = qo;
-    d.ph[i] = pho;
+    gen_solve_lanes(in, sub, po, qo, pho);
+    if (sub == 0) {
+        d.p[i] = po;
+        d.q[i] = qo;
+        d.ph[i] = pho;
+    }
 }
 
 __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
@@ -411,7 +516,9 @@ void launch_gen(const Dev &d, cudaStream_t s, int tail) {
     const int warps = 4;
     launch_hi_prio(k_gen, dim3((d.G + warps - 1) / warps), dim3(warps * 32), gen_smem(d.T, warps), s, d, tail);
 }
-void launch_genx(const Dev &d, cudaStream_t s) { launch_hi_prio(k_genx, dim3((d.G * d.T + 127) / 128), dim3(128), 0, s, d); }
+void launch_genx(const Dev &d, cudaStream_t s) {
+    launch_hi_prio(k_genx, dim3((GENX_LANES * d.G * d.T + 127) / 128), dim3(128), 0, s, d);
+}
 
 cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                             const int *hold, int8_t *sched, double *cost, cudaStream_t s) {
