@@ -977,6 +977,9 @@ void launch_branch(const Dev &d, cudaStream_t s) {
     if (d.variant & 8) k_branch<true><<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
     else k_branch<false><<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
 }
+#ifndef UCAC_AL_PRIO
+#define UCAC_AL_PRIO 0
+#endif
 #ifndef UCAC_AL_SMEM
 #define UCAC_AL_SMEM 0   // dynamic shared memory per AL block (bytes): > 0 reserves SMs for the AL work
 #endif
@@ -985,8 +988,14 @@ void launch_branch_al(const Dev &d, cudaStream_t s) {
         cudaFuncSetAttribute(k_branch_al<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
         cudaFuncSetAttribute(k_branch_al<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
     }
-    if (d.variant & 8) k_branch_al<true><<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, UCAC_AL_SMEM, s>>>(d);
-    else k_branch_al<false><<<148 * UCAC_AL_BLOCKS_PER_SM, UCAC_AL_TPB, UCAC_AL_SMEM, s>>>(d);
+    const dim3 grid(148 * UCAC_AL_BLOCKS_PER_SM), block(UCAC_AL_TPB);
+    if (UCAC_AL_PRIO) {   // high launch priority: its full-SM blocks take SMs as k_branch drains
+        if (d.variant & 8) launch_hi_prio(k_branch_al<true>, grid, block, (size_t)UCAC_AL_SMEM, s, d);
+        else launch_hi_prio(k_branch_al<false>, grid, block, (size_t)UCAC_AL_SMEM, s, d);
+    } else {
+        if (d.variant & 8) k_branch_al<true><<<grid, block, UCAC_AL_SMEM, s>>>(d);
+        else k_branch_al<false><<<grid, block, UCAC_AL_SMEM, s>>>(d);
+    }
 }
 
 }  // namespace ucac
