@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
 // by every thread of a persistent grid, so the heavy tail is spread over all SMs.
 template <bool NOANG>
 __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
+    pdl_wait();
     TL_KERNEL(K_BRANCH_AL);
     if (d.st->done) return;
     const size_t LTs = (size_t)d.L * d.T;
@@ -989,9 +990,10 @@ void launch_branch_al(const Dev &d, cudaStream_t s) {
         cudaFuncSetAttribute(k_branch_al<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UCAC_AL_SMEM);
     }
     const dim3 grid(148 * UCAC_AL_BLOCKS_PER_SM), block(UCAC_AL_TPB);
-    if (UCAC_AL_PRIO) {   // high launch priority: its full-SM blocks take SMs as k_branch drains
-        if (d.variant & 8) launch_hi_prio(k_branch_al<true>, grid, block, (size_t)UCAC_AL_SMEM, s, d);
-        else launch_hi_prio(k_branch_al<false>, grid, block, (size_t)UCAC_AL_SMEM, s, d);
+    const bool pdl = (pdl_mask() & 1) != 0;
+    if (UCAC_AL_PRIO || pdl) {   // high launch priority: its full-SM blocks take SMs as k_branch drains
+        if (d.variant & 8) launch_ex(k_branch_al<true>, grid, block, (size_t)UCAC_AL_SMEM, s, UCAC_AL_PRIO != 0, pdl, d);
+        else launch_ex(k_branch_al<false>, grid, block, (size_t)UCAC_AL_SMEM, s, UCAC_AL_PRIO != 0, pdl, d);
     } else {
         if (d.variant & 8) k_branch_al<true><<<grid, block, UCAC_AL_SMEM, s>>>(d);
         else k_branch_al<false><<<grid, block, UCAC_AL_SMEM, s>>>(d);

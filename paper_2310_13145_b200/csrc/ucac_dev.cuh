@@ -5,6 +5,10 @@
 // so that a warp whose lanes are consecutive periods of one component (or consecutive
 // (component, period) pairs) reads each row kind as one coalesced 256-B segment.
 #pragma once
+#ifndef UCAC_PDL_DEFAULT
+#define UCAC_PDL_DEFAULT 0
+#endif
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -158,6 +162,39 @@ void launch_branch_al(const Dev &d, cudaStream_t s);
 // Launch with the device's highest execution priority (a launch attribute, kept by graph capture):
 // the generator chain (k_gen, k_genx, k_ubar) forks at the start of the iteration and should take
 // SM slots as k_branch blocks retire rather than queue behind them.
+// Programmatic dependent launch (PDL) of the critical chain's kernels, bit mask from UCAC_PDL
+// (1 = k_branch_al after k_branch, 2 = k_bus_late after k_branch_al, 4 = k_rows_late after
+// k_bus_late): the dependent grid is scheduled as the primary's blocks exit and waits in
+// griddepcontrol.wait (pdl_wait, first statement of those kernels; a no-op without the attribute)
+// until the primary grid has completed and its memory is visible.  Experiments.
+inline int pdl_mask() {
+    static const int m = [] { const char *e = getenv("UCAC_PDL"); return e ? atoi(e) : UCAC_PDL_DEFAULT; }();
+    return m;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs>
+inline cudaError_t launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool hi,
+                             bool pdl, KArgs... args) {
+    static int prio = [] { int lo = 0, hi_ = 0; cudaDeviceGetStreamPriorityRange(&lo, &hi_); return hi_; }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    if (hi) {
+        at[n].id = cudaLaunchAttributePriority;
+        at[n++].val.priority = prio;
+    }
+    if (pdl) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
 template <typename... KArgs>
 inline cudaError_t launch_hi_prio(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, KArgs... args) {
     static int prio = [] { int lo = 0, hi = 0; cudaDeviceGetStreamPriorityRange(&lo, &hi); return hi; }();

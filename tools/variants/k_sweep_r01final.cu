@@ -14,7 +14,6 @@
 // applied lazily by the owning thread at the start of its row update in iteration l+1 (the
 // x-steps never read lambda), which saves a full pass over all rows.
 #include <algorithm>
-#include <cstdlib>
 
 #include "ucac_dev.cuh"
 
@@ -88,33 +87,20 @@ __device__ __forceinline__ void zy_vals_div(double r, double rho, double bpr, do
     zy_vals(r, rho, 0.0, z, y, lam, pending, beta_lam, lmax, dxb, a, bpr);
 }
 
-#ifndef UCAC_RED_SKIP
-#define UCAC_RED_SKIP 1   // idle warps skip the block reduction's shuffle tree (bitwise neutral)
-#endif
 // deterministic block reduction -> part[blockIdx.x][NPART]
 __device__ void block_reduce_store(Acc &a, double *part) {
     __shared__ double sh[32][NPART];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // A warp none of whose lanes touched its accumulator (every slot still +0.0, compared
-    // bitwise) folds to +0.0 in every slot (0 + 0 and fmax(0, 0)), so it skips the shuffle tree
-    // and stores that directly: the same bits.  Most warps of the late kernels are such warps.
-    bool touched = !UCAC_RED_SKIP;
 #pragma unroll
-    for (int k = 0; k < NPART; k++) touched |= __double_as_longlong(a.v[k]) != 0;
-    if (!__any_sync(0xffffffffu, touched)) {
-        if (lane < NPART) sh[warp][lane] = 0.0;
-    } else {
+    for (int k = 0; k < NPART; k++) {
+        double v = a.v[k];
+        const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
 #pragma unroll
-        for (int k = 0; k < NPART; k++) {
-            double v = a.v[k];
-            const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                double w = __shfl_down_sync(0xffffffffu, v, o);
-                v = isum ? v + w : fmax(v, w);
-            }
-            if (lane == 0) sh[warp][k] = v;
+        for (int o = 16; o > 0; o >>= 1) {
+            double w = __shfl_down_sync(0xffffffffu, v, o);
+            v = isum ? v + w : fmax(v, w);
         }
+        if (lane == 0) sh[warp][k] = v;
     }
     __syncthreads();
     if (threadIdx.x < NPART) {
@@ -163,30 +149,21 @@ enum RecKind { RK_EARLY = 0, RK_BUS_LATE, RK_ROWS_LATE, NRK };
 __device__ __forceinline__ double fold(int k, double a, double b) {
     return (k == P_RZ2 || k == P_Z2 || k == P_OBJ) ? a + b : fmax(a, b);
 }
-#ifndef UCAC_FOLD_BATCH
-#define UCAC_FOLD_BATCH 16
-#endif
-constexpr int FOLD_BATCH = UCAC_FOLD_BATCH;
 __device__ void fold_slots(const double *part, int n, double *out) {
     __shared__ double grp[32][NPART];
     const int ng = min(32, (int)blockDim.x / NPART);   // groups (blockDim is a multiple of NPART)
     const int k = threadIdx.x % NPART, g = threadIdx.x / NPART;
     if (g < ng) {
         double v = 0.0;
-        // FOLD_BATCH independent loads in flight per round trip, folded in slot order (g, g+ng, ...):
-        // the last block's fold is on the iteration's critical path, and with 4 in flight the
-        // ~860 partials of k_rows_late took 7 dependent L2 round trips
-        for (int j = g; j < n; j += FOLD_BATCH * ng) {
-            double a[FOLD_BATCH];
-#pragma unroll
-            for (int u = 0; u < FOLD_BATCH; u++) {
-                const int jj = j + u * ng;
-                a[u] = jj < n ? __ldcg(part + (size_t)jj * NPART + k) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < FOLD_BATCH; u++)
-                if (j + u * ng < n) v = fold(k, v, a[u]);
+        int j = g;
+        for (; j + 3 * ng < n; j += 4 * ng) {   // four independent loads in flight, folded in slot order
+            const double a0 = __ldcg(part + (size_t)j * NPART + k);
+            const double a1 = __ldcg(part + (size_t)(j + ng) * NPART + k);
+            const double a2 = __ldcg(part + (size_t)(j + 2 * ng) * NPART + k);
+            const double a3 = __ldcg(part + (size_t)(j + 3 * ng) * NPART + k);
+            v = fold(k, fold(k, fold(k, fold(k, v, a0), a1), a2), a3);
         }
+        for (; j < n; j += ng) v = fold(k, v, __ldcg(part + (size_t)j * NPART + k));
         grp[g][k] = v;
     }
     __syncthreads();
@@ -488,18 +465,15 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
 }
 
 // Late phase (after the AL tail): k_bus_late solves the marked bus-periods, k_rows_late updates
-// the marked ends (k_bus_late: 1024-thread blocks, few partial slots, so the final fold is short;
-// k_rows_late: 256-thread blocks, one wave grid-striding over (l,t)).
+// the marked ends (1024-thread blocks: few partial slots, so the final fold is short).
 // Single GPU: k_rows_late is the last kernel of the iteration (final = 1).
 __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
-    pdl_wait();
     TL_KERNEL(K_BUS_LATE);
     if (d.st->done) return;
+    const Ctl c(d);
     Acc acc;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    // the control values (two divisions) only for the marked few: most late threads skip
-    if (k < d.B_own * d.T && d.bmark[k] == mark_stamp(d)) {
-        const Ctl c(d);
+    if (k < d.B_own * d.T && d.bmark[k] == c.stamp) {
         bus_solve(d, c, k, acc);
         if (d.fuse_rows) bus_end_rows(d, c, k, acc);
     }
@@ -542,20 +516,15 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
 }
 
 __global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
-    pdl_wait();
     TL_KERNEL(K_ROWS_LATE);
     if (d.st->done) return;
+    const Ctl c(d);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc;
-    // grid-stride: one pass per thread at the default grid (UCAC_LROWS_GRID caps it, experiments)
-    const unsigned stamp = mark_stamp(d);
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d.L * d.T; k += gridDim.x * blockDim.x) {
-        const bool m0 = d.rmark[0][k] == stamp, m1 = d.rmark[1][k] == stamp;
-        if (m0 || m1) {   // the control values (two divisions) only for the marked few
-            const Ctl c(d);
-            const int l = k / d.T, t = k - l * d.T;
-            if (m0) end_rows(d, c, l, t, 0, acc);
-            if (m1) end_rows(d, c, l, t, 1, acc);
-        }
+    if (k < d.L * d.T) {
+        const int l = k / d.T, t = k - l * d.T;
+        if (d.rmark[0][k] == c.stamp) end_rows(d, c, l, t, 0, acc);
+        if (d.rmark[1][k] == c.stamp) end_rows(d, c, l, t, 1, acc);
     }
     kernel_tail(d, acc, d.part_lrows, RK_ROWS_LATE, final != 0);
 }
@@ -947,27 +916,10 @@ void launch_rows(const Dev &d, cudaStream_t s) { launch_sweep(UCAC_SWEEP_PRIO, k
 // the late kernels at high priority: when the AL tail frees its SMs, k_bus_late's full-SM blocks
 // take them ahead of k_rows' pending blocks
 void launch_bus_late(const Dev &d, cudaStream_t s) {
-    launch_ex(k_bus_late, dim3(d.nblk_lbus), dim3(LBUS_THREADS), 0, s, UCAC_SWEEP_PRIO || UCAC_LATE_PRIO,
-              (pdl_mask() & 2) != 0, d);
+    launch_sweep(UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, k_bus_late, dim3(d.nblk_lbus), dim3(LBUS_THREADS), s, d);
 }
 void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
-    // One wave: at most (resident blocks per SM) x SMs blocks, grid-striding over the (l,t) range.
-    // The default grid (one thread per (l,t), ~860 blocks on pegase at 2 resident per SM) ran in
-    // three waves, each paying a marked end's dependent load chain and the block tail: 28.2 ->
-    // 22.5 us in the graph, step -2.4 %.  UCAC_LROWS_GRID=n caps the grid at n
-    // instead; n < 0 restores one thread per (l,t).
-    static const int lrows_cap = [] {
-        const char *e = getenv("UCAC_LROWS_GRID");
-        if (e) return atoi(e);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_late, LROWS_THREADS, 0);
-        return std::max(1, sms * per_sm);
-    }();
-    const int g = lrows_cap > 0 ? std::min(d.nblk_lrows, lrows_cap) : d.nblk_lrows;
-    launch_ex(k_rows_late, dim3(g), dim3(LROWS_THREADS), 0, s, UCAC_SWEEP_PRIO || UCAC_LATE_PRIO,
-              (pdl_mask() & 4) != 0, d, final);
+    launch_sweep(UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, k_rows_late, dim3(d.nblk_lrows), dim3(LROWS_THREADS), s, d, final);
 }
 int nblk_lbus(int n) { return (n + LBUS_THREADS - 1) / LBUS_THREADS; }
 int nblk_lrows(int n) { return (n + LROWS_THREADS - 1) / LROWS_THREADS; }
