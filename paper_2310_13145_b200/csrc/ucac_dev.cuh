@@ -6,7 +6,7 @@
 // (component, period) pairs) reads each row kind as one coalesced 256-B segment.
 #pragma once
 #ifndef UCAC_PDL_DEFAULT
-#define UCAC_PDL_DEFAULT 0
+#define UCAC_PDL_DEFAULT 1   // k_branch_al after k_branch (measured)
 #endif
 #include <cstdlib>
 #include <cuda_runtime.h>
