@@ -508,7 +508,10 @@ __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
 }
 
 // k_fold_early: the block partials of k_bus, k_ubar and k_rows (in that order) -> rec_part[RK_EARLY]
-constexpr int FOLD_BLOCKS = 64, FOLD_THREADS = 256;
+#ifndef UCAC_FOLD_BLOCKS
+#define UCAC_FOLD_BLOCKS 64
+#endif
+constexpr int FOLD_BLOCKS = UCAC_FOLD_BLOCKS, FOLD_THREADS = 256;
 __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
     TL_KERNEL(K_FOLD);
     if (d.st->done) return;
@@ -518,10 +521,20 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
     __shared__ double grp[FOLD_THREADS / NPART][NPART];
     const int k = threadIdx.x % NPART, g = threadIdx.x / NPART, ng = FOLD_THREADS / NPART;
     double v = 0.0;
-    for (int j = j0 + g; j < j1; j += ng) {
-        const double *p = j < nb ? d.part_bus + (size_t)j * NPART
-                        : j < nb + nu ? d.part_ubar + (size_t)(j - nb) * NPART : d.part_rows + (size_t)(j - nb - nu) * NPART;
-        v = fold(k, v, __ldcg(p + k));
+    // FOLD_BATCH loads in flight, folded in slot order (as fold_slots)
+    for (int j = j0 + g; j < j1; j += FOLD_BATCH * ng) {
+        double a[FOLD_BATCH];
+#pragma unroll
+        for (int u = 0; u < FOLD_BATCH; u++) {
+            const int jj = j + u * ng;
+            const double *p = jj < nb ? d.part_bus + (size_t)jj * NPART
+                            : jj < nb + nu ? d.part_ubar + (size_t)(jj - nb) * NPART
+                                           : d.part_rows + (size_t)(jj - nb - nu) * NPART;
+            a[u] = jj < j1 ? __ldcg(p + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < FOLD_BATCH; u++)
+            if (j + u * ng < j1) v = fold(k, v, a[u]);
     }
     grp[g][k] = v;
     __syncthreads();
