@@ -739,6 +739,7 @@ __device__ __forceinline__ void emit_tauhat(const Dev &d, int k, const double *x
 #endif
 template <bool NOANG>
 __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(Dev d) {
+    pdl_wait();
     TL_KERNEL(K_BRANCH);
     if (d.st->done) return;
     const int LT = d.L * d.T;
@@ -975,6 +976,11 @@ void launch_branch(const Dev &d, cudaStream_t s) {
     const int n = d.L * d.T, chunks = (n + UCAC_BRANCH_TPB - 1) / UCAC_BRANCH_TPB;
     // 148 SMs x UCAC_BRANCH_MINB resident blocks, minus the slots left to the generator chain
     const int grid = std::max(1, std::min(chunks, 148 * UCAC_BRANCH_MINB - UCAC_BRANCH_FREE_SLOTS));
+    if (pdl_mask() & 8) {   // after the previous iteration's last kernel (experiments)
+        if (d.variant & 8) launch_ex(k_branch<true>, dim3(grid), dim3(UCAC_BRANCH_TPB), 0, s, false, true, d);
+        else launch_ex(k_branch<false>, dim3(grid), dim3(UCAC_BRANCH_TPB), 0, s, false, true, d);
+        return;
+    }
     if (d.variant & 8) k_branch<true><<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
     else k_branch<false><<<grid, UCAC_BRANCH_TPB, 0, s>>>(d);
 }

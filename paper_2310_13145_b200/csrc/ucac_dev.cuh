@@ -164,7 +164,7 @@ void launch_branch_al(const Dev &d, cudaStream_t s);
 // SM slots as k_branch blocks retire rather than queue behind them.
 // Programmatic dependent launch (PDL) of the critical chain's kernels, bit mask from UCAC_PDL
 // (1 = k_branch_al after k_branch, 2 = k_bus_late after k_branch_al, 4 = k_rows_late after
-// k_bus_late): the dependent grid is scheduled as the primary's blocks exit and waits in
+// k_bus_late, 8 = k_branch after the previous iteration's last kernel): the dependent grid is scheduled as the primary's blocks exit and waits in
 // griddepcontrol.wait (pdl_wait, first statement of those kernels; a no-op without the attribute)
 // until the primary grid has completed and its memory is visible.  Experiments.
 inline int pdl_mask() {
