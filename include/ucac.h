@@ -233,7 +233,10 @@ ucac_status ucac_uc_warm_start(const ucac_network *net, const ucac_horizon *hz, 
  * L^UC_{g,t}(a, b).  Outputs sched [ngen*T] (int8) and cost [ngen].  Tie -> stay
  * (P:380), windows clipped at T (R15), forced prefix of hold periods (R14).  When on_device
  * != 0 all five array arguments are device pointers and the call runs asynchronously on
- * cuda_stream (NULL = legacy default stream); otherwise they are host pointers. */
+ * cuda_stream (NULL = legacy default stream); otherwise they are host pointers.  Host inputs are
+ * validated (min_up, min_dn in [1, T], hold in [0, T], u0 in {0, 1}; else UCAC_EINVAL); device
+ * inputs cannot be checked without a sync, so an out-of-range instance gets cost NaN and an
+ * all-zero schedule from the kernel (no out-of-range access). */
 ucac_status ucac_dp_batch(int32_t ngen, int32_t T, const double *L, const int32_t *min_up,
                           const int32_t *min_dn, const int32_t *u0, const int32_t *hold,
                           int8_t *sched, double *cost, int32_t on_device, void *cuda_stream);

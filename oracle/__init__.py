@@ -68,7 +68,8 @@ class Params_c(C.Structure):
                 ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
-                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32)]
+                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32),
+                ("plain", C.c_int32)]
 
 
 class Report_c(C.Structure):
@@ -77,7 +78,9 @@ class Report_c(C.Structure):
                 ("objective", C.c_double), ("beta", C.c_double),
                 ("inner_total", C.c_int64), ("outer_total", C.c_int64), ("tron_iters", C.c_int64),
                 ("tron_capped", C.c_int64), ("al_active", C.c_int64), ("al_capped", C.c_int64),
-                ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32)]
+                ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32),
+                ("flops_fast", C.c_double), ("flops_al", C.c_double),
+                ("newton_fast", C.c_int64), ("newton_al", C.c_int64)]
 
 
 STATE_FIELDS = [("u", np.int8, "GT"), ("p", np.float64, "GT"), ("q", np.float64, "GT"),
@@ -117,6 +120,10 @@ def _declare(L):
     L.orc_tron_quadratic.argtypes = [C.c_int32, dp, dp, dp, dp, C.c_double, C.c_int32, dp]
     L.orc_tron_quadratic.restype = C.c_int
     L.orc_branch_flows.argtypes = [dp, dp, dp, dp, dp]
+    L.orc_sincos.argtypes = [C.c_double, dp, dp]
+    L.orc_sincos.restype = None
+    L.orc_get_slacks.argtypes = [C.c_void_p, dp]
+    L.orc_get_slacks.restype = None
 
 
 def _p(a, t=dp):
@@ -127,17 +134,18 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def params_c(pr) -> Params_c:
+def params_c(pr, plain: bool = False) -> Params_c:
+    """plain: the branch solver without the accelerations R41-R44/R48/R49 (oracle-only twin)"""
     return Params_c(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max,
                     pr.beta_max, pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled,
                     pr.tron_gtol_rel, pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel,
-                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed, pr.variant)
+                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed, pr.variant, int(plain))
 
 
 class Oracle:
     """One oracle context (Algorithm 1 run on the CPU)."""
 
-    def __init__(self, pb, pr):
+    def __init__(self, pb, pr, plain: bool = False):
         self.L = lib()
         pb = pb.normalized()
         self.pb = pb
@@ -159,7 +167,7 @@ class Oracle:
                               k(pb.c2), k(pb.c1), k(pb.c0), k(pb.csu), k(pb.csd),
                               k(pb.ramp_up), k(pb.ramp_dn), k(pb.su_ramp), k(pb.sd_ramp),
                               k(pb.min_up, ip), k(pb.min_dn, ip), k(pb.u0, ip), k(pb.hold, ip), k(pb.p0), ui)
-        self._prc = params_c(pr)
+        self._prc = params_c(pr, plain)
         h = C.c_void_p()
         rc = self.L.orc_create(C.byref(self._pbc), C.byref(self._prc), C.byref(h))
         if rc != 0:
@@ -200,6 +208,12 @@ class Oracle:
         sc = State_c(*[_p(st[n], i8p if t == np.int8 else dp) for n, t, _ in STATE_FIELDS])
         self.L.orc_get_state(self.h, C.byref(sc))
         return st
+
+    def slacks(self) -> np.ndarray:
+        """generator slacks of the current x, [ngen*T, 6] (pl, pu, ql, qu, rd, ru)"""
+        out = np.zeros(6 * self.pb.ngen * self.pb.T)
+        self.L.orc_get_slacks(self.h, _p(out))
+        return out.reshape(-1, 6)
 
     def set_state(self, st: dict):
         sz = self._sizes()
@@ -275,12 +289,14 @@ def bus_kkt(alpha, beta, a, tauhat, P, Q):
     return v, mu
 
 
-def branch_solve(y, wlo, whi, rate, tau, rho_pq, rho_va, pr, x, al):
+def branch_solve(y, wlo, whi, rate, tau, rho_pq, rho_va, pr, x, al, plain=False):
+    """stats: tron its, capped, al active, al rounds, al capped, flops fast, flops al,
+    Newton its fast, Newton its al"""
     x = _f64(x).copy()
     al = _f64(al).copy()
     f = np.zeros(4)
-    st = np.zeros(5, dtype=np.int64)
-    prc = params_c(pr)
+    st = np.zeros(9, dtype=np.int64)
+    prc = params_c(pr, plain)
     lib().orc_branch_solve(_p(_f64(y)), _p(_f64(wlo)), _p(_f64(whi)), rate, _p(_f64(tau)),
                            rho_pq, rho_va, C.byref(prc), _p(x), _p(al), _p(f), _p(st, i64p))
     return x, al, f, st
@@ -293,6 +309,13 @@ def tron_quadratic(A, b, lo, hi, x0, gtol=1e-10, maxit=200):
     it = lib().orc_tron_quadratic(n, _p(A.reshape(-1)), _p(_f64(b)), _p(_f64(lo)), _p(_f64(hi)),
                                   gtol, maxit, _p(x))
     return x, it
+
+
+def sincos(a):
+    """(sin a, cos a) by the oracle's explicit polynomial (R54)"""
+    s, c = C.c_double(), C.c_double()
+    lib().orc_sincos(float(a), C.byref(s), C.byref(c))
+    return s.value, c.value
 
 
 def branch_flows(y, x):

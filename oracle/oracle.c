@@ -62,6 +62,50 @@ static double dmax(double a, double b) { return a > b ? a : b; }
 static double dmin(double a, double b) { return a < b ? a : b; }
 static double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+/* Algorithmic flop counter of the branch solves (R55): each +, -, *, /, sqrt is one
+ * flop, counted per operation as the plain algorithm states it (comparisons, clamps, copies and
+ * sign flips are not flops).  Per thread, so the OpenMP build counts per solve. */
+static __thread double g_fl;
+#define FL(n) (g_fl += (double)(n))
+
+/* sin and cos of one argument (R54).  An explicit polynomial instead of libm, so the
+ * strict_fp GPU build can run the identical operation sequence and the two codes agree bit for
+ * bit.  Cody-Waite reduction a = k pi/2 + r with k = floor(a 2/pi + 1/2) and fdlibm's split of
+ * pi/2 (33 leading bits + tail), then the Taylor series of sin to r^17 and of cos to r^18 on
+ * |r| <= pi/4 (truncation < 1e-19); quadrant by k mod 4.  Pinned against libm in
+ * tests/test_oracle_branch.py (<= 2 ulp on [-4 pi, 4 pi], the range of theta_i - theta_j).
+ * 43 flops. */
+void orc_sincos(double a, double *s, double *c) {
+    const double k = floor(a * 0x1.45f306dc9c883p-1 + 0.5);
+    const double r = (a - k * 0x1.921fb544p+0) - k * 0x1.0b4611a626331p-34;
+    const double z = r * r;
+    double ps = 0x1.952c77030ad4ap-49;
+    ps = ps * z + -0x1.ae7f3e733b81fp-41;
+    ps = ps * z + 0x1.6124613a86d09p-33;
+    ps = ps * z + -0x1.ae64567f544e4p-26;
+    ps = ps * z + 0x1.71de3a556c734p-19;
+    ps = ps * z + -0x1.a01a01a01a01ap-13;
+    ps = ps * z + 0x1.1111111111111p-7;
+    ps = ps * z + -0x1.5555555555555p-3;
+    const double sr = r + (r * z) * ps;
+    double pc = -0x1.6827863b97d97p-53;
+    pc = pc * z + 0x1.ae7f3e733b81fp-45;
+    pc = pc * z + -0x1.93974a8c07c9dp-37;
+    pc = pc * z + 0x1.1eed8eff8d898p-29;
+    pc = pc * z + -0x1.27e4fb7789f5cp-22;
+    pc = pc * z + 0x1.a01a01a01a01ap-16;
+    pc = pc * z + -0x1.6c16c16c16c17p-10;
+    pc = pc * z + 0x1.5555555555555p-5;
+    const double cr = (1.0 - 0.5 * z) + (z * z) * pc;
+    FL(43);
+    switch (((long long)k) & 3) {
+        case 0: *s = sr; *c = cr; break;
+        case 1: *s = cr; *c = -sr; break;
+        case 2: *s = -sr; *c = -cr; break;
+        default: *s = -cr; *c = sr; break;
+    }
+}
+
 /* ========================================================================== */
 /* S1: UC subproblem by dynamic programming (Section III-B, Algorithm 2).      */
 /* ========================================================================== */
@@ -414,7 +458,13 @@ void orc_branch_flows(const double *y, const double *x, double *f, double *J, do
     double Bii = y[4], Bij = y[5], Bji = y[6], Bjj = y[7];
     double wi = x[0], wj = x[1], d = x[2] - x[3];
     double R = sqrt(wi * wj);
-    double C = R * cos(d), S = R * sin(d);
+    double sn, cs;
+    orc_sincos(d, &sn, &cs);
+    double C = R * cs, S = R * sn;
+    /* flops: R, d, C, S 5 (+ 43 sincos); f 28; with J, H the textbook tables: dC, dS 8, HC/HS 34,
+     * J 56, H 192 (R55) */
+    FL(5 + 28);
+    if (J || H) FL(8 + 34 + (J ? 56 : 0) + (H ? 192 : 0));
     double dC[4] = {C / (2.0 * wi), C / (2.0 * wj), -S, S};
     double dS[4] = {S / (2.0 * wi), S / (2.0 * wj), C, -C};
     double HC[4][4], HS[4][4];
@@ -456,12 +506,14 @@ void orc_branch_flows(const double *y, const double *x, double *f, double *J, do
 typedef void (*eval_fn)(void *ctx, const double *x, double *f, double *g, double *H);
 
 static double dot(int n, const double *a, const double *b) {
+    FL(2 * n);
     double s = 0.0;
     for (int i = 0; i < n; i++) s = s + a[i] * b[i];
     return s;
 }
-static double nrm2(int n, const double *a) { return sqrt(dot(n, a, a)); }
+static double nrm2(int n, const double *a) { FL(1); return sqrt(dot(n, a, a)); }
 static void matvec(int n, const double *H, const double *v, double *o) {
+    FL(2 * n * n);
     for (int i = 0; i < n; i++) {
         double s = 0.0;
         for (int j = 0; j < n; j++) s = s + H[i * n + j] * v[j];
@@ -472,6 +524,7 @@ static void matvec(int n, const double *H, const double *v, double *o) {
 static double qmodel(int n, const double *g, const double *H, const double *s) {
     double Hs[MAXN];
     matvec(n, H, s, Hs);
+    FL(2);
     return dot(n, g, s) + 0.5 * dot(n, s, Hs);
 }
 
@@ -480,12 +533,15 @@ static double qmodel(int n, const double *g, const double *H, const double *s) {
 static const double TR_MU0 = 0.01, TR_ETA0 = 1e-4, TR_ETA1 = 0.25, TR_ETA2 = 0.75;
 static const double TR_SIG1 = 0.25, TR_SIG3 = 4.0, TR_DELTA0 = 1.0, TR_CGTOL = 1e-12;
 static const double TR_EPSF = 1e-10, TR_STALL = 1e-13;   /* R48 */
+static const double TR_STALL_R34 = 1e-14;                  /* R34, the plain mode */
 
 static void pstep(int n, const double *x, const double *lo, const double *hi,
                   const double *d, double a, double *s) {
+    FL(3 * n);
     for (int i = 0; i < n; i++) s[i] = clampd(x[i] + a * d[i], lo[i], hi[i]) - x[i];
 }
 static int cauchy_ok(int n, const double *g, const double *H, const double *s, double delta) {
+    FL(1);
     return nrm2(n, s) <= delta && qmodel(n, g, H, s) <= TR_MU0 * dot(n, g, s);
 }
 static void cauchy(int n, const double *x, const double *lo, const double *hi,
@@ -497,6 +553,7 @@ static void cauchy(int n, const double *x, const double *lo, const double *hi,
     if (!cauchy_ok(n, g, H, s, delta)) {
         for (int k = 0; k < 60; k++) {
             a = a * 0.1;
+            FL(1);
             pstep(n, x, lo, hi, mg, a, s);
             if (cauchy_ok(n, g, H, s, delta)) break;
         }
@@ -505,6 +562,7 @@ static void cauchy(int n, const double *x, const double *lo, const double *hi,
             double ap = a;
             for (int i = 0; i < n; i++) sp[i] = s[i];
             a = a * 10.0;
+            FL(1);
             pstep(n, x, lo, hi, mg, a, s);
             int same = 1;
             for (int i = 0; i < n; i++) if (s[i] != sp[i]) same = 0;
@@ -521,6 +579,7 @@ static void cauchy(int n, const double *x, const double *lo, const double *hi,
 static double bnd_tau(int n, const double *a, const double *p, double delta) {
     double aa = dot(n, a, a), ap = dot(n, a, p), pp = dot(n, p, p);
     if (pp <= 0.0) return 0.0;
+    FL(8);
     double gap = delta * delta - aa;
     if (gap < 0.0) gap = 0.0;
     double rad = sqrt(ap * ap + pp * gap);
@@ -540,29 +599,36 @@ static void steihaug(int n, const double *H, const double *gq, const int *fr,
     double rr = dot(n, r, r);
     if (rr == 0.0) return;
     double tol2 = TR_CGTOL * TR_CGTOL * rr;
+    FL(2);
     for (int k = 0; k < n; k++) {
         matvec(n, H, p, Hp);
         for (int i = 0; i < n; i++) if (!fr[i]) Hp[i] = 0.0;
         double kap = dot(n, p, Hp);
         for (int i = 0; i < n; i++) t[i] = sc[i] + w[i];
+        FL(n);
         if (kap <= 0.0) {
             double tau = bnd_tau(n, t, p, delta);
             for (int i = 0; i < n; i++) w[i] = w[i] + tau * p[i];
+            FL(2 * n);
             return;
         }
         double a = rr / kap;
         for (int i = 0; i < n; i++) t[i] = sc[i] + w[i] + a * p[i];
+        FL(1 + 3 * n);
         if (nrm2(n, t) >= delta) {
             for (int i = 0; i < n; i++) t[i] = sc[i] + w[i];
             double tau = bnd_tau(n, t, p, delta);
             for (int i = 0; i < n; i++) w[i] = w[i] + tau * p[i];
+            FL(3 * n);
             return;
         }
         for (int i = 0; i < n; i++) { w[i] = w[i] + a * p[i]; r[i] = r[i] - a * Hp[i]; }
+        FL(4 * n);
         double rn = dot(n, r, r);
         if (rn <= tol2) return;
         double b = rn / rr;
         for (int i = 0; i < n; i++) p[i] = r[i] + b * p[i];
+        FL(1 + 2 * n);
         rr = rn;
     }
 }
@@ -573,6 +639,7 @@ static void prsrch(int n, const double *x, const double *lo, const double *hi,
     double gq[MAXN], Hs[MAXN], ds[MAXN];
     matvec(n, H, sc, Hs);
     for (int i = 0; i < n; i++) gq[i] = g[i] + Hs[i];
+    FL(n);
     double qc = qmodel(n, g, H, sc);
     double b = 1.0;
     for (int k = 0; k < 20; k++) {
@@ -580,13 +647,16 @@ static void prsrch(int n, const double *x, const double *lo, const double *hi,
             s[i] = clampd(x[i] + sc[i] + b * w[i], lo[i], hi[i]) - x[i];
             ds[i] = s[i] - sc[i];
         }
+        FL(5 * n + 2);
         if (qmodel(n, g, H, s) <= qc + TR_MU0 * dot(n, gq, ds)) return;
         b = b * 0.5;
+        FL(1);
     }
     for (int i = 0; i < n; i++) s[i] = sc[i];
 }
 static double pgnorm(int n, const double *x, const double *g, const double *lo,
                      const double *hi) {
+    FL(2 * n);
     double m = 0.0;
     for (int i = 0; i < n; i++) {
         double v = fabs(clampd(x[i] - g[i], lo[i], hi[i]) - x[i]);
@@ -594,26 +664,29 @@ static double pgnorm(int n, const double *x, const double *g, const double *lo,
     }
     return m;
 }
+/* plain = 1: the first-order reading of SURVEY 8(c) S3 with none of the solver accelerations
+ * R41 (first Cauchy trial = model minimiser) or R48 (stall step 1e-13; plain keeps R34's 1e-14) */
 static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn ev, void *ctx,
-                  double gtol, int maxit, int *iters, double delta0);
+                  double gtol, int maxit, int *iters, double delta0, int plain);
 static int tron(int n, double *x, const double *lo, const double *hi, eval_fn ev, void *ctx,
                 double gtol, int maxit, int *iters) {
-    return tron_r(n, x, lo, hi, ev, ctx, gtol, maxit, iters, TR_DELTA0);
+    return tron_r(n, x, lo, hi, ev, ctx, gtol, maxit, iters, TR_DELTA0, 0);
 }
 static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn ev, void *ctx,
-                  double gtol, int maxit, int *iters, double delta0) {
+                  double gtol, int maxit, int *iters, double delta0, int plain) {
     double f, g[MAXN], H[MAXN * MAXN], fn, gn[MAXN], Hn[MAXN * MAXN];
     double sc[MAXN], w[MAXN], s[MAXN], xn[MAXN], gq[MAXN], Hs[MAXN];
     int fr[MAXN];
+    const double stall = plain ? TR_STALL_R34 : TR_STALL;
     for (int i = 0; i < n; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     ev(ctx, x, &f, g, H);
     double delta = delta0, alpha = 1.0;
-    {
+    if (!plain) {
         /* first Cauchy trial length: the model minimiser along -g (R41) */
         double Hg[MAXN];
         matvec(n, H, g, Hg);
         double gHg = dot(n, g, Hg), gg = dot(n, g, g);
-        if (gHg > 0.0 && gg > 0.0) alpha = gg / gHg;
+        if (gHg > 0.0 && gg > 0.0) { alpha = gg / gHg; FL(1); }
     }
     int it;
     for (it = 0; it < maxit; it++) {
@@ -625,6 +698,7 @@ static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn 
         }
         matvec(n, H, sc, Hs);
         for (int i = 0; i < n; i++) gq[i] = g[i] + Hs[i];
+        FL(2 * n);
         steihaug(n, H, gq, fr, sc, delta, w);
         prsrch(n, x, lo, hi, g, H, sc, w, s);
         /* stall: a step below 1e-13 (1 + |x|) means the rounding floor of the gradient is reached;
@@ -632,16 +706,20 @@ static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn 
         {
             double xm = 0.0;
             for (int i = 0; i < n; i++) xm = dmax(xm, fabs(x[i]));
-            if (nrm2(n, s) <= TR_STALL * (1.0 + xm)) { *iters = it; return 1; }
+            FL(2);
+            if (nrm2(n, s) <= stall * (1.0 + xm)) { *iters = it; return 1; }
         }
         double pred = -qmodel(n, g, H, s);
         for (int i = 0; i < n; i++) xn[i] = clampd(x[i] + s[i], lo[i], hi[i]);
         ev(ctx, xn, &fn, gn, Hn);
         double ared = f - fn;
+        FL(n + 1);
         /* when the predicted reduction is below the rounding level of f, f - fn is noise:
          * use the trapezoidal estimate -(g + gn)'s / 2 instead. */
-        if (fabs(pred) <= TR_EPSF * fabs(f)) ared = -0.5 * (dot(n, g, s) + dot(n, gn, s));
+        if (fabs(pred) <= TR_EPSF * fabs(f)) { ared = -0.5 * (dot(n, g, s) + dot(n, gn, s)); FL(2); }
+        FL(1);
         double ratio = (pred > 0.0) ? ared / pred : -1.0;
+        FL(pred > 0.0);
         double snorm = nrm2(n, s);
         if (ratio > TR_ETA0) {
             for (int i = 0; i < n; i++) x[i] = xn[i];
@@ -649,8 +727,8 @@ static int tron_r(int n, double *x, const double *lo, const double *hi, eval_fn 
             memcpy(g, gn, sizeof(double) * n);
             memcpy(H, Hn, sizeof(double) * n * n);
         }
-        if (ratio < TR_ETA1) delta = TR_SIG1 * dmin(snorm, delta);
-        else if (ratio > TR_ETA2) delta = dmax(delta, TR_SIG3 * snorm);
+        if (ratio < TR_ETA1) { delta = TR_SIG1 * dmin(snorm, delta); FL(1); }
+        else if (ratio > TR_ETA2) { delta = dmax(delta, TR_SIG3 * snorm); FL(1); }
     }
     *iters = it;
     return pgnorm(n, x, g, lo, hi) <= gtol;
@@ -687,6 +765,8 @@ static void br_eval(void *vc, const double *X, double *fo, double *g, double *H)
     int n = c->al ? 6 : 4;
     double f[4], J[16], Hf[64];
     orc_branch_flows(c->y, X, f, J, Hf);
+    /* flops (R55): flow rows 4 x 97, va rows 8 each, AL 2 x 334 (dense 6x6 Hessian terms) */
+    FL(4 * 97 + 8 * c->nva + (c->al ? 2 * 334 : 0));
     double F = 0.0;
     for (int i = 0; i < n; i++) g[i] = 0.0;
     for (int i = 0; i < n * n; i++) H[i] = 0.0;
@@ -748,6 +828,7 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
     for (int m = 0; m < 2; m++) {
         int kp = 2 * m, kq = 2 * m + 1;
         for (int a = 0; a < 4; a++) J[m][a] = 2.0 * (f[kp] * Jf[kp * 4 + a] + f[kq] * Jf[kq * 4 + a]) / c->r2;
+        FL(4 * 5);
         J[m][4] = m == 0 ? 1.0 : 0.0;
         J[m][5] = m == 1 ? 1.0 : 0.0;
     }
@@ -759,12 +840,14 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
     for (int j = 0; j < nf; j++) {
         double d = H[idx[j] * 6 + idx[j]];
         for (int k = 0; k < j; k++) d = d - L[j * 6 + k] * L[j * 6 + k];
+        FL(2 * j + 1);
         if (!(d > 0.0)) return 0;
         L[j * 6 + j] = sqrt(d);
         for (int i = j + 1; i < nf; i++) {
             double v = H[idx[i] * 6 + idx[j]];
             for (int k = 0; k < j; k++) v = v - L[i * 6 + k] * L[j * 6 + k];
             L[i * 6 + j] = v / L[j * 6 + j];
+            FL(2 * j + 1);
         }
     }
     /* V_m = H_FF^{-1} J_m,F by forward and back substitution; M_mn = J_m,F . V_n */
@@ -781,6 +864,7 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
             for (int k = i + 1; k < nf; k++) v = v - L[k * 6 + i] * V[m][k];
             V[m][i] = v / L[i * 6 + i];
         }
+        FL(2 * nf * nf);
     }
     double M[2][2];
     for (int m = 0; m < 2; m++)
@@ -788,6 +872,7 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
             double v = 0.0;
             for (int i = 0; i < nf; i++) v = v + J[m][idx[i]] * V[n][i];
             M[m][n] = v;
+            FL(2 * nf);
         }
     /* Spectral safeguard: in each eigen-direction v of M (eigenvalue lam in (0, 1/sigma]) take
      * the Newton factor 1/lam where lam >= 1/(C sigma), and the first-order factor sigma where M
@@ -797,15 +882,18 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
     double mean = 0.5 * (a + d), half = 0.5 * (a - d);
     double r = sqrt(half * half + b * b);
     double lam[2] = {mean + r, mean - r};
+    FL(13);
     double v[2][2];
     if (r == 0.0) {
         v[0][0] = 1.0; v[0][1] = 0.0;
     } else if (a >= d) {
         double n = sqrt((lam[0] - d) * (lam[0] - d) + b * b);
         v[0][0] = (lam[0] - d) / n; v[0][1] = b / n;
+        FL(9);
     } else {
         double n = sqrt(b * b + (lam[0] - a) * (lam[0] - a));
         v[0][0] = b / n; v[0][1] = (lam[0] - a) / n;
+        FL(9);
     }
     v[1][0] = -v[0][1]; v[1][1] = v[0][0];
     dmu[0] = 0.0;
@@ -815,20 +903,28 @@ static int al_newton_dmu(bctx *c, const double *X, const double *lo, const doubl
         double ph = v[e][0] * h[0] + v[e][1] * h[1];
         dmu[0] = dmu[0] + fac * ph * v[e][0];
         dmu[1] = dmu[1] + fac * ph * v[e][1];
+        FL(3 + 3 + 4);
     }
     /* first-order move of the round's minimiser with mu (R43): dX_F = -H_FF^{-1} J_F' dmu */
     for (int i = 0; i < 6; i++) dx[i] = 0.0;
     for (int i = 0; i < nf; i++) dx[idx[i]] = -(V[0][i] * dmu[0] + V[1][i] * dmu[1]);
+    FL(3 * nf);
     return 1;
 }
 
 /* One branch solve (R9/R10/R12): TRON on the 4-variable box; if the rate is
  * 0 (unlimited) or both ends satisfy Eq. 2c-2d, done (thermal multipliers 0).  Otherwise
- * method of multipliers on the 6-variable slack form, warm-starting (mu, sigma). */
+ * method of multipliers on the 6-variable slack form, warm-starting (mu, sigma).
+ * pr->plain = 1 switches off every solver acceleration (R41-R44, R48, R49): the first-order
+ * AL of SURVEY 8(c) S3 with R36's sigma rule -- the plain twin that pins the accelerated path
+ * (tests/test_oracle_branch.py::test_plain_and_accelerated_al_same_kkt_point).
+ * stats: 0 TRON iterations, 1 TRON capped, 2 AL active, 3 AL rounds, 4 AL capped,
+ *        5 flops of the fast path, 6 flops of the AL, 7 fast-path Newton its, 8 AL Newton its (R55). */
 void orc_branch_solve(const double *y, const double *wlo, const double *whi, double rate,
                       const double *tau, double rpq, double rva, const orc_params *pr,
                       double *x, double *al, double *f, int64_t *stats) {
     const double TWO_PI = 6.283185307179586;
+    const int plain = pr->plain != 0;
     double lo[6] = {wlo[0], wlo[1], -TWO_PI, -TWO_PI, 0.0, 0.0};
     double hi[6] = {whi[0], whi[1], TWO_PI, TWO_PI, 1.0, 1.0};
     /* NEXT-3 variant 8 (R51): no angle consensus rows; the line's angles are local,
@@ -840,6 +936,7 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
     c.nva = (pr->variant & 8) ? 2 : 4;
     c.r2 = rate * rate; c.mu[0] = c.mu[1] = 0.0; c.sig = 0.0;
     int it = 0;
+    const double fl0 = g_fl;
     /* NEXT-3 variant 1 (R47): every rated branch goes straight to the six-variable AL from the
      * warm start (clipped to the box), as ExaTron solves it; else the 4-variable fast path first */
     const int al_always = (pr->variant & 1) && rate > 0.0;
@@ -850,15 +947,19 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
     if (al_always)
         for (int i = 0; i < 4; i++) x[i] = clampd(x[i], lo[i], hi[i]);
     else
-        ok = tron(4, x, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it);
+        ok = tron_r(4, x, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it, TR_DELTA0, plain);
     stats[0] = it; stats[1] = !ok; stats[2] = 0; stats[3] = 0; stats[4] = 0;
+    stats[7] = it; stats[8] = 0;
     double sig0 = pr->al_sigma0_rel * rpq * c.r2;
     orc_branch_flows(y, x, f, NULL, NULL);
+    const double fl1 = g_fl;
+    stats[5] = (int64_t)(fl1 - fl0); stats[6] = 0;
     if (rate > 0.0) {
         double s1 = f[0] * f[0] + f[1] * f[1], s2 = f[2] * f[2] + f[3] * f[3];
         if (al_always || s1 > c.r2 || s2 > c.r2) {
             double X[6] = {x[0], x[1], x[2], x[3],
                            clampd(1.0 - s1 / c.r2, 0.0, 1.0), clampd(1.0 - s2 / c.r2, 0.0, 1.0)};
+            FL(6 + 4);
             c.al = 1;
             c.mu[0] = al[0]; c.mu[1] = al[1];
             c.sig = dmax(sig0, al[2] * pr->al_sigma_decay);
@@ -866,7 +967,7 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
             double hprev = INFINITY;
             int k;
             stats[2] = 1;
-            {
+            if (!plain) {
                 /* R49: round 1 starts from whichever of the fast-path point and the previous
                  * iterate (each with its slacks from its flows) has the lower AL value */
                 double fp[4], Xp[6], Fa, Fb, gs[6], Hs[36];
@@ -874,6 +975,7 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
                 for (int i = 0; i < 4; i++) Xp[i] = xprev[i];
                 Xp[4] = clampd(1.0 - (fp[0] * fp[0] + fp[1] * fp[1]) / c.r2, 0.0, 1.0);
                 Xp[5] = clampd(1.0 - (fp[2] * fp[2] + fp[3] * fp[3]) / c.r2, 0.0, 1.0);
+                FL(10);
                 br_eval(&c, X, &Fa, gs, Hs);
                 br_eval(&c, Xp, &Fb, gs, Hs);
                 if (Fb < Fa)
@@ -882,32 +984,40 @@ void orc_branch_solve(const double *y, const double *wlo, const double *whi, dou
             for (k = 0; k < pr->al_maxit; k++) {
                 /* round 1 starts at the fast-path point, which violates Eq. 2c-2d: a small first
                  * trust region (R44) keeps the first model step where sigma h^2 is modelled well */
-                ok = tron_r(6, X, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it, k == 0 ? AL_R1_DELTA0 : TR_DELTA0);
+                const double d0 = (k == 0 && !plain) ? AL_R1_DELTA0 : TR_DELTA0;
+                ok = tron_r(6, X, lo, hi, br_eval, &c, gtol, pr->tron_maxit, &it, d0, plain);
                 stats[0] += it;
+                stats[8] += it;
                 stats[1] += !ok;
                 orc_branch_flows(y, X, f, NULL, NULL);
                 double h1 = (f[0] * f[0] + f[1] * f[1]) / c.r2 - 1.0 + X[4];
                 double h2 = (f[2] * f[2] + f[3] * f[3]) / c.r2 - 1.0 + X[5];
+                FL(12);
                 double hm = dmax(fabs(h1), fabs(h2));
                 if (hm <= pr->al_eta_star) break;
                 double hv[2] = {h1, h2}, dmu[2], dx[6];
-                if (al_newton_dmu(&c, X, lo, hi, hv, dmu, dx)) {
+                if (!plain && al_newton_dmu(&c, X, lo, hi, hv, dmu, dx)) {
 #ifndef ORC_NO_PREDICTOR
                     for (int i = 0; i < 6; i++) X[i] = clampd(X[i] + dx[i], lo[i], hi[i]);
+                    FL(6);
 #endif
                 } else {
+                    /* first-order method of multipliers (Nocedal-Wright 17.4), R36 */
                     dmu[0] = c.sig * h1;
                     dmu[1] = c.sig * h2;
+                    FL(2);
                 }
                 c.mu[0] = c.mu[0] + dmu[0];
                 c.mu[1] = c.mu[1] + dmu[1];
-                if (hm > 0.25 * hprev) c.sig = dmin(10.0 * c.sig, smax);
+                FL(3);
+                if (hm > 0.25 * hprev) { c.sig = dmin(10.0 * c.sig, smax); FL(1); }
                 hprev = hm;
             }
             stats[3] = k < pr->al_maxit ? k + 1 : k;
             stats[4] = k >= pr->al_maxit;
             for (int i = 0; i < 4; i++) x[i] = X[i];
             al[0] = c.mu[0]; al[1] = c.mu[1]; al[2] = c.sig;
+            stats[6] = (int64_t)(g_fl - fl1);
             return;
         }
     }
@@ -1161,7 +1271,8 @@ static void one_iteration(orc_ctx *c) {
         }
     }
     /* ---- (7b) x^OPF: branches ("six variables", P:456 ExaTron) ---- */
-    int64_t tit = 0, tcap = 0, alact = 0, alcap = 0;
+    int64_t tit = 0, tcap = 0, alact = 0, alcap = 0, nfast = 0, nal = 0;
+    double ffast = 0.0, fal = 0.0;
     for (int l = 0; l < L; l++) {
         int bi = q->br_from[l], bj = q->br_to[l];
         double wlo[2] = {q->bus_vmin[bi] * q->bus_vmin[bi], q->bus_vmin[bj] * q->bus_vmin[bj]};
@@ -1174,13 +1285,17 @@ static void one_iteration(orc_ctx *c) {
             tau[5] = c->wbar[(size_t)bj * T + t] - ZB(W_J, i) - YB(W_J, i) / rva;
             tau[6] = c->thbar[(size_t)bi * T + t] - ZB(A_I, i) - YB(A_I, i) / rva;
             tau[7] = c->thbar[(size_t)bj * T + t] - ZB(A_J, i) - YB(A_J, i) / rva;
-            int64_t st[5];
+            int64_t st[9];
             orc_branch_solve(q->br_y + 8 * l, wlo, whi, q->br_rate[l], tau, rpq, rva, pr,
                              c->x + 4 * i, c->al + 3 * i, c->f + 4 * i, st);
             tit += st[0];
             tcap += st[1];
             alact += st[2];
             alcap += st[4];
+            ffast += (double)st[5];
+            fal += (double)st[6];
+            nfast += st[7];
+            nal += st[8];
         }
     }
     memcpy(c->u, unew, GT);
@@ -1392,6 +1507,7 @@ static void one_iteration(orc_ctx *c) {
     rp->primal_inf = nm.pinf; rp->rz_inf = nm.rzinf; rp->rz_2 = sqrt(nm.rz2);
     rp->z_inf = nm.zinf; rp->z_2 = sqrt(nm.z2); rp->dual_inf = nm.dinf; rp->objective = obj;
     rp->tron_iters += tit; rp->tron_capped += tcap; rp->al_active += alact; rp->al_capped += alcap;
+    rp->flops_fast = ffast; rp->flops_al = fal; rp->newton_fast = nfast; rp->newton_al = nal;
 
     /* ---- S8 inner test, S9 outer update (Alg. 1 line 10; R20-R22) ---- */
     if (pr->outer_enabled && c->inner_since >= pr->inner_min) {
@@ -1462,4 +1578,8 @@ void orc_set_state(orc_ctx *c, const orc_state *s) {
     memcpy(c->wbar, s->wbar, D * BT); memcpy(c->thbar, s->thbar, D * BT);
     c->beta = s->scal[0]; c->znorm_prev = s->scal[1]; c->outer_k = (int64_t)s->scal[2];
     c->inner_total = (int64_t)s->scal[3]; c->inner_since = (int64_t)s->scal[4];
+}
+
+void orc_get_slacks(const orc_ctx *c, double *sl) {
+    memcpy(sl, c->sl, sizeof(double) * 6 * (size_t)c->pb.ngen * c->pb.T);
 }

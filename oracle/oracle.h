@@ -50,12 +50,18 @@ typedef struct {
     int32_t uc_fixed;   /* 1: step (7a) keeps u (the NEXT-2 warm start's multiperiod ACOPF) */
     int32_t variant;    /* NEXT-3 formulation variants (bitmask, R47): 1 = every rated branch solves the
                            six-variable AL (no fast path), 2 = wbar clipped to [Vmin^2, Vmax^2] */
+    int32_t plain;      /* 1: the branch solver without the accelerations R41-R44, R48, R49 (the plain
+                           first-order AL that pins the accelerated one; oracle only) */
 } orc_params;
 
 typedef struct {
     double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective, beta;
     int64_t inner_total, outer_total, tron_iters, tron_capped, al_active, al_capped;
     int32_t inner_since_outer, outer_k;
+    /* the last iteration's branch solves (R55): algorithmic flops and Newton iterations of the
+     * 4-variable fast path and of the 6-variable AL */
+    double flops_fast, flops_al;
+    int64_t newton_fast, newton_al;
 } orc_report;
 
 /* Canonical state (section 4 of DESIGN.md).  Row kinds:
@@ -106,8 +112,9 @@ void orc_boxqp3(int32_t n, int32_t m, const double *c, const double *e, double *
 void orc_bus_kkt(int32_t k, const double *alpha, const double *beta, const double *a,
                  const double *tauhat, double P, double Q, double *v, double *mu);
 /* S3 branch solve.  y[8] admittance, lo/hi[2] w bounds (i,j), rate (0=unlimited),
- * tau[8] row targets, x[4] in/out, al[3] in/out, f[4] out, stats[5] out
- * (tron iterations, tron capped, al active, al iterations, al capped). */
+ * tau[8] row targets, x[4] in/out, al[3] in/out, f[4] out, stats[9] out
+ * (tron iterations, tron capped, al active, al iterations, al capped, flops fast path,
+ * flops AL, Newton its fast path, Newton its AL). */
 void orc_branch_solve(const double *y, const double *wlo, const double *whi, double rate,
                       const double *tau, double rho_pq, double rho_va, const orc_params *pr,
                       double *x, double *al, double *f, int64_t *stats);
@@ -117,6 +124,10 @@ int orc_tron_quadratic(int32_t n, const double *A, const double *b, const double
 /* Flows of one branch (Eq. 2e-2h) and derivative tables, for finite-difference pins. */
 void orc_branch_flows(const double *y, const double *x, double *f, double *J /*[16]*/,
                       double *H /*[64]*/);
+/* sin and cos by the explicit polynomial of R54 (the flows' only transcendental). */
+void orc_sincos(double a, double *s, double *c);
+/* the generator slacks of the current x (s^pl s^pu s^ql s^qu s^rd s^ru per (g,t), [6*ngen*T]) */
+void orc_get_slacks(const orc_ctx *c, double *sl);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,7 @@
 // switch-window sums and the per-(g,t) generator x-update (t = lane, lane+32, ...); the
 // backward recursion of Algorithm 2 is inherently sequential in t and runs on
 // lane 0 over a shared-memory table (O(T) with 2 states).
+#include <mutex>
 #include <algorithm>
 
 #include "ucac_dev.cuh"
@@ -433,6 +434,13 @@ __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const i
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x * (blockDim.x >> 5) + warp;
     if (g >= G) return;
+    // on-device inputs are not validated by the host: an out-of-range instance gets a NaN cost and
+    // an all-zero schedule instead of indexing past its shared-memory slice (ucac.h ucac_dp_batch)
+    if (tu[g] < 1 || tu[g] > T || td[g] < 1 || td[g] > T || hold[g] < 0 || hold[g] > T || (u0[g] != 0 && u0[g] != 1)) {
+        for (int t = lane; t < T; t += 32) sched[(size_t)g * T + t] = 0;
+        if (lane == 0) cost[g] = __longlong_as_double(0x7ff8000000000000ll);
+        return;
+    }
     DpSmem s = dp_carve(smem + (size_t)warp * dp_smem_bytes(T), T);
     for (int k = lane; k < T * 4; k += 32) s.L[k] = L[(size_t)g * T * 4 + k];
     __syncwarp();
@@ -537,11 +545,19 @@ void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s) {
 }
 
 size_t gen_smem_bytes(int T) { return gen_smem(T, 4); }
+// The attribute is process-wide per kernel: only ever raise it, so a later context or dp_batch
+// with a smaller T never lowers the limit under a live larger-T context.
 cudaError_t gen_set_smem_attr(int T) {
-    size_t b = gen_smem(T, 4);
+    static std::mutex mu;
+    static size_t cur = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    const size_t b = gen_smem(T, 4);
+    if (b <= cur) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    e = cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    if (e == cudaSuccess) cur = b;
+    return e;
 }
 
 }  // namespace ucac

@@ -398,6 +398,15 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         } else if (partition_buses(net->nbus, net->nbranch, net->br_from, net->br_to, dist->bus_xy, nranks, part.data())) {
             return fail(nullptr, UCAC_EINVAL, "partitioner failed");
         }
+        // every rank checks every part (the partition is global and deterministic), so a part
+        // without generators or branches fails on all ranks together, before any of them enters
+        // ncclCommInitRank and waits there for the others
+        std::vector<int> ng(nranks, 0), nl(nranks, 0);
+        for (int g = 0; g < net->ngen; g++) ng[part[net->gen_bus[g]]]++;
+        for (int l = 0; l < net->nbranch; l++) nl[part[net->br_from[l]]]++;
+        for (int r = 0; r < nranks; r++)
+            if (ng[r] == 0 || nl[r] == 0)
+                return fail(nullptr, UCAC_EUNSUPPORTED, "part %d owns no generator or no branch; use fewer ranks", r);
     }
     ucac_ctx *ctx = new ucac_ctx();
     ctx->prm = *prm;
@@ -826,6 +835,9 @@ extern "C" ucac_status ucac_set_rho(ucac_ctx *ctx, double rho_pq, double rho_va,
     d.rpq = rho_pq; d.rva = rho_va; d.ruc = rho_uc;
     d.irpq = 1.0 / rho_pq; d.irva = 1.0 / rho_va; d.iruc = 1.0 / rho_uc;
     d.tron_gtol = prm.tron_gtol_rel * std::max(rho_pq, rho_va);
+    // the pipelined tail DP (k_gen tail) already ran the next (7a) with the old rho_uc: drop it
+    CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
     // the graphs captured the old Dev by value: re-instantiate them
     for (auto &g : ctx->gexec)
         if (g) {

@@ -260,3 +260,79 @@ def test_branch_al_kkt_multipliers(seed, variant):
         else:
             assert al[m] >= -1e-6 * scale
     assert st[3] <= 6 and st[0] <= 40 + 20 * variant, st
+
+
+def test_sincos_polynomial_against_libm():
+    """R54: the oracle's explicit sin/cos polynomial (shared operation sequence with the strict_fp
+    GPU build) is within 2 ulp of libm on [-4 pi, 4 pi] (the range of theta_i - theta_j over the
+    box [-2 pi, 2 pi]^2), exact at 0, and odd/even."""
+    rng = np.random.default_rng(54)
+    a = np.concatenate([rng.uniform(-4 * np.pi, 4 * np.pi, 20000), rng.normal(0, 0.3, 20000),
+                        np.arange(-8, 9) * np.pi / 2 + rng.normal(0, 1e-3, 17), [0.0, 1e-300, -1e-8, 0.7853981633974483]])
+    worst = 0.0
+    for v in a:
+        s, c = oracle.sincos(v)
+        rs, rc = np.sin(v), np.cos(v)
+        # error in ulps of the larger of the value and 1e-16 (|sin| near k pi is limited by the
+        # absolute accuracy of the argument reduction, ~1e-26)
+        es = abs(s - rs) / np.spacing(max(abs(rs), 1e-16))
+        ec = abs(c - rc) / np.spacing(max(abs(rc), 1e-16))
+        worst = max(worst, es, ec)
+        s2, c2 = oracle.sincos(-v)
+        assert s2 == -s and c2 == c
+    assert worst <= 2.0, worst
+    assert oracle.sincos(0.0) == (0.0, 1.0)
+
+
+def _harvest(name, iters):
+    """every (l,t) branch-solve input of the oracle's next iteration at its state after `iters`
+    iterations (targets tau = xbar - z - y/rho, warm x, AL state)"""
+    pb, pr = inputs.build_config(name)
+    pb = pb.normalized()
+    o = oracle.Oracle(pb, pr)
+    o.iterate(iters)
+    st = o.get_state()
+    o.close()
+    L, T = pb.nbranch, pb.T
+    LT = L * T
+    zb, yb = st["zb"].reshape(8, LT), st["yb"].reshape(8, LT)
+    fb, x, al = st["fbar"].reshape(LT, 4), st["x"].reshape(LT, 4), st["al"].reshape(LT, 3)
+    wb, tb = st["wbar"].reshape(pb.nbus, T), st["thbar"].reshape(pb.nbus, T)
+    rho = np.array([pr.rho_pq] * 4 + [pr.rho_va] * 4)
+    for l in range(L):
+        i, j = pb.br_from[l], pb.br_to[l]
+        for t in range(T):
+            k = l * T + t
+            xb = np.array([fb[k, 0], fb[k, 1], fb[k, 2], fb[k, 3], wb[i, t], wb[j, t], tb[i, t], tb[j, t]])
+            tau = xb - zb[:, k] - yb[:, k] / rho
+            yield pr, (pb.br_y[l], [pb.bus_vmin[i] ** 2, pb.bus_vmin[j] ** 2],
+                       [pb.bus_vmax[i] ** 2, pb.bus_vmax[j] ** 2], pb.br_rate[l], tau, x[k].copy(), al[k].copy())
+
+
+def test_plain_and_accelerated_al_same_kkt_point():
+    """The accelerated branch solver (R41-R44, R48, R49: solver engineering, not readings of the
+    paper) and the plain first-order AL of SURVEY 8(c) S3 (oracle plain mode) reach the same KKT
+    point on every solve of the case300 and pegase-shaped configs' states: x within 1e-11, the
+    flows within 1e-9 relative, the thermal multipliers within 10 sigma eta* (the AL stops at
+    |h| <= eta*, so mu is only defined to sigma eta*).  All thermally active solves
+    are compared, plus every 20th inactive one."""
+    n_al = n_fast = 0
+    its = np.zeros(2)
+    for name, iters in (("case300", 20), ("pegase2869", 3)):
+        for k, (pr, (y, lo, hi, rate, tau, x0, al0)) in enumerate(_harvest(name, iters)):
+            xa, ala, fa, sa = oracle.branch_solve(y, lo, hi, rate, tau, pr.rho_pq, pr.rho_va, pr, x0, al0)
+            if sa[2] == 0 and k % 20:
+                continue
+            xp, alp, fp, sp = oracle.branch_solve(y, lo, hi, rate, tau, pr.rho_pq, pr.rho_va, pr, x0, al0, plain=True)
+            assert sa[1] == 0 and sp[1] == 0 and sp[2] == sa[2] and sp[4] == 0
+            assert np.max(np.abs(xa - xp)) <= 1e-11, (name, k, xa, xp)
+            assert np.max(np.abs(fa - fp)) <= 1e-9 * max(1.0, np.max(np.abs(fa))), (name, k)
+            if sa[2]:
+                sig = max(ala[2], alp[2])
+                assert np.max(np.abs(ala[:2] - alp[:2])) <= 10 * sig * pr.al_eta_star + 1e-9 * np.max(np.abs(ala[:2])), (name, k, ala, alp)
+                n_al += 1
+                its += (sa[8], sp[8])
+            else:
+                n_fast += 1
+    assert n_al + n_fast >= 1000 and n_al >= 250, (n_al, n_fast)
+    assert its[0] < its[1]   # the accelerations cut the AL's Newton iterations

@@ -84,22 +84,8 @@ def test_stage_cost_spec():
     assert L[0, 1, 1] == 0.0
 
 
-def test_stage_cost_definition():
-    """L_t(a,b) = c0 b + CSU su + CSD sd + sum_v y_v(x_v - ub_v + z_v) + rho/2 (...)^2."""
-    rng = np.random.default_rng(3)
-    T = 5
-    ub, y, z = rng.uniform(0, 1, (3, T)), rng.normal(size=(3, T)), rng.normal(size=(3, T)) * 0.1
-    c0, csu, csd, rho = 7.0, 11.0, 3.0, 2.5
-    L = oracle.stage_costs(T, c0, csu, csd, rho, ub, y, z)
-    for t in range(T):
-        for a in (0, 1):
-            for b in (0, 1):
-                x = [b, max(0, b - a), max(0, a - b)]
-                ref = c0 * b + csu * x[1] + csd * x[2]
-                for v in range(3):
-                    e = x[v] - ub[v, t] + z[v, t]
-                    ref += y[v, t] * e + 0.5 * rho * e * e
-                assert L[t, a, b] == pytest.approx(ref, rel=1e-14, abs=1e-14)
+# The stage cost's definition is pinned against the full augmented Lagrangian in
+# tests/test_oracle_al_pins.py::test_stage_cost_equals_full_al_difference.
 
 
 @pytest.mark.parametrize("seed", range(6))
