@@ -108,6 +108,11 @@ typedef struct {
                            its own angle difference; thetabar is not updated,
                            16 = the literal Eq. 5f ramp-down row R_D ubar^on_{t-1} + S_D ubar^su_t
                            (R52) instead of Eq. 4d's R_D ubar^on_t + S_D ubar^sd_t */
+    int32_t strict_fp;  /* 1 = strict parity mode: the branch solves run the plain
+                           oracle algorithm (k_strict.cu) and every quotient is the IEEE quotient, no
+                           FMA contraction, sin/cos by the explicit polynomial of R54 -- the iterate
+                           then equals the CPU oracle's bit for bit (up to the order of the S8 sums,
+                           which feed only the inner/outer decisions).  Slower; for parity runs. */
 } ucac_params;
 
 /* Multi-GPU (bus-graph cut).  NULL = single GPU.
@@ -189,6 +194,8 @@ typedef struct {
     int64_t al_tron_iters;            /* TRON iterations inside thermal-AL solves (part of tron_iters) */
     int32_t inner_since_outer, outer_k;
     int32_t err_kernel, err_iter;     /* first non-finite: kernel id + 1 (0 = none), iteration */
+    int32_t err_comp, err_period;     /* ... and where: the component (global generator, branch or
+                                         bus index, by the kernel's kind) and the period (0-based) */
 } ucac_report;
 ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *rep);
 
@@ -248,6 +255,20 @@ typedef struct {
     int64_t alg_bytes[UCAC_NKERNELS];   /* per kernel                                     */
 } ucac_sizes;
 ucac_status ucac_get_sizes(ucac_ctx *ctx, ucac_sizes *sz);
+
+/* Fault injection for the non-finite path: overwrite one element of a row-state
+ * array with NaN, between iterations.  field: 0 = branch-row z, 1 = branch-row y, 2 = generator-row
+ * z, 3 = generator-row y; index in the canonical [kind][comp*T + t] layout of ucac_state (local
+ * components on a multi-rank context).  The next ucac_iterate then returns UCAC_ENUMERIC and
+ * ucac_residuals names the first kernel that met the value (err_kernel, err_comp, err_period,
+ * err_iter).  EINVAL for a bad field or index.  Synchronous.  Test use only. */
+ucac_status ucac_debug_poison(ucac_ctx *ctx, int32_t field, int64_t index);
+
+/* Measured FP64 (non-tensor) pipe peak of the current device, the denominator of the branch
+ * kernels' roofline: a DFMA-chain microbenchmark (8 independent fma chains per
+ * thread, 8 x 256-thread blocks per SM, best of 5 timed launches of 64 x iters DFMA per thread).
+ * *tflops = 2 flop x DFMA count / time; *ms (may be NULL) the best launch time. */
+ucac_status ucac_measure_fp64_peak(int32_t iters, double *tflops, double *ms);
 
 void *ucac_stream(ucac_ctx *ctx);                 /* the cudaStream_t the context runs on */
 const char *ucac_last_error(const ucac_ctx *ctx); /* NULL ctx: last create failure (thread-local) */

@@ -17,31 +17,48 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _HDR = os.path.join(_HERE, "oracle.h")
 _LIB = os.path.join(_HERE, "_build", "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "_build", "liboracle_omp.so")
 _lock = threading.Lock()
 _lib = None
+_lib_omp = None
 
-CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall",
+          "-Wno-unknown-pragmas"]
 
 
 def build(force: bool = False) -> str:
-    """compile liboracle.so with gcc (-O2 -ffp-contract=off, no fast-math)."""
+    """compile liboracle.so with gcc (-O2 -ffp-contract=off, no fast-math, single thread) and the
+    all-core twin liboracle_omp.so (the same source with -fopenmp)."""
     os.makedirs(os.path.dirname(_LIB), exist_ok=True)
-    stale = force or not os.path.exists(_LIB) or any(
-        os.path.getmtime(p) > os.path.getmtime(_LIB) for p in (_SRC, _HDR))
-    if stale:
-        tmp = _LIB + f".{os.getpid()}.tmp"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    for out, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        stale = force or not os.path.exists(out) or any(
+            os.path.getmtime(p) > os.path.getmtime(out) for p in (_SRC, _HDR))
+        if stale:
+            tmp = out + f".{os.getpid()}.tmp"
+            subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, out)
     return _LIB
 
 
-def lib():
-    global _lib
+def lib(omp: bool = False):
+    """the single-thread oracle, or (omp=True) its all-core OpenMP build"""
+    global _lib, _lib_omp
     with _lock:
+        if omp:
+            if _lib_omp is None:
+                build()
+                _lib_omp = C.CDLL(_LIB_OMP)
+                _declare(_lib_omp)
+            return _lib_omp
         if _lib is None:
             _lib = C.CDLL(build())
             _declare(_lib)
     return _lib
+
+
+def threads(n: int = 0) -> int:
+    """threads of the all-core build (n > 0 sets them)"""
+    return lib(omp=True).orc_threads(int(n))
 
 
 dp = C.POINTER(C.c_double)
@@ -124,6 +141,8 @@ def _declare(L):
     L.orc_sincos.restype = None
     L.orc_get_slacks.argtypes = [C.c_void_p, dp]
     L.orc_get_slacks.restype = None
+    L.orc_threads.argtypes = [C.c_int32]
+    L.orc_threads.restype = C.c_int
 
 
 def _p(a, t=dp):
@@ -145,8 +164,9 @@ def params_c(pr, plain: bool = False) -> Params_c:
 class Oracle:
     """One oracle context (Algorithm 1 run on the CPU)."""
 
-    def __init__(self, pb, pr, plain: bool = False):
-        self.L = lib()
+    def __init__(self, pb, pr, plain: bool = False, omp: bool = False):
+        """omp: the all-core build (bitwise the same iterates)"""
+        self.L = lib(omp)
         pb = pb.normalized()
         self.pb = pb
         self.pr = pr

@@ -14,6 +14,9 @@
  */
 #include "oracle.h"
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -1171,18 +1174,25 @@ void orc_destroy(orc_ctx *c) {
 typedef struct { double pinf, rzinf, rz2, zinf, z2, dinf; } norms;
 /* (7e) z = argmin_z L = -(lambda + y + rho r)/(beta + rho), (7f) y += rho(r+z)
  * (P:238); norms for S8. */
+/* the row's S8 terms are returned in rec[4] = (r, r + z, z, rho |dxbar|) and folded into the norms
+ * afterwards in the canonical row order (so the OpenMP build sums in the same order) */
 static void zy_row(double r, double rho, double beta, double *z, double *y, const double *lam,
-                   double dxb, norms *n) {
+                   double dxb, double *rec) {
     double zz = -((*lam + *y) + rho * r) / (beta + rho);
     *z = zz;
     *y = *y + rho * (r + zz);
-    double rz = r + zz;
-    n->pinf = dmax(n->pinf, fabs(r));
-    n->rzinf = dmax(n->rzinf, fabs(rz));
-    n->rz2 = n->rz2 + rz * rz;
-    n->zinf = dmax(n->zinf, fabs(zz));
-    n->z2 = n->z2 + zz * zz;
-    n->dinf = dmax(n->dinf, rho * fabs(dxb));
+    rec[0] = r;
+    rec[1] = r + zz;
+    rec[2] = zz;
+    rec[3] = rho * fabs(dxb);
+}
+static void fold_row(const double *rec, norms *n) {
+    n->pinf = dmax(n->pinf, fabs(rec[0]));
+    n->rzinf = dmax(n->rzinf, fabs(rec[1]));
+    n->rz2 = n->rz2 + rec[1] * rec[1];
+    n->zinf = dmax(n->zinf, fabs(rec[2]));
+    n->z2 = n->z2 + rec[2] * rec[2];
+    n->dinf = dmax(n->dinf, rec[3]);
 }
 
 static void one_iteration(orc_ctx *c) {
@@ -1206,7 +1216,10 @@ static void one_iteration(orc_ctx *c) {
     if (pr->uc_fixed) {
         memcpy(unew, c->u, GT);   /* NEXT-2: the multiperiod ACOPF with the schedule held */
     } else {
+#pragma omp parallel
+        {
         double *Lt = dz((size_t)T * 4), *ub3 = dz((size_t)3 * T), *y3 = dz((size_t)3 * T), *z3 = dz((size_t)3 * T);
+#pragma omp for schedule(static)
         for (int g = 0; g < G; g++) {
             for (int v = 0; v < 3; v++)
                 for (int t = 0; t < T; t++) {
@@ -1227,9 +1240,11 @@ static void one_iteration(orc_ctx *c) {
             orc_dp(T, Lt, q->min_up[g], q->min_dn[g], q->u0[g], q->hold[g], unew + (size_t)g * T);
         }
         free(Lt); free(ub3); free(y3); free(z3);
+        }
     }
 
     /* ---- (7b) x^OPF: generators on iterate l ---- */
+#pragma omp parallel for schedule(static)
     for (int g = 0; g < G; g++) {
         double pL = dmin(0.0, q->pmin[g]), pU = q->pmax[g];
         double qL = dmin(0.0, q->qmin[g]), qU = dmax(0.0, q->qmax[g]);
@@ -1273,6 +1288,8 @@ static void one_iteration(orc_ctx *c) {
     /* ---- (7b) x^OPF: branches ("six variables", P:456 ExaTron) ---- */
     int64_t tit = 0, tcap = 0, alact = 0, alcap = 0, nfast = 0, nal = 0;
     double ffast = 0.0, fal = 0.0;
+    /* integer-valued sums: exact in any order */
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : tit, tcap, alact, alcap, nfast, nal, ffast, fal)
     for (int l = 0; l < L; l++) {
         int bi = q->br_from[l], bj = q->br_to[l];
         double wlo[2] = {q->bus_vmin[bi] * q->bus_vmin[bi], q->bus_vmin[bj] * q->bus_vmin[bj]};
@@ -1303,6 +1320,7 @@ static void one_iteration(orc_ctx *c) {
 
     /* ---- (7c) xbar^UC: ubar per (g, group) on x^{l+1}, u^{l+1} (R19) ---- */
     const int lit5f = (pr->variant & 16) != 0;
+#pragma omp parallel for schedule(static)
     for (int g = 0; g < G; g++) {
         double Pm = q->pmin[g], PM = q->pmax[g], Qm = q->qmin[g], QM = q->qmax[g];
         double RDn = q->ramp_dn[g], SDn = q->sd_ramp[g], RUp = q->ramp_up[g], SUp = q->su_ramp[g];
@@ -1365,7 +1383,10 @@ static void one_iteration(orc_ctx *c) {
             int k = 2 * (c->bg_ptr[i + 1] - c->bg_ptr[i]) + 2 * (c->be_ptr[i + 1] - c->be_ptr[i]) + 1;
             if (k > maxk) maxk = k;
         }
+#pragma omp parallel
+        {
         double *al_ = dz(maxk), *be_ = dz(maxk), *aa = dz(maxk), *th = dz(maxk), *vv = dz(maxk);
+#pragma omp for schedule(static)
         for (int i = 0; i < B; i++) {
             int ne = c->be_ptr[i + 1] - c->be_ptr[i];
             for (int t = 0; t < T; t++) {
@@ -1429,11 +1450,15 @@ static void one_iteration(orc_ctx *c) {
             }
         }
         free(al_); free(be_); free(aa); free(th); free(vv);
+        }
     }
 
     /* ---- (7e) z and (7f) y for every row; S8 norms ---- */
     norms nm = {0, 0, 0, 0, 0, 0};
     double obj = 0.0;
+    /* per-row S8 terms (4 each) and per-(g,t) costs, folded below in the canonical row order */
+    double *grec = dz((size_t)GT * NGR * 4), *brec = dz((size_t)LT * NBR * 4), *gcost = dz(GT);
+#pragma omp parallel for schedule(static)
     for (int g = 0; g < G; g++) {
         double Pm = q->pmin[g], PM = q->pmax[g], Qm = q->qmin[g], QM = q->qmax[g];
         for (int t = 0; t < T; t++) {
@@ -1470,13 +1495,14 @@ static void one_iteration(orc_ctx *c) {
             for (int k = 0; k < NGR; k++) {
                 if (k == RC && t == 0) continue;
                 double rho = (k >= GP) ? rpq : ruc;
-                zy_row(r[k], rho, beta, &ZG(k, i), &YG(k, i), &LG(k, i), dx[k], &nm);
+                zy_row(r[k], rho, beta, &ZG(k, i), &YG(k, i), &LG(k, i), dx[k], grec + (i * NGR + k) * 4);
             }
             double Sp = S * p;
-            obj = obj + (q->c2[g] * Sp * Sp + q->c1[g] * Sp + q->c0[g] * (double)ut
-                         + q->csu[g] * (double)su + q->csd[g] * (double)sd);
+            gcost[i] = q->c2[g] * Sp * Sp + q->c1[g] * Sp + q->c0[g] * (double)ut
+                     + q->csu[g] * (double)su + q->csd[g] * (double)sd;
         }
     }
+#pragma omp parallel for schedule(static)
     for (int l = 0; l < L; l++) {
         int bi = q->br_from[l], bj = q->br_to[l];
         for (int t = 0; t < T; t++) {
@@ -1494,10 +1520,26 @@ static void one_iteration(orc_ctx *c) {
             for (int k = 0; k < NBR; k++) {
                 if ((pr->variant & 8) && (k == A_I || k == A_J)) continue;   /* R51 */
                 double rho = (k < W_I) ? rpq : rva;
-                zy_row(r[k], rho, beta, &ZB(k, i), &YB(k, i), &LB(k, i), dx[k], &nm);
+                zy_row(r[k], rho, beta, &ZB(k, i), &YB(k, i), &LB(k, i), dx[k], brec + (i * NBR + k) * 4);
             }
         }
     }
+    /* S8 norms and the objective (Eq. 1a), sequential in the canonical order: gens (g, t, row
+     * kind), then branches (l, t, row kind) */
+    for (size_t i = 0; i < GT; i++) {
+        int t = (int)(i % (size_t)T);
+        for (int k = 0; k < NGR; k++) {
+            if (k == RC && t == 0) continue;
+            fold_row(grec + (i * NGR + k) * 4, &nm);
+        }
+        obj = obj + gcost[i];
+    }
+    for (size_t i = 0; i < LT; i++)
+        for (int k = 0; k < NBR; k++) {
+            if ((pr->variant & 8) && (k == A_I || k == A_J)) continue;
+            fold_row(brec + (i * NBR + k) * 4, &nm);
+        }
+    free(grec); free(brec); free(gcost);
     for (int k = 0; k < 3; k++) free(ubo[k]);
     free(pbo); free(qbo); free(fbo); free(wbo); free(tbo);
 
@@ -1582,4 +1624,18 @@ void orc_set_state(orc_ctx *c, const orc_state *s) {
 
 void orc_get_slacks(const orc_ctx *c, double *sl) {
     memcpy(sl, c->sl, sizeof(double) * 6 * (size_t)c->pb.ngen * c->pb.T);
+}
+
+/* The all-core build (liboracle_omp.so, -fopenmp): the per-component loops of
+ * each step run in parallel, every reduction (S8 norms, objective) stays sequential in the
+ * canonical order, so its iterates are bitwise those of the single-thread build
+ * (tests/test_oracle_admm.py::test_openmp_build_is_bitwise_the_serial_oracle). */
+int orc_threads(int32_t n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
 }

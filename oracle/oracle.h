@@ -128,6 +128,8 @@ void orc_branch_flows(const double *y, const double *x, double *f, double *J /*[
 void orc_sincos(double a, double *s, double *c);
 /* the generator slacks of the current x (s^pl s^pu s^ql s^qu s^rd s^ru per (g,t), [6*ngen*T]) */
 void orc_get_slacks(const orc_ctx *c, double *sl);
+/* threads of the all-core build (n > 0 sets them); 1 for the single-thread build */
+int orc_threads(int32_t n);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,8 @@ UNITS = {
     "k_branch.cu": ["-fmad=true"],
     "k_gen.cu": ["-fmad=false"],
     "k_sweep.cu": ["-fmad=false"],
+    "k_strict.cu": ["-fmad=false"],
+    "k_measure.cu": [],
     "ucac.cu": [],
     "partition.cu": [],
 }

@@ -775,6 +775,12 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         }
         double C, S, f0, f1, f2, f3;
         F4.flows(x, C, S, f0, f1, f2, f3);
+        {
+            double chk = nf0(f0) + nf0(f1) + nf0(f2) + nf0(f3);
+#pragma unroll
+            for (int r = 0; r < 8; r++) chk += nf0(F4.tau[r]);
+            if (!isfinite(chk)) report_nonfinite(d, K_BRANCH, k / d.T, k - (k / d.T) * d.T);
+        }
         const bool queue = rate > 0.0 && (al_always || f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2);
         unsigned pos = 0;
         if (queue) {
@@ -927,6 +933,8 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
         }
         c_alcap += kk >= d.al_maxit;
         F6.flows(x, C, S, f0, f1, f2, f3);
+        if (!isfinite(nf0(f0) + nf0(f1) + nf0(f2) + nf0(f3) + nf0(mu0) + nf0(mu1)))
+            report_nonfinite(d, K_BRANCH_AL, k / d.T, k - (k / d.T) * d.T);
 #pragma unroll
         for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
         d.f[0 * LTs + k] = f0;

@@ -356,6 +356,9 @@ __global__ void __launch_bounds__(128) k_gen(Dev d, int tail) {
         double ub[3] = {d.ub_on[i], d.ub_su[i], d.ub_sd[i]};
         double yy[3] = {YG(G_DON, i), YG(G_DSU, i), YG(G_DSD, i)};
         double zz[3] = {ZG(G_DON, i), ZG(G_DSU, i), ZG(G_DSD, i)};
+        if (!isfinite(nf0(ub[0]) + nf0(ub[1]) + nf0(ub[2]) + nf0(yy[0]) + nf0(yy[1]) + nf0(yy[2]) + nf0(zz[0]) +
+                      nf0(zz[1]) + nf0(zz[2])))
+            report_nonfinite(d, K_GEN, g, t);
 #pragma unroll
         for (int a = 0; a < 2; a++)
 #pragma unroll
@@ -425,6 +428,9 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
         d.p[i] = po;
         d.q[i] = qo;
         d.ph[i] = pho;
+        if (!isfinite(nf0(in.tp) + nf0(in.tq) + nf0(in.tph) + nf0(in.bpl) + nf0(in.bpu) + nf0(in.bql) + nf0(in.bqu) +
+                      nf0(in.brl) + nf0(in.bru) + nf0(po) + nf0(qo) + nf0(pho)))
+            report_nonfinite(d, K_GENX, g, t);
     }
 }
 

@@ -267,16 +267,29 @@ __device__ __forceinline__ void kernel_tail(const Dev &d, Acc &acc, double *part
 // Split: k_bus (early) takes the bus-periods with no thermal-AL solve at an
 // incident branch end -- their inputs are final after the fast path, so in the single-GPU graph
 // it runs in the shadow of k_branch_al -- and k_late the marked ones after the AL tail.
+// STRICT (strict_fp parity mode): the oracle's quotients y/rho, mu/rho and /(beta + rho)
+// instead of products with reciprocals, so the bus and row updates are the oracle's bits
 struct Ctl {
-    double rpq, rva, irpq, beta, beta_lam, lmax, ibpq, ibva;
+    double rpq, rva, irpq, beta, beta_lam, lmax, ibpq, ibva, bpq, bva;
     int pending;
     unsigned stamp;
     __device__ explicit Ctl(const Dev &d)
         : rpq(d.rpq), rva(d.rva), irpq(d.irpq), beta(d.st->beta), beta_lam(d.st->beta_lam), lmax(d.lambda_max),
-          ibpq(1.0 / (beta + d.rpq)), ibva(1.0 / (beta + d.rva)), pending(d.st->pending_outer), stamp(mark_stamp(d)) {}
+          ibpq(1.0 / (beta + d.rpq)), ibva(1.0 / (beta + d.rva)), bpq(beta + d.rpq), bva(beta + d.rva),
+          pending(d.st->pending_outer), stamp(mark_stamp(d)) {}
 };
+template <bool STRICT>
+__device__ __forceinline__ double over_rho(double v, double rho, double irho) { return STRICT ? v / rho : v * irho; }
+// (7e)/(7f) of one row with the reciprocal (default) or the oracle's quotient (STRICT)
+template <bool STRICT>
+__device__ __forceinline__ void zy_s(double r, double rho, double ib, double bpr, double &z, double &y, double &lam,
+                                     int pending, double beta_lam, double lmax, double dxb, Acc &a) {
+    if (STRICT) zy_vals(r, rho, 0.0, z, y, lam, pending, beta_lam, lmax, dxb, a, bpr);
+    else zy_vals(r, rho, ib, z, y, lam, pending, beta_lam, lmax, dxb, a);
+}
 
 // bus-period k = i*T + t of an owned bus (ghost buses are solved by their owner)
+template <bool STRICT>
 __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc &acc) {
     const int T = d.T;
     const size_t GT = (size_t)d.G * T, BT = (size_t)d.B * T;
@@ -296,10 +309,10 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
 #pragma unroll 2
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
-            const double tgp = d.p[gi] + ZG(G_GP, gi) + YG(G_GP, gi) * irpq;
+            const double tgp = d.p[gi] + ZG(G_GP, gi) + over_rho<STRICT>(YG(G_GP, gi), rpq, irpq);
             double th, aa;
             if (t < T - 1) {
-                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + YG(G_RC, gi + 1) * irpq;
+                const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + over_rho<STRICT>(YG(G_RC, gi + 1), rpq, irpq);
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
             } else {
@@ -308,7 +321,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
             }
             AP = AP + 1.0 / aa;
             rP = rP - th;
-            const double thq = d.q[gi] + ZG(G_GQ, gi) + YG(G_GQ, gi) * irpq;
+            const double thq = d.q[gi] + ZG(G_GQ, gi) + over_rho<STRICT>(YG(G_GQ, gi), rpq, irpq);
             AQ = AQ + irpq;
             rQ = rQ - thq;
         }
@@ -339,6 +352,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
         const double det = AP * AQ - C * C;
         const double muP = (rP * AQ - C * rQ) / det;
         const double muQ = (AP * rQ - C * rP) / det;
+        if (!isfinite(muP + muQ)) report_nonfinite(d, K_BUS, i, t);
         // ---- generator copies and their rows (each gen: all loads, then the updates, then the stores)
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
@@ -353,10 +367,10 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
                 yr = YG(G_RC, gi + 1);
                 lr = LG(G_RC, gi + 1);
             }
-            const double tgp = pg + zp + yp * irpq;
+            const double tgp = pg + zp + over_rho<STRICT>(yp, rpq, irpq);
             double th, aa;
             if (rc) {
-                const double trc = phn + zr + yr * irpq;
+                const double trc = phn + zr + over_rho<STRICT>(yr, rpq, irpq);
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
             } else {
@@ -364,11 +378,11 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
                 aa = rpq;
             }
             const double pb = th + muP / aa;
-            const double thq = qg + zq + yq * irpq;
-            const double qb = thq + muQ * irpq;
-            zy_vals(pg - pb, rpq, ibpq, zp, yp, lp, pending, beta_lam, lmax, pb - pbo, acc);
-            zy_vals(qg - qb, rpq, ibpq, zq, yq, lq, pending, beta_lam, lmax, qb - qbo, acc);
-            if (rc) zy_vals(phn - pb, rpq, ibpq, zr, yr, lr, pending, beta_lam, lmax, pb - pbo, acc);
+            const double thq = qg + zq + over_rho<STRICT>(yq, rpq, irpq);
+            const double qb = thq + over_rho<STRICT>(muQ, rpq, irpq);
+            zy_s<STRICT>(pg - pb, rpq, ibpq, c.bpq, zp, yp, lp, pending, beta_lam, lmax, pb - pbo, acc);
+            zy_s<STRICT>(qg - qb, rpq, ibpq, c.bpq, zq, yq, lq, pending, beta_lam, lmax, qb - qbo, acc);
+            if (rc) zy_s<STRICT>(phn - pb, rpq, ibpq, c.bpq, zr, yr, lr, pending, beta_lam, lmax, pb - pbo, acc);
             d.pbar[gi] = pb;
             d.qbar[gi] = qb;
             ZG(G_GP, gi) = zp;
@@ -405,15 +419,18 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
 // branch end at bus i (they need only this bus's result; a bus is marked iff all its ends are),
 // so the end rows need no kernel of their own.  Consecutive threads are consecutive t of one bus,
 // so each end's row accesses stay coalesced.
+template <bool STRICT>
 __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int t, int side, Acc &acc);
+template <bool STRICT>
 __device__ __forceinline__ void bus_end_rows(const Dev &d, const Ctl &c, int k, Acc &acc) {
     const int i = k / d.T, t = k - i * d.T;
     for (int a = d.be_ptr[i]; a < d.be_ptr[i + 1]; a++) {
         const int code = d.be_idx[a];
-        end_rows(d, c, code >> 1, t, code & 1, acc);
+        end_rows<STRICT>(d, c, code >> 1, t, code & 1, acc);
     }
 }
 
+template <bool STRICT>
 __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     TL_KERNEL(K_BUS);
     if (d.st->done) return;
@@ -421,14 +438,15 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc;
     if (k < d.B_own * d.T && d.bmark[k] != c.stamp) {
-        bus_solve(d, c, k, acc);
-        if (d.fuse_rows) bus_end_rows(d, c, k, acc);
+        bus_solve<STRICT>(d, c, k, acc);
+        if (d.fuse_rows) bus_end_rows<STRICT>(d, c, k, acc);
     }
     block_reduce_store(acc, d.part_bus);
 }
 
 // The four rows of branch end (l, side) at period t -- flow copies fbar = tauhat - mu/rho_pq,
 // then (7e)/(7f) for FP, FQ, W, A of that end -- need only that end's bus result.
+template <bool STRICT>
 __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int t, int side, Acc &acc) {
     const int T = d.T;
     const size_t LT = (size_t)d.L * T, BT = (size_t)d.B * T;
@@ -452,13 +470,15 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
         y[r] = YB(rows[r], k);
         lam[r] = LB(rows[r], k);
     }
-    const double pb = thp + (-muP) * c.irpq;
-    const double qb = thq + (-muQ) * c.irpq;
-    zy_vals(fp - pb, c.rpq, c.ibpq, z[0], y[0], lam[0], c.pending, c.beta_lam, c.lmax, pb - pbo, acc);
-    zy_vals(fq - qb, c.rpq, c.ibpq, z[1], y[1], lam[1], c.pending, c.beta_lam, c.lmax, qb - qbo, acc);
-    zy_vals(xw - wb, c.rva, c.ibva, z[2], y[2], lam[2], c.pending, c.beta_lam, c.lmax, dwb, acc);
+    const double pb = thp + over_rho<STRICT>(-muP, c.rpq, c.irpq);
+    const double qb = thq + over_rho<STRICT>(-muQ, c.rpq, c.irpq);
+    zy_s<STRICT>(fp - pb, c.rpq, c.ibpq, c.bpq, z[0], y[0], lam[0], c.pending, c.beta_lam, c.lmax, pb - pbo, acc);
+    zy_s<STRICT>(fq - qb, c.rpq, c.ibpq, c.bpq, z[1], y[1], lam[1], c.pending, c.beta_lam, c.lmax, qb - qbo, acc);
+    zy_s<STRICT>(xw - wb, c.rva, c.ibva, c.bva, z[2], y[2], lam[2], c.pending, c.beta_lam, c.lmax, dwb, acc);
     if (!(d.variant & 8))   // R51: without angle rows their z, y, lambda stay 0
-        zy_vals(xa - tb, c.rva, c.ibva, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
+        zy_s<STRICT>(xa - tb, c.rva, c.ibva, c.bva, z[3], y[3], lam[3], c.pending, c.beta_lam, c.lmax, dtb, acc);
+    if (!isfinite(nf0(z[0]) + nf0(z[1]) + nf0(z[2]) + nf0(z[3]) + nf0(y[0]) + nf0(y[1]) + nf0(y[2]) + nf0(y[3])))
+        report_nonfinite(d, K_ROWS, l, t);
     FB(kp, k) = pb;
     FB(kq, k) = qb;
 #pragma unroll
@@ -473,6 +493,7 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
 
 // k_rows (early): one thread per (l,t), the ends whose bus is not marked (coalesced row
 // arrays, as k_branch); the marked ends are done by k_rows_late.
+template <bool STRICT>
 __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
     TL_KERNEL(K_ROWS);
     if (d.st->done) return;
@@ -481,8 +502,8 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
     Acc acc;
     if (k < d.L * d.T) {
         const int l = k / d.T, t = k - l * d.T;
-        if (d.rmark[0][k] != c.stamp) end_rows(d, c, l, t, 0, acc);
-        if (d.rmark[1][k] != c.stamp) end_rows(d, c, l, t, 1, acc);
+        if (d.rmark[0][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 0, acc);
+        if (d.rmark[1][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 1, acc);
     }
     block_reduce_store(acc, d.part_rows);
 }
@@ -491,6 +512,7 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
 // the marked ends (k_bus_late: 1024-thread blocks, few partial slots, so the final fold is short;
 // k_rows_late: 256-thread blocks, one wave grid-striding over (l,t)).
 // Single GPU: k_rows_late is the last kernel of the iteration (final = 1).
+template <bool STRICT>
 __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
     pdl_wait();
     TL_KERNEL(K_BUS_LATE);
@@ -500,8 +522,8 @@ __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
     // the control values (two divisions) only for the marked few: most late threads skip
     if (k < d.B_own * d.T && d.bmark[k] == mark_stamp(d)) {
         const Ctl c(d);
-        bus_solve(d, c, k, acc);
-        if (d.fuse_rows) bus_end_rows(d, c, k, acc);
+        bus_solve<STRICT>(d, c, k, acc);
+        if (d.fuse_rows) bus_end_rows<STRICT>(d, c, k, acc);
     }
     // fused rows: this is the iteration's last kernel and does the final fold
     kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, d.fuse_rows != 0);
@@ -554,6 +576,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold_early(Dev d) {
     fold_slots(d.part_efold, gridDim.x, d.rec_part + RK_EARLY * NPART);
 }
 
+template <bool STRICT>
 __global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
     pdl_wait();
     TL_KERNEL(K_ROWS_LATE);
@@ -566,8 +589,8 @@ __global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
         if (m0 || m1) {   // the control values (two divisions) only for the marked few
             const Ctl c(d);
             const int l = k / d.T, t = k - l * d.T;
-            if (m0) end_rows(d, c, l, t, 0, acc);
-            if (m1) end_rows(d, c, l, t, 1, acc);
+            if (m0) end_rows<STRICT>(d, c, l, t, 0, acc);
+            if (m1) end_rows<STRICT>(d, c, l, t, 1, acc);
         }
     }
     kernel_tail(d, acc, d.part_lrows, RK_ROWS_LATE, final != 0);
@@ -747,6 +770,11 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         }
         double v[3];
         boxqp3(n, m, cm, e, v);
+        {
+            double chk = nf0(v[0]) + nf0(v[1]) + nf0(v[2]);
+            for (int q2 = 0; q2 < m; q2++) chk = chk + nf0(e[q2]);
+            if (!isfinite(chk)) report_nonfinite(d, K_UBAR, g, t);
+        }
         const double on_n = v[0], sd_n = v[1];
         // rows of the group with the new ubar (r = x-part - c'ubar)
         const double don = on_n - on_o, dsd = sd_n - sd_o;
@@ -952,16 +980,20 @@ static void launch_sweep(bool hi, void (*k)(KArgs...), dim3 g, dim3 b, cudaStrea
     if (hi) launch_hi_prio(k, g, b, 0, s, args...);
     else k<<<g, b, 0, s>>>(args...);
 }
-void launch_bus(const Dev &d, cudaStream_t s) { launch_sweep(UCAC_SWEEP_PRIO, k_bus, dim3(d.nblk_bus), dim3(BUS_THREADS), s, d); }
-void launch_rows(const Dev &d, cudaStream_t s) { launch_sweep(UCAC_SWEEP_PRIO, k_rows, dim3(d.nblk_rows), dim3(ROWS_THREADS), s, d); }
+void launch_bus(const Dev &d, cudaStream_t s) {
+    launch_sweep(UCAC_SWEEP_PRIO, d.strict ? k_bus<true> : k_bus<false>, dim3(d.nblk_bus), dim3(BUS_THREADS), s, d);
+}
+void launch_rows(const Dev &d, cudaStream_t s) {
+    launch_sweep(UCAC_SWEEP_PRIO, d.strict ? k_rows<true> : k_rows<false>, dim3(d.nblk_rows), dim3(ROWS_THREADS), s, d);
+}
 #ifndef UCAC_LATE_PRIO
 #define UCAC_LATE_PRIO 1
 #endif
 // the late kernels at high priority: when the AL tail frees its SMs, k_bus_late's full-SM blocks
 // take them ahead of k_rows' pending blocks
 void launch_bus_late(const Dev &d, cudaStream_t s) {
-    launch_ex(k_bus_late, dim3(d.nblk_lbus), dim3(LBUS_THREADS), 0, s, UCAC_SWEEP_PRIO || UCAC_LATE_PRIO,
-              (pdl_mask() & 2) != 0, d);
+    launch_ex(d.strict ? k_bus_late<true> : k_bus_late<false>, dim3(d.nblk_lbus), dim3(LBUS_THREADS), 0, s,
+              UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, (pdl_mask() & 2) != 0, d);
 }
 void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
     // One wave: at most (resident blocks per SM) x SMs blocks, grid-striding over the (l,t) range.
@@ -975,12 +1007,12 @@ void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_late, LROWS_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_late<false>, LROWS_THREADS, 0);
         return std::max(1, sms * per_sm);
     }();
     const int g = lrows_cap > 0 ? std::min(d.nblk_lrows, lrows_cap) : d.nblk_lrows;
-    launch_ex(k_rows_late, dim3(g), dim3(LROWS_THREADS), 0, s, UCAC_SWEEP_PRIO || UCAC_LATE_PRIO,
-              (pdl_mask() & 4) != 0, d, final);
+    launch_ex(d.strict ? k_rows_late<true> : k_rows_late<false>, dim3(g), dim3(LROWS_THREADS), 0, s,
+              UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, (pdl_mask() & 4) != 0, d, final);
 }
 int nblk_lbus(int n) { return (n + LBUS_THREADS - 1) / LBUS_THREADS; }
 int nblk_lrows(int n) { return (n + LROWS_THREADS - 1) / LROWS_THREADS; }

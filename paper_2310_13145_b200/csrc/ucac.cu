@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <limits>
 #include <vector>
 
 #include "ucac.h"
@@ -482,6 +483,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.uc_fixed = prm->uc_fixed;
     d.fuse_rows = (nranks == 1 && UCAC_FUSE_ROWS) ? 1 : 0;
     d.variant = prm->variant;
+    d.strict = prm->strict_fp != 0;
     d.nblk_bus = nblk_bus(P.Bo, T);
     d.nblk_ubar = nblk_ubar(G, T);
     d.nblk_rows = nblk_rows(L, T);
@@ -661,7 +663,7 @@ static const int kOrder[NKERN] = {K_GEN, K_GENX, K_BRANCH, K_BUS, K_ROWS, K_BRAN
 
 static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
     switch (k) {
-        case K_BRANCH: launch_branch(ctx->d, s); break;
+        case K_BRANCH: if (ctx->d.strict) launch_branch_strict(ctx->d, s); else launch_branch(ctx->d, s); break;
         case K_BRANCH_AL: launch_branch_al(ctx->d, s); break;
         case K_GEN: launch_gen(ctx->d, s); break;
         case K_GENX: launch_genx(ctx->d, s); break;
@@ -971,6 +973,16 @@ extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kern
     return UCAC_OK;
 }
 
+// the component of a non-finite report as a global index of the kernel's component kind
+static int32_t err_global_comp(const ucac_ctx *ctx, int err_kernel, int comp) {
+    if (!err_kernel || comp < 0) return -1;
+    const int k = err_kernel - 1;
+    const std::vector<int> &v = (k == K_BRANCH || k == K_BRANCH_AL || k == K_ROWS || k == K_ROWS_LATE)
+                                    ? ctx->P.branch_global
+                                    : (k == K_BUS || k == K_BUS_LATE) ? ctx->P.bus_global : ctx->P.gen_global;
+    return comp < (int)v.size() ? v[comp] : comp;
+}
+
 extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
     if (!ctx || !r) return UCAC_EINVAL;
     ucac_status s = pull_status(ctx);
@@ -995,6 +1007,8 @@ extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
     r->outer_k = (int32_t)h->outer_k;
     r->err_kernel = h->err_kernel;
     r->err_iter = h->err_iter;
+    r->err_comp = err_global_comp(ctx, h->err_kernel, h->err_comp);
+    r->err_period = h->err_kernel ? h->err_period : -1;
     if (h->err_kernel) return fail(ctx, UCAC_ENUMERIC, "non-finite iterate at iteration %d", h->err_iter);
     return UCAC_OK;
 }
@@ -1109,6 +1123,9 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     h->pending_outer = 0;
     h->done = 0;
     h->err_kernel = 0;
+    h->err_iter = 0;
+    h->err_comp = -1;
+    h->err_period = -1;
     CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
     CK(cudaMemsetAsync(d.cnt, 0, NCNT * sizeof(unsigned long long), ctx->s));
     CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));   // the pipelined DP result is stale
@@ -1329,3 +1346,18 @@ extern "C" int ucac_debug_timeline(ucac_ctx *ctx, unsigned long long *host, int 
     return (int)cudaMemcpy(host, ctx->d.tl, 2 * NKERN * 8, cudaMemcpyDeviceToHost);
 }
 #endif
+
+extern "C" ucac_status ucac_debug_poison(ucac_ctx *ctx, int32_t field, int64_t index) {
+    if (!ctx) return UCAC_EINVAL;
+    const Dev &d = ctx->d;
+    const int64_t GT = (int64_t)ctx->G * ctx->T, LT = (int64_t)ctx->L * ctx->T;
+    double *base = field == 0 ? d.zb : field == 1 ? d.yb : field == 2 ? d.zg : field == 3 ? d.yg : nullptr;
+    const int64_t n = field < 2 ? NBROW * LT : NGROW * GT;
+    if (!base || index < 0 || index >= n) return fail(ctx, UCAC_EINVAL, "poison: field %d index %lld", field, (long long)index);
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    CK(cudaStreamSynchronize(ctx->s));
+    CK(cudaMemcpyAsync(base + index, &nan, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));   // the pipelined DP read the old value
+    CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}

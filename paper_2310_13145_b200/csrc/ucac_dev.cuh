@@ -41,7 +41,8 @@ struct DevStatus {
     int pending_outer;    // lambda <- clip(lambda + beta_lam z) to apply at the next sweep
     int done;             // stop_on_primal reached: kernels return immediately
     int stop_on_primal;
-    int err_kernel, err_iter;
+    int err_kernel, err_iter;         // first non-finite value: kernel id + 1, iteration (1-based)
+    int err_comp, err_period;         // ... its component (rank-local index) and period
     int pad_;
     double primal_target;
     double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective;
@@ -62,6 +63,7 @@ struct Dev {
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
     int uc_fixed;                     // 1: k_gen keeps u (NEXT-2)
     int variant;                      // NEXT-3 bitmask: 1 = AL for every rated branch, 2 = wbar clip
+    int strict;                       // strict_fp parity mode: oracle quotients / operation order (k_strict.cu)
 
     // ---- static generator data [G]
     const int *gbus, *tu, *td, *u0, *hold;
@@ -150,6 +152,18 @@ struct TlGuard {
 #endif
 
 __host__ __device__ inline size_t gi(const Dev &d, int g, int t) { return (size_t)g * d.T + t; }
+
+// SPEC S:322 non-finite handling: the first kernel that meets a NaN/inf records (kernel,
+// component, period, iteration); ucac_iterate / ucac_residuals then return UCAC_ENUMERIC
+__device__ __forceinline__ void report_nonfinite(const Dev &d, int kid, int comp, int t) {
+    if (atomicCAS(&d.st->err_kernel, 0, kid + 1) == 0) {
+        d.st->err_comp = comp;
+        d.st->err_period = t;
+        d.st->err_iter = (int)d.st->inner_total + 1;
+    }
+}
+// 0 for finite v, NaN otherwise: sums of these flag a non-finite operand
+__device__ __forceinline__ double nf0(double v) { return v * 0.0; }
 // per-iteration stamp of bmark (read before k_reduce advances inner_total; never 0)
 __device__ __forceinline__ unsigned mark_stamp(const Dev &d) { return (unsigned)(d.st->inner_total + 1); }
 
@@ -159,6 +173,7 @@ __device__ __forceinline__ unsigned mark_stamp(const Dev &d) { return (unsigned)
 namespace ucac {
 void launch_branch(const Dev &d, cudaStream_t s);
 void launch_branch_al(const Dev &d, cudaStream_t s);
+void launch_branch_strict(const Dev &d, cudaStream_t s);
 // Launch with the device's highest execution priority (a launch attribute, kept by graph capture):
 // the generator chain (k_gen, k_genx, k_ubar) forks at the start of the iteration and should take
 // SM slots as k_branch blocks retire rather than queue behind them.

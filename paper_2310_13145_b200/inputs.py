@@ -187,6 +187,7 @@ class Params:
     al_sigma_decay: float = 0.1
     uc_fixed: int = 0          # 1: step (7a) keeps u (NEXT-2 warm start's multiperiod ACOPF)
     variant: int = 0           # NEXT-3 bitmask: 1 = AL for every rated branch (no fast path), 2 = wbar clip
+    strict_fp: int = 0         # 1: strict parity mode (oracle operation order / quotients, R54 sin/cos)
 
 
 # --------------------------------------------------------------------------------------

@@ -59,7 +59,8 @@ class Params(C.Structure):
                 ("inner_min", C.c_int32), ("inner_cap", C.c_int32), ("outer_enabled", C.c_int32),
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
-                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32)]
+                ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32),
+                ("strict_fp", C.c_int32)]
 
 
 class Dist(C.Structure):
@@ -75,7 +76,8 @@ class Report(C.Structure):
                 ("tron_capped", C.c_int64), ("al_active", C.c_int64), ("al_capped", C.c_int64),
                 ("al_tron_iters", C.c_int64),
                 ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32),
-                ("err_kernel", C.c_int32), ("err_iter", C.c_int32)]
+                ("err_kernel", C.c_int32), ("err_iter", C.c_int32),
+                ("err_comp", C.c_int32), ("err_period", C.c_int32)]
 
 
 class Solution(C.Structure):
@@ -165,12 +167,17 @@ def _declare(L):
     L.ucac_iterate_group.restype = C.c_int
     L.ucac_local_map.argtypes = [C.c_void_p, C.c_int32, ip, ip]
     L.ucac_local_map.restype = C.c_int
+    L.ucac_debug_poison.argtypes = [C.c_void_p, C.c_int32, C.c_int64]
+    L.ucac_debug_poison.restype = C.c_int
+    L.ucac_measure_fp64_peak.argtypes = [C.c_int32, dp, dp]
+    L.ucac_measure_fp64_peak.restype = C.c_int
 
 
 EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed", "ucac_kernel_name", "ucac_residuals",
             "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
-            "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start"]
+            "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start",
+            "ucac_debug_poison", "ucac_measure_fp64_peak"]
 
 
 def _check(rc, h=None):
@@ -183,7 +190,7 @@ def params_struct(pr) -> Params:
     return Params(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max, pr.beta_max,
                   pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled, pr.tron_gtol_rel,
                   pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel, pr.al_sigma_max_rel,
-                  pr.al_sigma_decay, pr.uc_fixed, pr.variant)
+                  pr.al_sigma_decay, pr.uc_fixed, pr.variant, pr.strict_fp)
 
 
 def problem_structs(pb, keep: list):
@@ -287,6 +294,18 @@ class Context:
         """NEXT-4(b), R53: new penalty classes between iterations (ucac_set_rho)."""
         _check(self.L.ucac_set_rho(self.h, float(rho_pq), float(rho_va), float(rho_uc)), self.h)
 
+    def poison(self, field: str, index: int):
+        """fault injection (ucac_debug_poison): NaN into one element of zb / yb / zg / yg"""
+        _check(self.L.ucac_debug_poison(self.h, {"zb": 0, "yb": 1, "zg": 2, "yg": 3}[field], int(index)), self.h)
+
+    def report_raw(self) -> dict:
+        """ucac_residuals without raising on UCAC_ENUMERIC (the err_* fields say where)"""
+        r = Report()
+        rc = self.L.ucac_residuals(self.h, C.byref(r))
+        d = {n: getattr(r, n) for n, _ in Report._fields_}
+        d["status"] = STATUS.get(rc, rc)
+        return d
+
     def iterate_timed(self, n: int):
         ms = np.zeros(NKERNELS)
         cnt = np.zeros(NKERNELS, dtype=np.int64)
@@ -337,6 +356,13 @@ class Context:
         d = {n: getattr(s, n) for n, _ in Sizes._fields_ if n != "alg_bytes"}
         d["alg_bytes"] = dict(zip(KERNELS, list(s.alg_bytes)))
         return d
+
+
+def measure_fp64_peak(iters: int = 4096) -> dict:
+    """ucac_measure_fp64_peak: the DFMA-chain FP64 peak of the current device"""
+    tf, ms = C.c_double(), C.c_double()
+    _check(lib().ucac_measure_fp64_peak(int(iters), C.byref(tf), C.byref(ms)), None)
+    return {"tflops": tf.value, "ms": ms.value, "iters": int(iters)}
 
 
 def dp_batch(L, min_up, min_dn, u0, hold):

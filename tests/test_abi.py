@@ -18,7 +18,7 @@ HDR = os.path.join(ROOT, "include", "ucac.h")
 def declared_functions():
     txt = open(HDR).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(ucac_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(ucac_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -408,3 +408,19 @@ def test_set_rho_equals_fresh_context_next4():
         assert np.array_equal(sa[k], sb[k]), k
     a.close()
     b.close()
+
+
+def test_openmp_build_is_bitwise_the_serial_oracle():
+    """the all-core oracle (liboracle_omp.so, the same source with -fopenmp,
+    per-component loops in parallel, reductions sequential in the canonical order) produces the
+    single-thread oracle's iterates bit for bit."""
+    import oracle
+    from paper_2310_13145_b200 import inputs
+    pb, pr = inputs.build_config("case30")
+    a, b = oracle.Oracle(pb, pr), oracle.Oracle(pb, pr, omp=True)
+    oracle.threads(4)
+    a.iterate(25)
+    b.iterate(25)
+    sa, sb = a.get_state(), b.get_state()
+    assert all(sa[k].tobytes() == sb[k].tobytes() for k in sa)
+    assert a.report() == b.report()
