@@ -29,11 +29,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ADMM iters/sec & branch-subproblem solves/sec; time-to-residual 1e-4, 1/2/4/8 B200"
 UNIT = "ADMM inner iterations/s"
-# FP64 flops per TRON Newton iteration of the two branch kernels: lane-level SASS counts of the
-# same launches (2 DFMA + DADD + DMUL) / the Newton iterations the solver counted in them
-# (tools/calibrate_flops.py; profiles/r01/flops_calibration.json).  The AL figure includes the
-# per-round work (Hessian at the round start, multiplier update) amortised over its iterations.
-FLOPS_PER_NEWTON_FAST = 717.0    # profiles/r01/flops_calibration.json (ncu SASS count, current code)
+# SASS-executed FP64 flops per TRON Newton iteration of the two branch kernels: lane-level SASS
+# counts of the same launches (2 DFMA + DADD + DMUL) / the Newton iterations the solver counted in
+# them (tools/calibrate_flops.py; profiles/r01/flops_calibration.json) -- reported beside the
+# algorithmic figure (the oracle's counted flops of the same solves, R55), which sets roofline.frac.
+FLOPS_PER_NEWTON_FAST = 717.0
 FLOPS_PER_NEWTON_AL = 2147.0
 
 
@@ -127,10 +127,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": self.src}
 
 
-def oracle_sample(pb, pr, steps: int, budget_s: float):
-    """time the oracle (single thread, as it stands) on a bounded number of iterations."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(pb, pr, steps: int, budget_s: float, omp: bool = False):
+    """time the oracle (as it stands; single thread, or its all-core OpenMP build) on a bounded
+    number of iterations."""
     import oracle
-    o = oracle.Oracle(pb, pr)
+    o = oracle.Oracle(pb, pr, omp=omp)
     t0 = time.perf_counter()
     n = 0
     while n < steps:
@@ -150,7 +161,10 @@ def run_reference(args, pb, pr, rank, world):
         return
     import numpy as np  # noqa: F401
     import oracle
-    o = oracle.Oracle(pb, pr)
+    # the all-core build of the oracle (same source with OpenMP over the components of each step,
+    # reductions in canonical order: bitwise the single-thread iterates) on every host core
+    ncores = oracle.threads(os.cpu_count() or 1)
+    o = oracle.Oracle(pb, pr, omp=True)
     for _ in range(args.warmup):
         o.iterate(1)
     # a bounded sample: at most REF_BUDGET_S seconds of timed oracle iterations (the oracle runs
@@ -171,9 +185,9 @@ def run_reference(args, pb, pr, rank, world):
         "data": "synthetic (seeded, paper_2310_13145_b200.inputs)",
         "config": {"workload": f"{args.config} (B={pb.nbus}, G={pb.ngen}, L={pb.nbranch}, T={pb.T})",
                    "rows": pb.nrows(), "branch_solves_per_step": pb.nbranch * pb.T, "l2": "n/a (CPU)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncores, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"{len(times)} timed inner iterations (of {args.steps} requested, {REF_BUDGET_S:.0f} s cap) after {args.warmup} warm-up, "
-                                   f"single-threaded C oracle (-O2 -ffp-contract=off)"},
+                                   f"C oracle, all-core OpenMP build (-O2 -ffp-contract=off -fopenmp, {ncores} threads)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "branch_solves_per_s": v * pb.nbranch * pb.T,
     }
@@ -347,6 +361,10 @@ def main():
     ap.add_argument("--config", default="pegase2869")
     ap.add_argument("--T", type=int, default=None, help="override the config's horizon (SURVEY 8(a) stress: pegase T=168)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cut", default="bus", choices=["bus", "time"],
+                    help="N > 1: bus-graph cut (DESIGN.md 9, default) or time cut (NEXT-4(c))")
+    ap.add_argument("--selfcheck-iters", type=int, default=10,
+                    help="N > 1: iterations of the rank-assembled vs 1-GPU bitwise self-check (0 = off)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--workload", default="admm", choices=["admm", "dp", "warmstart"],
                     help="admm: the inner-iteration hot path (default); dp: NEXT-1 batched UC DP; "
@@ -386,7 +404,7 @@ def main():
             return None
         obj = [ucac.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        return {"rank": rank, "nranks": world, "comm_mode": 0, "nccl_id": obj[0]}
+        return {"rank": rank, "nranks": world, "comm_mode": 0, "nccl_id": obj[0], "cut": int(args.cut == "time")}
 
     ctx = ucac.Context(pb, pr, dist=make_dist())
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -439,22 +457,55 @@ def main():
     # ---- per-kernel device times (same kernels launched eagerly with an event pair each), 1 GPU
     roofline, kernels, kms = None, None, None
     fused = False
+    fp64_meas = None
     if world == 1:
         kms, klaunch = ctx.iterate_timed(args.steps)
         rep2 = ctx.report()
         n_al = rep2["al_tron_iters"] - rep1["al_tron_iters"]
         n_fast = rep2["tron_iters"] - rep1["tron_iters"] - n_al
+        al_solves = (rep2["al_active"] - rep1["al_active"]) / args.steps
         ksum = sum(kms.values())
-        fp64 = fp64_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
+        # the FP64 (non-tensor) peak measured in this process: DFMA chains, ucac_measure_fp64_peak
+        with ClockSampler(local) as clk64:
+            fp64_meas = ucac.measure_fp64_peak()
+        fp64_meas["clocks"] = clk64.summary()
+        fp64 = fp64_meas["tflops"]
         hbm = peaks.get("hbm_gbs", 6650.0)
-        fp64_note = ("FP64 non-tensor peak derived: 148 SM x 64 DFMA lanes/clk x 2 flop at sm_max_mhz of "
-                     "MEASURED_PEAKS.json (DESIGN.md 8)")
+        fp64_note = ("FP64 non-tensor peak measured in this run (DFMA-chain microbenchmark, "
+                     "ucac_measure_fp64_peak; see fp64_peak)")
+        # algorithmic flops (R55): the oracle replays one iteration from the GPU's state and counts the
+        # flops of its branch solves (per-operation counts of the plain algorithm); per fast-path solve
+        # and per AL solve, times the GPU's live solve counts
+        alg = None
+        if rank == 0:
+            import oracle
+            oracle.threads(os.cpu_count() or 1)
+            o = oracle.Oracle(pb, pr, omp=True)
+            o.set_state(ctx.get_state())
+            o.iterate(1)
+            ro = o.report()
+            o.close()
+            LT = pb.nbranch * pb.T
+            alg = {"flops_per_fast_solve": ro["flops_fast"] / LT,
+                   "flops_per_al_solve": ro["flops_al"] / max(1, ro["al_active"]),
+                   "oracle_newton_per_fast_solve": ro["newton_fast"] / LT,
+                   "oracle_newton_per_al_solve": ro["newton_al"] / max(1, ro["al_active"]),
+                   "oracle_al_solves": ro["al_active"],
+                   "source": "oracle one-step replay from the GPU state after the per-kernel window (R55)"}
         kernels = {}
-        for k, n, fpn in (("k_branch", n_fast, FLOPS_PER_NEWTON_FAST), ("k_branch_al", n_al, FLOPS_PER_NEWTON_AL)):
-            a_ = n * fpn / (kms[k] * 1e-3) / 1e12
+        for k, n, fpn, alg_flops in (
+                ("k_branch", n_fast, FLOPS_PER_NEWTON_FAST,
+                 alg["flops_per_fast_solve"] * pb.nbranch * pb.T if alg else None),
+                ("k_branch_al", n_al, FLOPS_PER_NEWTON_AL,
+                 alg["flops_per_al_solve"] * al_solves if alg else None)):
+            sass = n * fpn / (kms[k] * 1e-3) / 1e12
+            a_ = alg_flops / (kms[k] / args.steps * 1e-3) / 1e12 if alg_flops is not None else sass
             kernels[k] = {"bound": "alu", "achieved": a_, "peak": fp64, "unit": "TFLOP/s", "frac": a_ / fp64,
-                          "newton_iters_per_step": n / args.steps, "flops_per_newton": fpn,
+                          "flops_per_step_algorithmic": alg_flops,
+                          "sass_achieved": sass, "sass_frac": sass / fp64,
+                          "newton_iters_per_step": n / args.steps, "sass_flops_per_newton": fpn,
                           "ms_per_step": kms[k] / args.steps, "share_of_step": kms[k] / ksum}
+        kernels["k_branch_al"]["al_solves_per_step"] = al_solves
         fused = kms.get("k_rows", 0.0) + kms.get("k_rows_late", 0.0) < 1e-3 * kms["k_bus"]
         for k in (("k_bus",) if fused else ("k_rows", "k_bus")) + ("k_ubar", "k_genx", "k_gen"):
             t = kms[k] + kms.get(k + "_late", 0.0)       # early + late launches
@@ -469,8 +520,9 @@ def main():
         if max(kms, key=kms.get) == dom:
             roofline = dict(kernels[dom], kernel=dom, traffic=traffic.get(dom),
                             traffic_note=traffic.get("_note"),
-                            peak_note=fp64_note + "; flops = the kernel's Newton iterations (live counter) x "
-                                      "its FP64 flops per Newton iteration (ncu SASS count, tools/calibrate_flops.py)")
+                            peak_note=fp64_note + "; achieved = algorithmic flops per step (the oracle's counted "
+                                      "flops per solve x the GPU's live solve counts, R55) / the kernel's "
+                                      "event-timed ms per step; sass_* = Newton iterations x ncu SASS flops")
         else:
             dom = max(kms, key=kms.get)
             roofline = {"bound": "hbm", "kernel": dom, "achieved": sizes["alg_bytes"][dom] * args.steps /
@@ -506,12 +558,42 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
         n, dt, _ = oracle_sample(pb, pr, 10 ** 6, args.cpu_budget)
+        ncores = oracle.threads(os.cpu_count() or 1)
+        n2, dt2, _ = oracle_sample(pb, pr, 10 ** 6, args.cpu_budget, omp=True)
         cpu = {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{n} inner iterations of the same workload from the cold start, "
-                         f"single-threaded C oracle ({dt:.1f} s budget {args.cpu_budget:.0f} s)"}
+                         f"single-threaded C oracle ({dt:.1f} s budget {args.cpu_budget:.0f} s)",
+               "all_cores": {"value": n2 / dt2, "unit": UNIT, "cores": ncores, "nproc": os.cpu_count(),
+                             "cpu_model": cpu_model(), "kind": "oracle (all-core OpenMP build, bitwise the same iterates)",
+                             "sample": f"{n2} inner iterations from the cold start ({dt2:.1f} s, budget {args.cpu_budget:.0f} s)"}}
 
     ttr = time_to_residual() if rank == 0 and world == 1 else None
+
+    # N > 1: on-box self-check -- a fresh partitioned run of K iterations, the local states gathered
+    # and assembled on rank 0, compared bitwise with a 1-GPU run of the same K iterations
+    selfcheck = None
+    if world > 1 and args.selfcheck_iters > 0:
+        kc = args.selfcheck_iters
+        cchk = ucac.Context(pb, pr, dist=make_dist())
+        info = cchk.comm_info()
+        cchk.iterate(kc)
+        torch.cuda.synchronize()
+        parts = [None] * world
+        dist.all_gather_object(parts, ucac.local_part(cchk))
+        cchk.close()
+        if rank == 0:
+            one = ucac.Context(pb, pr)
+            one.iterate(kc)
+            ref = one.get_state()
+            one.close()
+            got = ucac.assemble_parts(pb, parts)
+            bad = [k for k in ref if k != "scal" and not np.array_equal(got[k], ref[k])]
+            if not np.array_equal(got["scal"][[0, 2, 3, 4]], ref["scal"][[0, 2, 3, 4]]):
+                bad.append("scal")
+            selfcheck = {"iterations": kc, "bitwise_equal_to_1gpu": not bad, "differ": bad,
+                         "nccl_nranks": info["nranks"], "cut": args.cut}
 
     if rank == 0:
         v = args.steps / (tot_ms * 1e-3)
@@ -523,8 +605,8 @@ def main():
             "config": {"workload": f"{args.config} (B={pb.nbus}, G={pb.ngen}, L={pb.nbranch}, T={pb.T})",
                        "rows": pb.nrows(), "branch_solves_per_step": pb.nbranch * pb.T,
                        "l2": "flushed (256 MiB memset) before every timed step",
-                       "parallelism": f"bus-graph cut over {world} GPUs, NCCL halo exchange" if world > 1
-                       else "single GPU"},
+                       "parallelism": (f"{args.cut} cut over {world} GPUs, NCCL exchange" if world > 1
+                                       else "single GPU")},
             "branch_solves_per_s": v * pb.nbranch * pb.T,
             "newton_iters_per_s": newton / (tot_ms * 1e-3),
             "newton_per_solve": newton / max(1, args.steps * pb.nbranch * pb.T),
@@ -532,14 +614,17 @@ def main():
                                       for k in ("tron_capped", "al_active", "al_capped")},
             "primal_inf": rep1["primal_inf"],
             "roofline": roofline,
+            "fp64_peak": fp64_meas,
+            "algorithmic_flops": alg if world == 1 else None,
             "kernels": kernels,
             "kernel_ms_per_step": {k: v_ / args.steps for k, v_ in kms.items()} if kms else None,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "time_to_residual": ttr,
+            "multi_gpu_selfcheck": selfcheck,
             # 1 GPU: branch, gen (head), genx, bus, rows, ubar, fold, branch_al, bus_late, rows_late and
             # the tail gen (9 with the rows fused into the bus kernels, UCAC_FUSE_ROWS)
-            "gpu_launches": ((9 if fused else 11) if world == 1 else 15) * args.steps,
+            "gpu_launches": ((9 if fused else 11) if world == 1 else (15 if args.cut == "bus" else 16)) * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

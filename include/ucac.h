@@ -130,6 +130,15 @@ typedef struct {
     unsigned char nccl_id[128];     /* ncclUniqueId (comm_mode 0)                          */
     const int32_t *bus_part;        /* [nbus] owner rank, or NULL = ucac_partition(bus_xy)  */
     const double *bus_xy;           /* [nbus*2] bus coordinates for the partitioner, or NULL */
+    int32_t cut;                    /* 0 = bus-graph cut (above); 1 = time cut (NEXT-4(c), SURVEY
+                                       8(f) row 4; P:166-167 temporal decomposition): rank r owns the
+                                       periods [r T / n, (r+1) T / n) of every component, keeps one
+                                       halo period on each side, all-gathers the DP stage costs
+                                       (4 doubles per (g,t)) for a full-horizon DP on every rank, and
+                                       exchanges with its neighbours the ramp rows' period-boundary
+                                       values (2 doubles per generator forward after (7b), 12 back
+                                       after (7c)/(7d)); bus_part / bus_xy are ignored.  Requires
+                                       T >= nranks; variant bits 4 and 16 are EUNSUPPORTED. */
 } ucac_dist;
 
 /* Deterministic bus-graph cut: weighted recursive coordinate bisection on bus_xy (weights
@@ -146,6 +155,14 @@ ucac_status ucac_halo_lists(int32_t nbus, int32_t nbranch, const int32_t *br_fro
                             int32_t *own_bus, int32_t *ghost_bus, int32_t *local_branch, int32_t *phantom,
                             int32_t *cut_branch, int32_t *export_bus);
 ucac_status ucac_nccl_unique_id(unsigned char *id /* [128] */);
+/* Period split of the time cut (ucac_dist.cut = 1, NEXT-4(c)), host only: rank owns the global
+ * periods [rank T / n, (rank + 1) T / n); out[4] = (global period of local period 0, first owned
+ * local period, end of the owned local periods, local periods incl. one halo period on each side
+ * that is not the horizon's end).  EINVAL unless 1 <= nranks <= T and 0 <= rank < nranks. */
+ucac_status ucac_time_split(int32_t T, int32_t nranks, int32_t rank, int32_t *out);
+/* The context's communicator: ncclCommCount / ncclCommUserRank for an NCCL context (comm_mode 0),
+ * else the ucac_dist ranks (1 / 0 for a single-GPU context). */
+ucac_status ucac_comm_info(ucac_ctx *ctx, int32_t *nranks, int32_t *rank);
 
 /* Create a context: validate (EINVAL with a message: non-finite data, vmin <= 0 or
  * vmin > vmax, pmin > pmax, qmin > qmax, c2 < 0, min_up/min_dn outside [1,T], hold outside
@@ -177,7 +194,10 @@ ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t iters);
 
 /* Global ids of the context's local components (which: 0 generators, 1 branches, 2 owned
  * buses), ascending; ids may be NULL to query *count.  The state/solution arrays of a
- * multi-rank context are laid out over exactly these components. */
+ * multi-rank context are laid out over exactly these components.  which = 3: the local periods,
+ * ids[4] = (global index of local period 0, first owned local period, end of the owned local
+ * periods, local periods); the state/solution arrays hold every local period (a time-cut rank's
+ * halo periods included), a rank's own values are those of its owned periods. */
 ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids, int32_t *count);
 
 /* Same iterations launched kernel by kernel with a CUDA event pair around every launch;

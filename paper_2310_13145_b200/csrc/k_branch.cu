@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
     // generator chain that runs beside this kernel (launch_branch)
     for (int base = blockIdx.x * blockDim.x; base < LT; base += gridDim.x * blockDim.x) {
     const int k = base + threadIdx.x;
-    if (k < LT) {
+    if (k < LT && own_t(d, k % d.T)) {   // (time cut: owned periods only)
         const size_t LTs = (size_t)LT;
         BrFun<false, NOANG> F4;
         double lo[4], hi[4];

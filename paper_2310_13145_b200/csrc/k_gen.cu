@@ -392,6 +392,8 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
         if (k == 0) *d.unext_ok = 0u;              // u_next is consumed: stale for the next state
     }
     const int g = k / T, t = k - g * T;
+    if (!own_t(d, t)) return;   // time cut: halo periods belong to the neighbour (the lane group leaves together)
+    const int tg = tglob(d, t);
     const double ruc = d.ruc, rpq = d.rpq;
     const double S = d.S;
     GenIn in;
@@ -409,11 +411,11 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
     const double u0 = (double)d.u0[g];
     const size_t i = (size_t)k;
     const double on = d.ub_on[i], su = d.ub_su[i], sd = d.ub_sd[i];
-    const double onp = t == 0 ? u0 : d.ub_on[i - 1];
-    in.first = t == 0;
+    const double onp = tg == 0 ? u0 : d.ub_on[i - 1];
+    in.first = tg == 0;
     in.tp = d.pbar[i] - ZG(G_GP, i) - YG(G_GP, i) / d.rpq;
     in.tq = d.qbar[i] - ZG(G_GQ, i) - YG(G_GQ, i) / d.rpq;
-    in.tph = t == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / d.rpq;
+    in.tph = tg == 0 ? 0.0 : d.pbar[i - 1] - ZG(G_RC, i) - YG(G_RC, i) / d.rpq;
     in.bpl = pmin * on - ZG(G_PL, i) - YG(G_PL, i) / d.ruc;
     in.bpu = pmax * on - ZG(G_PU, i) - YG(G_PU, i) / d.ruc;
     in.bql = qmin * on - ZG(G_QL, i) - YG(G_QL, i) / d.ruc;
@@ -431,6 +433,111 @@ __global__ void __launch_bounds__(128) k_genx(Dev d) {
         if (!isfinite(nf0(in.tp) + nf0(in.tq) + nf0(in.tph) + nf0(in.bpl) + nf0(in.bpu) + nf0(in.bql) + nf0(in.bqu) +
                       nf0(in.brl) + nf0(in.bru) + nf0(po) + nf0(qo) + nf0(pho)))
             report_nonfinite(d, K_GENX, g, t);
+    }
+}
+
+// ---------------------------------------------------------------- NEXT-4(c) time cut
+// (P:166-167).  Stage costs of the owned periods (the same stage_cost as k_gen), laid out
+// [g][Tmax][4] for the all-gather.
+__global__ void k_stage_tc(Dev d) {
+    if (d.st->done || d.uc_fixed) return;
+    const int T = d.T, n = d.own1 - d.own0;
+    const size_t GT = (size_t)d.G * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d.G * n; k += gridDim.x * blockDim.x) {
+        const int g = k / n, t = d.own0 + (k - g * n);
+        const size_t i = (size_t)g * T + t;
+        double ub[3] = {d.ub_on[i], d.ub_su[i], d.ub_sd[i]};
+        double yy[3] = {YG(G_DON, i), YG(G_DSU, i), YG(G_DSD, i)};
+        double zz[3] = {ZG(G_DON, i), ZG(G_DSU, i), ZG(G_DSD, i)};
+        if (!isfinite(nf0(ub[0]) + nf0(ub[1]) + nf0(ub[2]) + nf0(yy[0]) + nf0(yy[1]) + nf0(yy[2]) + nf0(zz[0]) +
+                      nf0(zz[1]) + nf0(zz[2])))
+            report_nonfinite(d, K_GEN, g, t);
+        double *o = d.tc_stage_send + ((size_t)g * d.Tmax + (t - d.own0)) * 4;
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) o[a * 2 + b] = stage_cost(a, b, d.c0[g], d.csu[g], d.csd[g], d.ruc, ub, yy, zz);
+    }
+}
+
+// the full-horizon DP (Alg. 2) on every rank from the gathered stage costs; the schedule of the
+// local periods (halos included) goes to u and u_next (k_genx's adoption is then a copy)
+__global__ void __launch_bounds__(128) k_dp_tc(Dev d) {
+    if (d.st->done || d.uc_fixed) return;
+    extern __shared__ __align__(16) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (g >= d.G) return;
+    const int Tg = d.Tg;
+    DpSmem s = dp_carve(smem + (size_t)warp * dp_smem_bytes(Tg), Tg);
+    for (int k = lane; k < Tg * 4; k += 32) {
+        const int tg = k >> 2;
+        int r = 0;
+        while (d.tc_t0[r + 1] <= tg) r++;
+        s.L[k] = __ldcg(d.tc_stage_recv + (((size_t)r * d.G + g) * d.Tmax + (tg - d.tc_t0[r])) * 4 + (k & 3));
+    }
+    __syncwarp();
+    dp_warp(s, Tg, d.tu[g], d.td[g], d.u0[g], d.hold[g]);
+    for (int t = lane; t < d.T; t += 32) {
+        const int8_t v = s.u[tglob(d, t)];
+        d.u[(size_t)g * d.T + t] = v;
+        d.u_next[(size_t)g * d.T + t] = v;
+    }
+}
+
+// p and phat of the first owned period, for the previous rank's last-period ramp rows
+__global__ void k_pack_tc2(Dev d) {
+    if (d.st->done) return;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < d.G; g += gridDim.x * blockDim.x) {
+        const size_t i = (size_t)g * d.T + d.own0;
+        d.tc2_send[(size_t)g * 2 + 0] = d.p[i];
+        d.tc2_send[(size_t)g * 2 + 1] = d.ph[i];
+    }
+}
+__global__ void k_unpack_tc2(Dev d) {
+    if (d.st->done || d.own1 >= d.T) return;   // no next rank
+    const double *src = d.tc2_recv + (size_t)(d.rank + 1) * d.G * 2;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < d.G; g += gridDim.x * blockDim.x) {
+        const size_t i = (size_t)g * d.T + d.own1;
+        d.p[i] = src[(size_t)g * 2 + 0];
+        d.ph[i] = src[(size_t)g * 2 + 1];
+    }
+}
+// the values this rank computed that the next rank owns or reads next iteration: ubar^on and pbar
+// of the last owned period, ubar^su and the D_SU / RU / RC rows (z, y, lambda) of the next period
+__global__ void k_pack_tc3(Dev d) {
+    if (d.st->done || d.own1 >= d.T) return;
+    const size_t GT = (size_t)d.G * d.T;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < d.G; g += gridDim.x * blockDim.x) {
+        const size_t i = (size_t)g * d.T + d.own1 - 1, j = i + 1;
+        double *o = d.tc3_send + (size_t)g * 12;
+        o[0] = d.ub_on[i];
+        o[1] = d.pbar[i];
+        o[2] = d.ub_su[j];
+        const int rows[3] = {G_DSU, G_RU, G_RC};
+        for (int q = 0; q < 3; q++) {
+            o[3 + 3 * q] = d.zg[(size_t)rows[q] * GT + j];
+            o[4 + 3 * q] = d.yg[(size_t)rows[q] * GT + j];
+            o[5 + 3 * q] = d.lg[(size_t)rows[q] * GT + j];
+        }
+    }
+}
+__global__ void k_unpack_tc3(Dev d) {
+    if (d.st->done || d.own0 == 0) return;   // no previous rank
+    const size_t GT = (size_t)d.G * d.T;
+    const double *src = d.tc3_recv + (size_t)(d.rank - 1) * d.G * 12;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < d.G; g += gridDim.x * blockDim.x) {
+        const size_t i = (size_t)g * d.T + d.own0 - 1, j = i + 1;
+        const double *o = src + (size_t)g * 12;
+        d.ub_on[i] = o[0];
+        d.pbar[i] = o[1];
+        d.ub_su[j] = o[2];
+        const int rows[3] = {G_DSU, G_RU, G_RC};
+        for (int q = 0; q < 3; q++) {
+            d.zg[(size_t)rows[q] * GT + j] = o[3 + 3 * q];
+            d.yg[(size_t)rows[q] * GT + j] = o[4 + 3 * q];
+            d.lg[(size_t)rows[q] * GT + j] = o[5 + 3 * q];
+        }
     }
 }
 
@@ -475,13 +582,15 @@ __global__ void k_init(Dev d, const int8_t *u_init) {
          k += (long long)gridDim.x * blockDim.x) {
         if (k < GT) {
             const int g = (int)(k / T), t = (int)(k - (long long)g * T);
+            const int tg = tglob(d, t);   // global period (time cut: local period 0 may be a halo)
             const int ut = u_init ? u_init[k] : d.u0[g];
-            const int up = t == 0 ? d.u0[g] : (u_init ? u_init[k - 1] : d.u0[g]);
+            // (a halo period's predecessor is not local: its ubar^su/sd are never read here)
+            const int up = tg == 0 ? d.u0[g] : (t == 0 ? ut : (u_init ? u_init[k - 1] : d.u0[g]));
             const double pm = 0.5 * (d.pmin[g] + d.pmax[g]);
             d.u[k] = (int8_t)ut;
             d.p[k] = pm;
             d.q[k] = 0.5 * (d.qmin[g] + d.qmax[g]);
-            d.ph[k] = t == 0 ? d.p0[g] : pm;
+            d.ph[k] = tg == 0 ? d.p0[g] : pm;
             d.ub_on[k] = (double)ut;
             d.ub_su[k] = ut > up ? 1.0 : 0.0;
             d.ub_sd[k] = up > ut ? 1.0 : 0.0;
@@ -551,6 +660,19 @@ void launch_init(const Dev &d, const int8_t *u_init_dev, cudaStream_t s) {
 }
 
 size_t gen_smem_bytes(int T) { return gen_smem(T, 4); }
+void launch_stage_tc(const Dev &d, cudaStream_t s) {
+    const int n = d.G * (d.own1 - d.own0);
+    k_stage_tc<<<std::max(1, std::min(592, (n + 127) / 128)), 128, 0, s>>>(d);
+}
+void launch_dp_tc(const Dev &d, cudaStream_t s) {
+    const int warps = 4;
+    k_dp_tc<<<(d.G + warps - 1) / warps, warps * 32, gen_smem(d.Tg, warps), s>>>(d);
+}
+static int tcgrid(int n) { return std::max(1, std::min(148, (n + 127) / 128)); }
+void launch_pack_tc2(const Dev &d, cudaStream_t s) { k_pack_tc2<<<tcgrid(d.G), 128, 0, s>>>(d); }
+void launch_unpack_tc2(const Dev &d, cudaStream_t s) { k_unpack_tc2<<<tcgrid(d.G), 128, 0, s>>>(d); }
+void launch_pack_tc3(const Dev &d, cudaStream_t s) { k_pack_tc3<<<tcgrid(d.G), 128, 0, s>>>(d); }
+void launch_unpack_tc3(const Dev &d, cudaStream_t s) { k_unpack_tc3<<<tcgrid(d.G), 128, 0, s>>>(d); }
 // The attribute is process-wide per kernel: only ever raise it, so a later context or dp_batch
 // with a smaller T never lowers the limit under a live larger-T context.
 cudaError_t gen_set_smem_attr(int T) {
@@ -562,6 +684,7 @@ cudaError_t gen_set_smem_attr(int T) {
     cudaError_t e = cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_dp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e == cudaSuccess) cur = b;
     return e;
 }

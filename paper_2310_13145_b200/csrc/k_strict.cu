@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(STRICT_TPB) k_branch_strict(Dev d) {
     unsigned long long cnt[NCNT] = {0, 0, 0, 0, 0};
     for (int base = blockIdx.x * blockDim.x; base < LT; base += gridDim.x * blockDim.x) {
         const int k = base + threadIdx.x;
-        if (k < LT) {
+        if (k < LT && own_t(d, k % d.T)) {   // (time cut: owned periods only)
             const int l = k / d.T, t = k - l * d.T;
             const int bi = d.bfrom[l], bj = d.bto[l];
             double y[8];

@@ -144,7 +144,7 @@ constexpr int ROWS_THREADS = 128;
 // The bus kernel keeps 1024-thread blocks; the rows kernel, whose row updates need more than the
 // 64 registers of a 1024-thread block, runs 256-thread blocks (measured)
 #ifndef UCAC_LBUS_THREADS
-#define UCAC_LBUS_THREADS 1024
+#define UCAC_LBUS_THREADS 128
 #endif
 #ifndef UCAC_LROWS_THREADS
 #define UCAC_LROWS_THREADS 256
@@ -288,6 +288,75 @@ __device__ __forceinline__ void zy_s(double r, double rho, double ib, double bpr
     else zy_vals(r, rho, ib, z, y, lam, pending, beta_lam, lmax, dxb, a);
 }
 
+// ---- compacted late lists.  The early kernels see every mark: each block writes its
+// marked items, in thread order, to its own fixed slot range list[blockIdx.x * cap ...] and the
+// count to cnt[blockIdx.x].  A late block turns the counts into exclusive offsets (shared memory)
+// and takes items j = its thread id + k * grid stride of the concatenation -- a deterministic
+// list in index order, so the late kernels need a grid sized to the marked work only, and
+// their fold order is fixed.
+__device__ __forceinline__ void block_compact(int nitems, const int *items, int *list, unsigned *cnt, int cap) {
+    __shared__ int wsum[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int incl = nitems;   // inclusive warp scan of the per-thread counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < nw; w++) {
+        if (w < warp) off += wsum[w];
+        tot += wsum[w];
+    }
+    off += incl - nitems;
+    for (int q = 0; q < nitems; q++) list[(size_t)blockIdx.x * cap + off + q] = items[q];
+    if (threadIdx.x == 0) cnt[blockIdx.x] = (unsigned)tot;
+    __syncthreads();
+}
+// exclusive offsets pre[0..n] of cnt[0..n) in shared memory (block-wide); returns the total
+__device__ __forceinline__ int block_offsets(const unsigned *cnt, int n, int *pre) {
+    __shared__ int wsum[32];
+    const int nt = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
+    // one coalesced pass of independent loads into shared memory, then the scan from there
+    for (int i = threadIdx.x; i < n; i += nt) pre[i] = (int)__ldcg(cnt + i);
+    __syncthreads();
+    const int per = (n + nt - 1) / nt;
+    const int beg = min(n, (int)threadIdx.x * per), end = min(n, beg + per);
+    int sum = 0;
+    for (int i = beg; i < end; i++) sum += pre[i];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; w++) off += wsum[w];
+    off += incl - sum;
+    for (int i = beg; i < end; i++) {
+        const int c = pre[i];
+        pre[i] = off;
+        off += c;
+    }
+    if (threadIdx.x == nt - 1) pre[n] = off;
+    __syncthreads();
+    return pre[n];
+}
+// item j of the concatenated lists: source block by binary search over the offsets
+__device__ __forceinline__ int list_item(const int *pre, int n, const int *list, int cap, int j) {
+    int lo = 0, hi = n;   // largest src with pre[src] <= j (pre[n] > j)
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= j) lo = mid;
+        else hi = mid;
+    }
+    return __ldcg(list + (size_t)lo * cap + (j - pre[lo]));
+}
+
 // bus-period k = i*T + t of an owned bus (ghost buses are solved by their owner)
 template <bool STRICT>
 __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc &acc) {
@@ -303,6 +372,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
         const int e0 = d.be_ptr[i], e1 = d.be_ptr[i + 1];
         const int ne = e1 - e0;
         // ---- sums of the 2x2 KKT system, canonical order (gens, ends, wbar)
+        const bool has_next = tglob(d, t) < d.Tg - 1;   // a ramp-copy row RC_{t+1} exists
         double AP = 0.0, AQ = 0.0, C = 0.0, rP = d.pd[k], rQ = d.qd[k];
         const double wbo = d.wbar[k], tbo = d.thbar[k];
         // (loops unrolled so the loads of several gens / ends are in flight together)
@@ -311,7 +381,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
             const double tgp = d.p[gi] + ZG(G_GP, gi) + over_rho<STRICT>(YG(G_GP, gi), rpq, irpq);
             double th, aa;
-            if (t < T - 1) {
+            if (has_next) {
                 const double trc = d.ph[gi + 1] + ZG(G_RC, gi + 1) + over_rho<STRICT>(YG(G_RC, gi + 1), rpq, irpq);
                 th = (tgp + trc) * 0.5;
                 aa = 2.0 * rpq;
@@ -356,7 +426,7 @@ __device__ __forceinline__ void bus_solve(const Dev &d, const Ctl &c, int k, Acc
         // ---- generator copies and their rows (each gen: all loads, then the updates, then the stores)
         for (int a = g0; a < g1; a++) {
             const size_t gi = (size_t)d.bg_idx[a] * T + t;
-            const bool rc = t < T - 1;
+            const bool rc = has_next;
             const double pg = d.p[gi], qg = d.q[gi], pbo = d.pbar[gi], qbo = d.qbar[gi];
             double zp = ZG(G_GP, gi), yp = YG(G_GP, gi), lp = LG(G_GP, gi);
             double zq = ZG(G_GQ, gi), yq = YG(G_GQ, gi), lq = LG(G_GQ, gi);
@@ -437,10 +507,13 @@ __global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc;
-    if (k < d.B_own * d.T && d.bmark[k] != c.stamp) {
+    const bool own = k < d.B_own * d.T && own_t(d, k % d.T);   // (time cut: owned periods only)
+    const bool marked = own && d.bmark[k] == c.stamp;
+    if (own && !marked) {
         bus_solve<STRICT>(d, c, k, acc);
         if (d.fuse_rows) bus_end_rows<STRICT>(d, c, k, acc);
     }
+    block_compact(marked ? 1 : 0, &k, d.lbus, d.lbus_cnt, BUS_THREADS);   // the late bus list
     block_reduce_store(acc, d.part_bus);
 }
 
@@ -500,11 +573,15 @@ __global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
     const Ctl c(d);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc;
-    if (k < d.L * d.T) {
+    int items[2], ni = 0;
+    if (k < d.L * d.T && own_t(d, k % d.T)) {
         const int l = k / d.T, t = k - l * d.T;
         if (d.rmark[0][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 0, acc);
+        else items[ni++] = k << 1;
         if (d.rmark[1][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 1, acc);
+        else items[ni++] = (k << 1) | 1;
     }
+    block_compact(ni, items, d.lrow, d.lrow_cnt, 2 * ROWS_THREADS);   // the late end list
     block_reduce_store(acc, d.part_rows);
 }
 
@@ -517,13 +594,16 @@ __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
     pdl_wait();
     TL_KERNEL(K_BUS_LATE);
     if (d.st->done) return;
+    extern __shared__ int pre[];   // [nblk_bus + 1] offsets of the compacted bus lists
     Acc acc;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    // the control values (two divisions) only for the marked few: most late threads skip
-    if (k < d.B_own * d.T && d.bmark[k] == mark_stamp(d)) {
+    const int n = block_offsets(d.lbus_cnt, d.nblk_bus, pre);
+    if ((int)(blockIdx.x * blockDim.x) < n) {   // the control values (two divisions) only with work
         const Ctl c(d);
-        bus_solve<STRICT>(d, c, k, acc);
-        if (d.fuse_rows) bus_end_rows<STRICT>(d, c, k, acc);
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+            const int k = list_item(pre, d.nblk_bus, d.lbus, BUS_THREADS, j);
+            bus_solve<STRICT>(d, c, k, acc);
+            if (d.fuse_rows) bus_end_rows<STRICT>(d, c, k, acc);
+        }
     }
     // fused rows: this is the iteration's last kernel and does the final fold
     kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, d.fuse_rows != 0);
@@ -581,16 +661,15 @@ __global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
     pdl_wait();
     TL_KERNEL(K_ROWS_LATE);
     if (d.st->done) return;
+    extern __shared__ int pre[];   // [nblk_rows + 1] offsets of the compacted end lists
     Acc acc;
-    // grid-stride: one pass per thread at the default grid (UCAC_LROWS_GRID caps it, experiments)
-    const unsigned stamp = mark_stamp(d);
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d.L * d.T; k += gridDim.x * blockDim.x) {
-        const bool m0 = d.rmark[0][k] == stamp, m1 = d.rmark[1][k] == stamp;
-        if (m0 || m1) {   // the control values (two divisions) only for the marked few
-            const Ctl c(d);
-            const int l = k / d.T, t = k - l * d.T;
-            if (m0) end_rows<STRICT>(d, c, l, t, 0, acc);
-            if (m1) end_rows<STRICT>(d, c, l, t, 1, acc);
+    const int n = block_offsets(d.lrow_cnt, d.nblk_rows, pre);
+    if ((int)(blockIdx.x * blockDim.x) < n) {
+        const Ctl c(d);
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+            const int code = list_item(pre, d.nblk_rows, d.lrow, 2 * ROWS_THREADS, j);
+            const int k = code >> 1, l = k / d.T, t = k - l * d.T;
+            end_rows<STRICT>(d, c, l, t, code & 1, acc);
         }
     }
     kernel_tail(d, acc, d.part_lrows, RK_ROWS_LATE, final != 0);
@@ -622,8 +701,11 @@ __device__ void solve_small(int nf, double A[3][3], const double *b, double *x) 
     }
 }
 
-// exact box-QP over [0,1]^n, n <= 3, by the 3^n activity states
-__device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, double *v) {
+// exact box-QP over [0,1]^n, n <= 3, by the 3^n activity states: candidates
+// [c0, c1) of the enumeration, first minimum kept (best, bidx); boxqp3 runs all of them
+__device__ __forceinline__ int boxqp3_ncand(int n) { return n == 3 ? 27 : (n == 2 ? 9 : 3); }
+__device__ void boxqp3_range(int n, int m, const double (*c)[3], const double *e, int c0, int c1, double *v,
+                             double &best, int &bidx) {
     double H[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, bb[3] = {0, 0, 0};
     for (int i = 0; i < n; i++) {
         for (int j = 0; j < n; j++) {
@@ -635,10 +717,10 @@ __device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, doub
         for (int k = 0; k < m; k++) s = s + c[k][i] * e[k];
         bb[i] = s;
     }
-    int ncand = n == 3 ? 27 : (n == 2 ? 9 : 3);
-    double best = INFINITY;
+    best = INFINITY;
+    bidx = 0x7fffffff;
     for (int i = 0; i < n; i++) v[i] = 0.0;
-    for (int idx = 0; idx < ncand; idx++) {
+    for (int idx = c0; idx < c1; idx++) {
         int st[3], r = idx;
         for (int i = 0; i < n; i++) {
             st[i] = r % 3;
@@ -671,7 +753,44 @@ __device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, doub
         }
         if (obj < best) {
             best = obj;
+            bidx = idx;
             for (int i = 0; i < n; i++) v[i] = vv[i];
+        }
+    }
+}
+__device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, double *v) {
+    double best;
+    int bidx;
+    boxqp3_range(n, m, c, e, 0, boxqp3_ncand(n), v, best, bidx);
+}
+// UBAR_LANES consecutive lanes per (g, group) split the enumeration into contiguous candidate
+// ranges; each keeps its first minimum, and the (objective, index) combine -- smaller objective,
+// then smaller index -- returns the sequential enumeration's pick bit for bit (as k_genx does)
+#ifndef UCAC_UBAR_LANES
+#define UCAC_UBAR_LANES 1   // measured (eager, pegase T=48): 1 lane 38.6 us, 2 lanes 54.6, 4 lanes 66.4 -- the
+                            // per-thread chain shrinks but 2-4x the threads (and their loads) run in 2-4 waves
+#endif
+constexpr int UBAR_LANES = UCAC_UBAR_LANES;
+__device__ void boxqp3_lanes(int n, int m, const double (*c)[3], const double *e, double *v, int sub,
+                             unsigned mask) {
+    const int nc = boxqp3_ncand(n);
+    v[0] = v[1] = v[2] = 0.0;
+    const int c0 = (nc * sub + UBAR_LANES - 1) / UBAR_LANES, c1 = (nc * (sub + 1) + UBAR_LANES - 1) / UBAR_LANES;
+    double best;
+    int bidx;
+    boxqp3_range(n, m, c, e, c0, c1, v, best, bidx);
+#pragma unroll
+    for (int o = 1; o < UBAR_LANES; o <<= 1) {
+        const double ob = __shfl_xor_sync(mask, best, o);
+        const int oi = __shfl_xor_sync(mask, bidx, o);
+        const double o0 = __shfl_xor_sync(mask, v[0], o), o1 = __shfl_xor_sync(mask, v[1], o),
+                     o2 = __shfl_xor_sync(mask, v[2], o);
+        if (ob < best || (ob == best && oi < bidx)) {
+            best = ob;
+            bidx = oi;
+            v[0] = o0;
+            v[1] = o1;
+            v[2] = o2;
         }
     }
 }
@@ -684,21 +803,25 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t GT = (size_t)d.G * T;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    // UBAR_LANES consecutive lanes per (g, group); the group's lanes are all in or all out of range
+    const int k4 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = k4 / UBAR_LANES, sub = k4 % UBAR_LANES;
+    const unsigned mask = __ballot_sync(0xffffffffu, k < d.G * T && own_t(d, k % T));
     const double ruc = d.ruc;
     const double beta_lam = d.st->beta_lam, lmax = d.lambda_max, bpr = d.st->beta + ruc;
     const int pending = d.st->pending_outer;
     Acc acc;
-    if (k < d.G * T) {
+    if (k < d.G * T && own_t(d, k % T)) {   // whole lane groups in or out (the shuffle mask above)
         const int g = k / T, t = k - g * T;
+        const int tg = tglob(d, t);
         const size_t i = (size_t)k;
         const double Pm = d.pmin[g], PM = d.pmax[g], Qm = d.qmin[g], QM = d.qmax[g];
         const double RDn = d.rdn[g], SDn = d.sdn[g], RUp = d.rup[g], SUp = d.sup[g];
         const int u0 = d.u0[g];
         // old group values (iterate l) -- the x-step's shifted bounds use them (R19)
         const double on_o = d.ub_on[i], sd_o = d.ub_sd[i], su_o = d.ub_su[i];
-        const double onp_o = t == 0 ? (double)u0 : d.ub_on[i - 1];
-        const int ut = d.u[i], up = t == 0 ? u0 : d.u[i - 1];
+        const double onp_o = tg == 0 ? (double)u0 : d.ub_on[i - 1];
+        const int ut = d.u[i], up = tg == 0 ? u0 : d.u[i - 1];
         const int sdt = up > ut, sut = ut > up;
         const double p = d.p[i], q = d.q[i], ph = d.ph[i];
         // slacks (x-variables of 7b) recomputed exactly as the x-step defines them
@@ -733,7 +856,8 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         int n = 2;
         int sun = 0;
         double pn = 0.0, phn = 0.0, sru_n = 0.0, su_on = 0.0, srd_n = 0.0;
-        if (t < T - 1) {
+        const bool nxt = tg < d.Tg - 1;
+        if (nxt) {
             const size_t j = i + 1;
             const int un = d.u[j];
             sun = un > ut;
@@ -762,14 +886,14 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
             yr[q2] = YG(rk[q2], i);
             lr[q2] = LG(rk[q2], i);
         }
-        const bool nxt = t < T - 1;
         if (nxt) {
             zr[7] = ZG(G_DSU, i + 1); yr[7] = YG(G_DSU, i + 1); lr[7] = LG(G_DSU, i + 1);
             zr[8] = ZG(G_RU, i + 1);  yr[8] = YG(G_RU, i + 1);  lr[8] = LG(G_RU, i + 1);
             if (lit) { zr[9] = ZG(G_RD, i + 1); yr[9] = YG(G_RD, i + 1); lr[9] = LG(G_RD, i + 1); }
         }
         double v[3];
-        boxqp3(n, m, cm, e, v);
+        boxqp3_lanes(n, m, cm, e, v, sub, mask);
+        if (sub == 0) {
         {
             double chk = nf0(v[0]) + nf0(v[1]) + nf0(v[2]);
             for (int q2 = 0; q2 < m; q2++) chk = chk + nf0(e[q2]);
@@ -821,7 +945,7 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
                 if (pending) LG(G_RD, i + 1) = lr[9];
             }
         }
-        if (t == 0) {
+        if (tg == 0) {
             // group 0 = (ubar^su_1): rows D_SU_1, RU_1 (ubar^on_0 := u0, R4)
             const double bru = RUp * onp_o + SUp * su_o - ZG(G_RU, i) - YG(G_RU, i) / ruc;
             const double sru = fmax(0.0, bru - dd);
@@ -847,6 +971,7 @@ __global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
         const double Sp = d.S * p;
         acc.v[P_OBJ] = d.c2[g] * Sp * Sp + d.c1[g] * Sp + d.c0[g] * (double)ut + d.csu[g] * (double)sut +
                        d.csd[g] * (double)sdt;
+        }   // sub == 0
     }
     block_reduce_store(acc, d.part_ubar);
 }
@@ -964,7 +1089,7 @@ __global__ void k_clear_pending(Dev d) { d.st->pending_outer = 0; }
 }  // namespace
 
 int nblk_bus(int B, int T) { return (B * T + BUS_THREADS - 1) / BUS_THREADS; }
-int nblk_ubar(int G, int T) { return (G * T + UBAR_THREADS - 1) / UBAR_THREADS; }
+int nblk_ubar(int G, int T) { return (G * T * UBAR_LANES + UBAR_THREADS - 1) / UBAR_THREADS; }
 int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; }
 
 // launch priority of the sweep chain k_bus -> k_rows -> (fold) -> k_rows_late, the critical path
@@ -989,33 +1114,41 @@ void launch_rows(const Dev &d, cudaStream_t s) {
 #ifndef UCAC_LATE_PRIO
 #define UCAC_LATE_PRIO 1
 #endif
-// the late kernels at high priority: when the AL tail frees its SMs, k_bus_late's full-SM blocks
-// take them ahead of k_rows' pending blocks
+// The late kernels: one wave, grid-striding over the compacted lists (their items are ~10 % of the
+// bus-periods / ends); at high launch priority, so they take SM slots ahead of pending early
+// blocks when the AL tail ends.  Dynamic shared memory: the offsets of the early blocks' lists.
+static int sm_count() {
+    static const int n = [] {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return std::max(1, sms);
+    }();
+    return n;
+}
+template <typename K>
+static size_t late_smem(K k, int nsrc) {
+    const size_t b = (size_t)(nsrc + 1) * sizeof(int);
+    if (b > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    return b;
+}
 void launch_bus_late(const Dev &d, cudaStream_t s) {
-    launch_ex(d.strict ? k_bus_late<true> : k_bus_late<false>, dim3(d.nblk_lbus), dim3(LBUS_THREADS), 0, s,
+    auto k = d.strict ? k_bus_late<true> : k_bus_late<false>;
+    launch_ex(k, dim3(d.nblk_lbus), dim3(LBUS_THREADS), late_smem(k, d.nblk_bus), s,
               UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, (pdl_mask() & 2) != 0, d);
 }
 void launch_rows_late(const Dev &d, cudaStream_t s, int final) {
-    // One wave: at most (resident blocks per SM) x SMs blocks, grid-striding over the (l,t) range.
-    // The default grid (one thread per (l,t), ~860 blocks on pegase at 2 resident per SM) ran in
-    // three waves, each paying a marked end's dependent load chain and the block tail: 28.2 ->
-    // 22.5 us in the graph, step -2.4 %.  UCAC_LROWS_GRID=n caps the grid at n
-    // instead; n < 0 restores one thread per (l,t).
-    static const int lrows_cap = [] {
-        const char *e = getenv("UCAC_LROWS_GRID");
-        if (e) return atoi(e);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_late<false>, LROWS_THREADS, 0);
-        return std::max(1, sms * per_sm);
-    }();
-    const int g = lrows_cap > 0 ? std::min(d.nblk_lrows, lrows_cap) : d.nblk_lrows;
-    launch_ex(d.strict ? k_rows_late<true> : k_rows_late<false>, dim3(g), dim3(LROWS_THREADS), 0, s,
+    auto k = d.strict ? k_rows_late<true> : k_rows_late<false>;
+    launch_ex(k, dim3(d.nblk_lrows), dim3(LROWS_THREADS), late_smem(k, d.nblk_rows), s,
               UCAC_SWEEP_PRIO || UCAC_LATE_PRIO, (pdl_mask() & 4) != 0, d, final);
 }
-int nblk_lbus(int n) { return (n + LBUS_THREADS - 1) / LBUS_THREADS; }
-int nblk_lrows(int n) { return (n + LROWS_THREADS - 1) / LROWS_THREADS; }
+#ifndef UCAC_LATE_WAVES
+#define UCAC_LATE_WAVES 1
+#endif
+// late grids: enough threads for every marked item of a wave-sized grid (at most one per SM x
+// UCAC_LATE_WAVES), never more blocks than the full range would need
+int nblk_lbus(int n) { return std::max(1, std::min((n + LBUS_THREADS - 1) / LBUS_THREADS, sm_count() * UCAC_LATE_WAVES)); }
+int nblk_lrows(int n) { return std::max(1, std::min((n + LROWS_THREADS - 1) / LROWS_THREADS, 2 * sm_count() * UCAC_LATE_WAVES)); }
 int fold_blocks() { return FOLD_BLOCKS; }
 void launch_fold_early(const Dev &d, cudaStream_t s) { k_fold_early<<<FOLD_BLOCKS, FOLD_THREADS, 0, s>>>(d); }
 void launch_ubar(const Dev &d, cudaStream_t s) {

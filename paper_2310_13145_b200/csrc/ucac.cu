@@ -72,7 +72,48 @@ struct Local {
     // halo
     std::vector<int> cut_local, export_local, phantom_src, ghost_src;
     int max_cut = 0, max_export = 0;
+    // periods: local period t = global t + t_off of Tg, owned [own0, own1) (time cut, NEXT-4(c))
+    int t_off = 0, Tg = 0, own0 = 0, own1 = 0, Tmax = 0;
+    std::vector<int> tstart;                                       // [nranks + 1] owned global ranges
 };
+
+// NEXT-4(c) time cut: rank r owns the global periods [r Tg / n, (r + 1) Tg / n) of every
+// component, plus one halo period on each side that is not the horizon's end.
+static void time_split(int Tg, int nranks, std::vector<int> &t0) {
+    t0.assign(nranks + 1, 0);
+    for (int r = 0; r <= nranks; r++) t0[r] = (int)(((long long)r * Tg) / nranks);
+}
+static Local localize_periods(Local P, const ucac_horizon *hz, const ucac_uc *uc, int nranks, int rank) {
+    const int Tg = P.T;
+    time_split(Tg, nranks, P.tstart);
+    const int g0 = P.tstart[rank], g1 = P.tstart[rank + 1];
+    const int hl = g0 > 0, hh = g1 < Tg;
+    const int Tl = (g1 - g0) + hl + hh;
+    P.Tg = Tg;
+    P.t_off = g0 - hl;
+    P.own0 = hl;
+    P.own1 = hl + (g1 - g0);
+    P.Tmax = 0;
+    for (int r = 0; r < nranks; r++) P.Tmax = std::max(P.Tmax, P.tstart[r + 1] - P.tstart[r]);
+    std::vector<double> pd((size_t)P.B * Tl), qd((size_t)P.B * Tl);
+    for (int a = 0; a < P.B; a++)
+        for (int t = 0; t < Tl; t++) {
+            pd[(size_t)a * Tl + t] = P.pdT[(size_t)a * Tg + P.t_off + t];
+            qd[(size_t)a * Tl + t] = P.qdT[(size_t)a * Tg + P.t_off + t];
+        }
+    P.pdT.swap(pd);
+    P.qdT.swap(qd);
+    if (!P.uinit.empty()) {
+        std::vector<int8_t> u((size_t)P.G * Tl);
+        for (int g = 0; g < P.G; g++)
+            for (int t = 0; t < Tl; t++) u[(size_t)g * Tl + t] = P.uinit[(size_t)g * Tg + P.t_off + t];
+        P.uinit.swap(u);
+    }
+    (void)hz;
+    (void)uc;
+    P.T = Tl;
+    return P;
+}
 
 static Local build_local(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co, const ucac_uc *uc,
                          const int32_t *part, int nranks, int rank) {
@@ -388,8 +429,13 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "%s", cudaGetErrorString(e));
     if (cc_major != 10) return fail(nullptr, UCAC_ECUDA, "libucac is built for sm_100a; device is sm_%d%d", cc_major, cc_minor);
 
+    const int tcut = (dist && nranks > 1) ? (dist->cut != 0) : 0;
+    if (dist && nranks > 1 && dist->cut != 0 && dist->cut != 1) return fail(nullptr, UCAC_EINVAL, "cut must be 0 or 1");
+    if (tcut && nranks > hz->T) return fail(nullptr, UCAC_EINVAL, "time cut: T=%d < nranks=%d", hz->T, nranks);
+    if (tcut && (prm->variant & (4 | 16)))
+        return fail(nullptr, UCAC_EUNSUPPORTED, "time cut: variant bits 4 (ramp-aware DP) and 16 (literal Eq. 5f) are not supported");
     std::vector<int32_t> part;
-    if (nranks > 1) {
+    if (nranks > 1 && !tcut) {
         part.assign(net->nbus, 0);
         if (dist->bus_part) {
             for (int i = 0; i < net->nbus; i++) {
@@ -415,7 +461,16 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ctx->rank = rank;
     ctx->comm_mode = dist && nranks > 1 ? dist->comm_mode : 0;
     mark("device/part");
-    ctx->P = build_local(net, hz, co, uc, part.data(), nranks, rank);
+    if (tcut) {
+        std::vector<int32_t> one(net->nbus, 0);
+        ctx->P = localize_periods(build_local(net, hz, co, uc, one.data(), 1, 0), hz, uc, nranks, rank);
+    } else {
+        ctx->P = build_local(net, hz, co, uc, part.data(), nranks, rank);
+        ctx->P.Tg = ctx->P.T;
+        ctx->P.own1 = ctx->P.T;
+        ctx->P.Tmax = ctx->P.T;
+        ctx->P.tstart = {0, ctx->P.T};
+    }
     mark("build_local");
     Local &P = ctx->P;
     const int B = P.B, G = P.G, L = P.L, T = P.T;
@@ -471,6 +526,13 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.max_export = P.max_export;
     d.ref_bus = P.ref;
     d.S = P.S;
+    d.t_off = P.t_off;
+    d.Tg = P.Tg;
+    d.own0 = P.own0;
+    d.own1 = P.own1;
+    d.tcut = tcut;
+    d.Tmax = P.Tmax;
+    d.rank = rank;
     d.rpq = prm->rho_pq; d.rva = prm->rho_va; d.ruc = prm->rho_uc;
     d.irpq = 1.0 / prm->rho_pq; d.irva = 1.0 / prm->rho_va; d.iruc = 1.0 / prm->rho_uc;
     d.tau = prm->tau; d.theta = prm->theta; d.lambda_max = prm->lambda_max; d.beta_max = prm->beta_max;
@@ -531,6 +593,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.export_local = A.put(P.export_local);
         d.phantom_src = A.put(P.phantom_src);
         d.ghost_src = A.put(P.ghost_src);
+        d.tc_t0 = A.put(P.tstart);
         uinit = P.uinit.empty() ? nullptr : A.put(P.uinit);
         A.up_end = A.off;
         // iterate (zeroed, then set by launch_init)
@@ -562,6 +625,10 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.nblk_lrows = nblk_lrows(L * T);
         d.part_lbus = A.take<double>((size_t)d.nblk_lbus * NPART);
         d.part_lrows = A.take<double>((size_t)d.nblk_lrows * NPART);
+        d.lbus = A.take<int>((size_t)d.nblk_bus * 128);          // BUS_THREADS items per k_bus block
+        d.lbus_cnt = A.take<unsigned>((size_t)d.nblk_bus);
+        d.lrow = A.take<int>((size_t)d.nblk_rows * 2 * 128);     // 2 ROWS_THREADS items per k_rows block
+        d.lrow_cnt = A.take<unsigned>((size_t)d.nblk_rows);
         d.part_efold = A.take<double>((size_t)fold_blocks() * NPART);
         d.rec_part = A.take<double>(3 * NPART);
         d.kdone = A.take<unsigned>(3);
@@ -581,6 +648,14 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.xsend2 = A.take<double>((size_t)P.max_export * 6 * T);
         d.xrecv2 = A.take<double>((size_t)nranks * P.max_export * 6 * T);
         d.st = A.take<DevStatus>(1);
+        if (tcut) {
+            d.tc_stage_send = A.take<double>((size_t)G * P.Tmax * 4);
+            d.tc_stage_recv = A.take<double>((size_t)nranks * G * P.Tmax * 4);
+            d.tc2_send = A.take<double>((size_t)G * 2);
+            d.tc2_recv = A.take<double>((size_t)nranks * G * 2);
+            d.tc3_send = A.take<double>((size_t)G * 12);
+            d.tc3_recv = A.take<double>((size_t)nranks * G * 12);
+        }
         d.rmark[0] = A.take<unsigned>((size_t)(L + P.Lp) * T);
         d.rmark[1] = A.take<unsigned>((size_t)(L + P.Lp) * T);
         ctx->xpose = A.take<double>(4 * LT);
@@ -622,7 +697,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     *ctx->st_host = st0;
     if (cudaMemcpyAsync(d.st, ctx->st_host, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s) != cudaSuccess)
         return bail(fail(ctx, UCAC_ECUDA, "status upload"));
-    if (gen_set_smem_attr(T) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "T=%d needs %zu B of shared memory", T, gen_smem_bytes(T)));
+    if (gen_set_smem_attr(P.Tg) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "T=%d needs %zu B of shared memory", P.Tg, gen_smem_bytes(P.Tg)));
     mark("arena");
     launch_init(d, uinit, ctx->s);
     e = cudaGetLastError();
@@ -677,7 +752,38 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
     }
 }
 
+// NEXT-4(c) time cut, one NCCL rank per GPU: every rank runs all components over its periods;
+// the DP stage costs are all-gathered for a full-horizon DP on every rank, p and phat of the first
+// owned period go to the previous rank (its ramp-copy and ramp-up rows at the boundary), and the
+// boundary values the previous rank computed (ubar, pbar of its last period, the ramp rows of this
+// rank's first period) come back after (7c)/(7d); one all-reduce of the S8 record.
+static void enqueue_iteration_tc(ucac_ctx *ctx) {
+    const Dev &d = ctx->d;
+    cudaStream_t s = ctx->s;
+    launch_stage_tc(d, s);
+    ncclAllGather(d.tc_stage_send, d.tc_stage_recv, (size_t)d.G * d.Tmax * 4, ncclDouble, ctx->comm, s);
+    launch_dp_tc(d, s);
+    launch_kernel(ctx, K_GENX, s);
+    launch_pack_tc2(d, s);
+    ncclAllGather(d.tc2_send, d.tc2_recv, (size_t)d.G * 2, ncclDouble, ctx->comm, s);
+    launch_unpack_tc2(d, s);
+    const int seq[] = {K_BRANCH, K_UBAR, K_BUS, K_BRANCH_AL, K_BUS_LATE, K_ROWS, K_FOLD, K_ROWS_LATE};
+    for (int k : seq) launch_kernel(ctx, k, s);
+    launch_pack_tc3(d, s);
+    ncclAllGather(d.tc3_send, d.tc3_recv, (size_t)d.G * 12, ncclDouble, ctx->comm, s);
+    launch_unpack_tc3(d, s);
+    ncclGroupStart();
+    ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, s);
+    ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, s);
+    ncclGroupEnd();
+    launch_finalize(d, s);
+}
+
 static void enqueue_iteration(ucac_ctx *ctx) {
+    if (ctx->d.tcut) {
+        enqueue_iteration_tc(ctx);
+        return;
+    }
     const Dev &d = ctx->d;
     const bool multi = ctx->nranks > 1;
     const bool early_fork = !multi && UCAC_EARLY_FORK;
@@ -705,7 +811,7 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         cudaStreamWaitEvent(ctx->s3, ctx->ev_genx, 0);
         if (early_fork) cudaStreamWaitEvent(ctx->s3, ctx->ev_branch, 0);
         launch_kernel(ctx, K_BUS, ctx->s3);
-        if (UCAC_UBAR_AFTER_BUS) cudaEventRecord(ctx->ev_bus, ctx->s3);
+        cudaEventRecord(ctx->ev_bus, ctx->s3);   // k_bus_late reads the bus lists k_bus compacts
         launch_kernel(ctx, K_ROWS, ctx->s3);
     }
     // k_ubar is off the critical path (it only has to finish before the early fold): after
@@ -735,6 +841,7 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         cudaStreamWaitEvent(ctx->s, ctx->ev_genx, 0);
         // fused rows: k_bus_late does the final fold, so it needs the folded early partials
         if (d.fuse_rows) cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
+        cudaStreamWaitEvent(ctx->s, ctx->ev_bus, 0);
         launch_kernel(ctx, K_BUS_LATE, ctx->s);
         cudaStreamWaitEvent(ctx->s, ctx->ev_early, 0);
         launch_kernel(ctx, K_ROWS_LATE, ctx->s);
@@ -870,7 +977,44 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
         ucac_status s = set_control(ctxs[r], 0, 0.0);
         if (s != UCAC_OK) return s;
     }
+    // all-gather of `count` doubles from every rank's send buffer into every rank's receive buffer
+    auto allgather = [&](double *Dev::*snd, double *Dev::*rcv, size_t count) -> cudaError_t {
+        for (int r = 0; r < n; r++)
+            for (int q = 0; q < n; q++) {
+                cudaError_t e = cudaMemcpyAsync(ctxs[r]->d.*rcv + (size_t)q * count, ctxs[q]->d.*snd, count * sizeof(double),
+                                                cudaMemcpyDeviceToDevice, ctxs[r]->s);
+                if (e != cudaSuccess) return e;
+            }
+        return cudaSuccess;
+    };
     for (int it = 0; it < iters; it++) {
+        if (ctx->d.tcut) {   // NEXT-4(c) time cut: the phases of enqueue_iteration_tc
+            for (int r = 0; r < n; r++) launch_stage_tc(ctxs[r]->d, ctxs[r]->s);
+            CK(sync_all());
+            CK(allgather(&Dev::tc_stage_send, &Dev::tc_stage_recv, (size_t)ctx->d.G * ctx->d.Tmax * 4));
+            CK(sync_all());
+            for (int r = 0; r < n; r++) {
+                ucac_ctx *c = ctxs[r];
+                launch_dp_tc(c->d, c->s);
+                launch_kernel(c, K_GENX, c->s);
+                launch_pack_tc2(c->d, c->s);
+            }
+            CK(sync_all());
+            CK(allgather(&Dev::tc2_send, &Dev::tc2_recv, (size_t)ctx->d.G * 2));
+            CK(sync_all());
+            for (int r = 0; r < n; r++) {
+                ucac_ctx *c = ctxs[r];
+                launch_unpack_tc2(c->d, c->s);
+                const int seq[] = {K_BRANCH, K_UBAR, K_BUS, K_BRANCH_AL, K_BUS_LATE, K_ROWS, K_FOLD, K_ROWS_LATE};
+                for (int k : seq) launch_kernel(c, k, c->s);
+                launch_pack_tc3(c->d, c->s);
+            }
+            CK(sync_all());
+            CK(allgather(&Dev::tc3_send, &Dev::tc3_recv, (size_t)ctx->d.G * 12));
+            CK(sync_all());
+            for (int r = 0; r < n; r++) launch_unpack_tc3(ctxs[r]->d, ctxs[r]->s);
+            CK(sync_all());
+        } else {
         for (int r = 0; r < n; r++) {
             ucac_ctx *c = ctxs[r];
             const int ph1[] = {K_BRANCH, K_GEN, K_GENX, K_UBAR, K_BRANCH_AL};
@@ -912,6 +1056,7 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
             launch_kernel(c, K_ROWS_LATE, c->s);
         }
         CK(sync_all());
+        }
         if (n > 1) {
             std::vector<double> all((size_t)n * NREC), red(NREC, 0.0);
             for (int r = 0; r < n; r++)
@@ -1202,7 +1347,17 @@ extern "C" ucac_status ucac_uc_warm_start(const ucac_network *net, const ucac_ho
 }
 
 extern "C" ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids, int32_t *count) {
-    if (!ctx || !count || which < 0 || which > 2) return UCAC_EINVAL;
+    if (!ctx || !count || which < 0 || which > 3) return UCAC_EINVAL;
+    if (which == 3) {
+        *count = 4;
+        if (ids) {
+            ids[0] = ctx->P.t_off;
+            ids[1] = ctx->P.own0;
+            ids[2] = ctx->P.own1;
+            ids[3] = ctx->P.T;
+        }
+        return UCAC_OK;
+    }
     const std::vector<int> &v = which == 0 ? ctx->P.gen_global : (which == 1 ? ctx->P.branch_global : ctx->P.bus_global);
     *count = (int32_t)v.size();
     if (ids) std::copy(v.begin(), v.end(), ids);
@@ -1359,5 +1514,33 @@ extern "C" ucac_status ucac_debug_poison(ucac_ctx *ctx, int32_t field, int64_t i
     CK(cudaMemcpyAsync(base + index, &nan, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
     CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));   // the pipelined DP read the old value
     CK(cudaStreamSynchronize(ctx->s));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_time_split(int32_t T, int32_t nranks, int32_t rank, int32_t *out) {
+    if (T < 1 || nranks < 1 || nranks > T || rank < 0 || rank >= nranks || !out) return UCAC_EINVAL;
+    std::vector<int> t0;
+    time_split(T, nranks, t0);
+    const int g0 = t0[rank], g1 = t0[rank + 1];
+    const int hl = g0 > 0, hh = g1 < T;
+    out[0] = g0 - hl;                 // global period of local period 0
+    out[1] = hl;                      // first owned local period
+    out[2] = hl + (g1 - g0);          // end of the owned local periods
+    out[3] = (g1 - g0) + hl + hh;     // local periods (halos included)
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_comm_info(ucac_ctx *ctx, int32_t *nranks, int32_t *rank) {
+    if (!ctx || !nranks || !rank) return UCAC_EINVAL;
+    if (ctx->comm) {   // what the NCCL communicator itself reports
+        int n = 0, r = 0;
+        NK(ncclCommCount(ctx->comm, &n));
+        NK(ncclCommUserRank(ctx->comm, &r));
+        *nranks = n;
+        *rank = r;
+    } else {
+        *nranks = ctx->nranks;
+        *rank = ctx->rank;
+    }
     return UCAC_OK;
 }

@@ -64,6 +64,14 @@ struct Dev {
     int uc_fixed;                     // 1: k_gen keeps u (NEXT-2)
     int variant;                      // NEXT-3 bitmask: 1 = AL for every rated branch, 2 = wbar clip
     int strict;                       // strict_fp parity mode: oracle quotients / operation order (k_strict.cu)
+    // ---- periods (NEXT-4(c) time cut): local period t is global period t + t_off of Tg; the kernels
+    // update the owned periods [own0, own1) only (single GPU / bus cut: 0, T, T, 0)
+    int t_off, Tg, own0, own1;
+    int tcut, Tmax, rank;                   // time cut on; longest owned range of any rank
+    const int *tc_t0;                 // [nranks + 1] owned global period ranges of the ranks
+    double *tc_stage_send, *tc_stage_recv;   // [G][Tmax][4], [nranks][G][Tmax][4]: DP stage costs
+    double *tc2_send, *tc2_recv;             // [G][2], [nranks][G][2]: p, phat of the first owned period
+    double *tc3_send, *tc3_recv;             // [G][12], [nranks][G][12]: the boundary values sent forward
 
     // ---- static generator data [G]
     const int *gbus, *tu, *td, *u0, *hold;
@@ -110,7 +118,11 @@ struct Dev {
     unsigned *bmark;                  // [B*T] = stamp(iteration) if an incident (l,t) is queued:
                                       // its bus solve waits for the AL tail (k_bus_late)
     unsigned *rmark[2];               // [(L+Lph)*T] per side: = stamp if that end's bus is marked
-    int nblk_lbus, nblk_lrows;        // late-phase grids (1024-thread blocks)
+    int nblk_lbus, nblk_lrows;        // late-phase grids (one wave over the compacted lists)
+    int *lbus;                        // [nblk_bus][BUS_THREADS]: marked bus-periods, per k_bus block
+    unsigned *lbus_cnt;               // [nblk_bus] their counts
+    int *lrow;                        // [nblk_rows][2 ROWS_THREADS]: marked ends (k << 1 | side), per k_rows block
+    unsigned *lrow_cnt;               // [nblk_rows]
     double *part_lbus, *part_lrows;   // their block partials
     double *part_efold;               // [fold_blocks()][NPART] first-level fold of the early partials
     double *rec_part;                 // [3][NPART] folded records: early, bus late, rows late
@@ -152,6 +164,9 @@ struct TlGuard {
 #endif
 
 __host__ __device__ inline size_t gi(const Dev &d, int g, int t) { return (size_t)g * d.T + t; }
+// owned local period / its global index (time cut, NEXT-4(c)); trivially true / t otherwise
+__device__ __forceinline__ bool own_t(const Dev &d, int t) { return t >= d.own0 && t < d.own1; }
+__device__ __forceinline__ int tglob(const Dev &d, int t) { return t + d.t_off; }
 
 // SPEC S:322 non-finite handling: the first kernel that meets a NaN/inf records (kernel,
 // component, period, iteration); ucac_iterate / ucac_residuals then return UCAC_ENUMERIC
@@ -174,6 +189,13 @@ namespace ucac {
 void launch_branch(const Dev &d, cudaStream_t s);
 void launch_branch_al(const Dev &d, cudaStream_t s);
 void launch_branch_strict(const Dev &d, cudaStream_t s);
+// time cut (NEXT-4(c)): DP stage costs of the owned periods, the full-horizon DP, boundary exchange
+void launch_stage_tc(const Dev &d, cudaStream_t s);
+void launch_dp_tc(const Dev &d, cudaStream_t s);
+void launch_pack_tc2(const Dev &d, cudaStream_t s);
+void launch_unpack_tc2(const Dev &d, cudaStream_t s);
+void launch_pack_tc3(const Dev &d, cudaStream_t s);
+void launch_unpack_tc3(const Dev &d, cudaStream_t s);
 // Launch with the device's highest execution priority (a launch attribute, kept by graph capture):
 // the generator chain (k_gen, k_genx, k_ubar) forks at the start of the iteration and should take
 // SM slots as k_branch blocks retire rather than queue behind them.

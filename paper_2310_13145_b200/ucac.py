@@ -65,7 +65,7 @@ class Params(C.Structure):
 
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("comm_mode", C.c_int32),
-                ("nccl_id", C.c_ubyte * 128), ("bus_part", ip), ("bus_xy", dp)]
+                ("nccl_id", C.c_ubyte * 128), ("bus_part", ip), ("bus_xy", dp), ("cut", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -169,6 +169,10 @@ def _declare(L):
     L.ucac_local_map.restype = C.c_int
     L.ucac_debug_poison.argtypes = [C.c_void_p, C.c_int32, C.c_int64]
     L.ucac_debug_poison.restype = C.c_int
+    L.ucac_comm_info.argtypes = [C.c_void_p, ip, ip]
+    L.ucac_comm_info.restype = C.c_int
+    L.ucac_time_split.argtypes = [C.c_int32, C.c_int32, C.c_int32, ip]
+    L.ucac_time_split.restype = C.c_int
     L.ucac_measure_fp64_peak.argtypes = [C.c_int32, dp, dp]
     L.ucac_measure_fp64_peak.restype = C.c_int
 
@@ -177,7 +181,7 @@ EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed",
             "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
             "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start",
-            "ucac_debug_poison", "ucac_measure_fp64_peak"]
+            "ucac_debug_poison", "ucac_measure_fp64_peak", "ucac_time_split", "ucac_comm_info"]
 
 
 def _check(rc, h=None):
@@ -227,7 +231,8 @@ class Context:
 
     def __init__(self, pb, pr, stream: int = 0, dist: dict | None = None):
         """dist: None (one GPU) or {"rank", "nranks", "comm_mode" (0 NCCL / 1 loopback group),
-        "nccl_id" (bytes, mode 0), "bus_part" (optional), "bus_xy" (optional)}"""
+        "nccl_id" (bytes, mode 0), "bus_part" (optional), "bus_xy" (optional),
+        "cut" (0 bus-graph cut, 1 time cut NEXT-4(c))}"""
         self.L = lib()
         pb = pb.normalized()
         self.pb, self.pr = pb, pr
@@ -248,6 +253,7 @@ class Context:
             dist_c.bus_part = a(np.asarray(dist["bus_part"], dtype=np.int32), ip) if dist.get("bus_part") is not None else None
             xy = dist.get("bus_xy", pb.bus_xy)
             dist_c.bus_xy = a(np.asarray(xy, dtype=np.float64).reshape(-1)) if xy is not None else None
+            dist_c.cut = int(dist.get("cut", 0))
         h = C.c_void_p()
         rc = self.L.ucac_create(C.byref(net), C.byref(hz), C.byref(co), C.byref(uc), C.byref(prm),
                                 C.byref(dist_c) if dist_c is not None else None,
@@ -262,6 +268,11 @@ class Context:
             ids = np.zeros(cnt.value, dtype=np.int32)
             _check(self.L.ucac_local_map(self.h, which, ids.ctypes.data_as(ip), C.byref(cnt)), self.h)
             self._local[name] = ids
+        per = np.zeros(4, dtype=np.int32)
+        cnt = C.c_int32(0)
+        _check(self.L.ucac_local_map(self.h, 3, per.ctypes.data_as(ip), C.byref(cnt)), self.h)
+        # local periods: global index of local period 0, owned [own0, own1), local count
+        self.t_off, self.own0, self.own1, self.Tl = (int(v) for v in per)
 
     def local_ids(self, which: str) -> np.ndarray:
         """global ids of the local generators / branches / owned buses (state layout order)"""
@@ -294,6 +305,12 @@ class Context:
         """NEXT-4(b), R53: new penalty classes between iterations (ucac_set_rho)."""
         _check(self.L.ucac_set_rho(self.h, float(rho_pq), float(rho_va), float(rho_uc)), self.h)
 
+    def comm_info(self) -> dict:
+        """ucac_comm_info: the communicator's own rank count and rank (NCCL contexts)"""
+        n, r = C.c_int32(), C.c_int32()
+        _check(self.L.ucac_comm_info(self.h, C.byref(n), C.byref(r)), self.h)
+        return {"nranks": n.value, "rank": r.value}
+
     def poison(self, field: str, index: int):
         """fault injection (ucac_debug_poison): NaN into one element of zb / yb / zg / yg"""
         _check(self.L.ucac_debug_poison(self.h, {"zb": 0, "yb": 1, "zg": 2, "yg": 3}[field], int(index)), self.h)
@@ -318,9 +335,8 @@ class Context:
         return {n: getattr(r, n) for n, _ in Report._fields_}
 
     def solution(self) -> dict:
-        pb = self.pb
-        GT, LT, BT = (len(self._local["gen"]) * pb.T, len(self._local["branch"]) * pb.T,
-                      len(self._local["bus"]) * pb.T)
+        GT, LT, BT = (len(self._local["gen"]) * self.Tl, len(self._local["branch"]) * self.Tl,
+                      len(self._local["bus"]) * self.Tl)
         out = {"u_on": np.zeros(GT, np.int8), "p": np.zeros(GT), "q": np.zeros(GT), "wbar": np.zeros(BT),
                "thetabar": np.zeros(BT), "flows": np.zeros(4 * LT)}
         s = Solution(out["u_on"].ctypes.data_as(i8p), *[out[k].ctypes.data_as(dp) for k in
@@ -329,9 +345,8 @@ class Context:
         return out
 
     def _sizes(self):
-        pb = self.pb
-        GT, LT, BT = (len(self._local["gen"]) * pb.T, len(self._local["branch"]) * pb.T,
-                      len(self._local["bus"]) * pb.T)
+        GT, LT, BT = (len(self._local["gen"]) * self.Tl, len(self._local["branch"]) * self.Tl,
+                      len(self._local["bus"]) * self.Tl)
         return {"GT": GT, "12GT": 12 * GT, "4LT": 4 * LT, "3LT": 3 * LT, "8LT": 8 * LT, "BT": BT, "8": 8}
 
     def get_state(self) -> dict:
@@ -411,6 +426,13 @@ def halo_lists(pb, part, rank: int) -> dict:
     return out
 
 
+def time_split(T: int, nranks: int, rank: int) -> dict:
+    """ucac_time_split: the periods of `rank` under the time cut (host only)"""
+    out = np.zeros(4, dtype=np.int32)
+    _check(lib().ucac_time_split(int(T), int(nranks), int(rank), out.ctypes.data_as(ip)), None)
+    return {"t_off": int(out[0]), "own0": int(out[1]), "own1": int(out[2]), "Tl": int(out[3])}
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     _check(lib().ucac_nccl_unique_id(buf), None)
@@ -423,31 +445,49 @@ def iterate_group(ctxs, iters: int):
     _check(lib().ucac_iterate_group(arr, len(ctxs), iters), ctxs[0].h)
 
 
+def local_part(ctx) -> dict:
+    """what a rank contributes to the global state: its local component ids, periods and state"""
+    return {"gen": ctx.local_ids("gen"), "branch": ctx.local_ids("branch"), "bus": ctx.local_ids("bus"),
+            "t_off": ctx.t_off, "own0": ctx.own0, "own1": ctx.own1, "Tl": ctx.Tl, "state": ctx.get_state()}
+
+
 def assemble_state(pb, ctxs) -> dict:
-    """global canonical state from the local states of a partition group"""
+    """global canonical state from the local states of a partition group (contexts, or the
+    local_part() dicts of the ranks)"""
+    return assemble_parts(pb, [c if isinstance(c, dict) else local_part(c) for c in ctxs])
+
+
+def assemble_parts(pb, parts) -> dict:
     pb = pb.normalized()
     T, G, L, B = pb.T, pb.ngen, pb.nbranch, pb.nbus
     out = {n: np.zeros({"GT": G * T, "12GT": 12 * G * T, "4LT": 4 * L * T, "3LT": 3 * L * T, "8LT": 8 * L * T,
                         "BT": B * T, "8": 8}[s], dtype=t) for n, t, s in STATE_FIELDS}
-    for c in ctxs:
-        st = c.get_state()
-        g, l, b = c.local_ids("gen"), c.local_ids("branch"), c.local_ids("bus")
-        gi = (g[:, None] * T + np.arange(T)).reshape(-1)
-        li = (l[:, None] * T + np.arange(T)).reshape(-1)
-        bi = (b[:, None] * T + np.arange(T)).reshape(-1)
+    for c in parts:
+        st = c["state"]
+        g, l, b = (np.asarray(c[k]) for k in ("gen", "branch", "bus"))
+        # the owned periods of this part (all of them unless time cut): local -> global index
+        tl = np.arange(c["own0"], c["own1"])
+        tg = tl + c["t_off"]
+        Tl = c["Tl"]
+        gl = (np.arange(len(g))[:, None] * Tl + tl).reshape(-1)
+        ll = (np.arange(len(l))[:, None] * Tl + tl).reshape(-1)
+        bl = (np.arange(len(b))[:, None] * Tl + tl).reshape(-1)
+        gi = (g[:, None] * T + tg).reshape(-1)
+        li = (l[:, None] * T + tg).reshape(-1)
+        bi = (b[:, None] * T + tg).reshape(-1)
         for n, t, s in STATE_FIELDS:
             v = st[n]
             if s == "GT":
-                out[n][gi] = v
+                out[n][gi] = v[gl]
             elif s == "12GT":
-                out[n].reshape(12, -1)[:, gi] = v.reshape(12, -1)
+                out[n].reshape(12, -1)[:, gi] = v.reshape(12, -1)[:, gl]
             elif s == "8LT":
-                out[n].reshape(8, -1)[:, li] = v.reshape(8, -1)
+                out[n].reshape(8, -1)[:, li] = v.reshape(8, -1)[:, ll]
             elif s in ("4LT", "3LT"):
                 k = 4 if s == "4LT" else 3
-                out[n].reshape(-1, k)[li] = v.reshape(-1, k)
+                out[n].reshape(-1, k)[li] = v.reshape(-1, k)[ll]
             elif s == "BT":
-                out[n][bi] = v
+                out[n][bi] = v[bl]
             else:
                 out[n] = v
     return out

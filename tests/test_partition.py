@@ -97,3 +97,52 @@ def test_halo_consistent_across_gloo_ranks(world, name):
         p.join(timeout=120)
     assert res[0], res[1]
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _time_split_worker(rank, world, port, T, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = ucac.time_split(T, world, rank)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine)
+    ok, msg = True, []
+    try:
+        # owned global ranges tile [0, T) in rank order
+        owned = [(g["t_off"] + g["own0"], g["t_off"] + g["own1"]) for g in gathered]
+        assert owned[0][0] == 0 and owned[-1][1] == T
+        assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(owned, owned[1:]))
+        for r, g in enumerate(gathered):
+            lo, hi = g["t_off"], g["t_off"] + g["Tl"]   # local periods, halos included
+            # a halo below iff not the horizon's start: the previous rank's last owned period
+            assert (g["own0"] == 1) == (r > 0) and (r == 0 or lo == owned[r - 1][1] - 1)
+            # a halo above iff not the horizon's end: the next rank's first owned period
+            assert (hi > owned[r][1]) == (r < world - 1) and (r == world - 1 or hi - 1 == owned[r + 1][0])
+    except AssertionError as e:
+        ok = False
+        msg.append(str(e))
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    if rank == 0:
+        out.put((all(flags), msg))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T", [(2, 24), (3, 48), (2, 3)])
+def test_time_split_consistent_across_gloo_ranks(world, T):
+    """NEXT-4(c) host logic: every rank's period split (ucac_time_split) agrees with its
+    neighbours' -- the owned ranges tile the horizon and each halo period is the neighbour's
+    boundary period (the values exchanged there)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_time_split_worker, args=(r, world, port, T, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert res[0], res[1]
+    assert all(p.exitcode == 0 for p in procs)
+    with pytest.raises(ucac.UcacError):
+        ucac.time_split(3, 4, 0)

@@ -18,7 +18,7 @@ from paper_2310_13145_b200 import inputs  # noqa: E402
 
 def profile(name="pegase2869", iters=10):
     pb, pr = inputs.build_config(name)
-    o = oracle.Oracle(pb, pr)
+    o = oracle.Oracle(pb, pr, omp=True)
     o.iterate(int(iters))
     s = o.get_state()
     L, T = pb.nbranch, pb.T
