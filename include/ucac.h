@@ -130,6 +130,7 @@ typedef struct {
     unsigned char nccl_id[128];     /* ncclUniqueId (comm_mode 0)                          */
     const int32_t *bus_part;        /* [nbus] owner rank, or NULL = ucac_partition(bus_xy)  */
     const double *bus_xy;           /* [nbus*2] bus coordinates for the partitioner, or NULL */
+    const double *branch_w;         /* [nbranch] partition weights (ucac_partition), or NULL = 1  */
     int32_t cut;                    /* 0 = bus-graph cut (above); 1 = time cut (NEXT-4(c), SURVEY
                                        8(f) row 4; P:166-167 temporal decomposition): rank r owns the
                                        periods [r T / n, (r+1) T / n) of every component, keeps one
@@ -141,11 +142,15 @@ typedef struct {
                                        T >= nranks; variant bits 4 and 16 are EUNSUPPORTED. */
 } ucac_dist;
 
-/* Deterministic bus-graph cut: weighted recursive coordinate bisection on bus_xy (weights
- * 1 + branches owned, balancing the branch solves), or weighted BFS-order chunks when bus_xy
- * is NULL.  part[nbus] receives ranks in [0, nparts).  Host only (no device needed). */
+/* Deterministic bus-graph cut: weighted recursive coordinate bisection on bus_xy, or weighted
+ * BFS-order chunks when bus_xy is NULL, then a greedy boundary refinement with Fiduccia-Mattheyses
+ * gains (a bus moves to a neighbouring part when that cuts fewer branches and both parts stay
+ * within 5 % of the mean weight; index order, deterministic).  Bus weight = 1 + the weights of its
+ * owned branches (branch_w[nbranch], NULL = 1 each: the branch solves dominate; pass the expected
+ * per-branch solve work, e.g. 1 + its thermal-AL share, to balance the AL tail).  part[nbus]
+ * receives ranks in [0, nparts).  Host only (no device needed). */
 ucac_status ucac_partition(int32_t nbus, int32_t nbranch, const int32_t *br_from, const int32_t *br_to,
-                           const double *bus_xy, int32_t nparts, int32_t *part);
+                           const double *bus_xy, int32_t nparts, int32_t *part, const double *branch_w);
 /* Halo of rank `rank` under `part` (host only): sizes[6] = owned buses, ghost buses, local
  * branches, phantom branches (remote branches whose to-bus is owned), cut branches (local
  * branches with a remote to-bus), export buses (owned to-buses of phantoms); the lists (global
@@ -163,6 +168,22 @@ ucac_status ucac_time_split(int32_t T, int32_t nranks, int32_t rank, int32_t *ou
 /* The context's communicator: ncclCommCount / ncclCommUserRank for an NCCL context (comm_mode 0),
  * else the ucac_dist ranks (1 / 0 for a single-GPU context). */
 ucac_status ucac_comm_info(ucac_ctx *ctx, int32_t *nranks, int32_t *rank);
+
+/* Device-initiated exchange of the time cut (NEXT-4(c)): the three exchanges of
+ * each iteration (stage costs to every rank, the boundary values to the neighbours) become stores
+ * by the sender's blocks into the receivers' buffers in peer memory, published by a system-scope
+ * release of the iteration's epoch in the receivers' flags; the receivers spin on acquire loads.
+ * Only the S8 all-reduce stays on NCCL.  Ranks of at most 8 (one NVSwitch node).
+ * ucac_p2p_export: this context's blob (UCAC_P2P_BLOB bytes: a CUDA IPC handle of its receive
+ * buffers + offsets); the caller all-gathers the blobs of the ranks (rank order) and passes them to
+ * ucac_p2p_import on every rank, which maps the peers (cudaIpcOpenMemHandle) and re-captures the
+ * iteration graph.  ucac_p2p_group: the same for a comm_mode-1 loopback group on one device, where
+ * every exchange is one cooperative launch over all ranks' blocks (co-resident, so their waits
+ * cannot deadlock).  EUNSUPPORTED unless time cut. */
+#define UCAC_P2P_BLOB 96
+ucac_status ucac_p2p_export(ucac_ctx *ctx, unsigned char *blob);
+ucac_status ucac_p2p_import(ucac_ctx *ctx, const unsigned char *blobs /* [nranks * UCAC_P2P_BLOB] */);
+ucac_status ucac_p2p_group(ucac_ctx **ctxs, int32_t n);
 
 /* Create a context: validate (EINVAL with a message: non-finite data, vmin <= 0 or
  * vmin > vmax, pmin > pmax, qmin > qmax, c2 < 0, min_up/min_dn outside [1,T], hold outside

@@ -29,6 +29,7 @@ UNITS = {
     "k_sweep.cu": ["-fmad=false"],
     "k_strict.cu": ["-fmad=false"],
     "k_measure.cu": [],
+    "k_xchg.cu": [],
     "ucac.cu": [],
     "partition.cu": [],
 }

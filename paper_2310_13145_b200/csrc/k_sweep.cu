@@ -320,7 +320,18 @@ __device__ __forceinline__ int block_offsets(const unsigned *cnt, int n, int *pr
     __shared__ int wsum[32];
     const int nt = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
     // one coalesced pass of independent loads into shared memory, then the scan from there
-    for (int i = threadIdx.x; i < n; i += nt) pre[i] = (int)__ldcg(cnt + i);
+    // (unrolled so all of a thread's loads are in flight together: one L2 round trip, not n / nt)
+    {
+        constexpr int U = 16;
+        for (int i0 = threadIdx.x; i0 < n; i0 += U * nt) {
+            int v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) v[u] = i0 + u * nt < n ? (int)__ldcg(cnt + i0 + u * nt) : 0;
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (i0 + u * nt < n) pre[i0 + u * nt] = v[u];
+        }
+    }
     __syncthreads();
     const int per = (n + nt - 1) / nt;
     const int beg = min(n, (int)threadIdx.x * per), end = min(n, beg + per);

@@ -54,16 +54,63 @@ static void rcb(std::vector<int> &idx, const double *xy, const std::vector<doubl
     rcb(b, xy, w, p0 + n1, np - n1, part);
 }
 
+// Greedy boundary refinement with Fiduccia-Mattheyses gains: a bus moves to the neighbouring part
+// that cuts the most incident branches less (gain = branches to that part - branches to its own),
+// if the gain is positive and both parts stay within +-tol of the mean weight.  Buses in index
+// order, passes until no move (at most 20): deterministic, and the cut only shrinks.
+static void fm_refine(int nbus, int nbranch, const int32_t *from, const int32_t *to, const std::vector<double> &w,
+                      int nparts, int32_t *part, double tol) {
+    std::vector<std::vector<int>> adj(nbus);
+    for (int l = 0; l < nbranch; l++) {
+        adj[from[l]].push_back(to[l]);
+        adj[to[l]].push_back(from[l]);
+    }
+    std::vector<double> load(nparts, 0.0);
+    double tot = 0.0;
+    for (int i = 0; i < nbus; i++) {
+        load[part[i]] += w[i];
+        tot += w[i];
+    }
+    const double hi = (1.0 + tol) * tot / nparts, lo = (1.0 - tol) * tot / nparts;
+    std::vector<int> cnt(nparts, 0);
+    for (int pass = 0; pass < 20; pass++) {
+        int moved = 0;
+        for (int i = 0; i < nbus; i++) {
+            const int a = part[i];
+            for (int v : adj[i]) cnt[part[v]]++;
+            int best = a, bg = 0;
+            for (int v : adj[i]) {
+                const int b = part[v];
+                const int g = cnt[b] - cnt[a];
+                if (b != a && (g > bg || (g == bg && best != a && b < best)) && load[b] + w[i] <= hi && load[a] - w[i] >= lo) {
+                    best = b;
+                    bg = g;
+                }
+            }
+            for (int v : adj[i]) cnt[part[v]] = 0;
+            if (best != a && bg > 0) {
+                part[i] = best;
+                load[a] -= w[i];
+                load[best] += w[i];
+                moved++;
+            }
+        }
+        if (!moved) break;
+    }
+}
+
 int partition_buses(int nbus, int nbranch, const int32_t *from, const int32_t *to, const double *xy, int nparts,
-                    int32_t *part) {
+                    int32_t *part, const double *branch_w) {
     if (nbus <= 0 || nparts <= 0 || nparts > nbus) return 1;
-    // weight: one unit per bus plus one per owned branch (the branch solves dominate)
+    // weight: one unit per bus plus, per owned branch, its expected solve work (1 when not given; a
+    // caller can pass e.g. 1 + the branch's thermal-AL Newton share)
     std::vector<double> w(nbus, 1.0);
-    for (int l = 0; l < nbranch; l++) w[from[l]] += 1.0;
+    for (int l = 0; l < nbranch; l++) w[from[l]] += branch_w ? branch_w[l] : 1.0;
     if (xy) {
         std::vector<int> idx(nbus);
         std::iota(idx.begin(), idx.end(), 0);
         rcb(idx, xy, w, 0, nparts, part);
+        fm_refine(nbus, nbranch, from, to, w, nparts, part, 0.05);
         return 0;
     }
     // no coordinates: BFS order from bus 0 (neighbours in id order), contiguous weighted chunks
@@ -97,6 +144,7 @@ int partition_buses(int nbus, int nbranch, const int32_t *from, const int32_t *t
         part[i] = p;
         acc += w[i];
     }
+    fm_refine(nbus, nbranch, from, to, w, nparts, part, 0.05);
     return 0;
 }
 
@@ -163,11 +211,11 @@ Halo build_halo(int nbus, int nbranch, const int32_t *from, const int32_t *to, c
 }  // namespace ucac
 
 extern "C" ucac_status ucac_partition(int32_t nbus, int32_t nbranch, const int32_t *br_from, const int32_t *br_to,
-                                      const double *bus_xy, int32_t nparts, int32_t *part) {
+                                      const double *bus_xy, int32_t nparts, int32_t *part, const double *branch_w) {
     if (!br_from || !br_to || !part || nbus <= 0 || nbranch < 0 || nparts < 1 || nparts > nbus) return UCAC_EINVAL;
     for (int l = 0; l < nbranch; l++)
         if (br_from[l] < 0 || br_from[l] >= nbus || br_to[l] < 0 || br_to[l] >= nbus) return UCAC_EINVAL;
-    return ucac::partition_buses(nbus, nbranch, br_from, br_to, bus_xy, nparts, part) ? UCAC_EINVAL : UCAC_OK;
+    return ucac::partition_buses(nbus, nbranch, br_from, br_to, bus_xy, nparts, part, branch_w) ? UCAC_EINVAL : UCAC_OK;
 }
 
 extern "C" ucac_status ucac_halo_lists(int32_t nbus, int32_t nbranch, const int32_t *br_from, const int32_t *br_to,

@@ -246,6 +246,11 @@ struct ucac_ctx {
     std::vector<cudaEvent_t> tev;        // timed-iteration event pool
     ucac_params prm{};
     bool ctl_dirty = true;               // device control fields may hold a stop/done state
+    void *xbuf = nullptr;                // time cut: receive buffers + flags (cudaMalloc, IPC-mappable)
+    size_t xoff[4] = {0, 0, 0, 0}, xbytes = 0;
+    std::vector<void *> peer_maps;       // CUDA IPC mappings of the peers' xbuf
+    Dev *xdevs = nullptr;                // loopback group: device copy of the group's Dev records
+    ncclResult_t nccl_err = ncclSuccess; // first failed collective of a graph capture
 };
 
 #define CK(call)                                                                           \
@@ -442,7 +447,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
                 if (dist->bus_part[i] < 0 || dist->bus_part[i] >= nranks) return fail(nullptr, UCAC_EINVAL, "bus_part out of range");
                 part[i] = dist->bus_part[i];
             }
-        } else if (partition_buses(net->nbus, net->nbranch, net->br_from, net->br_to, dist->bus_xy, nranks, part.data())) {
+        } else if (partition_buses(net->nbus, net->nbranch, net->br_from, net->br_to, dist->bus_xy, nranks, part.data(),
+                                   dist->branch_w)) {
             return fail(nullptr, UCAC_EINVAL, "partitioner failed");
         }
         // every rank checks every part (the partition is global and deterministic), so a part
@@ -648,13 +654,11 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.xsend2 = A.take<double>((size_t)P.max_export * 6 * T);
         d.xrecv2 = A.take<double>((size_t)nranks * P.max_export * 6 * T);
         d.st = A.take<DevStatus>(1);
-        if (tcut) {
+        if (tcut) {   // (the receive buffers live in ctx->xbuf, a plain cudaMalloc block peers can map)
             d.tc_stage_send = A.take<double>((size_t)G * P.Tmax * 4);
-            d.tc_stage_recv = A.take<double>((size_t)nranks * G * P.Tmax * 4);
             d.tc2_send = A.take<double>((size_t)G * 2);
-            d.tc2_recv = A.take<double>((size_t)nranks * G * 2);
             d.tc3_send = A.take<double>((size_t)G * 12);
-            d.tc3_recv = A.take<double>((size_t)nranks * G * 12);
+            d.xarrive = A.take<unsigned>(3);
         }
         d.rmark[0] = A.take<unsigned>((size_t)(L + P.Lp) * T);
         d.rmark[1] = A.take<unsigned>((size_t)(L + P.Lp) * T);
@@ -689,6 +693,21 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
             return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
         // the pageable staging buffer must outlive the copy
         if (cudaStreamSynchronize(ctx->s) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
+    }
+    if (tcut) {
+        // receive buffers and arrival flags of the time cut's exchanges, one cudaMalloc block (not
+        // the pool arena) so a device-initiated exchange can map it from other processes (CUDA IPC)
+        const size_t a0 = 0, a1 = a0 + (size_t)nranks * G * P.Tmax * 4 * 8, a2 = a1 + (size_t)nranks * G * 2 * 8,
+                     a3 = a2 + (size_t)nranks * G * 12 * 8, a4 = a3 + 3 * UCAC_MAX_P2P * 8;
+        if (cudaMalloc(&ctx->xbuf, a4) != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "exchange buffers"));
+        if (cudaMemset(ctx->xbuf, 0, a4) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "exchange buffers"));
+        char *xb = (char *)ctx->xbuf;
+        d.tc_stage_recv = (double *)(xb + a0);
+        d.tc2_recv = (double *)(xb + a1);
+        d.tc3_recv = (double *)(xb + a2);
+        d.xflags = (unsigned long long *)(xb + a3);
+        ctx->xoff[0] = a0; ctx->xoff[1] = a1; ctx->xoff[2] = a2; ctx->xoff[3] = a3;
+        ctx->xbytes = a4;
     }
     // status: beta = beta0, k = 1 (R21)
     DevStatus st0{};
@@ -757,25 +776,35 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
 // owned period go to the previous rank (its ramp-copy and ramp-up rows at the boundary), and the
 // boundary values the previous rank computed (ubar, pbar of its last period, the ramp rows of this
 // rank's first period) come back after (7c)/(7d); one all-reduce of the S8 record.
+// NCCL return codes of the captured collectives: the first failure is kept and reported by build_graphs
+#define NC(call)                                                              \
+    do {                                                                      \
+        ncclResult_t r_ = (call);                                             \
+        if (r_ != ncclSuccess && ctx->nccl_err == ncclSuccess) ctx->nccl_err = r_; \
+    } while (0)
 static void enqueue_iteration_tc(ucac_ctx *ctx) {
     const Dev &d = ctx->d;
     cudaStream_t s = ctx->s;
+    // d.p2p: the three exchanges are device-initiated stores into the peers' buffers (k_xchg.cu)
     launch_stage_tc(d, s);
-    ncclAllGather(d.tc_stage_send, d.tc_stage_recv, (size_t)d.G * d.Tmax * 4, ncclDouble, ctx->comm, s);
+    if (d.p2p) launch_xchg(d, 1, s);
+    else NC(ncclAllGather(d.tc_stage_send, d.tc_stage_recv, (size_t)d.G * d.Tmax * 4, ncclDouble, ctx->comm, s));
     launch_dp_tc(d, s);
     launch_kernel(ctx, K_GENX, s);
     launch_pack_tc2(d, s);
-    ncclAllGather(d.tc2_send, d.tc2_recv, (size_t)d.G * 2, ncclDouble, ctx->comm, s);
+    if (d.p2p) launch_xchg(d, 2, s);
+    else NC(ncclAllGather(d.tc2_send, d.tc2_recv, (size_t)d.G * 2, ncclDouble, ctx->comm, s));
     launch_unpack_tc2(d, s);
     const int seq[] = {K_BRANCH, K_UBAR, K_BUS, K_BRANCH_AL, K_BUS_LATE, K_ROWS, K_FOLD, K_ROWS_LATE};
     for (int k : seq) launch_kernel(ctx, k, s);
     launch_pack_tc3(d, s);
-    ncclAllGather(d.tc3_send, d.tc3_recv, (size_t)d.G * 12, ncclDouble, ctx->comm, s);
+    if (d.p2p) launch_xchg(d, 3, s);
+    else NC(ncclAllGather(d.tc3_send, d.tc3_recv, (size_t)d.G * 12, ncclDouble, ctx->comm, s));
     launch_unpack_tc3(d, s);
-    ncclGroupStart();
-    ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, s);
-    ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, s);
-    ncclGroupEnd();
+    NC(ncclGroupStart());
+    NC(ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, s));
+    NC(ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, s));
+    NC(ncclGroupEnd());
     launch_finalize(d, s);
 }
 
@@ -832,7 +861,7 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     launch_kernel(ctx, K_BRANCH_AL, ctx->s);
     if (multi && d.max_cut > 0) {
         launch_pack_tau(d, ctx->s);
-        ncclAllGather(d.xsend1, d.xrecv1, (size_t)d.max_cut * 4 * d.T, ncclDouble, ctx->comm, ctx->s);
+        NC(ncclAllGather(d.xsend1, d.xrecv1, (size_t)d.max_cut * 4 * d.T, ncclDouble, ctx->comm, ctx->s));
         launch_unpack_tau(d, ctx->s);
     }
     if (!multi) {
@@ -853,16 +882,16 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     launch_kernel(ctx, K_BUS_LATE, ctx->s);
     if (d.max_export > 0) {
         launch_pack_bus(d, ctx->s);
-        ncclAllGather(d.xsend2, d.xrecv2, (size_t)d.max_export * 6 * d.T, ncclDouble, ctx->comm, ctx->s);
+        NC(ncclAllGather(d.xsend2, d.xrecv2, (size_t)d.max_export * 6 * d.T, ncclDouble, ctx->comm, ctx->s));
         launch_unpack_bus(d, ctx->s);
     }
     launch_kernel(ctx, K_ROWS, ctx->s);
     launch_kernel(ctx, K_FOLD, ctx->s);
     launch_kernel(ctx, K_ROWS_LATE, ctx->s);
-    ncclGroupStart();
-    ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, ctx->s);
-    ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, ctx->s);
-    ncclGroupEnd();
+    NC(ncclGroupStart());
+    NC(ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, ctx->s));
+    NC(ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, ctx->s));
+    NC(ncclGroupEnd());
     launch_finalize(d, ctx->s);
 }
 
@@ -870,8 +899,13 @@ static ucac_status build_graphs(ucac_ctx *ctx) {
     for (int gi = 0; gi < 2; gi++) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
+        ctx->nccl_err = ncclSuccess;
         for (int k = 0; k < ctx->gunroll[gi]; k++) enqueue_iteration(ctx);
         CK(cudaStreamEndCapture(ctx->s, &g));
+        if (ctx->nccl_err != ncclSuccess) {
+            cudaGraphDestroy(g);
+            return fail(ctx, UCAC_ENCCL, "NCCL collective in the iteration graph: %s", ncclGetErrorString(ctx->nccl_err));
+        }
         // per-node launch priorities (launch_hi_prio) are honoured only with this flag
         cudaError_t e = cudaGraphInstantiate(&ctx->gexec[gi], g, UCAC_NODE_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
         cudaGraphDestroy(g);
@@ -989,9 +1023,17 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
     };
     for (int it = 0; it < iters; it++) {
         if (ctx->d.tcut) {   // NEXT-4(c) time cut: the phases of enqueue_iteration_tc
+            // d.p2p: each exchange is ONE cooperative launch emulating every rank's device-initiated
+            // sends and waits (k_xchg.cu); else host-driven device-to-device copies
+            std::vector<Dev> devs;
+            for (int r = 0; r < n; r++) devs.push_back(ctxs[r]->d);
+            auto exchange = [&](int phase, double *Dev::*snd, double *Dev::*rcv, size_t count) -> cudaError_t {
+                if (ctx->d.p2p) return launch_xchg_group(devs.data(), n, phase, ctx->s, ctx->xdevs);
+                return allgather(snd, rcv, count);
+            };
             for (int r = 0; r < n; r++) launch_stage_tc(ctxs[r]->d, ctxs[r]->s);
             CK(sync_all());
-            CK(allgather(&Dev::tc_stage_send, &Dev::tc_stage_recv, (size_t)ctx->d.G * ctx->d.Tmax * 4));
+            CK(exchange(1, &Dev::tc_stage_send, &Dev::tc_stage_recv, (size_t)ctx->d.G * ctx->d.Tmax * 4));
             CK(sync_all());
             for (int r = 0; r < n; r++) {
                 ucac_ctx *c = ctxs[r];
@@ -1000,7 +1042,7 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
                 launch_pack_tc2(c->d, c->s);
             }
             CK(sync_all());
-            CK(allgather(&Dev::tc2_send, &Dev::tc2_recv, (size_t)ctx->d.G * 2));
+            CK(exchange(2, &Dev::tc2_send, &Dev::tc2_recv, (size_t)ctx->d.G * 2));
             CK(sync_all());
             for (int r = 0; r < n; r++) {
                 ucac_ctx *c = ctxs[r];
@@ -1010,7 +1052,7 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
                 launch_pack_tc3(c->d, c->s);
             }
             CK(sync_all());
-            CK(allgather(&Dev::tc3_send, &Dev::tc3_recv, (size_t)ctx->d.G * 12));
+            CK(exchange(3, &Dev::tc3_send, &Dev::tc3_recv, (size_t)ctx->d.G * 12));
             CK(sync_all());
             for (int r = 0; r < n; r++) launch_unpack_tc3(ctxs[r]->d, ctxs[r]->s);
             CK(sync_all());
@@ -1472,6 +1514,9 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     for (auto ev : ctx->tev) cudaEventDestroy(ev);
     for (void *p : ctx->dalloc) cudaFreeAsync(p, ctx->s);
     if (ctx->s && !ctx->dalloc.empty()) cudaStreamSynchronize(ctx->s);
+    for (void *p : ctx->peer_maps) cudaIpcCloseMemHandle(p);
+    if (ctx->xbuf) cudaFree(ctx->xbuf);
+    if (ctx->xdevs) cudaFree(ctx->xdevs);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->st_host) pinned_status_put(ctx->st_host);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
@@ -1543,4 +1588,69 @@ extern "C" ucac_status ucac_comm_info(ucac_ctx *ctx, int32_t *nranks, int32_t *r
         *rank = ctx->rank;
     }
     return UCAC_OK;
+}
+
+// ---- device-initiated exchange of the time cut (NEXT-4(c), k_xchg.cu)
+static void set_peer(Dev &d, int q, char *xb, const size_t *off) {
+    d.peer_stage_recv[q] = (double *)(xb + off[0]);
+    d.peer_tc2_recv[q] = (double *)(xb + off[1]);
+    d.peer_tc3_recv[q] = (double *)(xb + off[2]);
+    d.peer_flags[q] = (unsigned long long *)(xb + off[3]);
+}
+
+extern "C" ucac_status ucac_p2p_group(ucac_ctx **ctxs, int32_t n) {
+    if (!ctxs || n < 2 || n > UCAC_MAX_P2P) return UCAC_EINVAL;
+    for (int r = 0; r < n; r++)
+        if (!ctxs[r] || !ctxs[r]->d.tcut || ctxs[r]->comm_mode != 1 || ctxs[r]->rank != r || ctxs[r]->nranks != n)
+            return fail(ctxs[r], UCAC_EINVAL, "p2p group: context %d is not rank %d of a time-cut loopback group", r, r);
+    for (int r = 0; r < n; r++) {
+        Dev &d = ctxs[r]->d;
+        for (int q = 0; q < n; q++) set_peer(d, q, (char *)ctxs[q]->xbuf, ctxs[q]->xoff);
+        d.p2p = 1;
+    }
+    ucac_ctx *ctx = ctxs[0];
+    if (!ctx->xdevs) CK(cudaMalloc(&ctx->xdevs, sizeof(Dev) * UCAC_MAX_P2P));
+    return UCAC_OK;
+}
+
+// blob = cudaIpcMemHandle_t of the exchange block, then its 4 offsets (uint64)
+extern "C" ucac_status ucac_p2p_export(ucac_ctx *ctx, unsigned char *blob) {
+    if (!ctx || !blob) return UCAC_EINVAL;
+    if (!ctx->d.tcut || !ctx->xbuf) return fail(ctx, UCAC_EUNSUPPORTED, "p2p: not a time-cut context");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->xbuf));
+    memcpy(blob, &h, sizeof(h));
+    uint64_t off[4] = {ctx->xoff[0], ctx->xoff[1], ctx->xoff[2], ctx->xoff[3]};
+    memcpy(blob + sizeof(h), off, sizeof(off));
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_p2p_import(ucac_ctx *ctx, const unsigned char *blobs) {
+    if (!ctx || !blobs) return UCAC_EINVAL;
+    if (!ctx->d.tcut || ctx->comm_mode != 0 || ctx->nranks > UCAC_MAX_P2P)
+        return fail(ctx, UCAC_EUNSUPPORTED, "p2p: an NCCL time-cut context of at most %d ranks", UCAC_MAX_P2P);
+    Dev &d = ctx->d;
+    for (int q = 0; q < ctx->nranks; q++) {
+        const unsigned char *b = blobs + (size_t)q * UCAC_P2P_BLOB;
+        uint64_t off64[4];
+        memcpy(off64, b + sizeof(cudaIpcMemHandle_t), sizeof(off64));
+        const size_t off[4] = {(size_t)off64[0], (size_t)off64[1], (size_t)off64[2], (size_t)off64[3]};
+        if (q == ctx->rank) {
+            set_peer(d, q, (char *)ctx->xbuf, off);
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, b, sizeof(h));
+        void *p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->peer_maps.push_back(p);
+        set_peer(d, q, (char *)p, off);
+    }
+    d.p2p = 1;
+    for (auto &g : ctx->gexec)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    return build_graphs(ctx);
 }

@@ -12,6 +12,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef UCAC_MAX_P2P
+#define UCAC_MAX_P2P 8   // ranks of a device-initiated exchange group (one node: 8 GPUs on NVSwitch)
+#endif
+
 namespace ucac {
 
 // coupling-row kinds (Eq. 5; R3 ramp-down in the Eq. 4d form, R6 ramp copy,
@@ -72,6 +76,13 @@ struct Dev {
     double *tc_stage_send, *tc_stage_recv;   // [G][Tmax][4], [nranks][G][Tmax][4]: DP stage costs
     double *tc2_send, *tc2_recv;             // [G][2], [nranks][G][2]: p, phat of the first owned period
     double *tc3_send, *tc3_recv;             // [G][12], [nranks][G][12]: the boundary values sent forward
+    // device-initiated exchange of the time cut (NEXT-4(c), k_xchg.cu): the other ranks' receive
+    // buffers and arrival flags (peer memory: CUDA IPC across GPUs, plain pointers in a loopback group)
+    int p2p;                                  // 1: the three exchanges by k_xchg instead of NCCL
+    double *peer_stage_recv[UCAC_MAX_P2P], *peer_tc2_recv[UCAC_MAX_P2P], *peer_tc3_recv[UCAC_MAX_P2P];
+    unsigned long long *peer_flags[UCAC_MAX_P2P];   // rank q's flags [3 phases][UCAC_MAX_P2P sources]
+    unsigned long long *xflags;               // mine, written by the senders
+    unsigned *xarrive;                        // [3] blocks of this rank done sending (last one signals)
 
     // ---- static generator data [G]
     const int *gbus, *tu, *td, *u0, *hold;
@@ -196,6 +207,10 @@ void launch_pack_tc2(const Dev &d, cudaStream_t s);
 void launch_unpack_tc2(const Dev &d, cudaStream_t s);
 void launch_pack_tc3(const Dev &d, cudaStream_t s);
 void launch_unpack_tc3(const Dev &d, cudaStream_t s);
+// device-initiated exchange (k_xchg.cu): phase 1 stage costs to every rank, 2 p/phat to the
+// previous rank, 3 the boundary values to the next rank; each sends, signals, then waits for its sources
+void launch_xchg(const Dev &d, int phase, cudaStream_t s);
+cudaError_t launch_xchg_group(const Dev *devs_host, int n, int phase, cudaStream_t s, Dev *scratch);
 // Launch with the device's highest execution priority (a launch attribute, kept by graph capture):
 // the generator chain (k_gen, k_genx, k_ubar) forks at the start of the iteration and should take
 // SM slots as k_branch blocks retire rather than queue behind them.

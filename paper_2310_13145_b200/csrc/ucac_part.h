@@ -19,7 +19,7 @@ struct Halo {
 };
 
 int partition_buses(int nbus, int nbranch, const int32_t *from, const int32_t *to, const double *xy, int nparts,
-                    int32_t *part);
+                    int32_t *part, const double *branch_w);
 Halo build_halo(int nbus, int nbranch, const int32_t *from, const int32_t *to, const int32_t *part, int nparts,
                 int rank);
 

@@ -65,7 +65,8 @@ class Params(C.Structure):
 
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("comm_mode", C.c_int32),
-                ("nccl_id", C.c_ubyte * 128), ("bus_part", ip), ("bus_xy", dp), ("cut", C.c_int32)]
+                ("nccl_id", C.c_ubyte * 128), ("bus_part", ip), ("bus_xy", dp), ("branch_w", dp),
+                ("cut", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -157,7 +158,7 @@ def _declare(L):
     L.ucac_last_error.restype = C.c_char_p
     L.ucac_destroy.argtypes = [C.c_void_p]
     L.ucac_destroy.restype = None
-    L.ucac_partition.argtypes = [C.c_int32, C.c_int32, ip, ip, dp, C.c_int32, ip]
+    L.ucac_partition.argtypes = [C.c_int32, C.c_int32, ip, ip, dp, C.c_int32, ip, dp]
     L.ucac_partition.restype = C.c_int
     L.ucac_halo_lists.argtypes = [C.c_int32, C.c_int32, ip, ip, ip, C.c_int32, C.c_int32, ip, ip, ip, ip, ip, ip, ip]
     L.ucac_halo_lists.restype = C.c_int
@@ -169,6 +170,12 @@ def _declare(L):
     L.ucac_local_map.restype = C.c_int
     L.ucac_debug_poison.argtypes = [C.c_void_p, C.c_int32, C.c_int64]
     L.ucac_debug_poison.restype = C.c_int
+    L.ucac_p2p_group.argtypes = [C.POINTER(C.c_void_p), C.c_int32]
+    L.ucac_p2p_group.restype = C.c_int
+    L.ucac_p2p_export.argtypes = [C.c_void_p, C.c_void_p]
+    L.ucac_p2p_export.restype = C.c_int
+    L.ucac_p2p_import.argtypes = [C.c_void_p, C.c_void_p]
+    L.ucac_p2p_import.restype = C.c_int
     L.ucac_comm_info.argtypes = [C.c_void_p, ip, ip]
     L.ucac_comm_info.restype = C.c_int
     L.ucac_time_split.argtypes = [C.c_int32, C.c_int32, C.c_int32, ip]
@@ -181,7 +188,8 @@ EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed",
             "ucac_get_solution", "ucac_get_state", "ucac_set_state", "ucac_dp_batch", "ucac_get_sizes",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
             "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start",
-            "ucac_debug_poison", "ucac_measure_fp64_peak", "ucac_time_split", "ucac_comm_info"]
+            "ucac_debug_poison", "ucac_measure_fp64_peak", "ucac_time_split", "ucac_comm_info",
+            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import"]
 
 
 def _check(rc, h=None):
@@ -254,6 +262,8 @@ class Context:
             xy = dist.get("bus_xy", pb.bus_xy)
             dist_c.bus_xy = a(np.asarray(xy, dtype=np.float64).reshape(-1)) if xy is not None else None
             dist_c.cut = int(dist.get("cut", 0))
+            if dist.get("branch_w") is not None:
+                dist_c.branch_w = a(np.asarray(dist["branch_w"], dtype=np.float64))
         h = C.c_void_p()
         rc = self.L.ucac_create(C.byref(net), C.byref(hz), C.byref(co), C.byref(uc), C.byref(prm),
                                 C.byref(dist_c) if dist_c is not None else None,
@@ -304,6 +314,18 @@ class Context:
     def set_rho(self, rho_pq: float, rho_va: float, rho_uc: float):
         """NEXT-4(b), R53: new penalty classes between iterations (ucac_set_rho)."""
         _check(self.L.ucac_set_rho(self.h, float(rho_pq), float(rho_va), float(rho_uc)), self.h)
+
+    def p2p_export(self) -> bytes:
+        """ucac_p2p_export: this rank's IPC blob for the device-initiated exchange (time cut)"""
+        buf = (C.c_ubyte * P2P_BLOB)()
+        _check(self.L.ucac_p2p_export(self.h, buf), self.h)
+        return bytes(buf)
+
+    def p2p_import(self, blobs):
+        """ucac_p2p_import: map every rank's exchange buffers (blobs in rank order)"""
+        raw = b"".join(blobs)
+        buf = (C.c_ubyte * len(raw)).from_buffer_copy(raw)
+        _check(self.L.ucac_p2p_import(self.h, buf), self.h)
 
     def comm_info(self) -> dict:
         """ucac_comm_info: the communicator's own rank count and rank (NCCL contexts)"""
@@ -400,13 +422,16 @@ def dp_batch_device(G, T, L_ptr, tu_ptr, td_ptr, u0_ptr, hold_ptr, sched_ptr, co
     _check(rc, None)
 
 
-def partition(pb, nparts: int, use_xy: bool = True) -> np.ndarray:
-    """bus -> rank (ucac_partition: weighted RCB on the bus coordinates, or BFS chunks)"""
+def partition(pb, nparts: int, use_xy: bool = True, branch_w=None) -> np.ndarray:
+    """bus -> rank (ucac_partition: weighted RCB on the bus coordinates, or BFS chunks, then FM-gain
+    boundary refinement; branch_w = per-branch solve weights or None)"""
     pb = pb.normalized()
     part = np.zeros(pb.nbus, dtype=np.int32)
     xy = np.ascontiguousarray(pb.bus_xy, dtype=np.float64).reshape(-1) if (use_xy and pb.bus_xy is not None) else None
+    bw = np.ascontiguousarray(branch_w, dtype=np.float64) if branch_w is not None else None
     rc = lib().ucac_partition(pb.nbus, pb.nbranch, pb.br_from.ctypes.data_as(ip), pb.br_to.ctypes.data_as(ip),
-                              xy.ctypes.data_as(dp) if xy is not None else None, nparts, part.ctypes.data_as(ip))
+                              xy.ctypes.data_as(dp) if xy is not None else None, nparts, part.ctypes.data_as(ip),
+                              bw.ctypes.data_as(dp) if bw is not None else None)
     _check(rc, None)
     return part
 
@@ -437,6 +462,15 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     _check(lib().ucac_nccl_unique_id(buf), None)
     return bytes(buf)
+
+
+P2P_BLOB = 96
+
+
+def p2p_group(ctxs):
+    """ucac_p2p_group: device-initiated exchanges for a time-cut loopback group (one device)"""
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    _check(lib().ucac_p2p_group(arr, len(ctxs)), ctxs[0].h)
 
 
 def iterate_group(ctxs, iters: int):

@@ -49,19 +49,25 @@ def test_group_rejects_mismatched_contexts():
         a.iterate(1)   # loopback contexts iterate as a group
 
 
-@pytest.mark.parametrize("name,P,iters", [("case30", 2, 30), ("case30", 5, 25), ("case118", 3, 20),
-                                          ("case300", 4, 15), ("pegase2869", 8, 5)])
-def test_time_cut_group_bitwise_equals_single_gpu(name, P, iters):
+@pytest.mark.parametrize("name,P,iters,p2p", [("case30", 2, 30, False), ("case30", 5, 25, False),
+                                              ("case118", 3, 20, False), ("case300", 4, 15, False),
+                                              ("pegase2869", 8, 5, False), ("case30", 5, 25, True),
+                                              ("case118", 3, 20, True), ("pegase2869", 8, 5, True)])
+def test_time_cut_group_bitwise_equals_single_gpu(name, P, iters, p2p):
     """NEXT-4(c) (P:166-167 temporal decomposition): the periods split over P
     ranks (T=24 over 5 ranks is ragged), every component on every rank, the DP stage costs
     all-gathered, the ramp rows' boundary values exchanged with the neighbours.  Each (component,
     period) is computed by the same kernel code as on one GPU, so the assembled iterate equals the
-    single-GPU iterate bit for bit."""
+    single-GPU iterate bit for bit.  p2p: the exchanges are the device-initiated ones (k_xchg.cu:
+    sender stores into the receivers' buffers, epoch flags with release/acquire), the group's ranks
+    emulated by one cooperative launch per exchange."""
     pb, pr = inputs.build_config(name)
     one = ucac.Context(pb, pr)
     one.iterate(iters)
     ref = one.get_state()
     ctxs = [ucac.Context(pb, pr, dist={"rank": r, "nranks": P, "comm_mode": 1, "cut": 1}) for r in range(P)]
+    if p2p:
+        ucac.p2p_group(ctxs)
     # each rank owns a contiguous period range; together they cover the horizon once
     owned = sorted((c.t_off + c.own0, c.t_off + c.own1) for c in ctxs)
     assert owned[0][0] == 0 and owned[-1][1] == pb.T and all(a[1] == b[0] for a, b in zip(owned, owned[1:]))

@@ -379,3 +379,31 @@ def test_case300_config_one_step_every_third():
     every third, free-running schedules and scalars exact throughout."""
     pb, pr = inputs.build_config("case300")
     run_pair(pb, pr, 45, check_every=3)
+
+
+@pytest.mark.parametrize("name", ["case30", "case118", "case300"])
+def test_time_to_residual_configs123_stop_iteration_matches_oracle(name):
+    """The metric's time-to-residual on configs[1]-[3] (case30/118/300-shaped, T=24): these
+    synthetic UC instances do not reach 1e-4, so the stop rule is checked at the
+    level they do reach early: the target is 1.05 x the best primal of the first 600 iterations.
+    The GPU's on-device stop fires at the first iteration the oracle's own primal infeasibility
+     is below it -- the same iteration -- with the objective within 1e-6."""
+    pb, pr = inputs.build_config(name)
+    probe = ucac.Context(pb, pr)
+    hist = []
+    for _ in range(600):
+        probe.iterate(1)
+        hist.append(probe.report()["primal_inf"])
+    target = 1.05 * min(hist)
+    first = next(i for i, v in enumerate(hist) if v <= target) + 1
+    c = ucac.Context(pb, pr)
+    n = c.iterate(5000, stop_on_primal=target)
+    rg = c.report()
+    assert n == first and rg["primal_inf"] <= target
+    o = oracle.Oracle(pb, pr, omp=True)
+    o.iterate(n - 1)
+    assert o.report()["primal_inf"] > target
+    o.iterate(1)
+    ro = o.report()
+    assert ro["primal_inf"] <= target and ro["outer_total"] == rg["outer_total"]
+    assert rg["objective"] == pytest.approx(ro["objective"], rel=1e-6)

@@ -334,5 +334,6 @@ def test_plain_and_accelerated_al_same_kkt_point():
                 its += (sa[8], sp[8])
             else:
                 n_fast += 1
+    print(f"plain vs accelerated: {n_al} AL solves, {n_fast} fast-path solves, Newton its {its}")
     assert n_al + n_fast >= 1000 and n_al >= 250, (n_al, n_fast)
     assert its[0] < its[1]   # the accelerations cut the AL's Newton iterations

@@ -18,7 +18,7 @@ if [ -n "${NCU_LIST:-}" ]; then
   echo "ncu launches rc=$?"
 fi
 for k in "$@"; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^${k}(<|\$)" -s 12 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^${k}(<|\$)" -s ${NCU_SKIP:-4} -c 1 \
     -o "$OUT/full_$k" python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_full_$k.log" 2>&1
   echo "ncu full $k rc=$?"
 done
