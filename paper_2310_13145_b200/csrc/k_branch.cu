@@ -50,6 +50,44 @@ __device__ __forceinline__ double rcp(double x) {
     return fma(r, e, r);
 }
 
+// sin and cos of the angle difference: CUDA's sincos, or (UCAC_POLY_SINCOS) R54's Cody-Waite +
+// Taylor polynomial (the oracle's operation sequence, here with FMA contraction: within 2 ulp, no
+// slow-path range reduction -- the angle differences stay in [-4 pi, 4 pi])
+#ifndef UCAC_POLY_SINCOS
+#define UCAC_POLY_SINCOS 0
+#endif
+__device__ __forceinline__ void br_sincos(double a, double *s, double *c) {
+    if (!UCAC_POLY_SINCOS) {
+        sincos(a, s, c);
+        return;
+    }
+    const double k = floor(a * 0x1.45f306dc9c883p-1 + 0.5);
+    const double r = (a - k * 0x1.921fb544p+0) - k * 0x1.0b4611a626331p-34;
+    const double z = r * r;
+    double ps = 0x1.952c77030ad4ap-49;
+    ps = ps * z + -0x1.ae7f3e733b81fp-41;
+    ps = ps * z + 0x1.6124613a86d09p-33;
+    ps = ps * z + -0x1.ae64567f544e4p-26;
+    ps = ps * z + 0x1.71de3a556c734p-19;
+    ps = ps * z + -0x1.a01a01a01a01ap-13;
+    ps = ps * z + 0x1.1111111111111p-7;
+    ps = ps * z + -0x1.5555555555555p-3;
+    const double sr = r + (r * z) * ps;
+    double pc = -0x1.6827863b97d97p-53;
+    pc = pc * z + 0x1.ae7f3e733b81fp-45;
+    pc = pc * z + -0x1.93974a8c07c9dp-37;
+    pc = pc * z + 0x1.1eed8eff8d898p-29;
+    pc = pc * z + -0x1.27e4fb7789f5cp-22;
+    pc = pc * z + 0x1.a01a01a01a01ap-16;
+    pc = pc * z + -0x1.6c16c16c16c17p-10;
+    pc = pc * z + 0x1.5555555555555p-5;
+    const double cr = (1.0 - 0.5 * z) + (z * z) * pc;
+    const int q = ((int)(long long)k) & 3;
+    const double sa = (q & 1) ? cr : sr, ca = (q & 1) ? sr : cr;
+    *s = (q & 2) ? -sa : sa;
+    *c = ((q + 1) & 2) ? -ca : ca;
+}
+
 // NOANG: no angle consensus rows (variant bit 8, R51) -- a separate instantiation, so the default
 // kernels carry none of its code
 template <bool AL, bool NOANG = false>
@@ -74,7 +112,7 @@ struct BrFun {
                                           double &f1, double &f2, double &f3) const {
         double R = sqrt(x[0] * x[1]);
         double sn, cs;
-        sincos(x[2] - x[3], &sn, &cs);
+        br_sincos(x[2] - x[3], &sn, &cs);
         C = R * cs;
         S = R * sn;
         f0 = Gii * x[0] + Gij * C + Bij * S;

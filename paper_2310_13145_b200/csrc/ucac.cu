@@ -434,8 +434,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     if (e != cudaSuccess) return fail(nullptr, UCAC_ECUDA, "%s", cudaGetErrorString(e));
     if (cc_major != 10) return fail(nullptr, UCAC_ECUDA, "libucac is built for sm_100a; device is sm_%d%d", cc_major, cc_minor);
 
-    const int tcut = (dist && nranks > 1) ? (dist->cut != 0) : 0;
-    if (dist && nranks > 1 && dist->cut != 0 && dist->cut != 1) return fail(nullptr, UCAC_EINVAL, "cut must be 0 or 1");
+    // (a one-rank time cut is allowed: it runs the time-cut graph with local exchanges, for tests)
+    const int tcut = dist ? (dist->cut != 0) : 0;
+    if (dist && dist->cut != 0 && dist->cut != 1) return fail(nullptr, UCAC_EINVAL, "cut must be 0 or 1");
     if (tcut && nranks > hz->T) return fail(nullptr, UCAC_EINVAL, "time cut: T=%d < nranks=%d", hz->T, nranks);
     if (tcut && (prm->variant & (4 | 16)))
         return fail(nullptr, UCAC_EUNSUPPORTED, "time cut: variant bits 4 (ramp-aware DP) and 16 (literal Eq. 5f) are not supported");
@@ -771,32 +772,66 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
     }
 }
 
-// NEXT-4(c) time cut, one NCCL rank per GPU: every rank runs all components over its periods;
-// the DP stage costs are all-gathered for a full-horizon DP on every rank, p and phat of the first
-// owned period go to the previous rank (its ramp-copy and ramp-up rows at the boundary), and the
-// boundary values the previous rank computed (ubar, pbar of its last period, the ramp rows of this
-// rank's first period) come back after (7c)/(7d); one all-reduce of the S8 record.
 // NCCL return codes of the captured collectives: the first failure is kept and reported by build_graphs
 #define NC(call)                                                              \
     do {                                                                      \
         ncclResult_t r_ = (call);                                             \
         if (r_ != ncclSuccess && ctx->nccl_err == ncclSuccess) ctx->nccl_err = r_; \
     } while (0)
+
+// NEXT-4(c) time cut, one rank per GPU.  The single-GPU graph's three streams with
+// the exchanges inserted where their data are final:
+//   s : k_branch ------------------------> k_branch_al -> [bus list] k_bus_late -> [fold] k_rows_late
+//         -> pack 3 -> exchange 3 -> unpack 3 -> S8 all-reduce -> finalize
+//   s2:   stage costs -> exchange 1 -> DP -> k_genx -> pack 2 -> exchange 2 -> unpack 2 -> k_ubar
+//   s3:   [k_branch, unpack 2] k_bus -> k_rows -> [k_ubar] k_fold_early
+// so the early bus/row sweep and the generator chain run in the shadow of the AL tail, as on one GPU.
+// The collectives are totally ordered by the graph's dependencies (1 and 2 on s2 after the iteration
+// fork, 3 and the all-reduce on s after the early fold), so one communicator serves them all.
+// d.p2p: the three exchanges are device-initiated stores into the peers' buffers (k_xchg.cu).
+// One rank (tests): the stage costs are copied locally and the neighbour exchanges vanish.
 static void enqueue_iteration_tc(ucac_ctx *ctx) {
     const Dev &d = ctx->d;
-    cudaStream_t s = ctx->s;
-    // d.p2p: the three exchanges are device-initiated stores into the peers' buffers (k_xchg.cu)
-    launch_stage_tc(d, s);
-    if (d.p2p) launch_xchg(d, 1, s);
-    else NC(ncclAllGather(d.tc_stage_send, d.tc_stage_recv, (size_t)d.G * d.Tmax * 4, ncclDouble, ctx->comm, s));
-    launch_dp_tc(d, s);
-    launch_kernel(ctx, K_GENX, s);
-    launch_pack_tc2(d, s);
-    if (d.p2p) launch_xchg(d, 2, s);
-    else NC(ncclAllGather(d.tc2_send, d.tc2_recv, (size_t)d.G * 2, ncclDouble, ctx->comm, s));
-    launch_unpack_tc2(d, s);
-    const int seq[] = {K_BRANCH, K_UBAR, K_BUS, K_BRANCH_AL, K_BUS_LATE, K_ROWS, K_FOLD, K_ROWS_LATE};
-    for (int k : seq) launch_kernel(ctx, k, s);
+    const bool multi = ctx->nranks > 1;
+    cudaStream_t s = ctx->s, s2 = ctx->s2, s3 = ctx->s3;
+    cudaEventRecord(ctx->ev_fork, s);
+    cudaStreamWaitEvent(s2, ctx->ev_fork, 0);
+    launch_kernel(ctx, K_BRANCH, s);
+    cudaEventRecord(ctx->ev_branch, s);
+    // generator chain with exchanges 1 and 2
+    launch_stage_tc(d, s2);
+    const size_t n1 = (size_t)d.G * d.Tmax * 4;
+    if (!multi) cudaMemcpyAsync(d.tc_stage_recv, d.tc_stage_send, n1 * sizeof(double), cudaMemcpyDeviceToDevice, s2);
+    else if (d.p2p) launch_xchg(d, 1, s2);
+    else NC(ncclAllGather(d.tc_stage_send, d.tc_stage_recv, n1, ncclDouble, ctx->comm, s2));
+    launch_dp_tc(d, s2);
+    launch_kernel(ctx, K_GENX, s2);
+    if (multi) {
+        launch_pack_tc2(d, s2);
+        if (d.p2p) launch_xchg(d, 2, s2);
+        else NC(ncclAllGather(d.tc2_send, d.tc2_recv, (size_t)d.G * 2, ncclDouble, ctx->comm, s2));
+        launch_unpack_tc2(d, s2);
+    }
+    cudaEventRecord(ctx->ev_genx, s2);
+    // early sweep
+    cudaStreamWaitEvent(s3, ctx->ev_genx, 0);
+    cudaStreamWaitEvent(s3, ctx->ev_branch, 0);
+    launch_kernel(ctx, K_BUS, s3);
+    cudaEventRecord(ctx->ev_bus, s3);
+    launch_kernel(ctx, K_ROWS, s3);
+    launch_kernel(ctx, K_UBAR, s2);
+    cudaEventRecord(ctx->ev_join, s2);
+    cudaStreamWaitEvent(s3, ctx->ev_join, 0);
+    launch_kernel(ctx, K_FOLD, s3);
+    cudaEventRecord(ctx->ev_early, s3);
+    // AL tail, late sweep
+    launch_kernel(ctx, K_BRANCH_AL, s);
+    cudaStreamWaitEvent(s, ctx->ev_genx, 0);
+    cudaStreamWaitEvent(s, ctx->ev_bus, 0);
+    launch_kernel(ctx, K_BUS_LATE, s);
+    cudaStreamWaitEvent(s, ctx->ev_early, 0);
+    launch_kernel(ctx, K_ROWS_LATE, s);
+    if (!multi) return;   // one rank: k_rows_late's final fold applied S8/S9 itself
     launch_pack_tc3(d, s);
     if (d.p2p) launch_xchg(d, 3, s);
     else NC(ncclAllGather(d.tc3_send, d.tc3_recv, (size_t)d.G * 12, ncclDouble, ctx->comm, s));

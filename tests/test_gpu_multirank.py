@@ -93,3 +93,21 @@ def test_time_cut_rejects_unsupported():
     import dataclasses
     with pytest.raises(ucac.UcacError):   # the ramp-aware DP needs p_{t-1} across the cut
         ucac.Context(pb, dataclasses.replace(pr, variant=4), dist={"rank": 0, "nranks": 2, "comm_mode": 1, "cut": 1})
+
+
+@pytest.mark.parametrize("name,iters", [("case30", 40), ("case300", 20), ("pegase2869", 6)])
+def test_time_cut_graph_one_rank_bitwise_equals_single_gpu(name, iters):
+    """The time cut's iteration GRAPH (three streams, the exchanges placed where their data are
+    final) run with one rank -- local exchanges, no NCCL -- gives the single-GPU
+    iterate bit for bit: its stream and event dependencies order every read after its write (the
+    loopback tests above check the exchanges themselves, phase by phase)."""
+    pb, pr = inputs.build_config(name)
+    one = ucac.Context(pb, pr)
+    one.iterate(iters)
+    ref = one.get_state()
+    tc = ucac.Context(pb, pr, dist={"rank": 0, "nranks": 1, "comm_mode": 0, "cut": 1})
+    tc.iterate(iters)
+    got = tc.get_state()
+    for k in ref:
+        assert np.array_equal(got[k], ref[k]), (name, k)
+    assert tc.report()["objective"] == one.report()["objective"]
