@@ -824,6 +824,7 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
         if (queue) {
             pos = atomicAdd(d.alq_cnt, 1u);
             d.alq[pos] = k;
+            d.qmark[k] = mark_stamp(d);   // (multi-rank: flags a cut end's tauhat as not final)
             // the previous iterate (still in d.x): the AL's second candidate start (R49)
 #pragma unroll
             for (int m = 0; m < 4; m++) d.alq_x[m * LTs + pos] = d.x[m * LTs + k];

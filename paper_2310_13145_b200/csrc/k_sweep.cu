@@ -1037,6 +1037,89 @@ __global__ void k_finalize(Dev d) {
 
 // ---- halo exchange: pack/unpack of the cut ends' tauhat and of bus results
 __device__ __forceinline__ int to_kind(int kk) { return kk == 0 ? B_FPJI : (kk == 1 ? B_FQJI : (kk == 2 ? B_WJ : B_AJ)); }
+// Early exchanges (before the AL tail ends): every cut branch-period's to-end tauhat with a flag
+// that the (l,t) went to the AL queue (its tauhat is then not final: the to-bus and its ends go late
+// on the owner), and every export bus-period's results with a flag that it is late (its ghost copies
+// and the local ends at them go late).  Late exchanges carry the final values of the flagged ones.
+__global__ void k_pack_tau_early(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t LTH = (size_t)(d.L + d.Lph) * T;
+    const unsigned stamp = mark_stamp(d);
+    const int n = d.ncut * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, c = k / T;
+        const size_t lk = (size_t)d.cut_local[c] * T + t;
+        const bool q = d.qmark[lk] == stamp;
+        double *o = d.xsend1 + (size_t)c * 5 * T;
+        for (int kk = 0; kk < 4; kk++) o[kk * T + t] = q ? 0.0 : TH(to_kind(kk), lk);
+        o[4 * T + t] = q ? 1.0 : 0.0;
+    }
+}
+__global__ void k_unpack_tau_early(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t LTH = (size_t)(d.L + d.Lph) * T;
+    const unsigned stamp = mark_stamp(d);
+    const int n = d.Lph * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, p = k / T;
+        const double *src = d.xrecv1 + (size_t)d.phantom_src[p] * 5 * T;
+        const size_t pk = (size_t)(d.L + p) * T + t;
+        if (src[4 * T + t] != 0.0) {
+            // a remote AL solve at this owned bus: the bus and every end at it go late (as k_branch marks)
+            d.qmark[pk] = stamp;
+            const int bus = d.phantom_bus[p];
+            d.bmark[(size_t)bus * T + t] = stamp;
+            for (int a = d.be_ptr[bus]; a < d.be_ptr[bus + 1]; a++) {
+                const int code = d.be_idx[a];
+                d.rmark[code & 1][(size_t)(code >> 1) * T + t] = stamp;
+            }
+        } else {
+            for (int kk = 0; kk < 4; kk++) TH(to_kind(kk), pk) = src[kk * T + t];
+        }
+    }
+}
+__global__ void k_pack_bus_early(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t BT = (size_t)d.B * T;
+    const unsigned stamp = mark_stamp(d);
+    const int n = d.nexport * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, e = k / T;
+        const size_t bk = (size_t)d.export_local[e] * T + t;
+        const bool late = d.bmark[bk] == stamp;
+        double *o = d.xsend2 + (size_t)e * 7 * T;
+        for (int f = 0; f < 6; f++) o[f * T + t] = late ? 0.0 : (f < 4 ? d.bmu[f * BT + bk] : (f == 4 ? d.wbar[bk] : d.thbar[bk]));
+        o[6 * T + t] = late ? 1.0 : 0.0;
+    }
+}
+__global__ void k_unpack_bus_early(Dev d) {
+    if (d.st->done) return;
+    const int T = d.T;
+    const size_t BT = (size_t)d.B * T;
+    const unsigned stamp = mark_stamp(d);
+    const int n = d.nghost * T;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int t = k % T, gb = k / T;
+        const double *src = d.xrecv2 + (size_t)d.ghost_src[gb] * 7 * T;
+        const size_t bk = (size_t)(d.B_own + gb) * T + t;
+        if (src[6 * T + t] != 0.0) {
+            // late on its owner: the local ends at this ghost bus wait for the late exchange
+            d.bmark[bk] = stamp;
+            for (int a = d.ghost_eptr[gb]; a < d.ghost_eptr[gb + 1]; a++) {
+                const int code = d.ghost_eidx[a];
+                d.rmark[code & 1][(size_t)(code >> 1) * T + t] = stamp;
+            }
+        } else {
+            for (int f = 0; f < 4; f++) d.bmu[f * BT + bk] = src[f * T + t];
+            d.wbar[bk] = src[4 * T + t];
+            d.thbar[bk] = src[5 * T + t];
+        }
+    }
+}
+// late: the final tauhat of the queued cut ends / the results of the late export buses
 __global__ void k_pack_tau(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
@@ -1044,17 +1127,19 @@ __global__ void k_pack_tau(Dev d) {
     const int n = d.ncut * 4 * T;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int t = k % T, kk = (k / T) % 4, c = k / (4 * T);
-        d.xsend1[k] = TH(to_kind(kk), (size_t)d.cut_local[c] * T + t);
+        d.xsend3[k] = TH(to_kind(kk), (size_t)d.cut_local[c] * T + t);
     }
 }
 __global__ void k_unpack_tau(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t LTH = (size_t)(d.L + d.Lph) * T;
+    const unsigned stamp = mark_stamp(d);
     const int n = d.Lph * 4 * T;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int t = k % T, kk = (k / T) % 4, p = k / (4 * T);
-        TH(to_kind(kk), (size_t)(d.L + p) * T + t) = d.xrecv1[((size_t)d.phantom_src[p] * 4 + kk) * T + t];
+        const size_t pk = (size_t)(d.L + p) * T + t;
+        if (d.qmark[pk] == stamp) TH(to_kind(kk), pk) = d.xrecv3[((size_t)d.phantom_src[p] * 4 + kk) * T + t];
     }
 }
 __global__ void k_pack_bus(Dev d) {
@@ -1065,18 +1150,20 @@ __global__ void k_pack_bus(Dev d) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int t = k % T, f = (k / T) % 6, e = k / (6 * T);
         const size_t bk = (size_t)d.export_local[e] * T + t;
-        d.xsend2[k] = f < 4 ? d.bmu[f * BT + bk] : (f == 4 ? d.wbar[bk] : d.thbar[bk]);
+        d.xsend4[k] = f < 4 ? d.bmu[f * BT + bk] : (f == 4 ? d.wbar[bk] : d.thbar[bk]);
     }
 }
 __global__ void k_unpack_bus(Dev d) {
     if (d.st->done) return;
     const int T = d.T;
     const size_t BT = (size_t)d.B * T;
+    const unsigned stamp = mark_stamp(d);
     const int n = d.nghost * 6 * T;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int t = k % T, f = (k / T) % 6, gb = k / (6 * T);
         const size_t bk = (size_t)(d.B_own + gb) * T + t;
-        const double v = d.xrecv2[((size_t)d.ghost_src[gb] * 6 + f) * T + t];
+        if (d.bmark[bk] != stamp) continue;   // early ghost: already delivered by the early exchange
+        const double v = d.xrecv4[((size_t)d.ghost_src[gb] * 6 + f) * T + t];
         if (f < 4) d.bmu[f * BT + bk] = v;
         else if (f == 4) d.wbar[bk] = v;
         else d.thbar[bk] = v;
@@ -1169,6 +1256,10 @@ void launch_ubar(const Dev &d, cudaStream_t s) {
 void launch_finalize(const Dev &d, cudaStream_t s) { k_finalize<<<1, 32, 0, s>>>(d); }
 static int xgrid(int n) { return std::max(1, std::min(296, (n + 255) / 256)); }
 void launch_pack_tau(const Dev &d, cudaStream_t s) { k_pack_tau<<<xgrid(d.ncut * 4 * d.T), 256, 0, s>>>(d); }
+void launch_pack_tau_early(const Dev &d, cudaStream_t s) { k_pack_tau_early<<<xgrid(d.ncut * d.T), 256, 0, s>>>(d); }
+void launch_unpack_tau_early(const Dev &d, cudaStream_t s) { k_unpack_tau_early<<<xgrid(d.Lph * d.T), 256, 0, s>>>(d); }
+void launch_pack_bus_early(const Dev &d, cudaStream_t s) { k_pack_bus_early<<<xgrid(d.nexport * d.T), 256, 0, s>>>(d); }
+void launch_unpack_bus_early(const Dev &d, cudaStream_t s) { k_unpack_bus_early<<<xgrid(d.nghost * d.T), 256, 0, s>>>(d); }
 void launch_unpack_tau(const Dev &d, cudaStream_t s) { k_unpack_tau<<<xgrid(d.Lph * 4 * d.T), 256, 0, s>>>(d); }
 void launch_pack_bus(const Dev &d, cudaStream_t s) { k_pack_bus<<<xgrid(d.nexport * 6 * d.T), 256, 0, s>>>(d); }
 void launch_unpack_bus(const Dev &d, cudaStream_t s) { k_unpack_bus<<<xgrid(d.nghost * 6 * d.T), 256, 0, s>>>(d); }

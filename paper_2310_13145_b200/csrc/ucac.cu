@@ -72,6 +72,8 @@ struct Local {
     // halo
     std::vector<int> cut_local, export_local, phantom_src, ghost_src;
     int max_cut = 0, max_export = 0;
+    std::vector<int> phantom_bus;                                 // [Lp] owned local bus of each phantom
+    std::vector<int> gep, gei;                                    // CSR ghost bus -> local end codes
     // periods: local period t = global t + t_off of Tg, owned [own0, own1) (time cut, NEXT-4(c))
     int t_off = 0, Tg = 0, own0 = 0, own1 = 0, Tmax = 0;
     std::vector<int> tstart;                                       // [nranks + 1] owned global ranges
@@ -224,6 +226,23 @@ static Local build_local(const ucac_network *net, const ucac_horizon *hz, const 
     P.ghost_src = h.ghost_src;
     P.max_cut = h.max_cut;
     P.max_export = h.max_export;
+    // early/late split across ranks: the owned to-bus of every phantom, and per ghost
+    // bus the local branch ends at it (end codes 2 l + 1, l ascending)
+    for (int p = 0; p < P.Lp; p++) P.phantom_bus.push_back(h.bus_local[net->br_to[h.phantom[p]]]);
+    const int Bg = P.B - P.Bo;
+    P.gep.assign(Bg + 1, 0);
+    for (int a = 0; a < P.L; a++)
+        if (P.to[a] >= P.Bo) P.gep[P.to[a] - P.Bo + 1]++;
+    for (int g = 0; g < Bg; g++) P.gep[g + 1] += P.gep[g];
+    P.gei.assign(P.gep[Bg], 0);
+    {
+        std::vector<int> fill(Bg, 0);
+        for (int a = 0; a < P.L; a++)
+            if (P.to[a] >= P.Bo) {
+                const int g = P.to[a] - P.Bo;
+                P.gei[P.gep[g] + fill[g]++] = 2 * a + 1;
+            }
+    }
     return P;
 }
 
@@ -233,6 +252,7 @@ struct ucac_ctx {
     int G = 0, L = 0, B = 0, T = 0;      // local counts (B = owned buses)
     int nranks = 1, rank = 0, comm_mode = 0;
     ncclComm_t comm = nullptr;
+    ncclComm_t comm2 = nullptr;          // bus cut: the early exchanges' communicator (stream s3)
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr, ev_branch = nullptr,
@@ -518,6 +538,10 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         memcpy(&id, dist->nccl_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
         if (r != ncclSuccess) return bail(fail(ctx, UCAC_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+        if (!tcut) {   // the early exchanges run on their own stream, so on their own communicator
+            r = ncclCommSplit(ctx->comm, 0, rank, &ctx->comm2, nullptr);
+            if (r != ncclSuccess) return bail(fail(ctx, UCAC_ENCCL, "ncclCommSplit: %s", ncclGetErrorString(r)));
+        }
     }
 
     Dev &d = ctx->d;
@@ -601,6 +625,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.phantom_src = A.put(P.phantom_src);
         d.ghost_src = A.put(P.ghost_src);
         d.tc_t0 = A.put(P.tstart);
+        d.phantom_bus = A.put(P.phantom_bus);
+        d.ghost_eptr = A.put(P.gep);
+        d.ghost_eidx = A.put(P.gei);
         uinit = P.uinit.empty() ? nullptr : A.put(P.uinit);
         A.up_end = A.off;
         // iterate (zeroed, then set by launch_init)
@@ -650,10 +677,16 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.unext_ok = A.take<unsigned>(1);
         d.rec = A.take<double>(NREC);
         d.tl = A.take<unsigned long long>(2 * NKERN);
-        d.xsend1 = A.take<double>((size_t)P.max_cut * 4 * T);
-        d.xrecv1 = A.take<double>((size_t)nranks * P.max_cut * 4 * T);
-        d.xsend2 = A.take<double>((size_t)P.max_export * 6 * T);
-        d.xrecv2 = A.take<double>((size_t)nranks * P.max_export * 6 * T);
+        // bus cut: early exchanges carry a late flag (5 and 7 values), late ones the plain values (4, 6)
+        d.xsend1 = A.take<double>((size_t)P.max_cut * 5 * T);
+        d.xrecv1 = A.take<double>((size_t)nranks * P.max_cut * 5 * T);
+        d.xsend2 = A.take<double>((size_t)P.max_export * 7 * T);
+        d.xrecv2 = A.take<double>((size_t)nranks * P.max_export * 7 * T);
+        d.xsend3 = A.take<double>((size_t)P.max_cut * 4 * T);
+        d.xrecv3 = A.take<double>((size_t)nranks * P.max_cut * 4 * T);
+        d.xsend4 = A.take<double>((size_t)P.max_export * 6 * T);
+        d.xrecv4 = A.take<double>((size_t)nranks * P.max_export * 6 * T);
+        d.qmark = A.take<unsigned>((size_t)(L + P.Lp) * T);
         d.st = A.take<DevStatus>(1);
         if (tcut) {   // (the receive buffers live in ctx->xbuf, a plain cudaMalloc block peers can map)
             d.tc_stage_send = A.take<double>((size_t)G * P.Tmax * 4);
@@ -843,9 +876,76 @@ static void enqueue_iteration_tc(ucac_ctx *ctx) {
     launch_finalize(d, s);
 }
 
+// Bus cut over NCCL ranks: the single-GPU overlap kept across ranks.  The early
+// exchanges (cut ends' tauhat with a "queued" flag, then early bus results with a "late" flag) run
+// on s3 on their own communicator, so the interior buses and rows proceed during the AL tail; the
+// late ones (final tauhat of the queued cut ends, late bus results) and the S8 all-reduce on s.
+//   s : k_branch ----------------> k_branch_al -> tau late -> [bus list] k_bus_late -> bus late
+//         -> [early fold] k_rows_late -> all-reduce -> finalize
+//   s2:   k_gen -> k_genx -> k_ubar
+//   s3:   [k_branch, k_genx] tau early -> k_bus -> bus early -> k_rows -> [k_ubar] k_fold_early
+static void enqueue_iteration_bus_multi(ucac_ctx *ctx) {
+    const Dev &d = ctx->d;
+    cudaStream_t s = ctx->s, s2 = ctx->s2, s3 = ctx->s3;
+    const size_t T = d.T;
+    cudaEventRecord(ctx->ev_fork, s);
+    cudaStreamWaitEvent(s2, ctx->ev_fork, 0);
+    launch_kernel(ctx, K_BRANCH, s);
+    cudaEventRecord(ctx->ev_branch, s);
+    launch_kernel(ctx, K_GEN, s2);
+    launch_kernel(ctx, K_GENX, s2);
+    cudaEventRecord(ctx->ev_genx, s2);
+    launch_kernel(ctx, K_UBAR, s2);
+    cudaEventRecord(ctx->ev_join, s2);
+    // early sweep with the early exchanges
+    cudaStreamWaitEvent(s3, ctx->ev_branch, 0);
+    cudaStreamWaitEvent(s3, ctx->ev_genx, 0);
+    if (d.max_cut > 0) {
+        launch_pack_tau_early(d, s3);
+        NC(ncclAllGather(d.xsend1, d.xrecv1, (size_t)d.max_cut * 5 * T, ncclDouble, ctx->comm2, s3));
+        launch_unpack_tau_early(d, s3);
+    }
+    launch_kernel(ctx, K_BUS, s3);
+    cudaEventRecord(ctx->ev_bus, s3);
+    if (d.max_export > 0) {
+        launch_pack_bus_early(d, s3);
+        NC(ncclAllGather(d.xsend2, d.xrecv2, (size_t)d.max_export * 7 * T, ncclDouble, ctx->comm2, s3));
+        launch_unpack_bus_early(d, s3);
+    }
+    launch_kernel(ctx, K_ROWS, s3);
+    cudaStreamWaitEvent(s3, ctx->ev_join, 0);
+    launch_kernel(ctx, K_FOLD, s3);
+    cudaEventRecord(ctx->ev_early, s3);
+    // AL tail, late exchanges, late sweep
+    launch_kernel(ctx, K_BRANCH_AL, s);
+    if (d.max_cut > 0) launch_pack_tau(d, s);
+    cudaStreamWaitEvent(s, ctx->ev_bus, 0);   // the early unpack's queued flags, the bus lists
+    if (d.max_cut > 0) {
+        NC(ncclAllGather(d.xsend3, d.xrecv3, (size_t)d.max_cut * 4 * T, ncclDouble, ctx->comm, s));
+        launch_unpack_tau(d, s);
+    }
+    launch_kernel(ctx, K_BUS_LATE, s);
+    if (d.max_export > 0) launch_pack_bus(d, s);
+    cudaStreamWaitEvent(s, ctx->ev_early, 0);   // the early ghost flags, the early rows and fold
+    if (d.max_export > 0) {
+        NC(ncclAllGather(d.xsend4, d.xrecv4, (size_t)d.max_export * 6 * T, ncclDouble, ctx->comm, s));
+        launch_unpack_bus(d, s);
+    }
+    launch_kernel(ctx, K_ROWS_LATE, s);
+    NC(ncclGroupStart());
+    NC(ncclAllReduce(d.rec, d.rec, NREC_SUM, ncclDouble, ncclSum, ctx->comm, s));
+    NC(ncclAllReduce(d.rec + NREC_SUM, d.rec + NREC_SUM, NREC - NREC_SUM, ncclDouble, ncclMax, ctx->comm, s));
+    NC(ncclGroupEnd());
+    launch_finalize(d, s);
+}
+
 static void enqueue_iteration(ucac_ctx *ctx) {
     if (ctx->d.tcut) {
         enqueue_iteration_tc(ctx);
+        return;
+    }
+    if (ctx->nranks > 1) {
+        enqueue_iteration_bus_multi(ctx);
         return;
     }
     const Dev &d = ctx->d;
@@ -1092,44 +1192,62 @@ extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t it
             for (int r = 0; r < n; r++) launch_unpack_tc3(ctxs[r]->d, ctxs[r]->s);
             CK(sync_all());
         } else {
+        // bus cut: the phases of enqueue_iteration_bus_multi (early exchanges before the AL tail's
+        // results are used, late ones after), each exchange a copy of every rank's send buffer
+        auto gather = [&](double *Dev::*snd, double *Dev::*rcv, int per, int Dev::*cnt, int Dev::*mx) -> cudaError_t {
+            for (int r = 0; r < n; r++)
+                for (int q = 0; q < n; q++) {
+                    const Dev &dr = ctxs[r]->d, &dq = ctxs[q]->d;
+                    const size_t blk = (size_t)(dr.*mx) * per * dr.T;
+                    if (dq.*cnt > 0) {
+                        cudaError_t e = cudaMemcpyAsync(dr.*rcv + q * blk, dq.*snd, (size_t)(dq.*cnt) * per * dq.T * sizeof(double),
+                                                        cudaMemcpyDeviceToDevice, ctxs[r]->s);
+                        if (e != cudaSuccess) return e;
+                    }
+                }
+            return cudaSuccess;
+        };
         for (int r = 0; r < n; r++) {
             ucac_ctx *c = ctxs[r];
-            const int ph1[] = {K_BRANCH, K_GEN, K_GENX, K_UBAR, K_BRANCH_AL};
+            const int ph1[] = {K_BRANCH, K_GEN, K_GENX, K_UBAR};
             for (int k : ph1) launch_kernel(c, k, c->s);
+            if (c->d.max_cut > 0) launch_pack_tau_early(c->d, c->s);
+        }
+        CK(sync_all());
+        CK(gather(&Dev::xsend1, &Dev::xrecv1, 5, &Dev::ncut, &Dev::max_cut));
+        CK(sync_all());
+        for (int r = 0; r < n; r++) {
+            ucac_ctx *c = ctxs[r];
+            if (c->d.max_cut > 0) launch_unpack_tau_early(c->d, c->s);
+            launch_kernel(c, K_BUS, c->s);
+            if (c->d.max_export > 0) launch_pack_bus_early(c->d, c->s);
+        }
+        CK(sync_all());
+        CK(gather(&Dev::xsend2, &Dev::xrecv2, 7, &Dev::nexport, &Dev::max_export));
+        CK(sync_all());
+        for (int r = 0; r < n; r++) {
+            ucac_ctx *c = ctxs[r];
+            if (c->d.max_export > 0) launch_unpack_bus_early(c->d, c->s);
+            launch_kernel(c, K_ROWS, c->s);
+            launch_kernel(c, K_FOLD, c->s);
+            launch_kernel(c, K_BRANCH_AL, c->s);
             if (c->d.max_cut > 0) launch_pack_tau(c->d, c->s);
         }
         CK(sync_all());
-        for (int r = 0; r < n; r++)
-            for (int q = 0; q < n; q++) {
-                const Dev &dr = ctxs[r]->d, &dq = ctxs[q]->d;
-                const size_t blk = (size_t)dr.max_cut * 4 * dr.T;
-                if (dq.ncut > 0)
-                    CK(cudaMemcpyAsync(dr.xrecv1 + q * blk, dq.xsend1, (size_t)dq.ncut * 4 * dq.T * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, ctxs[r]->s));
-            }
+        CK(gather(&Dev::xsend3, &Dev::xrecv3, 4, &Dev::ncut, &Dev::max_cut));
         CK(sync_all());
         for (int r = 0; r < n; r++) {
             ucac_ctx *c = ctxs[r];
             if (c->d.max_cut > 0) launch_unpack_tau(c->d, c->s);
-            launch_kernel(c, K_BUS, c->s);
             launch_kernel(c, K_BUS_LATE, c->s);
             if (c->d.max_export > 0) launch_pack_bus(c->d, c->s);
         }
         CK(sync_all());
-        for (int r = 0; r < n; r++)
-            for (int q = 0; q < n; q++) {
-                const Dev &dr = ctxs[r]->d, &dq = ctxs[q]->d;
-                const size_t blk = (size_t)dr.max_export * 6 * dr.T;
-                if (dq.nexport > 0)
-                    CK(cudaMemcpyAsync(dr.xrecv2 + q * blk, dq.xsend2, (size_t)dq.nexport * 6 * dq.T * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, ctxs[r]->s));
-            }
+        CK(gather(&Dev::xsend4, &Dev::xrecv4, 6, &Dev::nexport, &Dev::max_export));
         CK(sync_all());
         for (int r = 0; r < n; r++) {
             ucac_ctx *c = ctxs[r];
             if (c->d.max_export > 0) launch_unpack_bus(c->d, c->s);
-            launch_kernel(c, K_ROWS, c->s);
-            launch_kernel(c, K_FOLD, c->s);
             launch_kernel(c, K_ROWS_LATE, c->s);
         }
         CK(sync_all());
@@ -1552,6 +1670,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     for (void *p : ctx->peer_maps) cudaIpcCloseMemHandle(p);
     if (ctx->xbuf) cudaFree(ctx->xbuf);
     if (ctx->xdevs) cudaFree(ctx->xdevs);
+    if (ctx->comm2) ncclCommDestroy(ctx->comm2);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->st_host) pinned_status_put(ctx->st_host);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);

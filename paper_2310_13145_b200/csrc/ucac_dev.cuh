@@ -120,7 +120,12 @@ struct Dev {
     int Lph;                          // phantom branches [L, L + Lph) (tauhat only)
     int ncut, nexport, nphantom_src, nghost, max_cut, max_export, nranks;
     const int *cut_local, *export_local, *phantom_src, *ghost_src;
-    double *xsend1, *xrecv1, *xsend2, *xrecv2;   // halo exchange buffers
+    double *xsend1, *xrecv1, *xsend2, *xrecv2;   // halo exchange buffers: early tauhat + late flag (5 per
+                                                 // cut branch-period), early bus results + late flag (7)
+    double *xsend3, *xrecv3, *xsend4, *xrecv4;   // late tauhat (4), late bus results (6)
+    const int *phantom_bus;           // [Lp] owned local bus of each phantom branch's to-end
+    const int *ghost_eptr, *ghost_eidx;   // CSR ghost bus -> local branch end codes at it
+    unsigned *qmark;                  // [(L + Lp) T] = stamp: the (l,t) went to the AL queue (local, or remote for a phantom)
     double *rec;                      // [NREC] local reduction record (sums then maxes)
     double *tauh;                     // [8][(L+Lph)*T] bus-side targets x + z + y/rho of the branch rows
     double *bmu;                      // [4][B*T] muP, muQ, wbar - wbar_old, thbar - thbar_old
@@ -276,6 +281,10 @@ int nblk_rows(int L, int T);
 // multi-rank
 void launch_finalize(const Dev &d, cudaStream_t s);
 void launch_pack_tau(const Dev &d, cudaStream_t s);
+void launch_pack_tau_early(const Dev &d, cudaStream_t s);
+void launch_unpack_tau_early(const Dev &d, cudaStream_t s);
+void launch_pack_bus_early(const Dev &d, cudaStream_t s);
+void launch_unpack_bus_early(const Dev &d, cudaStream_t s);
 void launch_unpack_tau(const Dev &d, cudaStream_t s);
 void launch_pack_bus(const Dev &d, cudaStream_t s);
 void launch_unpack_bus(const Dev &d, cudaStream_t s);
