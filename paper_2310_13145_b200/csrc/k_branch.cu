@@ -820,14 +820,20 @@ __global__ void __launch_bounds__(UCAC_BRANCH_TPB, UCAC_BRANCH_MINB) k_branch(De
             if (!isfinite(chk)) report_nonfinite(d, K_BRANCH, k / d.T, k - (k / d.T) * d.T);
         }
         const bool queue = rate > 0.0 && (al_always || f0 * f0 + f1 * f1 > r2 || f2 * f2 + f3 * f3 > r2);
-        unsigned pos = 0;
         if (queue) {
-            pos = atomicAdd(d.alq_cnt, 1u);
-            d.alq[pos] = k;
+            // AL queue buckets by the solve's previous AL Newton count: heavy and newly
+            // active solves first, so the block-major dealing groups similar chains per warp and the
+            // blocks holding light solves release their SMs early
+            const int pit = UCAC_AL_BUCKETS > 1 ? d.alits[k] : 0;
+            const int b = UCAC_AL_BUCKETS == 1 ? 0 : (pit == 0 || pit >= 9 ? 0 : (pit >= 6 || UCAC_AL_BUCKETS == 2 ? 1 : 2));
+            const unsigned pos = atomicAdd(d.alq_cnt + b, 1u);
+            d.alq[(size_t)b * LTs + pos] = k;
             d.qmark[k] = mark_stamp(d);   // (multi-rank: flags a cut end's tauhat as not final)
             // the previous iterate (still in d.x): the AL's second candidate start (R49)
 #pragma unroll
-            for (int m = 0; m < 4; m++) d.alq_x[m * LTs + pos] = d.x[m * LTs + k];
+            for (int m = 0; m < 4; m++) d.alq_x[m * LTs + k] = d.x[m * LTs + k];
+        } else if (UCAC_AL_BUCKETS > 1 && d.alits[k]) {
+            d.alits[k] = 0;
         }
 #pragma unroll
         for (int m = 0; m < 4; m++) d.x[m * LTs + k] = x[m];
@@ -870,7 +876,12 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
     TL_KERNEL(K_BRANCH_AL);
     if (d.st->done) return;
     const size_t LTs = (size_t)d.L * d.T;
-    const unsigned n = *((volatile unsigned *)d.alq_cnt);
+    unsigned nb[UCAC_AL_BUCKETS], n = 0;
+#pragma unroll
+    for (int b = 0; b < UCAC_AL_BUCKETS; b++) {
+        nb[b] = *((volatile unsigned *)d.alq_cnt + b);
+        n += nb[b];
+    }
     unsigned long long c_it = 0, c_cap = 0, c_al = 0, c_alcap = 0, c_alit = 0;
 #if UCAC_AL_DEAL == 2
     // block-major static dealing: the queue fills the first blocks, so the AL work sits on few SMs
@@ -883,10 +894,16 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
     for (unsigned idx = lane * nwarps + gwarp; idx < n; idx += 32 * nwarps) {
 #else
     for (;;) {
-        const unsigned idx = atomicAdd(d.alq_cnt + 1, 1u);
+        const unsigned idx = atomicAdd(d.alq_cnt + UCAC_AL_BUCKETS, 1u);
         if (idx >= n) break;
 #endif
-        const int k = d.alq[idx];
+        int k;
+        {
+            unsigned b = 0, p = idx;
+            while (b + 1 < UCAC_AL_BUCKETS && p >= nb[b]) p -= nb[b++];
+            k = d.alq[(size_t)b * LTs + p];
+        }
+        const unsigned long long alit0 = c_alit;
 #ifdef UCAC_PROF
         unsigned long long t_start;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -927,7 +944,7 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
             // (each with its slacks from its flows) has the lower AL value
             double xp[6], C0, S0, p0, p1, p2, p3;
 #pragma unroll
-            for (int m = 0; m < 4; m++) xp[m] = clampd(d.alq_x[m * LTs + idx], lo[m], hi[m]);
+            for (int m = 0; m < 4; m++) xp[m] = clampd(d.alq_x[m * LTs + k], lo[m], hi[m]);
             F6.flows(xp, C0, S0, p0, p1, p2, p3);
             xp[4] = clampd(1.0 - (p0 * p0 + p1 * p1) * F6.r2inv, 0.0, 1.0);
             xp[5] = clampd(1.0 - (p2 * p2 + p3 * p3) * F6.r2inv, 0.0, 1.0);
@@ -983,6 +1000,7 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
         d.al[0 * LTs + k] = mu0;
         d.al[1 * LTs + k] = mu1;
         d.al[2 * LTs + k] = sig;
+        if (UCAC_AL_BUCKETS > 1) d.alits[k] = (uint8_t)min(255ull, max(1ull, c_alit - alit0));
         emit_tauhat(d, k, x, f0, f1, f2, f3);
 #ifdef UCAC_PROF
         {

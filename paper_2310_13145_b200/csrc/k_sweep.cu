@@ -138,6 +138,16 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 #define TH(k, i) d.tauh[(size_t)(k) * LTH + (i)]
 
 constexpr int BUS_THREADS = 128;
+// minimum resident blocks per SM the compiler must fit (register cap), tuning knobs (0: none)
+#ifndef UCAC_BUS_MINB
+#define UCAC_BUS_MINB 1
+#endif
+#ifndef UCAC_ROWS_MINB
+#define UCAC_ROWS_MINB 1
+#endif
+#ifndef UCAC_UBAR_MINB
+#define UCAC_UBAR_MINB 1
+#endif
 constexpr int UBAR_THREADS = 64;
 constexpr int ROWS_THREADS = 128;
 // late kernels: most threads skip (unmarked rows), so the block waits on its slowest chain.
@@ -237,8 +247,7 @@ __device__ void final_fold(const Dev &d) {
         rec[R_DINF] = fin[P_DINF];
         rec[R_BAD] = fin[P_BAD];
         for (int q = 0; q < NCNT; q++) d.cnt[q] = 0;
-        d.alq_cnt[0] = 0;
-        d.alq_cnt[1] = 0;
+        for (int q = 0; q <= UCAC_AL_BUCKETS; q++) d.alq_cnt[q] = 0;
         if (d.nranks > 1) {
             for (int q = 0; q < NREC; q++) d.rec[q] = rec[q];   // cross-rank all-reduce, then k_finalize
         } else {
@@ -512,7 +521,7 @@ __device__ __forceinline__ void bus_end_rows(const Dev &d, const Ctl &c, int k, 
 }
 
 template <bool STRICT>
-__global__ void __launch_bounds__(BUS_THREADS) k_bus(Dev d) {
+__global__ void __launch_bounds__(BUS_THREADS, UCAC_BUS_MINB) k_bus(Dev d) {
     TL_KERNEL(K_BUS);
     if (d.st->done) return;
     const Ctl c(d);
@@ -578,7 +587,7 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
 // k_rows (early): one thread per (l,t), the ends whose bus is not marked (coalesced row
 // arrays, as k_branch); the marked ends are done by k_rows_late.
 template <bool STRICT>
-__global__ void __launch_bounds__(ROWS_THREADS) k_rows(Dev d) {
+__global__ void __launch_bounds__(ROWS_THREADS, UCAC_ROWS_MINB) k_rows(Dev d) {
     TL_KERNEL(K_ROWS);
     if (d.st->done) return;
     const Ctl c(d);
@@ -809,7 +818,7 @@ __device__ void boxqp3_lanes(int n, int m, const double (*c)[3], const double *e
 // LIT: the literal Eq. 5f ramp-down row (variant bit 16, R52), a separate instantiation so the
 // default kernel carries none of its code
 template <bool LIT>
-__global__ void __launch_bounds__(UBAR_THREADS) k_ubar(Dev d) {
+__global__ void __launch_bounds__(UBAR_THREADS, UCAC_UBAR_MINB) k_ubar(Dev d) {
     TL_KERNEL(K_UBAR);
     if (d.st->done) return;
     const int T = d.T;

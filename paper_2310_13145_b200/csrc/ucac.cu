@@ -670,9 +670,10 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.tauh = A.take<double>((size_t)NBROW * (L + P.Lp) * T);
         d.bmu = A.take<double>(4 * BT);
         d.cnt = A.take<unsigned long long>(NCNT);
-        d.alq = A.take<int>(LT);
-        d.alq_cnt = A.take<unsigned>(2);
+        d.alq = A.take<int>((size_t)UCAC_AL_BUCKETS * LT);
+        d.alq_cnt = A.take<unsigned>(UCAC_AL_BUCKETS + 1);
         d.alq_x = A.take<double>(4 * LT);
+        d.alits = A.take<uint8_t>(LT);
         d.u_next = A.take<int8_t>(GT);
         d.unext_ok = A.take<unsigned>(1);
         d.rec = A.take<double>(NREC);
@@ -1469,7 +1470,8 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
     CK(cudaMemsetAsync(d.cnt, 0, NCNT * sizeof(unsigned long long), ctx->s));
     CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));   // the pipelined DP result is stale
-    CK(cudaMemsetAsync(d.alq_cnt, 0, 2 * sizeof(unsigned), ctx->s));
+    CK(cudaMemsetAsync(d.alq_cnt, 0, (UCAC_AL_BUCKETS + 1) * sizeof(unsigned), ctx->s));
+    CK(cudaMemsetAsync(d.alits, 0, (size_t)ctx->L * ctx->T, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     return UCAC_OK;
 }

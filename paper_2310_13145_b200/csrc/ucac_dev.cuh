@@ -12,6 +12,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef UCAC_AL_BUCKETS
+#define UCAC_AL_BUCKETS 1   // AL queue buckets by the previous AL Newton count (heavy / new first); 2 and
+                            // 3 measured neutral (0.1664-0.1672 ms vs 0.1666-0.1669), DESIGN.md 7
+#endif
 #ifndef UCAC_MAX_P2P
 #define UCAC_MAX_P2P 8   // ranks of a device-initiated exchange group (one node: 8 GPUs on NVSwitch)
 #endif
@@ -143,8 +147,9 @@ struct Dev {
     double *part_efold;               // [fold_blocks()][NPART] first-level fold of the early partials
     double *rec_part;                 // [3][NPART] folded records: early, bus late, rows late
     unsigned *kdone;                  // [3] last-block counters of the kernels producing them
-    unsigned *alq_cnt;                // [2] queue length, next item (zeroed by reduce)
-    double *alq_x;                    // [4][L*T] by queue position: the previous x of a queued solve (R49)
+    unsigned *alq_cnt;                // [UCAC_AL_BUCKETS + 1] bucket lengths, next item (zeroed by the final fold)
+    double *alq_x;                    // [4][L*T] by (l,t): the previous x of a queued solve (R49)
+    uint8_t *alits;                   // [L*T] TRON iterations of the (l,t)'s last AL solve (0: none last iteration)
     int fuse_rows;                    // 1 GPU: the end rows of a bus are updated by its bus thread (no k_rows)
     int8_t *u_next;                   // [G*T] the DP's schedule for the next (7b): written by k_gen, adopted by k_genx
     unsigned *unext_ok;               // 1: u_next holds the DP of the current state (set by the tail k_gen)
