@@ -92,7 +92,8 @@ __device__ __forceinline__ void zy_vals_div(double r, double rho, double bpr, do
 #define UCAC_RED_SKIP 1   // idle warps skip the block reduction's shuffle tree (bitwise neutral)
 #endif
 // deterministic block reduction -> part[blockIdx.x][NPART]
-__device__ void block_reduce_store(Acc &a, double *part) {
+__device__ void block_reduce_store(Acc &a, double *part, int vb = -1) {
+    if (vb < 0) vb = blockIdx.x;
     __shared__ double sh[32][NPART];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // A warp none of whose lanes touched its accumulator (every slot still +0.0, compared
@@ -122,7 +123,7 @@ __device__ void block_reduce_store(Acc &a, double *part) {
         const bool isum = (k == P_RZ2 || k == P_Z2 || k == P_OBJ);
         double v = sh[0][k];
         for (int w = 1; w < nw; w++) v = isum ? v + sh[w][k] : fmax(v, sh[w][k]);
-        part[(size_t)blockIdx.x * NPART + k] = v;
+        part[(size_t)vb * NPART + k] = v;
     }
 }
 
@@ -138,15 +139,23 @@ __device__ void block_reduce_store(Acc &a, double *part) {
 #define TH(k, i) d.tauh[(size_t)(k) * LTH + (i)]
 
 constexpr int BUS_THREADS = 128;
-// minimum resident blocks per SM the compiler must fit (register cap), tuning knobs (0: none)
-#ifndef UCAC_BUS_MINB
-#define UCAC_BUS_MINB 1
+// __launch_bounds__ minimum resident blocks per SM (register caps), unset = none: an explicit 1
+// is not the same as none (ptxas gave k_bus 148 instead of 128 registers, +3 us); measured
+// DESIGN.md 7
+#ifdef UCAC_BUS_MINB
+#define BUS_BOUNDS __launch_bounds__(BUS_THREADS, UCAC_BUS_MINB)
+#else
+#define BUS_BOUNDS __launch_bounds__(BUS_THREADS)
 #endif
-#ifndef UCAC_ROWS_MINB
-#define UCAC_ROWS_MINB 1
+#ifdef UCAC_ROWS_MINB
+#define ROWS_BOUNDS __launch_bounds__(ROWS_THREADS, UCAC_ROWS_MINB)
+#else
+#define ROWS_BOUNDS __launch_bounds__(ROWS_THREADS)
 #endif
-#ifndef UCAC_UBAR_MINB
-#define UCAC_UBAR_MINB 1
+#ifdef UCAC_UBAR_MINB
+#define UBAR_BOUNDS __launch_bounds__(UBAR_THREADS, UCAC_UBAR_MINB)
+#else
+#define UBAR_BOUNDS __launch_bounds__(UBAR_THREADS)
 #endif
 constexpr int UBAR_THREADS = 64;
 constexpr int ROWS_THREADS = 128;
@@ -303,7 +312,8 @@ __device__ __forceinline__ void zy_s(double r, double rho, double ib, double bpr
 // and takes items j = its thread id + k * grid stride of the concatenation -- a deterministic
 // list in index order, so the late kernels need a grid sized to the marked work only, and
 // their fold order is fixed.
-__device__ __forceinline__ void block_compact(int nitems, const int *items, int *list, unsigned *cnt, int cap) {
+__device__ __forceinline__ void block_compact(int nitems, const int *items, int *list, unsigned *cnt, int cap, int vb = -1) {
+    if (vb < 0) vb = blockIdx.x;
     __shared__ int wsum[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int incl = nitems;   // inclusive warp scan of the per-thread counts
@@ -320,8 +330,8 @@ __device__ __forceinline__ void block_compact(int nitems, const int *items, int 
         tot += wsum[w];
     }
     off += incl - nitems;
-    for (int q = 0; q < nitems; q++) list[(size_t)blockIdx.x * cap + off + q] = items[q];
-    if (threadIdx.x == 0) cnt[blockIdx.x] = (unsigned)tot;
+    for (int q = 0; q < nitems; q++) list[(size_t)vb * cap + off + q] = items[q];
+    if (threadIdx.x == 0) cnt[vb] = (unsigned)tot;
     __syncthreads();
 }
 // exclusive offsets pre[0..n] of cnt[0..n) in shared memory (block-wide); returns the total
@@ -521,7 +531,7 @@ __device__ __forceinline__ void bus_end_rows(const Dev &d, const Ctl &c, int k, 
 }
 
 template <bool STRICT>
-__global__ void __launch_bounds__(BUS_THREADS, UCAC_BUS_MINB) k_bus(Dev d) {
+__global__ void BUS_BOUNDS k_bus(Dev d) {
     TL_KERNEL(K_BUS);
     if (d.st->done) return;
     const Ctl c(d);
@@ -587,22 +597,28 @@ __device__ __forceinline__ void end_rows(const Dev &d, const Ctl &c, int l, int 
 // k_rows (early): one thread per (l,t), the ends whose bus is not marked (coalesced row
 // arrays, as k_branch); the marked ends are done by k_rows_late.
 template <bool STRICT>
-__global__ void __launch_bounds__(ROWS_THREADS, UCAC_ROWS_MINB) k_rows(Dev d) {
+__global__ void ROWS_BOUNDS k_rows(Dev d) {
     TL_KERNEL(K_ROWS);
     if (d.st->done) return;
     const Ctl c(d);
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    Acc acc;
-    int items[2], ni = 0;
-    if (k < d.L * d.T && own_t(d, k % d.T)) {
-        const int l = k / d.T, t = k - l * d.T;
-        if (d.rmark[0][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 0, acc);
-        else items[ni++] = k << 1;
-        if (d.rmark[1][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 1, acc);
-        else items[ni++] = (k << 1) | 1;
+    // virtual blocks: with a capped grid (UCAC_ROWS_BPSM) each block takes blocks vb, vb + grid, ...
+    // of the full launch, each with its own list slot range and partial slot -- the same lists and
+    // partials, so the same bits, in fewer SM slots (room for k_bus_late when the AL tail ends)
+    for (int vb = blockIdx.x; vb < d.nblk_rows; vb += gridDim.x) {
+        if (vb != (int)blockIdx.x) __syncthreads();   // shared scratch of the previous pass
+        const int k = vb * blockDim.x + threadIdx.x;
+        Acc acc;
+        int items[2], ni = 0;
+        if (k < d.L * d.T && own_t(d, k % d.T)) {
+            const int l = k / d.T, t = k - l * d.T;
+            if (d.rmark[0][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 0, acc);
+            else items[ni++] = k << 1;
+            if (d.rmark[1][k] != c.stamp) end_rows<STRICT>(d, c, l, t, 1, acc);
+            else items[ni++] = (k << 1) | 1;
+        }
+        block_compact(ni, items, d.lrow, d.lrow_cnt, 2 * ROWS_THREADS, vb);   // the late end list
+        block_reduce_store(acc, d.part_rows, vb);
     }
-    block_compact(ni, items, d.lrow, d.lrow_cnt, 2 * ROWS_THREADS);   // the late end list
-    block_reduce_store(acc, d.part_rows);
 }
 
 // Late phase (after the AL tail): k_bus_late solves the marked bus-periods, k_rows_late updates
@@ -818,7 +834,7 @@ __device__ void boxqp3_lanes(int n, int m, const double (*c)[3], const double *e
 // LIT: the literal Eq. 5f ramp-down row (variant bit 16, R52), a separate instantiation so the
 // default kernel carries none of its code
 template <bool LIT>
-__global__ void __launch_bounds__(UBAR_THREADS, UCAC_UBAR_MINB) k_ubar(Dev d) {
+__global__ void UBAR_BOUNDS k_ubar(Dev d) {
     TL_KERNEL(K_UBAR);
     if (d.st->done) return;
     const int T = d.T;
@@ -1207,6 +1223,7 @@ int nblk_rows(int L, int T) { return (L * T + ROWS_THREADS - 1) / ROWS_THREADS; 
 #ifndef UCAC_UBAR_PRIO
 #define UCAC_UBAR_PRIO 1
 #endif
+static int sm_count();
 template <typename... KArgs>
 static void launch_sweep(bool hi, void (*k)(KArgs...), dim3 g, dim3 b, cudaStream_t s, KArgs... args) {
     if (hi) launch_hi_prio(k, g, b, 0, s, args...);
@@ -1215,8 +1232,16 @@ static void launch_sweep(bool hi, void (*k)(KArgs...), dim3 g, dim3 b, cudaStrea
 void launch_bus(const Dev &d, cudaStream_t s) {
     launch_sweep(UCAC_SWEEP_PRIO, d.strict ? k_bus<true> : k_bus<false>, dim3(d.nblk_bus), dim3(BUS_THREADS), s, d);
 }
+// k_rows grid: UCAC_ROWS_BPSM blocks per SM (virtual blocks; 0 = one block per 128 (l,t)).  At 112
+// registers 4 blocks fit an SM; 3 leave one block's registers free, so k_bus_late starts as soon as
+// the AL tail ends instead of after k_rows' last blocks (timeline: 131 -> 124 us; step 0.1676 ->
+// 0.1656 ms, iterate bitwise unchanged; 2: 0.1699, 4: 0.1670)
+#ifndef UCAC_ROWS_BPSM
+#define UCAC_ROWS_BPSM 3
+#endif
 void launch_rows(const Dev &d, cudaStream_t s) {
-    launch_sweep(UCAC_SWEEP_PRIO, d.strict ? k_rows<true> : k_rows<false>, dim3(d.nblk_rows), dim3(ROWS_THREADS), s, d);
+    const int grid = UCAC_ROWS_BPSM > 0 ? std::min(d.nblk_rows, UCAC_ROWS_BPSM * sm_count()) : d.nblk_rows;
+    launch_sweep(UCAC_SWEEP_PRIO, d.strict ? k_rows<true> : k_rows<false>, dim3(grid), dim3(ROWS_THREADS), s, d);
 }
 #ifndef UCAC_LATE_PRIO
 #define UCAC_LATE_PRIO 1
