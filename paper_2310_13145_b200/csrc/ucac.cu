@@ -27,6 +27,9 @@
 #ifndef UCAC_EARLY_FORK
 #define UCAC_EARLY_FORK 1
 #endif
+#ifndef UCAC_UNROLL_MAX_LT
+#define UCAC_UNROLL_MAX_LT 50000   // L*T above which no 16-iteration graph is built
+#endif
 #ifndef UCAC_NODE_PRIO
 #define UCAC_NODE_PRIO 0   // honouring node priorities measured neutral (0.1700-0.1712 ms)
 #endif
@@ -61,7 +64,7 @@ static thread_local std::string g_create_err;
 struct Local {
     int B = 0, Bo = 0, G = 0, L = 0, Lp = 0, T = 0, ref = -1;
     double S = 100.0;
-    std::vector<double> gs, bs, vmin, vmax, pdT, qdT;            // buses (own + ghost)
+    std::vector<double> gs, bs, vmin, vmax;                      // buses (own + ghost)
     std::vector<int> from, to;                                    // local branches (local bus ids)
     std::vector<double> ysoa, rate;
     std::vector<int> gbus, tu, td, u0, hold;                      // local generators
@@ -97,14 +100,6 @@ static Local localize_periods(Local P, const ucac_horizon *hz, const ucac_uc *uc
     P.own1 = hl + (g1 - g0);
     P.Tmax = 0;
     for (int r = 0; r < nranks; r++) P.Tmax = std::max(P.Tmax, P.tstart[r + 1] - P.tstart[r]);
-    std::vector<double> pd((size_t)P.B * Tl), qd((size_t)P.B * Tl);
-    for (int a = 0; a < P.B; a++)
-        for (int t = 0; t < Tl; t++) {
-            pd[(size_t)a * Tl + t] = P.pdT[(size_t)a * Tg + P.t_off + t];
-            qd[(size_t)a * Tl + t] = P.qdT[(size_t)a * Tg + P.t_off + t];
-        }
-    P.pdT.swap(pd);
-    P.qdT.swap(qd);
     if (!P.uinit.empty()) {
         std::vector<int8_t> u((size_t)P.G * Tl);
         for (int g = 0; g < P.G; g++)
@@ -151,13 +146,6 @@ static Local build_local(const ucac_network *net, const ucac_horizon *hz, const 
         P.vmax.push_back(net->bus_vmax[i]);
     }
     P.ref = h.bus_local[net->ref_bus] >= 0 && h.bus_local[net->ref_bus] < P.Bo ? h.bus_local[net->ref_bus] : -1;
-    P.pdT.assign((size_t)P.B * T, 0.0);
-    P.qdT.assign((size_t)P.B * T, 0.0);
-    for (int a = 0; a < P.Bo; a++)
-        for (int t = 0; t < T; t++) {
-            P.pdT[(size_t)a * T + t] = hz->pd[(size_t)t * B + bus_glob[a]];
-            P.qdT[(size_t)a * T + t] = hz->qd[(size_t)t * B + bus_glob[a]];
-        }
     P.ysoa.assign((size_t)8 * P.L, 0.0);
     for (int a = 0; a < P.L; a++) {
         int l = h.local_branch[a];
@@ -328,6 +316,25 @@ static void pinned_status_put(DevStatus *p) {
     g_pinned_free.push_back(p);
 }
 
+// Page-locked staging image for ucac_create's upload, kept across contexts and grown on demand
+// (the upload is one DMA from it instead of the driver's pageable double copy); held under its
+// mutex from the host-side layout to the end of the upload.
+static std::mutex g_stage_mu;
+static char *g_stage = nullptr;
+static size_t g_stage_cap = 0;
+static char *stage_get(size_t n) {   // caller holds g_stage_mu
+    if (n <= g_stage_cap) return g_stage;
+    if (g_stage) cudaFreeHost(g_stage);
+    g_stage = nullptr;
+    g_stage_cap = 0;
+    const size_t cap = std::max<size_t>(n + n / 4, 1 << 20);
+    void *p = nullptr;
+    if (cudaMallocHost(&p, cap) != cudaSuccess) return nullptr;
+    g_stage = (char *)p;
+    g_stage_cap = cap;
+    return g_stage;
+}
+
 // Bump allocator over one device allocation: 256-byte aligned slices.  With base == 0 it only
 // measures (the sizing pass); with `stage` set, put() also copies the host vector into the
 // staging image at the slice's offset.
@@ -340,18 +347,32 @@ struct Arena {
         off = o + std::max<size_t>(n, 1) * sizeof(Tp);
         return base ? (Tp *)(base + o) : nullptr;
     }
+    // a slice of n elements written by fill(dst) straight into the staging image
+    template <class Tp, class F> Tp *put_fill(size_t n, F fill) {
+        const size_t o = (off + 255) & ~(size_t)255;
+        Tp *p = take<Tp>(n);
+        if (stage) fill((Tp *)(stage + o));
+        return p;
+    }
     template <class Tp> Tp *put(const std::vector<Tp> &v) {
         const size_t o = (off + 255) & ~(size_t)255;
         Tp *p = take<Tp>(v.size());
         if (stage && !v.empty()) memcpy(stage + o, v.data(), v.size() * sizeof(Tp));
+        if (stage && v.empty()) memset(stage + o, 0, sizeof(Tp));   // (the staging image is reused)
         return p;
     }
 };
 
 static bool finite_all(const double *a, size_t n) {
-    for (size_t i = 0; i < n; i++)
-        if (!std::isfinite(a[i])) return false;
-    return true;
+    // exponent all ones <=> inf or NaN; a branch-free OR over the bits (vectorises)
+    const uint64_t E = 0x7ff0000000000000ull;
+    uint64_t bad = 0;
+    for (size_t i = 0; i < n; i++) {
+        uint64_t b;
+        memcpy(&b, a + i, sizeof b);
+        bad |= (uint64_t)((b & E) == E);
+    }
+    return bad == 0;
 }
 
 static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co,
@@ -505,6 +526,10 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ctx->G = G;
     ctx->L = L;
     ctx->T = T;
+    // the 16-iteration graph amortises launch latency where an iteration is short; a large case
+    // (an iteration of ~0.1 ms) runs single-iteration graphs back to back and skips capturing and
+    // instantiating the long one in ucac_create
+    if ((long long)L * T > UCAC_UNROLL_MAX_LT) ctx->gunroll[1] = 1;
     auto bail = [&](ucac_status s) {
         g_create_err = ctx->err;
         ucac_destroy(ctx);
@@ -614,8 +639,19 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.bs = A.put(P.bs);
         d.vmin = A.put(P.vmin);
         d.vmax = A.put(P.vmax);
-        d.pd = A.put(P.pdT);
-        d.qd = A.put(P.qdT);
+        // demand [bus][local period], owned buses (ghost rows 0), transposed from the caller's
+        // [period][bus] arrays straight into the staging image (reads in input order)
+        auto demand = [&](const double *src) {
+            return [&, src](double *dst) {
+                for (int a = P.Bo; a < P.B; a++)
+                    for (int t = 0; t < T; t++) dst[(size_t)a * T + t] = 0.0;
+                for (int t = 0; t < T; t++)
+                    for (int a = 0; a < P.Bo; a++)
+                        dst[(size_t)a * T + t] = src[(size_t)(P.t_off + t) * net->nbus + P.bus_global[a]];
+            };
+        };
+        d.pd = A.put_fill<double>((size_t)B * T, demand(hz->pd));
+        d.qd = A.put_fill<double>((size_t)B * T, demand(hz->qd));
         d.bg_ptr = A.put(P.bgp);
         d.bg_idx = A.put(P.bgi);
         d.be_ptr = A.put(P.bep);
@@ -718,15 +754,21 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         e = cudaMallocAsync(&base, sizing.off, ctx->s);
         if (e != cudaSuccess) return bail(fail(ctx, UCAC_ENOMEM, "cudaMalloc arena of %zu B", sizing.off));
         ctx->dalloc.push_back(base);
-        std::vector<char> stage(sizing.up_end, 0);
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        std::vector<char> pageable;   // if no page-locked memory can be had
+        char *stage = stage_get(sizing.up_end);
+        if (!stage) {
+            pageable.assign(sizing.up_end, 0);
+            stage = pageable.data();
+        }
         Arena A;
         A.base = (uintptr_t)base;
-        A.stage = stage.data();
+        A.stage = stage;
         layout(A);
-        if (cudaMemcpyAsync(base, stage.data(), A.up_end, cudaMemcpyHostToDevice, ctx->s) != cudaSuccess ||
+        if (cudaMemcpyAsync(base, stage, A.up_end, cudaMemcpyHostToDevice, ctx->s) != cudaSuccess ||
             cudaMemsetAsync((char *)base + A.up_end, 0, A.off - A.up_end, ctx->s) != cudaSuccess)
             return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
-        // the pageable staging buffer must outlive the copy
+        // the staging image is reused by the next create: the copy must have finished
         if (cudaStreamSynchronize(ctx->s) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
     }
     if (tcut) {
@@ -1033,6 +1075,7 @@ static void enqueue_iteration(ucac_ctx *ctx) {
 
 static ucac_status build_graphs(ucac_ctx *ctx) {
     for (int gi = 0; gi < 2; gi++) {
+        if (gi == 1 && ctx->gunroll[1] == 1) break;   // single-iteration graphs only
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
         ctx->nccl_err = ncclSuccess;
@@ -1086,8 +1129,8 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
     }
     ucac_status s = set_control(ctx, stop_on_primal > 0, primal_target);
     if (s != UCAC_OK) return s;
-    int big = ctx->gunroll[1];
-    int nb = n / big, nr = n % big;
+    const int big = ctx->gexec[1] ? ctx->gunroll[1] : n + 1;
+    const int nb = n / big, nr = n % big;
     for (int k = 0; k < nb; k++) CK(cudaGraphLaunch(ctx->gexec[1], ctx->s));
     for (int k = 0; k < nr; k++) CK(cudaGraphLaunch(ctx->gexec[0], ctx->s));
     CK(cudaGetLastError());

@@ -356,11 +356,24 @@ class Context:
         _check(self.L.ucac_residuals(self.h, C.byref(r)), self.h)
         return {n: getattr(r, n) for n, _ in Report._fields_}
 
-    def solution(self) -> dict:
+    def solution_shapes(self) -> dict:
+        """{field: (size, dtype)} of solution()'s arrays (for caller-owned, e.g. pinned, buffers)"""
         GT, LT, BT = (len(self._local["gen"]) * self.Tl, len(self._local["branch"]) * self.Tl,
                       len(self._local["bus"]) * self.Tl)
-        out = {"u_on": np.zeros(GT, np.int8), "p": np.zeros(GT), "q": np.zeros(GT), "wbar": np.zeros(BT),
-               "thetabar": np.zeros(BT), "flows": np.zeros(4 * LT)}
+        return {"u_on": (GT, np.int8), "p": (GT, np.float64), "q": (GT, np.float64), "wbar": (BT, np.float64),
+                "thetabar": (BT, np.float64), "flows": (4 * LT, np.float64)}
+
+    def solution(self, out: dict | None = None) -> dict:
+        """ucac_get_solution into fresh arrays, or into `out` (caller-owned contiguous arrays of
+        solution_shapes(), e.g. page-locked buffers reused across calls)"""
+        shapes = self.solution_shapes()
+        if out is None:
+            out = {k: np.zeros(n, t) for k, (n, t) in shapes.items()}
+        else:
+            for k, (n, t) in shapes.items():
+                a = out[k]
+                if a.dtype != t or a.size != n or not a.flags["C_CONTIGUOUS"]:
+                    raise ValueError(f"solution buffer {k}: need {n} contiguous {np.dtype(t)}")
         s = Solution(out["u_on"].ctypes.data_as(i8p), *[out[k].ctypes.data_as(dp) for k in
                                                          ("p", "q", "wbar", "thetabar", "flows")])
         _check(self.L.ucac_get_solution(self.h, C.byref(s)), self.h)

@@ -248,6 +248,30 @@ def test_stop_on_primal_and_report():
     assert rep["objective"] == pytest.approx(o.report()["objective"], rel=1e-6)
     sol = c.solution()
     assert sol["p"].shape == (3,) and np.all(sol["u_on"] == 1)
+    # caller-owned page-locked buffers (the e2e bench path): the same bytes
+    import torch
+    buf = {k: torch.empty(n, dtype=torch.int8 if t == np.int8 else torch.float64, pin_memory=True).numpy()
+           for k, (n, t) in c.solution_shapes().items()}
+    for a in buf.values():
+        a.fill(7)
+    sol2 = c.solution(out=buf)
+    assert all(sol2[k] is buf[k] and sol2[k].tobytes() == sol[k].tobytes() for k in sol)
+    with pytest.raises(ValueError):
+        c.solution(out={**buf, "p": np.zeros(2)})
+
+
+def test_pegase_create_uses_single_iteration_graphs_same_bits():
+    """ucac_create builds no 16-iteration graph above L*T = 50,000 (UCAC_UNROLL_MAX_LT): a 20-
+    iteration call is 20 single-iteration graph launches; case300's unrolled graph path and
+    pegase's single-graph path both reproduce iteration-by-iteration calls bitwise."""
+    for name in ("case300", "pegase2869"):
+        pb, pr = inputs.build_config(name)
+        a, b = ucac.Context(pb, pr), ucac.Context(pb, pr)
+        a.iterate(20)
+        for _ in range(20):
+            b.iterate(1)
+        sa, sb = a.get_state(), b.get_state()
+        assert all(sa[k].tobytes() == sb[k].tobytes() for k in sa), name
 
 
 def test_edge_cases():
@@ -271,6 +295,13 @@ def test_edge_cases():
         ucac.Context(bad, pr)
     with pytest.raises(ucac.UcacError):
         ucac.Context(inputs.case9(T=4), inputs.Params(rho_pq=-1, rho_va=1, rho_uc=1))
+    # non-finite inputs (the bitwise finiteness scan of validate): EINVAL
+    for field, idx, v in (("pd", (3, 5), np.nan), ("br_y", (2, 6), np.inf), ("pmax", (1,), -np.inf)):
+        bad = inputs.case9(T=4)
+        getattr(bad, field)[idx] = v
+        with pytest.raises(ucac.UcacError) as e:
+            ucac.Context(bad, pr)
+        assert e.value.code == 1, field
 
 
 @pytest.mark.parametrize("name,iters", [("case9", 40), ("case30", 60), ("case118", 40)])
