@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
 // ------------------------------------------------------------------------- (7c) ubar
 __device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
-__device__ void solve_small(int nf, double A[3][3], const double *b, double *x) {
+__device__ __forceinline__ void solve_small(int nf, double A[3][3], const double *b, double *x) {
     if (nf == 1) {
         x[0] = b[0] / A[0][0];
         return;
@@ -794,6 +794,86 @@ __device__ void boxqp3_range(int n, int m, const double (*c)[3], const double *e
         }
     }
 }
+// The same enumeration with the problem size fixed at compile time: every loop unrolls, the
+// activity states, the free index lists and the reduced systems become constants and registers
+// (boxqp3_range's runtime n, m keep them in local memory, a ~30-cycle dependent access each), and
+// the 3^N independent candidates interleave.  Identical operations in identical order (this unit
+// builds with -fmad=false and IEEE division), so the pick and its bits are boxqp3_range's.
+template <int N, int M>
+__device__ __forceinline__ void boxqp3_fixed(const double (*c)[3], const double *e, double *v) {
+    double H[3][3], bb[3];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < M; k++) s = s + c[k][i] * c[k][j];
+            H[i][j] = s;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; k++) s = s + c[k][i] * e[k];
+        bb[i] = s;
+    }
+    double best = INFINITY;
+#pragma unroll
+    for (int i = 0; i < 3; i++) v[i] = 0.0;
+    constexpr int NC = N == 3 ? 27 : (N == 2 ? 9 : 3);
+#pragma unroll
+    for (int idx = 0; idx < NC; idx++) {
+        int st[3] = {0, 0, 0}, r = idx;
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            st[i] = r % 3;
+            r /= 3;
+        }
+        double vv[3] = {0, 0, 0};
+        int fi[3] = {0, 0, 0}, nf = 0;
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            if (st[i] == 0) fi[nf++] = i;
+            else vv[i] = (st[i] == 1) ? 0.0 : 1.0;
+        }
+        if (nf > 0) {
+            double A[3][3], rhs[3], sol[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                if (a >= nf) break;
+                double s = bb[fi[a]];
+#pragma unroll
+                for (int j = 0; j < N; j++)
+                    if (st[j] != 0) s = s - H[fi[a]][j] * vv[j];
+                rhs[a] = s;
+#pragma unroll
+                for (int b2 = 0; b2 < 3; b2++)
+                    if (b2 < nf) A[a][b2] = H[fi[a]][fi[b2]];
+            }
+            solve_small(nf, A, rhs, sol);
+#pragma unroll
+            for (int a = 0; a < 3; a++)
+                if (a < nf) vv[fi[a]] = sol[a];
+        }
+#pragma unroll
+        for (int i = 0; i < N; i++) vv[i] = clamp01(vv[i]);
+        double obj = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; k++) {
+            double rr = e[k];
+#pragma unroll
+            for (int i = 0; i < N; i++) rr = rr - c[k][i] * vv[i];
+            obj = obj + 0.5 * rr * rr;
+        }
+        if (obj < best) {
+            best = obj;
+#pragma unroll
+            for (int i = 0; i < N; i++) v[i] = vv[i];
+        }
+    }
+}
+#ifndef UCAC_UBAR_FIXED
+#define UCAC_UBAR_FIXED 1
+#endif
 __device__ void boxqp3(int n, int m, const double (*c)[3], const double *e, double *v) {
     double best;
     int bidx;
@@ -928,11 +1008,18 @@ __global__ void UBAR_BOUNDS k_ubar(Dev d) {
             if (lit) { zr[9] = ZG(G_RD, i + 1); yr[9] = YG(G_RD, i + 1); lr[9] = LG(G_RD, i + 1); }
         }
         double v[3];
-        boxqp3_lanes(n, m, cm, e, v, sub, mask);
+        if (UBAR_LANES == 1 && UCAC_UBAR_FIXED) {   // (the row arrays stay in registers)
+            if (nxt) boxqp3_fixed<3, 9>(cm, e, v);
+            else boxqp3_fixed<2, lit ? 6 : 7>(cm, e, v);
+        } else {
+            boxqp3_lanes(n, m, cm, e, v, sub, mask);
+        }
         if (sub == 0) {
         {
             double chk = nf0(v[0]) + nf0(v[1]) + nf0(v[2]);
-            for (int q2 = 0; q2 < m; q2++) chk = chk + nf0(e[q2]);
+#pragma unroll
+            for (int q2 = 0; q2 < 9; q2++)
+                if (q2 < m) chk = chk + nf0(e[q2]);
             if (!isfinite(chk)) report_nonfinite(d, K_UBAR, g, t);
         }
         const double on_n = v[0], sd_n = v[1];
@@ -992,7 +1079,8 @@ __global__ void UBAR_BOUNDS k_ubar(Dev d) {
             // literal Eq. 5f (R52): RD_1 = (d - s) + R_D u0 + S_D ubar^su_1 joins this group
             e1[2] = ((dd - srd) + RDn * (double)u0) + ZG(G_RD, i) + YG(G_RD, i) / ruc;
             double v1[3];
-            boxqp3(1, lit ? 3 : 2, c1, e1, v1);
+            if (UCAC_UBAR_FIXED) boxqp3_fixed<1, lit ? 3 : 2>(c1, e1, v1);
+            else boxqp3(1, lit ? 3 : 2, c1, e1, v1);
             d.ub_su[i] = v1[0];
             const double dsu = v1[0] - su_o;
             zy_row_div((double)sut - v1[0], ruc, bpr, &ZG(G_DSU, i), &YG(G_DSU, i), &LG(G_DSU, i), pending, beta_lam, lmax, dsu,
