@@ -157,8 +157,9 @@ struct Dev {
     unsigned long long *tl;           // [2*NKERN] diagnostic timeline (UCAC_PROF builds only)
 };
 
-// UCAC_PROF builds: per kernel, the earliest block start and the latest block-thread-0 exit on the
-// global timer (ns), for graph timelines (tools/timeline.py).  Empty otherwise.
+// UCAC_PROF builds: per kernel, the earliest block start and the latest warp exit (lane 0 of every
+// warp: a block's warps can outlive its thread 0, as the AL solves do) on the global timer (ns),
+// for graph timelines (tools/timeline.py).  Empty otherwise.
 #ifdef UCAC_PROF
 struct TlGuard {
     unsigned long long *p;
@@ -170,7 +171,7 @@ struct TlGuard {
         }
     }
     __device__ ~TlGuard() {
-        if (threadIdx.x == 0) {
+        if ((threadIdx.x & 31) == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             atomicMax(p + 1, t);
