@@ -113,6 +113,13 @@ typedef struct {
                            FMA contraction, sin/cos by the explicit polynomial of R54 -- the iterate
                            then equals the CPU oracle's bit for bit (up to the order of the S8 sums,
                            which feed only the inner/outer decisions).  Slower; for parity runs. */
+    int32_t diverge_window;  /* divergence detector ("primal residual grows 10x over 200
+                                inner iterations -> abort with diagnostics"): 0 = off; in [1, 255] an
+                                ucac_iterate call stops (as at stop_on_primal) at the first iteration i
+                                with primal_inf_i > diverge_factor * primal_inf_{i - diverge_window},
+                                once per run; ucac_report.diverged_iter names it.  The next call
+                                continues.  EINVAL outside [0, 255]. */
+    double diverge_factor;   /* (SPEC: window 200, factor 10) */
 } ucac_params;
 
 /* Multi-GPU (bus-graph cut).  NULL = single GPU.
@@ -237,8 +244,18 @@ typedef struct {
     int32_t err_kernel, err_iter;     /* first non-finite: kernel id + 1 (0 = none), iteration */
     int32_t err_comp, err_period;     /* ... and where: the component (global generator, branch or
                                          bus index, by the kernel's kind) and the period (0-based) */
+    int32_t diverged_iter;            /* first iteration the divergence detector fired (0 = never) */
+    int32_t hist_len;                 /* records in ucac_history (min(inner_total, UCAC_HIST_CAP)) */
 } ucac_report;
 ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *rep);
+
+/* Per-iteration record history ("||z|| history"): the device keeps the last
+ * UCAC_HIST_CAP inner iterations' (primal_inf, dual_inf, z_inf, z_2, objective, beta), written by
+ * the iteration's final fold.  out (host) receives the last min(n, hist_len) records, oldest first,
+ * UCAC_HIST_FIELDS doubles each; *got their number.  ucac_set_state empties it. */
+#define UCAC_HIST_CAP 256
+#define UCAC_HIST_FIELDS 6
+ucac_status ucac_history(ucac_ctx *ctx, double *out, int32_t n, int32_t *got);
 
 /* Solution (host buffers): u_on [ngen*T]; p, q [ngen*T]; wbar, thetabar [nbus*T];
  * flows [nbranch*T*4] = (p_ij, q_ij, p_ji, q_ji) of the branch x-side. */

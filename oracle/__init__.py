@@ -86,7 +86,7 @@ class Params_c(C.Structure):
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
                 ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32),
-                ("plain", C.c_int32)]
+                ("plain", C.c_int32), ("diverge_window", C.c_int32), ("diverge_factor", C.c_double)]
 
 
 class Report_c(C.Structure):
@@ -97,7 +97,8 @@ class Report_c(C.Structure):
                 ("tron_capped", C.c_int64), ("al_active", C.c_int64), ("al_capped", C.c_int64),
                 ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32),
                 ("flops_fast", C.c_double), ("flops_al", C.c_double),
-                ("newton_fast", C.c_int64), ("newton_al", C.c_int64)]
+                ("newton_fast", C.c_int64), ("newton_al", C.c_int64),
+                ("diverged_iter", C.c_int32), ("pad_", C.c_int32)]
 
 
 STATE_FIELDS = [("u", np.int8, "GT"), ("p", np.float64, "GT"), ("q", np.float64, "GT"),
@@ -158,7 +159,8 @@ def params_c(pr, plain: bool = False) -> Params_c:
     return Params_c(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max,
                     pr.beta_max, pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled,
                     pr.tron_gtol_rel, pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel,
-                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed, pr.variant, int(plain))
+                    pr.al_sigma_max_rel, pr.al_sigma_decay, pr.uc_fixed, pr.variant, int(plain),
+                    pr.diverge_window, pr.diverge_factor)
 
 
 class Oracle:

@@ -47,6 +47,9 @@ struct orc_ctx {
     double *zb, *yb, *lb;           /* [8*L*T] */
     double beta, znorm_prev;
     int64_t outer_k, inner_total, inner_since;
+    /* divergence detector: primal residual of the last 256 iterations (NaN = none) */
+    double phist[256];
+    int done;
     /* CSR incidence, canonical order (gens by index, then ends by (l, side)) */
     int32_t *bg_ptr, *bg_idx, *be_ptr, *be_idx;
     orc_report rep;
@@ -1035,6 +1038,7 @@ static int bad(double v) { return !(v == v) || v == INFINITY || v == -INFINITY; 
 
 int orc_create(const orc_problem *pb, const orc_params *pr, orc_ctx **out) {
     *out = NULL;
+    if (pr->diverge_window < 0 || pr->diverge_window >= 256) return 1;
     int B = pb->nbus, G = pb->ngen, L = pb->nbranch, T = pb->T;
     if (B <= 0 || G <= 0 || L <= 0 || T <= 0 || pb->ref_bus < 0 || pb->ref_bus >= B) return 1;
     if (!(pr->rho_pq > 0) || !(pr->rho_va > 0) || !(pr->rho_uc > 0)) return 1;
@@ -1148,6 +1152,8 @@ int orc_create(const orc_problem *pb, const orc_params *pr, orc_ctx **out) {
     c->inner_since = 0;
     memset(&c->rep, 0, sizeof(c->rep));
     c->rep.beta = c->beta;
+    for (int k = 0; k < 256; k++) c->phist[k] = NAN;
+    c->done = 0;
     *out = c;
     return 0;
 }
@@ -1572,10 +1578,26 @@ static void one_iteration(orc_ctx *c) {
     rp->outer_total = c->outer_k - 1;
     rp->inner_since_outer = (int32_t)c->inner_since;
     rp->outer_k = (int32_t)c->outer_k;
+
+    /* ---- divergence detector ("primal residual grows 10x over 200 inner iterations
+     * -> abort with diagnostics"): primal_i > factor * primal_{i - window} ends the call ---- */
+    {
+        const int64_t it = c->inner_total;
+        c->phist[(it - 1) % 256] = nm.pinf;
+        const int w = pr->diverge_window;
+        if (w > 0 && it > w && rp->diverged_iter == 0) {
+            const double old = c->phist[(it - 1 - w) % 256];
+            if (nm.pinf > pr->diverge_factor * old) {
+                rp->diverged_iter = (int32_t)it;
+                c->done = 1;
+            }
+        }
+    }
 }
 
 int orc_iterate(orc_ctx *c, int32_t n) {
-    for (int k = 0; k < n; k++) one_iteration(c);
+    c->done = 0;   /* (a call that the detector ended: the next call continues) */
+    for (int k = 0; k < n && !c->done; k++) one_iteration(c);
     return 0;
 }
 
@@ -1620,6 +1642,9 @@ void orc_set_state(orc_ctx *c, const orc_state *s) {
     memcpy(c->wbar, s->wbar, D * BT); memcpy(c->thbar, s->thbar, D * BT);
     c->beta = s->scal[0]; c->znorm_prev = s->scal[1]; c->outer_k = (int64_t)s->scal[2];
     c->inner_total = (int64_t)s->scal[3]; c->inner_since = (int64_t)s->scal[4];
+    /* the residual history belongs to the replaced trajectory */
+    for (int k = 0; k < 256; k++) c->phist[k] = NAN;
+    c->rep.diverged_iter = 0;
 }
 
 void orc_get_slacks(const orc_ctx *c, double *sl) {

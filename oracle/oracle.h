@@ -52,6 +52,10 @@ typedef struct {
                            six-variable AL (no fast path), 2 = wbar clipped to [Vmin^2, Vmax^2] */
     int32_t plain;      /* 1: the branch solver without the accelerations R41-R44, R48, R49 (the plain
                            first-order AL that pins the accelerated one; oracle only) */
+    int32_t diverge_window;   /* SPEC S:431 divergence detector: > 0 = an iterate call stops when the
+                                 primal residual exceeds diverge_factor x its value diverge_window
+                                 iterations earlier (first time only); 0 = off */
+    double diverge_factor;
 } orc_params;
 
 typedef struct {
@@ -62,6 +66,7 @@ typedef struct {
      * 4-variable fast path and of the 6-variable AL */
     double flops_fast, flops_al;
     int64_t newton_fast, newton_al;
+    int32_t diverged_iter, pad_;   /* first iteration the divergence detector fired (0 = never) */
 } orc_report;
 
 /* Canonical state (section 4 of DESIGN.md).  Row kinds:

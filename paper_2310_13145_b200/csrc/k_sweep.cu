@@ -1135,6 +1135,25 @@ __device__ void finalize_status(const Dev &d, const double *rec) {
             st->inner_since = 0;
         }
     }
+    // the iteration's record (ucac_history) and the divergence detector: primal_inf >
+    // factor x its value div_window iterations earlier ends the call (done), once per run
+    {
+        const long long it = st->inner_total;
+        double *hr = d.hist + (size_t)((it - 1) % HIST_CAP) * HIST_FIELDS;
+        hr[0] = st->primal_inf;
+        hr[1] = st->dual_inf;
+        hr[2] = st->z_inf;
+        hr[3] = st->z_2;
+        hr[4] = st->objective;
+        hr[5] = st->beta;
+        if (d.div_window > 0 && it > d.div_window && st->diverged_iter == 0) {
+            const double old = d.hist[(size_t)((it - 1 - d.div_window) % HIST_CAP) * HIST_FIELDS];
+            if (st->primal_inf > d.div_factor * old) {   // (false against a NaN: an emptied history)
+                st->diverged_iter = (int)it;
+                st->done = 1;
+            }
+        }
+    }
     if (st->stop_on_primal && st->primal_inf <= st->primal_target) st->done = 1;
 }
 

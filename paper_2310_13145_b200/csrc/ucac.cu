@@ -22,6 +22,20 @@
 
 #include "ucac.h"
 
+// NVTX ranges (tracing): one per public call, one per ucac_create phase and one per eager
+// kernel of ucac_iterate_timed, named as the call / phase / kernel.  Header-only NVTX v3: without a
+// profiler attached each push/pop is a test of a null callback.
+#include <nvtx3/nvToolsExt.h>
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace
+#define UCAC_NVTX(name) NvtxRange nvtx_range_(name)
+
 // graph shape: the generator chain forks at the start of the iteration, on a
 // higher-priority stream
 #ifndef UCAC_EARLY_FORK
@@ -46,6 +60,7 @@
 #define UCAC_S2_PRIO 1
 #endif
 #include "ucac_dev.cuh"
+static_assert(UCAC_HIST_CAP == ucac::HIST_CAP && UCAC_HIST_FIELDS == ucac::HIST_FIELDS, "ucac_history layout");
 #include "ucac_part.h"
 
 namespace ucac {
@@ -243,6 +258,7 @@ struct ucac_ctx {
     ncclComm_t comm2 = nullptr;          // bus cut: the early exchanges' communicator (stream s3)
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
     bool own_stream = false;
+    long long hist_base = 0;             // inner_total when the record history was last emptied
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_genx = nullptr, ev_early = nullptr, ev_branch = nullptr,
                 ev_tail = nullptr, ev_bus = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -424,6 +440,8 @@ static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, con
         for (size_t k = 0; k < (size_t)G * T; k++)
             if (uc->u_init[k] != 0 && uc->u_init[k] != 1) BAD("u_init must be 0/1");
     if (p->tron_maxit < 1 || p->al_maxit < 1 || p->inner_min < 0 || p->inner_cap < 1) BAD("bad iteration caps");
+    if (p->diverge_window < 0 || p->diverge_window >= HIST_CAP || (p->diverge_window > 0 && !std::isfinite(p->diverge_factor)))
+        BAD("diverge_window must be in [0, %d) with a finite diverge_factor", HIST_CAP);
     return UCAC_OK;
 #undef BAD
 }
@@ -446,12 +464,14 @@ extern "C" ucac_status ucac_nccl_unique_id(unsigned char *id) {
 extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co,
                                    const ucac_uc *uc, const ucac_params *prm, const ucac_dist *dist,
                                    void *cuda_stream, ucac_ctx **out) {
+    UCAC_NVTX("ucac_create");
     if (!out) return fail(nullptr, UCAC_EINVAL, "out is NULL");
     *out = nullptr;
     // UCAC_CREATE_TRACE=1: phase times of ucac_create on stderr (diagnostics)
     static const bool trace = getenv("UCAC_CREATE_TRACE") != nullptr;
     auto tp0 = std::chrono::steady_clock::now(), tpl = tp0;
     auto mark = [&](const char *what) {
+        nvtxMarkA(what);   // (phase boundaries on the NVTX timeline)
         if (!trace) return;
         auto now = std::chrono::steady_clock::now();
         fprintf(stderr, "ucac_create %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tpl).count());
@@ -599,6 +619,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.al_eta_star = prm->al_eta_star; d.al_sigma0_rel = prm->al_sigma0_rel;
     d.al_sigma_max_rel = prm->al_sigma_max_rel; d.al_sigma_decay = prm->al_sigma_decay;
     d.uc_fixed = prm->uc_fixed;
+    d.div_window = prm->diverge_window;
+    d.div_factor = prm->diverge_factor;
     d.fuse_rows = (nranks == 1 && UCAC_FUSE_ROWS) ? 1 : 0;
     d.variant = prm->variant;
     d.strict = prm->strict_fp != 0;
@@ -713,6 +735,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.u_next = A.take<int8_t>(GT);
         d.unext_ok = A.take<unsigned>(1);
         d.rec = A.take<double>(NREC);
+        d.hist = A.take<double>((size_t)HIST_CAP * HIST_FIELDS);
         d.tl = A.take<unsigned long long>(2 * NKERN);
         // bus cut: early exchanges carry a late flag (5 and 7 values), late ones the plain values (4, 6)
         d.xsend1 = A.take<double>((size_t)P.max_cut * 5 * T);
@@ -795,6 +818,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         return bail(fail(ctx, UCAC_ECUDA, "status upload"));
     if (gen_set_smem_attr(P.Tg) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "T=%d needs %zu B of shared memory", P.Tg, gen_smem_bytes(P.Tg)));
     mark("arena");
+    // an empty record history: all-ones bytes are NaN doubles, which the detector's test rejects
+    if (cudaMemsetAsync(d.hist, 0xFF, (size_t)HIST_CAP * HIST_FIELDS * sizeof(double), ctx->s) != cudaSuccess)
+        return bail(fail(ctx, UCAC_ECUDA, "history"));
     launch_init(d, uinit, ctx->s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init kernel: %s", cudaGetErrorString(e)));
@@ -1096,7 +1122,8 @@ static ucac_status build_graphs(ucac_ctx *ctx) {
 static ucac_status set_control(ucac_ctx *ctx, int stop, double target) {
     // write stop_on_primal, primal_target and clear done (three fields of the device status);
     // nothing to do when the last call ran without stop_on_primal and this one does too
-    if (!stop && !ctx->ctl_dirty) return UCAC_OK;
+    // (with the divergence detector on, every call starts with done cleared: a call it ended is over)
+    if (!stop && !ctx->ctl_dirty && ctx->prm.diverge_window == 0) return UCAC_OK;
     ctx->ctl_dirty = stop != 0;
     DevStatus *h = ctx->st_host;
     h->stop_on_primal = stop;
@@ -1117,6 +1144,7 @@ static ucac_status pull_status(ucac_ctx *ctx) {
 
 extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_primal, double primal_target,
                                     int32_t *n_done) {
+    UCAC_NVTX("ucac_iterate");
     if (!ctx) return UCAC_EINVAL;
     if (n < 0) return fail(ctx, UCAC_EINVAL, "n < 0");
     if (ctx->nranks > 1 && ctx->comm_mode == 1)
@@ -1144,6 +1172,7 @@ extern "C" ucac_status ucac_iterate(ucac_ctx *ctx, int32_t n, int32_t stop_on_pr
 }
 
 extern "C" ucac_status ucac_set_rho(ucac_ctx *ctx, double rho_pq, double rho_va, double rho_uc) {
+    UCAC_NVTX("ucac_set_rho");
     if (!ctx) return UCAC_EINVAL;
     if (!(rho_pq > 0.0 && rho_va > 0.0 && rho_uc > 0.0) || !std::isfinite(rho_pq) || !std::isfinite(rho_va) ||
         !std::isfinite(rho_uc))
@@ -1174,6 +1203,7 @@ extern "C" ucac_status ucac_set_rho(ucac_ctx *ctx, double rho_pq, double rho_va,
 // step through the same phases as the NCCL graph; the exchanges are device-to-device copies
 // driven from the host between phases (no kernel ever waits on another context).
 extern "C" ucac_status ucac_iterate_group(ucac_ctx **ctxs, int32_t n, int32_t iters) {
+    UCAC_NVTX("ucac_iterate_group");
     if (!ctxs || n < 1 || iters < 0) return UCAC_EINVAL;
     for (int r = 0; r < n; r++)
         if (!ctxs[r] || ctxs[r]->nranks != n || ctxs[r]->rank != r || (n > 1 && ctxs[r]->comm_mode != 1))
@@ -1321,6 +1351,7 @@ static const char *kNames[NKERN] = {"k_branch", "k_gen", "k_bus", "k_ubar", "k_b
 extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN) ? kNames[k] : "?"; }
 
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
+    UCAC_NVTX("ucac_iterate_timed");
     if (!ctx || n < 0) return UCAC_EINVAL;
     if (ctx->nranks > 1) return fail(ctx, UCAC_EUNSUPPORTED, "timed iterations are single-GPU");
     ucac_status s = set_control(ctx, 0, 0.0);
@@ -1338,7 +1369,10 @@ extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kern
             const int k = kOrder[j];   // the graph's dependency order; events indexed by kernel id
             cudaEvent_t a = ctx->tev[((size_t)it * NKERN + k) * 2], b = ctx->tev[((size_t)it * NKERN + k) * 2 + 1];
             CK(cudaEventRecord(a, ctx->s));
-            launch_kernel(ctx, k, ctx->s);
+            {
+                UCAC_NVTX(kNames[k]);
+                launch_kernel(ctx, k, ctx->s);
+            }
             CK(cudaEventRecord(b, ctx->s));
         }
     }
@@ -1368,6 +1402,7 @@ static int32_t err_global_comp(const ucac_ctx *ctx, int err_kernel, int comp) {
 }
 
 extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
+    UCAC_NVTX("ucac_residuals");
     if (!ctx || !r) return UCAC_EINVAL;
     ucac_status s = pull_status(ctx);
     if (s != UCAC_OK) return s;
@@ -1393,7 +1428,29 @@ extern "C" ucac_status ucac_residuals(ucac_ctx *ctx, ucac_report *r) {
     r->err_iter = h->err_iter;
     r->err_comp = err_global_comp(ctx, h->err_kernel, h->err_comp);
     r->err_period = h->err_kernel ? h->err_period : -1;
+    r->diverged_iter = h->diverged_iter;
+    r->hist_len = (int32_t)std::max(0LL, std::min<long long>(h->inner_total - ctx->hist_base, HIST_CAP));
     if (h->err_kernel) return fail(ctx, UCAC_ENUMERIC, "non-finite iterate at iteration %d", h->err_iter);
+    return UCAC_OK;
+}
+
+extern "C" ucac_status ucac_history(ucac_ctx *ctx, double *out, int32_t n, int32_t *got) {
+    UCAC_NVTX("ucac_history");
+    if (!ctx || n < 0 || (n > 0 && !out)) return UCAC_EINVAL;
+    ucac_status s = pull_status(ctx);
+    if (s != UCAC_OK) return s;
+    const long long it = ctx->st_host->inner_total;
+    const int have = (int)std::max(0LL, std::min<long long>(it - ctx->hist_base, HIST_CAP));
+    const int m = std::min<int>(n, have);
+    std::vector<double> all((size_t)HIST_CAP * HIST_FIELDS);
+    CK(cudaMemcpyAsync(all.data(), ctx->d.hist, all.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    for (int j = 0; j < m; j++) {   // iterations it - m + 1 ... it, oldest first
+        const long long iter = it - m + 1 + j;
+        memcpy(out + (size_t)j * HIST_FIELDS, all.data() + (size_t)((iter - 1) % HIST_CAP) * HIST_FIELDS,
+               HIST_FIELDS * sizeof(double));
+    }
+    if (got) *got = m;
     return UCAC_OK;
 }
 
@@ -1430,6 +1487,7 @@ static ucac_status aos_to_soa(ucac_ctx *ctx, double *dev, const double *host, si
 
 // State of the (rank-local) problem: generators, local branches and OWNED buses.
 extern "C" ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st) {
+    UCAC_NVTX("ucac_get_state");
     if (!ctx || !st) return UCAC_EINVAL;
     launch_apply_outer(ctx->d, ctx->s);
     CK(cudaGetLastError());
@@ -1469,6 +1527,7 @@ extern "C" ucac_status ucac_get_state(ucac_ctx *ctx, ucac_state *st) {
 }
 
 extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
+    UCAC_NVTX("ucac_set_state");
     if (!ctx || !st) return UCAC_EINVAL;
     if (ctx->nranks > 1) return fail(ctx, UCAC_EUNSUPPORTED, "set_state is single-GPU (ghost buses would be stale)");
     const Dev &d = ctx->d;
@@ -1510,7 +1569,11 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
     h->err_iter = 0;
     h->err_comp = -1;
     h->err_period = -1;
+    h->diverged_iter = 0;
     CK(cudaMemcpyAsync(d.st, h, sizeof(DevStatus), cudaMemcpyHostToDevice, ctx->s));
+    // the record history belongs to the replaced trajectory
+    CK(cudaMemsetAsync(d.hist, 0xFF, (size_t)HIST_CAP * HIST_FIELDS * sizeof(double), ctx->s));
+    ctx->hist_base = h->inner_total;
     CK(cudaMemsetAsync(d.cnt, 0, NCNT * sizeof(unsigned long long), ctx->s));
     CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));   // the pipelined DP result is stale
     CK(cudaMemsetAsync(d.alq_cnt, 0, (UCAC_AL_BUCKETS + 1) * sizeof(unsigned), ctx->s));
@@ -1520,6 +1583,7 @@ extern "C" ucac_status ucac_set_state(ucac_ctx *ctx, const ucac_state *st) {
 }
 
 extern "C" ucac_status ucac_get_solution(ucac_ctx *ctx, ucac_solution *sol) {
+    UCAC_NVTX("ucac_get_solution");
     if (!ctx || !sol) return UCAC_EINVAL;
     const Dev &d = ctx->d;
     const size_t GT = (size_t)ctx->G * ctx->T, LT = (size_t)ctx->L * ctx->T, BT = (size_t)ctx->B * ctx->T;
@@ -1543,6 +1607,7 @@ extern "C" ucac_status ucac_get_solution(ucac_ctx *ctx, ucac_solution *sol) {
 extern "C" ucac_status ucac_uc_warm_start(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *cost,
                                           const ucac_uc *uc, const ucac_params *prm, int32_t iters,
                                           double threshold, int8_t *u_out) {
+    UCAC_NVTX("ucac_uc_warm_start");
     if (!net || !hz || !cost || !uc || !prm || !u_out || iters < 0) {
         g_create_err = "ucac_uc_warm_start: bad arguments";
         return UCAC_EINVAL;
@@ -1607,6 +1672,7 @@ extern "C" ucac_status ucac_local_map(ucac_ctx *ctx, int32_t which, int32_t *ids
 extern "C" ucac_status ucac_dp_batch(int32_t ngen, int32_t T, const double *L, const int32_t *min_up,
                                      const int32_t *min_dn, const int32_t *u0, const int32_t *hold, int8_t *sched,
                                      double *cost, int32_t on_device, void *cuda_stream) {
+    UCAC_NVTX("ucac_dp_batch");
     if (ngen <= 0 || T <= 0 || !L || !min_up || !min_dn || !u0 || !hold || !sched || !cost) {
         g_create_err = "ucac_dp_batch: bad arguments";
         return UCAC_EINVAL;
@@ -1798,6 +1864,7 @@ static void set_peer(Dev &d, int q, char *xb, const size_t *off) {
 }
 
 extern "C" ucac_status ucac_p2p_group(ucac_ctx **ctxs, int32_t n) {
+    UCAC_NVTX("ucac_p2p_group");
     if (!ctxs || n < 2 || n > UCAC_MAX_P2P) return UCAC_EINVAL;
     for (int r = 0; r < n; r++)
         if (!ctxs[r] || !ctxs[r]->d.tcut || ctxs[r]->comm_mode != 1 || ctxs[r]->rank != r || ctxs[r]->nranks != n)
@@ -1825,6 +1892,7 @@ extern "C" ucac_status ucac_p2p_export(ucac_ctx *ctx, unsigned char *blob) {
 }
 
 extern "C" ucac_status ucac_p2p_import(ucac_ctx *ctx, const unsigned char *blobs) {
+    UCAC_NVTX("ucac_p2p_import");
     if (!ctx || !blobs) return UCAC_EINVAL;
     if (!ctx->d.tcut || ctx->comm_mode != 0 || ctx->nranks > UCAC_MAX_P2P)
         return fail(ctx, UCAC_EUNSUPPORTED, "p2p: an NCCL time-cut context of at most %d ranks", UCAC_MAX_P2P);

@@ -51,11 +51,14 @@ struct DevStatus {
     int stop_on_primal;
     int err_kernel, err_iter;         // first non-finite value: kernel id + 1, iteration (1-based)
     int err_comp, err_period;         // ... its component (rank-local index) and period
-    int pad_;
+    int diverged_iter;                // divergence detector: first iteration it fired
     double primal_target;
     double primal_inf, rz_inf, rz_2, z_inf, z_2, dual_inf, objective;
     unsigned long long tron_iters, tron_capped, al_active, al_capped, al_tron_iters;
 };
+
+// per-iteration records (ucac_history): primal_inf, dual_inf, z_inf, z_2, objective, beta
+constexpr int HIST_CAP = 256, HIST_FIELDS = 6;
 
 struct Dev {
     int G, L, B, T;
@@ -70,6 +73,9 @@ struct Dev {
     int tron_maxit, al_maxit;
     double al_eta_star, al_sigma0_rel, al_sigma_max_rel, al_sigma_decay;
     int uc_fixed;                     // 1: k_gen keeps u (NEXT-2)
+    int div_window;                   // divergence detector (0 = off)
+    double div_factor;
+    double *hist;                     // [HIST_CAP][HIST_FIELDS], slot (iteration - 1) % HIST_CAP
     int variant;                      // NEXT-3 bitmask: 1 = AL for every rated branch, 2 = wbar clip
     int strict;                       // strict_fp parity mode: oracle quotients / operation order (k_strict.cu)
     // ---- periods (NEXT-4(c) time cut): local period t is global period t + t_off of Tg; the kernels

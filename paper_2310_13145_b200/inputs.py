@@ -188,6 +188,8 @@ class Params:
     uc_fixed: int = 0          # 1: step (7a) keeps u (NEXT-2 warm start's multiperiod ACOPF)
     variant: int = 0           # NEXT-3 bitmask: 1 = AL for every rated branch (no fast path), 2 = wbar clip
     strict_fp: int = 0         # 1: strict parity mode (oracle operation order / quotients, R54 sin/cos)
+    diverge_window: int = 0    # SPEC S:431 divergence detector (0 = off, < 256): an iterate call stops when
+    diverge_factor: float = 10.0   # primal > factor x its value `window` iterations earlier (SPEC: 200, 10)
 
 
 # --------------------------------------------------------------------------------------

@@ -60,7 +60,7 @@ class Params(C.Structure):
                 ("tron_gtol_rel", C.c_double), ("tron_maxit", C.c_int32), ("al_maxit", C.c_int32),
                 ("al_eta_star", C.c_double), ("al_sigma0_rel", C.c_double), ("al_sigma_max_rel", C.c_double),
                 ("al_sigma_decay", C.c_double), ("uc_fixed", C.c_int32), ("variant", C.c_int32),
-                ("strict_fp", C.c_int32)]
+                ("strict_fp", C.c_int32), ("diverge_window", C.c_int32), ("diverge_factor", C.c_double)]
 
 
 class Dist(C.Structure):
@@ -78,7 +78,8 @@ class Report(C.Structure):
                 ("al_tron_iters", C.c_int64),
                 ("inner_since_outer", C.c_int32), ("outer_k", C.c_int32),
                 ("err_kernel", C.c_int32), ("err_iter", C.c_int32),
-                ("err_comp", C.c_int32), ("err_period", C.c_int32)]
+                ("err_comp", C.c_int32), ("err_period", C.c_int32),
+                ("diverged_iter", C.c_int32), ("hist_len", C.c_int32)]
 
 
 class Solution(C.Structure):
@@ -141,6 +142,8 @@ def _declare(L):
     L.ucac_kernel_name.restype = C.c_char_p
     L.ucac_residuals.argtypes = [C.c_void_p, C.POINTER(Report)]
     L.ucac_residuals.restype = C.c_int
+    L.ucac_history.argtypes = [C.c_void_p, dp, C.c_int32, C.POINTER(C.c_int32)]
+    L.ucac_history.restype = C.c_int
     L.ucac_get_solution.argtypes = [C.c_void_p, C.POINTER(Solution)]
     L.ucac_get_solution.restype = C.c_int
     L.ucac_get_state.argtypes = [C.c_void_p, C.POINTER(State)]
@@ -189,7 +192,7 @@ EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
             "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start",
             "ucac_debug_poison", "ucac_measure_fp64_peak", "ucac_time_split", "ucac_comm_info",
-            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import"]
+            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import", "ucac_history"]
 
 
 def _check(rc, h=None):
@@ -202,7 +205,7 @@ def params_struct(pr) -> Params:
     return Params(pr.rho_pq, pr.rho_va, pr.rho_uc, pr.beta0, pr.tau, pr.theta, pr.lambda_max, pr.beta_max,
                   pr.eps_inner_abs, pr.inner_min, pr.inner_cap, pr.outer_enabled, pr.tron_gtol_rel,
                   pr.tron_maxit, pr.al_maxit, pr.al_eta_star, pr.al_sigma0_rel, pr.al_sigma_max_rel,
-                  pr.al_sigma_decay, pr.uc_fixed, pr.variant, pr.strict_fp)
+                  pr.al_sigma_decay, pr.uc_fixed, pr.variant, pr.strict_fp, pr.diverge_window, pr.diverge_factor)
 
 
 def problem_structs(pb, keep: list):
@@ -350,6 +353,16 @@ class Context:
         cnt = np.zeros(NKERNELS, dtype=np.int64)
         _check(self.L.ucac_iterate_timed(self.h, n, ms.ctypes.data_as(dp), cnt.ctypes.data_as(i64p)), self.h)
         return dict(zip(KERNELS, ms)), dict(zip(KERNELS, cnt))
+
+    HIST_FIELDS = ("primal_inf", "dual_inf", "z_inf", "z_2", "objective", "beta")
+
+    def history(self, n: int = 256) -> np.ndarray:
+        """the last min(n, 256) iterations' records (ucac_history), oldest first: a structured
+        array with the fields HIST_FIELDS"""
+        buf = np.zeros((max(0, int(n)), len(self.HIST_FIELDS)))
+        got = C.c_int32(0)
+        _check(self.L.ucac_history(self.h, buf.ctypes.data_as(dp), int(n), C.byref(got)), self.h)
+        return np.rec.fromarrays(buf[:got.value].T.copy(), names=list(self.HIST_FIELDS))
 
     def report(self) -> dict:
         r = Report()

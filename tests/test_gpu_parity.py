@@ -438,3 +438,44 @@ def test_time_to_residual_configs123_stop_iteration_matches_oracle(name):
     ro = o.report()
     assert ro["primal_inf"] <= target and ro["outer_total"] == rg["outer_total"]
     assert rg["objective"] == pytest.approx(ro["objective"], rel=1e-6)
+
+
+def test_divergence_detector_and_history():
+    """SPEC S:431's divergence detector (ucac_params.diverge_window/factor) stops the call
+    at the oracle's iteration (exact rules: factor 0 fires at window + 1, a huge factor never; a real
+    factor at the first i with p_i > factor p_(i-w) of the GPU's own history), the next call goes on;
+    ucac_history holds the per-iteration reports."""
+    import dataclasses
+    pb, pr = inputs.build_config("case9")
+    for w, factor in ((5, 0.0), (7, 1e300)):
+        prd = dataclasses.replace(pr, diverge_window=w, diverge_factor=factor)
+        g, o = ucac.Context(pb, prd), oracle.Oracle(pb, prd)
+        n = g.iterate(60, stop_on_primal=0.0)
+        o.iterate(60)
+        rg, ro = g.report(), o.report()
+        assert rg["diverged_iter"] == ro["diverged_iter"] == (w + 1 if factor == 0.0 else 0)
+        assert n == rg["inner_total"] == ro["inner_total"]
+        g.iterate(4)
+        assert g.report()["inner_total"] == n + 4 and g.report()["diverged_iter"] == rg["diverged_iter"]
+    for w, factor in ((3, 1.0), (20, 0.5)):
+        g = ucac.Context(pb, dataclasses.replace(pr, diverge_window=w, diverge_factor=factor))
+        n = g.iterate(200, stop_on_primal=0.0)
+        h = g.history(256)
+        p = h.primal_inf
+        first = next(i for i in range(w + 1, len(p) + 1) if p[i - 1] > factor * p[i - 1 - w])
+        assert g.report()["diverged_iter"] == first == n
+    # the history is the per-iteration report
+    g = ucac.Context(pb, pr)
+    reps = []
+    for _ in range(12):
+        g.iterate(1)
+        reps.append(g.report())
+    h = g.history(10)
+    assert len(h) == 10 and g.report()["hist_len"] == 12
+    for j, r in enumerate(reps[2:]):
+        for f in ucac.Context.HIST_FIELDS:
+            assert h[f][j] == r[f], (j, f)
+    g.set_state(g.get_state())
+    assert len(g.history(10)) == 0 and g.report()["hist_len"] == 0
+    with pytest.raises(ucac.UcacError):
+        ucac.Context(pb, dataclasses.replace(pr, diverge_window=256))
