@@ -134,8 +134,41 @@ def grid2(out, max_iters="20000", cases="case30,case118,case300"):
                                                                "final_primal", "to", "u_flips_last")}), flush=True)
 
 
+def grid3(out, max_iters="20000", cases="case30,case118,case300"):
+    """third pass: the schedule held at all-on (uc_fixed: the continuous multiperiod ACOPF of the
+    NEXT-2 warm start), minimum output x {1, 0}, beta capped at rho_min x {0.05, 0.5, inf}"""
+    f = open(out, "a")
+    for name in cases.split(","):
+        pb0, pr0 = inputs.build_config(name)
+        G = pb0.ngen
+        for rho_name, rho in (("bench", (pr0.rho_pq, pr0.rho_va, pr0.rho_uc)), ("table1", TABLE1_RHO[name])):
+            if rho_name == "table1" and tuple(rho) == (pr0.rho_pq, pr0.rho_va, pr0.rho_uc):
+                continue
+            for pscale in (1.0, 0.0):
+                lowmin = pb0.pmin * pscale
+                pb = dataclasses.replace(pb0, pmin=lowmin, u_init=np.ones((G, pb0.T), np.int8),
+                                         su_ramp=np.maximum(np.maximum(lowmin, pb0.ramp_up), pb0.p0),
+                                         sd_ramp=np.maximum(np.maximum(lowmin, pb0.ramp_up), pb0.p0))
+                for bfac in (0.05, 0.5, None):
+                    bmax = 1e12 if bfac is None else bfac * min(rho)
+                    pr = dataclasses.replace(pr0, rho_pq=rho[0], rho_va=rho[1], rho_uc=rho[2], beta_max=bmax,
+                                             beta0=min(pr0.beta0, bmax), uc_fixed=1)
+                    row = {"config": name, "rho": rho_name, "variant": "uc_fixed(all on)", "pmin_scale": pscale,
+                           "beta_max": bmax}
+                    try:
+                        row.update(run(pb.normalized(), pr, int(max_iters)))
+                    except Exception as e:
+                        row["error"] = str(e)
+                    f.write(json.dumps(row) + "\n")
+                    f.flush()
+                    print(json.dumps({k: row.get(k) for k in ("config", "rho", "pmin_scale", "beta_max", "best_primal",
+                                                               "final_primal", "to", "iterations")}), flush=True)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "grid2":
         grid2(*sys.argv[2:])
+    elif len(sys.argv) > 1 and sys.argv[1] == "grid3":
+        grid3(*sys.argv[2:])
     else:
         main(*sys.argv[1:])
