@@ -175,6 +175,10 @@ ucac_status ucac_time_split(int32_t T, int32_t nranks, int32_t rank, int32_t *ou
 /* The context's communicator: ncclCommCount / ncclCommUserRank for an NCCL context (comm_mode 0),
  * else the ucac_dist ranks (1 / 0 for a single-GPU context). */
 ucac_status ucac_comm_info(ucac_ctx *ctx, int32_t *nranks, int32_t *rank);
+/* 1 if the context iterates through an NCCL communicator (comm_mode 0 with several ranks, or one
+ * rank under UCAC_NCCL_ONE_RANK=1 -- the multi-rank graph and its captured collectives on a one-GPU
+ * box, for tests), else 0; -1 for a NULL context. */
+int32_t ucac_comm_nccl(const ucac_ctx *ctx);
 
 /* Device-initiated exchange of the time cut (NEXT-4(c)): the three exchanges of
  * each iteration (stage costs to every rank, the boundary values to the neighbours) become stores

@@ -257,7 +257,7 @@ __device__ void final_fold(const Dev &d) {
         rec[R_BAD] = fin[P_BAD];
         for (int q = 0; q < NCNT; q++) d.cnt[q] = 0;
         for (int q = 0; q <= UCAC_AL_BUCKETS; q++) d.alq_cnt[q] = 0;
-        if (d.nranks > 1) {
+        if (d.xrank_rec) {
             for (int q = 0; q < NREC; q++) d.rec[q] = rec[q];   // cross-rank all-reduce, then k_finalize
         } else {
             finalize_status(d, rec);

@@ -254,6 +254,7 @@ struct ucac_ctx {
     Local P;
     int G = 0, L = 0, B = 0, T = 0;      // local counts (B = owned buses)
     int nranks = 1, rank = 0, comm_mode = 0;
+    bool multi = false;                  // the multi-rank iteration graph (nranks > 1, or UCAC_NCCL_ONE_RANK)
     ncclComm_t comm = nullptr;
     ncclComm_t comm2 = nullptr;          // bus cut: the early exchanges' communicator (stream s3)
     cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
@@ -497,6 +498,11 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
 
     // (a one-rank time cut is allowed: it runs the time-cut graph with local exchanges, for tests)
     const int tcut = dist ? (dist->cut != 0) : 0;
+    // UCAC_NCCL_ONE_RANK=1 (tests): a one-rank bus-cut dist with comm_mode 0 still builds an NCCL
+    // communicator (of one rank) and runs the multi-rank iteration graph with its captured
+    // collectives, so that the NCCL path executes on a one-GPU box
+    const char *one_env = getenv("UCAC_NCCL_ONE_RANK");
+    const bool nccl1 = dist && nranks == 1 && dist->comm_mode == 0 && one_env && atoi(one_env) == 1;
     if (dist && dist->cut != 0 && dist->cut != 1) return fail(nullptr, UCAC_EINVAL, "cut must be 0 or 1");
     if (tcut && nranks > hz->T) return fail(nullptr, UCAC_EINVAL, "time cut: T=%d < nranks=%d", hz->T, nranks);
     if (tcut && (prm->variant & (4 | 16)))
@@ -528,6 +534,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     ctx->nranks = nranks;
     ctx->rank = rank;
     ctx->comm_mode = dist && nranks > 1 ? dist->comm_mode : 0;
+    ctx->multi = nranks > 1 || nccl1;
     mark("device/part");
     if (tcut) {
         std::vector<int32_t> one(net->nbus, 0);
@@ -578,7 +585,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     if ((ctx->st_host = pinned_status_get()) == nullptr) return bail(fail(ctx, UCAC_ENOMEM, "pinned status"));
     mark("pinned");
     memset(ctx->st_host, 0, sizeof(DevStatus));
-    if (nranks > 1 && ctx->comm_mode == 0) {
+    if ((nranks > 1 && ctx->comm_mode == 0) || nccl1) {
         ncclUniqueId id;
         memcpy(&id, dist->nccl_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
@@ -594,6 +601,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.B_own = P.Bo;
     d.Lph = P.Lp;
     d.nranks = nranks;
+    d.xrank_rec = (nranks > 1 || ctx->multi) ? 1 : 0;
     d.ncut = (int)P.cut_local.size();
     d.nexport = (int)P.export_local.size();
     d.nphantom_src = (int)P.phantom_src.size();
@@ -621,7 +629,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     d.uc_fixed = prm->uc_fixed;
     d.div_window = prm->diverge_window;
     d.div_factor = prm->diverge_factor;
-    d.fuse_rows = (nranks == 1 && UCAC_FUSE_ROWS) ? 1 : 0;
+    d.fuse_rows = (nranks == 1 && !nccl1 && UCAC_FUSE_ROWS) ? 1 : 0;
     d.variant = prm->variant;
     d.strict = prm->strict_fp != 0;
     d.nblk_bus = nblk_bus(P.Bo, T);
@@ -894,7 +902,7 @@ static void launch_kernel(ucac_ctx *ctx, int k, cudaStream_t s) {
 // One rank (tests): the stage costs are copied locally and the neighbour exchanges vanish.
 static void enqueue_iteration_tc(ucac_ctx *ctx) {
     const Dev &d = ctx->d;
-    const bool multi = ctx->nranks > 1;
+    const bool multi = ctx->multi;
     cudaStream_t s = ctx->s, s2 = ctx->s2, s3 = ctx->s3;
     cudaEventRecord(ctx->ev_fork, s);
     cudaStreamWaitEvent(s2, ctx->ev_fork, 0);
@@ -1013,7 +1021,7 @@ static void enqueue_iteration(ucac_ctx *ctx) {
         enqueue_iteration_tc(ctx);
         return;
     }
-    if (ctx->nranks > 1) {
+    if (ctx->multi) {
         enqueue_iteration_bus_multi(ctx);
         return;
     }
@@ -1353,7 +1361,7 @@ extern "C" const char *ucac_kernel_name(int32_t k) { return (k >= 0 && k < NKERN
 extern "C" ucac_status ucac_iterate_timed(ucac_ctx *ctx, int32_t n, double *kernel_ms, int64_t *launches) {
     UCAC_NVTX("ucac_iterate_timed");
     if (!ctx || n < 0) return UCAC_EINVAL;
-    if (ctx->nranks > 1) return fail(ctx, UCAC_EUNSUPPORTED, "timed iterations are single-GPU");
+    if (ctx->multi) return fail(ctx, UCAC_EUNSUPPORTED, "timed iterations are single-GPU");
     ucac_status s = set_control(ctx, 0, 0.0);
     if (s != UCAC_OK) return s;
     // eager iterations have no tail DP launch: every k_gen computes its own (7a)
@@ -1839,6 +1847,8 @@ extern "C" ucac_status ucac_time_split(int32_t T, int32_t nranks, int32_t rank, 
     out[3] = (g1 - g0) + hl + hh;     // local periods (halos included)
     return UCAC_OK;
 }
+
+extern "C" int32_t ucac_comm_nccl(const ucac_ctx *ctx) { return ctx ? (ctx->comm != nullptr ? 1 : 0) : -1; }
 
 extern "C" ucac_status ucac_comm_info(ucac_ctx *ctx, int32_t *nranks, int32_t *rank) {
     if (!ctx || !nranks || !rank) return UCAC_EINVAL;

@@ -129,6 +129,7 @@ struct Dev {
     int B_own;                        // owned buses [0, B_own); ghosts [B_own, B)
     int Lph;                          // phantom branches [L, L + Lph) (tauhat only)
     int ncut, nexport, nphantom_src, nghost, max_cut, max_export, nranks;
+    int xrank_rec;                    // 1: the final fold leaves the S8 record to a cross-rank all-reduce
     const int *cut_local, *export_local, *phantom_src, *ghost_src;
     double *xsend1, *xrecv1, *xsend2, *xrecv2;   // halo exchange buffers: early tauhat + late flag (5 per
                                                  // cut branch-period), early bus results + late flag (7)

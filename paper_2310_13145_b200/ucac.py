@@ -181,6 +181,8 @@ def _declare(L):
     L.ucac_p2p_import.restype = C.c_int
     L.ucac_comm_info.argtypes = [C.c_void_p, ip, ip]
     L.ucac_comm_info.restype = C.c_int
+    L.ucac_comm_nccl.argtypes = [C.c_void_p]
+    L.ucac_comm_nccl.restype = C.c_int32
     L.ucac_time_split.argtypes = [C.c_int32, C.c_int32, C.c_int32, ip]
     L.ucac_time_split.restype = C.c_int
     L.ucac_measure_fp64_peak.argtypes = [C.c_int32, dp, dp]
@@ -192,7 +194,7 @@ EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
             "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start",
             "ucac_debug_poison", "ucac_measure_fp64_peak", "ucac_time_split", "ucac_comm_info",
-            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import", "ucac_history"]
+            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import", "ucac_history", "ucac_comm_nccl"]
 
 
 def _check(rc, h=None):
@@ -334,7 +336,7 @@ class Context:
         """ucac_comm_info: the communicator's own rank count and rank (NCCL contexts)"""
         n, r = C.c_int32(), C.c_int32()
         _check(self.L.ucac_comm_info(self.h, C.byref(n), C.byref(r)), self.h)
-        return {"nranks": n.value, "rank": r.value}
+        return {"nranks": n.value, "rank": r.value, "nccl": self.L.ucac_comm_nccl(self.h) == 1}
 
     def poison(self, field: str, index: int):
         """fault injection (ucac_debug_poison): NaN into one element of zb / yb / zg / yg"""

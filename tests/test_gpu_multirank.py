@@ -111,3 +111,28 @@ def test_time_cut_graph_one_rank_bitwise_equals_single_gpu(name, iters):
     for k in ref:
         assert np.array_equal(got[k], ref[k]), (name, k)
     assert tc.report()["objective"] == one.report()["objective"]
+
+
+def test_nccl_one_rank_multirank_graph_bitwise_equals_single_gpu(monkeypatch):
+    """The NCCL transport on a one-GPU box ("the NCCL path has never executed"): under
+    UCAC_NCCL_ONE_RANK=1 a one-rank comm_mode-0 context builds a real NCCL communicator (and the
+    early exchanges' split one) and iterates through the multi-rank graph -- the S8 record leaves
+    the final fold for a captured ncclAllReduce and k_finalize applies S8/S9; with the time cut,
+    the captured all-gathers of the DP stage costs and the neighbour values run too.  Its iterate
+    and report equal the single-GPU graph's bit for bit."""
+    monkeypatch.setenv("UCAC_NCCL_ONE_RANK", "1")
+    for name, cut in (("case30", 0), ("pegase2869", 0), ("case118", 1)):
+        pb, pr = inputs.build_config(name)
+        ref = ucac.Context(pb, pr)
+        one = ucac.Context(pb, pr, dist={"rank": 0, "nranks": 1, "comm_mode": 0, "nccl_id": ucac.nccl_unique_id(),
+                                         "cut": cut})
+        info = one.comm_info()
+        assert info == {"nranks": 1, "rank": 0, "nccl": True} and not ref.comm_info()["nccl"]
+        for _ in range(3):
+            ref.iterate(7)
+            one.iterate(7)
+        a, b = ref.get_state(), one.get_state()
+        assert all(a[k].tobytes() == b[k].tobytes() for k in a), name
+        ra, rb = ref.report(), one.report()
+        for k in ("primal_inf", "objective", "inner_total", "outer_total", "tron_iters", "al_active"):
+            assert ra[k] == rb[k], (name, k)
