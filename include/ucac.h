@@ -331,6 +331,11 @@ ucac_status ucac_debug_poison(ucac_ctx *ctx, int32_t field, int64_t index);
  * thread, 8 x 256-thread blocks per SM, best of 5 timed launches of 64 x iters DFMA per thread).
  * *tflops = 2 flop x DFMA count / time; *ms (may be NULL) the best launch time. */
 ucac_status ucac_measure_fp64_peak(int32_t iters, double *tflops, double *ms);
+/* Dependent-chain latencies of the current device in SM cycles per link, one warp, clock64:
+ * cycles[0] DFMA, [1] DADD, [2] a double __shfl_xor_sync + add (one warp-reduction step), [3] the
+ * branch kernels' reciprocal (rcp.approx.f64 + two Newton steps), [4] IEEE sqrt.  Diagnostics
+ * (why one lane per small solve). */
+ucac_status ucac_measure_latencies(double *cycles);
 
 void *ucac_stream(ucac_ctx *ctx);                 /* the cudaStream_t the context runs on */
 const char *ucac_last_error(const ucac_ctx *ctx); /* NULL ctx: last create failure (thread-local) */

@@ -23,7 +23,77 @@ __global__ void __launch_bounds__(256) k_dfma_chain(int iters, double b, double 
     if (s == 123.456) sink[blockIdx.x] = s;   // never true; keeps the chains live
 }
 
+// Dependent-chain latencies (cycles per link), one warp, clock64 around each chain: the numbers
+// behind DESIGN.md 11's argument on splitting one small solve over several lanes.
+constexpr int LAT_N = 512;
+__global__ void k_latency(double b, double c, double *out) {
+    double a = threadIdx.x * 1e-12 + 1.0;
+    long long t0, t1;
+    const int lane = threadIdx.x & 31;
+    // [0] DFMA
+    t0 = clock64();
+#pragma unroll 16
+    for (int i = 0; i < LAT_N; i++) a = fma(a, b, c);
+    t1 = clock64();
+    const double r0 = (double)(t1 - t0) / LAT_N;
+    // [1] DADD
+    double s = a;
+    t0 = clock64();
+#pragma unroll 16
+    for (int i = 0; i < LAT_N; i++) s = s + c;
+    t1 = clock64();
+    const double r1 = (double)(t1 - t0) / LAT_N;
+    // [2] one butterfly step of a warp reduction on doubles: v += shfl_xor(v, 1)
+    double v = s;
+    t0 = clock64();
+#pragma unroll 16
+    for (int i = 0; i < LAT_N; i++) v = v + __shfl_xor_sync(0xffffffffu, v, 1);
+    t1 = clock64();
+    const double r2 = (double)(t1 - t0) / LAT_N;
+    // [3] the branch kernels' reciprocal (MUFU.RCP64H + two Newton steps)
+    double q = v * 1e-300 + 1.5;
+    t0 = clock64();
+#pragma unroll 4
+    for (int i = 0; i < LAT_N / 8; i++) {
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+        double e = fma(-q, r, 1.0);
+        r = fma(r, e, r);
+        e = fma(-q, r, 1.0);
+        q = fma(r, e, r) + 1.0;
+    }
+    t1 = clock64();
+    const double r3 = (double)(t1 - t0) / (LAT_N / 8);
+    // [4] IEEE sqrt
+    double w = q;
+    t0 = clock64();
+#pragma unroll 4
+    for (int i = 0; i < LAT_N / 8; i++) w = sqrt(w) + 1.0;
+    t1 = clock64();
+    const double r4 = (double)(t1 - t0) / (LAT_N / 8);
+    if (lane == 0) {
+        out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3; out[4] = r4;
+        out[5] = a + s + v + q + w;   // keeps every chain live
+    }
+}
+
 }  // namespace
+
+/* dependent-chain latencies in cycles: [0] DFMA, [1] DADD, [2] double shuffle + add (one
+ * warp-reduction step), [3] the reciprocal of k_branch.cu (rcp.approx + 2 Newton steps), [4] IEEE sqrt */
+extern "C" ucac_status ucac_measure_latencies(double *cycles5) {
+    if (!cycles5) return UCAC_EINVAL;
+    double *buf = nullptr;
+    if (cudaMalloc(&buf, 6 * sizeof(double)) != cudaSuccess) return UCAC_ENOMEM;
+    k_latency<<<1, 32>>>(0.999999, 1e-7, buf);   // warm-up
+    k_latency<<<1, 32>>>(0.999999, 1e-7, buf);
+    double h[6];
+    cudaError_t e = cudaMemcpy(h, buf, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return UCAC_ECUDA;
+    for (int k = 0; k < 5; k++) cycles5[k] = h[k];
+    return UCAC_OK;
+}
 
 extern "C" ucac_status ucac_measure_fp64_peak(int32_t iters, double *tflops, double *ms_out) {
     if (iters <= 0 || !tflops) return UCAC_EINVAL;

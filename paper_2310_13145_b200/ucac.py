@@ -183,6 +183,8 @@ def _declare(L):
     L.ucac_comm_info.restype = C.c_int
     L.ucac_comm_nccl.argtypes = [C.c_void_p]
     L.ucac_comm_nccl.restype = C.c_int32
+    L.ucac_measure_latencies.argtypes = [dp]
+    L.ucac_measure_latencies.restype = C.c_int
     L.ucac_time_split.argtypes = [C.c_int32, C.c_int32, C.c_int32, ip]
     L.ucac_time_split.restype = C.c_int
     L.ucac_measure_fp64_peak.argtypes = [C.c_int32, dp, dp]
@@ -194,7 +196,8 @@ EXPORTED = ["ucac_create", "ucac_iterate", "ucac_set_rho", "ucac_iterate_timed",
             "ucac_stream", "ucac_last_error", "ucac_destroy", "ucac_partition", "ucac_halo_lists",
             "ucac_nccl_unique_id", "ucac_iterate_group", "ucac_local_map", "ucac_uc_warm_start",
             "ucac_debug_poison", "ucac_measure_fp64_peak", "ucac_time_split", "ucac_comm_info",
-            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import", "ucac_history", "ucac_comm_nccl"]
+            "ucac_p2p_group", "ucac_p2p_export", "ucac_p2p_import", "ucac_history", "ucac_comm_nccl",
+            "ucac_measure_latencies"]
 
 
 def _check(rc, h=None):
@@ -428,6 +431,13 @@ def measure_fp64_peak(iters: int = 4096) -> dict:
     tf, ms = C.c_double(), C.c_double()
     _check(lib().ucac_measure_fp64_peak(int(iters), C.byref(tf), C.byref(ms)), None)
     return {"tflops": tf.value, "ms": ms.value, "iters": int(iters)}
+
+
+def measure_latencies() -> dict:
+    """ucac_measure_latencies: dependent-chain latencies (SM cycles per link) of the current device"""
+    out = np.zeros(5)
+    _check(lib().ucac_measure_latencies(out.ctypes.data_as(dp)), None)
+    return dict(zip(("dfma", "dadd", "shfl_add", "rcp", "sqrt"), (float(v) for v in out)))
 
 
 def dp_batch(L, min_up, min_dn, u0, hold):

@@ -198,3 +198,11 @@ def test_gen_smem_attribute_survives_smaller_T():
     c.set_rho(pr.rho_pq, pr.rho_va, pr.rho_uc)
     c.iterate(2)
     assert c.report()["inner_total"] == 4
+
+
+def test_measure_latencies_sane():
+    """ucac_measure_latencies (DESIGN.md 11's lane-split argument): positive cycle counts, a DFMA
+    link no shorter than the pipe's issue interval, a shuffle-and-add step longer than an add"""
+    lat = ucac.measure_latencies()
+    assert all(v > 0 for v in lat.values()), lat
+    assert lat["dfma"] >= 2 and lat["shfl_add"] > lat["dadd"], lat
