@@ -376,6 +376,10 @@ def main():
     ap.add_argument("--ttr-cap", type=int, default=20000,
                     help="iteration cap of the time-to-residual runs on configs[1]-[3]")
     ap.add_argument("--no-ttr-all", action="store_true", help="time-to-residual on configs[0] only")
+    ap.add_argument("--kernel-window", type=int, default=100,
+                    help="eager iterations (at least --steps) for the per-kernel figures and the roofline")
+    ap.add_argument("--kernel-window-start", type=int, default=106,
+                    help="first iteration of that window (the default 100-step run's: warm-up 5 + 100 timed + 1)")
     ap.add_argument("--p2p", action="store_true",
                     help="N > 1 with --cut time: device-initiated NVLink exchanges (CUDA IPC peer stores) instead of NCCL")
     ap.add_argument("--selfcheck-iters", type=int, default=10,
@@ -492,14 +496,26 @@ def main():
 
     # ---- per-kernel device times (same kernels launched eagerly with an event pair each), 1 GPU
     roofline, kernels, kms = None, None, None
+    kw = args.steps
     fused = False
     fp64_meas = None
     if world == 1:
-        kms, klaunch = ctx.iterate_timed(args.steps)
+        # a fixed window of >= 100 eager iterations right after the timed region, so that the
+        # per-kernel figures do not depend on --steps (the AL tail's length is set by its longest
+        # solve, its flops by the number of thermal-active lines, which grows over the first ~50)
+        kw = max(args.steps, args.kernel_window)
+        # ... starting at a fixed iteration (untimed graph iterations up to it when --steps is small),
+        # so that runs with different --steps report the same window
+        k0 = args.warmup + args.steps + 1
+        if k0 < args.kernel_window_start:
+            ctx.iterate(args.kernel_window_start - k0)
+            k0 = args.kernel_window_start
+        repk = ctx.report()
+        kms, klaunch = ctx.iterate_timed(kw)
         rep2 = ctx.report()
-        n_al = rep2["al_tron_iters"] - rep1["al_tron_iters"]
-        n_fast = rep2["tron_iters"] - rep1["tron_iters"] - n_al
-        al_solves = (rep2["al_active"] - rep1["al_active"]) / args.steps
+        n_al = rep2["al_tron_iters"] - repk["al_tron_iters"]
+        n_fast = rep2["tron_iters"] - repk["tron_iters"] - n_al
+        al_solves = (rep2["al_active"] - repk["al_active"]) / kw
         ksum = sum(kms.values())
         # the FP64 (non-tensor) peak measured in this process: DFMA chains, ucac_measure_fp64_peak
         with ClockSampler(local) as clk64:
@@ -535,22 +551,22 @@ def main():
                 ("k_branch_al", n_al, FLOPS_PER_NEWTON_AL,
                  alg["flops_per_al_solve"] * al_solves if alg else None)):
             sass = n * fpn / (kms[k] * 1e-3) / 1e12
-            a_ = alg_flops / (kms[k] / args.steps * 1e-3) / 1e12 if alg_flops is not None else sass
+            a_ = alg_flops / (kms[k] / kw * 1e-3) / 1e12 if alg_flops is not None else sass
             kernels[k] = {"bound": "alu", "achieved": a_, "peak": fp64, "unit": "TFLOP/s", "frac": a_ / fp64,
                           "flops_per_step_algorithmic": alg_flops,
                           "sass_achieved": sass, "sass_frac": sass / fp64,
-                          "newton_iters_per_step": n / args.steps, "sass_flops_per_newton": fpn,
-                          "ms_per_step": kms[k] / args.steps, "share_of_step": kms[k] / ksum}
+                          "newton_iters_per_step": n / kw, "sass_flops_per_newton": fpn,
+                          "ms_per_step": kms[k] / kw, "share_of_step": kms[k] / ksum}
         kernels["k_branch_al"]["al_solves_per_step"] = al_solves
         fused = kms.get("k_rows", 0.0) + kms.get("k_rows_late", 0.0) < 1e-3 * kms["k_bus"]
         for k in (("k_bus",) if fused else ("k_rows", "k_bus")) + ("k_ubar", "k_genx", "k_gen"):
             t = kms[k] + kms.get(k + "_late", 0.0)       # early + late launches
             nbytes = sizes["alg_bytes"][k] + (sizes["alg_bytes"]["k_rows"] if fused and k == "k_bus" else 0)
-            gbs = nbytes * args.steps / (t * 1e-3) / 1e9
+            gbs = nbytes * kw / (t * 1e-3) / 1e9
             name = "k_bus+rows(+late)" if fused and k == "k_bus" else k + ("+late" if k + "_late" in kms else "")
             kernels[name] = {
                 "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                "ms_per_step": t / args.steps, "share_of_step": t / ksum}
+                "ms_per_step": t / kw, "share_of_step": t / ksum}
         dom = max(("k_branch", "k_branch_al"), key=lambda k: kms[k])
         traffic = ncu_traffic()
         if max(kms, key=kms.get) == dom:
@@ -561,9 +577,9 @@ def main():
                                       "event-timed ms per step; sass_* = Newton iterations x ncu SASS flops")
         else:
             dom = max(kms, key=kms.get)
-            roofline = {"bound": "hbm", "kernel": dom, "achieved": sizes["alg_bytes"][dom] * args.steps /
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": sizes["alg_bytes"][dom] * kw /
                         (kms[dom] * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s", "traffic": traffic.get(dom),
-                        "ms_per_step": kms[dom] / args.steps, "share_of_step": kms[dom] / ksum}
+                        "ms_per_step": kms[dom] / kw, "share_of_step": kms[dom] / ksum}
             roofline["frac"] = roofline["achieved"] / hbm
 
     # ---- e2e: the public API from host buffers (create = H2D of the problem, iterate,
@@ -664,7 +680,11 @@ def main():
             "fp64_peak": fp64_meas,
             "algorithmic_flops": alg if world == 1 else None,
             "kernels": kernels,
-            "kernel_ms_per_step": {k: v_ / args.steps for k, v_ in kms.items()} if kms else None,
+            "kernel_ms_per_step": {k: v_ / kw for k, v_ in kms.items()} if kms else None,
+            "kernel_window": ({"iterations": kw, "first": k0,
+                               "note": "per-kernel figures (kernels, roofline, kernel_ms_per_step): the same kernels "
+                                       "launched eagerly with an event pair each over this window of iterations, "
+                                       "after the timed region"} if kms else None),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "time_to_residual": ttr,
