@@ -10,6 +10,7 @@ to rounding-level noise; the non-finite fault path (err_kernel / err_comp / err_
 err_iter); the ADVICE r01 regressions (set_rho and the pipelined DP, the k_gen shared-memory
 attribute across contexts)."""
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -76,6 +77,23 @@ def test_strict_pegase_one_iteration_bitwise():
     gpu.iterate(1)
     orc.iterate(1)
     assert elementwise(gpu.get_state(), orc.get_state(), "pegase strict") == len(FLOAT_FIELDS)
+
+
+def test_strict_pegase_free_run_50_iterations_bitwise():
+    """The full-size case (pegase-shaped, T = 48, 220 k branch solves per iteration) free-running
+    from the cold start for 50 iterations in strict mode against the all-core oracle build (bitwise
+    the serial oracle's iterates, test_openmp_build_is_bitwise_the_serial_oracle): every field of
+    every iteration bitwise."""
+    pb, pr = inputs.build_config("pegase2869")
+    pr = dataclasses.replace(pr, strict_fp=1)
+    oracle.threads(os.cpu_count() or 1)
+    gpu = ucac.Context(pb, pr)
+    orc = oracle.Oracle(pb, pr, omp=True)
+    for it in range(50):
+        gpu.iterate(1)
+        orc.iterate(1)
+        assert elementwise(gpu.get_state(), orc.get_state(), f"pegase strict iteration {it + 1}") == len(FLOAT_FIELDS)
+    assert gpu.report()["tron_iters"] == orc.report()["tron_iters"]
 
 
 def _perturbed(st, rel, rng):
