@@ -136,3 +136,30 @@ def test_nccl_one_rank_multirank_graph_bitwise_equals_single_gpu(monkeypatch):
         ra, rb = ref.report(), one.report()
         for k in ("primal_inf", "objective", "inner_total", "outer_total", "tron_iters", "al_active"):
             assert ra[k] == rb[k], (name, k)
+
+
+@pytest.mark.parametrize("cut,P", [(0, 3), (1, 4)])
+def test_strict_multirank_groups_bitwise_equal_the_oracle(cut, P):
+    """The multi-rank paths in strict mode against the CPU oracle itself (not only against one
+    GPU): the bus cut (halo exchanges, early/late flags) and the time cut (stage-cost all-gather,
+    neighbour ramp values) on the case118-shaped config, 25 free-running iterations, the assembled
+    iterate bitwise equal to the oracle's."""
+    import dataclasses
+    import oracle
+    pb, pr = inputs.build_config("case118")
+    pr = dataclasses.replace(pr, strict_fp=1)
+    if cut == 0:
+        part = ucac.partition(pb, P)
+        ctxs = [ucac.Context(pb, pr, dist={"rank": r, "nranks": P, "comm_mode": 1, "bus_part": part}) for r in range(P)]
+    else:
+        ctxs = [ucac.Context(pb, pr, dist={"rank": r, "nranks": P, "comm_mode": 1, "cut": 1}) for r in range(P)]
+    orc = oracle.Oracle(pb, pr)
+    for it in range(25):
+        ucac.iterate_group(ctxs, 1)
+        orc.iterate(1)
+        got, ref = ucac.assemble_state(pb, ctxs), orc.get_state()
+        for k in ref:
+            if k == "scal":
+                assert np.array_equal(got[k][[0, 2, 3, 4]], ref[k][[0, 2, 3, 4]]), (it, k)
+                continue
+            assert got[k].tobytes() == ref[k].tobytes(), (cut, P, it + 1, k)

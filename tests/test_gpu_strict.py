@@ -96,6 +96,34 @@ def test_strict_pegase_free_run_50_iterations_bitwise():
     assert gpu.report()["tron_iters"] == orc.report()["tron_iters"]
 
 
+def test_strict_t168_free_run_bitwise():
+    """The horizon of P:478's longest runs (pegase-shaped, T = 168), strict mode, 10 free-running
+    iterations from the cold start: every field bitwise."""
+    pb, pr = inputs.build_config("pegase2869", 168)
+    pr = dataclasses.replace(pr, strict_fp=1)
+    oracle.threads(os.cpu_count() or 1)
+    gpu = ucac.Context(pb, pr)
+    orc = oracle.Oracle(pb, pr, omp=True)
+    for it in range(10):
+        gpu.iterate(1)
+        orc.iterate(1)
+        assert elementwise(gpu.get_state(), orc.get_state(), f"T=168 strict iteration {it + 1}") == len(FLOAT_FIELDS)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 4, 8, 16])
+def test_strict_variants_free_run_bitwise(variant):
+    """Each NEXT-3/NEXT-4(a) formulation variant (R47, R50-R52) in strict mode: 30 free-running
+    iterations of the case30-shaped config bitwise equal to the oracle's same variant."""
+    pb, pr = inputs.build_config("case30")
+    pr = dataclasses.replace(pr, strict_fp=1, variant=variant)
+    gpu = ucac.Context(pb, pr)
+    orc = oracle.Oracle(pb, pr)
+    for it in range(30):
+        gpu.iterate(1)
+        orc.iterate(1)
+        assert elementwise(gpu.get_state(), orc.get_state(), f"variant {variant} iteration {it + 1}") == len(FLOAT_FIELDS)
+
+
 def _perturbed(st, rel, rng):
     return {k: (v * (1.0 + rel * rng.uniform(-1.0, 1.0, v.shape)) if v.dtype == np.float64 and k != "scal" else v)
             for k, v in st.items()}
