@@ -1343,11 +1343,18 @@ void launch_bus(const Dev &d, cudaStream_t s) {
 // registers 4 blocks fit an SM; 3 leave one block's registers free, so k_bus_late starts as soon as
 // the AL tail ends instead of after k_rows' last blocks (timeline: 131 -> 124 us; step 0.1676 ->
 // 0.1656 ms, iterate bitwise unchanged; 2: 0.1699, 4: 0.1670)
+// Only where the row sweep is short next to the AL tail: at T = 168 (L*T = 770 k) the sweep is
+// HBM-bound and the full grid is faster (k_rows 85.0 -> 72.3 us, step 0.4023/0.4040 -> 0.3988/0.4002
+// ms), so the cap applies up to L*T = UCAC_ROWS_BPSM_MAX_LT (pegase T = 48: 220 k).
 #ifndef UCAC_ROWS_BPSM
 #define UCAC_ROWS_BPSM 3
 #endif
+#ifndef UCAC_ROWS_BPSM_MAX_LT
+#define UCAC_ROWS_BPSM_MAX_LT 400000
+#endif
 void launch_rows(const Dev &d, cudaStream_t s) {
-    const int grid = UCAC_ROWS_BPSM > 0 ? std::min(d.nblk_rows, UCAC_ROWS_BPSM * sm_count()) : d.nblk_rows;
+    const bool cap = UCAC_ROWS_BPSM > 0 && (long long)d.L * d.T <= UCAC_ROWS_BPSM_MAX_LT;
+    const int grid = cap ? std::min(d.nblk_rows, UCAC_ROWS_BPSM * sm_count()) : d.nblk_rows;
     launch_sweep(UCAC_SWEEP_PRIO, d.strict ? k_rows<true> : k_rows<false>, dim3(grid), dim3(ROWS_THREADS), s, d);
 }
 #ifndef UCAC_LATE_PRIO
