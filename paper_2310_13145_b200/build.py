@@ -33,7 +33,31 @@ UNITS = {
     "ucac.cu": [],
     "partition.cu": [],
 }
-LIBS = ["-lnccl"]
+
+
+def _nccl_dirs():
+    """The NCCL that PyTorch loads (the venv's nvidia-nccl wheel): libucac is compiled against its
+    header and linked to its libnccl.so.2 with an rpath, so that both libraries resolve to the same
+    NCCL whichever is imported first (linked to the system libnccl.so.2 instead, loading libucac
+    before torch made torch's own NCCL symbols unresolvable).  (None, None) if absent."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for base in (list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []):
+            inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+            if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+                return inc, lib
+    except Exception:
+        pass
+    return None, None
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
+if NCCL_LIB:
+    COMMON = COMMON + ["-I", NCCL_INC]
+    LIBS = ["-L", NCCL_LIB, "-Xlinker", "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", NCCL_LIB]
+else:
+    LIBS = ["-lnccl"]
 
 
 def nvcc() -> str:

@@ -79,3 +79,15 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(ucac.UcacError) as e:
         ucac.Context(pb, pr)
     assert e.value.code == 3
+
+
+def test_library_then_torch_import_order():
+    """libucac.so links the NCCL that PyTorch loads (the venv's nvidia-nccl wheel, by rpath): loading
+    the library before torch must not leave torch's NCCL symbols unresolved (linked to the system
+    libnccl.so.2, `import torch` after `ucac.lib()` failed with an undefined ncclDevCommCreate)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); from paper_2310_13145_b200 import ucac; ucac.lib(); "
+            "import torch; print('ok', torch.__version__)") % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
