@@ -60,6 +60,9 @@ __device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
     return s;
 }
 
+#ifndef UCAC_DP_REGCHAIN
+#define UCAC_DP_REGCHAIN 1
+#endif
 // Algorithm 2 on a warp; s.L must be filled.  Returns the optimal cost on lane 0.
 __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int hold) {
     const int lane = threadIdx.x & 31;
@@ -81,6 +84,26 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
     if (lane == 0) {
         s.c[T * 2 + 0] = 0.0;
         s.c[T * 2 + 1] = 0.0;
+#if UCAC_DP_REGCHAIN
+        // the same recursion with its short dependency (stay: c_{t+1}) carried in registers and the
+        // window ends computed, not loaded: the chain per period is an add, a compare and a select,
+        // the switch term's c_{e+1} (written >= 1 period earlier) a load off the chain.  Same
+        // operations, same order: the same costs and decisions bit for bit.
+        double cn0 = 0.0, cn1 = 0.0;   // c_{t+1}(off), c_{t+1}(on)
+        for (int t = T - 1; t >= 0; t--) {
+            const int e0 = min(t + TU - 1, T - 1), e1 = min(t + TD - 1, T - 1);   // R15 clip, as s.e
+            const double sw0 = s.acc[t * 2 + 0] + s.c[(e0 + 1) * 2 + 1];            // Eq. 11
+            const double sw1 = s.acc[t * 2 + 1] + s.c[(e1 + 1) * 2 + 0];
+            const double stay0 = s.L[t * 4 + 0] + cn0, stay1 = s.L[t * 4 + 3] + cn1;   // Eq. 10
+            const bool k0 = stay0 <= sw0, k1 = stay1 <= sw1;
+            cn0 = k0 ? stay0 : sw0;
+            cn1 = k1 ? stay1 : sw1;
+            s.c[t * 2 + 0] = cn0;
+            s.c[t * 2 + 1] = cn1;
+            s.dd[t * 2 + 0] = k0 ? -1 : e0;
+            s.dd[t * 2 + 1] = k1 ? -1 : e1;
+        }
+#else
         for (int t = T - 1; t >= 0; t--) {
 #pragma unroll
             for (int st = 0; st < 2; st++) {
@@ -96,6 +119,7 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
                 }
             }
         }
+#endif
         for (int t = 0; t < hold; t++) {                                                  // R14
             s.u[t] = (int8_t)u0;
             cost = cost + s.L[t * 4 + u0 * 2 + u0];
