@@ -335,7 +335,9 @@ static void pinned_status_put(DevStatus *p) {
 
 // Page-locked staging image for ucac_create's upload, kept across contexts and grown on demand
 // (the upload is one DMA from it instead of the driver's pageable double copy); held under its
-// mutex from the host-side layout to the end of the upload.
+// mutex from the host-side layout to the end of the upload.  It lives for the process (as the
+// pinned status records do): its size is the largest problem's input image (2.8 MB for pegase
+// T = 48), and freeing it at the last context would make the next ucac_create pay the pinning.
 static std::mutex g_stage_mu;
 static char *g_stage = nullptr;
 static size_t g_stage_cap = 0;
