@@ -40,13 +40,15 @@ struct DpSmem {
     double *L;     // [T*4]
     double *acc;   // [T*2] switch cost before continuation: L_t(s,n) + sum_{t'} L_{t'}(n,n)
     double *c;     // [(T+1)*2]
-    int *e;        // [T*2] last period of the forced window (R15: clipped at T)
-    int *dd;       // [T*2] decision: -1 stay, else window end
+    double *Ld;    // [T*2] the stay costs L_t(s,s), interleaved: one 16-byte load per period
+    unsigned *sw;  // [2][W], W = ceil(T/32): decision "switch" of state s at t, bit t%32 of word t/32
     int8_t *u;     // [T]
 };
 
 __host__ __device__ inline size_t dp_smem_bytes(int T) {
-    return (size_t)(T * 4 + T * 2 + (T + 1) * 2) * 8 + (size_t)T * 2 * 4 * 2 + (size_t)((T + 7) / 8) * 8;
+    const size_t W = (size_t)(T + 31) / 32;
+    const size_t b = (size_t)(T * 4 + T * 2 + (T + 1) * 2 + T * 2) * 8 + 2 * W * 4 + (size_t)T;
+    return (b + 15) & ~(size_t)15;   // every warp's slice 16-byte aligned (the paired loads below)
 }
 
 __device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
@@ -54,16 +56,19 @@ __device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
     s.L = (double *)base;
     s.acc = s.L + T * 4;
     s.c = s.acc + T * 2;
-    s.e = (int *)(s.c + (T + 1) * 2);
-    s.dd = s.e + T * 2;
-    s.u = (int8_t *)(s.dd + T * 2);
+    s.Ld = s.c + (T + 1) * 2;
+    s.sw = (unsigned *)(s.Ld + T * 2);
+    s.u = (int8_t *)(s.sw + 2 * ((T + 31) / 32));
     return s;
 }
 
-#ifndef UCAC_DP_REGCHAIN
-#define UCAC_DP_REGCHAIN 1
-#endif
 // Algorithm 2 on a warp; s.L must be filled.  Returns the optimal cost on lane 0.
+// Lanes: the switch costs of every (t, state) (Eq. 11's window sums).  Lane 0: the backward
+// recursion (Eq. 10-11, P:380's tie rule) and the traceback.  The recursion's short
+// dependency c_{t+1} is carried in registers, the window ends are computed, the stay costs and the
+// switch costs come in one 16-byte shared load each, the decisions are kept as bits and the
+// traceback jumps to the next switch bit instead of stepping through every period -- the same
+// additions and comparisons in the same order, so the same costs and decisions bit for bit.
 __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int hold) {
     const int lane = threadIdx.x & 31;
     for (int t = lane; t < T; t += 32) {
@@ -76,7 +81,7 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
             double acc = s.L[t * 4 + st * 2 + n];
             for (int tt = t + 1; tt <= e; tt++) acc = acc + s.L[tt * 4 + n * 2 + n];   // R17
             s.acc[t * 2 + st] = acc;
-            s.e[t * 2 + st] = e;
+            s.Ld[t * 2 + st] = s.L[t * 4 + st * 2 + st];
         }
     }
     __syncwarp();
@@ -84,58 +89,52 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
     if (lane == 0) {
         s.c[T * 2 + 0] = 0.0;
         s.c[T * 2 + 1] = 0.0;
-#if UCAC_DP_REGCHAIN
-        // the same recursion with its short dependency (stay: c_{t+1}) carried in registers and the
-        // window ends computed, not loaded: the chain per period is an add, a compare and a select,
-        // the switch term's c_{e+1} (written >= 1 period earlier) a load off the chain.  Same
-        // operations, same order: the same costs and decisions bit for bit.
+        const int W = (T + 31) / 32;
         double cn0 = 0.0, cn1 = 0.0;   // c_{t+1}(off), c_{t+1}(on)
+        unsigned b0 = 0u, b1 = 0u;
         for (int t = T - 1; t >= 0; t--) {
-            const int e0 = min(t + TU - 1, T - 1), e1 = min(t + TD - 1, T - 1);   // R15 clip, as s.e
-            const double sw0 = s.acc[t * 2 + 0] + s.c[(e0 + 1) * 2 + 1];            // Eq. 11
-            const double sw1 = s.acc[t * 2 + 1] + s.c[(e1 + 1) * 2 + 0];
-            const double stay0 = s.L[t * 4 + 0] + cn0, stay1 = s.L[t * 4 + 3] + cn1;   // Eq. 10
-            const bool k0 = stay0 <= sw0, k1 = stay1 <= sw1;                           // P:380
+            const int e0 = min(t + TU - 1, T - 1), e1 = min(t + TD - 1, T - 1);   // R15 clip
+            const double2 a2 = *reinterpret_cast<const double2 *>(s.acc + t * 2);
+            const double2 l2 = *reinterpret_cast<const double2 *>(s.Ld + t * 2);
+            const double sw0 = a2.x + s.c[(e0 + 1) * 2 + 1];                            // Eq. 11
+            const double sw1 = a2.y + s.c[(e1 + 1) * 2 + 0];
+            const double stay0 = l2.x + cn0, stay1 = l2.y + cn1;                          // Eq. 10
+            const bool k0 = stay0 <= sw0, k1 = stay1 <= sw1;                              // P:380
             cn0 = k0 ? stay0 : sw0;
             cn1 = k1 ? stay1 : sw1;
-            s.c[t * 2 + 0] = cn0;
-            s.c[t * 2 + 1] = cn1;
-            s.dd[t * 2 + 0] = k0 ? -1 : e0;
-            s.dd[t * 2 + 1] = k1 ? -1 : e1;
-        }
-#else
-        for (int t = T - 1; t >= 0; t--) {
-#pragma unroll
-            for (int st = 0; st < 2; st++) {
-                double stay = s.L[t * 4 + st * 2 + st] + s.c[(t + 1) * 2 + st];        // Eq. 10
-                int e = s.e[t * 2 + st];
-                double sw = s.acc[t * 2 + st] + s.c[(e + 1) * 2 + (1 - st)];             // Eq. 11
-                if (stay <= sw) {
-                    s.c[t * 2 + st] = stay;
-                    s.dd[t * 2 + st] = -1;
-                } else {
-                    s.c[t * 2 + st] = sw;
-                    s.dd[t * 2 + st] = e;
-                }
+            *reinterpret_cast<double2 *>(s.c + t * 2) = make_double2(cn0, cn1);
+            b0 |= (k0 ? 0u : 1u) << (t & 31);
+            b1 |= (k1 ? 0u : 1u) << (t & 31);
+            if ((t & 31) == 0) {
+                s.sw[t >> 5] = b0;
+                s.sw[W + (t >> 5)] = b1;
+                b0 = b1 = 0u;
             }
         }
-#endif
         for (int t = 0; t < hold; t++) {                                                  // R14
             s.u[t] = (int8_t)u0;
-            cost = cost + s.L[t * 4 + u0 * 2 + u0];
+            cost = cost + s.Ld[t * 2 + u0];
         }
         cost = cost + s.c[hold * 2 + u0];
         int t = hold, st = u0;
         while (t < T) {
-            int dec = s.dd[t * 2 + st];
-            if (dec < 0) {
-                s.u[t] = (int8_t)st;
-                t++;
-            } else {
-                for (int tt = t; tt <= dec; tt++) s.u[tt] = (int8_t)(1 - st);
-                st = 1 - st;
-                t = dec + 1;
+            // the next period from t on where state st switches (the stay run before it keeps st)
+            const unsigned *bits = s.sw + st * W;
+            int tp = T;
+            for (int w = t >> 5; w < W; w++) {
+                unsigned word = bits[w];
+                if (w == (t >> 5)) word &= ~0u << (t & 31);
+                if (word) {
+                    tp = (w << 5) + __ffs(word) - 1;
+                    break;
+                }
             }
+            for (int tt = t; tt < tp; tt++) s.u[tt] = (int8_t)st;
+            if (tp >= T) break;
+            const int e = min(tp + (st == 0 ? TU : TD) - 1, T - 1);   // the forced window of 1 - st
+            for (int tt = tp; tt <= e; tt++) s.u[tt] = (int8_t)(1 - st);
+            st = 1 - st;
+            t = e + 1;
         }
     }
     __syncwarp();
