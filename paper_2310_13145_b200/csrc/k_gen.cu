@@ -36,6 +36,9 @@ __device__ __forceinline__ double stage_cost(int a, int b, double c0, double csu
     return v;
 }
 
+#ifndef UCAC_DP_PAIR
+#define UCAC_DP_PAIR 1   // the batch kernel (NEXT-1): two instances per warp
+#endif
 struct DpSmem {
     double *L;     // [T*4]
     double *acc;   // [T*2] switch cost before continuation: L_t(s,n) + sum_{t'} L_{t'}(n,n)
@@ -69,9 +72,13 @@ __device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
 // switch costs come in one 16-byte shared load each, the decisions are kept as bits and the
 // traceback jumps to the next switch bit instead of stepping through every period -- the same
 // additions and comparisons in the same order, so the same costs and decisions bit for bit.
-__device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int hold) {
-    const int lane = threadIdx.x & 31;
-    for (int t = lane; t < T; t += 32) {
+// GL: lanes per instance (32: a warp; 16: two instances per warp, each half running its own serial
+// part on its lane 0 -- the batch kernel, whose single active lane left the issue slots idle);
+// act = false: this group has no instance but still meets the warp's __syncwarp.
+template <int GL = 32>
+__device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int hold, bool act = true) {
+    const int lane = threadIdx.x & (GL - 1);
+    for (int t = lane; t < T && act; t += GL) {
 #pragma unroll
         for (int st = 0; st < 2; st++) {
             int n = 1 - st;
@@ -86,7 +93,7 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
     }
     __syncwarp();
     double cost = 0.0;
-    if (lane == 0) {
+    if (lane == 0 && act) {
         s.c[T * 2 + 0] = 0.0;
         s.c[T * 2 + 1] = 0.0;
         const int W = (T + 31) / 32;
@@ -584,6 +591,34 @@ __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const i
     for (int t = lane; t < T; t += 32) sched[(size_t)g * T + t] = s.u[t];
     if (lane == 0) cost[g] = c;
 }
+// two instances per warp (16 lanes each, DP_PAIR): the same per-instance code and arithmetic
+constexpr int DP_PAIR_WARPS = 4;
+// only while three such blocks fit an SM (24 instances in flight against the warp kernel's 16): at
+// T = 168 two fit, and the warp kernel's 16 warps per SM hide more latency (G = 10^4: 0.179 vs
+// 0.170 ms; at T = 24/48/96 the pairs win, 0.025/0.041/0.078 vs 0.030/0.049/0.084 ms)
+inline bool dp_pair_fits(int T) { return dp_smem_bytes(T) * DP_PAIR_WARPS * 2 <= 76 * 1024; }
+__global__ void k_dp_batch_pair(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
+                                const int *hold, int8_t *sched, double *cost) {
+    extern __shared__ __align__(16) char smem[];
+    const int half = threadIdx.x >> 4, lane = threadIdx.x & 15;
+    const int g = blockIdx.x * (DP_PAIR_WARPS * 2) + half;
+    const bool in = g < G;
+    const bool ok = in && !(tu[g] < 1 || tu[g] > T || td[g] < 1 || td[g] > T || hold[g] < 0 || hold[g] > T ||
+                            (u0[g] != 0 && u0[g] != 1));
+    if (in && !ok) {   // as k_dp_batch: an out-of-range instance gets a NaN cost and a zero schedule
+        for (int t = lane; t < T; t += 16) sched[(size_t)g * T + t] = 0;
+        if (lane == 0) cost[g] = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    DpSmem s = dp_carve(smem + (size_t)half * dp_smem_bytes(T), T);
+    if (ok)
+        for (int k = lane; k < T * 4; k += 16) s.L[k] = L[(size_t)g * T * 4 + k];
+    __syncwarp();
+    const double c = dp_warp<16>(s, T, ok ? tu[g] : 1, ok ? td[g] : 1, ok ? u0[g] : 0, ok ? hold[g] : 0, ok);
+    if (ok) {
+        for (int t = lane; t < T; t += 16) sched[(size_t)g * T + t] = s.u[t];
+        if (lane == 0) cost[g] = c;
+    }
+}
 
 // NEXT-2: stage costs of the repair DP, L_t(a, b) = [b != (p_t > threshold)] -- the
 // Hamming distance to the thresholded multiperiod-ACOPF dispatch (SPEC warm_start_uc)
@@ -669,6 +704,12 @@ void launch_genx(const Dev &d, cudaStream_t s) {
 cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                             const int *hold, int8_t *sched, double *cost, cudaStream_t s) {
     const int warps = 4;
+    if (UCAC_DP_PAIR && dp_pair_fits(T)) {
+        const int per = DP_PAIR_WARPS * 2;
+        k_dp_batch_pair<<<(G + per - 1) / per, DP_PAIR_WARPS * 32, dp_smem_bytes(T) * per, s>>>(
+            G, T, L, tu, td, u0, hold, sched, cost);
+        return cudaGetLastError();
+    }
     k_dp_batch<<<(G + warps - 1) / warps, warps * 32, gen_smem(T, warps), s>>>(G, T, L, tu, td, u0, hold,
                                                                                 sched, cost);
     return cudaGetLastError();
@@ -707,6 +748,9 @@ cudaError_t gen_set_smem_attr(int T) {
     cudaError_t e = cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    if (e == cudaSuccess && dp_pair_fits(T))
+        e = cudaFuncSetAttribute(k_dp_batch_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(dp_smem_bytes(T) * DP_PAIR_WARPS * 2));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_dp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e == cudaSuccess) cur = b;
     return e;
