@@ -1,3 +1,6 @@
+"""Phase times of the public-API path on pegase T=48 (create / iterate 100 / report / solution /
+close), three times; with UCAC_CREATE_TRACE=1 also ucac_create's phases (diagnostic).
+usage: UCAC_CREATE_TRACE=1 python tools/e2e_probe.py"""
 import time, torch, sys
 sys.path.insert(0, ".")
 from paper_2310_13145_b200 import inputs, ucac
