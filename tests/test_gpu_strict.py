@@ -124,6 +124,18 @@ def test_strict_variants_free_run_bitwise(variant):
         assert elementwise(gpu.get_state(), orc.get_state(), f"variant {variant} iteration {it + 1}") == len(FLOAT_FIELDS)
 
 
+@pytest.mark.parametrize("name,iters", [("case30", 60), ("case118", 40)])
+def test_strict_uc_warm_start_bitwise(name, iters):
+    """NEXT-2 in strict mode: the held-schedule multiperiod ACOPF, the device Hamming costs and
+    the repair DP reproduce the oracle's repaired schedule exactly -- no rounding-ambiguous
+    thresholds to excuse, since the dispatch p the threshold reads is the oracle's bit for bit."""
+    pb, pr = inputs.build_config(name)
+    pr = dataclasses.replace(pr, strict_fp=1)
+    ug = ucac.uc_warm_start(pb, pr, iters)
+    uo, _ = oracle.uc_warm_start(pb, pr, iters)
+    assert np.array_equal(ug, uo)
+
+
 def _perturbed(st, rel, rng):
     return {k: (v * (1.0 + rel * rng.uniform(-1.0, 1.0, v.shape)) if v.dtype == np.float64 and k != "scal" else v)
             for k, v in st.items()}
