@@ -40,27 +40,26 @@ __device__ __forceinline__ double stage_cost(int a, int b, double c0, double csu
 #define UCAC_DP_PAIR 1   // the batch kernel (NEXT-1): two instances per warp
 #endif
 struct DpSmem {
-    double *L;     // [T*4]
+    double *L;     // [T*4 + 4] L_t(a, b) at t*4 + 2a + b; once the switch costs are formed, the
+                   // continuation costs c_t(s) (Eq. 10-11) reuse the dead off-diagonal slots,
+                   // c_t(s) at t*4 + 1 + s (t = 0..T): per instance ~8.3 KB at T = 168, not 13.7
     double *acc;   // [T*2] switch cost before continuation: L_t(s,n) + sum_{t'} L_{t'}(n,n)
-    double *c;     // [(T+1)*2]
-    double *Ld;    // [T*2] the stay costs L_t(s,s), interleaved: one 16-byte load per period
     unsigned *sw;  // [2][W], W = ceil(T/32): decision "switch" of state s at t, bit t%32 of word t/32
     int8_t *u;     // [T]
 };
+#define DP_C(t, st) s.L[(t) * 4 + 1 + (st)]
 
 __host__ __device__ inline size_t dp_smem_bytes(int T) {
     const size_t W = (size_t)(T + 31) / 32;
-    const size_t b = (size_t)(T * 4 + T * 2 + (T + 1) * 2 + T * 2) * 8 + 2 * W * 4 + (size_t)T;
+    const size_t b = (size_t)(T * 4 + 4 + T * 2) * 8 + 2 * W * 4 + (size_t)T;
     return (b + 15) & ~(size_t)15;   // every warp's slice 16-byte aligned (the paired loads below)
 }
 
 __device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
     DpSmem s;
     s.L = (double *)base;
-    s.acc = s.L + T * 4;
-    s.c = s.acc + T * 2;
-    s.Ld = s.c + (T + 1) * 2;
-    s.sw = (unsigned *)(s.Ld + T * 2);
+    s.acc = s.L + T * 4 + 4;
+    s.sw = (unsigned *)(s.acc + T * 2);
     s.u = (int8_t *)(s.sw + 2 * ((T + 31) / 32));
     return s;
 }
@@ -68,8 +67,8 @@ __device__ __forceinline__ DpSmem dp_carve(char *base, int T) {
 // Algorithm 2 on a warp; s.L must be filled.  Returns the optimal cost on lane 0.
 // Lanes: the switch costs of every (t, state) (Eq. 11's window sums).  Lane 0: the backward
 // recursion (Eq. 10-11, P:380's tie rule) and the traceback.  The recursion's short
-// dependency c_{t+1} is carried in registers, the window ends are computed, the stay costs and the
-// switch costs come in one 16-byte shared load each, the decisions are kept as bits and the
+// dependency c_{t+1} is carried in registers, the window ends are computed, the switch costs of a
+// period come in one 16-byte shared load, the decisions are kept as bits and the
 // traceback jumps to the next switch bit instead of stepping through every period -- the same
 // additions and comparisons in the same order, so the same costs and decisions bit for bit.
 // GL: lanes per instance (32: a warp; 16: two instances per warp, each half running its own serial
@@ -88,28 +87,27 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
             double acc = s.L[t * 4 + st * 2 + n];
             for (int tt = t + 1; tt <= e; tt++) acc = acc + s.L[tt * 4 + n * 2 + n];   // R17
             s.acc[t * 2 + st] = acc;
-            s.Ld[t * 2 + st] = s.L[t * 4 + st * 2 + st];
         }
     }
     __syncwarp();
     double cost = 0.0;
     if (lane == 0 && act) {
-        s.c[T * 2 + 0] = 0.0;
-        s.c[T * 2 + 1] = 0.0;
+        DP_C(T, 0) = 0.0;   // (L's off-diagonal slots are dead from here on)
+        DP_C(T, 1) = 0.0;
         const int W = (T + 31) / 32;
         double cn0 = 0.0, cn1 = 0.0;   // c_{t+1}(off), c_{t+1}(on)
         unsigned b0 = 0u, b1 = 0u;
         for (int t = T - 1; t >= 0; t--) {
             const int e0 = min(t + TU - 1, T - 1), e1 = min(t + TD - 1, T - 1);   // R15 clip
             const double2 a2 = *reinterpret_cast<const double2 *>(s.acc + t * 2);
-            const double2 l2 = *reinterpret_cast<const double2 *>(s.Ld + t * 2);
-            const double sw0 = a2.x + s.c[(e0 + 1) * 2 + 1];                            // Eq. 11
-            const double sw1 = a2.y + s.c[(e1 + 1) * 2 + 0];
-            const double stay0 = l2.x + cn0, stay1 = l2.y + cn1;                          // Eq. 10
+            const double sw0 = a2.x + DP_C(e0 + 1, 1);                                    // Eq. 11
+            const double sw1 = a2.y + DP_C(e1 + 1, 0);
+            const double stay0 = s.L[t * 4 + 0] + cn0, stay1 = s.L[t * 4 + 3] + cn1;      // Eq. 10
             const bool k0 = stay0 <= sw0, k1 = stay1 <= sw1;
             cn0 = k0 ? stay0 : sw0;
             cn1 = k1 ? stay1 : sw1;
-            *reinterpret_cast<double2 *>(s.c + t * 2) = make_double2(cn0, cn1);
+            DP_C(t, 0) = cn0;
+            DP_C(t, 1) = cn1;
             b0 |= (k0 ? 0u : 1u) << (t & 31);
             b1 |= (k1 ? 0u : 1u) << (t & 31);
             if ((t & 31) == 0) {
@@ -120,9 +118,9 @@ __device__ double dp_warp(const DpSmem &s, int T, int TU, int TD, int u0, int ho
         }
         for (int t = 0; t < hold; t++) {                                                  // R14
             s.u[t] = (int8_t)u0;
-            cost = cost + s.Ld[t * 2 + u0];
+            cost = cost + s.L[t * 4 + u0 * 3];
         }
-        cost = cost + s.c[hold * 2 + u0];
+        cost = cost + DP_C(hold, u0);
         int t = hold, st = u0;
         while (t < T) {
             // the next period from t on where state st switches (the stay run before it keeps st)
@@ -593,9 +591,10 @@ __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const i
 }
 // two instances per warp (16 lanes each, DP_PAIR): the same per-instance code and arithmetic
 constexpr int DP_PAIR_WARPS = 4;
-// only while three such blocks fit an SM (24 instances in flight against the warp kernel's 16): at
-// T = 168 two fit, and the warp kernel's 16 warps per SM hide more latency (G = 10^4: 0.179 vs
-// 0.170 ms; at T = 24/48/96 the pairs win, 0.025/0.041/0.078 vs 0.030/0.049/0.084 ms)
+// only while three such blocks fit an SM (24 instances in flight against the warp kernel's 16; with
+// two, the warp kernel's 16 warps per SM hid more latency: 0.179 vs 0.170 ms at G = 10^4, T = 168
+// before the continuation costs shared L's storage).  With the ~8.3 KB layout T = 168 fits three:
+// G = 10^4, T = 24/48/96/168: 0.023/0.038/0.064/0.132 ms against 0.029/0.047/0.079/0.142
 inline bool dp_pair_fits(int T) { return dp_smem_bytes(T) * DP_PAIR_WARPS * 2 <= 76 * 1024; }
 __global__ void k_dp_batch_pair(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
                                 const int *hold, int8_t *sched, double *cost) {
