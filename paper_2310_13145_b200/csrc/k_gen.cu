@@ -589,32 +589,36 @@ __global__ void k_dp_batch(int G, int T, const double *L, const int *tu, const i
     for (int t = lane; t < T; t += 32) sched[(size_t)g * T + t] = s.u[t];
     if (lane == 0) cost[g] = c;
 }
-// two instances per warp (16 lanes each, DP_PAIR): the same per-instance code and arithmetic
-constexpr int DP_PAIR_WARPS = 4;
-// only while three such blocks fit an SM (24 instances in flight against the warp kernel's 16; with
-// two, the warp kernel's 16 warps per SM hid more latency: 0.179 vs 0.170 ms at G = 10^4, T = 168
-// before the continuation costs shared L's storage).  With the ~8.3 KB layout T = 168 fits three:
-// G = 10^4, T = 24/48/96/168: 0.023/0.038/0.064/0.132 ms against 0.029/0.047/0.079/0.142
-inline bool dp_pair_fits(int T) { return dp_smem_bytes(T) * DP_PAIR_WARPS * 2 <= 76 * 1024; }
-__global__ void k_dp_batch_pair(int G, int T, const double *L, const int *tu, const int *td, const int *u0,
-                                const int *hold, int8_t *sched, double *cost) {
+// several instances per warp (GL lanes each, UCAC_DP_PAIR): the same per-instance code and
+// arithmetic.  Worth it while the block (WARPS x 32/GL instances) stays small enough for three or
+// more blocks per SM; measured (G = 10^4; ms at T = 24/48/96/168): one instance per warp (4 warps)
+// 0.029/0.047/0.079/0.142; 16 lanes x 4 warps 0.023/0.038/0.064/0.132; 16 x 3 0.023/0.039/0.063/
+// 0.128; 16 x 2 0.024/0.037/0.063/0.129; 8 x 2 0.021/0.032/0.063/0.149; 8 x 1 0.020/0.031/0.062/
+// 0.145 -- so 8 lanes x 2 warps up to T = 48 and 16 x 3 above
+inline int dp_group_per(int T) { return T <= 48 ? 8 : 6; }
+inline bool dp_pair_fits(int T) { return dp_smem_bytes(T) * dp_group_per(T) <= 76 * 1024; }
+template <int GL, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_dp_batch_group(int G, int T, const double *L, const int *tu,
+                                                              const int *td, const int *u0, const int *hold,
+                                                              int8_t *sched, double *cost) {
     extern __shared__ __align__(16) char smem[];
-    const int half = threadIdx.x >> 4, lane = threadIdx.x & 15;
-    const int g = blockIdx.x * (DP_PAIR_WARPS * 2) + half;
+    constexpr int PER = WARPS * (32 / GL);
+    const int half = threadIdx.x / GL, lane = threadIdx.x & (GL - 1);
+    const int g = blockIdx.x * PER + half;
     const bool in = g < G;
     const bool ok = in && !(tu[g] < 1 || tu[g] > T || td[g] < 1 || td[g] > T || hold[g] < 0 || hold[g] > T ||
                             (u0[g] != 0 && u0[g] != 1));
     if (in && !ok) {   // as k_dp_batch: an out-of-range instance gets a NaN cost and a zero schedule
-        for (int t = lane; t < T; t += 16) sched[(size_t)g * T + t] = 0;
+        for (int t = lane; t < T; t += GL) sched[(size_t)g * T + t] = 0;
         if (lane == 0) cost[g] = __longlong_as_double(0x7ff8000000000000ll);
     }
     DpSmem s = dp_carve(smem + (size_t)half * dp_smem_bytes(T), T);
     if (ok)
-        for (int k = lane; k < T * 4; k += 16) s.L[k] = L[(size_t)g * T * 4 + k];
+        for (int k = lane; k < T * 4; k += GL) s.L[k] = L[(size_t)g * T * 4 + k];
     __syncwarp();
-    const double c = dp_warp<16>(s, T, ok ? tu[g] : 1, ok ? td[g] : 1, ok ? u0[g] : 0, ok ? hold[g] : 0, ok);
+    const double c = dp_warp<GL>(s, T, ok ? tu[g] : 1, ok ? td[g] : 1, ok ? u0[g] : 0, ok ? hold[g] : 0, ok);
     if (ok) {
-        for (int t = lane; t < T; t += 16) sched[(size_t)g * T + t] = s.u[t];
+        for (int t = lane; t < T; t += GL) sched[(size_t)g * T + t] = s.u[t];
         if (lane == 0) cost[g] = c;
     }
 }
@@ -704,9 +708,12 @@ cudaError_t launch_dp_batch(int G, int T, const double *L, const int *tu, const 
                             const int *hold, int8_t *sched, double *cost, cudaStream_t s) {
     const int warps = 4;
     if (UCAC_DP_PAIR && dp_pair_fits(T)) {
-        const int per = DP_PAIR_WARPS * 2;
-        k_dp_batch_pair<<<(G + per - 1) / per, DP_PAIR_WARPS * 32, dp_smem_bytes(T) * per, s>>>(
-            G, T, L, tu, td, u0, hold, sched, cost);
+        const int per = dp_group_per(T);
+        const size_t sm = dp_smem_bytes(T) * per;
+        if (T <= 48)
+            k_dp_batch_group<8, 2><<<(G + per - 1) / per, 64, sm, s>>>(G, T, L, tu, td, u0, hold, sched, cost);
+        else
+            k_dp_batch_group<16, 3><<<(G + per - 1) / per, 96, sm, s>>>(G, T, L, tu, td, u0, hold, sched, cost);
         return cudaGetLastError();
     }
     k_dp_batch<<<(G + warps - 1) / warps, warps * 32, gen_smem(T, warps), s>>>(G, T, L, tu, td, u0, hold,
@@ -742,14 +749,22 @@ cudaError_t gen_set_smem_attr(int T) {
     static std::mutex mu;
     static size_t cur = 0;
     std::lock_guard<std::mutex> lk(mu);
+    // the grouped batch kernels run only while their block needs <= 76 KB (dp_pair_fits): that
+    // limit, once, whatever T comes first
+    static bool group_set = false;
+    if (!group_set) {
+        cudaError_t eg = cudaFuncSetAttribute(k_dp_batch_group<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 76 * 1024);
+        if (eg == cudaSuccess)
+            eg = cudaFuncSetAttribute(k_dp_batch_group<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 76 * 1024);
+        if (eg != cudaSuccess) return eg;
+        group_set = true;
+    }
     const size_t b = gen_smem(T, 4);
     if (b <= cur) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_dp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
-    if (e == cudaSuccess && dp_pair_fits(T))
-        e = cudaFuncSetAttribute(k_dp_batch_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(dp_smem_bytes(T) * DP_PAIR_WARPS * 2));
+
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_dp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     if (e == cudaSuccess) cur = b;
     return e;
