@@ -92,6 +92,36 @@ def test_dp_batch_next1_sizes_bit_exact(G, T):
         assert np.array_equal(s[g], so) and c[g] == co, (G, T, g)
 
 
+@pytest.mark.parametrize("T", [24, 168])
+def test_dp_batch_device_inputs_guarded(T):
+    """ucac_dp_batch on device inputs (not validated by the host, ucac.h): an out-of-range instance
+    (min-up 0, hold > T, u0 = 2) gets a NaN cost and an all-zero schedule instead of indexing past
+    its shared-memory slice; the other instances of the same groups are still the oracle's, bit
+    for bit (T = 24 and 168 run the two grouped batch kernels)."""
+    import torch
+    G = 37
+    L, tu, td, u0, hold = inputs.dp_workload(G, T, seed=5)
+    tu, hold, u0 = tu.copy(), hold.copy(), u0.copy()
+    bad = {3: "tu", 10: "hold", 17: "u0"}
+    tu[3] = 0
+    hold[10] = T + 1
+    u0[17] = 2
+    dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
+    dL, dtu, dtd, du0, dh = dev(L.reshape(-1), np.float64), dev(tu, np.int32), dev(td, np.int32), dev(u0, np.int32), dev(hold, np.int32)
+    sched = torch.full((G * T,), 7, dtype=torch.int8, device="cuda")
+    cost = torch.zeros(G, dtype=torch.float64, device="cuda")
+    ucac.dp_batch_device(G, T, dL.data_ptr(), dtu.data_ptr(), dtd.data_ptr(), du0.data_ptr(), dh.data_ptr(),
+                         sched.data_ptr(), cost.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    s, c = sched.cpu().numpy().reshape(G, T), cost.cpu().numpy()
+    for g in range(G):
+        if g in bad:
+            assert np.isnan(c[g]) and not s[g].any(), (g, bad[g])
+            continue
+        so, co = oracle.dp_solve(L[g], int(tu[g]), int(td[g]), int(u0[g]), int(hold[g]))
+        assert np.array_equal(s[g], so) and c[g] == co, g
+
+
 def ulp_sensitivity(pb, pr, st, k_margin=10.0, n=2, seed=0):
     """Per-field relative tolerance from the oracle's own conditioning (R47): the
     oracle takes the iteration from `st` and from `n` copies of `st` perturbed by one ulp per
