@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(UCAC_AL_TPB) k_branch_al(Dev d) {
 #endif
 void launch_branch(const Dev &d, cudaStream_t s) {
     // shared-memory carveout: 3 k_branch blocks need 52 KB; a larger carveout lets the generator
-    // chain's blocks (k_gen: 4 x dp_smem_bytes(T), ~8 KB at T = 48) co-reside in the free slots instead of waiting for the
+    // chain's blocks (k_gen: 4 x dp_smem_bytes(T), ~10 KB at T = 48) co-reside in the free slots instead of waiting for the
     // SM to drain
     static const bool carve = [] {
         return UCAC_BRANCH_CARVEOUT < 0 ||
