@@ -1820,6 +1820,22 @@ extern "C" int ucac_debug_timeline(ucac_ctx *ctx, unsigned long long *host, int 
     }
     return (int)cudaMemcpy(host, ctx->d.tl, 2 * NKERN * 8, cudaMemcpyDeviceToHost);
 }
+// diagnostic builds only: a one-thread kernel on the context's stream stores the global timer in
+// slot (0..7) when the stream reaches it (graph start / end latencies, tools/timeline.py); slot < 0
+// copies the 8 slots to host
+__device__ unsigned long long g_stamp[8];
+__global__ void k_stamp(int slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_stamp[slot] = t;
+}
+extern "C" int ucac_debug_stamp(ucac_ctx *ctx, unsigned long long *host, int slot) {
+    if (slot >= 0 && slot < 8) {
+        k_stamp<<<1, 1, 0, ctx->s>>>(slot);
+        return (int)cudaGetLastError();
+    }
+    return (int)cudaMemcpyFromSymbol(host, g_stamp, sizeof(g_stamp));
+}
 #endif
 
 extern "C" ucac_status ucac_debug_poison(ucac_ctx *ctx, int32_t field, int64_t index) {
