@@ -338,10 +338,18 @@ static void pinned_status_put(DevStatus *p) {
 // mutex from the host-side layout to the end of the upload.  It lives for the process (as the
 // pinned status records do): its size is the largest problem's input image (2.8 MB for pegase
 // T = 48), and freeing it at the last context would make the next ucac_create pay the pinning.
+// The upload out of it is asynchronous: g_stage_ev, recorded after the copy, is waited for before
+// the image is written or freed again.
 static std::mutex g_stage_mu;
 static char *g_stage = nullptr;
 static size_t g_stage_cap = 0;
+static cudaEvent_t g_stage_ev = nullptr;
+static bool g_stage_ev_pending = false;
 static char *stage_get(size_t n) {   // caller holds g_stage_mu
+    if (g_stage_ev_pending) {
+        if (cudaEventSynchronize(g_stage_ev) != cudaSuccess) return nullptr;
+        g_stage_ev_pending = false;
+    }
     if (n <= g_stage_cap) return g_stage;
     if (g_stage) cudaFreeHost(g_stage);
     g_stage = nullptr;
@@ -394,8 +402,10 @@ static bool finite_all(const double *a, size_t n) {
     return bad == 0;
 }
 
+// scan_demand = false: the demand's finiteness is checked while ucac_create transposes it into the
+// staging image (one pass over the caller's arrays instead of two; single rank only)
 static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, const ucac_costs *co,
-                            const ucac_uc *uc, const ucac_params *p) {
+                            const ucac_uc *uc, const ucac_params *p, bool scan_demand) {
 #define BAD(...) return fail(nullptr, UCAC_EINVAL, __VA_ARGS__)
     if (!net || !hz || !co || !uc || !p) BAD("null argument");
     const int B = net->nbus, G = net->ngen, L = net->nbranch, T = hz->T;
@@ -409,7 +419,8 @@ static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, con
         if (!a || !finite_all(a, B)) BAD("bus arrays must be finite");
     for (int i = 0; i < B; i++)
         if (!(net->bus_vmin[i] > 0) || net->bus_vmin[i] > net->bus_vmax[i]) BAD("bus %d: need 0 < vmin <= vmax", i);
-    if (!hz->pd || !hz->qd || !finite_all(hz->pd, (size_t)T * B) || !finite_all(hz->qd, (size_t)T * B))
+    if (!hz->pd || !hz->qd) BAD("demand arrays missing");
+    if (scan_demand && (!finite_all(hz->pd, (size_t)T * B) || !finite_all(hz->qd, (size_t)T * B)))
         BAD("demand must be finite");
     if (!net->br_from || !net->br_to || !net->br_y || !net->br_rate) BAD("branch arrays missing");
     if (!finite_all(net->br_y, (size_t)L * 8) || !finite_all(net->br_rate, L)) BAD("branch data must be finite");
@@ -451,6 +462,50 @@ static ucac_status validate(const ucac_network *net, const ucac_horizon *hz, con
 
 static ucac_status build_graphs(ucac_ctx *ctx);
 
+// The side streams and fork/join events of destroyed contexts, kept for the next ucac_create on
+// the same device (creating them took ~0.17 ms of every create; the e2e path creates per call).
+struct StreamSet {
+    int dev;
+    cudaStream_t s2, s3;
+    cudaEvent_t ev[7];
+};
+static std::mutex g_ss_mu;
+static std::vector<StreamSet> g_ss_free;
+static bool stream_set_get(ucac_ctx *ctx) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(g_ss_mu);
+    for (size_t i = 0; i < g_ss_free.size(); i++) {
+        if (g_ss_free[i].dev != dev) continue;
+        const StreamSet q = g_ss_free[i];
+        g_ss_free.erase(g_ss_free.begin() + i);
+        ctx->s2 = q.s2; ctx->s3 = q.s3;
+        ctx->ev_fork = q.ev[0]; ctx->ev_join = q.ev[1]; ctx->ev_genx = q.ev[2]; ctx->ev_early = q.ev[3];
+        ctx->ev_branch = q.ev[4]; ctx->ev_tail = q.ev[5]; ctx->ev_bus = q.ev[6];
+        return true;
+    }
+    return false;
+}
+static void stream_set_put(ucac_ctx *ctx) {
+    const cudaEvent_t ev[7] = {ctx->ev_fork, ctx->ev_join, ctx->ev_genx, ctx->ev_early, ctx->ev_branch, ctx->ev_tail, ctx->ev_bus};
+    if (!ctx->s2 || !ctx->s3) return;
+    for (auto e : ev)
+        if (!e) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaStreamSynchronize(ctx->s2) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->s3) != cudaSuccess)
+        return;
+    StreamSet q{dev, ctx->s2, ctx->s3, {}};
+    for (int i = 0; i < 7; i++) q.ev[i] = ev[i];
+    {
+        std::lock_guard<std::mutex> lk(g_ss_mu);
+        if (g_ss_free.size() >= 16) return;   // (then ucac_destroy destroys them)
+        g_ss_free.push_back(q);
+    }
+    ctx->s2 = ctx->s3 = nullptr;
+    ctx->ev_fork = ctx->ev_join = ctx->ev_genx = ctx->ev_early = ctx->ev_branch = ctx->ev_tail = ctx->ev_bus = nullptr;
+}
+
 extern "C" ucac_status ucac_nccl_unique_id(unsigned char *id) {
     if (!id) return UCAC_EINVAL;
     ncclUniqueId u;
@@ -480,7 +535,8 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         fprintf(stderr, "ucac_create %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tpl).count());
         tpl = now;
     };
-    ucac_status vs = validate(net, hz, co, uc, prm);
+    const bool stage_scan = !dist || dist->nranks == 1;   // demand finiteness checked while staging it
+    ucac_status vs = validate(net, hz, co, uc, prm, !stage_scan);
     mark("validate");
     if (vs != UCAC_OK) return vs;
     const int nranks = dist ? dist->nranks : 1;
@@ -573,7 +629,9 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-    if (cudaStreamCreateWithPriority(&ctx->s2, cudaStreamNonBlocking, UCAC_S2_PRIO ? prio_hi : prio_lo) != cudaSuccess ||
+    if (stream_set_get(ctx)) {
+        // recycled from a destroyed context (stream_set_put)
+    } else if (cudaStreamCreateWithPriority(&ctx->s2, cudaStreamNonBlocking, UCAC_S2_PRIO ? prio_hi : prio_lo) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->s3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
@@ -643,6 +701,7 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     // its prefix, staged contiguously on the host and sent with one copy; the rest is zeroed with
     // one memset.  A first pass over the same layout sizes it.
     int8_t *uinit = nullptr;
+    uint64_t demand_bad = 0;   // inf/NaN met while staging the demand (single rank)
     auto layout = [&](Arena &A) {
         d.gbus = A.put(P.gbus);
         d.tu = A.put(P.tu);
@@ -673,13 +732,27 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         d.vmax = A.put(P.vmax);
         // demand [bus][local period], owned buses (ghost rows 0), transposed from the caller's
         // [period][bus] arrays straight into the staging image (reads in input order)
+        // (single rank: every value passes here, and an exponent of all ones flags inf/NaN, the
+        // finiteness check validate() leaves to this pass)
         auto demand = [&](const double *src) {
             return [&, src](double *dst) {
+                const uint64_t E = 0x7ff0000000000000ull;
+                uint64_t bad = 0;
                 for (int a = P.Bo; a < P.B; a++)
                     for (int t = 0; t < T; t++) dst[(size_t)a * T + t] = 0.0;
-                for (int t = 0; t < T; t++)
-                    for (int a = 0; a < P.Bo; a++)
-                        dst[(size_t)a * T + t] = src[(size_t)(P.t_off + t) * net->nbus + P.bus_global[a]];
+                // blocks of 64 buses: the transposed writes of a block stay in a few KB of cache
+                for (int a0 = 0; a0 < P.Bo; a0 += 64) {
+                    const int a1 = std::min(P.Bo, a0 + 64);
+                    for (int t = 0; t < T; t++)
+                        for (int a = a0; a < a1; a++) {
+                            const double v = src[(size_t)(P.t_off + t) * net->nbus + P.bus_global[a]];
+                            uint64_t b;
+                            memcpy(&b, &v, sizeof b);
+                            bad |= (uint64_t)((b & E) == E);
+                            dst[(size_t)a * T + t] = v;
+                        }
+                }
+                demand_bad |= bad;
             };
         };
         d.pd = A.put_fill<double>((size_t)B * T, demand(hz->pd));
@@ -798,11 +871,18 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
         A.base = (uintptr_t)base;
         A.stage = stage;
         layout(A);
+        if (stage_scan && demand_bad) return bail(fail(ctx, UCAC_EINVAL, "demand must be finite"));
         if (cudaMemcpyAsync(base, stage, A.up_end, cudaMemcpyHostToDevice, ctx->s) != cudaSuccess ||
             cudaMemsetAsync((char *)base + A.up_end, 0, A.off - A.up_end, ctx->s) != cudaSuccess)
             return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
-        // the staging image is reused by the next create: the copy must have finished
-        if (cudaStreamSynchronize(ctx->s) != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
+        // the staging image is reused by the next create: it waits for this event (stage_get);
+        // without the event (or with a page-able image), the copy is waited for here
+        if (!g_stage_ev && cudaEventCreateWithFlags(&g_stage_ev, cudaEventDisableTiming) != cudaSuccess) g_stage_ev = nullptr;
+        if (stage == g_stage && g_stage_ev && cudaEventRecord(g_stage_ev, ctx->s) == cudaSuccess) {
+            g_stage_ev_pending = true;
+        } else if (cudaStreamSynchronize(ctx->s) != cudaSuccess) {
+            return bail(fail(ctx, UCAC_ECUDA, "arena upload"));
+        }
     }
     if (tcut) {
         // receive buffers and arrival flags of the time cut's exchanges, one cudaMalloc block (not
@@ -834,14 +914,20 @@ extern "C" ucac_status ucac_create(const ucac_network *net, const ucac_horizon *
     launch_init(d, uinit, ctx->s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init kernel: %s", cudaGetErrorString(e)));
-    e = cudaStreamSynchronize(ctx->s);
-    if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init: %s", cudaGetErrorString(e)));
+    mark("init");
+    // the graphs are captured while the upload, the memset and the init kernel run (capture
+    // records only the work enqueued after it begins), then the stream is waited for once
     if (!(nranks > 1 && ctx->comm_mode == 1)) {
-        mark("init");
         ucac_status gs = build_graphs(ctx);
-        if (gs != UCAC_OK) return bail(gs);
+        if (gs != UCAC_OK) {
+            cudaStreamSynchronize(ctx->s);
+            return bail(gs);
+        }
     }
     mark("graphs");
+    e = cudaStreamSynchronize(ctx->s);
+    if (e != cudaSuccess) return bail(fail(ctx, UCAC_ECUDA, "init: %s", cudaGetErrorString(e)));
+    mark("sync");
     *out = ctx;
     return UCAC_OK;
 #undef ALLOC
@@ -1782,6 +1868,7 @@ extern "C" const char *ucac_last_error(const ucac_ctx *ctx) {
 
 extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (!ctx) return;
+    stream_set_put(ctx);   // (its streams are idle once s is: every fork in the graphs joins s)
     if (ctx->s) cudaStreamSynchronize(ctx->s);
     for (auto &g : ctx->gexec)
         if (g) cudaGraphExecDestroy(g);

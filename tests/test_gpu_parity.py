@@ -325,13 +325,23 @@ def test_edge_cases():
         ucac.Context(bad, pr)
     with pytest.raises(ucac.UcacError):
         ucac.Context(inputs.case9(T=4), inputs.Params(rho_pq=-1, rho_va=1, rho_uc=1))
-    # non-finite inputs (the bitwise finiteness scan of validate): EINVAL
-    for field, idx, v in (("pd", (3, 5), np.nan), ("br_y", (2, 6), np.inf), ("pmax", (1,), -np.inf)):
+    # non-finite inputs (the bitwise finiteness scan of validate; for the demand of a single-rank
+    # context, the same test while ucac_create stages it): EINVAL
+    for field, idx, v in (("pd", (3, 5), np.nan), ("qd", (0, 8), -np.inf), ("br_y", (2, 6), np.inf),
+                          ("pmax", (1,), -np.inf)):
         bad = inputs.case9(T=4)
         getattr(bad, field)[idx] = v
         with pytest.raises(ucac.UcacError) as e:
             ucac.Context(bad, pr)
         assert e.value.code == 1, field
+        assert "finite" in str(e.value), field
+    # a create after a failed one (staging image, recycled streams) is a normal context
+    good = inputs.case9(T=4)
+    a, b = ucac.Context(good, pr), ucac.Context(good, pr)
+    a.iterate(3)
+    b.iterate(3)
+    sa, sb = a.get_state(), b.get_state()
+    assert all(sa[k].tobytes() == sb[k].tobytes() for k in sa)
 
 
 @pytest.mark.parametrize("name,iters", [("case9", 40), ("case30", 60), ("case118", 40)])

@@ -5,7 +5,7 @@ import time, torch, sys
 sys.path.insert(0, ".")
 from paper_2310_13145_b200 import inputs, ucac
 pb, pr = inputs.build_config("pegase2869")
-for rep in range(3):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     c = ucac.Context(pb, pr); torch.cuda.synchronize(); t1 = time.perf_counter()
     c.iterate(100); torch.cuda.synchronize(); t2 = time.perf_counter()
