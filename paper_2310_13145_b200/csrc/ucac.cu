@@ -162,6 +162,9 @@ static Local build_local(const ucac_network *net, const ucac_horizon *hz, const 
     }
     P.ref = h.bus_local[net->ref_bus] >= 0 && h.bus_local[net->ref_bus] < P.Bo ? h.bus_local[net->ref_bus] : -1;
     P.ysoa.assign((size_t)8 * P.L, 0.0);
+    P.from.reserve(P.L);
+    P.to.reserve(P.L);
+    P.rate.reserve(P.L);
     for (int a = 0; a < P.L; a++) {
         int l = h.local_branch[a];
         P.from.push_back(h.bus_local[net->br_from[l]]);
@@ -204,6 +207,7 @@ static Local build_local(const ucac_network *net, const ucac_horizon *hz, const 
     for (int a = 0; a < P.G; a++) P.bgp[P.gbus[a] + 1]++;
     struct End { int gl, side, bus, code; };
     std::vector<End> ends;
+    ends.reserve((size_t)2 * L);
     for (int l = 0; l < L; l++) {
         int lf = h.bus_local[net->br_from[l]], lt = h.bus_local[net->br_to[l]];
         int ll = h.br_local[l];
