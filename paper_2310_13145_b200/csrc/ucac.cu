@@ -50,6 +50,9 @@ struct NvtxRange {
 #ifndef UCAC_UBAR_AFTER_BUS
 #define UCAC_UBAR_AFTER_BUS 0   // 1 measured slower (0.186 vs 0.181 ms): k_ubar then delays the early fold
 #endif
+#ifndef UCAC_EXEC_POOL
+#define UCAC_EXEC_POOL 1   // recycle instantiated graphs across contexts (cudaGraphExecUpdate)
+#endif
 #ifndef UCAC_FUSE_ROWS
 #define UCAC_FUSE_ROWS 0   // measured slower: 0.203 vs 0.182 ms (per-thread end loops lengthen the late chains)
 #endif
@@ -1199,6 +1202,33 @@ static void enqueue_iteration(ucac_ctx *ctx) {
     launch_finalize(d, ctx->s);
 }
 
+// Instantiated single-iteration graphs of destroyed single-rank contexts: the next ucac_create
+// captures its own graph and, where the topology is the same (same kernels, same edges), loads it
+// into one of these with cudaGraphExecUpdate (new kernel parameters and grids) instead of
+// instantiating anew.  A pooled graph is never launched before that update.
+static std::mutex g_exec_mu;
+static std::vector<std::pair<int, cudaGraphExec_t>> g_exec_free;   // (device, graph)
+static cudaGraphExec_t exec_pool_get() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(g_exec_mu);
+    for (size_t i = 0; i < g_exec_free.size(); i++)
+        if (g_exec_free[i].first == dev) {
+            cudaGraphExec_t x = g_exec_free[i].second;
+            g_exec_free.erase(g_exec_free.begin() + i);
+            return x;
+        }
+    return nullptr;
+}
+static bool exec_pool_put(cudaGraphExec_t x) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(g_exec_mu);
+    if (g_exec_free.size() >= 4) return false;
+    g_exec_free.emplace_back(dev, x);
+    return true;
+}
+
 static ucac_status build_graphs(ucac_ctx *ctx) {
     for (int gi = 0; gi < 2; gi++) {
         if (gi == 1 && ctx->gunroll[1] == 1) break;   // single-iteration graphs only
@@ -1210,6 +1240,18 @@ static ucac_status build_graphs(ucac_ctx *ctx) {
         if (ctx->nccl_err != ncclSuccess) {
             cudaGraphDestroy(g);
             return fail(ctx, UCAC_ENCCL, "NCCL collective in the iteration graph: %s", ncclGetErrorString(ctx->nccl_err));
+        }
+        if (gi == 0 && !ctx->multi && !ctx->gexec[0] && UCAC_EXEC_POOL) {
+            if (cudaGraphExec_t x = exec_pool_get()) {
+                cudaGraphExecUpdateResultInfo info;
+                if (cudaGraphExecUpdate(x, g, &info) == cudaSuccess) {
+                    ctx->gexec[0] = x;
+                    cudaGraphDestroy(g);
+                    continue;
+                }
+                cudaGetLastError();   // (a different topology: instantiate instead)
+                cudaGraphExecDestroy(x);
+            }
         }
         // per-node launch priorities (launch_hi_prio) are honoured only with this flag
         cudaError_t e = cudaGraphInstantiate(&ctx->gexec[gi], g, UCAC_NODE_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
@@ -1874,6 +1916,7 @@ extern "C" void ucac_destroy(ucac_ctx *ctx) {
     if (!ctx) return;
     stream_set_put(ctx);   // (its streams are idle once s is: every fork in the graphs joins s)
     if (ctx->s) cudaStreamSynchronize(ctx->s);
+    if (ctx->gexec[0] && !ctx->multi && UCAC_EXEC_POOL && exec_pool_put(ctx->gexec[0])) ctx->gexec[0] = nullptr;
     for (auto &g : ctx->gexec)
         if (g) cudaGraphExecDestroy(g);
     for (auto ev : ctx->tev) cudaEventDestroy(ev);

@@ -519,3 +519,25 @@ def test_divergence_detector_and_history():
     assert len(g.history(10)) == 0 and g.report()["hist_len"] == 0
     with pytest.raises(ucac.UcacError):
         ucac.Context(pb, dataclasses.replace(pr, diverge_window=256))
+
+
+@pytest.mark.gpu
+def test_recycled_graph_equals_eager_launches():
+    """ucac_create loads a destroyed context's instantiated iteration graph with
+    cudaGraphExecUpdate when the topology matches (here: a pegase context's graph re-used for
+    case30, new kernel parameters and grids): its iterate equals the same iterations launched
+    eagerly (ucac_iterate_timed, no graph) bit for bit, and so does a second recycling."""
+    pa, ra = inputs.build_config("pegase2869")
+    a = ucac.Context(pa, ra)
+    a.iterate(2)
+    a.close()
+    pb, pr = inputs.build_config("case30")
+    for _ in range(2):
+        y, w = ucac.Context(pb, pr), ucac.Context(pb, pr)
+        y.iterate(12)
+        w.iterate_timed(12)
+        sy, sw = y.get_state(), w.get_state()
+        assert all(sy[k].tobytes() == sw[k].tobytes() for k in sy)
+        assert y.report()["inner_total"] == w.report()["inner_total"] == 12
+        y.close()
+        w.close()
