@@ -1241,18 +1241,21 @@ static ucac_status build_graphs(ucac_ctx *ctx) {
             cudaGraphDestroy(g);
             return fail(ctx, UCAC_ENCCL, "NCCL collective in the iteration graph: %s", ncclGetErrorString(ctx->nccl_err));
         }
-        if (gi == 0 && !ctx->multi && !ctx->gexec[0] && UCAC_EXEC_POOL) {
-            if (cudaGraphExec_t x = exec_pool_get()) {
-                cudaGraphExecUpdateResultInfo info;
-                if (cudaGraphExecUpdate(x, g, &info) == cudaSuccess) {
-                    ctx->gexec[0] = x;
-                    cudaGraphDestroy(g);
-                    continue;
-                }
-                cudaGetLastError();   // (a different topology: instantiate instead)
-                cudaGraphExecDestroy(x);
+        // single rank: load the new graph into this context's previous one (ucac_set_rho) or a
+        // pooled one; multi-rank graphs are instantiated anew
+        cudaGraphExec_t x = ctx->gexec[gi];
+        ctx->gexec[gi] = nullptr;
+        if (!x && gi == 0 && !ctx->multi && UCAC_EXEC_POOL) x = exec_pool_get();
+        if (x && !ctx->multi) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(x, g, &info) == cudaSuccess) {
+                ctx->gexec[gi] = x;
+                cudaGraphDestroy(g);
+                continue;
             }
+            cudaGetLastError();   // (a different topology: instantiate instead)
         }
+        if (x) cudaGraphExecDestroy(x);
         // per-node launch priorities (launch_hi_prio) are honoured only with this flag
         cudaError_t e = cudaGraphInstantiate(&ctx->gexec[gi], g, UCAC_NODE_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
         cudaGraphDestroy(g);
@@ -1331,12 +1334,8 @@ extern "C" ucac_status ucac_set_rho(ucac_ctx *ctx, double rho_pq, double rho_va,
     // the pipelined tail DP (k_gen tail) already ran the next (7a) with the old rho_uc: drop it
     CK(cudaMemsetAsync(d.unext_ok, 0, sizeof(unsigned), ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
-    // the graphs captured the old Dev by value: re-instantiate them
-    for (auto &g : ctx->gexec)
-        if (g) {
-            cudaGraphExecDestroy(g);
-            g = nullptr;
-        }
+    // the graphs captured the old Dev by value: capture them again (build_graphs updates the
+    // instantiated ones in place where it can)
     if (!(ctx->nranks > 1 && ctx->comm_mode == 1)) return build_graphs(ctx);
     return UCAC_OK;
 }

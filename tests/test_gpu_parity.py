@@ -427,6 +427,15 @@ def test_set_rho_mid_run_next4():
         os_ = orc.get_state()
         assert np.array_equal(gs["u"], os_["u"])
         assert np.array_equal(gs["scal"][[0, 2, 3, 4]], os_["scal"][[0, 2, 3, 4]])
+    # the 16-iteration graph, updated in place by set_rho (cudaGraphExecUpdate), against the same
+    # iterations launched eagerly from the same state by a context created with the new rho
+    twin = ucac.Context(pb, pr2)
+    twin.set_state(gpu.get_state())
+    gpu.iterate(16)
+    twin.iterate_timed(16)
+    ga, tw = gpu.get_state(), twin.get_state()
+    assert all(ga[k].tobytes() == tw[k].tobytes() for k in ga)
+    twin.close()
     with pytest.raises(ucac.UcacError):
         gpu.set_rho(-1.0, 1.0, 1.0)
 
