@@ -641,8 +641,11 @@ __global__ void __launch_bounds__(LBUS_THREADS) k_bus_late(Dev d) {
             if (d.fuse_rows) bus_end_rows<STRICT>(d, c, k, acc);
         }
     }
-    // fused rows: this is the iteration's last kernel and does the final fold
-    kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, d.fuse_rows != 0);
+    // fused rows: this is the iteration's last kernel and does the final fold; otherwise its
+    // partials are folded by k_rows_late's last block, after its own (no last-block fold here, on
+    // the critical path between the AL tail and the late rows)
+    if (d.fuse_rows) kernel_tail(d, acc, d.part_lbus, RK_BUS_LATE, true);
+    else block_reduce_store(acc, d.part_lbus);
 }
 
 // k_fold_early: the block partials of k_bus, k_ubar and k_rows (in that order) -> rec_part[RK_EARLY]
@@ -708,7 +711,14 @@ __global__ void __launch_bounds__(LROWS_THREADS) k_rows_late(Dev d, int final) {
             end_rows<STRICT>(d, c, l, t, code & 1, acc);
         }
     }
-    kernel_tail(d, acc, d.part_lrows, RK_ROWS_LATE, final != 0);
+    if (store_partial_last(acc, d.part_lrows, d.kdone + RK_ROWS_LATE)) {
+        fold_slots(d.part_lbus, d.nblk_lbus, d.rec_part + RK_BUS_LATE * NPART);   // k_bus_late's partials
+        fold_slots(d.part_lrows, gridDim.x, d.rec_part + RK_ROWS_LATE * NPART);
+        if (final) {
+            __threadfence();
+            final_fold(d);
+        }
+    }
 }
 
 // ------------------------------------------------------------------------- (7c) ubar
