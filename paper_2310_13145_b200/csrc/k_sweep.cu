@@ -173,8 +173,9 @@ constexpr int LBUS_THREADS = UCAC_LBUS_THREADS, LROWS_THREADS = UCAC_LROWS_THREA
 // ------------------------------------------------------------------------- S8 partials
 // Every kernel that updates rows leaves one partial per block.  The early ones (k_bus, k_ubar,
 // k_rows) are folded by k_fold_early off the critical path (in the shadow of the AL tail); the
-// late kernels fold their own in their LAST block (threadfence + counter), and the last block of
-// the iteration's last kernel folds the three records.  Fixed slots, fixed order: deterministic.
+// LAST block of k_rows_late (threadfence + counter) folds the late kernels' partials (k_bus_late's,
+// then its own; k_bus_late itself when the rows are fused into it), and the last block of the
+// iteration's last kernel folds the three records.  Fixed slots, fixed order: deterministic.
 enum RecKind { RK_EARLY = 0, RK_BUS_LATE, RK_ROWS_LATE, NRK };
 
 // fold slots [0, n) of part into out[NPART]: 32 groups of NPART threads take every 32nd slot
