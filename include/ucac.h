@@ -339,6 +339,10 @@ ucac_status ucac_measure_latencies(double *cycles);
 
 void *ucac_stream(ucac_ctx *ctx);                 /* the cudaStream_t the context runs on */
 const char *ucac_last_error(const ucac_ctx *ctx); /* NULL ctx: last create failure (thread-local) */
+/* Waits for the context's stream, frees its device memory and destroys it.  Its side streams,
+ * fork/join events and instantiated single-iteration graph are kept (process lifetime, per device)
+ * for the next ucac_create, which loads its own graph into the kept one (cudaGraphExecUpdate) --
+ * so no cudaDeviceReset between contexts.  NULL: no-op. */
 void ucac_destroy(ucac_ctx *ctx);
 
 #ifdef __cplusplus
