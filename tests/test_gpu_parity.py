@@ -550,3 +550,36 @@ def test_recycled_graph_equals_eager_launches():
         assert y.report()["inner_total"] == w.report()["inner_total"] == 12
         y.close()
         w.close()
+
+
+@pytest.mark.gpu
+def test_concurrent_create_destroy_threads():
+    """ucac_create/ucac_destroy from several host threads at once (the staging image, the recycled
+    streams/events and graphs are shared under their mutexes; ctypes releases the GIL): every
+    context iterates bitwise like a reference context created alone."""
+    import threading
+    pb, pr = inputs.build_config("case30")
+    ref = ucac.Context(pb, pr)
+    ref.iterate(6)
+    want = ref.get_state()
+    ref.close()
+    errors = []
+
+    def work(seed):
+        try:
+            for _ in range(3):
+                c = ucac.Context(pb, pr)
+                c.iterate(6)
+                got = c.get_state()
+                c.close()
+                if not all(got[k].tobytes() == want[k].tobytes() for k in want):
+                    errors.append(f"thread {seed}: iterate differs")
+        except Exception as e:   # noqa: BLE001 -- reported below
+            errors.append(f"thread {seed}: {e!r}")
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
