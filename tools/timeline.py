@@ -1,6 +1,6 @@
 """Graph timeline of one inner iteration (diagnostic; needs a -DUCAC_PROF build): per kernel the
 first block start and the last block exit relative to the iteration start (global timer).
-usage: python tools/timeline.py [config] [warm iterations]"""
+usage: python tools/timeline.py [config] [warm iterations] [T]"""
 import ctypes as C
 import os
 import sys
@@ -13,9 +13,9 @@ sys.path.insert(0, ROOT)
 from paper_2310_13145_b200 import inputs, ucac  # noqa: E402
 
 
-def main(name="pegase2869", warm=10):
+def main(name="pegase2869", warm=10, T=None):
     import torch
-    pb, pr = inputs.build_config(name)
+    pb, pr = inputs.build_config(name, int(T)) if T else inputs.build_config(name)
     c = ucac.Context(pb, pr)
     c.iterate(int(warm))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
